@@ -1,0 +1,252 @@
+"""ctypes front-end for the CPU oracles -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+arm may import this module. The product (paper_2511_12235_b200) never does.
+
+Four interchangeable libraries export the same ``ref_*`` C-ABI
+(oracle/ref_shim.cpp == oracle/ctsm_oracle.h):
+
+=========  =================================================================
+variant    library
+=========  =================================================================
+ref_glibc  oracle/_ref/libctsm_ref_glibc.so  unmodified reference + glibc libm
+ref_cr     oracle/_ref/libctsm_ref_cr.so     unmodified reference + crmath libm
+port_glibc oracle/_build/libctsm_oracle_glibc.so  C restatement + glibc libm
+port_cr    oracle/_build/libctsm_oracle_cr.so     C restatement + crmath libm
+=========  =================================================================
+
+``ref_*`` exist only where /root/reference was present at build time (they are
+prebuilt here and travel to the GPU box with the snapshot).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+LIBS = {
+    "ref_glibc": os.path.join(HERE, "_ref", "libctsm_ref_glibc.so"),
+    "ref_cr": os.path.join(HERE, "_ref", "libctsm_ref_cr.so"),
+    "port_glibc": os.path.join(HERE, "_build", "libctsm_oracle_glibc.so"),
+    "port_cr": os.path.join(HERE, "_build", "libctsm_oracle_cr.so"),
+}
+
+ERROR_NAMES = [
+    "DegenerateGeometry", "RayParallelToFace", "SingularPhi", "CentralRow",
+    "ZRestrictionViolation", "DimensionMismatch", "NonFinite", "ZeroMatrix", "TooLarge",
+    "InvalidSpec", "OutOfMemory", "InvalidConfig", "IoFailure",
+]
+
+
+class OGeom(ctypes.Structure):
+    """Mirror of ScanGeometry (geometry.hpp:29-44) == ctsm_geometry."""
+
+    _fields_ = [
+        ("s", ctypes.c_double), ("d", ctypes.c_double), ("d_y", ctypes.c_double),
+        ("d_z", ctypes.c_double), ("n_det_y", ctypes.c_int32), ("n_det_z", ctypes.c_int32),
+        ("n_angles", ctypes.c_int32), ("pad0", ctypes.c_int32),
+        ("angle_start", ctypes.c_double), ("angle_end", ctypes.c_double),
+        ("a", ctypes.c_double), ("b", ctypes.c_double), ("c", ctypes.c_double),
+        ("n_x", ctypes.c_int32), ("n_y", ctypes.c_int32), ("n_z", ctypes.c_int32),
+        ("pad1", ctypes.c_int32),
+    ]
+
+
+def to_ogeom(g) -> OGeom:
+    o = OGeom()
+    for name, _ in OGeom._fields_:
+        if name.startswith("pad"):
+            continue
+        setattr(o, name, getattr(g, name))
+    return o
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        self.code = ERROR_NAMES[code] if 0 <= code < len(ERROR_NAMES) else f"code{code}"
+        super().__init__(msg)
+
+
+_P = ctypes.c_void_p
+_cache: dict[str, "Oracle"] = {}
+
+
+def available(variant: str) -> bool:
+    return os.path.exists(LIBS[variant])
+
+
+def load(variant: str = "port_cr") -> "Oracle":
+    if variant not in _cache:
+        _cache[variant] = Oracle(variant)
+    return _cache[variant]
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(_P)
+
+
+@dataclass
+class Csr:
+    row_start: np.ndarray
+    col: np.ndarray
+    val: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col.size)
+
+
+class Oracle:
+    def __init__(self, variant: str):
+        path = LIBS[variant]
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"oracle library {path} not built (run `make -C oracle`)")
+        self.variant = variant
+        L = self.lib = ctypes.CDLL(path)
+        L.ref_last_error.restype = ctypes.c_char_p
+        L.ref_validate.argtypes = [_P]
+        L.ref_angle.argtypes = [_P, ctypes.c_int]
+        L.ref_angle.restype = ctypes.c_double
+        L.ref_pixel_area_factors.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.c_double, _P, _P, ctypes.c_long]
+        L.ref_pixel_area_factors.restype = ctypes.c_long
+        L.ref_voxel_volume_factors.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, _P, _P, _P, ctypes.c_long]
+        L.ref_voxel_volume_factors.restype = ctypes.c_long
+        L.ref_angle_block_entries.argtypes = [_P, ctypes.c_int, _P, _P, _P, ctypes.c_long]
+        L.ref_angle_block_entries.restype = ctypes.c_long
+        L.ref_build_system_matrix.argtypes = [_P, ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int)]
+        L.ref_build_system_matrix.restype = _P
+        L.ref_csr_nnz.argtypes = [_P]
+        L.ref_csr_nnz.restype = ctypes.c_uint64
+        L.ref_csr_rows.argtypes = [_P]
+        L.ref_csr_rows.restype = ctypes.c_uint64
+        L.ref_csr_copy.argtypes = [_P, _P, _P, _P]
+        L.ref_csr_free.argtypes = [_P]
+        for f in ("ref_forward_project", "ref_back_project"):
+            getattr(L, f).argtypes = [_P, _P, _P]
+        L.ref_forward_project_matrix_free.argtypes = [_P, _P, _P, ctypes.c_int]
+        L.ref_back_project_matrix_free.argtypes = [_P, _P, _P, ctypes.c_int]
+        L.ref_forward_mf_angles.argtypes = [_P, _P, ctypes.c_int, _P, _P, ctypes.c_int]
+        L.ref_back_mf_angles.argtypes = [_P, _P, ctypes.c_int, _P, _P, ctypes.c_int]
+        L.ref_sirt.argtypes = [_P, _P, _P, ctypes.c_int, ctypes.c_int]
+        L.ref_angle_column_sums.argtypes = [_P, ctypes.c_int, _P]
+
+    # -- helpers -----------------------------------------------------------
+    def _check(self, st: int):
+        if st < 0:
+            code = -st - 1
+            raise OracleError(code, self.lib.ref_last_error().decode())
+
+    @staticmethod
+    def _g(g):
+        og = to_ogeom(g)
+        return og, ctypes.byref(og)
+
+    # -- API ---------------------------------------------------------------
+    def validate(self, g):
+        og, p = self._g(g)
+        self._check(self.lib.ref_validate(p))
+
+    def angle(self, g, i: int) -> float:
+        og, p = self._g(g)
+        return self.lib.ref_angle(p, i)
+
+    def pixel_area_factors(self, g, ix: int, iy: int, phi: float):
+        og, p = self._g(g)
+        my = np.zeros(256, np.int32)
+        w = np.zeros(256, np.float64)
+        n = self.lib.ref_pixel_area_factors(p, ix, iy, phi, _ptr(my), _ptr(w), 256)
+        self._check(n)
+        return my[:n].copy(), w[:n].copy()
+
+    def voxel_volume_factors(self, g, ix: int, iy: int, iz: int, phi: float):
+        og, p = self._g(g)
+        my = np.zeros(256, np.int32)
+        mz = np.zeros(256, np.int32)
+        w = np.zeros(256, np.float64)
+        n = self.lib.ref_voxel_volume_factors(p, ix, iy, iz, phi, _ptr(my), _ptr(mz), _ptr(w), 256)
+        self._check(n)
+        return my[:n].copy(), mz[:n].copy(), w[:n].copy()
+
+    def angle_block_entries(self, g, ip: int):
+        """(row_raster u32, col u32, w f64) in emission order (projector.cpp:44-84)."""
+        og, p = self._g(g)
+        n = self.lib.ref_angle_block_entries(p, ip, None, None, None, 0)
+        self._check(n)
+        row = np.empty(n, np.uint32)
+        col = np.empty(n, np.uint32)
+        w = np.empty(n, np.float64)
+        n2 = self.lib.ref_angle_block_entries(p, ip, _ptr(row), _ptr(col), _ptr(w), n)
+        self._check(n2)
+        return row, col, w
+
+    def build_system_matrix(self, g, threads: int = 1, budget: int = 5 << 30) -> Csr:
+        og, p = self._g(g)
+        st = ctypes.c_int(0)
+        h = self.lib.ref_build_system_matrix(p, threads, budget, ctypes.byref(st))
+        self._check(st.value)
+        try:
+            nnz = self.lib.ref_csr_nnz(h)
+            rows = self.lib.ref_csr_rows(h)
+            rs = np.empty(rows + 1, np.uint64)
+            col = np.empty(nnz, np.uint32)
+            val = np.empty(nnz, np.float64)
+            self.lib.ref_csr_copy(h, _ptr(rs), _ptr(col), _ptr(val))
+        finally:
+            self.lib.ref_csr_free(h)
+        return Csr(rs, col, val)
+
+    def forward_project_matrix_free(self, g, x: np.ndarray, threads: int = 1) -> np.ndarray:
+        og, p = self._g(g)
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros(g.n_angles * g.n_det_y * g.n_det_z, np.float64)
+        self._check(self.lib.ref_forward_project_matrix_free(p, _ptr(x), _ptr(y), threads))
+        return y
+
+    def back_project_matrix_free(self, g, y: np.ndarray, threads: int = 1) -> np.ndarray:
+        og, p = self._g(g)
+        y = np.ascontiguousarray(y, np.float64)
+        x = np.zeros(g.n_x * g.n_y * g.n_z, np.float64)
+        self._check(self.lib.ref_back_project_matrix_free(p, _ptr(y), _ptr(x), threads))
+        return x
+
+    def forward_mf_angles(self, g, angles, x: np.ndarray, threads: int = 1) -> np.ndarray:
+        og, p = self._g(g)
+        a = np.ascontiguousarray(angles, np.int32)
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros(a.size * g.n_det_y * g.n_det_z, np.float64)
+        self._check(self.lib.ref_forward_mf_angles(p, _ptr(a), a.size, _ptr(x), _ptr(y), threads))
+        return y
+
+    def back_mf_angles(self, g, angles, y: np.ndarray, threads: int = 1) -> np.ndarray:
+        og, p = self._g(g)
+        a = np.ascontiguousarray(angles, np.int32)
+        y = np.ascontiguousarray(y, np.float64)
+        x = np.zeros(g.n_x * g.n_y * g.n_z, np.float64)
+        self._check(self.lib.ref_back_mf_angles(p, _ptr(a), a.size, _ptr(y), _ptr(x), threads))
+        return x
+
+    def sirt(self, g, y: np.ndarray, x0: np.ndarray, iters: int, threads: int = 1) -> np.ndarray:
+        og, p = self._g(g)
+        y = np.ascontiguousarray(y, np.float64)
+        x = np.array(x0, np.float64, copy=True)
+        self._check(self.lib.ref_sirt(p, _ptr(y), _ptr(x), iters, threads))
+        return x
+
+    def angle_column_sums(self, g, ip: int) -> np.ndarray:
+        og, p = self._g(g)
+        s = np.zeros(g.n_x * g.n_y * g.n_z, np.float64)
+        self._check(self.lib.ref_angle_column_sums(p, ip, _ptr(s)))
+        return s
+
+
+def csr_forward(c: Csr, x: np.ndarray) -> np.ndarray:
+    """Row-ordered CSR A x in numpy (same association as projector.cpp:203-217
+    only up to summation order; use for tolerance checks)."""
+    rows = np.repeat(np.arange(c.row_start.size - 1), np.diff(c.row_start).astype(np.int64))
+    y = np.zeros(c.row_start.size - 1)
+    np.add.at(y, rows, c.val * x[c.col])
+    return y

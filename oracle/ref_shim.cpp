@@ -1,0 +1,287 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY (never linked into the product).
+//
+// A thin extern "C" adapter over the UNMODIFIED reference library
+// (/root/reference/proj/src/*.cpp, compiled where they lie by oracle/Makefile)
+// so the Python tests and bench.py's reference arm can drive the reference's
+// own public API: pixel_area_factors (weights2d.hpp:31), voxel_volume_factors
+// (weights3d.hpp:90), detail::angle_block_entries (projector.hpp:76),
+// build_system_matrix / forward_project / back_project /
+// forward_project_matrix_free (projector.hpp:41-59).
+//
+// Two restatements the reference lacks are composed here from its own calls,
+// exactly as SURVEY.md §8(a) a16 prescribes:
+//  * matrix-free A^T y: x[c] += w * y[r] through detail::angle_block_entries,
+//    per-angle partial volumes summed in ascending angle order (deterministic
+//    for any thread count, like ordered_parallel_for, projector.cpp:114-140);
+//  * SIRT: x <- x + C .* A^T (R .* (y - A x)), R = 1/(A 1), C = 1/(A^T 1),
+//    zero sums -> 0 (BASELINE.json configs[4]).
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "ctsm/geometry.hpp"
+#include "ctsm/projector.hpp"
+#include "ctsm/weights2d.hpp"
+#include "ctsm/weights3d.hpp"
+
+namespace {
+
+struct RefGeom {  // layout == ctsm_geometry in include/ctsm_b200.h
+  double s, d, d_y, d_z;
+  int32_t n_det_y, n_det_z, n_angles, pad0;
+  double angle_start, angle_end;
+  double a, b, c;
+  int32_t n_x, n_y, n_z, pad1;
+};
+
+ctsm::ScanGeometry to_g(const RefGeom* r) {
+  ctsm::ScanGeometry g;
+  g.s = r->s;
+  g.d = r->d;
+  g.d_y = r->d_y;
+  g.d_z = r->d_z;
+  g.n_det_y = r->n_det_y;
+  g.n_det_z = r->n_det_z;
+  g.n_angles = r->n_angles;
+  g.angle_start = r->angle_start;
+  g.angle_end = r->angle_end;
+  g.a = r->a;
+  g.b = r->b;
+  g.c = r->c;
+  g.n_x = r->n_x;
+  g.n_y = r->n_y;
+  g.n_z = r->n_z;
+  return g;
+}
+
+thread_local std::string g_err;
+
+int fail_code(const ctsm::Error& e) {
+  g_err = e.what();
+  return -(static_cast<int>(e.code()) + 1);
+}
+
+#define REF_GUARD(...)                           \
+  try {                                          \
+    __VA_ARGS__                                  \
+  } catch (const ctsm::Error& e) {               \
+    return fail_code(e);                         \
+  } catch (const std::exception& e) {            \
+    g_err = e.what();                            \
+    return -100;                                 \
+  }
+
+// Runs fn(i) for i in [0,count) on up to `threads` workers, each worker taking
+// a contiguous index range; rethrows the first error.
+template <typename Fn>
+void parallel_range(int count, int threads, Fn fn) {
+  threads = std::max(1, std::min(threads, count));
+  if (threads == 1) {
+    for (int i = 0; i < count; ++i) fn(i);
+    return;
+  }
+  std::vector<std::exception_ptr> errs(threads);
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) {
+    pool.emplace_back([&, t] {
+      const int lo = (int)((int64_t)count * t / threads);
+      const int hi = (int)((int64_t)count * (t + 1) / threads);
+      try {
+        for (int i = lo; i < hi; ++i) fn(i);
+      } catch (...) {
+        errs[t] = std::current_exception();
+      }
+    });
+  }
+  for (auto& th : pool) th.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_validate(const RefGeom* rg) {
+  REF_GUARD(to_g(rg).validate(); return 0;)
+}
+
+double ref_angle(const RefGeom* rg, int i) { return to_g(rg).angle(i); }
+
+// pixel_area_factors (weights2d.cpp:105-129). Returns the count (<= cap written).
+long ref_pixel_area_factors(const RefGeom* rg, int ix, int iy, double phi, int32_t* my,
+                            double* w, long cap) {
+  REF_GUARD(const auto ws = ctsm::pixel_area_factors(ctsm::VoxelIndex{ix, iy, 0}, phi,
+                                                     to_g(rg));
+            for (long i = 0; i < (long)ws.size() && i < cap; ++i) {
+              my[i] = ws[i].m_y;
+              w[i] = ws[i].w;
+            } return (long)ws.size();)
+}
+
+// voxel_volume_factors (weights3d.cpp:354-462).
+long ref_voxel_volume_factors(const RefGeom* rg, int ix, int iy, int iz, double phi,
+                              int32_t* my, int32_t* mz, double* w, long cap) {
+  REF_GUARD(const auto ws = ctsm::voxel_volume_factors(ctsm::VoxelIndex{ix, iy, iz}, phi,
+                                                       to_g(rg));
+            for (long i = 0; i < (long)ws.size() && i < cap; ++i) {
+              my[i] = ws[i].m_y;
+              mz[i] = ws[i].m_z;
+              w[i] = ws[i].w;
+            } return (long)ws.size();)
+}
+
+// detail::angle_block_entries (projector.cpp:44-84), consistent mode. Entries
+// in emission order; returns the total count (only the first cap are stored).
+long ref_angle_block_entries(const RefGeom* rg, int ip, uint32_t* row, uint32_t* col,
+                             double* w, long cap) {
+  REF_GUARD(long n = 0; ctsm::detail::angle_block_entries(
+                to_g(rg), ctsm::MatrixMode::consistent, 1, ip,
+                [&](uint32_t r, uint32_t c, double v) {
+                  if (n < cap) {
+                    row[n] = r;
+                    col[n] = c;
+                    w[n] = v;
+                  }
+                  ++n;
+                });
+            return n;)
+}
+
+// build_system_matrix (projector.cpp:144-201) -> opaque handle.
+void* ref_build_system_matrix(const RefGeom* rg, int threads, uint64_t budget, int* status) {
+  try {
+    auto* m = new ctsm::SparseSystemMatrix(
+        ctsm::build_system_matrix(to_g(rg), ctsm::MatrixMode::consistent, 1, threads, budget));
+    *status = 0;
+    return m;
+  } catch (const ctsm::Error& e) {
+    *status = fail_code(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    *status = -100;
+  }
+  return nullptr;
+}
+
+uint64_t ref_csr_nnz(void* h) { return static_cast<ctsm::SparseSystemMatrix*>(h)->nnz(); }
+uint64_t ref_csr_rows(void* h) { return static_cast<ctsm::SparseSystemMatrix*>(h)->n_rows; }
+
+void ref_csr_copy(void* h, uint64_t* row_start, uint32_t* col, double* val) {
+  auto* m = static_cast<ctsm::SparseSystemMatrix*>(h);
+  std::memcpy(row_start, m->row_start.data(), m->row_start.size() * sizeof(uint64_t));
+  std::memcpy(col, m->col.data(), m->col.size() * sizeof(uint32_t));
+  std::memcpy(val, m->val.data(), m->val.size() * sizeof(double));
+}
+
+void ref_csr_free(void* h) { delete static_cast<ctsm::SparseSystemMatrix*>(h); }
+
+// forward_project / back_project (projector.cpp:203-233).
+int ref_forward_project(void* h, const double* x, double* y) {
+  auto* m = static_cast<ctsm::SparseSystemMatrix*>(h);
+  REF_GUARD(const std::vector<double> xv(x, x + m->n_cols);
+            const auto yv = ctsm::forward_project(*m, xv);
+            std::copy(yv.begin(), yv.end(), y); return 0;)
+}
+
+int ref_back_project(void* h, const double* y, double* x) {
+  auto* m = static_cast<ctsm::SparseSystemMatrix*>(h);
+  REF_GUARD(const std::vector<double> yv(y, y + m->n_rows);
+            const auto xv = ctsm::back_project(*m, yv);
+            std::copy(xv.begin(), xv.end(), x); return 0;)
+}
+
+// forward_project_matrix_free (projector.cpp:235-260), all angles.
+int ref_forward_project_matrix_free(const RefGeom* rg, const double* x, double* y,
+                                    int threads) {
+  REF_GUARD(const ctsm::ScanGeometry g = to_g(rg);
+            const std::vector<double> xv(x, x + g.n_voxels());
+            const auto yv = ctsm::forward_project_matrix_free(
+                g, ctsm::MatrixMode::consistent, 1, xv, threads);
+            std::copy(yv.begin(), yv.end(), y); return 0;)
+}
+
+// A x restricted to a list of angles (sampled timing / parity at C3/C4):
+// y_sel[k * rows_per_angle + r] = (A x)[angles[k] * rows_per_angle + r].
+// Same per-angle accumulation as forward_project_matrix_free (249-252).
+int ref_forward_mf_angles(const RefGeom* rg, const int32_t* angles, int n_sel,
+                          const double* x, double* y_sel, int threads) {
+  REF_GUARD(const ctsm::ScanGeometry g = to_g(rg); g.validate();
+            const uint64_t rpa = (uint64_t)g.n_det_y * g.n_det_z;
+            parallel_range(n_sel, threads, [&](int k) {
+              double* block = y_sel + (uint64_t)k * rpa;
+              std::fill(block, block + rpa, 0.0);
+              ctsm::detail::angle_block_entries(
+                  g, ctsm::MatrixMode::consistent, 1, angles[k],
+                  [&](uint32_t r, uint32_t c, double wv) { block[r] += wv * x[c]; });
+            });
+            return 0;)
+}
+
+// Matrix-free A^T y over a list of angles (restatement):
+// x = sum over listed angles (in list order) of the per-angle partial volume.
+// y is indexed like the full sinogram: y[angles[k] * rows_per_angle + r].
+int ref_back_mf_angles(const RefGeom* rg, const int32_t* angles, int n_sel, const double* y,
+                       double* x, int threads) {
+  REF_GUARD(const ctsm::ScanGeometry g = to_g(rg); g.validate();
+            const uint64_t rpa = (uint64_t)g.n_det_y * g.n_det_z;
+            const uint64_t nv = g.n_voxels(); std::fill(x, x + nv, 0.0);
+            const int chunk = std::max(1, threads);
+            std::vector<std::vector<double>> part(chunk);
+            for (int k0 = 0; k0 < n_sel; k0 += chunk) {
+              const int n = std::min(chunk, n_sel - k0);
+              parallel_range(n, threads, [&](int t) {
+                auto& p = part[t];
+                p.assign(nv, 0.0);
+                const double* yb = y + (uint64_t)angles[k0 + t] * rpa;
+                ctsm::detail::angle_block_entries(
+                    g, ctsm::MatrixMode::consistent, 1, angles[k0 + t],
+                    [&](uint32_t r, uint32_t c, double wv) { p[c] += wv * yb[r]; });
+              });
+              for (int t = 0; t < n; ++t)
+                for (uint64_t i = 0; i < nv; ++i) x[i] += part[t][i];
+            } return 0;)
+}
+
+int ref_back_project_matrix_free(const RefGeom* rg, const double* y, double* x, int threads) {
+  std::vector<int32_t> all(rg->n_angles);
+  for (int i = 0; i < rg->n_angles; ++i) all[i] = i;
+  return ref_back_mf_angles(rg, all.data(), rg->n_angles, y, x, threads);
+}
+
+// SIRT (BASELINE.json configs[4]) composed from the reference's projector:
+// R = 1/(A 1), C = 1/(A^T 1) (zero sums -> 0); iters x (x += C (A^T (R (y - A x)))).
+int ref_sirt(const RefGeom* rg, const double* y, double* x, int iters, int threads) {
+  const uint64_t nv = (uint64_t)rg->n_x * rg->n_y * rg->n_z;
+  const uint64_t nm = (uint64_t)rg->n_angles * rg->n_det_y * rg->n_det_z;
+  std::vector<double> ones_v(nv, 1.0), ones_m(nm, 1.0), R(nm), C(nv), ax(nm), r(nm), bp(nv);
+  int st = ref_forward_project_matrix_free(rg, ones_v.data(), R.data(), threads);
+  if (st) return st;
+  st = ref_back_project_matrix_free(rg, ones_m.data(), C.data(), threads);
+  if (st) return st;
+  for (auto& v : R) v = v != 0.0 ? 1.0 / v : 0.0;
+  for (auto& v : C) v = v != 0.0 ? 1.0 / v : 0.0;
+  for (int it = 0; it < iters; ++it) {
+    st = ref_forward_project_matrix_free(rg, x, ax.data(), threads);
+    if (st) return st;
+    for (uint64_t i = 0; i < nm; ++i) r[i] = R[i] * (y[i] - ax[i]);
+    st = ref_back_project_matrix_free(rg, r.data(), bp.data(), threads);
+    if (st) return st;
+    for (uint64_t i = 0; i < nv; ++i) x[i] += C[i] * bp[i];
+  }
+  return 0;
+}
+
+// angle_column_sums (projector.cpp:288-295).
+int ref_angle_column_sums(const RefGeom* rg, int ip, double* sums) {
+  REF_GUARD(const auto v = ctsm::angle_column_sums(to_g(rg), ctsm::MatrixMode::consistent, 1, ip);
+            std::copy(v.begin(), v.end(), sums); return 0;)
+}
+
+}  // extern "C"
