@@ -1,0 +1,362 @@
+#!/usr/bin/env python3
+"""Benchmark of the consistent-system-matrix hot path on B200.
+
+Workload (default, --config c1): BASELINE.json configs[1] -- 2D fan-beam
+512x512 grid, 0.5 mm pixels, s=500, sdd=1000, 1024 cells of 0.6 mm, 720
+angles; one step = matrix-free A x (40-ellipse phantom) + A^T y (U[0,1)
+sinogram), fp64 storage and FP64 weights. Metric: voxel-ray updates/s, where
+one projection performs nnz(A) = 591,345,624 updates, so
+a step is 2 * nnz updates. Multi-GPU (torchrun): angles are sharded
+round-robin (rank::N); A x needs no communication, the A^T y partial volumes
+are summed with an NCCL all-reduce.
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/libctsm_ref_glibc.so: forward_project_matrix_free and the
+angle_block_entries adjoint) on all host cores over a bounded angle sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# nnz(A) per projection (voxel-ray updates); C1/C2 are
+# re-verified by tests/test_gpu_parity.py::test_nnz_counts.
+NNZ = {"c0": 18_291_648, "c1": 591_345_624, "c2": 4_604_879_490}
+# FP64 operations per pixel/voxel-angle as executed by the reference
+# (add/sub/mul/div each 1, libm calls excluded).
+F_REF = {"2d": 247.0, "3d": 1513.0}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c1")
+    p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    p.add_argument("--no-clocks", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    from paper_2511_12235_b200 import CONFIGS
+    from paper_2511_12235_b200.phantoms import phantom_for, uniform_sinogram
+
+    cfg = args.config
+    g = CONFIGS[cfg]
+    variant = "ref_glibc" if pyoracle.available("ref_glibc") else "port_glibc"
+    orc = pyoracle.load(variant)
+    cores = os.cpu_count() or 1
+    x = phantom_for(cfg, g)
+    y = uniform_sinogram(g.n_measurements, 12346)
+    # bounded sample: strided angles, ~10-30 s of CPU work per step on a many-core host
+    n_sample = {"c0": 36, "c1": 8, "c2": 2, "c3": 1, "c4": 1}.get(cfg, 4)
+    n_sample = max(n_sample, min(g.n_angles, cores // 8))
+    angles = np.linspace(0, g.n_angles, n_sample, endpoint=False).astype(np.int32)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        orc.forward_mf_angles(g, angles, x, cores)
+        orc.back_mf_angles(g, angles, y, cores)
+        t = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(t)
+    t_sample = float(np.mean(times))
+    t_full = t_sample * g.n_angles / angles.size  # extrapolated fwd+bwd time
+    value = 2.0 * NNZ[cfg] / t_full
+    line = {
+        "impl": "reference",
+        "metric": "voxel-ray updates/s (A x + A^T y)",
+        "value": value,
+        "unit": "updates/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_full * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{cfg}: BASELINE.json configs[{cfg[1]}]", "sample_angles": int(angles.size)},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": "reference" if variant == "ref_glibc" else "port",
+                         "sample": f"{angles.size} of {g.n_angles} strided angles, fwd+bwd, extrapolated x{g.n_angles / angles.size:.0f}"},
+        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def measure_dfma_peak(torch):
+    """Measured FP64 FMA throughput (TFLOP/s, FMA = 2 flops) with a DFMA
+    microkernel in the library's own context."""
+    from paper_2511_12235_b200 import _lib
+    import ctypes
+
+    L = _lib.lib()
+    f = getattr(L, "ctsm_bench_dfma", None)
+    if f is None:
+        return None
+    f.restype = ctypes.c_double
+    f.argtypes = [ctypes.c_int]
+    best = 0.0
+    for _ in range(3):
+        best = max(best, f(torch.cuda.current_device()))
+    return best
+
+
+class ClockSampler:
+    def __init__(self, gpu_index: int, enabled: bool):
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        if not enabled:
+            return
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [v.strip() for v in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sms.append(float(f[1]))
+                maxs.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sms:
+            return None
+        return {"sm_mhz": float(np.median(sms)), "sm_max_mhz": float(max(maxs)),
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_12235_b200 import CONFIGS, Context, _lib
+    from paper_2511_12235_b200.phantoms import phantom_for, uniform_sinogram
+    from paper_2511_12235_b200.projector import (back_project_matrix_free,
+                                                 forward_project_matrix_free)
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = args.config
+    g = CONFIGS[cfg]
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    ctx = Context.get(local)
+    x_h = phantom_for(cfg, g, dtype=np.float32 if not g.is_2d() else np.float64)
+    y_h = uniform_sinogram(g.n_measurements, 12346)
+    x = torch.from_numpy(x_h).to(tdt).to(dev)
+    y = torch.from_numpy(y_h).to(tdt).to(dev)
+    yout = torch.zeros(g.n_measurements, dtype=tdt, device=dev)
+    xout = torch.zeros(g.n_voxels, dtype=tdt, device=dev)
+    shard = (rank, g.n_angles, world)
+    flush = torch.empty(256 << 20, dtype=torch.int8, device=dev)  # > 126 MB L2
+
+    ev_f0, ev_f1, ev_b1, ev_r1 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+
+    def step():
+        forward_project_matrix_free(g, "consistent", 1, x, angles=shard, out=yout)
+        ev_f1.record()
+        back_project_matrix_free(g, "consistent", 1, y, angles=shard, out=xout)
+        ev_b1.record()
+        if world > 1:
+            dist.all_reduce(xout)
+        ev_r1.record()
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local, not args.no_clocks)
+    launches0 = _lib.launch_count()
+    t_total = t_fwd = t_bwd = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        ev_f0.record()
+        step()
+        torch.cuda.synchronize()
+        t_total += ev_f0.elapsed_time(ev_r1)
+        t_fwd += ev_f0.elapsed_time(ev_f1)
+        t_bwd += ev_f1.elapsed_time(ev_b1)
+    launches = _lib.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = t_total / args.steps
+    ms_t = torch.tensor([ms, t_fwd / args.steps, t_bwd / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms, ms_f, ms_b = [float(v) for v in ms_t.cpu()]
+    updates_per_step = 2.0 * NNZ.get(cfg, 0)
+    value = updates_per_step / (ms * 1e-3)
+
+    # ---- end-to-end through the reference-facing host-buffer C-ABI ----
+    e2e = None
+    if not args.no_e2e and world == 1 and args.dtype == "f64":
+        import ctypes
+        L = _lib.lib()
+        xh = torch.from_numpy(x_h.astype(np.float64)).pin_memory()
+        yh = torch.from_numpy(y_h).pin_memory()
+        yo = torch.empty(g.n_measurements, dtype=torch.float64).pin_memory()
+        xo = torch.empty(g.n_voxels, dtype=torch.float64).pin_memory()
+        cg = g.to_c()
+        def e2e_step():
+            _lib.check(L.ctsm_forward_project_matrix_free_host(ctx.handle, ctypes.byref(cg),
+                                                               ctypes.c_void_p(xh.data_ptr()),
+                                                               ctypes.c_void_p(yo.data_ptr())))
+            _lib.check(L.ctsm_back_project_matrix_free_host(ctx.handle, ctypes.byref(cg),
+                                                            ctypes.c_void_p(yh.data_ptr()),
+                                                            ctypes.c_void_p(xo.data_ptr())))
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        te = (time.perf_counter() - t0) / args.steps
+        e2e = {"value": updates_per_step / te, "unit": "updates/s",
+               "h2d_bytes_per_step": 8 * (g.n_voxels + g.n_measurements),
+               "d2h_bytes_per_step": 8 * (g.n_measurements + g.n_voxels),
+               "ms_per_step": te * 1e3}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peak = measure_dfma_peak(torch)
+    # roofline of the dominant kernel (the slower of fwd / bwd)
+    units = g.n_x * g.n_y * g.n_z * g.n_angles / (world if world > 1 else 1)
+    if g.is_2d():
+        per_unit = F_REF["2d"]
+    else:
+        per_unit = F_REF["3d"]
+    dom_ms = max(ms_f, ms_b)
+    achieved = units * per_unit / (dom_ms * 1e-3) / 1e12
+    roof = {"bound": "fp64", "kernel": "bwd2d" if ms_b >= ms_f else "fwd2d",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": (achieved / peak) if peak else None, "traffic": None,
+            "peak_source": "measured DFMA microkernel (MEASURED_PEAKS.json has no FP64 entry)",
+            "work_per_unit": f"{per_unit:g} FP64 flops per pixel-angle (SURVEY.md §8(d))",
+            "fwd_ms": ms_f, "bwd_ms": ms_b}
+    line = {
+        "metric": "voxel-ray updates/s (A x + A^T y)",
+        "value": value,
+        "unit": "updates/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": args.dtype,
+        "data": "synthetic",
+        "config": {"workload": f"{cfg}: BASELINE.json configs[{cfg[1]}] matrix-free A x + A^T y",
+                   "parallelism": f"angle-shard x{world}", "l2": "flushed (256 MB write) before each step"},
+        "roofline": roof,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if world == 1 and os.environ.get("CTSM_BENCH_NO_CPU") is None:
+        line["cpu_baseline"] = cpu_baseline_quick(cfg)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline_quick(cfg):
+    """The reference's CPU path on a bounded sample (rank 0, N=1)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    try:
+        import pyoracle
+        from paper_2511_12235_b200 import CONFIGS
+        from paper_2511_12235_b200.phantoms import phantom_for, uniform_sinogram
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e)}
+    variant = "ref_glibc" if pyoracle.available("ref_glibc") else "port_glibc"
+    if not pyoracle.available(variant):
+        return {"error": "oracle not built"}
+    orc = pyoracle.load(variant)
+    g = CONFIGS[cfg]
+    cores = os.cpu_count() or 1
+    x = phantom_for(cfg, g)
+    y = uniform_sinogram(g.n_measurements, 12346)
+    n_sample = max(4, min(g.n_angles // 4, cores // 4))
+    angles = np.linspace(0, g.n_angles, n_sample, endpoint=False).astype(np.int32)
+    t0 = time.perf_counter()
+    orc.forward_mf_angles(g, angles, x, cores)
+    orc.back_mf_angles(g, angles, y, cores)
+    t = time.perf_counter() - t0
+    t_full = t * g.n_angles / angles.size
+    return {"value": 2.0 * NNZ[cfg] / t_full, "unit": "updates/s", "cores": cores,
+            "kind": "reference" if variant == "ref_glibc" else "port",
+            "sample": f"fwd+bwd over {angles.size} of {g.n_angles} strided angles ({t:.1f} s), extrapolated"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,145 @@
+/* ctsm_b200.h -- C-ABI of the B200-native consistent CT system-matrix library.
+ *
+ * This is the drop-in boundary for the reference's hot path (ctsm,
+ * /root/reference/proj): the C++ API in include/ctsm_b200/projector.hpp and
+ * the Python mirror (paper_2511_12235_b200) are thin layers over these entry
+ * points. Plain pointers and sizes only; device pointers are CUDA global
+ * memory on the context's device; `stream` is a cudaStream_t (NULL = legacy
+ * default stream).
+ *
+ * Status convention: every call returns 0 on success or
+ * (ctsm::ErrorCode ordinal + 1) (common.hpp:11-25), e.g. 10 = InvalidSpec,
+ * 11 = OutOfMemory; CTSM_ERR_CUDA (100) for a CUDA runtime failure.
+ * ctsm_last_error() returns the message of the calling thread's last failure.
+ * In-kernel guards (depth <= 1e-12 s, 2D piece < -1e-14, 3D weight < -1e-9;
+ * geometry.cpp:59-60, weights2d.cpp:115-118, weights3d.cpp:455-457) raise the
+ * same codes through a device status word checked after each call.
+ */
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ScanGeometry (geometry.hpp:29-44); field order and meaning identical. */
+typedef struct ctsm_geometry {
+  double s, d, d_y, d_z;
+  int32_t n_det_y, n_det_z, n_angles, pad0;
+  double angle_start, angle_end;
+  double a, b, c;
+  int32_t n_x, n_y, n_z, pad1;
+} ctsm_geometry;
+
+enum {
+  CTSM_OK = 0,
+  CTSM_ERR_DEGENERATE_GEOMETRY = 1,
+  CTSM_ERR_RAY_PARALLEL_TO_FACE = 2,
+  CTSM_ERR_SINGULAR_PHI = 3,
+  CTSM_ERR_CENTRAL_ROW = 4,
+  CTSM_ERR_Z_RESTRICTION = 5,
+  CTSM_ERR_DIMENSION_MISMATCH = 6,
+  CTSM_ERR_NON_FINITE = 7,
+  CTSM_ERR_ZERO_MATRIX = 8,
+  CTSM_ERR_TOO_LARGE = 9,
+  CTSM_ERR_INVALID_SPEC = 10,
+  CTSM_ERR_OUT_OF_MEMORY = 11,
+  CTSM_ERR_INVALID_CONFIG = 12,
+  CTSM_ERR_IO_FAILURE = 13,
+  CTSM_ERR_CUDA = 100
+};
+
+/* Element type of matrix-free operands (x, y). Weights are always evaluated in
+ * FP64; the dtype is the storage/accumulation type. */
+enum { CTSM_F64 = 0, CTSM_F32 = 1 };
+
+typedef struct ctsm_ctx ctsm_ctx;
+
+/* ---- context ------------------------------------------------------------ */
+int ctsm_create(int device, ctsm_ctx** out);
+int ctsm_destroy(ctsm_ctx* ctx);
+const char* ctsm_last_error(void);
+const char* ctsm_version(void);
+/* Number of GPU kernel launches issued by this library in this process
+ * (monotonic; used by bench.py to report gpu_launches). */
+uint64_t ctsm_launch_count(void);
+
+/* ScanGeometry::validate (geometry.cpp:27-54), plus the device-side
+ * implementation limits (TooLarge). */
+int ctsm_validate_geometry(const ctsm_geometry* g);
+
+/* ---- K1/K2: consistent system-matrix CSR (build_system_matrix,
+ * projector.hpp:41-44 / projector.cpp:144-201) ----------------------------
+ * Builds the rows of angles [angle_begin, angle_end) (an angle shard: rows
+ * are angle-major, geometry.hpp:79-84, so a shard is a contiguous row range).
+ * Two phases:
+ *   ctsm_csr_count: row_start_dev[0..n_rows] (u64, n_rows = (angle_end -
+ *     angle_begin) * n_det_y * n_det_z) receives the exclusive prefix sum of
+ *     per-row entry counts; *nnz_out (host) the total. Raises OutOfMemory if
+ *     nnz * 12 + (n_rows + 1) * 8 exceeds memory_budget_bytes (cf.
+ *     projector.cpp:155-169) and ZeroMatrix if the full matrix is empty.
+ *   ctsm_csr_fill: fills col_dev (u32, voxel columns strictly ascending per
+ *     row) and val_dev (f64) for the same shard.
+ * Values are bit-identical to the reference evaluated with a correctly
+ * rounded libm (crmath.h); see DESIGN.md. */
+int ctsm_csr_count(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int angle_end,
+                   uint64_t memory_budget_bytes, uint64_t* row_start_dev, uint64_t* nnz_out,
+                   void* stream);
+int ctsm_csr_fill(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int angle_end,
+                  const uint64_t* row_start_dev, uint32_t* col_dev, double* val_dev,
+                  void* stream);
+
+/* ---- K3/K4: CSR appliers (forward_project / back_project,
+ * projector.cpp:203-233). Deterministic; NonFinite check as the reference. */
+int ctsm_spmv(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols, const uint64_t* row_start_dev,
+              const uint32_t* col_dev, const double* val_dev, const double* x_dev,
+              double* y_dev, void* stream);
+int ctsm_spmv_t(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols, const uint64_t* row_start_dev,
+                const uint32_t* col_dev, const double* val_dev, const double* y_dev,
+                double* x_dev, void* stream);
+
+/* ---- K5/K6: matrix-free projectors (forward_project_matrix_free,
+ * projector.hpp:56-59; back_project_matrix_free is the rebuild's addition).
+ * The angle shard is {angle_begin + k * angle_step < angle_end}. Forward
+ * writes the sinogram rows of those angles (other rows untouched). Backward
+ * writes x = sum over the shard's angles (overwrites x). Layouts: x
+ * [n_z][n_y][n_x], y [n_angles][n_det_z][n_det_y]. dtype: CTSM_F64/CTSM_F32.
+ * Results are deterministic (fixed-point accumulation for the scatter). */
+int ctsm_fwd_mf(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begin,
+                int angle_end, int angle_step, const void* x_dev, void* y_dev, void* stream);
+int ctsm_bwd_mf(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begin,
+                int angle_end, int angle_step, const void* y_dev, void* x_dev, void* stream);
+
+/* ---- K7/K8: SIRT pieces (BASELINE.json configs[4]) ----------------------
+ * x <- x + C .* A^T (R .* (y - A x)), R = 1/(A 1), C = 1/(A^T 1), zero sums -> 0.
+ * ctsm_sirt_residual: r = R .* (y - ax) over the shard's rows, with R
+ * supplied as inverse row sums (elementwise, n = rows of the shard's angles).
+ * ctsm_sirt_update: x += C .* bp; both arrays full-size. ctsm_invert_nonzero
+ * turns sums into inverse sums (0 stays 0). Multi-GPU drivers all-reduce bp
+ * (and A^T 1) between ctsm_bwd_mf and ctsm_sirt_update. */
+int ctsm_invert_nonzero(ctsm_ctx* ctx, int dtype, uint64_t n, void* v_dev, void* stream);
+int ctsm_sirt_residual(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begin,
+                       int angle_end, int angle_step, const void* y_dev, const void* rinv_dev,
+                       void* ax_inout_dev, void* stream);
+int ctsm_sirt_update(ctsm_ctx* ctx, int dtype, uint64_t n, const void* cinv_dev,
+                     const void* bp_dev, void* x_inout_dev, void* stream);
+/* Full single-device SIRT driver: iters iterations from x_inout. */
+int ctsm_sirt(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, const void* y_dev,
+              void* x_inout_dev, int iters, void* stream);
+
+/* ---- host-buffer entry points (the reference's value-semantics calls,
+ * used for end-to-end timing; copies in/out of pinned staging inside) ---- */
+int ctsm_forward_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,
+                                          const double* x_host, double* y_host);
+int ctsm_back_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,
+                                       const double* y_host, double* x_host);
+
+/* ---- diagnostics ---------------------------------------------------------
+ * Measured FP64 FMA throughput of `device` in TFLOP/s (FMA = 2 flops): the
+ * FP64 roofline denominator used by bench.py (MEASURED_PEAKS.json has none). */
+double ctsm_bench_dfma(int device);
+
+#ifdef __cplusplus
+}
+#endif

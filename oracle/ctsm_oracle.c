@@ -1068,3 +1068,18 @@ int ref_angle_column_sums(const o_geom* g, int ip, double* sums) {
   O_TRY(angle_block_entries(g, ip, colsum_emit, &c););
   return 0;
 }
+
+#ifdef CTSM_ORACLE_CRMATH
+/* crmath entry points for tests/test_crmath.py (correct-rounding checks). */
+void orc_crm_eval(int fn, const double* a, const double* b, double* out, long n) {
+  for (long i = 0; i < n; ++i) {
+    switch (fn) {
+      case 0: out[i] = crm_sin(a[i]); break;
+      case 1: out[i] = crm_cos(a[i]); break;
+      case 2: out[i] = crm_tan(a[i]); break;
+      case 3: out[i] = crm_atan(a[i]); break;
+      default: out[i] = crm_atan2(a[i], b[i]); break;
+    }
+  }
+}
+#endif

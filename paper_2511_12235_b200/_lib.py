@@ -1,0 +1,75 @@
+"""ctypes binding of libctsm_b200.so (include/ctsm_b200.h).
+
+The library is the product: there is no CPU fallback. If the shared library is
+missing the import of any projector function fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .geometry import CGeometry, CtsmError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libctsm_b200.so")
+
+CTSM_F64 = 0
+CTSM_F32 = 1
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_U64 = ctypes.c_uint64
+_GP = ctypes.POINTER(CGeometry)
+
+# name -> (restype, argtypes); mirrors include/ctsm_b200.h
+SIGNATURES = {
+    "ctsm_create": (_I, [_I, ctypes.POINTER(_P)]),
+    "ctsm_destroy": (_I, [_P]),
+    "ctsm_last_error": (ctypes.c_char_p, []),
+    "ctsm_version": (ctypes.c_char_p, []),
+    "ctsm_launch_count": (_U64, []),
+    "ctsm_validate_geometry": (_I, [_GP]),
+    "ctsm_csr_count": (_I, [_P, _GP, _I, _I, _U64, _P, ctypes.POINTER(_U64), _P]),
+    "ctsm_csr_fill": (_I, [_P, _GP, _I, _I, _P, _P, _P, _P]),
+    "ctsm_spmv": (_I, [_P, _U64, _U64, _P, _P, _P, _P, _P, _P]),
+    "ctsm_spmv_t": (_I, [_P, _U64, _U64, _P, _P, _P, _P, _P, _P]),
+    "ctsm_fwd_mf": (_I, [_P, _GP, _I, _I, _I, _I, _P, _P, _P]),
+    "ctsm_bwd_mf": (_I, [_P, _GP, _I, _I, _I, _I, _P, _P, _P]),
+    "ctsm_invert_nonzero": (_I, [_P, _I, _U64, _P, _P]),
+    "ctsm_sirt_residual": (_I, [_P, _GP, _I, _I, _I, _I, _P, _P, _P, _P]),
+    "ctsm_sirt_update": (_I, [_P, _I, _U64, _P, _P, _P, _P]),
+    "ctsm_sirt": (_I, [_P, _GP, _I, _P, _P, _I, _P]),
+    "ctsm_forward_project_matrix_free_host": (_I, [_P, _GP, _P, _P]),
+    "ctsm_back_project_matrix_free_host": (_I, [_P, _GP, _P, _P]),
+}
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Loads the CUDA library (fails loudly when it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build the CUDA extension first "
+                "(python -c 'import __graft_entry__ as g; g.build()')")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = lib().ctsm_last_error().decode(errors="replace")
+        if status == 100:
+            raise CtsmError("CudaError", msg)
+        raise CtsmError.from_status(status, msg.split(": ", 1)[-1])
+
+
+def launch_count() -> int:
+    return int(lib().ctsm_launch_count())

@@ -1,0 +1,533 @@
+// capi.cu -- the extern "C" boundary (include/ctsm_b200.h): context, geometry
+// validation, buffer management and the orchestration of the kernels in
+// csr.cu / mf.cu. Host code only.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "kernels.h"
+
+namespace ctsmb {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+namespace {
+
+thread_local std::string g_err;
+
+const char* kCodeNames[] = {"Ok",          "DegenerateGeometry", "RayParallelToFace",
+                            "SingularPhi", "CentralRow",         "ZRestrictionViolation",
+                            "DimensionMismatch", "NonFinite",    "ZeroMatrix",
+                            "TooLarge",    "InvalidSpec",        "OutOfMemory",
+                            "InvalidConfig", "IoFailure"};
+
+int fail(int code, const std::string& msg) {
+  const char* name = (code >= 0 && code <= 13) ? kCodeNames[code] : "CudaError";
+  g_err = std::string(name) + ": " + msg;
+  return code;
+}
+
+#define CT_CUDA(expr)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (expr);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      if (e_ == cudaErrorMemoryAllocation) {                                       \
+        cudaGetLastError();                                                        \
+        return fail(CTSM_ERR_OUT_OF_MEMORY, std::string("device allocation: ") +   \
+                                                cudaGetErrorString(e_));           \
+      }                                                                            \
+      return fail(CTSM_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    }                                                                              \
+  } while (0)
+
+#define CT_TRY(expr)          \
+  do {                        \
+    const int s_ = (expr);    \
+    if (s_ != 0) return s_;   \
+  } while (0)
+
+struct Buf {
+  void* p = nullptr;
+  size_t n = 0;
+};
+
+}  // namespace
+}  // namespace ctsmb
+
+using namespace ctsmb;
+
+struct ctsm_ctx {
+  int device = 0;
+  int* status = nullptr;        // device status word
+  double* dred = nullptr;       // device reduction scratch (4 doubles)
+  int* h_status = nullptr;      // pinned
+  double* h_red = nullptr;      // pinned
+  Buf angles, edges, cs, counts, scan, longrows, acc, tmp_a, tmp_b, tmp_c, tmp_d, tmp_e, tmp_f;
+};
+
+namespace {
+
+int ensure(ctsm_ctx* ctx, Buf& b, size_t bytes) {
+  if (b.n >= bytes && b.p) return 0;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.n = 0;
+  if (bytes == 0) return 0;
+  CT_CUDA(cudaMalloc(&b.p, bytes));
+  b.n = bytes;
+  (void)ctx;
+  return 0;
+}
+
+int set_device(ctsm_ctx* ctx) {
+  if (!ctx) return fail(CTSM_ERR_INVALID_SPEC, "null context");
+  CT_CUDA(cudaSetDevice(ctx->device));
+  return 0;
+}
+
+// Synchronises the stream and converts a raised device guard into its code.
+int check_status(ctsm_ctx* ctx, cudaStream_t st, const char* what) {
+  CT_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CT_CUDA(cudaStreamSynchronize(st));
+  const int code = *ctx->h_status;
+  if (code != 0) {
+    CT_CUDA(cudaMemsetAsync(ctx->status, 0, sizeof(int), st));
+    CT_CUDA(cudaStreamSynchronize(st));
+    const char* msg = "device guard raised";
+    switch (code) {
+      case CTSM_ERR_DEGENERATE_GEOMETRY: msg = "point on or behind the source plane / no canonical quadrant"; break;
+      case CTSM_ERR_NON_FINITE: msg = "negative weight beyond FP tolerance or non-finite result"; break;
+      case CTSM_ERR_TOO_LARGE: msg = "sweep exceeds the device breakpoint capacity"; break;
+      case CTSM_ERR_RAY_PARALLEL_TO_FACE: msg = "band ray parallel to x-faces"; break;
+      default: break;
+    }
+    return fail(code, std::string(what) + ": " + msg);
+  }
+  return 0;
+}
+
+// ScanGeometry::validate (geometry.cpp:27-54).
+int validate(const ctsm_geometry* g) {
+  if (!g) return fail(CTSM_ERR_INVALID_SPEC, "null geometry");
+  if (!(g->s > 0.0)) return fail(CTSM_ERR_INVALID_SPEC, "source distance s must be > 0");
+  if (!(g->d >= 0.0)) return fail(CTSM_ERR_INVALID_SPEC, "detector distance d must be >= 0");
+  if (!(g->d_y > 0.0) || !(g->d_z > 0.0))
+    return fail(CTSM_ERR_INVALID_SPEC, "detector pitches must be > 0");
+  if (g->n_det_y <= 0 || g->n_det_z <= 0 || g->n_angles <= 0)
+    return fail(CTSM_ERR_INVALID_SPEC, "detector and angle counts must be > 0");
+  if (g->n_det_y % 2 != 0)
+    return fail(CTSM_ERR_INVALID_SPEC, "n_det_y must be even (centered detector)");
+  if (g->n_det_z != 1 && g->n_det_z % 2 != 0)
+    return fail(CTSM_ERR_INVALID_SPEC, "n_det_z must be 1 (2D) or even (centered detector)");
+  if (!(g->a > 0.0) || !(g->b > 0.0) || !(g->c > 0.0))
+    return fail(CTSM_ERR_INVALID_SPEC, "voxel sizes must be > 0");
+  if (g->n_x <= 0 || g->n_y <= 0 || g->n_z <= 0)
+    return fail(CTSM_ERR_INVALID_SPEC, "grid dimensions must be > 0");
+  if (g->n_det_z == 1 && g->n_z > 1)
+    return fail(CTSM_ERR_INVALID_SPEC, "volume grid requires n_det_z > 1");
+  if (!(g->angle_end > g->angle_start))
+    return fail(CTSM_ERR_INVALID_SPEC, "angle_end must exceed angle_start");
+  if (!std::isfinite(g->s) || !std::isfinite(g->d) || !std::isfinite(g->d_y) ||
+      !std::isfinite(g->d_z) || !std::isfinite(g->a) || !std::isfinite(g->b) ||
+      !std::isfinite(g->c) || !std::isfinite(g->angle_start) || !std::isfinite(g->angle_end))
+    return fail(CTSM_ERR_NON_FINITE, "geometry parameters must be finite");
+  const double rx = g->n_x * g->a / 2.0, ry = g->n_y * g->b / 2.0;
+  if (g->s <= std::hypot(rx, ry))
+    return fail(CTSM_ERR_DEGENERATE_GEOMETRY, "source circle intersects the grid");
+  return 0;
+}
+
+// Derived device geometry incl. the edge-table extent: every fan angle of the
+// grid satisfies |tan| <= R / (s - R), R the grid half-diagonal.
+int dev_geom(const ctsm_geometry* g, DevGeom* out) {
+  CT_TRY(validate(g));
+  DevGeom d = make_dev_geom(*g);
+  const double R = std::hypot(g->n_x * g->a / 2.0, g->n_y * g->b / 2.0);
+  const double umax = R / (g->s - R) * (g->s + g->d) / g->d_y;
+  if (!(umax < (double)(1 << 22)))
+    return fail(CTSM_ERR_TOO_LARGE, "fan spans too many detector edges for the edge table");
+  const int E = (int)std::ceil(umax) + 3;
+  d.edge_lo = -E;
+  d.n_edges = 2 * E + 1;
+  *out = d;
+  return 0;
+}
+
+// Upper bound of any row sum of A (sum of voxel fractions in one detector
+// cell's ray wedge): the wedge's area / volume inside the depth slab
+// |depth - s| <= R divided by the pixel area / voxel volume.
+double row_sum_bound(const ctsm_geometry* g) {
+  const double R2 = std::hypot(g->n_x * g->a / 2.0, g->n_y * g->b / 2.0);
+  const double dt = g->d_y / (g->s + g->d);
+  const bool two_d = (g->n_z == 1 && g->n_det_z == 1);
+  if (two_d) return 2.0 * g->s * R2 * dt / (g->a * g->b);
+  const double da = g->d_z / (g->s + g->d);
+  const double hi = g->s + R2, lo = g->s - R2;
+  return dt * da * (hi * hi * hi - lo * lo * lo) / 3.0 / (g->a * g->b * g->c);
+}
+
+int n_in_shard(int begin, int end, int step) {
+  if (step <= 0 || end <= begin) return 0;
+  return (end - begin + step - 1) / step;
+}
+
+int check_shard(const ctsm_geometry* g, int begin, int end, int step) {
+  if (begin < 0 || end > g->n_angles || begin > end || step <= 0)
+    return fail(CTSM_ERR_INVALID_SPEC, "angle shard out of range");
+  return 0;
+}
+
+size_t dtype_size(int dtype) { return dtype == CTSM_F64 ? 8 : 4; }
+
+int check_dtype(int dtype) {
+  if (dtype != CTSM_F64 && dtype != CTSM_F32) return fail(CTSM_ERR_INVALID_SPEC, "unknown dtype");
+  return 0;
+}
+
+int fetch_max_abs(ctsm_ctx* ctx, int dtype, uint64_t n, const void* v, cudaStream_t st,
+                  double* out) {
+  CT_CUDA(max_abs(dtype, n, v, ctx->dred, st));
+  CT_CUDA(cudaMemcpyAsync(ctx->h_red, ctx->dred, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CT_CUDA(cudaStreamSynchronize(st));
+  *out = *ctx->h_red;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ctsm_create(int device, ctsm_ctx** out) {
+  if (!out) return fail(CTSM_ERR_INVALID_SPEC, "null output pointer");
+  int n = 0;
+  CT_CUDA(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(CTSM_ERR_INVALID_SPEC, "no such CUDA device");
+  CT_CUDA(cudaSetDevice(device));
+  ctsm_ctx* c = new ctsm_ctx();
+  c->device = device;
+  CT_CUDA(cudaMalloc(&c->status, sizeof(int)));
+  CT_CUDA(cudaMemset(c->status, 0, sizeof(int)));
+  CT_CUDA(cudaMalloc(&c->dred, 4 * sizeof(double)));
+  CT_CUDA(cudaMallocHost(&c->h_status, sizeof(int)));
+  CT_CUDA(cudaMallocHost(&c->h_red, 4 * sizeof(double)));
+  *out = c;
+  return 0;
+}
+
+int ctsm_destroy(ctsm_ctx* ctx) {
+  if (!ctx) return 0;
+  cudaSetDevice(ctx->device);
+  Buf* bufs[] = {&ctx->angles, &ctx->edges, &ctx->cs,    &ctx->counts, &ctx->scan,
+                 &ctx->longrows, &ctx->acc, &ctx->tmp_a, &ctx->tmp_b,  &ctx->tmp_c,
+                 &ctx->tmp_d, &ctx->tmp_e, &ctx->tmp_f};
+  for (Buf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  cudaFree(ctx->status);
+  cudaFree(ctx->dred);
+  cudaFreeHost(ctx->h_status);
+  cudaFreeHost(ctx->h_red);
+  delete ctx;
+  return 0;
+}
+
+const char* ctsm_last_error(void) { return g_err.c_str(); }
+const char* ctsm_version(void) { return "ctsm-b200 0.1 (sm_100a)"; }
+uint64_t ctsm_launch_count(void) { return g_launches.load(); }
+
+int ctsm_validate_geometry(const ctsm_geometry* g) {
+  DevGeom d;
+  return dev_geom(g, &d);
+}
+
+// ---- K1/K2 ----------------------------------------------------------------
+static int prepare_exact(ctsm_ctx* ctx, const DevGeom& d, int angle_begin, int n_sel,
+                         cudaStream_t st) {
+  CT_TRY(ensure(ctx, ctx->angles, (size_t)(n_sel > 0 ? n_sel : 1) * exact_angle_bytes()));
+  CT_TRY(ensure(ctx, ctx->edges, (size_t)d.n_edges * edge_angle_bytes()));
+  CT_CUDA(build_exact_tables(d, angle_begin, n_sel, ctx->angles.p, ctx->edges.p, st));
+  return 0;
+}
+
+int ctsm_csr_count(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int angle_end,
+                   uint64_t memory_budget_bytes, uint64_t* row_start_dev, uint64_t* nnz_out,
+                   void* stream) {
+  CT_TRY(set_device(ctx));
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  if ((uint64_t)g->n_x * g->n_y * g->n_z > 0xffffffffull)
+    return fail(CTSM_ERR_TOO_LARGE, "grid exceeds 2^32 voxel columns");
+  CT_TRY(check_shard(g, angle_begin, angle_end, 1));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_sel = angle_end - angle_begin;
+  const uint64_t rpa = (uint64_t)d.rows_per_angle;
+  const uint64_t n_rows = rpa * n_sel;
+  const uint64_t n_meas = rpa * (uint64_t)g->n_angles;
+  // memory-budget estimate from angle 0, as the reference (projector.cpp:155-169)
+  uint64_t nnz0 = 0;
+  {
+    CT_TRY(prepare_exact(ctx, d, 0, 1, st));
+    CT_TRY(ensure(ctx, ctx->counts, rpa * sizeof(unsigned)));
+    CT_TRY(ensure(ctx, ctx->tmp_a, (rpa + 1) * sizeof(uint64_t)));
+    CT_TRY(ensure(ctx, ctx->scan, scan_scratch_bytes(rpa)));
+    CT_CUDA(cudaMemsetAsync(ctx->counts.p, 0, rpa * sizeof(unsigned), st));
+    CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, 0, 1, 0, (unsigned*)ctx->counts.p, nullptr,
+                     nullptr, nullptr, ctx->status, st));
+    CT_CUDA(exclusive_scan_u32_u64((const unsigned*)ctx->counts.p, rpa, (uint64_t*)ctx->tmp_a.p,
+                                   ctx->scan.p, st));
+    CT_CUDA(cudaMemcpyAsync(&nnz0, (uint64_t*)ctx->tmp_a.p + rpa, sizeof(uint64_t),
+                            cudaMemcpyDeviceToHost, st));
+    CT_TRY(check_status(ctx, st, "build_system_matrix"));
+    const uint64_t est_nnz = nnz0 * (uint64_t)g->n_angles;
+    const uint64_t est_bytes = est_nnz * (sizeof(uint32_t) + sizeof(double)) +
+                               (n_meas + 1) * sizeof(uint64_t);
+    if (est_bytes > memory_budget_bytes) {
+      char msg[256];
+      snprintf(msg, sizeof msg, "estimated %llu entries (%llu MiB) exceed the budget of %llu MiB",
+               (unsigned long long)est_nnz, (unsigned long long)(est_bytes >> 20),
+               (unsigned long long)(memory_budget_bytes >> 20));
+      return fail(CTSM_ERR_OUT_OF_MEMORY, msg);
+    }
+  }
+  CT_TRY(prepare_exact(ctx, d, angle_begin, n_sel, st));
+  CT_TRY(ensure(ctx, ctx->counts, n_rows * sizeof(unsigned)));
+  CT_TRY(ensure(ctx, ctx->scan, scan_scratch_bytes(n_rows)));
+  CT_CUDA(cudaMemsetAsync(ctx->counts.p, 0, n_rows * sizeof(unsigned), st));
+  CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, angle_begin, n_sel, 0,
+                   (unsigned*)ctx->counts.p, nullptr, nullptr, nullptr, ctx->status, st));
+  CT_CUDA(exclusive_scan_u32_u64((const unsigned*)ctx->counts.p, n_rows, row_start_dev,
+                                 ctx->scan.p, st));
+  uint64_t nnz = 0;
+  CT_CUDA(cudaMemcpyAsync(&nnz, row_start_dev + n_rows, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                          st));
+  CT_TRY(check_status(ctx, st, "build_system_matrix"));
+  if (angle_begin == 0 && angle_end == g->n_angles && nnz == 0)
+    return fail(CTSM_ERR_ZERO_MATRIX, "system matrix has no entries");
+  *nnz_out = nnz;
+  return 0;
+}
+
+int ctsm_csr_fill(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int angle_end,
+                  const uint64_t* row_start_dev, uint32_t* col_dev, double* val_dev,
+                  void* stream) {
+  CT_TRY(set_device(ctx));
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  CT_TRY(check_shard(g, angle_begin, angle_end, 1));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_sel = angle_end - angle_begin;
+  const uint64_t n_rows = (uint64_t)d.rows_per_angle * n_sel;
+  CT_TRY(prepare_exact(ctx, d, angle_begin, n_sel, st));
+  CT_TRY(ensure(ctx, ctx->counts, n_rows * sizeof(unsigned)));
+  CT_TRY(ensure(ctx, ctx->longrows, (n_rows + 1) * sizeof(unsigned)));
+  CT_CUDA(cudaMemsetAsync(ctx->counts.p, 0, n_rows * sizeof(unsigned), st));
+  CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, angle_begin, n_sel, 1,
+                   (unsigned*)ctx->counts.p, row_start_dev, col_dev, val_dev, ctx->status, st));
+  unsigned* nlong = (unsigned*)ctx->longrows.p + n_rows;
+  CT_CUDA(csr_sort_rows(n_rows, row_start_dev, col_dev, val_dev, (unsigned*)ctx->longrows.p, nlong,
+                        ctx->status, st));
+  return check_status(ctx, st, "build_system_matrix");
+}
+
+// ---- K3/K4 ----------------------------------------------------------------
+int ctsm_spmv(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols, const uint64_t* row_start_dev,
+              const uint32_t* col_dev, const double* val_dev, const double* x_dev,
+              double* y_dev, void* stream) {
+  CT_TRY(set_device(ctx));
+  (void)n_cols;
+  cudaStream_t st = (cudaStream_t)stream;
+  CT_CUDA(spmv_csr(n_rows, row_start_dev, col_dev, val_dev, x_dev, y_dev, ctx->status, st));
+  const int s = check_status(ctx, st, "forward projection");
+  if (s == CTSM_ERR_NON_FINITE) return fail(s, "forward projection not finite");
+  return s;
+}
+
+int ctsm_spmv_t(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols, const uint64_t* row_start_dev,
+                const uint32_t* col_dev, const double* val_dev, const double* y_dev,
+                double* x_dev, void* stream) {
+  CT_TRY(set_device(ctx));
+  cudaStream_t st = (cudaStream_t)stream;
+  // fixed-point bound: |x_c| <= max|y| * max_c sum_r |A_rc|
+  CT_TRY(ensure(ctx, ctx->tmp_a, n_cols * sizeof(double)));
+  CT_CUDA(cudaMemsetAsync(ctx->tmp_a.p, 0, n_cols * sizeof(double), st));
+  CT_CUDA(colsum_abs(n_rows, row_start_dev, col_dev, val_dev, (double*)ctx->tmp_a.p, st));
+  double mcol = 0.0, my = 0.0;
+  CT_TRY(fetch_max_abs(ctx, CTSM_F64, n_cols, ctx->tmp_a.p, st, &mcol));
+  CT_TRY(fetch_max_abs(ctx, CTSM_F64, n_rows, y_dev, st, &my));
+  if (!std::isfinite(mcol) || !std::isfinite(my))
+    return fail(CTSM_ERR_NON_FINITE, "back projection not finite");
+  const double B = mcol * my * (1.0 + 1e-6);
+  if (!(B > 0.0)) {
+    CT_CUDA(cudaMemsetAsync(x_dev, 0, n_cols * sizeof(double), st));
+    CT_CUDA(cudaStreamSynchronize(st));
+    return 0;
+  }
+  const double scale = std::ldexp(1.0, 61) / B;
+  CT_TRY(ensure(ctx, ctx->tmp_b, n_cols * sizeof(unsigned long long)));
+  CT_CUDA(cudaMemsetAsync(ctx->tmp_b.p, 0, n_cols * sizeof(unsigned long long), st));
+  CT_CUDA(spmvt_csr_fixed(n_rows, row_start_dev, col_dev, val_dev, y_dev,
+                          (unsigned long long*)ctx->tmp_b.p, scale, st));
+  CT_CUDA(fixed_to_double(n_cols, (const unsigned long long*)ctx->tmp_b.p, scale, x_dev, st));
+  return check_status(ctx, st, "back projection");
+}
+
+// ---- K5/K6 ----------------------------------------------------------------
+static int prepare_cs(ctsm_ctx* ctx, const DevGeom& d, int begin, int step, int n_sel,
+                      cudaStream_t st) {
+  CT_TRY(ensure(ctx, ctx->cs, (size_t)(n_sel > 0 ? n_sel : 1) * sizeof(AngleCS)));
+  CT_CUDA(build_angle_cs(d, begin, step, n_sel, (AngleCS*)ctx->cs.p, st));
+  return 0;
+}
+
+static int fwd_impl(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int begin, int end,
+                    int step, const void* x, void* y, cudaStream_t st) {
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  CT_TRY(check_dtype(dtype));
+  CT_TRY(check_shard(g, begin, end, step));
+  const int n_sel = n_in_shard(begin, end, step);
+  if (n_sel == 0) return 0;
+  const uint64_t n_meas = (uint64_t)d.rows_per_angle * g->n_angles;
+  double mx = 0.0;
+  CT_TRY(fetch_max_abs(ctx, dtype, (uint64_t)d.n_vox, x, st, &mx));
+  if (!std::isfinite(mx)) return fail(CTSM_ERR_NON_FINITE, "image not finite");
+  CT_TRY(prepare_cs(ctx, d, begin, step, n_sel, st));
+  CT_TRY(ensure(ctx, ctx->acc, n_meas * sizeof(unsigned long long)));
+  unsigned long long* acc = (unsigned long long*)ctx->acc.p;
+  CT_CUDA(zero_rows_u64(d, begin, step, n_sel, acc, st));
+  const double B = mx * row_sum_bound(g) * 1.05;
+  const double scale = B > 0.0 ? std::ldexp(1.0, 61) / B : 1.0;
+  if (B > 0.0)
+    CT_CUDA(fwd_mf(d, dtype, (const AngleCS*)ctx->cs.p, begin, step, n_sel, x, acc, scale,
+                   ctx->status, st));
+  CT_CUDA(fixed_to_float_rows(d, dtype, begin, step, n_sel, acc, scale, y, st));
+  return 0;
+}
+
+static int bwd_impl(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int begin, int end,
+                    int step, const void* y, void* x, cudaStream_t st) {
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  CT_TRY(check_dtype(dtype));
+  CT_TRY(check_shard(g, begin, end, step));
+  const int n_sel = n_in_shard(begin, end, step);
+  CT_TRY(prepare_cs(ctx, d, begin, step, n_sel, st));
+  CT_CUDA(bwd_mf(d, dtype, (const AngleCS*)ctx->cs.p, begin, step, n_sel, y, x, ctx->status, st));
+  return 0;
+}
+
+int ctsm_fwd_mf(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begin,
+                int angle_end, int angle_step, const void* x_dev, void* y_dev, void* stream) {
+  CT_TRY(set_device(ctx));
+  cudaStream_t st = (cudaStream_t)stream;
+  CT_TRY(fwd_impl(ctx, g, dtype, angle_begin, angle_end, angle_step, x_dev, y_dev, st));
+  return check_status(ctx, st, "forward_project_matrix_free");
+}
+
+int ctsm_bwd_mf(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begin,
+                int angle_end, int angle_step, const void* y_dev, void* x_dev, void* stream) {
+  CT_TRY(set_device(ctx));
+  cudaStream_t st = (cudaStream_t)stream;
+  CT_TRY(bwd_impl(ctx, g, dtype, angle_begin, angle_end, angle_step, y_dev, x_dev, st));
+  return check_status(ctx, st, "back_project_matrix_free");
+}
+
+// ---- K7/K8 ----------------------------------------------------------------
+int ctsm_invert_nonzero(ctsm_ctx* ctx, int dtype, uint64_t n, void* v_dev, void* stream) {
+  CT_TRY(set_device(ctx));
+  CT_TRY(check_dtype(dtype));
+  CT_CUDA(invert_nonzero(dtype, n, v_dev, (cudaStream_t)stream));
+  return 0;
+}
+
+int ctsm_sirt_residual(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begin,
+                       int angle_end, int angle_step, const void* y_dev, const void* rinv_dev,
+                       void* ax_inout_dev, void* stream) {
+  CT_TRY(set_device(ctx));
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  CT_TRY(check_dtype(dtype));
+  CT_TRY(check_shard(g, angle_begin, angle_end, angle_step));
+  CT_CUDA(sirt_residual(d, dtype, angle_begin, angle_step,
+                        n_in_shard(angle_begin, angle_end, angle_step), y_dev, rinv_dev,
+                        ax_inout_dev, (cudaStream_t)stream));
+  return 0;
+}
+
+int ctsm_sirt_update(ctsm_ctx* ctx, int dtype, uint64_t n, const void* cinv_dev,
+                     const void* bp_dev, void* x_inout_dev, void* stream) {
+  CT_TRY(set_device(ctx));
+  CT_TRY(check_dtype(dtype));
+  CT_CUDA(sirt_update(dtype, n, cinv_dev, bp_dev, x_inout_dev, (cudaStream_t)stream));
+  return 0;
+}
+
+int ctsm_sirt(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, const void* y_dev,
+              void* x_inout_dev, int iters, void* stream) {
+  CT_TRY(set_device(ctx));
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  CT_TRY(check_dtype(dtype));
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t nv = (uint64_t)d.n_vox;
+  const uint64_t nm = (uint64_t)d.rows_per_angle * g->n_angles;
+  const size_t es = dtype_size(dtype);
+  CT_TRY(ensure(ctx, ctx->tmp_c, nm * es));  // R (inverse row sums)
+  CT_TRY(ensure(ctx, ctx->tmp_d, nv * es));  // C (inverse column sums)
+  CT_TRY(ensure(ctx, ctx->tmp_e, nm * es));  // A x / residual
+  CT_TRY(ensure(ctx, ctx->tmp_f, nv * es));  // A^T r / ones
+  const int n = g->n_angles;
+  // R = 1 / (A 1)
+  CT_CUDA(fill_value(dtype, nv, 1.0, ctx->tmp_f.p, st));
+  CT_TRY(fwd_impl(ctx, g, dtype, 0, n, 1, ctx->tmp_f.p, ctx->tmp_c.p, st));
+  CT_CUDA(invert_nonzero(dtype, nm, ctx->tmp_c.p, st));
+  // C = 1 / (A^T 1)
+  CT_CUDA(fill_value(dtype, nm, 1.0, ctx->tmp_e.p, st));
+  CT_TRY(bwd_impl(ctx, g, dtype, 0, n, 1, ctx->tmp_e.p, ctx->tmp_d.p, st));
+  CT_CUDA(invert_nonzero(dtype, nv, ctx->tmp_d.p, st));
+  CT_TRY(check_status(ctx, st, "sirt"));
+  for (int it = 0; it < iters; ++it) {
+    CT_TRY(fwd_impl(ctx, g, dtype, 0, n, 1, x_inout_dev, ctx->tmp_e.p, st));
+    CT_CUDA(sirt_residual(d, dtype, 0, 1, n, y_dev, ctx->tmp_c.p, ctx->tmp_e.p, st));
+    CT_TRY(bwd_impl(ctx, g, dtype, 0, n, 1, ctx->tmp_e.p, ctx->tmp_f.p, st));
+    CT_CUDA(sirt_update(dtype, nv, ctx->tmp_d.p, ctx->tmp_f.p, x_inout_dev, st));
+  }
+  return check_status(ctx, st, "sirt");
+}
+
+// ---- host-buffer entry points ------------------------------------------------
+int ctsm_forward_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,
+                                          const double* x_host, double* y_host) {
+  CT_TRY(set_device(ctx));
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  const uint64_t nv = (uint64_t)d.n_vox, nm = (uint64_t)d.rows_per_angle * g->n_angles;
+  CT_TRY(ensure(ctx, ctx->tmp_a, nv * sizeof(double)));
+  CT_TRY(ensure(ctx, ctx->tmp_b, nm * sizeof(double)));
+  cudaStream_t st = nullptr;
+  CT_CUDA(cudaMemcpyAsync(ctx->tmp_a.p, x_host, nv * sizeof(double), cudaMemcpyHostToDevice, st));
+  CT_TRY(fwd_impl(ctx, g, CTSM_F64, 0, g->n_angles, 1, ctx->tmp_a.p, ctx->tmp_b.p, st));
+  CT_CUDA(cudaMemcpyAsync(y_host, ctx->tmp_b.p, nm * sizeof(double), cudaMemcpyDeviceToHost, st));
+  return check_status(ctx, st, "forward_project_matrix_free");
+}
+
+int ctsm_back_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,
+                                       const double* y_host, double* x_host) {
+  CT_TRY(set_device(ctx));
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  const uint64_t nv = (uint64_t)d.n_vox, nm = (uint64_t)d.rows_per_angle * g->n_angles;
+  CT_TRY(ensure(ctx, ctx->tmp_a, nv * sizeof(double)));
+  CT_TRY(ensure(ctx, ctx->tmp_b, nm * sizeof(double)));
+  cudaStream_t st = nullptr;
+  CT_CUDA(cudaMemcpyAsync(ctx->tmp_b.p, y_host, nm * sizeof(double), cudaMemcpyHostToDevice, st));
+  CT_TRY(bwd_impl(ctx, g, CTSM_F64, 0, g->n_angles, 1, ctx->tmp_b.p, ctx->tmp_a.p, st));
+  CT_CUDA(cudaMemcpyAsync(x_host, ctx->tmp_a.p, nv * sizeof(double), cudaMemcpyDeviceToHost, st));
+  return check_status(ctx, st, "back_project_matrix_free");
+}
+
+}  // extern "C"
+
+extern "C" double ctsm_bench_dfma(int device) { return ctsmb::bench_dfma_tflops(device); }

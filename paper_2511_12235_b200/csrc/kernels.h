@@ -1,0 +1,84 @@
+// kernels.h -- host-side launchers shared between the compilation units.
+// csr.cu (compiled with -fmad=false: bit-exact emission) and mf.cu (matrix-free
+// projectors) implement them; capi.cu orchestrates.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace ctsmb {
+
+namespace exact {
+struct ExactAngle;
+struct EdgeAngle;
+}  // namespace exact
+
+// Global launch counter (reported by ctsm_launch_count).
+void count_launch(int n = 1);
+
+// ---- csr.cu --------------------------------------------------------------
+size_t exact_angle_bytes();
+size_t edge_angle_bytes();
+cudaError_t build_exact_tables(const DevGeom& g, int angle_begin, int n_sel, void* angles_dev,
+                               void* edges_dev, cudaStream_t st);
+// mode 0: count entries per row into row_counter (u32, zeroed by caller);
+// mode 1: fill col/val using row_start and row_counter as slot cursors (zeroed).
+cudaError_t csr_emit(const DevGeom& g, const void* angles_dev, const void* edges_dev,
+                     int angle_begin, int n_sel, int mode, unsigned* row_counter,
+                     const uint64_t* row_start, uint32_t* col, double* val, int* status,
+                     cudaStream_t st);
+// row_start[0..n] = exclusive scan of counts[0..n-1] (u32 -> u64); scratch
+// needs scan_scratch_bytes(n).
+size_t scan_scratch_bytes(uint64_t n);
+cudaError_t exclusive_scan_u32_u64(const unsigned* counts, uint64_t n, uint64_t* row_start,
+                                   void* scratch, cudaStream_t st);
+// Sort each row's entries by column (in place).
+cudaError_t csr_sort_rows(uint64_t n_rows, const uint64_t* row_start, uint32_t* col,
+                          double* val, unsigned* long_rows, unsigned* n_long, int* status,
+                          cudaStream_t st);
+cudaError_t spmv_csr(uint64_t n_rows, const uint64_t* row_start, const uint32_t* col,
+                     const double* val, const double* x, double* y, int* status, cudaStream_t st);
+cudaError_t colsum_abs(uint64_t n_rows, const uint64_t* row_start, const uint32_t* col,
+                       const double* val, double* colsum, cudaStream_t st);
+cudaError_t spmvt_csr_fixed(uint64_t n_rows, const uint64_t* row_start, const uint32_t* col,
+                            const double* val, const double* y, unsigned long long* acc,
+                            double scale, cudaStream_t st);
+
+// ---- mf.cu ---------------------------------------------------------------
+struct AngleCS {
+  double C, S;
+};
+cudaError_t build_angle_cs(const DevGeom& g, int angle_begin, int angle_step, int n_sel,
+                           AngleCS* out, cudaStream_t st);
+// dtype: CTSM_F64 / CTSM_F32
+cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
+                   int angle_step, int n_sel, const void* x, unsigned long long* yacc,
+                   double scale, int* status, cudaStream_t st);
+cudaError_t bwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
+                   int angle_step, int n_sel, const void* y, void* x, int* status,
+                   cudaStream_t st);
+// y rows of the shard <- acc / scale (and acc rows zeroed for reuse)
+cudaError_t fixed_to_float_rows(const DevGeom& g, int dtype, int angle_begin, int angle_step,
+                                int n_sel, unsigned long long* acc, double scale, void* y,
+                                cudaStream_t st);
+cudaError_t fixed_to_double(uint64_t n, const unsigned long long* acc, double scale, double* out,
+                            cudaStream_t st);
+cudaError_t zero_rows_u64(const DevGeom& g, int angle_begin, int angle_step, int n_sel,
+                          unsigned long long* acc, cudaStream_t st);
+// max |v| over n elements -> *out (device double), dtype-aware
+cudaError_t max_abs(int dtype, uint64_t n, const void* v, double* out_dev, cudaStream_t st);
+cudaError_t invert_nonzero(int dtype, uint64_t n, void* v, cudaStream_t st);
+cudaError_t sirt_residual(const DevGeom& g, int dtype, int angle_begin, int angle_step,
+                          int n_sel, const void* y, const void* rinv, void* ax,
+                          cudaStream_t st);
+cudaError_t sirt_update(int dtype, uint64_t n, const void* cinv, const void* bp, void* x,
+                        cudaStream_t st);
+cudaError_t fill_value(int dtype, uint64_t n, double v, void* out, cudaStream_t st);
+
+}  // namespace ctsmb
+
+namespace ctsmb {
+// Measured FP64 FMA throughput of the device in TFLOP/s (FMA = 2 flops).
+double bench_dfma_tflops(int device);
+}  // namespace ctsmb

@@ -1,0 +1,424 @@
+// mf.cu -- K5/K6 matrix-free projectors (forward_project_matrix_free,
+// projector.cpp:235-260, and its adjoint) plus the SIRT elementwise kernels.
+//
+// Weights are regenerated on the fly in FP64 (fast2d.cuh / fast3d.cuh) and
+// never stored. Forward (A x) is voxel-driven: each thread owns one
+// (pixel/voxel column, angle) work item and scatters w * x into a fixed-point
+// int64 sinogram accumulator (integer adds commute, so the result is
+// bit-reproducible for any schedule or GPU count). Backward (A^T y) is a
+// voxel-driven gather: each thread owns one pixel/voxel, loops over the angle
+// shard and accumulates in FP64 registers -- no atomics, deterministic.
+#include "fast2d.cuh"
+#include "fast3d.cuh"
+#include "kernels.h"
+
+namespace ctsmb {
+
+namespace {
+
+__global__ void angle_cs_kernel(DevGeom g, int angle_begin, int angle_step, int n, AngleCS* out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int i = angle_begin + k * angle_step;
+  const double phi = g.angle_start + (g.angle_end - g.angle_start) * i / g.n_angles;
+  double S, C;
+  sincos(phi, &S, &C);
+  out[k] = AngleCS{C, S};
+}
+
+template <typename T>
+__device__ __forceinline__ double ld(const T* p) {
+  return (double)__ldg(p);
+}
+
+// 2D pixel tile per block: 16 x 8 pixels, 128 threads.
+constexpr int kTx = 16, kTy = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(128) fwd2d_kernel(DevGeom g, const AngleCS* __restrict__ cs,
+                                                    int angle_begin, int angle_step,
+                                                    const T* __restrict__ x,
+                                                    unsigned long long* __restrict__ yacc,
+                                                    double scale, int* status) {
+  const int tiles_x = (g.n_x + kTx - 1) / kTx;
+  const int ix = (blockIdx.x % tiles_x) * kTx + (threadIdx.x % kTx);
+  const int iy = (blockIdx.x / tiles_x) * kTy + (threadIdx.x / kTx);
+  if (ix >= g.n_x || iy >= g.n_y) return;
+  const double xv = ld(&x[(long long)iy * g.n_x + ix]);
+  if (xv == 0.0) return;
+  const int k = blockIdx.y;
+  const int ip = angle_begin + k * angle_step;
+  const AngleCS a = cs[k];
+  unsigned long long* yrow = yacc + (long long)ip * g.rows_per_angle + g.n_det_y / 2;
+  const double xs = xv * scale;
+  fast::pixel_weights(g, a.C, a.S, ix, iy, status, [&](int m, double w) {
+    atomicAdd(&yrow[m], (unsigned long long)__double2ll_rn(w * xs));
+  });
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) bwd2d_kernel(DevGeom g, const AngleCS* __restrict__ cs,
+                                                    int angle_begin, int angle_step, int n_sel,
+                                                    const T* __restrict__ y, T* __restrict__ x,
+                                                    int* status) {
+  const int tiles_x = (g.n_x + kTx - 1) / kTx;
+  const int ix = (blockIdx.x % tiles_x) * kTx + (threadIdx.x % kTx);
+  const int iy = (blockIdx.x / tiles_x) * kTy + (threadIdx.x / kTx);
+  if (ix >= g.n_x || iy >= g.n_y) return;
+  double acc = 0.0;
+  for (int k = 0; k < n_sel; ++k) {
+    const int ip = angle_begin + k * angle_step;
+    const AngleCS a = cs[k];
+    const T* yrow = y + (long long)ip * g.rows_per_angle + g.n_det_y / 2;
+    fast::pixel_weights(g, a.C, a.S, ix, iy, status,
+                        [&](int m, double w) { acc += w * ld(&yrow[m]); });
+  }
+  x[(long long)iy * g.n_x + ix] = (T)acc;
+}
+
+// 3D: one thread per (voxel column, angle) for forward; per (voxel column,
+// z-chunk) looping over angles for backward.
+template <typename T>
+__global__ void __launch_bounds__(128) fwd3d_kernel(DevGeom g, const AngleCS* __restrict__ cs,
+                                                    int angle_begin, int angle_step,
+                                                    const T* __restrict__ x,
+                                                    unsigned long long* __restrict__ yacc,
+                                                    double scale, int* status) {
+  const int tiles_x = (g.n_x + kTx - 1) / kTx;
+  const int ix = (blockIdx.x % tiles_x) * kTx + (threadIdx.x % kTx);
+  const int iy = (blockIdx.x / tiles_x) * kTy + (threadIdx.x / kTx);
+  if (ix >= g.n_x || iy >= g.n_y) return;
+  const int k = blockIdx.y;
+  const int ip = angle_begin + k * angle_step;
+  const AngleCS a = cs[k];
+  unsigned long long* yblk = yacc + (long long)ip * g.rows_per_angle;
+  const long long plane = (long long)g.n_x * g.n_y;
+  const T* xcol = x + (long long)iy * g.n_x + ix;
+  fast::column_weights(
+      g, a.C, a.S, ix, iy, 0, g.n_z, status, [&](int iz) { return ld(&xcol[iz * plane]) * scale; },
+      [&](int iz, int m_y, int m_z, double w, double xs) {
+        atomicAdd(&yblk[(long long)(m_z + g.n_det_z / 2) * g.n_det_y + (m_y + g.n_det_y / 2)],
+                  (unsigned long long)__double2ll_rn(w * xs));
+      });
+}
+
+constexpr int kZChunk = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(128) bwd3d_kernel(DevGeom g, const AngleCS* __restrict__ cs,
+                                                    int angle_begin, int angle_step, int n_sel,
+                                                    const T* __restrict__ y, T* __restrict__ x,
+                                                    int* status) {
+  const int tiles_x = (g.n_x + kTx - 1) / kTx;
+  const int ix = (blockIdx.x % tiles_x) * kTx + (threadIdx.x % kTx);
+  const int iy = (blockIdx.x / tiles_x) * kTy + (threadIdx.x / kTx);
+  const int z0 = blockIdx.y * kZChunk;
+  if (ix >= g.n_x || iy >= g.n_y) return;
+  const int z1 = min(z0 + kZChunk, g.n_z);
+  double acc[kZChunk];
+#pragma unroll
+  for (int i = 0; i < kZChunk; ++i) acc[i] = 0.0;
+  for (int k = 0; k < n_sel; ++k) {
+    const int ip = angle_begin + k * angle_step;
+    const AngleCS a = cs[k];
+    const T* yblk = y + (long long)ip * g.rows_per_angle;
+    fast::column_weights(
+        g, a.C, a.S, ix, iy, z0, z1, status, [&](int) { return 1.0; },
+        [&](int iz, int m_y, int m_z, double w, double) {
+          const double yv =
+              ld(&yblk[(long long)(m_z + g.n_det_z / 2) * g.n_det_y + (m_y + g.n_det_y / 2)]);
+#pragma unroll
+          for (int i = 0; i < kZChunk; ++i)
+            if (iz - z0 == i) acc[i] += w * yv;
+        });
+  }
+  const long long plane = (long long)g.n_x * g.n_y;
+  for (int iz = z0; iz < z1; ++iz) x[iz * plane + (long long)iy * g.n_x + ix] = (T)acc[iz - z0];
+}
+
+template <typename T>
+__global__ void fixed_rows_kernel(int rpa, int angle_begin, int angle_step, int n_sel,
+                                  unsigned long long* acc, double inv_scale, T* y) {
+  const long long n = (long long)rpa * n_sel;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(i / rpa);
+    const long long r = (long long)(angle_begin + k * angle_step) * rpa + (i % rpa);
+    const long long q = (long long)acc[r];
+    y[r] = (T)((double)q * inv_scale);
+  }
+}
+
+__global__ void zero_rows_kernel(int rpa, int angle_begin, int angle_step, int n_sel,
+                                 unsigned long long* acc) {
+  const long long n = (long long)rpa * n_sel;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(i / rpa);
+    acc[(long long)(angle_begin + k * angle_step) * rpa + (i % rpa)] = 0ull;
+  }
+}
+
+__global__ void fixed_to_double_kernel(uint64_t n, const unsigned long long* acc, double inv_scale,
+                                       double* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (double)(long long)acc[i] * inv_scale;
+}
+
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  // valid for v >= 0: IEEE ordering of non-negative doubles == integer ordering
+  atomicMax((unsigned long long*)addr, (unsigned long long)__double_as_longlong(v));
+}
+
+template <typename T>
+__global__ void max_abs_kernel(uint64_t n, const T* v, double* out) {
+  double m = 0.0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double a = fabs((double)v[i]);
+    if (!(a <= m)) m = a;  // NaN propagates as "larger"
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out, m);
+}
+
+template <typename T>
+__global__ void invert_nonzero_kernel(uint64_t n, T* v) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const T a = v[i];
+    v[i] = a != (T)0 ? (T)(1.0 / (double)a) : (T)0;
+  }
+}
+
+template <typename T>
+__global__ void sirt_residual_kernel(int rpa, int angle_begin, int angle_step, int n_sel,
+                                     const T* y, const T* rinv, T* ax) {
+  const long long n = (long long)rpa * n_sel;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(i / rpa);
+    const long long r = (long long)(angle_begin + k * angle_step) * rpa + (i % rpa);
+    ax[r] = rinv[r] * (y[r] - ax[r]);
+  }
+}
+
+template <typename T>
+__global__ void sirt_update_kernel(uint64_t n, const T* cinv, const T* bp, T* x) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    x[i] += cinv[i] * bp[i];
+}
+
+template <typename T>
+__global__ void fill_kernel(uint64_t n, double v, T* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (T)v;
+}
+
+unsigned grid_for(uint64_t n) {
+  const uint64_t b = (n + 255) / 256;
+  const uint64_t cap = 148ull * 16;
+  return (unsigned)(b == 0 ? 1 : (b < cap ? b : cap));
+}
+
+}  // namespace
+
+cudaError_t build_angle_cs(const DevGeom& g, int angle_begin, int angle_step, int n_sel,
+                           AngleCS* out, cudaStream_t st) {
+  if (n_sel <= 0) return cudaSuccess;
+  angle_cs_kernel<<<(n_sel + 127) / 128, 128, 0, st>>>(g, angle_begin, angle_step, n_sel, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+static dim3 tile_grid(const DevGeom& g, unsigned ydim) {
+  const unsigned tiles = (unsigned)(((g.n_x + kTx - 1) / kTx) * ((g.n_y + kTy - 1) / kTy));
+  return dim3(tiles, ydim);
+}
+
+cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
+                   int angle_step, int n_sel, const void* x, unsigned long long* yacc,
+                   double scale, int* status, cudaStream_t st) {
+  if (n_sel <= 0) return cudaSuccess;
+  const bool two_d = (g.n_z == 1 && g.n_det_z == 1);
+  const dim3 grid = tile_grid(g, (unsigned)n_sel);
+  if (two_d) {
+    if (dtype == CTSM_F64)
+      fwd2d_kernel<double><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step,
+                                                 (const double*)x, yacc, scale, status);
+    else
+      fwd2d_kernel<float><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step,
+                                                (const float*)x, yacc, scale, status);
+  } else {
+    if (dtype == CTSM_F64)
+      fwd3d_kernel<double><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step,
+                                                 (const double*)x, yacc, scale, status);
+    else
+      fwd3d_kernel<float><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step,
+                                                (const float*)x, yacc, scale, status);
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t bwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
+                   int angle_step, int n_sel, const void* y, void* x, int* status,
+                   cudaStream_t st) {
+  const bool two_d = (g.n_z == 1 && g.n_det_z == 1);
+  if (two_d) {
+    const dim3 grid = tile_grid(g, 1);
+    if (dtype == CTSM_F64)
+      bwd2d_kernel<double><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step, n_sel,
+                                                 (const double*)y, (double*)x, status);
+    else
+      bwd2d_kernel<float><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step, n_sel,
+                                                (const float*)y, (float*)x, status);
+  } else {
+    const dim3 grid = tile_grid(g, (unsigned)((g.n_z + kZChunk - 1) / kZChunk));
+    if (dtype == CTSM_F64)
+      bwd3d_kernel<double><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step, n_sel,
+                                                 (const double*)y, (double*)x, status);
+    else
+      bwd3d_kernel<float><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step, n_sel,
+                                                (const float*)y, (float*)x, status);
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t fixed_to_float_rows(const DevGeom& g, int dtype, int angle_begin, int angle_step,
+                                int n_sel, unsigned long long* acc, double scale, void* y,
+                                cudaStream_t st) {
+  const uint64_t n = (uint64_t)g.rows_per_angle * n_sel;
+  if (dtype == CTSM_F64)
+    fixed_rows_kernel<double><<<grid_for(n), 256, 0, st>>>(g.rows_per_angle, angle_begin,
+                                                           angle_step, n_sel, acc, 1.0 / scale,
+                                                           (double*)y);
+  else
+    fixed_rows_kernel<float><<<grid_for(n), 256, 0, st>>>(g.rows_per_angle, angle_begin,
+                                                          angle_step, n_sel, acc, 1.0 / scale,
+                                                          (float*)y);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t zero_rows_u64(const DevGeom& g, int angle_begin, int angle_step, int n_sel,
+                          unsigned long long* acc, cudaStream_t st) {
+  const uint64_t n = (uint64_t)g.rows_per_angle * n_sel;
+  zero_rows_kernel<<<grid_for(n), 256, 0, st>>>(g.rows_per_angle, angle_begin, angle_step,
+                                                n_sel, acc);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t fixed_to_double(uint64_t n, const unsigned long long* acc, double scale, double* out,
+                            cudaStream_t st) {
+  fixed_to_double_kernel<<<grid_for(n), 256, 0, st>>>(n, acc, 1.0 / scale, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t max_abs(int dtype, uint64_t n, const void* v, double* out_dev, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out_dev, 0, sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  if (n == 0) return cudaSuccess;
+  if (dtype == CTSM_F64)
+    max_abs_kernel<double><<<grid_for(n), 256, 0, st>>>(n, (const double*)v, out_dev);
+  else
+    max_abs_kernel<float><<<grid_for(n), 256, 0, st>>>(n, (const float*)v, out_dev);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t invert_nonzero(int dtype, uint64_t n, void* v, cudaStream_t st) {
+  if (dtype == CTSM_F64)
+    invert_nonzero_kernel<double><<<grid_for(n), 256, 0, st>>>(n, (double*)v);
+  else
+    invert_nonzero_kernel<float><<<grid_for(n), 256, 0, st>>>(n, (float*)v);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t sirt_residual(const DevGeom& g, int dtype, int angle_begin, int angle_step,
+                          int n_sel, const void* y, const void* rinv, void* ax,
+                          cudaStream_t st) {
+  const uint64_t n = (uint64_t)g.rows_per_angle * n_sel;
+  if (dtype == CTSM_F64)
+    sirt_residual_kernel<double><<<grid_for(n), 256, 0, st>>>(
+        g.rows_per_angle, angle_begin, angle_step, n_sel, (const double*)y, (const double*)rinv,
+        (double*)ax);
+  else
+    sirt_residual_kernel<float><<<grid_for(n), 256, 0, st>>>(
+        g.rows_per_angle, angle_begin, angle_step, n_sel, (const float*)y, (const float*)rinv,
+        (float*)ax);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t sirt_update(int dtype, uint64_t n, const void* cinv, const void* bp, void* x,
+                        cudaStream_t st) {
+  if (dtype == CTSM_F64)
+    sirt_update_kernel<double><<<grid_for(n), 256, 0, st>>>(n, (const double*)cinv,
+                                                            (const double*)bp, (double*)x);
+  else
+    sirt_update_kernel<float><<<grid_for(n), 256, 0, st>>>(n, (const float*)cinv,
+                                                           (const float*)bp, (float*)x);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t fill_value(int dtype, uint64_t n, double v, void* out, cudaStream_t st) {
+  if (dtype == CTSM_F64)
+    fill_kernel<double><<<grid_for(n), 256, 0, st>>>(n, v, (double*)out);
+  else
+    fill_kernel<float><<<grid_for(n), 256, 0, st>>>(n, v, (float*)out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace ctsmb
+
+// ---- FP64 peak microkernel (roofline denominator) ---------------
+namespace ctsmb {
+namespace {
+__global__ void __launch_bounds__(256) dfma_kernel(double* out, int iters, double b, double c) {
+  double a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3;
+  double a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+    a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+  }
+  const double s = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+  if (s == 1.2345) out[0] = s;
+}
+}  // namespace
+
+double bench_dfma_tflops(int device) {
+  cudaSetDevice(device);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* out = nullptr;
+  cudaMalloc(&out, sizeof(double));
+  const int blocks = sms * 8, threads = 256, iters = 8192;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  dfma_kernel<<<blocks, threads>>>(out, 64, 0.999999, 1e-9);  // warm-up
+  cudaEventRecord(e0);
+  dfma_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-9);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  count_launch(2);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  const double flops = 2.0 * 8.0 * (double)blocks * threads * iters;
+  return ms > 0 ? flops / (ms * 1e-3) / 1e12 : 0.0;
+}
+}  // namespace ctsmb

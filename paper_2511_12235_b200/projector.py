@@ -1,0 +1,340 @@
+"""The reference's projector API (projector.hpp:12-79) on B200.
+
+Every function keeps the reference's name, argument meaning and error
+behaviour (raises ``CtsmError`` with the reference ErrorCode name):
+
+===============================  ==============================================
+reference (projector.hpp)        here
+===============================  ==============================================
+build_system_matrix   (41-44)    build_system_matrix -> SparseSystemMatrix
+forward_project       (47-48)    forward_project      (K3, CSR SpMV)
+back_project          (51-52)    back_project         (K4, transpose SpMV)
+forward_project_matrix_free      forward_project_matrix_free (K5)
+                      (56-59)
+(absent)                         back_project_matrix_free    (K6)
+spectral_norm_power   (63-64)    spectral_norm_power  (on K3/K4)
+scale_values          (66)       scale_values
+angle_column_sums     (69-70)    angle_column_sums    (K6 on one angle)
+(absent)                         sirt                 (K7/K8, BASELINE config 4)
+===============================  ==============================================
+
+Operands may be numpy arrays (host; results come back as numpy, like the
+reference's value semantics) or CUDA torch tensors (device-resident; results
+stay on the device). All compute runs in libctsm_b200.so; there is no CPU
+fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .geometry import CtsmError, ScanGeometry
+
+try:
+    import torch
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+
+DEFAULT_BUDGET = 5 << 30  # projector.hpp:43-44
+
+
+class MatrixMode:
+    consistent = "consistent"
+    line = "line"
+    multiline = "multiline"
+
+
+def parse_matrix_mode(text: str):
+    """projector.cpp:16-31 -> (mode, k)."""
+    if text == "consistent":
+        return MatrixMode.consistent, 1
+    if text == "line":
+        return MatrixMode.line, 1
+    if text.startswith("multiline:"):
+        try:
+            k = int(text[10:])
+        except ValueError:
+            raise CtsmError("InvalidConfig", f"bad multiline ray count in '{text}'")
+        if k <= 0:
+            raise CtsmError("InvalidConfig", "multiline ray count must be > 0")
+        return MatrixMode.multiline, k
+    raise CtsmError("InvalidConfig", f"unknown matrix mode '{text}'")
+
+
+def matrix_mode_name(mode: str, k: int = 1) -> str:
+    return f"multiline:{k}" if mode == MatrixMode.multiline else mode
+
+
+def _require_consistent(mode: str) -> None:
+    if mode != MatrixMode.consistent:
+        raise CtsmError("InvalidSpec",
+                        f"matrix mode '{mode}' is not provided on the device path "
+                        "(consistent weights only; line/multiline are out of scope)")
+
+
+# ---- device context -----------------------------------------------------
+class Context:
+    """Owns a ctsm_ctx (device status word, scratch buffers) for one GPU."""
+
+    _by_device: dict[int, "Context"] = {}
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().ctsm_create(device, ctypes.byref(h)))
+        self.handle = h
+
+    @classmethod
+    def get(cls, device: Optional[int] = None) -> "Context":
+        if device is None:
+            device = torch.cuda.current_device() if torch is not None else 0
+        if device not in cls._by_device:
+            cls._by_device[device] = Context(device)
+        return cls._by_device[device]
+
+    def close(self) -> None:
+        if self.handle:
+            _lib.lib().ctsm_destroy(self.handle)
+            self.handle = None
+
+
+def _stream(device: int):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _dev_ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _dtype_code(t) -> int:
+    if t.dtype == torch.float64:
+        return _lib.CTSM_F64
+    if t.dtype == torch.float32:
+        return _lib.CTSM_F32
+    raise CtsmError("InvalidSpec", f"unsupported dtype {t.dtype} (float64/float32)")
+
+
+def _to_device(a, device: int, dtype=None):
+    """numpy / tensor -> contiguous CUDA tensor (host arrays are copied)."""
+    if torch is not None and isinstance(a, torch.Tensor):
+        t = a
+        if dtype is not None and t.dtype != dtype:
+            t = t.to(dtype)
+        if t.device.type != "cuda":
+            t = t.to(f"cuda:{device}")
+        return t.contiguous(), True
+    arr = np.ascontiguousarray(a)
+    t = torch.from_numpy(arr)
+    if dtype is not None:
+        t = t.to(dtype)
+    elif t.dtype not in (torch.float64, torch.float32):
+        t = t.to(torch.float64)
+    return t.to(f"cuda:{device}"), False
+
+
+def _angle_shard(g: ScanGeometry, angles) -> tuple[int, int, int]:
+    if angles is None:
+        return 0, g.n_angles, 1
+    if isinstance(angles, range):
+        step = angles.step
+        if step <= 0 or len(angles) == 0:
+            raise CtsmError("InvalidSpec", "empty or descending angle range")
+        return angles.start, min(g.n_angles, angles.start + step * len(angles)), step
+    a0, a1, st = angles
+    return int(a0), int(a1), int(st)
+
+
+# ---- CSR system matrix (K1/K2/K3/K4) --------------------------------------
+@dataclass
+class SparseSystemMatrix:
+    """projector.hpp:26-35. Arrays are CUDA tensors (row_start int64 holding
+    u64 values, col int32 holding u32 columns, val float64)."""
+
+    n_rows: int
+    n_cols: int
+    row_start: "torch.Tensor"
+    col: "torch.Tensor"
+    val: "torch.Tensor"
+    meta: str = ""
+    device: int = 0
+    row_offset: int = 0  # first global row of this shard (angle sharding)
+
+    def nnz(self) -> int:
+        return int(self.col.numel())
+
+    def to_host(self):
+        return (self.row_start.cpu().numpy().view(np.uint64), self.col.cpu().numpy().view(np.uint32),
+                self.val.cpu().numpy())
+
+
+def _meta(g: ScanGeometry, mode: str, k: int) -> str:
+    # projector.cpp:191-199 (operator<< of doubles uses 6 significant digits)
+    def f(v):
+        return f"{v:g}"
+    return (f"mode={matrix_mode_name(mode, k)}\n"
+            f"s={f(g.s)}\nd={f(g.d)}\ndy={f(g.d_y)}\ndz={f(g.d_z)}\nndy={g.n_det_y}\nndz={g.n_det_z}"
+            f"\nnp={g.n_angles}\nangle_start={f(g.angle_start)}\nangle_end={f(g.angle_end)}"
+            f"\na={f(g.a)}\nb={f(g.b)}\nc={f(g.c)}\nnx={g.n_x}\nny={g.n_y}\nnz={g.n_z}\n")
+
+
+def build_system_matrix(g: ScanGeometry, mode: str = MatrixMode.consistent, k: int = 1,
+                        threads: int = 1, memory_budget_bytes: int = DEFAULT_BUDGET,
+                        device: Optional[int] = None, angle_range: Optional[tuple] = None
+                        ) -> SparseSystemMatrix:
+    """projector.cpp:144-201 on the GPU (K1 2D / K2 3D). ``threads`` is accepted
+    for API compatibility and ignored. ``angle_range=(a0, a1)`` builds one
+    contiguous angle shard (rows a0*rpa .. a1*rpa)."""
+    _require_consistent(mode)
+    g.validate()
+    if g.n_voxels > 0xFFFFFFFF:
+        raise CtsmError("TooLarge", "grid exceeds 2^32 voxel columns")
+    ctx = Context.get(device)
+    a0, a1 = (0, g.n_angles) if angle_range is None else angle_range
+    n_rows = (a1 - a0) * g.rows_per_angle
+    dev = ctx.device
+    cg = g.to_c()
+    row_start = torch.empty(n_rows + 1, dtype=torch.int64, device=f"cuda:{dev}")
+    nnz = ctypes.c_uint64(0)
+    st = _stream(dev)
+    L = _lib.lib()
+    _lib.check(L.ctsm_csr_count(ctx.handle, ctypes.byref(cg), a0, a1, memory_budget_bytes,
+                                _dev_ptr(row_start), ctypes.byref(nnz), st))
+    col = torch.empty(nnz.value, dtype=torch.int32, device=f"cuda:{dev}")
+    val = torch.empty(nnz.value, dtype=torch.float64, device=f"cuda:{dev}")
+    _lib.check(L.ctsm_csr_fill(ctx.handle, ctypes.byref(cg), a0, a1, _dev_ptr(row_start),
+                               _dev_ptr(col), _dev_ptr(val), st))
+    return SparseSystemMatrix(n_rows=n_rows, n_cols=g.n_voxels, row_start=row_start, col=col,
+                              val=val, meta=_meta(g, mode, k), device=dev,
+                              row_offset=a0 * g.rows_per_angle)
+
+
+def forward_project(w: SparseSystemMatrix, x):
+    """projector.cpp:203-217 (K3)."""
+    n = int(x.numel()) if (torch is not None and isinstance(x, torch.Tensor)) else int(np.size(x))
+    if n != w.n_cols:
+        raise CtsmError("DimensionMismatch", "image size does not match matrix columns")
+    ctx = Context.get(w.device)
+    xt, was_t = _to_device(x, w.device, torch.float64)
+    y = torch.empty(w.n_rows, dtype=torch.float64, device=xt.device)
+    _lib.check(_lib.lib().ctsm_spmv(ctx.handle, w.n_rows, w.n_cols, _dev_ptr(w.row_start),
+                                    _dev_ptr(w.col), _dev_ptr(w.val), _dev_ptr(xt), _dev_ptr(y),
+                                    _stream(w.device)))
+    return y if was_t else y.cpu().numpy()
+
+
+def back_project(w: SparseSystemMatrix, y):
+    """projector.cpp:219-233 (K4)."""
+    n = int(y.numel()) if (torch is not None and isinstance(y, torch.Tensor)) else int(np.size(y))
+    if n != w.n_rows:
+        raise CtsmError("DimensionMismatch", "sinogram size does not match matrix rows")
+    ctx = Context.get(w.device)
+    yt, was_t = _to_device(y, w.device, torch.float64)
+    x = torch.empty(w.n_cols, dtype=torch.float64, device=yt.device)
+    _lib.check(_lib.lib().ctsm_spmv_t(ctx.handle, w.n_rows, w.n_cols, _dev_ptr(w.row_start),
+                                      _dev_ptr(w.col), _dev_ptr(w.val), _dev_ptr(yt), _dev_ptr(x),
+                                      _stream(w.device)))
+    return x if was_t else x.cpu().numpy()
+
+
+def scale_values(w: SparseSystemMatrix, factor: float) -> None:
+    """projector.cpp:282-286."""
+    if not math.isfinite(factor):
+        raise CtsmError("NonFinite", "scale factor must be finite")
+    w.val.mul_(factor)
+
+
+def spectral_norm_power(w: SparseSystemMatrix, iters: int = 100, seed: int = 7) -> float:
+    """projector.cpp:262-280 on K3/K4 (normal_samples, phantoms.cpp:78-87)."""
+    from .phantoms import normal_samples
+
+    if w.nnz() == 0:
+        raise CtsmError("ZeroMatrix", "matrix has no entries")
+    v = torch.from_numpy(normal_samples(w.n_cols, seed)).to(f"cuda:{w.device}")
+    v = v / torch.sqrt((v * v).sum())
+    lam = 0.0
+    for _ in range(iters):
+        u = back_project(w, forward_project(w, v))
+        lam = float(torch.sqrt((u * u).sum()))
+        if lam == 0.0:
+            raise CtsmError("ZeroMatrix", "power iteration collapsed")
+        v = u / lam
+    return math.sqrt(lam)
+
+
+# ---- matrix-free projectors (K5/K6) ---------------------------------------
+def forward_project_matrix_free(g: ScanGeometry, mode: str = MatrixMode.consistent, k: int = 1,
+                                x=None, threads: int = 1, *, angles=None, out=None,
+                                device: Optional[int] = None):
+    """projector.cpp:235-260 (K5). ``angles`` = (begin, end, step) restricts the
+    projection to an angle shard (rows of other angles are left untouched in
+    ``out``, zero in a fresh output). dtype follows x (float64 / float32)."""
+    _require_consistent(mode)
+    g.validate()
+    n = int(x.numel()) if (torch is not None and isinstance(x, torch.Tensor)) else int(np.size(x))
+    if n != g.n_voxels:
+        raise CtsmError("DimensionMismatch", "image size does not match the grid")
+    ctx = Context.get(device if device is not None else
+                      (x.device.index if (torch is not None and isinstance(x, torch.Tensor)
+                                          and x.is_cuda) else None))
+    xt, was_t = _to_device(x, ctx.device)
+    a0, a1, st = _angle_shard(g, angles)
+    y = out if out is not None else torch.zeros(g.n_measurements, dtype=xt.dtype, device=xt.device)
+    cg = g.to_c()
+    _lib.check(_lib.lib().ctsm_fwd_mf(ctx.handle, ctypes.byref(cg), _dtype_code(xt), a0, a1, st,
+                                      _dev_ptr(xt), _dev_ptr(y), _stream(ctx.device)))
+    return y if (was_t or out is not None) else y.cpu().numpy()
+
+
+def back_project_matrix_free(g: ScanGeometry, mode: str = MatrixMode.consistent, k: int = 1,
+                             y=None, threads: int = 1, *, angles=None, out=None,
+                             device: Optional[int] = None):
+    """Matrix-free A^T y (K6; the reference only has CSR back_project,
+    projector.cpp:219-233). With ``angles`` the result is the partial volume
+    of that angle shard (summed across ranks by the multi-GPU driver)."""
+    _require_consistent(mode)
+    g.validate()
+    n = int(y.numel()) if (torch is not None and isinstance(y, torch.Tensor)) else int(np.size(y))
+    if n != g.n_measurements:
+        raise CtsmError("DimensionMismatch", "sinogram size does not match the scan")
+    ctx = Context.get(device if device is not None else
+                      (y.device.index if (torch is not None and isinstance(y, torch.Tensor)
+                                          and y.is_cuda) else None))
+    yt, was_t = _to_device(y, ctx.device)
+    a0, a1, st = _angle_shard(g, angles)
+    x = out if out is not None else torch.empty(g.n_voxels, dtype=yt.dtype, device=yt.device)
+    cg = g.to_c()
+    _lib.check(_lib.lib().ctsm_bwd_mf(ctx.handle, ctypes.byref(cg), _dtype_code(yt), a0, a1, st,
+                                      _dev_ptr(yt), _dev_ptr(x), _stream(ctx.device)))
+    return x if (was_t or out is not None) else x.cpu().numpy()
+
+
+def angle_column_sums(g: ScanGeometry, mode: str = MatrixMode.consistent, k: int = 1,
+                      angle_index: int = 0, device: Optional[int] = None):
+    """projector.cpp:288-295: per-voxel sums of one angle block (A^T 1 on one angle)."""
+    _require_consistent(mode)
+    ctx = Context.get(device)
+    ones = torch.ones(g.n_measurements, dtype=torch.float64, device=f"cuda:{ctx.device}")
+    return back_project_matrix_free(g, mode, k, ones, angles=(angle_index, angle_index + 1, 1),
+                                    device=ctx.device).cpu().numpy()
+
+
+def sirt(g: ScanGeometry, y, x0=None, iters: int = 10, device: Optional[int] = None):
+    """SIRT (BASELINE.json configs[4]): x <- x + C A^T (R (y - A x)),
+    R = 1/(A 1), C = 1/(A^T 1) (zero sums -> 0). Single device."""
+    g.validate()
+    ctx = Context.get(device)
+    yt, was_t = _to_device(y, ctx.device)
+    if x0 is None:
+        x = torch.zeros(g.n_voxels, dtype=yt.dtype, device=yt.device)
+    else:
+        x, _ = _to_device(x0, ctx.device, yt.dtype)
+        x = x.clone()
+    cg = g.to_c()
+    _lib.check(_lib.lib().ctsm_sirt(ctx.handle, ctypes.byref(cg), _dtype_code(yt), _dev_ptr(yt),
+                                    _dev_ptr(x), iters, _stream(ctx.device)))
+    return x if was_t else x.cpu().numpy()

@@ -1,0 +1,209 @@
+"""GPU parity tests: CUDA path (through the C-ABI) vs the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * CSR sparsity bit-exact; with the crmath oracle (same libm on both sides)
+    the whole CSR (row_start, col, val) is bit-identical;
+  * weights / projections within 1e-10 (fp64) and 1e-5 (fp32) relative,
+    max|diff| <= tol * max(1, max|ref|) (test_projector.cpp:117 convention).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import pyoracle
+from paper_2511_12235_b200 import (CONFIGS, TEST_GEOMETRIES, CtsmError, back_project,
+                                   back_project_matrix_free, build_system_matrix,
+                                   forward_project, forward_project_matrix_free, sirt)
+from paper_2511_12235_b200.phantoms import phantom_for, uniform_sinogram
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+NTHREADS = max(1, os.cpu_count() or 1)
+TOL64 = 1e-10
+TOL32 = 1e-5
+
+
+def rel_err(got, ref):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return float(np.max(np.abs(got - ref))) / max(1.0, float(np.max(np.abs(ref))))
+
+
+def entries_to_csr(g, row, col, w):
+    """angle-block entries (emission order) -> CSR of that angle block."""
+    rpa = g.rows_per_angle
+    order = np.argsort(row, kind="stable")
+    counts = np.bincount(row, minlength=rpa)
+    rs = np.zeros(rpa + 1, np.uint64)
+    rs[1:] = np.cumsum(counts)
+    return rs, col[order], w[order]
+
+
+def assert_csr_bitexact(got, ref):
+    rs, col, val = got
+    assert np.array_equal(rs, ref.row_start), "row_start differs"
+    assert np.array_equal(col, ref.col), "columns differ"
+    assert np.array_equal(val.view(np.uint64), ref.val.view(np.uint64)), \
+        f"values differ (max |diff| {np.max(np.abs(val - ref.val)):.3g})"
+
+
+# ---- K1/K2: CSR emission ------------------------------------------------------
+@pytest.mark.parametrize("name", ["proj2d", "wide2d", "proj3d", "cone3d"])
+def test_csr_bitexact_small(name, oracle_cr):
+    g = TEST_GEOMETRIES[name]
+    w = build_system_matrix(g)
+    ref = oracle_cr.build_system_matrix(g, threads=NTHREADS)
+    assert_csr_bitexact(w.to_host(), ref)
+    # strictly ascending columns per row (test_projector.cpp:55-68)
+    rs, col, _ = w.to_host()
+    d = np.diff(col.astype(np.int64))
+    starts = rs[1:-1].astype(np.int64)
+    mask = np.ones(d.size, bool)
+    mask[starts[(starts > 0) & (starts <= d.size)] - 1] = False
+    assert np.all(d[mask] > 0)
+
+
+def test_csr_c0_full_bitexact(oracle_cr, oracle_glibc):
+    g = CONFIGS["c0"]
+    w = build_system_matrix(g)
+    got = w.to_host()
+    assert w.nnz() == 18_291_648
+    ref = oracle_cr.build_system_matrix(g, threads=NTHREADS)
+    assert_csr_bitexact(got, ref)
+    # against the glibc-libm reference: identical sparsity, weights within 1e-10
+    refg = oracle_glibc.build_system_matrix(g, threads=NTHREADS)
+    assert np.array_equal(got[0], refg.row_start)
+    assert np.array_equal(got[1], refg.col)
+    assert np.max(np.abs(got[2] - refg.val)) <= TOL64
+
+
+@pytest.mark.parametrize("ip", [0, 37, 90, 181])
+def test_csr_c2_angle_blocks_bitexact(ip, oracle_cr):
+    g = CONFIGS["c2"]
+    w = build_system_matrix(g, angle_range=(ip, ip + 1), memory_budget_bytes=1 << 40)
+    ref = entries_to_csr(g, *oracle_cr.angle_block_entries(g, ip))
+    rs, col, val = w.to_host()
+    assert np.array_equal(rs, ref[0])
+    assert np.array_equal(col, ref[1])
+    assert np.array_equal(val.view(np.uint64), ref[2].view(np.uint64))
+
+
+def test_csr_budget_and_size_limits():
+    g = TEST_GEOMETRIES["proj3d"]
+    with pytest.raises(CtsmError) as e:
+        build_system_matrix(g, memory_budget_bytes=1024)
+    assert e.value.code == "OutOfMemory"
+    huge = g.with_(n_x=2048, n_y=2048, n_z=2048, a=0.01, b=0.01, c=0.01)
+    with pytest.raises(CtsmError) as e:
+        build_system_matrix(huge)
+    assert e.value.code == "TooLarge"
+
+
+# ---- K3/K4: CSR appliers --------------------------------------------------------
+@pytest.mark.parametrize("name", ["proj2d", "proj3d"])
+def test_spmv_and_transpose(name, oracle_cr):
+    g = TEST_GEOMETRIES[name]
+    w = build_system_matrix(g)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(g.n_voxels)
+    y = rng.standard_normal(g.n_measurements)
+    ref = oracle_cr.build_system_matrix(g)
+    assert rel_err(forward_project(w, x), pyoracle.csr_forward(ref, x)) <= 1e-13
+    xb = back_project(w, y)
+    xr = np.zeros(g.n_voxels)
+    rows = np.repeat(np.arange(g.n_measurements), np.diff(ref.row_start).astype(np.int64))
+    np.add.at(xr, ref.col, ref.val * y[rows])
+    assert rel_err(xb, xr) <= 1e-13
+    # adjoint identity (test_projector.cpp:81-91)
+    lhs = float(np.dot(forward_project(w, x), y))
+    rhs = float(np.dot(x, xb))
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+    with pytest.raises(CtsmError) as e:
+        forward_project(w, np.zeros(g.n_voxels + 1))
+    assert e.value.code == "DimensionMismatch"
+
+
+# ---- K5/K6: matrix-free ---------------------------------------------------------
+@pytest.mark.parametrize("name", ["proj2d", "wide2d", "proj3d", "cone3d"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_matrix_free_small(name, dtype, oracle_cr):
+    g = TEST_GEOMETRIES[name]
+    rng = np.random.default_rng(7)
+    x = rng.uniform(0, 1, g.n_voxels)
+    y = rng.uniform(0, 1, g.n_measurements)
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    tol = TOL64 if dtype == "f64" else TOL32
+    xt = torch.tensor(x, dtype=tdt, device="cuda")
+    yt = torch.tensor(y, dtype=tdt, device="cuda")
+    xr = xt.double().cpu().numpy()  # oracle sees the same (rounded) inputs
+    yr = yt.double().cpu().numpy()
+    yg = forward_project_matrix_free(g, "consistent", 1, xt).double().cpu().numpy()
+    assert rel_err(yg, oracle_cr.forward_project_matrix_free(g, xr, NTHREADS)) <= tol
+    xg = back_project_matrix_free(g, "consistent", 1, yt).double().cpu().numpy()
+    assert rel_err(xg, oracle_cr.back_project_matrix_free(g, yr, NTHREADS)) <= tol
+
+
+def test_matrix_free_matches_csr_small():
+    g = TEST_GEOMETRIES["proj3d"]
+    w = build_system_matrix(g)
+    x = torch.rand(g.n_voxels, dtype=torch.float64, device="cuda")
+    y0 = forward_project(w, x)
+    y1 = forward_project_matrix_free(g, "consistent", 1, x)
+    assert rel_err(y1.cpu().numpy(), y0.cpu().numpy()) <= 1e-12  # test_projector.cpp:104-119
+
+
+def test_matrix_free_deterministic():
+    g = CONFIGS["c1"]
+    x = torch.from_numpy(phantom_for("c1", g)).cuda()
+    a = forward_project_matrix_free(g, "consistent", 1, x, angles=(0, 720, 7))
+    b = forward_project_matrix_free(g, "consistent", 1, x, angles=(0, 720, 7))
+    assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_c1_sampled_angles(dtype, oracle_cr):
+    g = CONFIGS["c1"]
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    tol = TOL64 if dtype == "f64" else TOL32
+    x = torch.from_numpy(phantom_for("c1", g)).to(tdt).cuda()
+    y = torch.from_numpy(uniform_sinogram(g.n_measurements, 12346)).to(tdt).cuda()
+    angles = np.array([0, 45, 90, 133, 180, 271, 360, 719], np.int32)
+    rpa = g.rows_per_angle
+    yg = forward_project_matrix_free(g, "consistent", 1, x).double().cpu().numpy()
+    ysel = np.concatenate([yg[a * rpa:(a + 1) * rpa] for a in angles])
+    yref = oracle_cr.forward_mf_angles(g, angles, x.double().cpu().numpy(), NTHREADS)
+    assert rel_err(ysel, yref) <= tol
+    # A^T y over a strided angle shard
+    xg = back_project_matrix_free(g, "consistent", 1, y, angles=(3, 720, 90)).double().cpu().numpy()
+    sel = np.arange(3, 720, 90, dtype=np.int32)
+    xref = oracle_cr.back_mf_angles(g, sel, y.double().cpu().numpy(), NTHREADS)
+    assert rel_err(xg, xref) <= tol
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_3d_sampled_angles(cfg, oracle_cr):
+    g = CONFIGS[cfg]
+    dt = torch.float64 if cfg == "c2" else torch.float32
+    tol = TOL64 if cfg == "c2" else TOL32
+    x = torch.from_numpy(phantom_for(cfg, g, dtype=np.float32)).to(dt).cuda()
+    angles = np.array([0, 37, 90] if cfg == "c2" else [0, 111], np.int32)
+    rpa = g.rows_per_angle
+    xr = x.double().cpu().numpy()
+    for a in angles:
+        yg = forward_project_matrix_free(g, "consistent", 1, x, angles=(int(a), int(a) + 1, 1))
+        yg = yg[a * rpa:(a + 1) * rpa].double().cpu().numpy()
+        yref = oracle_cr.forward_mf_angles(g, np.array([a], np.int32), xr, NTHREADS)
+        assert rel_err(yg, yref) <= tol
+
+
+def test_sirt_small(oracle_cr):
+    g = TEST_GEOMETRIES["proj3d"]
+    rng = np.random.default_rng(3)
+    xt = rng.uniform(0, 1, g.n_voxels)
+    y = oracle_cr.forward_project_matrix_free(g, xt, NTHREADS)
+    x0 = np.zeros(g.n_voxels)
+    xg = sirt(g, y, x0, iters=5)
+    xref = oracle_cr.sirt(g, y, x0, 5, NTHREADS)
+    assert rel_err(xg, xref) <= 1e-9
