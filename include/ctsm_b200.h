@@ -111,6 +111,10 @@ int ctsm_fwd_mf(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begi
 int ctsm_bwd_mf(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begin,
                 int angle_end, int angle_step, const void* y_dev, void* x_dev, void* stream);
 
+/* Voxel-ray updates (nonzero weights applied, i.e. nnz of the shard's rows of
+ * A) counted live by the last successful ctsm_fwd_mf call on ctx. */
+uint64_t ctsm_last_update_count(ctsm_ctx* ctx);
+
 /* ---- K7/K8: SIRT pieces (BASELINE.json configs[4]) ----------------------
  * x <- x + C .* A^T (R .* (y - A x)), R = 1/(A 1), C = 1/(A^T 1), zero sums -> 0.
  * ctsm_sirt_residual: r = R .* (y - ax) over the shard's rows, with R

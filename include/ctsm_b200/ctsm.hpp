@@ -1,0 +1,121 @@
+// ctsm_b200/ctsm.hpp -- C++ drop-in for the reference's projector hot path.
+//
+// Same namespace, types and signatures as the reference headers
+// (/root/reference/proj/include/ctsm/{common,geometry,projector}.hpp), so a
+// caller of the reference switches by pointing its include path here and
+// linking libctsm_b200.so instead of libctsm.a. Implemented in
+// paper_2511_12235_b200/csrc/api.cpp over the C-ABI (include/ctsm_b200.h);
+// all compute runs on the GPU (no CPU fallback).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace ctsm {
+
+// common.hpp:11-25
+enum class ErrorCode {
+  DegenerateGeometry,
+  RayParallelToFace,
+  SingularPhi,
+  CentralRow,
+  ZRestrictionViolation,
+  DimensionMismatch,
+  NonFinite,
+  ZeroMatrix,
+  TooLarge,
+  InvalidSpec,
+  OutOfMemory,
+  InvalidConfig,
+  IoFailure,
+};
+
+const char* error_code_name(ErrorCode code);
+
+// common.hpp:29-38
+class Error : public std::runtime_error {
+ public:
+  Error(ErrorCode code, const std::string& message)
+      : std::runtime_error(std::string(error_code_name(code)) + ": " + message), code_(code) {}
+  ErrorCode code() const { return code_; }
+
+ private:
+  ErrorCode code_;
+};
+
+inline constexpr double k_pi = 3.14159265358979323846;
+
+// geometry.hpp:29-64
+struct ScanGeometry {
+  double s = 0.0;
+  double d = 0.0;
+  double d_y = 1.0;
+  double d_z = 1.0;
+  int n_det_y = 0;
+  int n_det_z = 1;
+  int n_angles = 0;
+  double angle_start = 0.0;
+  double angle_end = 2.0 * k_pi;
+  double a = 1.0;
+  double b = 1.0;
+  double c = 1.0;
+  int n_x = 0;
+  int n_y = 0;
+  int n_z = 1;
+
+  void validate() const;  // throws InvalidSpec / DegenerateGeometry / NonFinite
+
+  bool is_2d() const { return n_z == 1 && n_det_z == 1; }
+  double sdd() const { return s + d; }
+  double angle(int i) const { return angle_start + (angle_end - angle_start) * i / n_angles; }
+  double face_x(double ix) const { return (ix - n_x / 2.0) * a; }
+  double face_y(double iy) const { return (iy - n_y / 2.0) * b; }
+  double face_z(double iz) const { return (iz - n_z / 2.0) * c; }
+  std::uint64_t n_voxels() const {
+    return std::uint64_t(n_x) * std::uint64_t(n_y) * std::uint64_t(n_z);
+  }
+  std::uint64_t n_measurements() const {
+    return std::uint64_t(n_angles) * std::uint64_t(n_det_y) * std::uint64_t(n_det_z);
+  }
+};
+
+// projector.hpp:12-16
+enum class MatrixMode { consistent, line, multiline };
+
+MatrixMode parse_matrix_mode(const std::string& text, int* k);
+std::string matrix_mode_name(MatrixMode mode, int k);
+
+// projector.hpp:26-35
+struct SparseSystemMatrix {
+  std::uint64_t n_rows = 0;
+  std::uint64_t n_cols = 0;
+  std::vector<std::uint64_t> row_start;
+  std::vector<std::uint32_t> col;
+  std::vector<double> val;
+  std::string meta;
+  std::uint64_t nnz() const { return col.size(); }
+};
+
+// projector.hpp:41-70 (threads is accepted and ignored: the work runs on the
+// GPU; only MatrixMode::consistent is provided on the device path).
+SparseSystemMatrix build_system_matrix(const ScanGeometry& g, MatrixMode mode, int k = 1,
+                                       int threads = 1,
+                                       std::uint64_t memory_budget_bytes = 5ull << 30);
+std::vector<double> forward_project(const SparseSystemMatrix& w, const std::vector<double>& x);
+std::vector<double> back_project(const SparseSystemMatrix& w, const std::vector<double>& y);
+std::vector<double> forward_project_matrix_free(const ScanGeometry& g, MatrixMode mode, int k,
+                                                const std::vector<double>& x, int threads = 1);
+// Addition: matrix-free adjoint.
+std::vector<double> back_project_matrix_free(const ScanGeometry& g, MatrixMode mode, int k,
+                                             const std::vector<double>& y, int threads = 1);
+double spectral_norm_power(const SparseSystemMatrix& w, int iters = 100, std::uint64_t seed = 7);
+void scale_values(SparseSystemMatrix* w, double factor);
+std::vector<double> angle_column_sums(const ScanGeometry& g, MatrixMode mode, int k,
+                                      int angle_index);
+// Addition: SIRT (BASELINE.json configs[4]) on one device.
+std::vector<double> sirt(const ScanGeometry& g, const std::vector<double>& y,
+                         const std::vector<double>& x0, int iters);
+
+}  // namespace ctsm

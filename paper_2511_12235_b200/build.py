@@ -22,6 +22,7 @@ UNITS = {
     "csr.cu": ["-fmad=false"],
     "mf.cu": [],
     "capi.cu": [],
+    "api.cpp": [],
 }
 
 
@@ -36,10 +37,11 @@ def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(HERE, "..", "include", "ctsm_b200.h"))
+    headers.append(os.path.join(HERE, "..", "include", "ctsm_b200", "ctsm.hpp"))
     objs = []
     for unit, extra in UNITS.items():
         src = os.path.join(CSRC, unit)
-        obj = os.path.join(OBJ, unit.replace(".cu", ".o"))
+        obj = os.path.join(OBJ, os.path.splitext(unit)[0] + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
             cmd = [NVCC, "-c", src, "-o", obj] + COMMON + extra

@@ -64,8 +64,11 @@ struct ctsm_ctx {
   int* status = nullptr;        // device status word
   double* dred = nullptr;       // device reduction scratch (4 doubles)
   int* h_status = nullptr;      // pinned
+  unsigned long long* n_upd = nullptr;    // device: voxel-ray updates of the last forward call
+  unsigned long long* h_upd = nullptr;    // pinned mirror
+  uint64_t last_updates = 0;
   double* h_red = nullptr;      // pinned
-  Buf angles, edges, cs, counts, scan, longrows, acc, tmp_a, tmp_b, tmp_c, tmp_d, tmp_e, tmp_f;
+  Buf angles, edges, cs, counts, scan, longrows, acc, part, tmp_a, tmp_b, tmp_c, tmp_d, tmp_e, tmp_f;
 };
 
 namespace {
@@ -213,6 +216,8 @@ int ctsm_create(int device, ctsm_ctx** out) {
   CT_CUDA(cudaMalloc(&c->dred, 4 * sizeof(double)));
   CT_CUDA(cudaMallocHost(&c->h_status, sizeof(int)));
   CT_CUDA(cudaMallocHost(&c->h_red, 4 * sizeof(double)));
+  CT_CUDA(cudaMalloc(&c->n_upd, sizeof(unsigned long long)));
+  CT_CUDA(cudaMallocHost(&c->h_upd, sizeof(unsigned long long)));
   *out = c;
   return 0;
 }
@@ -221,7 +226,7 @@ int ctsm_destroy(ctsm_ctx* ctx) {
   if (!ctx) return 0;
   cudaSetDevice(ctx->device);
   Buf* bufs[] = {&ctx->angles, &ctx->edges, &ctx->cs,    &ctx->counts, &ctx->scan,
-                 &ctx->longrows, &ctx->acc, &ctx->tmp_a, &ctx->tmp_b,  &ctx->tmp_c,
+                 &ctx->longrows, &ctx->acc, &ctx->part, &ctx->tmp_a, &ctx->tmp_b,  &ctx->tmp_c,
                  &ctx->tmp_d, &ctx->tmp_e, &ctx->tmp_f};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
@@ -229,6 +234,8 @@ int ctsm_destroy(ctsm_ctx* ctx) {
   cudaFree(ctx->dred);
   cudaFreeHost(ctx->h_status);
   cudaFreeHost(ctx->h_red);
+  cudaFree(ctx->n_upd);
+  cudaFreeHost(ctx->h_upd);
   delete ctx;
   return 0;
 }
@@ -399,10 +406,12 @@ static int fwd_impl(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int begin,
   CT_CUDA(zero_rows_u64(d, begin, step, n_sel, acc, st));
   const double B = mx * row_sum_bound(g) * 1.05;
   const double scale = B > 0.0 ? std::ldexp(1.0, 61) / B : 1.0;
-  if (B > 0.0)
-    CT_CUDA(fwd_mf(d, dtype, (const AngleCS*)ctx->cs.p, begin, step, n_sel, x, acc, scale,
-                   ctx->status, st));
+  CT_CUDA(cudaMemsetAsync(ctx->n_upd, 0, sizeof(unsigned long long), st));
+  CT_CUDA(fwd_mf(d, dtype, (const AngleCS*)ctx->cs.p, begin, step, n_sel, x, acc, scale,
+                 ctx->n_upd, ctx->status, st));
   CT_CUDA(fixed_to_float_rows(d, dtype, begin, step, n_sel, acc, scale, y, st));
+  CT_CUDA(cudaMemcpyAsync(ctx->h_upd, ctx->n_upd, sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, st));
   return 0;
 }
 
@@ -414,7 +423,10 @@ static int bwd_impl(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int begin,
   CT_TRY(check_shard(g, begin, end, step));
   const int n_sel = n_in_shard(begin, end, step);
   CT_TRY(prepare_cs(ctx, d, begin, step, n_sel, st));
-  CT_CUDA(bwd_mf(d, dtype, (const AngleCS*)ctx->cs.p, begin, step, n_sel, y, x, ctx->status, st));
+  const int nc = bwd_chunks(d, n_sel);
+  if (nc > 1) CT_TRY(ensure(ctx, ctx->part, (size_t)nc * g->n_x * g->n_y * sizeof(double)));
+  CT_CUDA(bwd_mf(d, dtype, (const AngleCS*)ctx->cs.p, begin, step, n_sel, y, x,
+                 (double*)ctx->part.p, nc, ctx->status, st));
   return 0;
 }
 
@@ -423,8 +435,12 @@ int ctsm_fwd_mf(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begi
   CT_TRY(set_device(ctx));
   cudaStream_t st = (cudaStream_t)stream;
   CT_TRY(fwd_impl(ctx, g, dtype, angle_begin, angle_end, angle_step, x_dev, y_dev, st));
-  return check_status(ctx, st, "forward_project_matrix_free");
+  CT_TRY(check_status(ctx, st, "forward_project_matrix_free"));
+  ctx->last_updates = *ctx->h_upd;
+  return 0;
 }
+
+uint64_t ctsm_last_update_count(ctsm_ctx* ctx) { return ctx ? ctx->last_updates : 0; }
 
 int ctsm_bwd_mf(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begin,
                 int angle_end, int angle_step, const void* y_dev, void* x_dev, void* stream) {

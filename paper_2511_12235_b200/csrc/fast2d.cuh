@@ -2,157 +2,230 @@
 // (pixel area fractions per detector cell) for the matrix-free projectors.
 //
 // Same quantity as pixel_area_factors (weights2d.cpp:105-129), reformulated
-// in the ray parameter t = tan(beta) (fan-angle tangent, detector coordinate
+// in the ray parameter t = tan(beta) (fan-angle tangent; detector coordinate
 // e_y = t (s+d) / d_y):
 //  * a point (x, y) projects to t = L / D with lateral L = y cos(phi) -
 //    x sin(phi) and depth D = s - x cos(phi) - y sin(phi) (geometry.cpp:56-62);
 //    t is invariant under the quarter-turn canonicalisation, so no frame
-//    search (geometry.cpp:76-97) and no atan2 are needed;
+//    search (geometry.cpp:76-97) and no atan2 are needed: the "low" face (the
+//    canonical y0 face) is the face whose larger corner t is smallest;
 //  * detector edge e sits at t_e = e d_y / (s+d) exactly (no atan/tan pair);
 //  * the corner-triangle area cut from apex corner (xa, ya) by the ray t
-//    (paper A3, weights2d.cpp:8-16) is
+//    (paper A3, weights2d.cpp:8-16) is the cumulative
 //        A(t) = Da^2 (t - ta)^2 / (2 a b |(C + t S)(t C - S)|),
 //    and the band between rays t1 < t2 crossing both faces x = x0, x1
 //    (paper A4, weights2d.cpp:19-27) is
 //        |(t2 - t1)(s C - xm)| / (b |(C + t1 S)(C + t2 S)|)
 //    (faces y = y0, y1: |(t2 - t1)(s S - ym)| / (a |(t1 C - S)(t2 C - S)|)).
-// These are algebraically identical to the reference's sine/tangent forms;
-// results agree with the reference to ~1e-13 (checked by tests against the
-// oracle at the 1e-10 fp64 tolerance).
+// These are algebraically identical to the reference's sine/tangent forms.
+// Each breakpoint costs one reciprocal; cumulative areas are carried from one
+// piece to the next, so a pixel-angle needs no transcendental and ~10
+// reciprocals. Results agree with the reference to ~1e-13 (tests check the
+// 1e-10 fp64 tolerance against the oracle).
 #pragma once
 #include "common.cuh"
 
 namespace ctsmb {
 namespace fast {
 
-// Division in the matrix-free kernels: IEEE double division (the compiler's
-// sequence). Kept in one place so it can be swapped for a reciprocal scheme.
-__device__ __forceinline__ double fdiv(double a, double b) { return a / b; }
+// 1/x to ~1 ulp: hardware approximation + two Newton steps.
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
 
-struct Corner {
-  double t, D;
-  double x, y;
+// Division used by the 3D atoms in the matrix-free path.
+__device__ __forceinline__ double fdiv(double a, double b) { return a * frcp(b); }
+
+// The sweep of one pixel at one angle in t-space (shared by 2D and 3D).
+struct Sweep2 {
+  double T1, T2, T3, T4;   // sorted corner parameters (T1 apex-low, T4 apex-high)
+  double K1, K4;           // Da^2 / (2ab) of the two apex corners
+  double band_k;           // |s C - xm| / b  or  |s S - ym| / a
+  bool band_vertical;      // band crosses x = const faces (low face horizontal)
+  int low_face;            // 0 bottom (y0), 1 right (x1), 2 top (y1), 3 left (x0)
+  double Ta_x, Ta_y, Tb_x, Tb_y;  // apex-low / apex-high corner coordinates
+  double D[4];             // corner depths (0 (x0,y0), 1 (x1,y0), 2 (x1,y1), 3 (x0,y1))
 };
 
-// Streams the cell weights of pixel (ix, iy) at an angle with cos/sin (C, S)
-// to emit(cell_m, w) in ascending cell order; cells outside the detector are
-// skipped (weights2d.cpp:110-113), as are weights <= 0. Returns false and
-// raises status on degenerate geometry.
-template <typename Emit>
-__device__ __forceinline__ bool pixel_weights(const DevGeom& g, double C, double S, int ix,
-                                              int iy, int* status, Emit&& emit) {
-  const double x0 = (ix - g.n_x / 2.0) * g.a, x1 = (ix + 1 - g.n_x / 2.0) * g.a;
-  const double y0 = (iy - g.n_y / 2.0) * g.b, y1 = (iy + 1 - g.n_y / 2.0) * g.b;
+__device__ __forceinline__ bool sweep_setup(const DevGeom& g, double C, double S, double x0,
+                                            double x1, double y0, double y1, int* status,
+                                            Sweep2& w) {
   const double s = g.s;
-  // corners counter-clockwise: 0 (x0,y0), 1 (x1,y0), 2 (x1,y1), 3 (x0,y1)
-  Corner c[4];
-  const double xs[4] = {x0, x1, x1, x0};
-  const double ys[4] = {y0, y0, y1, y1};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const double D = s - xs[k] * C - ys[k] * S;
-    const double L = ys[k] * C - xs[k] * S;
-    if (!(D > kEpsDenRel * s)) {
-      raise_status(status, CTSM_ERR_DEGENERATE_GEOMETRY);
-      return false;
-    }
-    c[k].t = fdiv(L, D);
-    c[k].D = D;
-    c[k].x = xs[k];
-    c[k].y = ys[k];
+  const double x0C = x0 * C, x1C = x1 * C, x0S = x0 * S, x1S = x1 * S;
+  const double y0C = y0 * C, y1C = y1 * C, y0S = y0 * S, y1S = y1 * S;
+  const double D0 = s - x0C - y0S, D1 = s - x1C - y0S, D2 = s - x1C - y1S, D3 = s - x0C - y1S;
+  const double dmin = fmin(fmin(D0, D1), fmin(D2, D3));
+  if (!(dmin > kEpsDenRel * s)) {
+    raise_status(status, CTSM_ERR_DEGENERATE_GEOMETRY);
+    return false;
   }
-  // apex1 = corner with the smallest t; the low face joins it to its
-  // neighbour with the smaller t; the high face is the opposite face.
-  int i1 = 0;
-#pragma unroll
-  for (int k = 1; k < 4; ++k)
-    if (c[k].t < c[i1].t) i1 = k;
-  const int na = (i1 + 1) & 3, nb = (i1 + 3) & 3, op = (i1 + 2) & 3;
-  const int i2 = (c[na].t <= c[nb].t) ? na : nb;   // low-face partner
-  const int i3o = (i2 == na) ? nb : na;            // remaining neighbour (high face)
-  // high face = {op, i3o}
-  const int i4 = (c[op].t >= c[i3o].t) ? op : i3o;
-  const int i3 = (i4 == op) ? i3o : op;
-  const double T1 = c[i1].t, T4 = c[i4].t;
-  double T2 = c[i2].t, T3 = c[i3].t;
-  if (T3 < T2) {  // rounding-level inconsistency at degenerate alignments
-    const double m = 0.5 * (T2 + T3);
-    T2 = m;
-    T3 = m;
+  const double t0 = (y0C - x0S) * frcp(D0), t1 = (y0C - x1S) * frcp(D1);
+  const double t2 = (y1C - x1S) * frcp(D2), t3 = (y1C - x0S) * frcp(D3);
+  w.D[0] = D0; w.D[1] = D1; w.D[2] = D2; w.D[3] = D3;
+  // low face = argmin over faces of max(corner t)
+  const double f0 = fmax(t0, t1), f1 = fmax(t1, t2), f2 = fmax(t2, t3), f3 = fmax(t3, t0);
+  int k = 0;
+  double fm = f0;
+  if (f1 < fm) { fm = f1; k = 1; }
+  if (f2 < fm) { fm = f2; k = 2; }
+  if (f3 < fm) { fm = f3; k = 3; }
+  w.low_face = k;
+  // corners of the low face (a, a+1) and of the high face (a+2, a+3)
+  double la, lb, ha, hb, Dla, Dlb, Dha, Dhb, xla, yla, xlb, ylb, xha, yha, xhb, yhb;
+  switch (k) {
+    case 0: la = t0; lb = t1; ha = t2; hb = t3; Dla = D0; Dlb = D1; Dha = D2; Dhb = D3;
+            xla = x0; yla = y0; xlb = x1; ylb = y0; xha = x1; yha = y1; xhb = x0; yhb = y1; break;
+    case 1: la = t1; lb = t2; ha = t3; hb = t0; Dla = D1; Dlb = D2; Dha = D3; Dhb = D0;
+            xla = x1; yla = y0; xlb = x1; ylb = y1; xha = x0; yha = y1; xhb = x0; yhb = y0; break;
+    case 2: la = t2; lb = t3; ha = t0; hb = t1; Dla = D2; Dlb = D3; Dha = D0; Dhb = D1;
+            xla = x1; yla = y1; xlb = x0; ylb = y1; xha = x0; yha = y0; xhb = x1; yhb = y0; break;
+    default: la = t3; lb = t0; ha = t1; hb = t2; Dla = D3; Dlb = D0; Dha = D1; Dhb = D2;
+            xla = x0; yla = y1; xlb = x0; ylb = y0; xha = x1; yha = y0; xhb = x1; yhb = y1; break;
   }
-  // low face horizontal (corners share y) -> band crosses the x = const faces
-  const bool low_horizontal = (c[i1].y == c[i2].y);
-  const double inv2ab = 1.0 / (2.0 * g.a * g.b);
-  const double K1 = c[i1].D * c[i1].D * inv2ab;
-  const double K4 = c[i4].D * c[i4].D * inv2ab;
-  double band_k;  // band = (t2 - t1) * band_k / |p(t1) p(t2)|
-  if (low_horizontal)
-    band_k = fabs(s * C - 0.5 * (x0 + x1)) / g.b;
-  else
-    band_k = fabs(s * S - 0.5 * (y0 + y1)) / g.a;
+  const bool lo_a = la <= lb;
+  w.T1 = lo_a ? la : lb;
+  w.T2 = lo_a ? lb : la;
+  const double Dap1 = lo_a ? Dla : Dlb;
+  w.Ta_x = lo_a ? xla : xlb;
+  w.Ta_y = lo_a ? yla : ylb;
+  const bool hi_a = ha >= hb;
+  w.T4 = hi_a ? ha : hb;
+  w.T3 = hi_a ? hb : ha;
+  const double Dap4 = hi_a ? Dha : Dhb;
+  w.Tb_x = hi_a ? xha : xhb;
+  w.Tb_y = hi_a ? yha : yhb;
+  if (w.T3 < w.T2) {  // rounding-level inconsistency at degenerate alignments
+    const double m = 0.5 * (w.T2 + w.T3);
+    w.T2 = m;
+    w.T3 = m;
+  }
+  const double inv2ab = 0.5 / (g.a * g.b);
+  w.K1 = Dap1 * Dap1 * inv2ab;
+  w.K4 = Dap4 * Dap4 * inv2ab;
+  w.band_vertical = (k & 1) == 0;
+  w.band_k = w.band_vertical ? fabs(s * C - 0.5 * (x0 + x1)) / g.b
+                             : fabs(s * S - 0.5 * (y0 + y1)) / g.a;
+  return true;
+}
 
-  // cumulative-area helpers at a breakpoint t
-  auto tri_den = [&](double t) { return fabs((C + t * S) * (t * C - S)); };
-  auto band_p = [&](double t) { return low_horizontal ? (C + t * S) : (t * C - S); };
-
-  // detector edges strictly inside (T1, T4)
-  const double scale = g.sdd / g.d_y;   // t -> edge coordinate
+// Walks the pieces of the sweep in ascending t; calls
+// piece(cell, tlo, thi, kind, w2d) for every piece of positive width and
+// cell_done(cell, w) when a detector cell is complete (w = its area weight,
+// possibly 0). Cells are not clipped here.
+template <typename Piece, typename CellDone>
+__device__ __forceinline__ void sweep_walk(const DevGeom& g, double C, double S, const Sweep2& w,
+                                           Piece&& piece, CellDone&& cell_done) {
+  const double scale = g.sdd / g.d_y;
   const double inv_scale = g.d_y / g.sdd;
-  const double u_lo = T1 * scale, u_hi = T4 * scale;
-  const long long e_lo = (long long)floor(u_lo) + 1;
-  const long long e_hi = (long long)ceil(u_hi) - 1;
+  const double T1 = w.T1, T2 = w.T2, T3 = w.T3, T4 = w.T4;
+  const long long e_lo = (long long)floor(T1 * scale) + 1;
+  const long long e_hi = (long long)ceil(T4 * scale) - 1;
   int cell = (int)(e_lo - 1);
-  const int cell_lo = -g.n_det_y / 2, cell_hi = g.n_det_y / 2 - 1;
-
-  // walk merged breakpoints: corners T1 < T2 <= T3 < T4 and edges
-  const double zt[4] = {T1, T2, T3, T4};
-  int zi = 1;               // next corner breakpoint index (T1 is the start)
+  const bool bv = w.band_vertical;
+  // A ray parallel to a pixel face makes a factor vanish; the reference then
+  // returns 0 for the triangle (|sin(beta - phi)| < 1e-12, weights2d.cpp:11)
+  // and such a ray bounds no band piece (weights2d.cpp:22-23): guard likewise.
+  auto pq_inv = [&](double t) {
+    const double v = fabs((C + t * S) * (t * C - S));
+    return v > kEpsAngle ? frcp(v) : 0.0;
+  };
+  auto p_inv = [&](double t) {
+    const double v = fabs(bv ? (C + t * S) : (t * C - S));
+    return v > kEpsAngle ? frcp(v) : 0.0;
+  };
+  // zone of the upcoming piece: 0 low triangle, 1 band, 2 high triangle
+  int zone;
+  double Aprev = 0.0, ipprev = 0.0;
+  if (T1 < T2) {
+    zone = 0;
+  } else if (T2 < T3) {
+    zone = 1;
+    ipprev = p_inv(T1);
+  } else {
+    zone = 2;
+    const double d = T4 - T1;
+    Aprev = w.K4 * d * d * pq_inv(T1);
+  }
+  double prev = T1;
+  double acc = 0.0;
+  int zi = 1;  // next corner: 1 -> T2, 2 -> T3, 3 -> T4
   long long e = e_lo;
-  double tlo = T1;
-  double acc = 0.0;         // current cell weight
-  while (true) {
-    const double te = (e <= e_hi) ? e * inv_scale : 0.0;
-    const bool have_e = (e <= e_hi);
-    double thi;
-    bool is_edge;
-    if (zi < 4 && (!have_e || !(te < zt[zi]))) {
-      thi = zt[zi];
-      is_edge = false;
-    } else if (have_e) {
-      thi = te;
-      is_edge = true;
-    } else {
-      break;
-    }
-    if (thi > tlo) {
-      // zone of the piece [tlo, thi]: 0 if thi <= T2, 2 if tlo >= T3, else band
-      double w;
-      if (thi <= T2) {
-        const double dh = thi - T1, dl = tlo - T1;
-        const double ah = dh == 0.0 ? 0.0 : fdiv(K1 * dh * dh, tri_den(thi));
-        const double al = dl == 0.0 ? 0.0 : fdiv(K1 * dl * dl, tri_den(tlo));
-        w = ah - al;
-      } else if (tlo >= T3) {
-        const double dh = T4 - thi, dl = T4 - tlo;
-        const double ah = dh == 0.0 ? 0.0 : fdiv(K4 * dh * dh, tri_den(thi));
-        const double al = dl == 0.0 ? 0.0 : fdiv(K4 * dl * dl, tri_den(tlo));
-        w = al - ah;
+  while (zi <= 3) {
+    const double tz = zi == 1 ? T2 : (zi == 2 ? T3 : T4);
+    const bool have_e = e <= e_hi;
+    const double te = e * inv_scale;
+    const bool is_edge = have_e && te < tz;
+    const double b = is_edge ? te : tz;
+    if (b > prev) {
+      double wv;
+      if (zone == 0) {
+        const double d = b - T1;
+        const double A = w.K1 * d * d * pq_inv(b);
+        wv = A - Aprev;
+        Aprev = A;
+      } else if (zone == 1) {
+        const double ip = p_inv(b);
+        wv = w.band_k * (b - prev) * (ipprev * ip);
+        ipprev = ip;
       } else {
-        w = fdiv((thi - tlo) * band_k, fabs(band_p(tlo) * band_p(thi)));
+        const double d = T4 - b;
+        const double A = w.K4 * d * d * pq_inv(b);
+        wv = Aprev - A;
+        Aprev = A;
       }
-      if (w > 0.0) acc += w;
+      if (wv > 0.0) {
+        acc += wv;
+        piece(cell, prev, b, zone, wv);
+      }
+      prev = b;
     }
-    tlo = thi;
     if (is_edge) {
-      if (acc > 0.0 && cell >= cell_lo && cell <= cell_hi) emit(cell, acc);
+      cell_done(cell, acc);
       acc = 0.0;
       ++cell;
       ++e;
     } else {
+      if (zi == 1) {  // leaving the low triangle
+        if (T2 < T3) {
+          zone = 1;
+          ipprev = p_inv(T2);
+        } else {
+          zone = 2;
+          const double d = T4 - T2;
+          Aprev = w.K4 * d * d * pq_inv(T2);
+        }
+      } else if (zi == 2 && zone == 1) {  // leaving the band
+        zone = 2;
+        const double d = T4 - T3;
+        Aprev = w.K4 * d * d * pq_inv(T3);
+      }
       ++zi;
     }
   }
-  if (acc > 0.0 && cell >= cell_lo && cell <= cell_hi) emit(cell, acc);
+  cell_done(cell, acc);
+}
+
+// Streams the cell weights of pixel (ix, iy) at an angle with cos/sin (C, S)
+// to emit(cell_m, w) in ascending cell order; cells outside the detector are
+// skipped (weights2d.cpp:110-113), as are weights <= 1e-16 (125-127).
+template <typename Emit>
+__device__ __forceinline__ bool pixel_weights(const DevGeom& g, double C, double S, int ix,
+                                              int iy, int* status, Emit&& emit) {
+  const double x0 = (ix - g.n_x / 2.0) * g.a, x1 = x0 + g.a;
+  const double y0 = (iy - g.n_y / 2.0) * g.b, y1 = y0 + g.b;
+  Sweep2 w;
+  if (!sweep_setup(g, C, S, x0, x1, y0, y1, status, w)) return false;
+  const int cell_lo = -g.n_det_y / 2, cell_hi = g.n_det_y / 2 - 1;
+  sweep_walk(
+      g, C, S, w, [](int, double, double, int, double) {},
+      [&](int cell, double acc) {
+        if (acc > kEpsWeight && cell >= cell_lo && cell <= cell_hi) emit(cell, acc);
+      });
   return true;
 }
 

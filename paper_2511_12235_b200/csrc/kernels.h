@@ -54,10 +54,13 @@ cudaError_t build_angle_cs(const DevGeom& g, int angle_begin, int angle_step, in
 // dtype: CTSM_F64 / CTSM_F32
 cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
                    int angle_step, int n_sel, const void* x, unsigned long long* yacc,
-                   double scale, int* status, cudaStream_t st);
+                   double scale, unsigned long long* n_upd, int* status, cudaStream_t st);
+// Backward uses n_chunks angle chunks (bwd_chunks) with a partial-sum buffer
+// part of n_chunks * n_x * n_y doubles when n_chunks > 1 (2D only).
+int bwd_chunks(const DevGeom& g, int n_sel);
 cudaError_t bwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
-                   int angle_step, int n_sel, const void* y, void* x, int* status,
-                   cudaStream_t st);
+                   int angle_step, int n_sel, const void* y, void* x, double* part, int n_chunks,
+                   int* status, cudaStream_t st);
 // y rows of the shard <- acc / scale (and acc rows zeroed for reuse)
 cudaError_t fixed_to_float_rows(const DevGeom& g, int dtype, int angle_begin, int angle_step,
                                 int n_sel, unsigned long long* acc, double scale, void* y,

@@ -31,6 +31,14 @@ __device__ __forceinline__ double ld(const T* p) {
   return (double)__ldg(p);
 }
 
+// Voxel-ray update counter: nonzero weights applied in a forward call (the
+// metric's unit, measured live). One atomic per warp.
+__device__ __forceinline__ void count_updates(unsigned long long* n_upd, unsigned cnt) {
+  if (!n_upd) return;
+  const unsigned tot = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0 && tot) atomicAdd(n_upd, (unsigned long long)tot);
+}
+
 // 2D pixel tile per block: 16 x 8 pixels, 128 threads.
 constexpr int kTx = 16, kTy = 8;
 
@@ -39,41 +47,66 @@ __global__ void __launch_bounds__(128) fwd2d_kernel(DevGeom g, const AngleCS* __
                                                     int angle_begin, int angle_step,
                                                     const T* __restrict__ x,
                                                     unsigned long long* __restrict__ yacc,
-                                                    double scale, int* status) {
+                                                    double scale, unsigned long long* n_upd,
+                                                    int* status) {
   const int tiles_x = (g.n_x + kTx - 1) / kTx;
   const int ix = (blockIdx.x % tiles_x) * kTx + (threadIdx.x % kTx);
   const int iy = (blockIdx.x / tiles_x) * kTy + (threadIdx.x / kTx);
-  if (ix >= g.n_x || iy >= g.n_y) return;
-  const double xv = ld(&x[(long long)iy * g.n_x + ix]);
-  if (xv == 0.0) return;
-  const int k = blockIdx.y;
-  const int ip = angle_begin + k * angle_step;
-  const AngleCS a = cs[k];
-  unsigned long long* yrow = yacc + (long long)ip * g.rows_per_angle + g.n_det_y / 2;
-  const double xs = xv * scale;
-  fast::pixel_weights(g, a.C, a.S, ix, iy, status, [&](int m, double w) {
-    atomicAdd(&yrow[m], (unsigned long long)__double2ll_rn(w * xs));
-  });
+  unsigned cnt = 0;
+  if (ix < g.n_x && iy < g.n_y) {
+    const double xv = ld(&x[(long long)iy * g.n_x + ix]);
+    const int k = blockIdx.y;
+    const int ip = angle_begin + k * angle_step;
+    const AngleCS a = cs[k];
+    unsigned long long* yrow = yacc + (long long)ip * g.rows_per_angle + g.n_det_y / 2;
+    const double xs = xv * scale;
+    fast::pixel_weights(g, a.C, a.S, ix, iy, status, [&](int m, double w) {
+      ++cnt;
+      if (xs != 0.0) atomicAdd(&yrow[m], (unsigned long long)__double2ll_rn(w * xs));
+    });
+  }
+  count_updates(n_upd, cnt);
 }
 
+// Backward 2D: block = pixel tile x angle chunk. With n_chunks > 1 each chunk
+// writes its partial sum to part[chunk][pixel] and bwd_reduce adds the chunks
+// in fixed order (deterministic); with one chunk x is written directly.
 template <typename T>
 __global__ void __launch_bounds__(128) bwd2d_kernel(DevGeom g, const AngleCS* __restrict__ cs,
                                                     int angle_begin, int angle_step, int n_sel,
-                                                    const T* __restrict__ y, T* __restrict__ x,
+                                                    int chunk, const T* __restrict__ y,
+                                                    T* __restrict__ x, double* __restrict__ part,
                                                     int* status) {
   const int tiles_x = (g.n_x + kTx - 1) / kTx;
   const int ix = (blockIdx.x % tiles_x) * kTx + (threadIdx.x % kTx);
   const int iy = (blockIdx.x / tiles_x) * kTy + (threadIdx.x / kTx);
   if (ix >= g.n_x || iy >= g.n_y) return;
+  const int k0 = blockIdx.y * chunk;
+  const int k1 = min(k0 + chunk, n_sel);
   double acc = 0.0;
-  for (int k = 0; k < n_sel; ++k) {
+  for (int k = k0; k < k1; ++k) {
     const int ip = angle_begin + k * angle_step;
     const AngleCS a = cs[k];
     const T* yrow = y + (long long)ip * g.rows_per_angle + g.n_det_y / 2;
     fast::pixel_weights(g, a.C, a.S, ix, iy, status,
                         [&](int m, double w) { acc += w * ld(&yrow[m]); });
   }
-  x[(long long)iy * g.n_x + ix] = (T)acc;
+  const long long pix = (long long)iy * g.n_x + ix;
+  if (part)
+    part[(long long)blockIdx.y * g.n_x * g.n_y + pix] = acc;
+  else
+    x[pix] = (T)acc;
+}
+
+template <typename T>
+__global__ void bwd_reduce_kernel(long long n, int n_chunks, const double* __restrict__ part,
+                                  T* __restrict__ x) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int c = 0; c < n_chunks; ++c) acc += part[(long long)c * n + i];
+    x[i] = (T)acc;
+  }
 }
 
 // 3D: one thread per (voxel column, angle) for forward; per (voxel column,
@@ -83,11 +116,13 @@ __global__ void __launch_bounds__(128) fwd3d_kernel(DevGeom g, const AngleCS* __
                                                     int angle_begin, int angle_step,
                                                     const T* __restrict__ x,
                                                     unsigned long long* __restrict__ yacc,
-                                                    double scale, int* status) {
+                                                    double scale, unsigned long long* n_upd,
+                                                    int* status) {
   const int tiles_x = (g.n_x + kTx - 1) / kTx;
   const int ix = (blockIdx.x % tiles_x) * kTx + (threadIdx.x % kTx);
   const int iy = (blockIdx.x / tiles_x) * kTy + (threadIdx.x / kTx);
-  if (ix >= g.n_x || iy >= g.n_y) return;
+  unsigned cnt = 0;
+  if (ix < g.n_x && iy < g.n_y) {
   const int k = blockIdx.y;
   const int ip = angle_begin + k * angle_step;
   const AngleCS a = cs[k];
@@ -95,11 +130,16 @@ __global__ void __launch_bounds__(128) fwd3d_kernel(DevGeom g, const AngleCS* __
   const long long plane = (long long)g.n_x * g.n_y;
   const T* xcol = x + (long long)iy * g.n_x + ix;
   fast::column_weights(
-      g, a.C, a.S, ix, iy, 0, g.n_z, status, [&](int iz) { return ld(&xcol[iz * plane]) * scale; },
+      g, a.C, a.S, ix, iy, 0, g.n_z, status,
+      [&](int iz) { return ld(&xcol[iz * plane]) * scale; },
       [&](int iz, int m_y, int m_z, double w, double xs) {
-        atomicAdd(&yblk[(long long)(m_z + g.n_det_z / 2) * g.n_det_y + (m_y + g.n_det_y / 2)],
-                  (unsigned long long)__double2ll_rn(w * xs));
+        ++cnt;
+        if (xs != 0.0)
+          atomicAdd(&yblk[(long long)(m_z + g.n_det_z / 2) * g.n_det_y + (m_y + g.n_det_y / 2)],
+                    (unsigned long long)__double2ll_rn(w * xs));
       });
+  }
+  count_updates(n_upd, cnt);
 }
 
 constexpr int kZChunk = 8;
@@ -242,41 +282,64 @@ static dim3 tile_grid(const DevGeom& g, unsigned ydim) {
 
 cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
                    int angle_step, int n_sel, const void* x, unsigned long long* yacc,
-                   double scale, int* status, cudaStream_t st) {
+                   double scale, unsigned long long* n_upd, int* status, cudaStream_t st) {
   if (n_sel <= 0) return cudaSuccess;
   const bool two_d = (g.n_z == 1 && g.n_det_z == 1);
   const dim3 grid = tile_grid(g, (unsigned)n_sel);
   if (two_d) {
     if (dtype == CTSM_F64)
       fwd2d_kernel<double><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step,
-                                                 (const double*)x, yacc, scale, status);
+                                                 (const double*)x, yacc, scale, n_upd, status);
     else
       fwd2d_kernel<float><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step,
-                                                (const float*)x, yacc, scale, status);
+                                                (const float*)x, yacc, scale, n_upd, status);
   } else {
     if (dtype == CTSM_F64)
       fwd3d_kernel<double><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step,
-                                                 (const double*)x, yacc, scale, status);
+                                                 (const double*)x, yacc, scale, n_upd, status);
     else
       fwd3d_kernel<float><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step,
-                                                (const float*)x, yacc, scale, status);
+                                                (const float*)x, yacc, scale, n_upd, status);
   }
   count_launch();
   return cudaGetLastError();
 }
 
+int bwd_chunks(const DevGeom& g, int n_sel) {
+  const bool two_d = (g.n_z == 1 && g.n_det_z == 1);
+  if (!two_d || n_sel <= 1) return 1;
+  const long long tiles = (long long)((g.n_x + kTx - 1) / kTx) * ((g.n_y + kTy - 1) / kTy);
+  // aim for >= ~16 resident-block waves (148 SMs x ~6 blocks of 128 threads)
+  long long c = (16LL * 148 * 6 + tiles - 1) / tiles;
+  if (c > n_sel) c = n_sel;
+  if (c > 64) c = 64;
+  return (int)(c < 1 ? 1 : c);
+}
+
 cudaError_t bwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
-                   int angle_step, int n_sel, const void* y, void* x, int* status,
-                   cudaStream_t st) {
+                   int angle_step, int n_sel, const void* y, void* x, double* part, int n_chunks,
+                   int* status, cudaStream_t st) {
   const bool two_d = (g.n_z == 1 && g.n_det_z == 1);
   if (two_d) {
-    const dim3 grid = tile_grid(g, 1);
+    const int chunk = (n_sel + n_chunks - 1) / (n_chunks > 0 ? n_chunks : 1);
+    const int nc = chunk > 0 ? (n_sel + chunk - 1) / chunk : 1;
+    const dim3 grid = tile_grid(g, (unsigned)(nc > 0 ? nc : 1));
+    double* p = nc > 1 ? part : nullptr;
     if (dtype == CTSM_F64)
-      bwd2d_kernel<double><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step, n_sel,
-                                                 (const double*)y, (double*)x, status);
+      bwd2d_kernel<double><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step, n_sel, chunk,
+                                                 (const double*)y, (double*)x, p, status);
     else
-      bwd2d_kernel<float><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step, n_sel,
-                                                (const float*)y, (float*)x, status);
+      bwd2d_kernel<float><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step, n_sel, chunk,
+                                                (const float*)y, (float*)x, p, status);
+    count_launch();
+    if (nc > 1) {
+      const long long n = (long long)g.n_x * g.n_y;
+      if (dtype == CTSM_F64)
+        bwd_reduce_kernel<double><<<grid_for(n), 256, 0, st>>>(n, nc, part, (double*)x);
+      else
+        bwd_reduce_kernel<float><<<grid_for(n), 256, 0, st>>>(n, nc, part, (float*)x);
+      count_launch();
+    }
   } else {
     const dim3 grid = tile_grid(g, (unsigned)((g.n_z + kZChunk - 1) / kZChunk));
     if (dtype == CTSM_F64)
@@ -285,8 +348,8 @@ cudaError_t bwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_beg
     else
       bwd3d_kernel<float><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step, n_sel,
                                                 (const float*)y, (float*)x, status);
+    count_launch();
   }
-  count_launch();
   return cudaGetLastError();
 }
 
