@@ -61,7 +61,7 @@ __device__ __forceinline__ bool column_weights(const DevGeom& g, double C, doubl
   // pieces (in range cells only) and per-cell 2D weights
   Piece3 pc[kMaxBrk];
   int np = 0;
-  int ng = 0;
+  int ng = 0, last_end = 0;
   unsigned char gbeg[kMaxBrk], gend[kMaxBrk];
   double gw2d[kMaxBrk];
   bool overflow = false;
@@ -81,12 +81,12 @@ __device__ __forceinline__ bool column_weights(const DevGeom& g, double C, doubl
       },
       [&](int cell, double acc) {
         if (cell < cell_lo || cell > cell_hi) return;
-        const int first = (ng == 0) ? 0 : gend[ng - 1];
-        if (np > first) {
-          gbeg[ng] = (unsigned char)first;
+        if (np > last_end) {
+          gbeg[ng] = (unsigned char)last_end;
           gend[ng] = (unsigned char)np;
           gw2d[ng] = acc > 0.0 ? acc : 0.0;
           ++ng;
+          last_end = np;
         }
       });
   if (overflow) {
