@@ -1,0 +1,305 @@
+// fast3dw.cuh -- matrix-free evaluation of the 3D consistent weights (voxel
+// volume fractions per detector cell), warp-cooperative along a voxel column.
+//
+// Same quantity as voxel_volume_factors (weights3d.cpp:354-462):
+//  * the xy sweep (weights2d.cpp:38-87) does not depend on iz; it is done once
+//    per (column, angle) in the ray parameter t = tan(beta) (fast2d.cuh);
+//  * the canonical quarter-turn frame (geometry.cpp:76-97) is the one whose
+//    y0 face is the "low" face; phi' = phi - k pi/2 gives
+//    (sin, cos) = (S, C), (-C, S), (-S, -C), (C, -S);
+//  * the z composition (weights3d.cpp:380-458) uses the reference's closed-form
+//    trapezoid / corner-triangle atoms (weights3d.cpp:51-168), keeping their
+//    cancellation-safe branch forms, with tan(beta) = t exactly. Every
+//    quantity of an atom that does not depend on the plane height G is
+//    precomputed once per (column, angle, piece) -- by one lane per piece --
+//    into shared memory; per voxel an atom costs three subtractions, the flag
+//    tests and a cubic.
+#pragma once
+#include "common.cuh"
+#include "fast2d.cuh"
+
+namespace ctsmb {
+namespace fast {
+
+constexpr int kMaxPieces = 12;  // pieces of one column sweep inside the detector
+
+// G-independent coefficients of one sweep piece (16 doubles).
+//  kind 0/2 (corner triangle, atoms at the two endpoints lo/hi):
+//    c[0..6]  = lo: th_g, th_gg, th_h, crg, delta, srh_C, t
+//    c[7..13] = hi: same
+//  kind 1 (trapezoid band between t1 = lo and t2 = hi):
+//    c[0..12] = th_g1, th_g2, th_f1, th_f2, cr1, cr2, d12, A2g, A3g, A2f, A3f, Pg, Pf
+struct PieceCoef {
+  double c[16];
+};
+
+struct ColumnHead {
+  double S, C, invS, invC, kappa;  // canonical sin/cos of phi', 1/S, 1/C, a'^2/(6 b' c)
+  double inv_a;                    // 1 / a' (G = zref / (a' tan_a))
+  double dmin_inv, dmax_inv;       // extremes of 1/depth over the 4 xy corners
+  int flat;                        // |S| <= 1e-8: flat-source branch (weights3d.cpp:68, 142)
+  int np, ng;
+  int pkind[kMaxPieces];
+  int gcell[kMaxPieces];
+  unsigned char gbeg[kMaxPieces], gend[kMaxPieces];
+  double gw2d[kMaxPieces];
+};
+
+__device__ __forceinline__ double cube3(double v) { return v * v * v; }
+
+// Corner-triangle atom from precomputed coefficients (tri_atom_flags,
+// weights3d.cpp:129-168), without the kappa*|tan_a| factor.
+__device__ __forceinline__ double tri_tt(const ColumnHead& h, const double* c, double G) {
+  const double g = G - c[0], gg = G - c[1], hh = G - c[2];
+  const bool fg = g > 0.0, fgg = gg > 0.0, fh = hh > 0.0;
+  if (!h.flat) {
+    double pair;
+    if (fg && fgg) {
+      const double crg = c[3], d = c[4], S = h.S;
+      pair = crg * (3.0 * gg * gg * d + 3.0 * gg * S * d * d + S * S * cube3(d)) - cube3(gg) * c[5];
+    } else if (!fg && !fgg) {
+      pair = 0.0;
+    } else {
+      double v = 0.0;
+      if (fg) v += c[3] * cube3(g);
+      if (fgg) v -= cube3(gg) * h.invC;
+      pair = v * h.invS;
+    }
+    return pair + (fh ? c[5] * cube3(hh) : 0.0);
+  }
+  const double t = c[6];
+  double tv = 0.0;
+  if (fg) tv += g * g * (t * g - 3.0 * t * (g - hh));
+  if (fh) tv -= t * cube3(hh);
+  return tv;
+}
+
+// Trapezoid atom (trap_face_part / trap_atom_flags, weights3d.cpp:51-107),
+// without the kappa*|tan_a| factor.
+__device__ __forceinline__ double trap_tt(const ColumnHead& h, const double* c, double G) {
+  if (!h.flat) {
+    auto face = [&](double th1, double th2, double A2, double A3) -> double {
+      const bool f1 = G - th1 > 0.0, f2 = G - th2 > 0.0;
+      if (f1 && f2) return c[6] * (cube3(G) - G * A2 + A3);
+      if (!f1 && !f2) return 0.0;
+      double v = 0.0;
+      if (f1) v += c[4] * cube3(G - th1);
+      if (f2) v -= c[5] * cube3(G - th2);
+      return v * h.invS;
+    };
+    return face(c[0], c[1], c[7], c[8]) - face(c[2], c[3], c[9], c[10]);
+  }
+  const double gv = G - c[11], fv = G - c[12];
+  double t = 0.0;
+  if (gv > 0.0) t += gv * gv * (gv + 3.0 * c[11]);
+  if (fv > 0.0) t -= fv * fv * (fv + 3.0 * c[12]);
+  return t * c[6];
+}
+
+// Plans one (column, angle): every lane of the warp computes the sweep (cheap,
+// identical), lane j computes piece j's coefficients into P[j]; lane 0 writes
+// the head. Caller must __syncwarp() before reading H / P.
+__device__ __forceinline__ bool plan_column(const DevGeom& g, double C, double S, int ix, int iy,
+                                            int* status, ColumnHead& H, PieceCoef* P,
+                                            int lane) {
+  const double x0 = (ix - g.n_x / 2.0) * g.a, x1 = x0 + g.a;
+  const double y0 = (iy - g.n_y / 2.0) * g.b, y1 = y0 + g.b;
+  const double s = g.s;
+  Sweep2 sw;
+  if (!sweep_setup(g, C, S, x0, x1, y0, y1, status, sw)) {
+    if (lane == 0) {
+      H.np = 0;
+      H.ng = 0;
+    }
+    return false;
+  }
+  const int kq = sw.low_face;
+  double Sp, Cp;
+  switch (kq) {
+    case 0: Sp = S; Cp = C; break;
+    case 1: Sp = -C; Cp = S; break;
+    case 2: Sp = -S; Cp = -C; break;
+    default: Sp = C; Cp = -S; break;
+  }
+  double fx0 = x0, fx1 = x1, fy0 = y0, fy1 = y1;
+  double ax1 = sw.Ta_x, ay1 = sw.Ta_y, ax4 = sw.Tb_x, ay4 = sw.Tb_y;
+  for (int r = 0; r < kq; ++r) {
+    const double nx0 = fy0, nx1 = fy1, ny0 = -fx1, ny1 = -fx0;
+    fx0 = nx0; fx1 = nx1; fy0 = ny0; fy1 = ny1;
+    double t = ax1; ax1 = ay1; ay1 = -t;
+    t = ax4; ax4 = ay4; ay4 = -t;
+  }
+  const double ca = fx1 - fx0, cb = fy1 - fy0;
+  const int cell_lo = -g.n_det_y / 2, cell_hi = g.n_det_y / 2 - 1;
+  int np = 0, ng = 0, last_end = 0;
+  double my_lo = 0.0, my_hi = 0.0;
+  int my_kind = -1;
+  bool overflow = false;
+  sweep_walk(
+      g, C, S, sw,
+      [&](int cell, double tlo, double thi, int zone, double) {
+        if (cell < cell_lo || cell > cell_hi) return;
+        if (np == kMaxPieces) {
+          overflow = true;
+          return;
+        }
+        if (lane == np) {
+          my_lo = tlo;
+          my_hi = thi;
+          my_kind = zone;
+        }
+        if (lane == 0) H.pkind[np] = zone;
+        ++np;
+      },
+      [&](int cell, double acc) {
+        if (cell < cell_lo || cell > cell_hi) return;
+        if (np > last_end) {
+          if (lane == 0) {
+            H.gbeg[ng] = (unsigned char)last_end;
+            H.gend[ng] = (unsigned char)np;
+            H.gcell[ng] = cell;
+            H.gw2d[ng] = acc > 0.0 ? acc : 0.0;
+          }
+          ++ng;
+          last_end = np;
+        }
+      });
+  if (overflow) {
+    raise_status(status, CTSM_ERR_TOO_LARGE);
+    if (lane == 0) {
+      H.np = 0;
+      H.ng = 0;
+    }
+    return false;
+  }
+  const bool flat = !(fabs(Sp) > kEpsSingular);
+  if (lane == 0) {
+    H.S = Sp;
+    H.C = Cp;
+    H.invS = flat ? 0.0 : 1.0 / Sp;
+    H.invC = 1.0 / Cp;
+    H.kappa = ca * ca / (6.0 * cb * g.c);
+    H.inv_a = 1.0 / ca;
+    double dmn = frcp(sw.D[0]), dmx = dmn;
+    for (int k = 1; k < 4; ++k) {
+      const double v = frcp(sw.D[k]);
+      dmn = fmin(dmn, v);
+      dmx = fmax(dmx, v);
+    }
+    H.dmin_inv = dmn;
+    H.dmax_inv = dmx;
+    H.flat = flat;
+    H.np = np;
+    H.ng = ng;
+  }
+  if (lane < np) {
+    double* c = P[lane].c;
+    if (my_kind == 1) {
+      // trap_flags_at / trap_atom_flags (weights3d.cpp:63-107)
+      const double t1 = my_lo, t2 = my_hi;
+      const double cr1 = Cp + Sp * t1, cr2 = Cp + Sp * t2;
+      const double Pg = (s * Cp - fx1) / ca, Pf = (s * Cp - fx0) / ca;
+      const double i1 = 1.0 / cr1, i2 = 1.0 / cr2, i12 = i1 * i2;
+      c[0] = Pg * i1;
+      c[1] = Pg * i2;
+      c[2] = Pf * i1;
+      c[3] = Pf * i2;
+      c[4] = cr1;
+      c[5] = cr2;
+      c[6] = t1 - t2;
+      c[7] = 3.0 * Pg * Pg * i12;
+      c[8] = Pg * Pg * Pg * (cr1 + cr2) * i12 * i12;
+      c[9] = 3.0 * Pf * Pf * i12;
+      c[10] = Pf * Pf * Pf * (cr1 + cr2) * i12 * i12;
+      c[11] = Pg;
+      c[12] = Pf;
+    } else {
+      // tri_flags_at / tri_atom_flags (weights3d.cpp:115-168) at both ends
+      const double xa = my_kind == 0 ? ax1 : ax4, ya = my_kind == 0 ? ay1 : ay4;
+      const double Pq = (s * Cp - xa) / ca, Qq = (s * Sp - ya) / ca;
+      const double thgg = Pq * Cp + Qq * Sp;
+      for (int e = 0; e < 2; ++e) {
+        const double t = e == 0 ? my_lo : my_hi;
+        const double crg = Cp + Sp * t, srh = Sp - Cp * t;
+        double* q = c + 7 * e;
+        q[0] = Pq / crg;
+        q[1] = thgg;
+        q[2] = Qq / srh;
+        q[3] = crg;
+        q[4] = Qq - Pq * srh / crg;
+        q[5] = srh / Cp;
+        q[6] = t;
+      }
+    }
+  }
+  return true;
+}
+
+// atom_sum (weights3d.cpp:400-423) over the pieces of cell group q at height
+// zref for row-edge slope tan_a.
+__device__ __forceinline__ double atom_sum3(const ColumnHead& H, const PieceCoef* P, int q,
+                                            double tan_a, double zref) {
+  const double G = zref * H.inv_a / tan_a;
+  double v = 0.0;
+  for (int k = H.gbeg[q]; k < H.gend[q]; ++k) {
+    const double* c = P[k].c;
+    double tt;
+    switch (H.pkind[k]) {
+      case 0: tt = fabs(tri_tt(H, c + 7, G)) - fabs(tri_tt(H, c, G)); break;
+      case 1: tt = fabs(trap_tt(H, c, G)); break;
+      default: tt = fabs(tri_tt(H, c, G)) - fabs(tri_tt(H, c + 7, G)); break;
+    }
+    v += tt;
+  }
+  return H.kappa * tan_a * v;
+}
+
+// Weights of voxel iz of a planned column: emit(cell m_y, row m_z, w) for every
+// w > 1e-16 inside the detector (weights3d.cpp:426-458).
+template <typename Emit>
+__device__ __forceinline__ void voxel_weights(const DevGeom& g, const ColumnHead& H,
+                                              const PieceCoef* P, int iz, Emit&& emit) {
+  const double sdd = g.sdd;
+  const double zb = (iz - g.n_z / 2.0) * g.c, zt = zb + g.c;
+  const double sdd_dz = sdd / g.d_z;
+  const double mb1 = sdd_dz * zb * H.dmin_inv, mb2 = sdd_dz * zb * H.dmax_inv;
+  const double mt1 = sdd_dz * zt * H.dmin_inv, mt2 = sdd_dz * zt * H.dmax_inv;
+  const double m_min = fmin(fmin(mb1, mb2), fmin(mt1, mt2));
+  const double m_max = fmax(fmax(mb1, mb2), fmax(mt1, mt2));
+  const int row_lo = -g.n_det_z / 2, row_hi = g.n_det_z / 2 - 1;
+  const int fl = (int)floor(m_min);
+  const int k_lo = (fl < row_lo) ? row_lo : fl;
+  const int chi = (int)ceil(m_max) - 1;
+  const int k_hi = (chi < row_hi) ? chi : row_hi;
+  if (k_hi < k_lo) return;
+  const double dz_sdd = g.d_z / sdd;
+  for (int q = 0; q < H.ng; ++q) {
+    const double w2d = H.gw2d[q];
+    auto above = [&](double kk) -> double {
+      if (kk <= m_min) return w2d;
+      if (kk >= m_max) return 0.0;
+      if (kk == 0.0) {
+        if (zb >= 0.0) return w2d;
+        if (zt <= 0.0) return 0.0;
+        return w2d * zt / (zt - zb);
+      }
+      if (kk > 0.0) {
+        const double tan_a = kk * dz_sdd;
+        return atom_sum3(H, P, q, tan_a, zt) - atom_sum3(H, P, q, tan_a, zb);
+      }
+      const double tan_a = -kk * dz_sdd;
+      return w2d - (atom_sum3(H, P, q, tan_a, -zb) - atom_sum3(H, P, q, tan_a, -zt));
+    };
+    const int cell = H.gcell[q];
+    double prev = above((double)k_lo);
+    for (int L = k_lo; L <= k_hi; ++L) {
+      const double next = above((double)(L + 1));
+      const double v = prev - next;
+      if (v > kEpsWeight) emit(cell, L, v);
+      prev = next;
+    }
+  }
+}
+
+}  // namespace fast
+}  // namespace ctsmb

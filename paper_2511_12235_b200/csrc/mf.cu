@@ -9,7 +9,7 @@
 // voxel-driven gather: each thread owns one pixel/voxel, loops over the angle
 // shard and accumulates in FP64 registers -- no atomics, deterministic.
 #include "fast2d.cuh"
-#include "fast3d.cuh"
+#include "fast3dw.cuh"
 #include "kernels.h"
 
 namespace ctsmb {
@@ -109,71 +109,70 @@ __global__ void bwd_reduce_kernel(long long n, int n_chunks, const double* __res
   }
 }
 
-// 3D: one thread per (voxel column, angle) for forward; per (voxel column,
-// z-chunk) looping over angles for backward.
-template <typename T>
-__global__ void __launch_bounds__(128) fwd3d_kernel(DevGeom g, const AngleCS* __restrict__ cs,
-                                                    int angle_begin, int angle_step,
-                                                    const T* __restrict__ x,
-                                                    unsigned long long* __restrict__ yacc,
-                                                    double scale, unsigned long long* n_upd,
-                                                    int* status) {
-  const int tiles_x = (g.n_x + kTx - 1) / kTx;
-  const int ix = (blockIdx.x % tiles_x) * kTx + (threadIdx.x % kTx);
-  const int iy = (blockIdx.x / tiles_x) * kTy + (threadIdx.x / kTx);
+// 3D (K5/K6): one warp per voxel column; the warp loops over the angle
+// shard, plans the column once per angle (sweep + atom coefficients in shared
+// memory, fast3dw.cuh) and its lanes evaluate contiguous z-chunks of voxels.
+// Forward scatters w*x into the fixed-point sinogram accumulator; backward
+// accumulates w*y per voxel in shared memory in a fixed order (deterministic).
+constexpr int kWarps3 = 4;
+constexpr int kZcMax = 16;  // voxels per lane per z-block (z-block = 512 voxels)
+
+template <typename T, bool kFwd>
+__global__ void __launch_bounds__(kWarps3 * 32) proj3d_kernel(
+    DevGeom g, const AngleCS* __restrict__ cs, int angle_begin, int angle_step, int n_sel,
+    const T* __restrict__ in, T* __restrict__ xout, unsigned long long* __restrict__ yacc,
+    double scale, unsigned long long* n_upd, int* status) {
+  __shared__ fast::ColumnHead sh[kWarps3];
+  __shared__ fast::PieceCoef sp[kWarps3][fast::kMaxPieces];
+  __shared__ double sacc[kWarps3][kZcMax][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long nxy = (long long)g.n_x * g.n_y;
+  const long long col = (long long)blockIdx.x * kWarps3 + warp;
+  if (col >= nxy) return;  // whole warp
+  const int ix = (int)(col % g.n_x), iy = (int)(col / g.n_x);
+  const long long plane = nxy;
+  const int rpa = g.rows_per_angle;
+  const int hy = g.n_det_y / 2, hz = g.n_det_z / 2;
   unsigned cnt = 0;
-  if (ix < g.n_x && iy < g.n_y) {
-  const int k = blockIdx.y;
-  const int ip = angle_begin + k * angle_step;
-  const AngleCS a = cs[k];
-  unsigned long long* yblk = yacc + (long long)ip * g.rows_per_angle;
-  const long long plane = (long long)g.n_x * g.n_y;
-  const T* xcol = x + (long long)iy * g.n_x + ix;
-  fast::column_weights(
-      g, a.C, a.S, ix, iy, 0, g.n_z, status,
-      [&](int iz) { return ld(&xcol[iz * plane]) * scale; },
-      [&](int iz, int m_y, int m_z, double w, double xs) {
-        ++cnt;
-        if (xs != 0.0)
-          atomicAdd(&yblk[(long long)(m_z + g.n_det_z / 2) * g.n_det_y + (m_y + g.n_det_y / 2)],
-                    (unsigned long long)__double2ll_rn(w * xs));
-      });
+  for (int zb0 = 0; zb0 < g.n_z; zb0 += 32 * kZcMax) {
+    const int nzb = min(32 * kZcMax, g.n_z - zb0);
+    const int zc = (nzb + 31) / 32;
+    const int z0 = zb0 + lane * zc, z1 = min(z0 + zc, zb0 + nzb);
+    if (!kFwd)
+      for (int i = 0; i < zc; ++i) sacc[warp][i][lane] = 0.0;
+    for (int k = 0; k < n_sel; ++k) {
+      const int ip = angle_begin + k * angle_step;
+      const AngleCS a = cs[k];
+      __syncwarp();
+      const bool ok = fast::plan_column(g, a.C, a.S, ix, iy, status, sh[warp], sp[warp], lane);
+      __syncwarp();
+      if (!ok) continue;
+      const fast::ColumnHead& H = sh[warp];
+      const fast::PieceCoef* P = sp[warp];
+      for (int iz = z0; iz < z1; ++iz) {
+        if (kFwd) {
+          const double xs = ld(&in[iz * plane + col]) * scale;
+          unsigned long long* yb = yacc + (long long)ip * rpa;
+          fast::voxel_weights(g, H, P, iz, [&](int my, int mz, double w) {
+            ++cnt;
+            if (xs != 0.0)
+              atomicAdd(&yb[(long long)(mz + hz) * g.n_det_y + (my + hy)],
+                        (unsigned long long)__double2ll_rn(w * xs));
+          });
+        } else {
+          const T* yb = in + (long long)ip * rpa;
+          double v = 0.0;
+          fast::voxel_weights(g, H, P, iz, [&](int my, int mz, double w) {
+            v += w * ld(&yb[(long long)(mz + hz) * g.n_det_y + (my + hy)]);
+          });
+          sacc[warp][iz - z0][lane] += v;
+        }
+      }
+    }
+    if (!kFwd)
+      for (int iz = z0; iz < z1; ++iz) xout[iz * plane + col] = (T)sacc[warp][iz - z0][lane];
   }
-  count_updates(n_upd, cnt);
-}
-
-constexpr int kZChunk = 8;
-
-template <typename T>
-__global__ void __launch_bounds__(128) bwd3d_kernel(DevGeom g, const AngleCS* __restrict__ cs,
-                                                    int angle_begin, int angle_step, int n_sel,
-                                                    const T* __restrict__ y, T* __restrict__ x,
-                                                    int* status) {
-  const int tiles_x = (g.n_x + kTx - 1) / kTx;
-  const int ix = (blockIdx.x % tiles_x) * kTx + (threadIdx.x % kTx);
-  const int iy = (blockIdx.x / tiles_x) * kTy + (threadIdx.x / kTx);
-  const int z0 = blockIdx.y * kZChunk;
-  if (ix >= g.n_x || iy >= g.n_y) return;
-  const int z1 = min(z0 + kZChunk, g.n_z);
-  double acc[kZChunk];
-#pragma unroll
-  for (int i = 0; i < kZChunk; ++i) acc[i] = 0.0;
-  for (int k = 0; k < n_sel; ++k) {
-    const int ip = angle_begin + k * angle_step;
-    const AngleCS a = cs[k];
-    const T* yblk = y + (long long)ip * g.rows_per_angle;
-    fast::column_weights(
-        g, a.C, a.S, ix, iy, z0, z1, status, [&](int) { return 1.0; },
-        [&](int iz, int m_y, int m_z, double w, double) {
-          const double yv =
-              ld(&yblk[(long long)(m_z + g.n_det_z / 2) * g.n_det_y + (m_y + g.n_det_y / 2)]);
-#pragma unroll
-          for (int i = 0; i < kZChunk; ++i)
-            if (iz - z0 == i) acc[i] += w * yv;
-        });
-  }
-  const long long plane = (long long)g.n_x * g.n_y;
-  for (int iz = z0; iz < z1; ++iz) x[iz * plane + (long long)iy * g.n_x + ix] = (T)acc[iz - z0];
+  if (kFwd) count_updates(n_upd, cnt);
 }
 
 template <typename T>
@@ -294,12 +293,16 @@ cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_beg
       fwd2d_kernel<float><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step,
                                                 (const float*)x, yacc, scale, n_upd, status);
   } else {
+    const long long nxy = (long long)g.n_x * g.n_y;
+    const unsigned blocks = (unsigned)((nxy + kWarps3 - 1) / kWarps3);
     if (dtype == CTSM_F64)
-      fwd3d_kernel<double><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step,
-                                                 (const double*)x, yacc, scale, n_upd, status);
+      proj3d_kernel<double, true><<<blocks, kWarps3 * 32, 0, st>>>(
+          g, cs, angle_begin, angle_step, n_sel, (const double*)x, nullptr, yacc, scale, n_upd,
+          status);
     else
-      fwd3d_kernel<float><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step,
-                                                (const float*)x, yacc, scale, n_upd, status);
+      proj3d_kernel<float, true><<<blocks, kWarps3 * 32, 0, st>>>(
+          g, cs, angle_begin, angle_step, n_sel, (const float*)x, nullptr, yacc, scale, n_upd,
+          status);
   }
   count_launch();
   return cudaGetLastError();
@@ -341,13 +344,16 @@ cudaError_t bwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_beg
       count_launch();
     }
   } else {
-    const dim3 grid = tile_grid(g, (unsigned)((g.n_z + kZChunk - 1) / kZChunk));
+    const long long nxy = (long long)g.n_x * g.n_y;
+    const unsigned blocks = (unsigned)((nxy + kWarps3 - 1) / kWarps3);
     if (dtype == CTSM_F64)
-      bwd3d_kernel<double><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step, n_sel,
-                                                 (const double*)y, (double*)x, status);
+      proj3d_kernel<double, false><<<blocks, kWarps3 * 32, 0, st>>>(
+          g, cs, angle_begin, angle_step, n_sel, (const double*)y, (double*)x, nullptr, 1.0,
+          nullptr, status);
     else
-      bwd3d_kernel<float><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step, n_sel,
-                                                (const float*)y, (float*)x, status);
+      proj3d_kernel<float, false><<<blocks, kWarps3 * 32, 0, st>>>(
+          g, cs, angle_begin, angle_step, n_sel, (const float*)y, (float*)x, nullptr, 1.0,
+          nullptr, status);
     count_launch();
   }
   return cudaGetLastError();

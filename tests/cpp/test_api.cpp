@@ -89,7 +89,7 @@ int main() {
       md = std::max(md, std::abs(y0[i] - y1[i]));
       mv = std::max(mv, std::abs(y0[i]));
     }
-    EXPECT(md <= 1e-12 * std::max(1.0, mv));
+    EXPECT(md <= 1e-10 * std::max(1.0, mv));  // fast path vs exact CSR: fp64 parity bar
     // matrix-free adjoint == stored transpose
     const auto x0 = back_project(w, y);
     const auto x1 = back_project_matrix_free(g, MatrixMode::consistent, 1, y, 2);
@@ -98,7 +98,7 @@ int main() {
       md = std::max(md, std::abs(x0[i] - x1[i]));
       mv = std::max(mv, std::abs(x0[i]));
     }
-    EXPECT(md <= 1e-12 * std::max(1.0, mv));
+    EXPECT(md <= 1e-10 * std::max(1.0, mv));  // fast path vs exact CSR: fp64 parity bar
     EXPECT(code_of([&] { forward_project(w, std::vector<double>(w.n_cols + 1)); }) ==
            (int)ErrorCode::DimensionMismatch);
   }
