@@ -5,6 +5,6 @@ python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke
 timeout ${PYTEST_TIMEOUT:-1500} python -m pytest tests -m gpu -q -p no:cacheprovider ${PYTEST_ARGS} > gpurun_out/pytest.log 2>&1; tail -25 gpurun_out/pytest.log
 for spec in ${BENCHES:-"c1:f64"}; do
   cfg=${spec%%:*}; dt=${spec##*:}
-  timeout 900 python bench.py --config $cfg --dtype $dt --steps ${STEPS:-5} --warmup 3 > gpurun_out/bench_${cfg}_${dt}.log 2>&1
+  timeout 900 python bench.py --config $cfg --dtype $dt --steps ${STEPS:-5} --warmup ${WARMUP:-3} > gpurun_out/bench_${cfg}_${dt}.log 2>&1
   tail -1 gpurun_out/bench_${cfg}_${dt}.log
 done
