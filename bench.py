@@ -81,8 +81,9 @@ def run_reference(args):
     t0 = time.perf_counter()
     orc.forward_mf_angles(g, probe, x, cores)
     orc.back_mf_angles(g, probe, y, cores)
-    per_angle = (time.perf_counter() - t0) / probe.size
-    n_sample = int(min(g.n_angles, max(2, round(10.0 / max(per_angle, 1e-6)))))
+    tau = time.perf_counter() - t0  # ~ one angle's fwd+bwd (the 2 probes run in parallel)
+    # the reference parallelises over angles: use >= one angle per core
+    n_sample = int(min(g.n_angles, cores * max(1, int(10.0 / max(tau, 1e-6)))))
     angles = np.linspace(0, g.n_angles, n_sample, endpoint=False).astype(np.int32)
     times = []
     for it in range(args.warmup + args.steps):
@@ -359,8 +360,9 @@ def cpu_baseline_quick(cfg):
     t0 = time.perf_counter()
     orc.forward_mf_angles(g, probe, x, cores)
     orc.back_mf_angles(g, probe, y, cores)
-    per_angle = (time.perf_counter() - t0) / probe.size
-    n_sample = int(min(g.n_angles, max(2, round(10.0 / max(per_angle, 1e-6)))))
+    tau = time.perf_counter() - t0  # ~ one angle's fwd+bwd (the 2 probes run in parallel)
+    # the reference parallelises over angles: use >= one angle per core
+    n_sample = int(min(g.n_angles, cores * max(1, int(10.0 / max(tau, 1e-6)))))
     angles = np.linspace(0, g.n_angles, n_sample, endpoint=False).astype(np.int32)
     t0 = time.perf_counter()
     orc.forward_mf_angles(g, angles, x, cores)

@@ -37,6 +37,10 @@ struct DevGeom {
   long long n_vox;
   int edge_lo;       // edge-angle table covers e in [edge_lo, edge_lo + n_edges)
   int n_edges;
+  // host-precomputed constants for the matrix-free (fast) path only
+  double inv_a, inv_b, inv_2ab;  // 1/a, 1/b, 1/(2ab)
+  double u_scale, t_scale;       // (s+d)/d_y, d_y/(s+d)
+  double sdd_dz, dz_sdd;         // (s+d)/d_z, d_z/(s+d)
 };
 
 inline DevGeom make_dev_geom(const ctsm_geometry& g) {
@@ -61,6 +65,13 @@ inline DevGeom make_dev_geom(const ctsm_geometry& g) {
   d.n_vox = (long long)g.n_x * g.n_y * g.n_z;
   d.edge_lo = 0;
   d.n_edges = 0;
+  d.inv_a = 1.0 / g.a;
+  d.inv_b = 1.0 / g.b;
+  d.inv_2ab = 0.5 / (g.a * g.b);
+  d.u_scale = d.sdd / g.d_y;
+  d.t_scale = g.d_y / d.sdd;
+  d.sdd_dz = d.sdd / g.d_z;
+  d.dz_sdd = g.d_z / d.sdd;
   return d;
 }
 

@@ -104,12 +104,11 @@ __device__ __forceinline__ bool sweep_setup(const DevGeom& g, double C, double S
     w.T2 = m;
     w.T3 = m;
   }
-  const double inv2ab = 0.5 / (g.a * g.b);
-  w.K1 = Dap1 * Dap1 * inv2ab;
-  w.K4 = Dap4 * Dap4 * inv2ab;
+  w.K1 = Dap1 * Dap1 * g.inv_2ab;
+  w.K4 = Dap4 * Dap4 * g.inv_2ab;
   w.band_vertical = (k & 1) == 0;
-  w.band_k = w.band_vertical ? fabs(s * C - 0.5 * (x0 + x1)) / g.b
-                             : fabs(s * S - 0.5 * (y0 + y1)) / g.a;
+  w.band_k = w.band_vertical ? fabs(s * C - 0.5 * (x0 + x1)) * g.inv_b
+                             : fabs(s * S - 0.5 * (y0 + y1)) * g.inv_a;
   return true;
 }
 
@@ -120,8 +119,8 @@ __device__ __forceinline__ bool sweep_setup(const DevGeom& g, double C, double S
 template <typename Piece, typename CellDone>
 __device__ __forceinline__ void sweep_walk(const DevGeom& g, double C, double S, const Sweep2& w,
                                            Piece&& piece, CellDone&& cell_done) {
-  const double scale = g.sdd / g.d_y;
-  const double inv_scale = g.d_y / g.sdd;
+  const double scale = g.u_scale;
+  const double inv_scale = g.t_scale;
   const double T1 = w.T1, T2 = w.T2, T3 = w.T3, T4 = w.T4;
   const long long e_lo = (long long)floor(T1 * scale) + 1;
   const long long e_hi = (long long)ceil(T4 * scale) - 1;
@@ -213,6 +212,14 @@ __device__ __forceinline__ void sweep_walk(const DevGeom& g, double C, double S,
 // Streams the cell weights of pixel (ix, iy) at an angle with cos/sin (C, S)
 // to emit(cell_m, w) in ascending cell order; cells outside the detector are
 // skipped (weights2d.cpp:110-113), as are weights <= 1e-16 (125-127).
+//
+// Cell weights are differences of the cumulative area CA(t) (fraction of the
+// pixel with ray parameter < t):
+//   CA = A1(t)                             T1 <= t <= T2  (low corner triangle)
+//      = A1(T2) + band(T2, t)              T2 <= t <= T3
+//      = A1(T2) + band(T2, T3) + A4(T3) - A4(t)   T3 <= t <= T4
+// so every detector edge costs one independent reciprocal (good ILP) and the
+// zone constants four more.
 template <typename Emit>
 __device__ __forceinline__ bool pixel_weights(const DevGeom& g, double C, double S, int ix,
                                               int iy, int* status, Emit&& emit) {
@@ -220,12 +227,49 @@ __device__ __forceinline__ bool pixel_weights(const DevGeom& g, double C, double
   const double y0 = (iy - g.n_y / 2.0) * g.b, y1 = y0 + g.b;
   Sweep2 w;
   if (!sweep_setup(g, C, S, x0, x1, y0, y1, status, w)) return false;
+  const double T1 = w.T1, T2 = w.T2, T3 = w.T3, T4 = w.T4;
+  const bool bv = w.band_vertical;
+  auto pq_inv = [&](double t) {
+    const double v = fabs((C + t * S) * (t * C - S));
+    return v > kEpsAngle ? frcp(v) : 0.0;
+  };
+  auto p_inv = [&](double t) {
+    const double v = fabs(bv ? (C + t * S) : (t * C - S));
+    return v > kEpsAngle ? frcp(v) : 0.0;
+  };
+  // zone constants (independent reciprocals)
+  const double d12 = T2 - T1, d34 = T4 - T3, d23 = T3 - T2;
+  const double A1T2 = d12 > 0.0 ? w.K1 * d12 * d12 * pq_inv(T2) : 0.0;
+  const double A4T3 = d34 > 0.0 ? w.K4 * d34 * d34 * pq_inv(T3) : 0.0;
+  const double ipT2 = d23 > 0.0 ? p_inv(T2) : 0.0;
+  const double bandT = d23 > 0.0 ? w.band_k * d23 * ipT2 * p_inv(T3) : 0.0;
+  const double base2 = A1T2 + bandT + A4T3;  // CA(T4) (== 1 up to rounding)
+  auto CA = [&](double t) -> double {
+    if (t <= T2) {
+      const double d = t - T1;
+      return d > 0.0 ? w.K1 * d * d * pq_inv(t) : 0.0;
+    }
+    if (t < T3) return A1T2 + w.band_k * (t - T2) * ipT2 * p_inv(t);
+    const double d = T4 - t;
+    return base2 - (d > 0.0 ? w.K4 * d * d * pq_inv(t) : 0.0);
+  };
+  const double scale = g.u_scale;
+  const double inv_scale = g.t_scale;
+  const long long e_lo = (long long)floor(T1 * scale) + 1;
+  const long long e_hi = (long long)ceil(T4 * scale) - 1;
   const int cell_lo = -g.n_det_y / 2, cell_hi = g.n_det_y / 2 - 1;
-  sweep_walk(
-      g, C, S, w, [](int, double, double, int, double) {},
-      [&](int cell, double acc) {
-        if (acc > kEpsWeight && cell >= cell_lo && cell <= cell_hi) emit(cell, acc);
-      });
+  double prev = 0.0;  // CA(T1)
+  int cell = (int)(e_lo - 1);
+#pragma unroll 2
+  for (long long e = e_lo; e <= e_hi; ++e, ++cell) {
+    const double te = fmin(fmax(e * inv_scale, T1), T4);
+    const double cur = CA(te);
+    const double wv = cur - prev;
+    prev = cur;
+    if (wv > kEpsWeight && cell >= cell_lo && cell <= cell_hi) emit(cell, wv);
+  }
+  const double wv = base2 - prev;
+  if (wv > kEpsWeight && cell >= cell_lo && cell <= cell_hi) emit(cell, wv);
   return true;
 }
 

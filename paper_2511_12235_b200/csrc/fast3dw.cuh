@@ -261,7 +261,7 @@ __device__ __forceinline__ void voxel_weights(const DevGeom& g, const ColumnHead
                                               const PieceCoef* P, int iz, Emit&& emit) {
   const double sdd = g.sdd;
   const double zb = (iz - g.n_z / 2.0) * g.c, zt = zb + g.c;
-  const double sdd_dz = sdd / g.d_z;
+  const double sdd_dz = g.sdd_dz;
   const double mb1 = sdd_dz * zb * H.dmin_inv, mb2 = sdd_dz * zb * H.dmax_inv;
   const double mt1 = sdd_dz * zt * H.dmin_inv, mt2 = sdd_dz * zt * H.dmax_inv;
   const double m_min = fmin(fmin(mb1, mb2), fmin(mt1, mt2));
@@ -272,7 +272,7 @@ __device__ __forceinline__ void voxel_weights(const DevGeom& g, const ColumnHead
   const int chi = (int)ceil(m_max) - 1;
   const int k_hi = (chi < row_hi) ? chi : row_hi;
   if (k_hi < k_lo) return;
-  const double dz_sdd = g.d_z / sdd;
+  const double dz_sdd = g.dz_sdd;
   for (int q = 0; q < H.ng; ++q) {
     const double w2d = H.gw2d[q];
     auto above = [&](double kk) -> double {
