@@ -49,6 +49,9 @@ def parse():
     p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     p.add_argument("--no-clocks", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--mode", default="proj", choices=["proj", "sirt"],
+                   help="proj: one A x + A^T y per step; sirt: one SIRT iteration per step "
+                        "(BASELINE configs[4]: y = A x_true + 1%% noise)")
     return p.parse_args()
 
 
@@ -374,10 +377,117 @@ def cpu_baseline_quick(cfg):
             "sample": f"fwd+bwd over {angles.size} of {g.n_angles} strided angles ({t:.1f} s), extrapolated"}
 
 
+def run_sirt(args):
+    """SIRT iterations (x <- x + C A^T (R (y - A x))), angle-sharded; one step =
+    one iteration = one A x + one A^T r + the all-reduce. The setup (y = A
+    x_true + noise, R = 1/(A 1), C = 1/(A^T 1)) runs once, untimed."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_12235_b200 import CONFIGS, Context, _lib
+    from paper_2511_12235_b200.dist import angle_shard, shard_rows
+    from paper_2511_12235_b200.phantoms import phantom_for
+    from paper_2511_12235_b200.projector import (back_project_matrix_free,
+                                                 forward_project_matrix_free)
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = args.config
+    g = CONFIGS[cfg]
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    ctx = Context.get(local)
+    shard = angle_shard(g, rank, world)
+    rows = shard_rows(g, shard).to(dev)
+    t_setup0 = time.perf_counter()
+    x_true = torch.from_numpy(phantom_for(cfg, g, dtype=np.float32)).to(tdt).to(dev)
+    y = torch.zeros(g.n_measurements, dtype=tdt, device=dev)
+    forward_project_matrix_free(g, "consistent", 1, x_true, angles=shard, out=y)
+    ymax = y.abs().max()
+    if world > 1:
+        dist.all_reduce(ymax, op=dist.ReduceOp.MAX)
+    gen = torch.Generator(device=dev).manual_seed(12347 + rank)
+    y[rows] += 0.01 * ymax * torch.randn(rows.numel(), dtype=tdt, device=dev, generator=gen)
+    R = torch.zeros_like(y)
+    forward_project_matrix_free(g, "consistent", 1, torch.ones_like(x_true), angles=shard, out=R)
+    R[rows] = torch.where(R[rows] != 0, 1.0 / R[rows], torch.zeros_like(R[rows]))
+    Cc = back_project_matrix_free(g, "consistent", 1, torch.ones_like(y), angles=shard)
+    if world > 1:
+        dist.all_reduce(Cc)
+    Cc = torch.where(Cc != 0, 1.0 / Cc, torch.zeros_like(Cc))
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup0
+    x = torch.zeros_like(x_true)
+    ax = torch.zeros_like(y)
+    r = torch.zeros_like(y)
+    bp = torch.empty_like(x)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def iteration():
+        forward_project_matrix_free(g, "consistent", 1, x, angles=shard, out=ax)
+        r[rows] = R[rows] * (y[rows] - ax[rows])
+        back_project_matrix_free(g, "consistent", 1, r, angles=shard, out=bp)
+        if world > 1:
+            dist.all_reduce(bp)
+        x.add_(Cc * bp)
+
+    clocks = ClockSampler(local, not args.no_clocks)
+    for _ in range(args.warmup):
+        iteration()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = _lib.launch_count()
+    ms_total = 0.0
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        ev0.record()
+        iteration()
+        ev1.record()
+        torch.cuda.synchronize()
+        ms_total += ev0.elapsed_time(ev1)
+    launches = _lib.launch_count() - launches0
+    clk = clocks.stop()
+    ms = ms_total / args.steps
+    cnt = torch.tensor([float(_lib.lib().ctsm_last_update_count(ctx.handle)), ms],
+                       dtype=torch.float64, device=dev)
+    if world > 1:
+        upd = cnt[0:1].clone()
+        dist.all_reduce(upd)
+        msx = cnt[1:2].clone()
+        dist.all_reduce(msx, op=dist.ReduceOp.MAX)
+        cnt = torch.cat([upd, msx])
+    nnz_live, ms = int(cnt[0].item()), float(cnt[1].item())
+    if rank == 0:
+        resid = float(((y[rows] - ax[rows]) ** 2).sum().sqrt())
+        line = {
+            "metric": "voxel-ray updates/s (SIRT iterations)",
+            "value": 2.0 * nnz_live / (ms * 1e-3),
+            "unit": "updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": f"{cfg}: BASELINE.json configs[{cfg[1]}] SIRT (one iteration per step)",
+                       "parallelism": f"angle-shard x{world}", "setup_s": t_setup,
+                       "iterations_total": args.warmup + args.steps},
+            "updates_per_projection": nnz_live,
+            "rank0_residual_norm": resid,
+            "gpu_launches": int(launches), "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.mode == "sirt":
+        run_sirt(args)
     else:
         run_ours(args)
 

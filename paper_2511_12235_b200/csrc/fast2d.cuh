@@ -64,51 +64,48 @@ __device__ __forceinline__ bool sweep_setup(const DevGeom& g, double C, double S
     raise_status(status, CTSM_ERR_DEGENERATE_GEOMETRY);
     return false;
   }
-  const double t0 = (y0C - x0S) * frcp(D0), t1 = (y0C - x1S) * frcp(D1);
-  const double t2 = (y1C - x1S) * frcp(D2), t3 = (y1C - x0S) * frcp(D3);
   w.D[0] = D0; w.D[1] = D1; w.D[2] = D2; w.D[3] = D3;
-  // low face = argmin over faces of max(corner t)
-  const double f0 = fmax(t0, t1), f1 = fmax(t1, t2), f2 = fmax(t2, t3), f3 = fmax(t3, t0);
-  int k = 0;
-  double fm = f0;
-  if (f1 < fm) { fm = f1; k = 1; }
-  if (f2 < fm) { fm = f2; k = 2; }
-  if (f3 < fm) { fm = f3; k = 3; }
-  w.low_face = k;
-  // corners of the low face (a, a+1) and of the high face (a+2, a+3)
-  double la, lb, ha, hb, Dla, Dlb, Dha, Dhb, xla, yla, xlb, ylb, xha, yha, xhb, yhb;
-  switch (k) {
-    case 0: la = t0; lb = t1; ha = t2; hb = t3; Dla = D0; Dlb = D1; Dha = D2; Dhb = D3;
-            xla = x0; yla = y0; xlb = x1; ylb = y0; xha = x1; yha = y1; xhb = x0; yhb = y1; break;
-    case 1: la = t1; lb = t2; ha = t3; hb = t0; Dla = D1; Dlb = D2; Dha = D3; Dhb = D0;
-            xla = x1; yla = y0; xlb = x1; ylb = y1; xha = x0; yha = y1; xhb = x0; yhb = y0; break;
-    case 2: la = t2; lb = t3; ha = t0; hb = t1; Dla = D2; Dlb = D3; Dha = D0; Dhb = D1;
-            xla = x1; yla = y1; xlb = x0; ylb = y1; xha = x0; yha = y0; xhb = x1; yhb = y0; break;
-    default: la = t3; lb = t0; ha = t1; hb = t2; Dla = D3; Dlb = D0; Dha = D1; Dhb = D2;
-            xla = x0; yla = y1; xlb = x0; ylb = y0; xha = x1; yha = y0; xhb = x1; yhb = y1; break;
+  // corner parameters; corners 0 (x0,y0), 1 (x1,y0), 2 (x1,y1), 3 (x0,y1)
+  double ta = (y0C - x0S) * frcp(D0), tb = (y0C - x1S) * frcp(D1);
+  double tc = (y1C - x1S) * frcp(D2), td = (y1C - x0S) * frcp(D3);
+  double Da = D0, Db = D1, Dc = D2, Dd = D3;
+  int ia = 0, ib = 1, ic = 2, id = 3;
+  // 5-comparator sorting network on t, carrying depth and corner index
+  auto ce = [](double& t0, double& t1, double& d0, double& d1, int& i0, int& i1) {
+    const bool sw = t1 < t0;
+    const double tt = sw ? t1 : t0, tu = sw ? t0 : t1;
+    const double dd = sw ? d1 : d0, du = sw ? d0 : d1;
+    const int ii = sw ? i1 : i0, iu = sw ? i0 : i1;
+    t0 = tt; t1 = tu; d0 = dd; d1 = du; i0 = ii; i1 = iu;
+  };
+  ce(ta, tb, Da, Db, ia, ib);
+  ce(tc, td, Dc, Dd, ic, id);
+  ce(ta, tc, Da, Dc, ia, ic);
+  ce(tb, td, Db, Dd, ib, id);
+  ce(tb, tc, Db, Dc, ib, ic);
+  // the two smallest corners must share a face (the canonical y0 face); at a
+  // rounding-level tie they can come out diagonal: then the third-smallest
+  // corner (a neighbour of the smallest) takes the second place.
+  if ((ia ^ ib) == 2) {
+    const double t = tb; tb = tc; tc = t;
+    const int i = ib; ib = ic; ic = i;
   }
-  const bool lo_a = la <= lb;
-  w.T1 = lo_a ? la : lb;
-  w.T2 = lo_a ? lb : la;
-  const double Dap1 = lo_a ? Dla : Dlb;
-  w.Ta_x = lo_a ? xla : xlb;
-  w.Ta_y = lo_a ? yla : ylb;
-  const bool hi_a = ha >= hb;
-  w.T4 = hi_a ? ha : hb;
-  w.T3 = hi_a ? hb : ha;
-  const double Dap4 = hi_a ? Dha : Dhb;
-  w.Tb_x = hi_a ? xha : xhb;
-  w.Tb_y = hi_a ? yha : yhb;
-  if (w.T3 < w.T2) {  // rounding-level inconsistency at degenerate alignments
-    const double m = 0.5 * (w.T2 + w.T3);
-    w.T2 = m;
-    w.T3 = m;
-  }
-  w.K1 = Dap1 * Dap1 * g.inv_2ab;
-  w.K4 = Dap4 * Dap4 * g.inv_2ab;
-  w.band_vertical = (k & 1) == 0;
-  w.band_k = w.band_vertical ? fabs(s * C - 0.5 * (x0 + x1)) * g.inv_b
-                             : fabs(s * S - 0.5 * (y0 + y1)) * g.inv_a;
+  w.T1 = ta;
+  w.T2 = tb;
+  w.T3 = tc;
+  w.T4 = td;
+  w.K1 = Da * Da * g.inv_2ab;
+  w.K4 = Dd * Dd * g.inv_2ab;
+  // low face: horizontal iff its corners share y (indices {0,1} or {2,3})
+  const bool horiz = (ia >> 1) == (ib >> 1);
+  w.band_vertical = horiz;
+  w.low_face = horiz ? ((ia >> 1) == 0 ? 0 : 2) : ((ia == 1 || ia == 2) ? 1 : 3);
+  w.Ta_x = (ia == 1 || ia == 2) ? x1 : x0;
+  w.Ta_y = (ia >= 2) ? y1 : y0;
+  w.Tb_x = (id == 1 || id == 2) ? x1 : x0;
+  w.Tb_y = (id >= 2) ? y1 : y0;
+  w.band_k = horiz ? fabs(s * C - 0.5 * (x0 + x1)) * g.inv_b
+                   : fabs(s * S - 0.5 * (y0 + y1)) * g.inv_a;
   return true;
 }
 
@@ -262,8 +259,7 @@ __device__ __forceinline__ bool pixel_weights(const DevGeom& g, double C, double
   int cell = (int)(e_lo - 1);
 #pragma unroll 2
   for (long long e = e_lo; e <= e_hi; ++e, ++cell) {
-    const double te = fmin(fmax(e * inv_scale, T1), T4);
-    const double cur = CA(te);
+    const double cur = CA(e * inv_scale);  // CA clamps outside [T1, T4]
     const double wv = cur - prev;
     prev = cur;
     if (wv > kEpsWeight && cell >= cell_lo && cell <= cell_hi) emit(cell, wv);

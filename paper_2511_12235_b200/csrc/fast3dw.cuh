@@ -15,6 +15,8 @@
 //    into shared memory; per voxel an atom costs three subtractions, the flag
 //    tests and a cubic.
 #pragma once
+#include <climits>
+
 #include "common.cuh"
 #include "fast2d.cuh"
 
@@ -297,6 +299,78 @@ __device__ __forceinline__ void voxel_weights(const DevGeom& g, const ColumnHead
       const double v = prev - next;
       if (v > kEpsWeight) emit(cell, L, v);
       prev = next;
+    }
+  }
+}
+
+// Weights of voxels [z0, z1) of a planned column, cell group by cell group,
+// with the z-face sharing of the reference's composition made explicit: the
+// top face of voxel iz is the bottom face of voxel iz+1, so the atom sums
+// F(L, zt) computed for voxel iz are exactly F(L, zb) of voxel iz+1 and are
+// reused (up to 4 row edges cached). emit(iz, cell, row, w).
+template <typename Emit>
+__device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead& H,
+                                              const PieceCoef* P, int z0, int z1, Emit&& emit) {
+  const int row_lo = -g.n_det_z / 2, row_hi = g.n_det_z / 2 - 1;
+  const double dz_sdd = g.dz_sdd, sdd_dz = g.sdd_dz;
+  const double c_mn = sdd_dz * H.dmin_inv, c_mx = sdd_dz * H.dmax_inv;
+  for (int q = 0; q < H.ng; ++q) {
+    const double w2d = H.gw2d[q];
+    const int cell = H.gcell[q];
+    // cache of F(L, z) at the current voxel's bottom face (signed L key)
+    int cL0 = INT_MIN, cL1 = INT_MIN, cL2 = INT_MIN, cL3 = INT_MIN;
+    double cF0 = 0.0, cF1 = 0.0, cF2 = 0.0, cF3 = 0.0;
+    for (int iz = z0; iz < z1; ++iz) {
+      const double zb = (iz - g.n_z / 2.0) * g.c, zt = zb + g.c;
+      const double mb1 = zb * c_mn, mb2 = zb * c_mx, mt1 = zt * c_mn, mt2 = zt * c_mx;
+      const double m_min = fmin(fmin(mb1, mb2), fmin(mt1, mt2));
+      const double m_max = fmax(fmax(mb1, mb2), fmax(mt1, mt2));
+      const int fl = (int)floor(m_min);
+      const int k_lo = (fl < row_lo) ? row_lo : fl;
+      const int chi = (int)ceil(m_max) - 1;
+      const int k_hi = (chi < row_hi) ? chi : row_hi;
+      int nL0 = INT_MIN, nL1 = INT_MIN, nL2 = INT_MIN, nL3 = INT_MIN;
+      double nF0 = 0.0, nF1 = 0.0, nF2 = 0.0, nF3 = 0.0;
+      int nn = 0;
+      auto above = [&](int L) -> double {
+        const double kk = (double)L;
+        if (kk <= m_min) return w2d;
+        if (kk >= m_max) return 0.0;
+        if (L == 0) {
+          if (zb >= 0.0) return w2d;
+          if (zt <= 0.0) return 0.0;
+          return w2d * zt / (zt - zb);
+        }
+        const double tan_a = fabs(kk) * dz_sdd;
+        const double zt_s = L > 0 ? zt : -zt, zb_s = L > 0 ? zb : -zb;
+        double Fb;
+        if (L == cL0) Fb = cF0;
+        else if (L == cL1) Fb = cF1;
+        else if (L == cL2) Fb = cF2;
+        else if (L == cL3) Fb = cF3;
+        else Fb = atom_sum3(H, P, q, tan_a, zb_s);
+        const double Ft = atom_sum3(H, P, q, tan_a, zt_s);
+        switch (nn) {
+          case 0: nL0 = L; nF0 = Ft; break;
+          case 1: nL1 = L; nF1 = Ft; break;
+          case 2: nL2 = L; nF2 = Ft; break;
+          case 3: nL3 = L; nF3 = Ft; break;
+          default: break;
+        }
+        ++nn;
+        return L > 0 ? Ft - Fb : w2d - (Fb - Ft);
+      };
+      if (k_hi >= k_lo) {
+        double prev = above(k_lo);
+        for (int L = k_lo; L <= k_hi; ++L) {
+          const double next = above(L + 1);
+          const double v = prev - next;
+          if (v > kEpsWeight) emit(iz, cell, L, v);
+          prev = next;
+        }
+      }
+      cL0 = nL0; cL1 = nL1; cL2 = nL2; cL3 = nL3;
+      cF0 = nF0; cF1 = nF1; cF2 = nF2; cF3 = nF3;
     }
   }
 }

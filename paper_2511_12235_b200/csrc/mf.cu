@@ -118,7 +118,7 @@ constexpr int kWarps3 = 4;
 constexpr int kZcMax = 16;  // voxels per lane per z-block (z-block = 512 voxels)
 
 template <typename T, bool kFwd>
-__global__ void __launch_bounds__(kWarps3 * 32) proj3d_kernel(
+__global__ void __launch_bounds__(kWarps3 * 32, 2) proj3d_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, int angle_begin, int angle_step, int n_sel,
     const T* __restrict__ in, T* __restrict__ xout, unsigned long long* __restrict__ yacc,
     double scale, unsigned long long* n_upd, int* status) {
@@ -149,24 +149,20 @@ __global__ void __launch_bounds__(kWarps3 * 32) proj3d_kernel(
       if (!ok) continue;
       const fast::ColumnHead& H = sh[warp];
       const fast::PieceCoef* P = sp[warp];
-      for (int iz = z0; iz < z1; ++iz) {
-        if (kFwd) {
+      if (kFwd) {
+        unsigned long long* yb = yacc + (long long)ip * rpa;
+        fast::chunk_weights(g, H, P, z0, z1, [&](int iz, int my, int mz, double w) {
+          ++cnt;
           const double xs = ld(&in[iz * plane + col]) * scale;
-          unsigned long long* yb = yacc + (long long)ip * rpa;
-          fast::voxel_weights(g, H, P, iz, [&](int my, int mz, double w) {
-            ++cnt;
-            if (xs != 0.0)
-              atomicAdd(&yb[(long long)(mz + hz) * g.n_det_y + (my + hy)],
-                        (unsigned long long)__double2ll_rn(w * xs));
-          });
-        } else {
-          const T* yb = in + (long long)ip * rpa;
-          double v = 0.0;
-          fast::voxel_weights(g, H, P, iz, [&](int my, int mz, double w) {
-            v += w * ld(&yb[(long long)(mz + hz) * g.n_det_y + (my + hy)]);
-          });
-          sacc[warp][iz - z0][lane] += v;
-        }
+          if (xs != 0.0)
+            atomicAdd(&yb[(long long)(mz + hz) * g.n_det_y + (my + hy)],
+                      (unsigned long long)__double2ll_rn(w * xs));
+        });
+      } else {
+        const T* yb = in + (long long)ip * rpa;
+        fast::chunk_weights(g, H, P, z0, z1, [&](int iz, int my, int mz, double w) {
+          sacc[warp][iz - z0][lane] += w * ld(&yb[(long long)(mz + hz) * g.n_det_y + (my + hy)]);
+        });
       }
     }
     if (!kFwd)
