@@ -42,9 +42,14 @@ __device__ __forceinline__ void count_updates(unsigned long long* n_upd, unsigne
 // 2D pixel tile per block: 16 x 8 pixels, 128 threads.
 constexpr int kTx = 16, kTy = 8;
 
+// Forward 2D: block = 16x8 pixel tile x a chunk of kFwdAngles angles; each
+// thread loops over its chunk's angles (x and the per-angle cos/sin are loaded
+// once per thread / prefetched, amortising the load latency).
+constexpr int kFwdAngles = 4;
+
 template <typename T>
 __global__ void __launch_bounds__(128) fwd2d_kernel(DevGeom g, const AngleCS* __restrict__ cs,
-                                                    int angle_begin, int angle_step,
+                                                    int angle_begin, int angle_step, int n_sel,
                                                     const T* __restrict__ x,
                                                     unsigned long long* __restrict__ yacc,
                                                     double scale, unsigned long long* n_upd,
@@ -54,16 +59,20 @@ __global__ void __launch_bounds__(128) fwd2d_kernel(DevGeom g, const AngleCS* __
   const int iy = (blockIdx.x / tiles_x) * kTy + (threadIdx.x / kTx);
   unsigned cnt = 0;
   if (ix < g.n_x && iy < g.n_y) {
-    const double xv = ld(&x[(long long)iy * g.n_x + ix]);
-    const int k = blockIdx.y;
-    const int ip = angle_begin + k * angle_step;
-    const AngleCS a = cs[k];
-    unsigned long long* yrow = yacc + (long long)ip * g.rows_per_angle + g.n_det_y / 2;
-    const double xs = xv * scale;
-    fast::pixel_weights(g, a.C, a.S, ix, iy, status, [&](int m, double w) {
-      ++cnt;
-      if (xs != 0.0) atomicAdd(&yrow[m], (unsigned long long)__double2ll_rn(w * xs));
-    });
+    const double xs = ld(&x[(long long)iy * g.n_x + ix]) * scale;
+    const int k0 = blockIdx.y * kFwdAngles;
+    const int k1 = min(k0 + kFwdAngles, n_sel);
+    AngleCS a = cs[k0];
+    for (int k = k0; k < k1; ++k) {
+      const AngleCS an = cs[min(k + 1, n_sel - 1)];  // prefetch
+      const int ip = angle_begin + k * angle_step;
+      unsigned long long* yrow = yacc + (long long)ip * g.rows_per_angle + g.n_det_y / 2;
+      fast::pixel_weights(g, a.C, a.S, ix, iy, status, [&](int m, double w) {
+        ++cnt;
+        if (xs != 0.0) atomicAdd(&yrow[m], (unsigned long long)__double2ll_rn(w * xs));
+      });
+      a = an;
+    }
   }
   count_updates(n_upd, cnt);
 }
@@ -280,13 +289,13 @@ cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_beg
                    double scale, unsigned long long* n_upd, int* status, cudaStream_t st) {
   if (n_sel <= 0) return cudaSuccess;
   const bool two_d = (g.n_z == 1 && g.n_det_z == 1);
-  const dim3 grid = tile_grid(g, (unsigned)n_sel);
   if (two_d) {
+    const dim3 grid = tile_grid(g, (unsigned)((n_sel + kFwdAngles - 1) / kFwdAngles));
     if (dtype == CTSM_F64)
-      fwd2d_kernel<double><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step,
+      fwd2d_kernel<double><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step, n_sel,
                                                  (const double*)x, yacc, scale, n_upd, status);
     else
-      fwd2d_kernel<float><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step,
+      fwd2d_kernel<float><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step, n_sel,
                                                 (const float*)x, yacc, scale, n_upd, status);
   } else {
     const long long nxy = (long long)g.n_x * g.n_y;
