@@ -49,7 +49,7 @@ def parse():
     p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     p.add_argument("--no-clocks", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--mode", default="proj", choices=["proj", "sirt"],
+    p.add_argument("--mode", default="proj", choices=["proj", "sirt", "csr"],
                    help="proj: one A x + A^T y per step; sirt: one SIRT iteration per step "
                         "(BASELINE configs[4]: y = A x_true + 1%% noise)")
     return p.parse_args()
@@ -482,12 +482,80 @@ def run_sirt(args):
         dist.destroy_process_group()
 
 
+def run_csr(args):
+    """K1/K2 consistent CSR assembly (bit-exact path) + K3 SpMV on one GPU.
+    One step = build_system_matrix (count, scan, fill, per-row sort) of the
+    whole config; metric SM weights/s = nnz / build time. K3 A x on the built
+    matrix is timed separately (HBM roofline: 12 B/nnz + 16 B/row)."""
+    import torch
+
+    from paper_2511_12235_b200 import CONFIGS, _lib
+    from paper_2511_12235_b200.phantoms import phantom_for
+    from paper_2511_12235_b200.projector import build_system_matrix, forward_project
+
+    cfg = args.config
+    g = CONFIGS[cfg]
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(0)
+    budget = 1 << 40
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w = None
+    for _ in range(args.warmup):
+        w = build_system_matrix(g, memory_budget_bytes=budget)
+        del w
+        torch.cuda.synchronize()
+    clocks = ClockSampler(0, not args.no_clocks)
+    launches0 = _lib.launch_count()
+    ms = 0.0
+    for _ in range(args.steps):
+        w = None
+        torch.cuda.synchronize()
+        ev0.record()
+        w = build_system_matrix(g, memory_budget_bytes=budget)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms += ev0.elapsed_time(ev1)
+    launches = _lib.launch_count() - launches0
+    ms /= args.steps
+    nnz = w.nnz()
+    x = torch.from_numpy(phantom_for(cfg, g, dtype=np.float64 if g.is_2d() else np.float32)).double().to(dev)
+    for _ in range(3):
+        forward_project(w, x)
+    torch.cuda.synchronize()
+    ms_spmv = 0.0
+    for _ in range(5):
+        ev0.record()
+        forward_project(w, x)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms_spmv += ev0.elapsed_time(ev1) / 5
+    clk = clocks.stop()
+    bytes_spmv = 12.0 * nnz + 16.0 * w.n_rows + 8.0 * w.n_cols
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    gbs = bytes_spmv / (ms_spmv * 1e-3) / 1e9
+    line = {
+        "metric": "SM weights/s (consistent CSR assembly)", "value": nnz / (ms * 1e-3),
+        "unit": "weights/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg}: BASELINE.json configs[{cfg[1]}] build_system_matrix"},
+        "nnz": nnz, "nnz_reference": NNZ.get(cfg),
+        "spmv": {"ms": ms_spmv, "GB/s": gbs, "algorithmic_bytes": bytes_spmv,
+                 "hbm_peak_gbs": peaks.get("hbm_gbs"), "frac": gbs / peaks.get("hbm_gbs", 6650.0)},
+        "gpu_launches": int(launches), "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
     elif args.mode == "sirt":
         run_sirt(args)
+    elif args.mode == "csr":
+        run_csr(args)
     else:
         run_ours(args)
 
