@@ -25,14 +25,25 @@ namespace fast {
 
 constexpr int kMaxPieces = 12;  // pieces of one column sweep inside the detector
 
-// G-independent coefficients of one sweep piece (16 doubles).
+// G-independent coefficients of one sweep piece (24 doubles).
 //  kind 0/2 (corner triangle, atoms at the two endpoints lo/hi):
-//    c[0..6]  = lo: th_g, th_gg, th_h, crg, delta, srh_C, t
-//    c[7..13] = hi: same
+//    c[0..6]   = lo: th_g, th_gg, th_h, crg, delta, srh_C, t
+//    c[7..13]  = hi: same
+//    c[14..17] = lo: th_min, th_max, slope, root   (linear / zero short cuts)
+//    c[18..21] = hi: same
 //  kind 1 (trapezoid band between t1 = lo and t2 = hi):
-//    c[0..12] = th_g1, th_g2, th_f1, th_f2, cr1, cr2, d12, A2g, A3g, A2f, A3f, Pg, Pf
+//    c[0..12]  = th_g1, th_g2, th_f1, th_f2, cr1, cr2, d12, A2g, A3g, A2f, A3f, Pg, Pf
+//    c[14..17] = th_min, th_max, slope, root
+// An atom's flags test the row-edge plane against zref at the vertices of the
+// atom's 2D region (weights3d.cpp:72-75, 123-125). With every flag set the
+// plane lies below zref over the whole region and the atom is exactly linear:
+// atom = Area (zref - tan_a D_centroid) / (a b c), i.e. tt = slope (G - root)
+// with slope = 6 Area / a^2, root = D_centroid / a; with no flag set it is 0.
+// Only mixed flags need the reference's cubic forms.
+constexpr int kCoef = 24;
+constexpr int kLin = 14;
 struct PieceCoef {
-  double c[16];
+  double c[kCoef];
 };
 
 struct ColumnHead {
@@ -215,11 +226,33 @@ __device__ __forceinline__ bool plan_column(const DevGeom& g, double C, double S
       c[10] = Pf * Pf * Pf * (cr1 + cr2) * i12 * i12;
       c[11] = Pg;
       c[12] = Pf;
+      // band quadrilateral between the rays t1, t2 and the faces x = fx0, fx1
+      // (canonical frame): y_t(X) = (t (s - X Cp) + X Sp) / (Cp + t Sp);
+      // Simpson over X is exact for the (quadratic) depth moment.
+      auto seg = [&](double X, double& len, double& dmid) {
+        const double ya = (t1 * (s - X * Cp) + X * Sp) * i1;
+        const double yb = (t2 * (s - X * Cp) + X * Sp) * i2;
+        len = fabs(yb - ya);
+        dmid = s - X * Cp - 0.5 * (ya + yb) * Sp;
+      };
+      double l0, d0, lm, dm, l1, d1;
+      seg(fx0, l0, d0);
+      seg(0.5 * (fx0 + fx1), lm, dm);
+      seg(fx1, l1, d1);
+      const double area = ca * (l0 + 4.0 * lm + l1) / 6.0;
+      const double mom = ca * (l0 * d0 + 4.0 * lm * dm + l1 * d1) / 6.0;
+      double* l = c + kLin;
+      l[0] = fmin(fmin(c[0], c[1]), fmin(c[2], c[3]));
+      l[1] = fmax(fmax(c[0], c[1]), fmax(c[2], c[3]));
+      l[2] = 6.0 * area / (ca * ca);
+      l[3] = area > 0.0 ? mom / area / ca : 0.0;
     } else {
       // tri_flags_at / tri_atom_flags (weights3d.cpp:115-168) at both ends
       const double xa = my_kind == 0 ? ax1 : ax4, ya = my_kind == 0 ? ay1 : ay4;
       const double Pq = (s * Cp - xa) / ca, Qq = (s * Sp - ya) / ca;
       const double thgg = Pq * Cp + Qq * Sp;
+      const double Da = s - xa * Cp - ya * Sp;       // apex depth (= a' thgg)
+      const double ta = my_kind == 0 ? sw.T1 : sw.T4;  // apex ray parameter
       for (int e = 0; e < 2; ++e) {
         const double t = e == 0 ? my_lo : my_hi;
         const double crg = Cp + Sp * t, srh = Sp - Cp * t;
@@ -231,10 +264,37 @@ __device__ __forceinline__ bool plan_column(const DevGeom& g, double C, double S
         q[4] = Qq - Pq * srh / crg;
         q[5] = srh / Cp;
         q[6] = t;
+        // corner triangle between the apex ray and ray t (canonical frame):
+        // legs dx = Da (t - ta) / (t Cp - Sp), dy = Da (t - ta) / (Cp + t Sp)
+        const double k = Da * (t - ta);
+        const double dx = k / (t * Cp - Sp), dy = k / crg;
+        const double area = 0.5 * fabs(dx * dy);
+        const double dcen = Da - (dx * Cp + dy * Sp) / 3.0;
+        double* l = c + kLin + 4 * e;
+        l[0] = fmin(fmin(q[0], q[1]), q[2]);
+        l[1] = fmax(fmax(q[0], q[1]), q[2]);
+        l[2] = 6.0 * area / (ca * ca);
+        l[3] = dcen / ca;
       }
     }
   }
   return true;
+}
+
+// |tt| of a triangle atom with the linear / zero short cuts (q: the 7 cubic
+// coefficients, l: th_min, th_max, slope, root).
+__device__ __forceinline__ double tri_abs(const ColumnHead& H, const double* q, const double* l,
+                                          double G) {
+  if (G <= l[0]) return 0.0;
+  if (G > l[1]) return l[2] * (G - l[3]);
+  return fabs(tri_tt(H, q, G));
+}
+
+__device__ __forceinline__ double trap_abs(const ColumnHead& H, const double* c, double G) {
+  const double* l = c + kLin;
+  if (G <= l[0]) return 0.0;
+  if (G > l[1]) return l[2] * (G - l[3]);
+  return fabs(trap_tt(H, c, G));
 }
 
 // atom_sum (weights3d.cpp:400-423) over the pieces of cell group q at height
@@ -247,9 +307,9 @@ __device__ __forceinline__ double atom_sum3(const ColumnHead& H, const PieceCoef
     const double* c = P[k].c;
     double tt;
     switch (H.pkind[k]) {
-      case 0: tt = fabs(tri_tt(H, c + 7, G)) - fabs(tri_tt(H, c, G)); break;
-      case 1: tt = fabs(trap_tt(H, c, G)); break;
-      default: tt = fabs(tri_tt(H, c, G)) - fabs(tri_tt(H, c + 7, G)); break;
+      case 0: tt = tri_abs(H, c + 7, c + kLin + 4, G) - tri_abs(H, c, c + kLin, G); break;
+      case 1: tt = trap_abs(H, c, G); break;
+      default: tt = tri_abs(H, c, c + kLin, G) - tri_abs(H, c + 7, c + kLin + 4, G); break;
     }
     v += tt;
   }

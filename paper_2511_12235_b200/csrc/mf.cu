@@ -48,7 +48,7 @@ constexpr int kTx = 16, kTy = 8;
 constexpr int kFwdAngles = 4;
 
 template <typename T>
-__global__ void __launch_bounds__(128) fwd2d_kernel(DevGeom g, const AngleCS* __restrict__ cs,
+__global__ void __launch_bounds__(128, 8) fwd2d_kernel(DevGeom g, const AngleCS* __restrict__ cs,
                                                     int angle_begin, int angle_step, int n_sel,
                                                     const T* __restrict__ x,
                                                     unsigned long long* __restrict__ yacc,
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(128) fwd2d_kernel(DevGeom g, const AngleCS* __
 // writes its partial sum to part[chunk][pixel] and bwd_reduce adds the chunks
 // in fixed order (deterministic); with one chunk x is written directly.
 template <typename T>
-__global__ void __launch_bounds__(128) bwd2d_kernel(DevGeom g, const AngleCS* __restrict__ cs,
+__global__ void __launch_bounds__(128, 8) bwd2d_kernel(DevGeom g, const AngleCS* __restrict__ cs,
                                                     int angle_begin, int angle_step, int n_sel,
                                                     int chunk, const T* __restrict__ y,
                                                     T* __restrict__ x, double* __restrict__ part,
