@@ -597,11 +597,15 @@ long ref_voxel_volume_factors(const o_geom* g, int ix, int iy, int iz, double ph
 /* ---- angle blocks (projector.cpp:44-84) ---------------------------------- */
 typedef void (*emit_fn)(void* ctx, uint32_t row, uint32_t col, double w);
 
-static void angle_block_entries(const o_geom* g, int ip, emit_fn emit, void* ctx) {
+/* Entries of the voxels with slow index (iz in 3D, iy in 2D) in [lo, hi), in
+ * the reference's emission order; the full block is [0, n). Splitting a block
+ * into slabs only parallelises the oracle; it does not change any weight. */
+static void angle_block_entries_slab(const o_geom* g, int ip, int lo, int hi, emit_fn emit,
+                                     void* ctx) {
   const double phi = g_angle(g, ip);
   weight buf[MAX_W];
   if (is_2d(g)) {
-    for (int iy = 0; iy < g->n_y; ++iy)
+    for (int iy = lo; iy < hi; ++iy)
       for (int ix = 0; ix < g->n_x; ++ix) {
         const uint32_t col = (uint32_t)((uint64_t)iy * g->n_x + ix);
         const int n = pixel_area_factors(ix, iy, phi, g, buf);
@@ -610,7 +614,7 @@ static void angle_block_entries(const o_geom* g, int ip, emit_fn emit, void* ctx
                col, buf[k].w);
       }
   } else {
-    for (int iz = 0; iz < g->n_z; ++iz)
+    for (int iz = lo; iz < hi; ++iz)
       for (int iy = 0; iy < g->n_y; ++iy)
         for (int ix = 0; ix < g->n_x; ++ix) {
           const uint32_t col = (uint32_t)(((uint64_t)iz * g->n_y + iy) * g->n_x + ix);
@@ -622,6 +626,12 @@ static void angle_block_entries(const o_geom* g, int ip, emit_fn emit, void* ctx
                  col, buf[k].w);
         }
   }
+}
+
+static int slab_extent(const o_geom* g) { return is_2d(g) ? g->n_y : g->n_z; }
+
+static void angle_block_entries(const o_geom* g, int ip, emit_fn emit, void* ctx) {
+  angle_block_entries_slab(g, ip, 0, slab_extent(g), emit, ctx);
 }
 
 typedef struct {
@@ -744,6 +754,50 @@ static int run_tasks(task* t) {
     return -(t->err_code + 1);
   }
   return 0;
+}
+
+/* angle_block_entries split into slabs on threads; the slab entry lists are
+ * concatenated in slab order, so the result is identical (same entries, same
+ * emission order) to the sequential reference loop. */
+typedef struct {
+  int ip, n_parts;
+  entry_vec* parts;
+} blockpar_user;
+static void blockpar_task(task* t, int item, int worker) {
+  (void)worker;
+  blockpar_user* u = (blockpar_user*)t->user;
+  const int n = slab_extent(t->g);
+  const int lo = (int)((int64_t)n * item / u->n_parts), hi = (int)((int64_t)n * (item + 1) / u->n_parts);
+  angle_block_entries_slab(t->g, u->ip, lo, hi, vec_emit, &u->parts[item]);
+}
+
+long ref_angle_block_entries_par(const o_geom* g, int ip, uint32_t* row, uint32_t* col, double* w,
+                                 long cap, int threads) {
+  O_TRY(validate(g););
+  int n_parts = threads < 1 ? 1 : threads;
+  if (n_parts > slab_extent(g)) n_parts = slab_extent(g);
+  entry_vec* parts = (entry_vec*)calloc(n_parts, sizeof(entry_vec));
+  blockpar_user u = {ip, n_parts, parts};
+  task t;
+  memset(&t, 0, sizeof t);
+  t.fn = blockpar_task;
+  t.g = g;
+  t.count = n_parts;
+  t.threads = threads;
+  t.user = &u;
+  const int st = run_tasks(&t);
+  long n = 0;
+  if (st == 0)
+    for (int p = 0; p < n_parts; ++p)
+      for (long k = 0; k < parts[p].n; ++k, ++n)
+        if (n < cap) {
+          row[n] = parts[p].row[k];
+          col[n] = parts[p].col[k];
+          w[n] = parts[p].w[k];
+        }
+  for (int p = 0; p < n_parts; ++p) vec_free(&parts[p]);
+  free(parts);
+  return st != 0 ? st : n;
 }
 
 /* ---- build_system_matrix (projector.cpp:144-201) -------------------------- */
@@ -916,10 +970,13 @@ int ref_back_project(void* h, const double* y, double* x) {
 }
 
 /* ---- matrix-free A x (projector.cpp:235-260) ----------------------------- */
+/* Work items are (angle, slab) pairs; with fewer angles than threads each
+ * angle is split into slabs whose partial blocks are summed in slab order. */
 typedef struct {
   const int32_t* angles;
   const double* x;
-  double* y_sel;
+  double* parts; /* n_sel * n_parts blocks of rpa */
+  int n_parts;
   uint64_t rpa;
 } fwd_user;
 typedef struct {
@@ -933,24 +990,59 @@ static void fwd_emit(void* ctx, uint32_t r, uint32_t c, double w) {
 static void fwd_task(task* t, int item, int worker) {
   (void)worker;
   fwd_user* u = (fwd_user*)t->user;
-  double* block = u->y_sel + (uint64_t)item * u->rpa;
+  const int k = item / u->n_parts, part = item % u->n_parts;
+  const int n = slab_extent(t->g);
+  const int lo = (int)((int64_t)n * part / u->n_parts), hi = (int)((int64_t)n * (part + 1) / u->n_parts);
+  double* block = u->parts + (uint64_t)item * u->rpa;
   memset(block, 0, u->rpa * sizeof(double));
   fwd_ctx c = {block, u->x};
-  angle_block_entries(t->g, u->angles[item], fwd_emit, &c);
+  angle_block_entries_slab(t->g, u->angles[k], lo, hi, fwd_emit, &c);
 }
 
-int ref_forward_mf_angles(const o_geom* g, const int32_t* angles, int n_sel, const double* x,
-                          double* y_sel, int threads) {
+static int forward_mf_angles_impl(const o_geom* g, const int32_t* angles, int n_sel,
+                                  const double* x, double* y_sel, int threads, int split) {
   O_TRY(validate(g););
-  fwd_user u = {angles, x, y_sel, (uint64_t)g->n_det_y * g->n_det_z};
+  const uint64_t rpa = (uint64_t)g->n_det_y * g->n_det_z;
+  int n_parts = 1;
+  if (split && n_sel > 0 && n_sel < threads) n_parts = (threads + n_sel - 1) / n_sel;
+  if (n_parts > slab_extent(g)) n_parts = slab_extent(g);
+  double* parts = y_sel;
+  if (n_parts > 1) parts = (double*)malloc((uint64_t)n_sel * n_parts * rpa * sizeof(double));
+  fwd_user u = {angles, x, parts, n_parts, rpa};
   task t;
   memset(&t, 0, sizeof t);
   t.fn = fwd_task;
   t.g = g;
-  t.count = n_sel;
+  t.count = n_sel * n_parts;
   t.threads = threads;
   t.user = &u;
-  return run_tasks(&t);
+  const int st = run_tasks(&t);
+  if (n_parts > 1) {
+    if (st == 0)
+      for (int k = 0; k < n_sel; ++k) {
+        double* out = y_sel + (uint64_t)k * rpa;
+        memset(out, 0, rpa * sizeof(double));
+        for (int p = 0; p < n_parts; ++p) {
+          const double* b = parts + ((uint64_t)k * n_parts + p) * rpa;
+          for (uint64_t r = 0; r < rpa; ++r) out[r] += b[r];
+        }
+      }
+    free(parts);
+  }
+  return st;
+}
+
+/* Reference order (bit-exact with forward_project_matrix_free's per-angle
+ * accumulation). */
+int ref_forward_mf_angles(const o_geom* g, const int32_t* angles, int n_sel, const double* x,
+                          double* y_sel, int threads) {
+  return forward_mf_angles_impl(g, angles, n_sel, x, y_sel, threads, 0);
+}
+/* Same values up to summation order; angles split into slabs so that a few
+ * large angle blocks use all threads (tolerance checks at C3/C4 scale). */
+int ref_forward_mf_angles_par(const o_geom* g, const int32_t* angles, int n_sel, const double* x,
+                              double* y_sel, int threads) {
+  return forward_mf_angles_impl(g, angles, n_sel, x, y_sel, threads, 1);
 }
 
 int ref_forward_project_matrix_free(const o_geom* g, const double* x, double* y, int threads) {
@@ -962,11 +1054,13 @@ int ref_forward_project_matrix_free(const o_geom* g, const double* x, double* y,
 }
 
 /* ---- matrix-free A^T y restatement --------------------------- */
+/* Per-angle partial volumes, summed in angle order; with fewer angles than
+ * threads each angle's block is also split into slabs (disjoint voxels). */
 typedef struct {
   const int32_t* angles;
   const double* y;
   double** part; /* per chunk slot */
-  int base;
+  int base, n_parts;
   uint64_t rpa, nv;
 } bwd_user;
 typedef struct {
@@ -980,30 +1074,38 @@ static void bwd_emit(void* ctx, uint32_t r, uint32_t c, double w) {
 static void bwd_task(task* t, int item, int worker) {
   (void)worker;
   bwd_user* u = (bwd_user*)t->user;
-  double* p = u->part[item];
-  memset(p, 0, u->nv * sizeof(double));
-  const int ang = u->angles[u->base + item];
+  const int k = item / u->n_parts, part = item % u->n_parts;
+  const int n = slab_extent(t->g);
+  const int lo = (int)((int64_t)n * part / u->n_parts), hi = (int)((int64_t)n * (part + 1) / u->n_parts);
+  const uint64_t plane = t->g->n_z > 1 || t->g->n_det_z > 1 ? (uint64_t)t->g->n_x * t->g->n_y
+                                                              : (uint64_t)t->g->n_x;
+  double* p = u->part[k];
+  memset(p + (uint64_t)lo * plane, 0, (uint64_t)(hi - lo) * plane * sizeof(double));
+  const int ang = u->angles[u->base + k];
   bwd_ctx c = {p, u->y + (uint64_t)ang * u->rpa};
-  angle_block_entries(t->g, ang, bwd_emit, &c);
+  angle_block_entries_slab(t->g, ang, lo, hi, bwd_emit, &c);
 }
 
-int ref_back_mf_angles(const o_geom* g, const int32_t* angles, int n_sel, const double* y,
-                       double* x, int threads) {
+static int back_mf_angles_impl(const o_geom* g, const int32_t* angles, int n_sel,
+                               const double* y, double* x, int threads, int split) {
   O_TRY(validate(g););
   const uint64_t nv = (uint64_t)g->n_x * g->n_y * g->n_z;
-  const int chunk = threads < 1 ? 1 : threads;
-  double** part = (double**)malloc(sizeof(double*) * chunk);
+  int n_parts = 1;
+  if (split && n_sel > 0 && n_sel < threads) n_parts = (threads + n_sel - 1) / n_sel;
+  if (n_parts > slab_extent(g)) n_parts = slab_extent(g);
+  const int chunk = n_parts > 1 ? n_sel : (threads < 1 ? 1 : threads);
+  double** part = (double**)malloc(sizeof(double*) * (chunk > 0 ? chunk : 1));
   for (int i = 0; i < chunk; ++i) part[i] = (double*)malloc(nv * sizeof(double));
   memset(x, 0, nv * sizeof(double));
   int st = 0;
   for (int k0 = 0; k0 < n_sel && st == 0; k0 += chunk) {
     const int n = (n_sel - k0) < chunk ? (n_sel - k0) : chunk;
-    bwd_user u = {angles, y, part, k0, (uint64_t)g->n_det_y * g->n_det_z, nv};
+    bwd_user u = {angles, y, part, k0, n_parts, (uint64_t)g->n_det_y * g->n_det_z, nv};
     task t;
     memset(&t, 0, sizeof t);
     t.fn = bwd_task;
     t.g = g;
-    t.count = n;
+    t.count = n * n_parts;
     t.threads = threads;
     t.user = &u;
     st = run_tasks(&t);
@@ -1014,6 +1116,15 @@ int ref_back_mf_angles(const o_geom* g, const int32_t* angles, int n_sel, const 
   for (int i = 0; i < chunk; ++i) free(part[i]);
   free(part);
   return st;
+}
+
+int ref_back_mf_angles(const o_geom* g, const int32_t* angles, int n_sel, const double* y,
+                       double* x, int threads) {
+  return back_mf_angles_impl(g, angles, n_sel, y, x, threads, 0);
+}
+int ref_back_mf_angles_par(const o_geom* g, const int32_t* angles, int n_sel, const double* y,
+                           double* x, int threads) {
+  return back_mf_angles_impl(g, angles, n_sel, y, x, threads, 1);
 }
 
 int ref_back_project_matrix_free(const o_geom* g, const double* y, double* x, int threads) {

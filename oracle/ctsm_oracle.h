@@ -48,6 +48,14 @@ int ref_forward_mf_angles(const o_geom* g, const int32_t* angles, int n_sel, con
 int ref_back_mf_angles(const o_geom* g, const int32_t* angles, int n_sel, const double* y,
                        double* x, int threads);
 int ref_back_project_matrix_free(const o_geom* g, const double* y, double* x, int threads);
+/* Restatement-only variants that also split each angle block into slabs (same
+ * values up to summation order) to use all threads on few large angles. */
+int ref_forward_mf_angles_par(const o_geom* g, const int32_t* angles, int n_sel, const double* x,
+                              double* y_sel, int threads);
+int ref_back_mf_angles_par(const o_geom* g, const int32_t* angles, int n_sel, const double* y,
+                           double* x, int threads);
+long ref_angle_block_entries_par(const o_geom* g, int ip, uint32_t* row, uint32_t* col, double* w,
+                                 long cap, int threads);
 int ref_sirt(const o_geom* g, const double* y, double* x, int iters, int threads);
 int ref_angle_column_sums(const o_geom* g, int ip, double* sums);
 

@@ -132,6 +132,13 @@ class Oracle:
         L.ref_forward_mf_angles.argtypes = [_P, _P, ctypes.c_int, _P, _P, ctypes.c_int]
         L.ref_back_mf_angles.argtypes = [_P, _P, ctypes.c_int, _P, _P, ctypes.c_int]
         L.ref_sirt.argtypes = [_P, _P, _P, ctypes.c_int, ctypes.c_int]
+        self.has_par = hasattr(L, "ref_forward_mf_angles_par")
+        if self.has_par:
+            L.ref_forward_mf_angles_par.argtypes = [_P, _P, ctypes.c_int, _P, _P, ctypes.c_int]
+            L.ref_back_mf_angles_par.argtypes = [_P, _P, ctypes.c_int, _P, _P, ctypes.c_int]
+            L.ref_angle_block_entries_par.argtypes = [_P, ctypes.c_int, _P, _P, _P, ctypes.c_long,
+                                                      ctypes.c_int]
+            L.ref_angle_block_entries_par.restype = ctypes.c_long
         L.ref_angle_column_sums.argtypes = [_P, ctypes.c_int, _P]
 
     # -- helpers -----------------------------------------------------------
@@ -171,9 +178,23 @@ class Oracle:
         self._check(n)
         return my[:n].copy(), mz[:n].copy(), w[:n].copy()
 
-    def angle_block_entries(self, g, ip: int):
-        """(row_raster u32, col u32, w f64) in emission order (projector.cpp:44-84)."""
+    def angle_block_entries(self, g, ip: int, threads: int = 1):
+        """(row_raster u32, col u32, w f64) in emission order (projector.cpp:44-84).
+        threads > 1 (restatement only) computes slabs in parallel; the result is
+        identical."""
         og, p = self._g(g)
+        if threads > 1 and self.has_par:
+            f = self.lib.ref_angle_block_entries_par
+            n = int(1.3 * 12 * g.n_x * g.n_y * g.n_z) + 1024
+            for _ in range(2):
+                row = np.empty(n, np.uint32)
+                col = np.empty(n, np.uint32)
+                w = np.empty(n, np.float64)
+                m = f(p, ip, _ptr(row), _ptr(col), _ptr(w), n, threads)
+                self._check(m)
+                if m <= n:
+                    return row[:m].copy(), col[:m].copy(), w[:m].copy()
+                n = m
         n = self.lib.ref_angle_block_entries(p, ip, None, None, None, 0)
         self._check(n)
         row = np.empty(n, np.uint32)
@@ -213,20 +234,27 @@ class Oracle:
         self._check(self.lib.ref_back_project_matrix_free(p, _ptr(y), _ptr(x), threads))
         return x
 
-    def forward_mf_angles(self, g, angles, x: np.ndarray, threads: int = 1) -> np.ndarray:
+    def forward_mf_angles(self, g, angles, x: np.ndarray, threads: int = 1,
+                          split: bool = False) -> np.ndarray:
+        """A x rows of the listed angles. split=True (restatement only) also
+        splits each angle into slabs to use all threads (same values up to
+        summation order)."""
         og, p = self._g(g)
         a = np.ascontiguousarray(angles, np.int32)
         x = np.ascontiguousarray(x, np.float64)
         y = np.zeros(a.size * g.n_det_y * g.n_det_z, np.float64)
-        self._check(self.lib.ref_forward_mf_angles(p, _ptr(a), a.size, _ptr(x), _ptr(y), threads))
+        f = self.lib.ref_forward_mf_angles_par if (split and self.has_par) else self.lib.ref_forward_mf_angles
+        self._check(f(p, _ptr(a), a.size, _ptr(x), _ptr(y), threads))
         return y
 
-    def back_mf_angles(self, g, angles, y: np.ndarray, threads: int = 1) -> np.ndarray:
+    def back_mf_angles(self, g, angles, y: np.ndarray, threads: int = 1,
+                       split: bool = False) -> np.ndarray:
         og, p = self._g(g)
         a = np.ascontiguousarray(angles, np.int32)
         y = np.ascontiguousarray(y, np.float64)
         x = np.zeros(g.n_x * g.n_y * g.n_z, np.float64)
-        self._check(self.lib.ref_back_mf_angles(p, _ptr(a), a.size, _ptr(y), _ptr(x), threads))
+        f = self.lib.ref_back_mf_angles_par if (split and self.has_par) else self.lib.ref_back_mf_angles
+        self._check(f(p, _ptr(a), a.size, _ptr(y), _ptr(x), threads))
         return x
 
     def sirt(self, g, y: np.ndarray, x0: np.ndarray, iters: int, threads: int = 1) -> np.ndarray:

@@ -135,3 +135,17 @@ def test_reference_error_codes_match():
         with pytest.raises(pyoracle.OracleError) as e:
             o.build_system_matrix(big, budget=1024)
         assert e.value.code == "OutOfMemory"
+
+
+def test_parallel_angle_block_is_identical():
+    """The slab-parallel oracle helpers reproduce the sequential emission."""
+    port = pyoracle.load("port_cr")
+    g = TEST_GEOMETRIES["cone3d"]
+    for ip in (0, 3):
+        a = port.angle_block_entries(g, ip)
+        b = port.angle_block_entries(g, ip, threads=4)
+        assert all(np.array_equal(u, v) for u, v in zip(a, b))
+    x = np.random.default_rng(1).uniform(0, 1, g.n_voxels)
+    ya = port.forward_mf_angles(g, [1, 5], x, 4)
+    yb = port.forward_mf_angles(g, [1, 5], x, 4, split=True)
+    assert np.max(np.abs(ya - yb)) <= 1e-13 * max(1.0, np.max(np.abs(ya)))
