@@ -56,6 +56,9 @@ struct ColumnHead {
   int gcell[kMaxPieces];
   unsigned char gbeg[kMaxPieces], gend[kMaxPieces];
   double gw2d[kMaxPieces];
+  // per cell group: every atom of the group is zero for G <= gmin and linear
+  // for G > gmax, where the group sum is galpha * G - gbeta
+  double gmin[kMaxPieces], gmax[kMaxPieces], galpha[kMaxPieces], gbeta[kMaxPieces];
 };
 
 __device__ __forceinline__ double cube3(double v) { return v * v * v; }
@@ -278,6 +281,31 @@ __device__ __forceinline__ bool plan_column(const DevGeom& g, double C, double S
       }
     }
   }
+  __syncwarp();
+  if (lane < ng) {  // group aggregates (lane q handles group q)
+    const int q = lane;
+    double mn = 1e300, mx = -1e300, al = 0.0, be = 0.0;
+    for (int k = H.gbeg[q]; k < H.gend[q]; ++k) {
+      const double* c = P[k].c;
+      const double* l = c + kLin;
+      if (H.pkind[k] == 1) {
+        mn = fmin(mn, l[0]);
+        mx = fmax(mx, l[1]);
+        al += l[2];
+        be += l[2] * l[3];
+      } else {
+        const double sg = H.pkind[k] == 0 ? 1.0 : -1.0;  // zone 0: hi - lo; zone 2: lo - hi
+        mn = fmin(mn, fmin(l[0], l[4]));
+        mx = fmax(mx, fmax(l[1], l[5]));
+        al += sg * (l[6] - l[2]);
+        be += sg * (l[6] * l[7] - l[2] * l[3]);
+      }
+    }
+    H.gmin[q] = mn;
+    H.gmax[q] = mx;
+    H.galpha[q] = al;
+    H.gbeta[q] = be;
+  }
   return true;
 }
 
@@ -298,10 +326,12 @@ __device__ __forceinline__ double trap_abs(const ColumnHead& H, const double* c,
 }
 
 // atom_sum (weights3d.cpp:400-423) over the pieces of cell group q at height
-// zref for row-edge slope tan_a.
+// zref for row-edge slope tan_a; gs = 1 / (a' tan_a) so G = zref * gs.
 __device__ __forceinline__ double atom_sum3(const ColumnHead& H, const PieceCoef* P, int q,
-                                            double tan_a, double zref) {
-  const double G = zref * H.inv_a / tan_a;
+                                            double tan_a, double gs, double zref) {
+  const double G = zref * gs;
+  if (G <= H.gmin[q]) return 0.0;
+  if (G > H.gmax[q]) return H.kappa * tan_a * (H.galpha[q] * G - H.gbeta[q]);
   double v = 0.0;
   for (int k = H.gbeg[q]; k < H.gend[q]; ++k) {
     const double* c = P[k].c;
@@ -345,12 +375,10 @@ __device__ __forceinline__ void voxel_weights(const DevGeom& g, const ColumnHead
         if (zt <= 0.0) return 0.0;
         return w2d * zt / (zt - zb);
       }
-      if (kk > 0.0) {
-        const double tan_a = kk * dz_sdd;
-        return atom_sum3(H, P, q, tan_a, zt) - atom_sum3(H, P, q, tan_a, zb);
-      }
-      const double tan_a = -kk * dz_sdd;
-      return w2d - (atom_sum3(H, P, q, tan_a, -zb) - atom_sum3(H, P, q, tan_a, -zt));
+      const double tan_a = fabs(kk) * dz_sdd;
+      const double gs = H.inv_a / tan_a;
+      if (kk > 0.0) return atom_sum3(H, P, q, tan_a, gs, zt) - atom_sum3(H, P, q, tan_a, gs, zb);
+      return w2d - (atom_sum3(H, P, q, tan_a, gs, -zb) - atom_sum3(H, P, q, tan_a, gs, -zt));
     };
     const int cell = H.gcell[q];
     double prev = above((double)k_lo);
@@ -374,6 +402,7 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
   const int row_lo = -g.n_det_z / 2, row_hi = g.n_det_z / 2 - 1;
   const double dz_sdd = g.dz_sdd, sdd_dz = g.sdd_dz;
   const double c_mn = sdd_dz * H.dmin_inv, c_mx = sdd_dz * H.dmax_inv;
+  const double ga = H.inv_a * sdd_dz;  // G = zref * ga / |L|
   for (int q = 0; q < H.ng; ++q) {
     const double w2d = H.gw2d[q];
     const int cell = H.gcell[q];
@@ -401,15 +430,17 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
           if (zt <= 0.0) return 0.0;
           return w2d * zt / (zt - zb);
         }
-        const double tan_a = fabs(kk) * dz_sdd;
+        const double aL = fabs(kk);
+        const double tan_a = aL * dz_sdd;
+        const double gs = ga * frcp(aL);  // 1 / (a' tan_a)
         const double zt_s = L > 0 ? zt : -zt, zb_s = L > 0 ? zb : -zb;
         double Fb;
         if (L == cL0) Fb = cF0;
         else if (L == cL1) Fb = cF1;
         else if (L == cL2) Fb = cF2;
         else if (L == cL3) Fb = cF3;
-        else Fb = atom_sum3(H, P, q, tan_a, zb_s);
-        const double Ft = atom_sum3(H, P, q, tan_a, zt_s);
+        else Fb = atom_sum3(H, P, q, tan_a, gs, zb_s);
+        const double Ft = atom_sum3(H, P, q, tan_a, gs, zt_s);
         switch (nn) {
           case 0: nL0 = L; nF0 = Ft; break;
           case 1: nL1 = L; nF1 = Ft; break;

@@ -127,7 +127,7 @@ constexpr int kWarps3 = 4;
 constexpr int kZcMax = 16;  // voxels per lane per z-block (z-block = 512 voxels)
 
 template <typename T, bool kFwd>
-__global__ void __launch_bounds__(kWarps3 * 32, 2) proj3d_kernel(
+__global__ void __launch_bounds__(kWarps3 * 32, 4) proj3d_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, int angle_begin, int angle_step, int n_sel,
     const T* __restrict__ in, T* __restrict__ xout, unsigned long long* __restrict__ yacc,
     double scale, unsigned long long* n_upd, int* status) {
