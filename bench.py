@@ -212,7 +212,8 @@ def run_ours(args):
     y = torch.from_numpy(y_h).to(tdt).to(dev)
     yout = torch.zeros(g.n_measurements, dtype=tdt, device=dev)
     xout = torch.zeros(g.n_voxels, dtype=tdt, device=dev)
-    shard = (rank, g.n_angles, world)
+    from paper_2511_12235_b200.dist import angle_shard
+    shard = angle_shard(g, rank, world)  # orbit shards for quarter-turn symmetric scans
     flush = torch.empty(256 << 20, dtype=torch.int8, device=dev)  # > 126 MB L2
 
     ev_f0, ev_f1, ev_b1, ev_r1 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]

@@ -111,6 +111,21 @@ int ctsm_fwd_mf(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begi
 int ctsm_bwd_mf(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begin,
                 int angle_end, int angle_step, const void* y_dev, void* x_dev, void* stream);
 
+/* Quarter-turn symmetric scans (square grid with even side, a == b,
+ * n_angles % 4 == 0, angles over exactly one turn): rotating the scanner by a
+ * quarter turn maps the setup onto itself, so each weight evaluation serves
+ * four (voxel, angle) pairs. ctsm_fwd_mf / ctsm_bwd_mf use this automatically
+ * for shards closed under +n_angles/4 (e.g. the full scan; disable with the
+ * environment variable CTSM_NO_SYMMETRY=1). The orbit entry points take the
+ * shard as base angles {base_begin + k * base_step < n_angles / 4} plus their
+ * quarter-turn images -- the load-balanced multi-GPU sharding of such scans.
+ * ctsm_quarter_symmetric returns 1 if the scan qualifies. */
+int ctsm_quarter_symmetric(const ctsm_geometry* g);
+int ctsm_fwd_mf_orbits(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int base_begin,
+                       int base_step, const void* x_dev, void* y_dev, void* stream);
+int ctsm_bwd_mf_orbits(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int base_begin,
+                       int base_step, const void* y_dev, void* x_dev, void* stream);
+
 /* Voxel-ray updates (nonzero weights applied, i.e. nnz of the shard's rows of
  * A) counted live by the last successful ctsm_fwd_mf call on ctx. */
 uint64_t ctsm_last_update_count(ctsm_ctx* ctx);

@@ -4,8 +4,10 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "kernels.h"
 
@@ -68,7 +70,8 @@ struct ctsm_ctx {
   unsigned long long* h_upd = nullptr;    // pinned mirror
   uint64_t last_updates = 0;
   double* h_red = nullptr;      // pinned
-  Buf angles, edges, cs, counts, scan, longrows, acc, part, tmp_a, tmp_b, tmp_c, tmp_d, tmp_e, tmp_f;
+  Buf angles, edges, cs, counts, scan, longrows, acc, part, base, tmp_a, tmp_b, tmp_c, tmp_d,
+      tmp_e, tmp_f;
 };
 
 namespace {
@@ -226,7 +229,7 @@ int ctsm_destroy(ctsm_ctx* ctx) {
   if (!ctx) return 0;
   cudaSetDevice(ctx->device);
   Buf* bufs[] = {&ctx->angles, &ctx->edges, &ctx->cs,    &ctx->counts, &ctx->scan,
-                 &ctx->longrows, &ctx->acc, &ctx->part, &ctx->tmp_a, &ctx->tmp_b,  &ctx->tmp_c,
+                 &ctx->longrows, &ctx->acc, &ctx->part, &ctx->base, &ctx->tmp_a, &ctx->tmp_b,  &ctx->tmp_c,
                  &ctx->tmp_d, &ctx->tmp_e, &ctx->tmp_f};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
@@ -388,6 +391,88 @@ static int prepare_cs(ctsm_ctx* ctx, const DevGeom& d, int begin, int step, int 
   return 0;
 }
 
+// Quarter-turn symmetry of the scan (see mf.cu): square grid with an even
+// side, a == b, n_angles % 4 == 0 and angles covering exactly one full turn.
+static bool symmetry_disabled() {
+  const char* e = std::getenv("CTSM_NO_SYMMETRY");
+  return e && e[0] && e[0] != '0';
+}
+static bool quarter_symmetric(const ctsm_geometry* g) {
+  if (symmetry_disabled()) return false;
+  if (g->n_x != g->n_y || g->n_x % 2 != 0 || g->a != g->b || g->n_angles % 4 != 0) return false;
+  const double span = g->angle_end - g->angle_start;
+  return std::fabs(span - 2.0 * 3.14159265358979323846) <= 1e-12 * span;
+}
+// Base angles (< n/4) of a shard closed under +n/4: (begin, end, step) with
+// end == n, begin < step and step dividing n/4. Returns false otherwise.
+static bool sym_base_of_shard(const ctsm_geometry* g, int begin, int end, int step,
+                              std::vector<int>* base) {
+  const int q = g->n_angles / 4;
+  if (end != g->n_angles || step <= 0 || begin >= step || q % step != 0) return false;
+  base->clear();
+  for (int i = begin; i < q; i += step) base->push_back(i);
+  return true;
+}
+static int upload_base(ctsm_ctx* ctx, const DevGeom& d, const std::vector<int>& base,
+                       cudaStream_t st) {
+  const size_t n = base.size();
+  CT_TRY(ensure(ctx, ctx->base, (n ? n : 1) * sizeof(int)));
+  if (n)
+    CT_CUDA(cudaMemcpyAsync(ctx->base.p, base.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
+  CT_TRY(ensure(ctx, ctx->cs, (n ? n : 1) * sizeof(AngleCS)));
+  CT_CUDA(build_angle_cs_list(d, (const int*)ctx->base.p, (int)n, (AngleCS*)ctx->cs.p, st));
+  CT_CUDA(cudaStreamSynchronize(st));  // base is pageable host memory
+  return 0;
+}
+
+// Symmetric forward over the orbit shard of `base` (rows of angles b + k n/4).
+static int fwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d, int dtype,
+                        const std::vector<int>& base, int base_step, const void* x, void* y,
+                        cudaStream_t st) {
+  const uint64_t n_meas = (uint64_t)d.rows_per_angle * g->n_angles;
+  double mx = 0.0;
+  CT_TRY(fetch_max_abs(ctx, dtype, (uint64_t)d.n_vox, x, st, &mx));
+  if (!std::isfinite(mx)) return fail(CTSM_ERR_NON_FINITE, "image not finite");
+  CT_TRY(upload_base(ctx, d, base, st));
+  CT_TRY(ensure(ctx, ctx->acc, n_meas * sizeof(unsigned long long)));
+  unsigned long long* acc = (unsigned long long*)ctx->acc.p;
+  const int q = g->n_angles / 4, nb = (int)base.size();
+  if (nb == 0) return 0;
+  for (int k = 0; k < 4; ++k) CT_CUDA(zero_rows_u64(d, base[0] + k * q, base_step, nb, acc, st));
+  const double B = mx * row_sum_bound(g) * 1.05;
+  const double scale = B > 0.0 ? std::ldexp(1.0, 61) / B : 1.0;
+  CT_CUDA(cudaMemsetAsync(ctx->n_upd, 0, sizeof(unsigned long long), st));
+  const bool two_d = (g->n_z == 1 && g->n_det_z == 1);
+  if (two_d)
+    CT_CUDA(fwd_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, x, acc,
+                       scale, ctx->n_upd, ctx->status, st));
+  else
+    CT_CUDA(fwd3d_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, x,
+                         acc, scale, ctx->n_upd, ctx->status, st));
+  for (int k = 0; k < 4; ++k)
+    CT_CUDA(fixed_to_float_rows(d, dtype, base[0] + k * q, base_step, nb, acc, scale, y, st));
+  CT_CUDA(cudaMemcpyAsync(ctx->h_upd, ctx->n_upd, sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, st));
+  return 0;
+}
+
+static int bwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d, int dtype,
+                        const std::vector<int>& base, const void* y, void* x, cudaStream_t st) {
+  CT_TRY(upload_base(ctx, d, base, st));
+  const int nb = (int)base.size();
+  const bool two_d = (g->n_z == 1 && g->n_det_z == 1);
+  if (two_d) {
+    const int nc = bwd_sym_chunks(d, nb);
+    if (nc > 1) CT_TRY(ensure(ctx, ctx->part, (size_t)nc * g->n_x * g->n_y * sizeof(double)));
+    CT_CUDA(bwd_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, y, x,
+                       (double*)ctx->part.p, nc, ctx->status, st));
+  } else {
+    CT_CUDA(bwd3d_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, y, x,
+                         ctx->status, st));
+  }
+  return 0;
+}
+
 static int fwd_impl(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int begin, int end,
                     int step, const void* x, void* y, cudaStream_t st) {
   DevGeom d;
@@ -396,6 +481,9 @@ static int fwd_impl(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int begin,
   CT_TRY(check_shard(g, begin, end, step));
   const int n_sel = n_in_shard(begin, end, step);
   if (n_sel == 0) return 0;
+  std::vector<int> base;
+  if (quarter_symmetric(g) && sym_base_of_shard(g, begin, end, step, &base))
+    return fwd_sym_impl(ctx, g, d, dtype, base, step, x, y, st);
   const uint64_t n_meas = (uint64_t)d.rows_per_angle * g->n_angles;
   double mx = 0.0;
   CT_TRY(fetch_max_abs(ctx, dtype, (uint64_t)d.n_vox, x, st, &mx));
@@ -422,6 +510,9 @@ static int bwd_impl(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int begin,
   CT_TRY(check_dtype(dtype));
   CT_TRY(check_shard(g, begin, end, step));
   const int n_sel = n_in_shard(begin, end, step);
+  std::vector<int> base;
+  if (n_sel > 0 && quarter_symmetric(g) && sym_base_of_shard(g, begin, end, step, &base))
+    return bwd_sym_impl(ctx, g, d, dtype, base, y, x, st);
   CT_TRY(prepare_cs(ctx, d, begin, step, n_sel, st));
   const int nc = bwd_chunks(d, n_sel);
   if (nc > 1) CT_TRY(ensure(ctx, ctx->part, (size_t)nc * g->n_x * g->n_y * sizeof(double)));
@@ -441,6 +532,56 @@ int ctsm_fwd_mf(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begi
 }
 
 uint64_t ctsm_last_update_count(ctsm_ctx* ctx) { return ctx ? ctx->last_updates : 0; }
+
+int ctsm_quarter_symmetric(const ctsm_geometry* g) {
+  DevGeom d;
+  if (dev_geom(g, &d) != 0) return 0;
+  return quarter_symmetric(g) ? 1 : 0;
+}
+
+static int orbit_base(const ctsm_geometry* g, int base_begin, int base_step,
+                      std::vector<int>* base) {
+  if (!quarter_symmetric(g))
+    return fail(CTSM_ERR_INVALID_SPEC, "orbit shards need a quarter-turn symmetric scan");
+  const int q = g->n_angles / 4;
+  if (base_begin < 0 || base_step <= 0) return fail(CTSM_ERR_INVALID_SPEC, "bad orbit shard");
+  base->clear();
+  for (int i = base_begin; i < q; i += base_step) base->push_back(i);
+  return 0;
+}
+
+int ctsm_fwd_mf_orbits(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int base_begin,
+                       int base_step, const void* x_dev, void* y_dev, void* stream) {
+  CT_TRY(set_device(ctx));
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  CT_TRY(check_dtype(dtype));
+  std::vector<int> base;
+  CT_TRY(orbit_base(g, base_begin, base_step, &base));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (base.empty()) return 0;
+  CT_TRY(fwd_sym_impl(ctx, g, d, dtype, base, base_step, x_dev, y_dev, st));
+  CT_TRY(check_status(ctx, st, "forward_project_matrix_free"));
+  ctx->last_updates = *ctx->h_upd;
+  return 0;
+}
+
+int ctsm_bwd_mf_orbits(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int base_begin,
+                       int base_step, const void* y_dev, void* x_dev, void* stream) {
+  CT_TRY(set_device(ctx));
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  CT_TRY(check_dtype(dtype));
+  std::vector<int> base;
+  CT_TRY(orbit_base(g, base_begin, base_step, &base));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (base.empty()) {
+    CT_CUDA(cudaMemsetAsync(x_dev, 0, (size_t)d.n_vox * (dtype == CTSM_F64 ? 8 : 4), st));
+    return check_status(ctx, st, "back_project_matrix_free");
+  }
+  CT_TRY(bwd_sym_impl(ctx, g, d, dtype, base, y_dev, x_dev, st));
+  return check_status(ctx, st, "back_project_matrix_free");
+}
 
 int ctsm_bwd_mf(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begin,
                 int angle_end, int angle_step, const void* y_dev, void* x_dev, void* stream) {

@@ -119,9 +119,9 @@ __device__ __forceinline__ void sweep_walk(const DevGeom& g, double C, double S,
   const double scale = g.u_scale;
   const double inv_scale = g.t_scale;
   const double T1 = w.T1, T2 = w.T2, T3 = w.T3, T4 = w.T4;
-  const long long e_lo = (long long)floor(T1 * scale) + 1;
-  const long long e_hi = (long long)ceil(T4 * scale) - 1;
-  int cell = (int)(e_lo - 1);
+  const int e_lo = (int)floor(T1 * scale) + 1;
+  const int e_hi = (int)ceil(T4 * scale) - 1;
+  int cell = e_lo - 1;
   const bool bv = w.band_vertical;
   // A ray parallel to a pixel face makes a factor vanish; the reference then
   // returns 0 for the triangle (|sin(beta - phi)| < 1e-12, weights2d.cpp:11)
@@ -150,7 +150,7 @@ __device__ __forceinline__ void sweep_walk(const DevGeom& g, double C, double S,
   double prev = T1;
   double acc = 0.0;
   int zi = 1;  // next corner: 1 -> T2, 2 -> T3, 3 -> T4
-  long long e = e_lo;
+  int e = e_lo;
   while (zi <= 3) {
     const double tz = zi == 1 ? T2 : (zi == 2 ? T3 : T4);
     const bool have_e = e <= e_hi;
@@ -252,13 +252,15 @@ __device__ __forceinline__ bool pixel_weights(const DevGeom& g, double C, double
   };
   const double scale = g.u_scale;
   const double inv_scale = g.t_scale;
-  const long long e_lo = (long long)floor(T1 * scale) + 1;
-  const long long e_hi = (long long)ceil(T4 * scale) - 1;
+  // |t| * scale is bounded by the edge-table extent (dev_geom), so 32-bit
+  // edge indices suffice (cheaper int <-> double conversions)
+  const int e_lo = (int)floor(T1 * scale) + 1;
+  const int e_hi = (int)ceil(T4 * scale) - 1;
   const int cell_lo = -g.n_det_y / 2, cell_hi = g.n_det_y / 2 - 1;
   double prev = 0.0;  // CA(T1)
-  int cell = (int)(e_lo - 1);
+  int cell = e_lo - 1;
 #pragma unroll 2
-  for (long long e = e_lo; e <= e_hi; ++e, ++cell) {
+  for (int e = e_lo; e <= e_hi; ++e, ++cell) {
     const double cur = CA(e * inv_scale);  // CA clamps outside [T1, T4]
     const double wv = cur - prev;
     prev = cur;

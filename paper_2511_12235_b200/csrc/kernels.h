@@ -52,6 +52,23 @@ struct AngleCS {
 cudaError_t build_angle_cs(const DevGeom& g, int angle_begin, int angle_step, int n_sel,
                            AngleCS* out, cudaStream_t st);
 // dtype: CTSM_F64 / CTSM_F32
+// Quarter-turn symmetric variants (square grid, full turn, n_angles % 4 == 0):
+// weights are evaluated at the base angles base[0..n_base) (< n_angles / 4)
+// and applied to all four quarter-turn images (angles base + k n_angles / 4).
+cudaError_t build_angle_cs_list(const DevGeom& g, const int* idx, int n, AngleCS* out,
+                                cudaStream_t st);
+cudaError_t fwd_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
+                       int n_base, const void* x, unsigned long long* yacc, double scale,
+                       unsigned long long* n_upd, int* status, cudaStream_t st);
+int bwd_sym_chunks(const DevGeom& g, int n_base);
+cudaError_t bwd_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
+                       int n_base, const void* y, void* x, double* part, int n_chunks,
+                       int* status, cudaStream_t st);
+cudaError_t fwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
+                         int n_base, const void* x, unsigned long long* yacc, double scale,
+                         unsigned long long* n_upd, int* status, cudaStream_t st);
+cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
+                         int n_base, const void* y, void* x, int* status, cudaStream_t st);
 cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
                    int angle_step, int n_sel, const void* x, unsigned long long* yacc,
                    double scale, unsigned long long* n_upd, int* status, cudaStream_t st);

@@ -180,6 +180,225 @@ __global__ void __launch_bounds__(kWarps3 * 32, 4) proj3d_kernel(
   if (kFwd) count_updates(n_upd, cnt);
 }
 
+// ---- quarter-turn symmetric kernels --------------------------------------
+// For a square grid (n_x == n_y, a == b) and angles uniform over a full turn
+// with n_angles % 4 == 0, rotating the scanner by a quarter turn maps the
+// setup onto itself: pixel (ix, iy) at angle i + n/4 sees exactly the weights
+// of pixel R^-1(ix, iy) at angle i, with R(ix, iy) = (n-1-iy, ix). Each weight
+// evaluation therefore serves four (pixel, angle) pairs; the kernels below
+// evaluate weights at the "base" angles i < n/4 only and apply every weight to
+// its four images. The updates applied are the same as in the general
+// kernels; only repeated weight evaluations are avoided.
+__device__ __forceinline__ void rot_pixel(int n, int ix, int iy, int k, int& ox, int& oy) {
+  int x = ix, y = iy;
+  for (int r = 0; r < k; ++r) {
+    const int t = x;
+    x = n - 1 - y;
+    y = t;
+  }
+  ox = x;
+  oy = y;
+}
+
+// Forward: thread = (pixel p, chunk of base angles); scatters w * x[R^k p] to
+// the rows of angle i + k n/4.
+template <typename T>
+__global__ void __launch_bounds__(128) fwd2d_sym_kernel(
+    DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
+    const T* __restrict__ x, unsigned long long* __restrict__ yacc, double scale,
+    unsigned long long* n_upd, int* status) {
+  const int tiles_x = (g.n_x + kTx - 1) / kTx;
+  const int ix = (blockIdx.x % tiles_x) * kTx + (threadIdx.x % kTx);
+  const int iy = (blockIdx.x / tiles_x) * kTy + (threadIdx.x / kTx);
+  unsigned cnt = 0;
+  if (ix < g.n_x && iy < g.n_y) {
+    const int n = g.n_x;
+    double xs[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int rx, ry;
+      rot_pixel(n, ix, iy, k, rx, ry);
+      xs[k] = ld(&x[(long long)ry * n + rx]) * scale;
+    }
+    const int q = g.n_angles / 4;
+    const int k0 = blockIdx.y * kFwdAngles;
+    const int k1 = min(k0 + kFwdAngles, n_base);
+    for (int kk = k0; kk < k1; ++kk) {
+      const AngleCS a = cs[kk];
+      const int i = base[kk];
+      unsigned long long* rows[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        rows[k] = yacc + (long long)((i + k * q) % g.n_angles) * g.rows_per_angle + g.n_det_y / 2;
+      fast::pixel_weights(g, a.C, a.S, ix, iy, status, [&](int m, double w) {
+        cnt += 4;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (xs[k] != 0.0) atomicAdd(&rows[k][m], (unsigned long long)__double2ll_rn(w * xs[k]));
+      });
+    }
+  }
+  count_updates(n_upd, cnt);
+}
+
+// Backward: thread = quarter-turn orbit {p, Rp, R^2p, R^3p} of a pixel of the
+// first quadrant x a chunk of base angles; every weight set of orbit member j
+// at base angle i is gathered against the rows of angles i + k n/4 into the
+// accumulator of member j + k.
+template <typename T>
+__global__ void __launch_bounds__(128) bwd2d_sym_kernel(
+    DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
+    int chunk, const T* __restrict__ y, T* __restrict__ x, double* __restrict__ part,
+    int* status) {
+  const int h = g.n_x / 2;
+  const int tiles_x = (h + kTx - 1) / kTx;
+  const int ix = (blockIdx.x % tiles_x) * kTx + (threadIdx.x % kTx);
+  const int iy = (blockIdx.x / tiles_x) * kTy + (threadIdx.x / kTx);
+  if (ix >= h || iy >= h) return;
+  const int n = g.n_x, q = g.n_angles / 4;
+  int px[4], py[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) rot_pixel(n, ix, iy, j, px[j], py[j]);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int k0 = blockIdx.y * chunk;
+  const int k1 = min(k0 + chunk, n_base);
+  for (int kk = k0; kk < k1; ++kk) {
+    const AngleCS a = cs[kk];
+    const int i = base[kk];
+    const T* rows[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      rows[k] = y + (long long)((i + k * q) % g.n_angles) * g.rows_per_angle + g.n_det_y / 2;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      fast::pixel_weights(g, a.C, a.S, px[j], py[j], status, [&](int m, double w) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[(j + k) & 3] += w * ld(&rows[k][m]);
+      });
+    }
+  }
+  const long long npix = (long long)n * n;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const long long pix = (long long)py[j] * n + px[j];
+    if (part)
+      part[(long long)blockIdx.y * npix + pix] = acc[j];
+    else
+      x[pix] = (T)acc[j];
+  }
+}
+
+// 3D quarter-turn symmetric forward: warp = column c, base angles only; each
+// weight of c at base angle i is scattered to the rows of angles i + k n/4
+// with the voxel values of the rotated columns R^k c.
+template <typename T>
+__global__ void __launch_bounds__(kWarps3 * 32, 4) fwd3d_sym_kernel(
+    DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
+    const T* __restrict__ in, unsigned long long* __restrict__ yacc, double scale,
+    unsigned long long* n_upd, int* status) {
+  __shared__ fast::ColumnHead sh[kWarps3];
+  __shared__ fast::PieceCoef sp[kWarps3][fast::kMaxPieces];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = g.n_x;
+  const long long nxy = (long long)n * g.n_y;
+  const long long col = (long long)blockIdx.x * kWarps3 + warp;
+  if (col >= nxy) return;  // whole warp
+  const int ix = (int)(col % n), iy = (int)(col / n);
+  long long rc[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    int rx, ry;
+    rot_pixel(n, ix, iy, k, rx, ry);
+    rc[k] = (long long)ry * n + rx;
+  }
+  const int rpa = g.rows_per_angle, q = g.n_angles / 4;
+  const int hy = g.n_det_y / 2, hz = g.n_det_z / 2;
+  unsigned cnt = 0;
+  for (int zb0 = 0; zb0 < g.n_z; zb0 += 32 * kZcMax) {
+    const int nzb = min(32 * kZcMax, g.n_z - zb0);
+    const int zc = (nzb + 31) / 32;
+    const int z0 = zb0 + lane * zc, z1 = min(z0 + zc, zb0 + nzb);
+    for (int kk = 0; kk < n_base; ++kk) {
+      const int i = base[kk];
+      const AngleCS a = cs[kk];
+      __syncwarp();
+      const bool ok = fast::plan_column(g, a.C, a.S, ix, iy, status, sh[warp], sp[warp], lane);
+      __syncwarp();
+      if (!ok) continue;
+      unsigned long long* yb[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) yb[k] = yacc + (long long)((i + k * q) % g.n_angles) * rpa;
+      fast::chunk_weights(g, sh[warp], sp[warp], z0, z1, [&](int iz, int my, int mz, double w) {
+        cnt += 4;
+        const long long r = (long long)(mz + hz) * g.n_det_y + (my + hy);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double xs = ld(&in[iz * nxy + rc[k]]) * scale;
+          if (xs != 0.0) atomicAdd(&yb[k][r], (unsigned long long)__double2ll_rn(w * xs));
+        }
+      });
+    }
+  }
+  count_updates(n_upd, cnt);
+}
+
+// 3D quarter-turn symmetric backward: warp = orbit {c, Rc, R^2c, R^3c} of a
+// first-quadrant column; per base angle the four members are planned in turn
+// and every weight set is gathered against the four image angles into the
+// shared-memory accumulators of the matching orbit member (fixed order).
+constexpr int kWarpsS = 2;
+constexpr int kZcS = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(kWarpsS * 32, 8) bwd3d_sym_kernel(
+    DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
+    const T* __restrict__ in, T* __restrict__ xout, int* status) {
+  __shared__ fast::ColumnHead sh[kWarpsS];
+  __shared__ fast::PieceCoef sp[kWarpsS][fast::kMaxPieces];
+  __shared__ double sacc[kWarpsS][4][kZcS][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = g.n_x, h = n / 2;
+  const long long orb = (long long)blockIdx.x * kWarpsS + warp;
+  if (orb >= (long long)h * h) return;  // whole warp
+  const int ix0 = (int)(orb % h), iy0 = (int)(orb / h);
+  int cx[4], cy[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) rot_pixel(n, ix0, iy0, j, cx[j], cy[j]);
+  const long long nxy = (long long)n * g.n_y;
+  const int rpa = g.rows_per_angle, q = g.n_angles / 4;
+  const int hy = g.n_det_y / 2, hz = g.n_det_z / 2;
+  for (int zb0 = 0; zb0 < g.n_z; zb0 += 32 * kZcS) {
+    const int nzb = min(32 * kZcS, g.n_z - zb0);
+    const int zc = (nzb + 31) / 32;
+    const int z0 = zb0 + lane * zc, z1 = min(z0 + zc, zb0 + nzb);
+    for (int j = 0; j < 4; ++j)
+      for (int t = 0; t < zc; ++t) sacc[warp][j][t][lane] = 0.0;
+    for (int kk = 0; kk < n_base; ++kk) {
+      const int i = base[kk];
+      const AngleCS a = cs[kk];
+      const T* yb[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) yb[k] = in + (long long)((i + k * q) % g.n_angles) * rpa;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        __syncwarp();
+        const bool ok = fast::plan_column(g, a.C, a.S, cx[j], cy[j], status, sh[warp], sp[warp], lane);
+        __syncwarp();
+        if (!ok) continue;
+        fast::chunk_weights(g, sh[warp], sp[warp], z0, z1, [&](int iz, int my, int mz, double w) {
+          const long long r = (long long)(mz + hz) * g.n_det_y + (my + hy);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) sacc[warp][(j + k) & 3][iz - z0][lane] += w * ld(&yb[k][r]);
+        });
+      }
+    }
+    for (int j = 0; j < 4; ++j) {
+      const long long c = (long long)cy[j] * n + cx[j];
+      for (int iz = z0; iz < z1; ++iz) xout[iz * nxy + c] = (T)sacc[warp][j][iz - z0][lane];
+    }
+  }
+}
+
 template <typename T>
 __global__ void fixed_rows_kernel(int rpa, int angle_begin, int angle_step, int n_sel,
                                   unsigned long long* acc, double inv_scale, T* y) {
@@ -361,6 +580,109 @@ cudaError_t bwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_beg
           nullptr, status);
     count_launch();
   }
+  return cudaGetLastError();
+}
+
+cudaError_t fwd_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
+                       int n_base, const void* x, unsigned long long* yacc, double scale,
+                       unsigned long long* n_upd, int* status, cudaStream_t st) {
+  if (n_base <= 0) return cudaSuccess;
+  const dim3 grid = tile_grid(g, (unsigned)((n_base + kFwdAngles - 1) / kFwdAngles));
+  if (dtype == CTSM_F64)
+    fwd2d_sym_kernel<double><<<grid, 128, 0, st>>>(g, cs, base, n_base, (const double*)x, yacc,
+                                                   scale, n_upd, status);
+  else
+    fwd2d_sym_kernel<float><<<grid, 128, 0, st>>>(g, cs, base, n_base, (const float*)x, yacc,
+                                                  scale, n_upd, status);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t fwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
+                         int n_base, const void* x, unsigned long long* yacc, double scale,
+                         unsigned long long* n_upd, int* status, cudaStream_t st) {
+  if (n_base <= 0) return cudaSuccess;
+  const long long nxy = (long long)g.n_x * g.n_y;
+  const unsigned blocks = (unsigned)((nxy + kWarps3 - 1) / kWarps3);
+  if (dtype == CTSM_F64)
+    fwd3d_sym_kernel<double><<<blocks, kWarps3 * 32, 0, st>>>(g, cs, base, n_base,
+                                                             (const double*)x, yacc, scale,
+                                                             n_upd, status);
+  else
+    fwd3d_sym_kernel<float><<<blocks, kWarps3 * 32, 0, st>>>(g, cs, base, n_base,
+                                                            (const float*)x, yacc, scale, n_upd,
+                                                            status);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
+                         int n_base, const void* y, void* x, int* status, cudaStream_t st) {
+  const long long h = g.n_x / 2;
+  const unsigned blocks = (unsigned)((h * h + kWarpsS - 1) / kWarpsS);
+  if (dtype == CTSM_F64)
+    bwd3d_sym_kernel<double><<<blocks, kWarpsS * 32, 0, st>>>(g, cs, base, n_base,
+                                                             (const double*)y, (double*)x,
+                                                             status);
+  else
+    bwd3d_sym_kernel<float><<<blocks, kWarpsS * 32, 0, st>>>(g, cs, base, n_base,
+                                                            (const float*)y, (float*)x, status);
+  count_launch();
+  return cudaGetLastError();
+}
+
+int bwd_sym_chunks(const DevGeom& g, int n_base) {
+  const int h = g.n_x / 2;
+  const long long tiles = (long long)((h + kTx - 1) / kTx) * ((h + kTy - 1) / kTy);
+  long long c = (16LL * 148 * 6 + tiles - 1) / tiles;
+  if (c > n_base) c = n_base;
+  if (c > 64) c = 64;
+  return (int)(c < 1 ? 1 : c);
+}
+
+cudaError_t bwd_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
+                       int n_base, const void* y, void* x, double* part, int n_chunks,
+                       int* status, cudaStream_t st) {
+  const int h = g.n_x / 2;
+  const unsigned tiles = (unsigned)(((h + kTx - 1) / kTx) * ((h + kTy - 1) / kTy));
+  const int chunk = (n_base + n_chunks - 1) / (n_chunks > 0 ? n_chunks : 1);
+  const int nc = chunk > 0 ? (n_base + chunk - 1) / chunk : 1;
+  double* p = nc > 1 ? part : nullptr;
+  const dim3 grid(tiles, (unsigned)(nc > 0 ? nc : 1));
+  if (dtype == CTSM_F64)
+    bwd2d_sym_kernel<double><<<grid, 128, 0, st>>>(g, cs, base, n_base, chunk, (const double*)y,
+                                                   (double*)x, p, status);
+  else
+    bwd2d_sym_kernel<float><<<grid, 128, 0, st>>>(g, cs, base, n_base, chunk, (const float*)y,
+                                                  (float*)x, p, status);
+  count_launch();
+  if (nc > 1) {
+    const long long n = (long long)g.n_x * g.n_y;
+    if (dtype == CTSM_F64)
+      bwd_reduce_kernel<double><<<grid_for(n), 256, 0, st>>>(n, nc, part, (double*)x);
+    else
+      bwd_reduce_kernel<float><<<grid_for(n), 256, 0, st>>>(n, nc, part, (float*)x);
+    count_launch();
+  }
+  return cudaGetLastError();
+}
+
+// (cos, sin) of an explicit angle list
+__global__ void angle_cs_list_kernel(DevGeom g, const int* idx, int n, AngleCS* out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int i = idx[k];
+  const double phi = g.angle_start + (g.angle_end - g.angle_start) * i / g.n_angles;
+  double S, C;
+  sincos(phi, &S, &C);
+  out[k] = AngleCS{C, S};
+}
+
+cudaError_t build_angle_cs_list(const DevGeom& g, const int* idx, int n, AngleCS* out,
+                                cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  angle_cs_list_kernel<<<(n + 127) / 128, 128, 0, st>>>(g, idx, n, out);
+  count_launch();
   return cudaGetLastError();
 }
 

@@ -24,15 +24,35 @@ import torch.distributed as dist
 from .geometry import ScanGeometry
 
 
-def angle_shard(g: ScanGeometry, rank: int, world: int) -> tuple[int, int, int]:
-    """(begin, end, step) of rank's strided angle shard."""
+def angle_shard(g: ScanGeometry, rank: int, world: int, symmetric: Optional[bool] = None):
+    """Rank's angle shard. Quarter-turn symmetric scans are sharded by orbits
+    ("orbits", rank, world): base angles rank, rank + world, ... < n/4 and
+    their quarter-turn images, so every rank keeps the 4x weight reuse;
+    otherwise the strided shard (rank, n_angles, world)."""
+    if symmetric is None:
+        try:
+            from .projector import quarter_symmetric
+            symmetric = quarter_symmetric(g)
+        except Exception:  # library unavailable (CPU-only tests)
+            symmetric = False
+    if symmetric:
+        return ("orbits", rank, world)
     return rank, g.n_angles, world
 
 
-def shard_rows(g: ScanGeometry, shard: tuple[int, int, int]) -> torch.Tensor:
-    """Indices of the sinogram entries owned by a shard (angle-major rows)."""
+def shard_angles(g: ScanGeometry, shard) -> torch.Tensor:
+    """Angle indices of a shard, ascending."""
+    if shard[0] == "orbits":
+        q = g.n_angles // 4
+        base = torch.arange(shard[1], q, shard[2])
+        return torch.sort(torch.cat([base + k * q for k in range(4)])).values
     a0, a1, st = shard
-    angles = torch.arange(a0, a1, st)
+    return torch.arange(a0, a1, st)
+
+
+def shard_rows(g: ScanGeometry, shard) -> torch.Tensor:
+    """Indices of the sinogram entries owned by a shard (angle-major rows)."""
+    angles = shard_angles(g, shard)
     rpa = g.rows_per_angle
     return (angles[:, None] * rpa + torch.arange(rpa)[None, :]).reshape(-1)
 

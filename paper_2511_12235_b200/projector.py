@@ -137,7 +137,17 @@ def _to_device(a, device: int, dtype=None):
     return t.to(f"cuda:{device}"), False
 
 
-def _angle_shard(g: ScanGeometry, angles) -> tuple[int, int, int]:
+def quarter_symmetric(g: ScanGeometry) -> bool:
+    """True if the scan is invariant under a quarter turn (square grid with an
+    even side, a == b, n_angles % 4 == 0, one full turn): the matrix-free
+    kernels then evaluate each weight once for four (voxel, angle) pairs."""
+    return bool(_lib.lib().ctsm_quarter_symmetric(ctypes.byref(g.to_c())))
+
+
+def _angle_shard(g: ScanGeometry, angles):
+    """(begin, end, step) or ("orbits", base_begin, base_step)."""
+    if isinstance(angles, tuple) and len(angles) == 3 and angles[0] == "orbits":
+        return angles
     if angles is None:
         return 0, g.n_angles, 1
     if isinstance(angles, range):
@@ -272,7 +282,9 @@ def forward_project_matrix_free(g: ScanGeometry, mode: str = MatrixMode.consiste
                                 device: Optional[int] = None):
     """projector.cpp:235-260 (K5). ``angles`` = (begin, end, step) restricts the
     projection to an angle shard (rows of other angles are left untouched in
-    ``out``, zero in a fresh output). dtype follows x (float64 / float32)."""
+    ``out``, zero in a fresh output); ("orbits", b0, bstep) selects the base
+    angles b0 + k bstep < n/4 of a quarter-turn symmetric scan together with
+    their quarter-turn images. dtype follows x (float64 / float32)."""
     _require_consistent(mode)
     g.validate()
     n = int(x.numel()) if (torch is not None and isinstance(x, torch.Tensor)) else int(np.size(x))
@@ -282,11 +294,17 @@ def forward_project_matrix_free(g: ScanGeometry, mode: str = MatrixMode.consiste
                       (x.device.index if (torch is not None and isinstance(x, torch.Tensor)
                                           and x.is_cuda) else None))
     xt, was_t = _to_device(x, ctx.device)
-    a0, a1, st = _angle_shard(g, angles)
+    sh = _angle_shard(g, angles)
     y = out if out is not None else torch.zeros(g.n_measurements, dtype=xt.dtype, device=xt.device)
     cg = g.to_c()
-    _lib.check(_lib.lib().ctsm_fwd_mf(ctx.handle, ctypes.byref(cg), _dtype_code(xt), a0, a1, st,
-                                      _dev_ptr(xt), _dev_ptr(y), _stream(ctx.device)))
+    if sh[0] == "orbits":
+        _lib.check(_lib.lib().ctsm_fwd_mf_orbits(ctx.handle, ctypes.byref(cg), _dtype_code(xt),
+                                                 sh[1], sh[2], _dev_ptr(xt), _dev_ptr(y),
+                                                 _stream(ctx.device)))
+    else:
+        a0, a1, st = sh
+        _lib.check(_lib.lib().ctsm_fwd_mf(ctx.handle, ctypes.byref(cg), _dtype_code(xt), a0, a1,
+                                          st, _dev_ptr(xt), _dev_ptr(y), _stream(ctx.device)))
     return y if (was_t or out is not None) else y.cpu().numpy()
 
 
@@ -305,11 +323,17 @@ def back_project_matrix_free(g: ScanGeometry, mode: str = MatrixMode.consistent,
                       (y.device.index if (torch is not None and isinstance(y, torch.Tensor)
                                           and y.is_cuda) else None))
     yt, was_t = _to_device(y, ctx.device)
-    a0, a1, st = _angle_shard(g, angles)
+    sh = _angle_shard(g, angles)
     x = out if out is not None else torch.empty(g.n_voxels, dtype=yt.dtype, device=yt.device)
     cg = g.to_c()
-    _lib.check(_lib.lib().ctsm_bwd_mf(ctx.handle, ctypes.byref(cg), _dtype_code(yt), a0, a1, st,
-                                      _dev_ptr(yt), _dev_ptr(x), _stream(ctx.device)))
+    if sh[0] == "orbits":
+        _lib.check(_lib.lib().ctsm_bwd_mf_orbits(ctx.handle, ctypes.byref(cg), _dtype_code(yt),
+                                                 sh[1], sh[2], _dev_ptr(yt), _dev_ptr(x),
+                                                 _stream(ctx.device)))
+    else:
+        a0, a1, st = sh
+        _lib.check(_lib.lib().ctsm_bwd_mf(ctx.handle, ctypes.byref(cg), _dtype_code(yt), a0, a1,
+                                          st, _dev_ptr(yt), _dev_ptr(x), _stream(ctx.device)))
     return x if (was_t or out is not None) else x.cpu().numpy()
 
 

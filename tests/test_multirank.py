@@ -28,9 +28,10 @@ def _oracle_fns():
     import pyoracle
     orc = pyoracle.load("port_cr")
 
+    from paper_2511_12235_b200.dist import shard_angles
+
     def fwd(g, x, shard, out):
-        a0, a1, st = shard
-        angles = np.arange(a0, a1, st, dtype=np.int32)
+        angles = shard_angles(g, shard).numpy().astype(np.int32)
         ysel = orc.forward_mf_angles(g, angles, x.numpy(), 1)
         rpa = g.rows_per_angle
         o = out.numpy()
@@ -39,8 +40,7 @@ def _oracle_fns():
         return out
 
     def bwd(g, y, shard, out):
-        a0, a1, st = shard
-        angles = np.arange(a0, a1, st, dtype=np.int32)
+        angles = shard_angles(g, shard).numpy().astype(np.int32)
         out.copy_(torch.from_numpy(orc.back_mf_angles(g, angles, y.numpy(), 1)))
         return out
 
@@ -73,7 +73,7 @@ def _worker(rank, world, port, name, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["proj2d", "proj3d"])
+@pytest.mark.parametrize("name", ["proj2d", "proj3d", "wide2d"])  # wide2d: orbit shards
 def test_two_rank_sharding_matches_unsharded(name):
     import pyoracle
     orc = pyoracle.load("port_cr")
@@ -99,9 +99,10 @@ def test_two_rank_sharding_matches_unsharded(name):
     assert np.max(np.abs(xs - s_ref)) <= 1e-10 * max(1.0, np.max(np.abs(s_ref)))
 
 
-def test_shard_rows_partition():
+@pytest.mark.parametrize("symmetric", [False, True])
+def test_shard_rows_partition(symmetric):
     from paper_2511_12235_b200.dist import angle_shard, shard_rows
-    g = TEST_GEOMETRIES["proj3d"]
-    world = 4
-    rows = torch.cat([shard_rows(g, angle_shard(g, r, world)) for r in range(world)])
+    g = TEST_GEOMETRIES["cone3d"]  # 8 angles, square grid: both shardings apply
+    world = 2
+    rows = torch.cat([shard_rows(g, angle_shard(g, r, world, symmetric)) for r in range(world)])
     assert torch.equal(torch.sort(rows).values, torch.arange(g.n_measurements))
