@@ -299,19 +299,28 @@ def run_ours(args):
             dist.destroy_process_group()
         return
     peak = measure_dfma_peak(torch)
-    # roofline of the dominant kernel (the slower of fwd / bwd)
-    units = g.n_x * g.n_y * g.n_z * g.n_angles / (world if world > 1 else 1)
-    if g.is_2d():
-        per_unit = F_REF["2d"]
-    else:
-        per_unit = F_REF["3d"]
+    # roofline of the dominant kernel (the slower of fwd / bwd). Units are the
+    # pixel/voxel-angle weight evaluations the kernel actually performs: with
+    # the quarter-turn symmetry each evaluation serves 4 pixel-angles of the
+    # workload, so units = pixel-angles / 4 (the workload-equivalent figure is
+    # reported beside it).
+    from paper_2511_12235_b200.projector import quarter_symmetric
+    reuse = 4 if (quarter_symmetric(g) and not os.environ.get("CTSM_NO_SYMMETRY")) else 1
+    pixel_angles = g.n_x * g.n_y * g.n_z * g.n_angles / (world if world > 1 else 1)
+    units = pixel_angles / reuse
+    per_unit = F_REF["2d"] if g.is_2d() else F_REF["3d"]
     dom_ms = max(ms_f, ms_b)
     achieved = units * per_unit / (dom_ms * 1e-3) / 1e12
-    roof = {"bound": "fp64", "kernel": "bwd2d" if ms_b >= ms_f else "fwd2d",
+    kname = ("fwd2d_sym" if reuse == 4 else "fwd2d") if ms_f >= ms_b else ("bwd2d_sym" if reuse == 4 else "bwd2d")
+    if not g.is_2d():
+        kname = kname.replace("2d", "3d")
+    roof = {"bound": "fp64", "kernel": kname,
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": (achieved / peak) if peak else None, "traffic": None,
             "peak_source": "measured DFMA microkernel (MEASURED_PEAKS.json has no FP64 entry)",
-            "work_per_unit": f"{per_unit:g} FP64 flops per pixel-angle (SURVEY.md §8(d))",
+            "work_per_unit": f"{per_unit:g} FP64 flops per weight evaluation (reference op count, SURVEY.md §8(d))",
+            "units_per_launch": units, "symmetry_reuse": reuse,
+            "workload_equivalent_TFLOPs": achieved * reuse,
             "fwd_ms": ms_f, "bwd_ms": ms_b}
     line = {
         "metric": "voxel-ray updates/s (A x + A^T y)",

@@ -19,8 +19,16 @@ n_ang = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 g = CONFIGS[cfg]
 x = torch.from_numpy(phantom_for(cfg, g, dtype=np.float32)).cuda()
 y = torch.rand(g.n_measurements, dtype=torch.float32, device="cuda")
-step = max(1, g.n_angles // n_ang)
-shard = (0, g.n_angles, step)
+from paper_2511_12235_b200.projector import quarter_symmetric  # noqa: E402
+
+if quarter_symmetric(g) and not os.environ.get("CTSM_NO_SYMMETRY"):
+    base_step = max(1, (g.n_angles // 4) // max(1, n_ang // 4))
+    shard = ("orbits", 0, base_step)  # base angles + their quarter-turn images
+    n_sel = 4 * len(range(0, g.n_angles // 4, base_step))
+else:
+    step = max(1, g.n_angles // n_ang)
+    shard = (0, g.n_angles, step)
+    n_sel = len(range(*shard))
 yo = torch.zeros_like(y)
 xo = torch.zeros_like(x)
 for it in range(2):
@@ -32,4 +40,7 @@ for it in range(2):
     back_project_matrix_free(g, "consistent", 1, y, angles=shard, out=xo)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
-    print(f"{cfg} {len(range(*shard))} angles: fwd {1e3*(t1-t0):.1f} ms  bwd {1e3*(t2-t1):.1f} ms")
+    print(f"{cfg} {n_sel} angles ({shard[0] if shard[0] == 'orbits' else 'strided'}): "
+          f"fwd {1e3*(t1-t0):.1f} ms  bwd {1e3*(t2-t1):.1f} ms  "
+          f"-> per full projection fwd {1e3*(t1-t0)*g.n_angles/n_sel:.0f} ms, "
+          f"bwd {1e3*(t2-t1)*g.n_angles/n_sel:.0f} ms")
