@@ -160,13 +160,24 @@ __global__ void __launch_bounds__(kWarps3 * 32, 4) proj3d_kernel(
       const fast::PieceCoef* P = sp[warp];
       if (kFwd) {
         unsigned long long* yb = yacc + (long long)ip * rpa;
+        // consecutive emits of a lane often hit the same (row, cell) as z
+        // advances: merge them (integer sums of the rounded contributions, so
+        // the result equals the unmerged atomics) before one atomic.
+        long long pr = -1, pv = 0;
         fast::chunk_weights(g, H, P, z0, z1, [&](int iz, int my, int mz, double w) {
           ++cnt;
           const double xs = ld(&in[iz * plane + col]) * scale;
-          if (xs != 0.0)
-            atomicAdd(&yb[(long long)(mz + hz) * g.n_det_y + (my + hy)],
-                      (unsigned long long)__double2ll_rn(w * xs));
+          const long long r = (long long)(mz + hz) * g.n_det_y + (my + hy);
+          const long long v = __double2ll_rn(w * xs);
+          if (r == pr) {
+            pv += v;
+          } else {
+            if (pr >= 0 && pv != 0) atomicAdd(&yb[pr], (unsigned long long)pv);
+            pr = r;
+            pv = v;
+          }
         });
+        if (pr >= 0 && pv != 0) atomicAdd(&yb[pr], (unsigned long long)pv);
       } else {
         const T* yb = in + (long long)ip * rpa;
         fast::chunk_weights(g, H, P, z0, z1, [&](int iz, int my, int mz, double w) {
@@ -328,15 +339,28 @@ __global__ void __launch_bounds__(kWarps3 * 32, 4) fwd3d_sym_kernel(
       unsigned long long* yb[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) yb[k] = yacc + (long long)((i + k * q) % g.n_angles) * rpa;
+      long long pr = -1, pv[4] = {0, 0, 0, 0};  // pending merge (see proj3d_kernel)
       fast::chunk_weights(g, sh[warp], sp[warp], z0, z1, [&](int iz, int my, int mz, double w) {
         cnt += 4;
         const long long r = (long long)(mz + hz) * g.n_det_y + (my + hy);
+        if (r != pr) {
+          if (pr >= 0) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double xs = ld(&in[iz * nxy + rc[k]]) * scale;
-          if (xs != 0.0) atomicAdd(&yb[k][r], (unsigned long long)__double2ll_rn(w * xs));
+            for (int k = 0; k < 4; ++k)
+              if (pv[k] != 0) atomicAdd(&yb[k][pr], (unsigned long long)pv[k]);
+          }
+          pr = r;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) pv[k] = 0;
         }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pv[k] += __double2ll_rn(w * (ld(&in[iz * nxy + rc[k]]) * scale));
       });
+      if (pr >= 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (pv[k] != 0) atomicAdd(&yb[k][pr], (unsigned long long)pv[k]);
+      }
     }
   }
   count_updates(n_upd, cnt);
@@ -379,7 +403,7 @@ __global__ void __launch_bounds__(kWarpsS * 32, 8) bwd3d_sym_kernel(
       const T* yb[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) yb[k] = in + (long long)((i + k * q) % g.n_angles) * rpa;
-#pragma unroll
+#pragma unroll 1
       for (int j = 0; j < 4; ++j) {
         __syncwarp();
         const bool ok = fast::plan_column(g, a.C, a.S, cx[j], cy[j], status, sh[warp], sp[warp], lane);
