@@ -304,14 +304,22 @@ def run_ours(args):
     # the quarter-turn symmetry each evaluation serves 4 pixel-angles of the
     # workload, so units = pixel-angles / 4 (the workload-equivalent figure is
     # reported beside it).
-    from paper_2511_12235_b200.projector import quarter_symmetric
-    reuse = 4 if (quarter_symmetric(g) and not os.environ.get("CTSM_NO_SYMMETRY")) else 1
-    pixel_angles = g.n_x * g.n_y * g.n_z * g.n_angles / (world if world > 1 else 1)
-    units = pixel_angles / reuse
+    from paper_2511_12235_b200.projector import symmetry_order
+    reuse = symmetry_order(g)
+    npix = g.n_x * g.n_y * g.n_z
+    if reuse == 8:  # base angles 0..n/8 (the two self-symmetric ones reuse 4x)
+        n_eval = g.n_angles // 8 + 1
+    elif reuse == 4:
+        n_eval = g.n_angles // 4
+    else:
+        n_eval = g.n_angles
+    units = npix * n_eval / (world if world > 1 else 1)
+    reuse = g.n_angles / n_eval
     per_unit = F_REF["2d"] if g.is_2d() else F_REF["3d"]
     dom_ms = max(ms_f, ms_b)
     achieved = units * per_unit / (dom_ms * 1e-3) / 1e12
-    kname = ("fwd2d_sym" if reuse == 4 else "fwd2d") if ms_f >= ms_b else ("bwd2d_sym" if reuse == 4 else "bwd2d")
+    suffix = {8: "_d8", 4: "_sym"}.get(symmetry_order(g), "")
+    kname = ("fwd2d" if ms_f >= ms_b else "bwd2d") + suffix
     if not g.is_2d():
         kname = kname.replace("2d", "3d")
     roof = {"bound": "fp64", "kernel": kname,

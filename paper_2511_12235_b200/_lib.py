@@ -37,6 +37,7 @@ SIGNATURES = {
     "ctsm_bwd_mf": (_I, [_P, _GP, _I, _I, _I, _I, _P, _P, _P]),
     "ctsm_last_update_count": (_U64, [_P]),
     "ctsm_quarter_symmetric": (_I, [_GP]),
+    "ctsm_symmetry_order": (_I, [_GP]),
     "ctsm_fwd_mf_orbits": (_I, [_P, _GP, _I, _I, _I, _P, _P, _P]),
     "ctsm_bwd_mf_orbits": (_I, [_P, _GP, _I, _I, _I, _P, _P, _P]),
     "ctsm_invert_nonzero": (_I, [_P, _I, _U64, _P, _P]),

@@ -70,7 +70,7 @@ struct ctsm_ctx {
   unsigned long long* h_upd = nullptr;    // pinned mirror
   uint64_t last_updates = 0;
   double* h_red = nullptr;      // pinned
-  Buf angles, edges, cs, counts, scan, longrows, acc, part, base, tmp_a, tmp_b, tmp_c, tmp_d,
+  Buf angles, edges, cs, counts, scan, longrows, acc, part, base, alist, tmp_a, tmp_b, tmp_c, tmp_d,
       tmp_e, tmp_f;
 };
 
@@ -229,7 +229,7 @@ int ctsm_destroy(ctsm_ctx* ctx) {
   if (!ctx) return 0;
   cudaSetDevice(ctx->device);
   Buf* bufs[] = {&ctx->angles, &ctx->edges, &ctx->cs,    &ctx->counts, &ctx->scan,
-                 &ctx->longrows, &ctx->acc, &ctx->part, &ctx->base, &ctx->tmp_a, &ctx->tmp_b,  &ctx->tmp_c,
+                 &ctx->longrows, &ctx->acc, &ctx->part, &ctx->base, &ctx->alist, &ctx->tmp_a, &ctx->tmp_b,  &ctx->tmp_c,
                  &ctx->tmp_d, &ctx->tmp_e, &ctx->tmp_f};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
@@ -403,10 +403,49 @@ static bool quarter_symmetric(const ctsm_geometry* g) {
   const double span = g->angle_end - g->angle_start;
   return std::fabs(span - 2.0 * 3.14159265358979323846) <= 1e-12 * span;
 }
+// Dihedral (8-fold) symmetry, 2D only: additionally angle_start == 0 and
+// n_angles % 8 == 0, so the angle set is closed under reflection phi -> -phi
+// (the grid and the detector are centred). CTSM_NO_DIHEDRAL=1 caps the order at 4.
+static bool dihedral_disabled() {
+  const char* e = std::getenv("CTSM_NO_DIHEDRAL");
+  return e && e[0] && e[0] != '0';
+}
+static int symmetry_order(const ctsm_geometry* g) {
+  if (!quarter_symmetric(g)) return 1;
+  if (!dihedral_disabled() && g->n_z == 1 && g->n_det_z == 1 && g->angle_start == 0.0 &&
+      g->n_angles % 8 == 0)
+    return 8;
+  return 4;
+}
+// Base angle set of a symmetry order: [0, n/4) for 4, [0, n/8] for 8.
+static int base_limit(const ctsm_geometry* g, int order) {
+  return order == 8 ? g->n_angles / 8 + 1 : g->n_angles / 4;
+}
+// All angles of the orbits of `base` (ascending) -- the sinogram rows written.
+static std::vector<int> orbit_angles(const ctsm_geometry* g, int order,
+                                     const std::vector<int>& base) {
+  const int n = g->n_angles, q = n / 4;
+  std::vector<char> hit(n, 0);
+  for (int i : base)
+    for (int k = 0; k < 4; ++k) {
+      hit[(i + k * q) % n] = 1;
+      if (order == 8) hit[((n - i) % n + k * q) % n] = 1;
+    }
+  std::vector<int> out;
+  for (int a = 0; a < n; ++a)
+    if (hit[a]) out.push_back(a);
+  return out;
+}
 // Base angles (< n/4) of a shard closed under +n/4: (begin, end, step) with
 // end == n, begin < step and step dividing n/4. Returns false otherwise.
 static bool sym_base_of_shard(const ctsm_geometry* g, int begin, int end, int step,
                               std::vector<int>* base) {
+  if (symmetry_order(g) == 8) {  // only the full range is closed under reflection
+    if (begin != 0 || end != g->n_angles || step != 1) return false;
+    base->clear();
+    for (int i = 0; i < base_limit(g, 8); ++i) base->push_back(i);
+    return true;
+  }
   const int q = g->n_angles / 4;
   if (end != g->n_angles || step <= 0 || begin >= step || q % step != 0) return false;
   base->clear();
@@ -425,6 +464,34 @@ static int upload_base(ctsm_ctx* ctx, const DevGeom& d, const std::vector<int>& 
   return 0;
 }
 
+// Dihedral forward: base angles in [0, n/8], rows of all their D4 images.
+static int fwd_d8_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d, int dtype,
+                       const std::vector<int>& base, double mx, const void* x, void* y,
+                       cudaStream_t st) {
+  const uint64_t n_meas = (uint64_t)d.rows_per_angle * g->n_angles;
+  const int nb = (int)base.size();
+  if (nb == 0) return 0;
+  const std::vector<int> rows = orbit_angles(g, 8, base);
+  CT_TRY(ensure(ctx, ctx->alist, rows.size() * sizeof(int)));
+  CT_CUDA(cudaMemcpyAsync(ctx->alist.p, rows.data(), rows.size() * sizeof(int),
+                          cudaMemcpyHostToDevice, st));
+  CT_TRY(upload_base(ctx, d, base, st));  // synchronizes: rows may go out of scope
+  CT_TRY(ensure(ctx, ctx->acc, n_meas * sizeof(unsigned long long)));
+  unsigned long long* acc = (unsigned long long*)ctx->acc.p;
+  const int* al = (const int*)ctx->alist.p;
+  const int nl = (int)rows.size();
+  CT_CUDA(rows_list(d, dtype, al, nl, acc, 1.0, nullptr, 0, st));
+  const double B = mx * row_sum_bound(g) * 1.05;
+  const double scale = B > 0.0 ? std::ldexp(1.0, 61) / B : 1.0;
+  CT_CUDA(cudaMemsetAsync(ctx->n_upd, 0, sizeof(unsigned long long), st));
+  CT_CUDA(fwd_mf_d8(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, x, acc,
+                    scale, ctx->n_upd, ctx->status, st));
+  CT_CUDA(rows_list(d, dtype, al, nl, acc, scale, y, 1, st));
+  CT_CUDA(cudaMemcpyAsync(ctx->h_upd, ctx->n_upd, sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, st));
+  return 0;
+}
+
 // Symmetric forward over the orbit shard of `base` (rows of angles b + k n/4).
 static int fwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d, int dtype,
                         const std::vector<int>& base, int base_step, const void* x, void* y,
@@ -433,6 +500,7 @@ static int fwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d,
   double mx = 0.0;
   CT_TRY(fetch_max_abs(ctx, dtype, (uint64_t)d.n_vox, x, st, &mx));
   if (!std::isfinite(mx)) return fail(CTSM_ERR_NON_FINITE, "image not finite");
+  if (symmetry_order(g) == 8) return fwd_d8_impl(ctx, g, d, dtype, base, mx, x, y, st);
   CT_TRY(upload_base(ctx, d, base, st));
   CT_TRY(ensure(ctx, ctx->acc, n_meas * sizeof(unsigned long long)));
   unsigned long long* acc = (unsigned long long*)ctx->acc.p;
@@ -461,7 +529,12 @@ static int bwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d,
   CT_TRY(upload_base(ctx, d, base, st));
   const int nb = (int)base.size();
   const bool two_d = (g->n_z == 1 && g->n_det_z == 1);
-  if (two_d) {
+  if (symmetry_order(g) == 8) {
+    const int nc = bwd_d8_chunks(d, nb);
+    if (nc > 1) CT_TRY(ensure(ctx, ctx->part, (size_t)nc * g->n_x * g->n_y * sizeof(double)));
+    CT_CUDA(bwd_mf_d8(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, y, x,
+                      (double*)ctx->part.p, nc, ctx->status, st));
+  } else if (two_d) {
     const int nc = bwd_sym_chunks(d, nb);
     if (nc > 1) CT_TRY(ensure(ctx, ctx->part, (size_t)nc * g->n_x * g->n_y * sizeof(double)));
     CT_CUDA(bwd_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, y, x,
@@ -539,14 +612,20 @@ int ctsm_quarter_symmetric(const ctsm_geometry* g) {
   return quarter_symmetric(g) ? 1 : 0;
 }
 
+int ctsm_symmetry_order(const ctsm_geometry* g) {
+  DevGeom d;
+  if (dev_geom(g, &d) != 0) return 1;
+  return symmetry_order(g);
+}
+
 static int orbit_base(const ctsm_geometry* g, int base_begin, int base_step,
                       std::vector<int>* base) {
   if (!quarter_symmetric(g))
     return fail(CTSM_ERR_INVALID_SPEC, "orbit shards need a quarter-turn symmetric scan");
-  const int q = g->n_angles / 4;
+  const int lim = base_limit(g, symmetry_order(g));
   if (base_begin < 0 || base_step <= 0) return fail(CTSM_ERR_INVALID_SPEC, "bad orbit shard");
   base->clear();
-  for (int i = base_begin; i < q; i += base_step) base->push_back(i);
+  for (int i = base_begin; i < lim; i += base_step) base->push_back(i);
   return 0;
 }
 

@@ -64,6 +64,17 @@ int bwd_sym_chunks(const DevGeom& g, int n_base);
 cudaError_t bwd_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                        int n_base, const void* y, void* x, double* part, int n_chunks,
                        int* status, cudaStream_t st);
+// Dihedral (8-fold) variants: base angles 0 <= i <= n/8 (2D only).
+cudaError_t fwd_mf_d8(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
+                      int n_base, const void* x, unsigned long long* yacc, double scale,
+                      unsigned long long* n_upd, int* status, cudaStream_t st);
+int bwd_d8_chunks(const DevGeom& g, int n_base);
+cudaError_t bwd_mf_d8(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
+                      int n_base, const void* y, void* x, double* part, int n_chunks,
+                      int* status, cudaStream_t st);
+// mode 0: zero the fixed-point rows of the listed angles; mode 1: convert them
+cudaError_t rows_list(const DevGeom& g, int dtype, const int* angles, int n_list,
+                      unsigned long long* acc, double scale, void* y, int mode, cudaStream_t st);
 cudaError_t fwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                          int n_base, const void* x, unsigned long long* yacc, double scale,
                          unsigned long long* n_upd, int* status, cudaStream_t st);

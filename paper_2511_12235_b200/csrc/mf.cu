@@ -299,6 +299,147 @@ __global__ void __launch_bounds__(128) bwd2d_sym_kernel(
   }
 }
 
+// ---- dihedral (8-fold) symmetric 2D kernels --------------------------------
+// With additionally angle_start == 0 and n_angles % 8 == 0, the reflection M
+// (y -> -y) maps the scan onto itself too: angle i -> n - i, pixel
+// (ix, iy) -> (ix, n-1-iy), detector cell m -> -1-m. The dihedral group D4 =
+// {R^k M^f} has 8 elements e = k + 4 f acting on pixels (apply M if f, then R
+// k times), angles (i -> (f ? -i : i) + k n/4) and cells (m -> f ? -1-m : m),
+// with w(e p, e i, e m) = w(p, i, m). Weights are evaluated at the base angles
+// 0 <= i <= n/8 only; the two self-symmetric base angles 0 and n/8 use the 4
+// rotations (their reflections coincide with rotations).
+__device__ __forceinline__ void d4_pixel(int n, int ix, int iy, int e, int& ox, int& oy) {
+  int x = ix, y = (e >= 4) ? n - 1 - iy : iy;
+  for (int r = 0; r < (e & 3); ++r) {
+    const int t = x;
+    x = n - 1 - y;
+    y = t;
+  }
+  ox = x;
+  oy = y;
+}
+__device__ __forceinline__ int d4_angle(int n_angles, int i, int e) {
+  const int q = n_angles / 4;
+  const int b = (e >= 4) ? (n_angles - i) % n_angles : i;
+  return (b + (e & 3) * q) % n_angles;
+}
+// composition g o h (apply h, then g)
+__host__ __device__ constexpr int d4_compose(int g, int h) {
+  return ((((g & 3) + ((g >= 4) ? (4 - (h & 3)) : (h & 3))) & 3) + 4 * (((g >> 2) ^ (h >> 2)) & 1));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) fwd2d_d8_kernel(
+    DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
+    const T* __restrict__ x, unsigned long long* __restrict__ yacc, double scale,
+    unsigned long long* n_upd, int* status) {
+  const int tiles_x = (g.n_x + kTx - 1) / kTx;
+  const int ix = (blockIdx.x % tiles_x) * kTx + (threadIdx.x % kTx);
+  const int iy = (blockIdx.x / tiles_x) * kTy + (threadIdx.x / kTx);
+  unsigned cnt = 0;
+  if (ix < g.n_x && iy < g.n_y) {
+    const int n = g.n_x;
+    double xs[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      int rx, ry;
+      d4_pixel(n, ix, iy, e, rx, ry);
+      xs[e] = ld(&x[(long long)ry * n + rx]) * scale;
+    }
+    const int k0 = blockIdx.y * kFwdAngles;
+    const int k1 = min(k0 + kFwdAngles, n_base);
+    for (int kk = k0; kk < k1; ++kk) {
+      const AngleCS a = cs[kk];
+      const int i = base[kk];
+      const bool full = (i != 0) && (8 * i != g.n_angles);
+      unsigned long long* rows[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        rows[e] = yacc + (long long)d4_angle(g.n_angles, i, e) * g.rows_per_angle + g.n_det_y / 2;
+      fast::pixel_weights(g, a.C, a.S, ix, iy, status, [&](int m, double w) {
+        cnt += full ? 8 : 4;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (xs[e] != 0.0) atomicAdd(&rows[e][m], (unsigned long long)__double2ll_rn(w * xs[e]));
+        if (full) {
+#pragma unroll
+          for (int e = 4; e < 8; ++e)
+            if (xs[e] != 0.0)
+              atomicAdd(&rows[e][-1 - m], (unsigned long long)__double2ll_rn(w * xs[e]));
+        }
+      });
+    }
+  }
+  count_updates(n_upd, cnt);
+}
+
+// Backward: thread = D4 orbit of a pixel p0 of the fundamental triangle
+// (iy0 <= ix0 < n/2); members p_h = h p0 (the 4 rotations only when p0 lies
+// on the diagonal, whose reflections coincide with rotations). The weight set
+// of member h at base angle i is gathered against angle g i, cell g m for
+// every group element g into the accumulator of pixel (g o h) p0.
+template <typename T>
+__global__ void __launch_bounds__(128) bwd2d_d8_kernel(
+    DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
+    int chunk, const T* __restrict__ y, T* __restrict__ x, double* __restrict__ part,
+    int* status) {
+  const int h = g.n_x / 2;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)h * (h + 1) / 2) return;
+  // triangular index -> (ix0 >= iy0)
+  int ix0 = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((long long)(ix0 + 1) * (ix0 + 2) / 2 <= t) ++ix0;
+  while ((long long)ix0 * (ix0 + 1) / 2 > t) --ix0;
+  const int iy0 = (int)(t - (long long)ix0 * (ix0 + 1) / 2);
+  const bool diag = (ix0 == iy0);
+  const int n = g.n_x;
+  int px[8], py[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) d4_pixel(n, ix0, iy0, e, px[e], py[e]);
+  double acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+  const int k0 = blockIdx.y * chunk;
+  const int k1 = min(k0 + chunk, n_base);
+  for (int kk = k0; kk < k1; ++kk) {
+    const AngleCS a = cs[kk];
+    const int i = base[kk];
+    const bool full = (i != 0) && (8 * i != g.n_angles);
+    const T* rows[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      rows[e] = y + (long long)d4_angle(g.n_angles, i, e) * g.rows_per_angle + g.n_det_y / 2;
+#pragma unroll
+    for (int hm = 0; hm < 8; ++hm) {
+      if (hm >= 4 && diag) continue;
+      fast::pixel_weights(g, a.C, a.S, px[hm], py[hm], status, [&](int m, double w) {
+#pragma unroll
+        for (int ge = 0; ge < 4; ++ge) acc[d4_compose(ge, hm)] += w * ld(&rows[ge][m]);
+        if (full) {
+#pragma unroll
+          for (int ge = 4; ge < 8; ++ge) acc[d4_compose(ge, hm)] += w * ld(&rows[ge][-1 - m]);
+        }
+      });
+    }
+  }
+  const long long npix = (long long)n * n;
+  auto put = [&](int e, double v) {
+    const long long pix = (long long)py[e] * n + px[e];
+    if (part)
+      part[(long long)blockIdx.y * npix + pix] = v;
+    else
+      x[pix] = (T)v;
+  };
+  if (diag) {
+    // pixel of e equals pixel of e o (R M) (= e o 5): fold the aliases
+#pragma unroll
+    for (int e = 0; e < 4; ++e) put(e, acc[e] + acc[d4_compose(e, 5)]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) put(e, acc[e]);
+  }
+}
+
 // 3D quarter-turn symmetric forward: warp = column c, base angles only; each
 // weight of c at base angle i is scattered to the rows of angles i + k n/4
 // with the voxel values of the rotated columns R^k c.
@@ -651,6 +792,86 @@ cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const i
   else
     bwd3d_sym_kernel<float><<<blocks, kWarpsS * 32, 0, st>>>(g, cs, base, n_base,
                                                             (const float*)y, (float*)x, status);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t fwd_mf_d8(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
+                      int n_base, const void* x, unsigned long long* yacc, double scale,
+                      unsigned long long* n_upd, int* status, cudaStream_t st) {
+  if (n_base <= 0) return cudaSuccess;
+  const dim3 grid = tile_grid(g, (unsigned)((n_base + kFwdAngles - 1) / kFwdAngles));
+  if (dtype == CTSM_F64)
+    fwd2d_d8_kernel<double><<<grid, 128, 0, st>>>(g, cs, base, n_base, (const double*)x, yacc,
+                                                  scale, n_upd, status);
+  else
+    fwd2d_d8_kernel<float><<<grid, 128, 0, st>>>(g, cs, base, n_base, (const float*)x, yacc,
+                                                 scale, n_upd, status);
+  count_launch();
+  return cudaGetLastError();
+}
+
+int bwd_d8_chunks(const DevGeom& g, int n_base) {
+  const long long h = g.n_x / 2;
+  const long long blocks = (h * (h + 1) / 2 + 127) / 128;
+  long long c = (16LL * 148 * 6 + blocks - 1) / blocks;
+  if (c > n_base) c = n_base;
+  if (c > 64) c = 64;
+  return (int)(c < 1 ? 1 : c);
+}
+
+cudaError_t bwd_mf_d8(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
+                      int n_base, const void* y, void* x, double* part, int n_chunks,
+                      int* status, cudaStream_t st) {
+  const long long h = g.n_x / 2;
+  const unsigned blocks = (unsigned)((h * (h + 1) / 2 + 127) / 128);
+  const int chunk = (n_base + n_chunks - 1) / (n_chunks > 0 ? n_chunks : 1);
+  const int nc = chunk > 0 ? (n_base + chunk - 1) / chunk : 1;
+  double* p = nc > 1 ? part : nullptr;
+  const dim3 grid(blocks, (unsigned)(nc > 0 ? nc : 1));
+  if (dtype == CTSM_F64)
+    bwd2d_d8_kernel<double><<<grid, 128, 0, st>>>(g, cs, base, n_base, chunk, (const double*)y,
+                                                  (double*)x, p, status);
+  else
+    bwd2d_d8_kernel<float><<<grid, 128, 0, st>>>(g, cs, base, n_base, chunk, (const float*)y,
+                                                 (float*)x, p, status);
+  count_launch();
+  if (nc > 1) {
+    const long long np = (long long)g.n_x * g.n_y;
+    if (dtype == CTSM_F64)
+      bwd_reduce_kernel<double><<<grid_for(np), 256, 0, st>>>(np, nc, part, (double*)x);
+    else
+      bwd_reduce_kernel<float><<<grid_for(np), 256, 0, st>>>(np, nc, part, (float*)x);
+    count_launch();
+  }
+  return cudaGetLastError();
+}
+
+// fixed-point rows of an explicit angle list (zero / convert)
+template <typename T>
+__global__ void rows_list_kernel(int rpa, const int* angles, int n_list, unsigned long long* acc,
+                                 double inv_scale, T* y, int mode) {
+  const long long n = (long long)rpa * n_list;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = (long long)angles[i / rpa] * rpa + (i % rpa);
+    if (mode == 0)
+      acc[r] = 0ull;
+    else
+      y[r] = (T)((double)(long long)acc[r] * inv_scale);
+  }
+}
+
+cudaError_t rows_list(const DevGeom& g, int dtype, const int* angles, int n_list,
+                      unsigned long long* acc, double scale, void* y, int mode, cudaStream_t st) {
+  const uint64_t n = (uint64_t)g.rows_per_angle * n_list;
+  if (n == 0) return cudaSuccess;
+  if (dtype == CTSM_F64)
+    rows_list_kernel<double><<<grid_for(n), 256, 0, st>>>(g.rows_per_angle, angles, n_list, acc,
+                                                          1.0 / scale, (double*)y, mode);
+  else
+    rows_list_kernel<float><<<grid_for(n), 256, 0, st>>>(g.rows_per_angle, angles, n_list, acc,
+                                                         1.0 / scale, (float*)y, mode);
   count_launch();
   return cudaGetLastError();
 }

@@ -25,9 +25,10 @@ from .geometry import ScanGeometry
 
 
 def angle_shard(g: ScanGeometry, rank: int, world: int, symmetric: Optional[bool] = None):
-    """Rank's angle shard. Quarter-turn symmetric scans are sharded by orbits
-    ("orbits", rank, world): base angles rank, rank + world, ... < n/4 and
-    their quarter-turn images, so every rank keeps the 4x weight reuse;
+    """Rank's angle shard. Symmetric scans are sharded by orbits
+    ("orbits", rank, world): base angles rank, rank + world, ... (< n/4, or
+    <= n/8 for dihedral scans) and their images under the symmetry group, so
+    every rank keeps the 4x / 8x weight reuse;
     otherwise the strided shard (rank, n_angles, world)."""
     if symmetric is None:
         try:
@@ -40,12 +41,25 @@ def angle_shard(g: ScanGeometry, rank: int, world: int, symmetric: Optional[bool
     return rank, g.n_angles, world
 
 
-def shard_angles(g: ScanGeometry, shard) -> torch.Tensor:
-    """Angle indices of a shard, ascending."""
+def _symmetry_order(g: ScanGeometry) -> int:
+    from .projector import symmetry_order
+    return symmetry_order(g)
+
+
+def shard_angles(g: ScanGeometry, shard, order: Optional[int] = None) -> torch.Tensor:
+    """Angle indices of a shard, ascending. Orbit shards of a dihedral (order
+    8) scan take base angles from [0, n/8] and add their reflections
+    i -> n - i; quarter-turn (order 4) ones from [0, n/4)."""
     if shard[0] == "orbits":
-        q = g.n_angles // 4
-        base = torch.arange(shard[1], q, shard[2])
-        return torch.sort(torch.cat([base + k * q for k in range(4)])).values
+        n = g.n_angles
+        q = n // 4
+        order = _symmetry_order(g) if order is None else order
+        lim = n // 8 + 1 if order == 8 else q
+        base = torch.arange(shard[1], lim, shard[2])
+        if order == 8:
+            base = torch.cat([base, (n - base) % n])
+        allb = torch.cat([(base + k * q) % n for k in range(4)])
+        return torch.unique(allb)  # sorted
     a0, a1, st = shard
     return torch.arange(a0, a1, st)
 

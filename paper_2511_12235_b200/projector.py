@@ -144,6 +144,14 @@ def quarter_symmetric(g: ScanGeometry) -> bool:
     return bool(_lib.lib().ctsm_quarter_symmetric(ctypes.byref(g.to_c())))
 
 
+def symmetry_order(g: ScanGeometry) -> int:
+    """8 (dihedral: quarter turns and the reflection phi -> -phi; 2D scans
+    starting at angle 0 with n_angles % 8 == 0), 4 (quarter turns) or 1: the
+    number of (pixel, angle) pairs each weight evaluation of the matrix-free
+    kernels serves."""
+    return int(_lib.lib().ctsm_symmetry_order(ctypes.byref(g.to_c())))
+
+
 def _angle_shard(g: ScanGeometry, angles):
     """(begin, end, step) or ("orbits", base_begin, base_step)."""
     if isinstance(angles, tuple) and len(angles) == 3 and angles[0] == "orbits":

@@ -247,3 +247,48 @@ def test_symmetric_path_matches_general(name, monkeypatch):
     if shard[2] == 1:
         assert rel_err(yo.cpu().numpy(), ys.cpu().numpy()) <= 1e-12
         assert rel_err(xo.cpu().numpy(), xs.cpu().numpy()) <= 1e-12
+
+
+# ---- dihedral (8-fold) symmetric 2D path ----------------------------------------
+@pytest.mark.parametrize("name", ["c1", "wide24", "odd_det"])
+def test_dihedral_path_matches_quarter_and_general(name, monkeypatch):
+    """The dihedral kernels (8x weight reuse: quarter turns + reflection)
+    reproduce the quarter-turn and the general kernels to rounding; orbit
+    shards over the dihedral base set tile the scan."""
+    from paper_2511_12235_b200.projector import symmetry_order
+    if name == "c1":
+        g = CONFIGS["c1"]
+    elif name == "wide24":
+        g = TEST_GEOMETRIES["wide2d"].with_(n_angles=24)
+    else:  # fewer detector cells than the shadow: clipped cells on both sides
+        g = TEST_GEOMETRIES["wide2d"].with_(n_angles=16, n_det_y=60)
+    assert symmetry_order(g) == 8
+    gen = torch.Generator().manual_seed(4)
+    x = torch.rand(g.n_voxels, generator=gen, dtype=torch.float64).cuda()
+    y = torch.rand(g.n_measurements, generator=gen, dtype=torch.float64).cuda()
+    res = {}
+    for mode in ("d8", "quarter", "general"):
+        monkeypatch.delenv("CTSM_NO_DIHEDRAL", raising=False)
+        monkeypatch.delenv("CTSM_NO_SYMMETRY", raising=False)
+        if mode == "quarter":
+            monkeypatch.setenv("CTSM_NO_DIHEDRAL", "1")
+            assert symmetry_order(g) == 4
+        elif mode == "general":
+            monkeypatch.setenv("CTSM_NO_SYMMETRY", "1")
+        res[mode] = (forward_project_matrix_free(g, "consistent", 1, x).cpu().numpy(),
+                     back_project_matrix_free(g, "consistent", 1, y).cpu().numpy())
+    monkeypatch.delenv("CTSM_NO_SYMMETRY", raising=False)
+    for other in ("quarter", "general"):
+        assert rel_err(res["d8"][0], res[other][0]) <= 1e-12
+        assert rel_err(res["d8"][1], res[other][1]) <= 1e-12
+    # f32 through the dihedral kernels
+    yf = forward_project_matrix_free(g, "consistent", 1, x.float()).cpu().numpy()
+    assert rel_err(yf, res["general"][0]) <= 1e-5
+    # orbit shards of 3 "ranks" add up to the full projections
+    yo = torch.zeros(g.n_measurements, dtype=torch.float64, device="cuda")
+    xo = torch.zeros(g.n_voxels, dtype=torch.float64, device="cuda")
+    for r in range(3):
+        forward_project_matrix_free(g, "consistent", 1, x, angles=("orbits", r, 3), out=yo)
+        xo += back_project_matrix_free(g, "consistent", 1, y, angles=("orbits", r, 3))
+    assert rel_err(yo.cpu().numpy(), res["d8"][0]) <= 1e-12
+    assert rel_err(xo.cpu().numpy(), res["d8"][1]) <= 1e-12

@@ -106,3 +106,12 @@ def test_shard_rows_partition(symmetric):
     world = 2
     rows = torch.cat([shard_rows(g, angle_shard(g, r, world, symmetric)) for r in range(world)])
     assert torch.equal(torch.sort(rows).values, torch.arange(g.n_measurements))
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+@pytest.mark.parametrize("order", [4, 8])
+def test_orbit_shards_partition_angles(world, order):
+    from paper_2511_12235_b200.dist import shard_angles
+    g = TEST_GEOMETRIES["wide2d"].with_(n_angles=48)
+    got = torch.cat([shard_angles(g, ("orbits", r, world), order) for r in range(world)])
+    assert torch.equal(torch.sort(got).values, torch.arange(g.n_angles))
