@@ -482,7 +482,10 @@ static int fwd_d8_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d, 
   const int nl = (int)rows.size();
   CT_CUDA(rows_list(d, dtype, al, nl, acc, 1.0, nullptr, 0, st));
   const double B = mx * row_sum_bound(g) * 1.05;
-  const double scale = B > 0.0 ? std::ldexp(1.0, 61) / B : 1.0;
+  double scale = B > 0.0 ? std::ldexp(1.0, 61) / B : 1.0;
+  // the kernel's shared-memory limbs need every contribution |w x| scale
+  // below 2^47 (f64) / 2^23 (f32); weights are area fractions <= 1
+  if (mx > 0.0) scale = std::min(scale, std::ldexp(1.0, dtype == CTSM_F64 ? 47 : 23) / (mx * 1.001));
   CT_CUDA(cudaMemsetAsync(ctx->n_upd, 0, sizeof(unsigned long long), st));
   CT_CUDA(fwd_mf_d8(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, x, acc,
                     scale, ctx->n_upd, ctx->status, st));

@@ -319,13 +319,40 @@ __device__ __forceinline__ void d4_pixel(int n, int ix, int iy, int e, int& ox, 
   oy = y;
 }
 __device__ __forceinline__ int d4_angle(int n_angles, int i, int e) {
-  const int q = n_angles / 4;
-  const int b = (e >= 4) ? (n_angles - i) % n_angles : i;
-  return (b + (e & 3) * q) % n_angles;
+  // 0 <= i <= n/8: no integer division
+  const int b = (e >= 4 && i != 0) ? n_angles - i : i;
+  const int r = b + (e & 3) * (n_angles >> 2);
+  return r >= n_angles ? r - n_angles : r;
 }
 // composition g o h (apply h, then g)
 __host__ __device__ constexpr int d4_compose(int g, int h) {
   return ((((g & 3) + ((g >= 4) ? (4 - (h & 3)) : (h & 3))) & 3) + 4 * (((g >> 2) ^ (h >> 2)) & 1));
+}
+
+// Forward: block = 16x8 pixel tile x a chunk of base angles. The tile's cell
+// weights of one base angle are summed in a shared-memory window of detector
+// cells (fixed point, exact integer adds) shared by the 8 images -- image e's
+// cell is m or -1-m -- and flushed once per cell to global memory: ~10x fewer
+// global atomics than one per weight. The window [clo, clo + W) is the
+// projection of the tile's corners (same t expressions as the pixel sweeps),
+// computed identically by every thread; a tile whose shadow exceeds the window
+// falls back to direct global atomics. Shared memory has no native 64-bit
+// atomic add, so the host caps the fixed-point scale so that every single
+// contribution is below 2^47 (f64; 2^23 for f32) -- a resolution of 2^-47
+// max|x| per weight, far below the f64 rounding of the sums -- and the window
+// holds 32-bit limbs: the low 24 bits and the signed rest (f64), or one signed
+// limb (f32). With <= 128 adds per cell (one per tile pixel) no limb
+// overflows; the flush recombines them exactly into the 64-bit accumulator.
+constexpr int kD8Angles = 8;
+constexpr int kD8Win = 64;
+template <int L>
+__device__ __forceinline__ void limb_add(unsigned* w, long long v) {
+  if (L == 1) {
+    atomicAdd(w, (unsigned)v);
+  } else {
+    atomicAdd(w, (unsigned)(v & 0xFFFFFF));
+    atomicAdd(w + kD8Win, (unsigned)(v >> 24));
+  }
 }
 
 template <typename T>
@@ -333,41 +360,96 @@ __global__ void __launch_bounds__(128) fwd2d_d8_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
     const T* __restrict__ x, unsigned long long* __restrict__ yacc, double scale,
     unsigned long long* n_upd, int* status) {
+  constexpr int L = sizeof(T) == 8 ? 2 : 1;  // limbs per window cell
+  __shared__ unsigned win[2][8][L][kD8Win];
+  for (int j = threadIdx.x; j < 2 * 8 * L * kD8Win; j += blockDim.x) (&win[0][0][0][0])[j] = 0u;
   const int tiles_x = (g.n_x + kTx - 1) / kTx;
-  const int ix = (blockIdx.x % tiles_x) * kTx + (threadIdx.x % kTx);
-  const int iy = (blockIdx.x / tiles_x) * kTy + (threadIdx.x / kTx);
+  const int tx0 = (blockIdx.x % tiles_x) * kTx, ty0 = (blockIdx.x / tiles_x) * kTy;
+  const int ix = tx0 + (threadIdx.x % kTx);
+  const int iy = ty0 + (threadIdx.x / kTx);
+  const int n = g.n_x;
+  const bool inside = ix < n && iy < g.n_y;
+  double xs[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    int rx, ry;
+    d4_pixel(n, ix, iy, e, rx, ry);
+    xs[e] = inside ? ld(&x[(long long)ry * n + rx]) * scale : 0.0;
+  }
+  // tile corners (world coordinates)
+  const double X0 = (tx0 - n / 2.0) * g.a, X1 = (min(tx0 + kTx, n) - n / 2.0) * g.a;
+  const double Y0 = (ty0 - g.n_y / 2.0) * g.b, Y1 = (min(ty0 + kTy, g.n_y) - g.n_y / 2.0) * g.b;
+  const int cell_lo = -g.n_det_y / 2, cell_hi = g.n_det_y / 2 - 1;
+  const long long rpa = g.rows_per_angle;
   unsigned cnt = 0;
-  if (ix < g.n_x && iy < g.n_y) {
-    const int n = g.n_x;
-    double xs[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      int rx, ry;
-      d4_pixel(n, ix, iy, e, rx, ry);
-      xs[e] = ld(&x[(long long)ry * n + rx]) * scale;
+  __syncthreads();
+  const int k0 = blockIdx.y * kD8Angles;
+  const int k1 = min(k0 + kD8Angles, n_base);
+  for (int kk = k0; kk < k1; ++kk) {
+    const int buf = (kk - k0) & 1;
+    const AngleCS a = cs[kk];
+    const int i = base[kk];
+    const bool full = (i != 0) && (8 * i != g.n_angles);
+    // shadow of the tile: t over the 4 corners (depths checked by the sweeps)
+    double tmin, tmax;
+    {
+      const double s = g.s;
+      const double t0 = (Y0 * a.C - X0 * a.S) * fast::frcp(s - X0 * a.C - Y0 * a.S);
+      const double t1 = (Y0 * a.C - X1 * a.S) * fast::frcp(s - X1 * a.C - Y0 * a.S);
+      const double t2 = (Y1 * a.C - X1 * a.S) * fast::frcp(s - X1 * a.C - Y1 * a.S);
+      const double t3 = (Y1 * a.C - X0 * a.S) * fast::frcp(s - X0 * a.C - Y1 * a.S);
+      tmin = fmin(fmin(t0, t1), fmin(t2, t3));
+      tmax = fmax(fmax(t0, t1), fmax(t2, t3));
     }
-    const int k0 = blockIdx.y * kFwdAngles;
-    const int k1 = min(k0 + kFwdAngles, n_base);
-    for (int kk = k0; kk < k1; ++kk) {
-      const AngleCS a = cs[kk];
-      const int i = base[kk];
-      const bool full = (i != 0) && (8 * i != g.n_angles);
-      unsigned long long* rows[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        rows[e] = yacc + (long long)d4_angle(g.n_angles, i, e) * g.rows_per_angle + g.n_det_y / 2;
+    const int clo = max((int)floor(tmin * g.u_scale) - 1, cell_lo);
+    const int chi = min((int)ceil(tmax * g.u_scale) + 1, cell_hi);
+    const int W = chi - clo + 1;
+    const bool use_win = W <= kD8Win;
+    if (inside) {
+      unsigned* wb = &win[buf][0][0][0] - clo;
       fast::pixel_weights(g, a.C, a.S, ix, iy, status, [&](int m, double w) {
         cnt += full ? 8 : 4;
+        if (use_win) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (xs[e] != 0.0) atomicAdd(&rows[e][m], (unsigned long long)__double2ll_rn(w * xs[e]));
-        if (full) {
+          for (int e = 0; e < 8; ++e)
+            if (e < 4 || full)
+              limb_add<L>(wb + e * L * kD8Win + m, __double2ll_rn(w * xs[e]));
+        } else {
 #pragma unroll
-          for (int e = 4; e < 8; ++e)
-            if (xs[e] != 0.0)
-              atomicAdd(&rows[e][-1 - m], (unsigned long long)__double2ll_rn(w * xs[e]));
+          for (int e = 0; e < 8; ++e)
+            if (e < 4 || full) {
+              unsigned long long* row =
+                  yacc + (long long)d4_angle(g.n_angles, i, e) * rpa + g.n_det_y / 2;
+              atomicAdd(row + (e >= 4 ? -1 - m : m),
+                        (unsigned long long)__double2ll_rn(w * xs[e]));
+            }
         }
       });
+    }
+    __syncthreads();
+    if (use_win) {
+#pragma unroll
+      for (int j0 = 0; j0 < 8 * kD8Win; j0 += 128) {
+        const int j = j0 + threadIdx.x;
+        const int e = j / kD8Win, c = j % kD8Win;
+        if (c < W && (e < 4 || full)) {
+          unsigned long long v;
+          if (L == 1) {
+            v = (unsigned long long)(long long)(int)win[buf][e][0][c];
+          } else {
+            v = (unsigned long long)win[buf][e][0][c] +
+                ((unsigned long long)(long long)(int)win[buf][e][L - 1][c] << 24);
+            win[buf][e][L - 1][c] = 0u;
+          }
+          win[buf][e][0][c] = 0u;
+          if (v) {
+            const int m = clo + c;
+            unsigned long long* row =
+                yacc + (long long)d4_angle(g.n_angles, i, e) * rpa + g.n_det_y / 2;
+            atomicAdd(row + (e >= 4 ? -1 - m : m), v);
+          }
+        }
+      }
     }
   }
   count_updates(n_upd, cnt);
@@ -800,7 +882,7 @@ cudaError_t fwd_mf_d8(const DevGeom& g, int dtype, const AngleCS* cs, const int*
                       int n_base, const void* x, unsigned long long* yacc, double scale,
                       unsigned long long* n_upd, int* status, cudaStream_t st) {
   if (n_base <= 0) return cudaSuccess;
-  const dim3 grid = tile_grid(g, (unsigned)((n_base + kFwdAngles - 1) / kFwdAngles));
+  const dim3 grid = tile_grid(g, (unsigned)((n_base + kD8Angles - 1) / kD8Angles));
   if (dtype == CTSM_F64)
     fwd2d_d8_kernel<double><<<grid, 128, 0, st>>>(g, cs, base, n_base, (const double*)x, yacc,
                                                   scale, n_upd, status);

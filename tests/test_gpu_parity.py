@@ -250,7 +250,7 @@ def test_symmetric_path_matches_general(name, monkeypatch):
 
 
 # ---- dihedral (8-fold) symmetric 2D path ----------------------------------------
-@pytest.mark.parametrize("name", ["c1", "wide24", "odd_det"])
+@pytest.mark.parametrize("name", ["c1", "wide24", "odd_det", "fine_det"])
 def test_dihedral_path_matches_quarter_and_general(name, monkeypatch):
     """The dihedral kernels (8x weight reuse: quarter turns + reflection)
     reproduce the quarter-turn and the general kernels to rounding; orbit
@@ -260,8 +260,10 @@ def test_dihedral_path_matches_quarter_and_general(name, monkeypatch):
         g = CONFIGS["c1"]
     elif name == "wide24":
         g = TEST_GEOMETRIES["wide2d"].with_(n_angles=24)
-    else:  # fewer detector cells than the shadow: clipped cells on both sides
+    elif name == "odd_det":  # fewer detector cells than the shadow: clipped cells
         g = TEST_GEOMETRIES["wide2d"].with_(n_angles=16, n_det_y=60)
+    else:  # tile shadows wider than the forward kernel's shared-memory window
+        g = TEST_GEOMETRIES["wide2d"].with_(n_angles=16, d_y=0.25, n_det_y=1000)
     assert symmetry_order(g) == 8
     gen = torch.Generator().manual_seed(4)
     x = torch.rand(g.n_voxels, generator=gen, dtype=torch.float64).cuda()
