@@ -42,7 +42,8 @@ F_REF = {"2d": 247.0, "3d": 1513.0}
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--steps", type=int, default=None,
+                   help="timed steps (default: 50 for proj, 5 for sirt, 3 for csr)")
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c1")
@@ -52,7 +53,10 @@ def parse():
     p.add_argument("--mode", default="proj", choices=["proj", "sirt", "csr"],
                    help="proj: one A x + A^T y per step; sirt: one SIRT iteration per step "
                         "(BASELINE configs[4]: y = A x_true + 1%% noise)")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.steps is None:
+        a.steps = {"proj": 50, "sirt": 5, "csr": 3}[a.mode]
+    return a
 
 
 def dist_env():
@@ -147,7 +151,7 @@ class ClockSampler:
         if not enabled:
             return
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
@@ -157,6 +161,19 @@ class ClockSampler:
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        # wait (<= 5 s) for the sampler's first line so the timed region is covered
+        t_end = time.time() + 5.0
+        while time.time() < t_end and os.path.getsize(self.path) == 0:
+            time.sleep(0.02)
+        self.t0 = self.t1 = None
+
+    def mark(self, start: bool):
+        """Wall-clock bounds of the timed region (samples outside are dropped)."""
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
 
     def stop(self):
         if self.proc is None:
@@ -167,24 +184,30 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         self.fh.close()
-        sms, maxs, reasons = [], [], set()
+        import datetime
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for line in open(self.path):
             f = [v.strip() for v in line.split(",")]
             if len(f) < 9:
                 continue
             try:
-                sms.append(float(f[1]))
-                maxs.append(float(f[2]))
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(f[1]), float(f[2]),
+                             {n for n, v in zip(names, f[5:9]) if v.lower().startswith("active")}))
             except ValueError:
                 continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        if not sms:
+        if not rows:
             return None
-        return {"sm_mhz": float(np.median(sms)), "sm_max_mhz": float(max(maxs)),
-                "reasons": sorted(reasons), "samples": len(sms)}
+        t0 = self.t0 if self.t0 is not None else rows[0][0]
+        t1 = self.t1 if self.t1 is not None else rows[-1][0]
+        inside = [r for r in rows if t0 - 0.025 <= r[0] <= t1 + 0.025]
+        sel = inside or [min(rows, key=lambda r: abs(r[0] - 0.5 * (t0 + t1)))]
+        reasons = set().union(*(r[3] for r in sel))
+        return {"sm_mhz": float(np.median([r[1] for r in sel])),
+                "sm_max_mhz": float(max(r[2] for r in sel)),
+                "reasons": sorted(reasons), "samples": len(inside),
+                "timed_region_s": round(t1 - t0, 4)}
 
 
 def run_ours(args):
@@ -236,6 +259,7 @@ def run_ours(args):
         dist.barrier()
     launches0 = _lib.launch_count()
     t_total = t_fwd = t_bwd = 0.0
+    clocks.mark(True)
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -246,6 +270,7 @@ def run_ours(args):
         t_fwd += ev_f0.elapsed_time(ev_f1)
         t_bwd += ev_f1.elapsed_time(ev_b1)
     launches = _lib.launch_count() - launches0
+    clocks.mark(False)
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -460,6 +485,7 @@ def run_sirt(args):
         dist.barrier()
     launches0 = _lib.launch_count()
     ms_total = 0.0
+    clocks.mark(True)
     for _ in range(args.steps):
         torch.cuda.synchronize()
         ev0.record()
@@ -468,6 +494,7 @@ def run_sirt(args):
         torch.cuda.synchronize()
         ms_total += ev0.elapsed_time(ev1)
     launches = _lib.launch_count() - launches0
+    clocks.mark(False)
     clk = clocks.stop()
     ms = ms_total / args.steps
     cnt = torch.tensor([float(_lib.lib().ctsm_last_update_count(ctx.handle)), ms],
@@ -525,6 +552,7 @@ def run_csr(args):
     clocks = ClockSampler(0, not args.no_clocks)
     launches0 = _lib.launch_count()
     ms = 0.0
+    clocks.mark(True)
     for _ in range(args.steps):
         w = None
         torch.cuda.synchronize()
@@ -534,6 +562,7 @@ def run_csr(args):
         torch.cuda.synchronize()
         ms += ev0.elapsed_time(ev1)
     launches = _lib.launch_count() - launches0
+    clocks.mark(False)
     ms /= args.steps
     nnz = w.nnz()
     x = torch.from_numpy(phantom_for(cfg, g, dtype=np.float64 if g.is_2d() else np.float32)).double().to(dev)

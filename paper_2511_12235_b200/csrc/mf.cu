@@ -487,21 +487,39 @@ __global__ void __launch_bounds__(128) bwd2d_d8_kernel(
     const AngleCS a = cs[kk];
     const int i = base[kk];
     const bool full = (i != 0) && (8 * i != g.n_angles);
-    const T* rows[8];
+    // 2D sinograms are < 2^31 entries: 32-bit row offsets
+    int rows[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e)
-      rows[e] = y + (long long)d4_angle(g.n_angles, i, e) * g.rows_per_angle + g.n_det_y / 2;
+      rows[e] = d4_angle(g.n_angles, i, e) * g.rows_per_angle + g.n_det_y / 2;
+    // one inlined sweep for all members (small code: the member loop is not
+    // unrolled); tsum[ge] collects member hm's sums per group element and is
+    // folded into acc[ge o hm] by a static permutation per member.
+    const int n_mem = diag ? 4 : 8;
+#pragma unroll 1
+    for (int hm = 0; hm < n_mem; ++hm) {
+      int mx, my;
+      d4_pixel(n, ix0, iy0, hm, mx, my);
+      double tsum[8];
 #pragma unroll
-    for (int hm = 0; hm < 8; ++hm) {
-      if (hm >= 4 && diag) continue;
-      fast::pixel_weights(g, a.C, a.S, px[hm], py[hm], status, [&](int m, double w) {
+      for (int e = 0; e < 8; ++e) tsum[e] = 0.0;
+      fast::pixel_weights(g, a.C, a.S, mx, my, status, [&](int m, double w) {
 #pragma unroll
-        for (int ge = 0; ge < 4; ++ge) acc[d4_compose(ge, hm)] += w * ld(&rows[ge][m]);
+        for (int ge = 0; ge < 4; ++ge) tsum[ge] += w * ld(&y[rows[ge] + m]);
         if (full) {
 #pragma unroll
-          for (int ge = 4; ge < 8; ++ge) acc[d4_compose(ge, hm)] += w * ld(&rows[ge][-1 - m]);
+          for (int ge = 4; ge < 8; ++ge) tsum[ge] += w * ld(&y[rows[ge] - 1 - m]);
         }
       });
+      switch (hm) {
+#define CTSM_FOLD(H)                                                      \
+  case H:                                                                 \
+    _Pragma("unroll") for (int ge = 0; ge < 8; ++ge) acc[d4_compose(ge, H)] += tsum[ge]; \
+    break;
+        CTSM_FOLD(0) CTSM_FOLD(1) CTSM_FOLD(2) CTSM_FOLD(3)
+        CTSM_FOLD(4) CTSM_FOLD(5) CTSM_FOLD(6) CTSM_FOLD(7)
+#undef CTSM_FOLD
+      }
     }
   }
   const long long npix = (long long)n * n;
