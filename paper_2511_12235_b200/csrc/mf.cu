@@ -345,18 +345,24 @@ __host__ __device__ constexpr int d4_compose(int g, int h) {
 // overflows; the flush recombines them exactly into the 64-bit accumulator.
 constexpr int kD8Angles = 8;
 constexpr int kD8Win = 64;
+// w * xs rounded to the nearest integer (|.| < 2^47) by the 1.5 * 2^52 shift:
+// the low 51 mantissa bits then hold the integer + 2^51 -- one DFMA instead of
+// a 64-bit float->int conversion.
 template <int L>
-__device__ __forceinline__ void limb_add(unsigned* w, long long v) {
+__device__ __forceinline__ void limb_add(unsigned* w, double wv, double xsv) {
+  const double sh = fma(wv, xsv, 6755399441055744.0);  // 1.5 * 2^52
+  const unsigned lo = (unsigned)__double2loint(sh);
   if (L == 1) {
-    atomicAdd(w, (unsigned)v);
+    atomicAdd(w, lo);  // |value| < 2^23: the low word is its two's complement
   } else {
-    atomicAdd(w, (unsigned)(v & 0xFFFFFF));
-    atomicAdd(w + kD8Win, (unsigned)(v >> 24));
+    const unsigned hi = (unsigned)__double2hiint(sh) & 0xFFFFFu;
+    atomicAdd(w, lo & 0xFFFFFFu);
+    atomicAdd(w + kD8Win, ((lo >> 24) | (hi << 8)) - (1u << 27));  // (value >> 24), signed
   }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(128) fwd2d_d8_kernel(
+__global__ void __launch_bounds__(128, 6) fwd2d_d8_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
     const T* __restrict__ x, unsigned long long* __restrict__ yacc, double scale,
     unsigned long long* n_upd, int* status) {
@@ -413,7 +419,7 @@ __global__ void __launch_bounds__(128) fwd2d_d8_kernel(
 #pragma unroll
           for (int e = 0; e < 8; ++e)
             if (e < 4 || full)
-              limb_add<L>(wb + e * L * kD8Win + m, __double2ll_rn(w * xs[e]));
+              limb_add<L>(wb + e * L * kD8Win + m, w, xs[e]);
         } else {
 #pragma unroll
           for (int e = 0; e < 8; ++e)
@@ -461,7 +467,7 @@ __global__ void __launch_bounds__(128) fwd2d_d8_kernel(
 // of member h at base angle i is gathered against angle g i, cell g m for
 // every group element g into the accumulator of pixel (g o h) p0.
 template <typename T>
-__global__ void __launch_bounds__(128) bwd2d_d8_kernel(
+__global__ void __launch_bounds__(128, 6) bwd2d_d8_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
     int chunk, const T* __restrict__ y, T* __restrict__ x, double* __restrict__ part,
     int* status) {
