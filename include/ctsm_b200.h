@@ -121,9 +121,9 @@ int ctsm_bwd_mf(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begi
  * quarter-turn images -- the load-balanced multi-GPU sharding of such scans.
  * ctsm_quarter_symmetric returns 1 if the scan qualifies.
  *
- * 2D scans that additionally start at angle 0 with n_angles % 8 == 0 are
- * also symmetric under the reflection phi -> -phi (dihedral group of order
- * 8; disable with CTSM_NO_DIHEDRAL=1): then only the full scan is detected
+ * Scans that additionally start at angle 0 with n_angles % 8 == 0 are also
+ * symmetric under the reflection phi -> -phi, y -> -y (dihedral group of
+ * order 8; disable with CTSM_NO_DIHEDRAL=1): then only the full scan is detected
  * automatically and the orbit base set is {0 <= i <= n_angles / 8} with each
  * base angle's 8 images (4 for i = 0 and i = n_angles / 8).
  * ctsm_symmetry_order returns 8, 4 or 1. */

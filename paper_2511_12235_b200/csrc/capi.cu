@@ -403,7 +403,7 @@ static bool quarter_symmetric(const ctsm_geometry* g) {
   const double span = g->angle_end - g->angle_start;
   return std::fabs(span - 2.0 * 3.14159265358979323846) <= 1e-12 * span;
 }
-// Dihedral (8-fold) symmetry, 2D only: additionally angle_start == 0 and
+// Dihedral (8-fold) symmetry: additionally angle_start == 0 and
 // n_angles % 8 == 0, so the angle set is closed under reflection phi -> -phi
 // (the grid and the detector are centred). CTSM_NO_DIHEDRAL=1 caps the order at 4.
 static bool dihedral_disabled() {
@@ -412,8 +412,7 @@ static bool dihedral_disabled() {
 }
 static int symmetry_order(const ctsm_geometry* g) {
   if (!quarter_symmetric(g)) return 1;
-  if (!dihedral_disabled() && g->n_z == 1 && g->n_det_z == 1 && g->angle_start == 0.0 &&
-      g->n_angles % 8 == 0)
+  if (!dihedral_disabled() && g->angle_start == 0.0 && g->n_angles % 8 == 0)
     return 8;
   return 4;
 }
@@ -485,10 +484,16 @@ static int fwd_d8_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d, 
   double scale = B > 0.0 ? std::ldexp(1.0, 61) / B : 1.0;
   // the kernel's shared-memory limbs need every contribution |w x| scale
   // below 2^47 (f64) / 2^23 (f32); weights are area fractions <= 1
-  if (mx > 0.0) scale = std::min(scale, std::ldexp(1.0, dtype == CTSM_F64 ? 47 : 23) / (mx * 1.001));
+  const bool two_d = (g->n_z == 1 && g->n_det_z == 1);
+  if (two_d && mx > 0.0)
+    scale = std::min(scale, std::ldexp(1.0, dtype == CTSM_F64 ? 47 : 23) / (mx * 1.001));
   CT_CUDA(cudaMemsetAsync(ctx->n_upd, 0, sizeof(unsigned long long), st));
-  CT_CUDA(fwd_mf_d8(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, x, acc,
-                    scale, ctx->n_upd, ctx->status, st));
+  if (two_d)
+    CT_CUDA(fwd_mf_d8(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, x, acc,
+                      scale, ctx->n_upd, ctx->status, st));
+  else
+    CT_CUDA(fwd3d_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, x,
+                         acc, scale, ctx->n_upd, ctx->status, st, 8));
   CT_CUDA(rows_list(d, dtype, al, nl, acc, scale, y, 1, st));
   CT_CUDA(cudaMemcpyAsync(ctx->h_upd, ctx->n_upd, sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, st));
@@ -519,7 +524,7 @@ static int fwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d,
                        scale, ctx->n_upd, ctx->status, st));
   else
     CT_CUDA(fwd3d_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, x,
-                         acc, scale, ctx->n_upd, ctx->status, st));
+                         acc, scale, ctx->n_upd, ctx->status, st, 4));
   for (int k = 0; k < 4; ++k)
     CT_CUDA(fixed_to_float_rows(d, dtype, base[0] + k * q, base_step, nb, acc, scale, y, st));
   CT_CUDA(cudaMemcpyAsync(ctx->h_upd, ctx->n_upd, sizeof(unsigned long long),
@@ -532,19 +537,19 @@ static int bwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d,
   CT_TRY(upload_base(ctx, d, base, st));
   const int nb = (int)base.size();
   const bool two_d = (g->n_z == 1 && g->n_det_z == 1);
-  if (symmetry_order(g) == 8) {
+  if (!two_d) {
+    CT_CUDA(bwd3d_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, y, x,
+                         ctx->status, st, symmetry_order(g)));
+  } else if (symmetry_order(g) == 8) {
     const int nc = bwd_d8_chunks(d, nb);
     if (nc > 1) CT_TRY(ensure(ctx, ctx->part, (size_t)nc * g->n_x * g->n_y * sizeof(double)));
     CT_CUDA(bwd_mf_d8(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, y, x,
                       (double*)ctx->part.p, nc, ctx->status, st));
-  } else if (two_d) {
+  } else {
     const int nc = bwd_sym_chunks(d, nb);
     if (nc > 1) CT_TRY(ensure(ctx, ctx->part, (size_t)nc * g->n_x * g->n_y * sizeof(double)));
     CT_CUDA(bwd_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, y, x,
                        (double*)ctx->part.p, nc, ctx->status, st));
-  } else {
-    CT_CUDA(bwd3d_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, y, x,
-                         ctx->status, st));
   }
   return 0;
 }

@@ -64,7 +64,8 @@ int bwd_sym_chunks(const DevGeom& g, int n_base);
 cudaError_t bwd_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                        int n_base, const void* y, void* x, double* part, int n_chunks,
                        int* status, cudaStream_t st);
-// Dihedral (8-fold) variants: base angles 0 <= i <= n/8 (2D only).
+// Dihedral (8-fold) 2D variants: base angles 0 <= i <= n/8 (3D: order 8 of
+// fwd3d_mf_sym / bwd3d_mf_sym).
 cudaError_t fwd_mf_d8(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                       int n_base, const void* x, unsigned long long* yacc, double scale,
                       unsigned long long* n_upd, int* status, cudaStream_t st);
@@ -77,9 +78,10 @@ cudaError_t rows_list(const DevGeom& g, int dtype, const int* angles, int n_list
                       unsigned long long* acc, double scale, void* y, int mode, cudaStream_t st);
 cudaError_t fwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                          int n_base, const void* x, unsigned long long* yacc, double scale,
-                         unsigned long long* n_upd, int* status, cudaStream_t st);
+                         unsigned long long* n_upd, int* status, cudaStream_t st, int order);
 cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
-                         int n_base, const void* y, void* x, int* status, cudaStream_t st);
+                         int n_base, const void* y, void* x, int* status, cudaStream_t st,
+                         int order);
 cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
                    int angle_step, int n_sel, const void* x, unsigned long long* yacc,
                    double scale, unsigned long long* n_upd, int* status, cudaStream_t st);

@@ -546,126 +546,181 @@ __global__ void __launch_bounds__(128, 6) bwd2d_d8_kernel(
   }
 }
 
-// 3D quarter-turn symmetric forward: warp = column c, base angles only; each
-// weight of c at base angle i is scattered to the rows of angles i + k n/4
-// with the voxel values of the rotated columns R^k c.
-template <typename T>
-__global__ void __launch_bounds__(kWarps3 * 32, 4) fwd3d_sym_kernel(
+// 3D symmetric forward (group order G = 4: quarter turns, base angles < n/4;
+// G = 8: dihedral, base angles 0..n/8, see the 2D kernels above): warp =
+// column c, base angles only; each weight of c at base angle i is scattered
+// to the rows of the image angles e i (image detector column -1-m_y for the
+// reflections) with the voxel values of the image columns e c.
+//
+// The voxel values of the G image columns are staged in shared memory once
+// per z-block ([image][slot][lane], conflict-free) and reused for all base
+// angles: the per-weight reads are shared-memory hits instead of G scattered
+// global loads.
+constexpr int kZcF = 8;  // z-block of 256 voxels for the staged values
+
+template <typename T, int G>
+constexpr size_t fwd3d_sym_dyn_smem() { return sizeof(T) * kWarps3 * G * kZcF * 32; }
+
+template <typename T, int G>
+__global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? 3 : 4) fwd3d_sym_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
     const T* __restrict__ in, unsigned long long* __restrict__ yacc, double scale,
     unsigned long long* n_upd, int* status) {
   __shared__ fast::ColumnHead sh[kWarps3];
   __shared__ fast::PieceCoef sp[kWarps3][fast::kMaxPieces];
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  T(*xsm)[G][kZcF][32] = reinterpret_cast<T(*)[G][kZcF][32]>(dyn_smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = g.n_x;
   const long long nxy = (long long)n * g.n_y;
   const long long col = (long long)blockIdx.x * kWarps3 + warp;
   if (col >= nxy) return;  // whole warp
   const int ix = (int)(col % n), iy = (int)(col / n);
-  long long rc[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    int rx, ry;
-    rot_pixel(n, ix, iy, k, rx, ry);
-    rc[k] = (long long)ry * n + rx;
-  }
-  const int rpa = g.rows_per_angle, q = g.n_angles / 4;
+  const int rpa = g.rows_per_angle, ndy = g.n_det_y;
   const int hy = g.n_det_y / 2, hz = g.n_det_z / 2;
   unsigned cnt = 0;
-  for (int zb0 = 0; zb0 < g.n_z; zb0 += 32 * kZcMax) {
-    const int nzb = min(32 * kZcMax, g.n_z - zb0);
+  for (int zb0 = 0; zb0 < g.n_z; zb0 += 32 * kZcF) {
+    const int nzb = min(32 * kZcF, g.n_z - zb0);
     const int zc = (nzb + 31) / 32;
     const int z0 = zb0 + lane * zc, z1 = min(z0 + zc, zb0 + nzb);
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < G; ++e) {
+      int rx, ry;
+      d4_pixel(n, ix, iy, e, rx, ry);
+      const T* src = in + (long long)ry * n + rx;
+      for (int t = 0; t < zc; ++t)
+        xsm[warp][e][t][lane] = (z0 + t < z1) ? src[(long long)(z0 + t) * nxy] : (T)0;
+    }
+    __syncwarp();
     for (int kk = 0; kk < n_base; ++kk) {
       const int i = base[kk];
       const AngleCS a = cs[kk];
+      const bool full = G == 4 || ((i != 0) && (8 * i != g.n_angles));
+      const int ne = full ? G : 4;
       __syncwarp();
       const bool ok = fast::plan_column(g, a.C, a.S, ix, iy, status, sh[warp], sp[warp], lane);
       __syncwarp();
       if (!ok) continue;
-      unsigned long long* yb[4];
+      // pending merge of consecutive emits to one row (see proj3d_kernel):
+      // row pr = (mz + hz) ndy + py, py = my + hy; reflections write -1-my
+      long long pr = -1, pv[G];
+      int py = 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) yb[k] = yacc + (long long)((i + k * q) % g.n_angles) * rpa;
-      long long pr = -1, pv[4] = {0, 0, 0, 0};  // pending merge (see proj3d_kernel)
-      fast::chunk_weights(g, sh[warp], sp[warp], z0, z1, [&](int iz, int my, int mz, double w) {
-        cnt += 4;
-        const long long r = (long long)(mz + hz) * g.n_det_y + (my + hy);
-        if (r != pr) {
-          if (pr >= 0) {
+      for (int e = 0; e < G; ++e) pv[e] = 0;
+      auto flush = [&]() {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              if (pv[k] != 0) atomicAdd(&yb[k][pr], (unsigned long long)pv[k]);
+        for (int e = 0; e < G; ++e)
+          if (e < ne && pv[e] != 0) {
+            const long long r = (e < 4) ? pr : pr + ndy - 1 - 2 * py;
+            atomicAdd(yacc + (long long)d4_angle(g.n_angles, i, e) * rpa + r,
+                      (unsigned long long)pv[e]);
           }
+      };
+      fast::chunk_weights(g, sh[warp], sp[warp], z0, z1, [&](int iz, int my, int mz, double w) {
+        cnt += ne;
+        const long long r = (long long)(mz + hz) * ndy + (my + hy);
+        if (r != pr) {
+          if (pr >= 0) flush();
           pr = r;
+          py = my + hy;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) pv[k] = 0;
+          for (int e = 0; e < G; ++e) pv[e] = 0;
         }
+        const double ws = w * scale;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) pv[k] += __double2ll_rn(w * (ld(&in[iz * nxy + rc[k]]) * scale));
+        for (int e = 0; e < G; ++e)
+          if (e < ne) pv[e] += __double2ll_rn(ws * (double)xsm[warp][e][iz - z0][lane]);
       });
-      if (pr >= 0) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (pv[k] != 0) atomicAdd(&yb[k][pr], (unsigned long long)pv[k]);
-      }
+      if (pr >= 0) flush();
     }
   }
   count_updates(n_upd, cnt);
 }
 
-// 3D quarter-turn symmetric backward: warp = orbit {c, Rc, R^2c, R^3c} of a
-// first-quadrant column; per base angle the four members are planned in turn
-// and every weight set is gathered against the four image angles into the
-// shared-memory accumulators of the matching orbit member (fixed order).
+// 3D symmetric backward: warp = orbit of a column of the fundamental domain
+// (G = 4: first quadrant, members R^j c; G = 8: triangle iy0 <= ix0 < n/2,
+// members h c, the 4 rotations only on the diagonal). Per base angle the
+// members are planned in turn and every weight set of member h is gathered
+// against the image angles e i into the shared-memory accumulator of member
+// e o h (fixed order: deterministic).
 constexpr int kWarpsS = 2;
 constexpr int kZcS = 8;
 
-template <typename T>
+template <typename T, int G>
 __global__ void __launch_bounds__(kWarpsS * 32, 8) bwd3d_sym_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
     const T* __restrict__ in, T* __restrict__ xout, int* status) {
   __shared__ fast::ColumnHead sh[kWarpsS];
   __shared__ fast::PieceCoef sp[kWarpsS][fast::kMaxPieces];
-  __shared__ double sacc[kWarpsS][4][kZcS][32];
+  __shared__ double sacc[kWarpsS][G][kZcS][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = g.n_x, h = n / 2;
   const long long orb = (long long)blockIdx.x * kWarpsS + warp;
-  if (orb >= (long long)h * h) return;  // whole warp
-  const int ix0 = (int)(orb % h), iy0 = (int)(orb / h);
-  int cx[4], cy[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) rot_pixel(n, ix0, iy0, j, cx[j], cy[j]);
+  int ix0, iy0;
+  if (G == 4) {
+    if (orb >= (long long)h * h) return;  // whole warp
+    ix0 = (int)(orb % h);
+    iy0 = (int)(orb / h);
+  } else {
+    if (orb >= (long long)h * (h + 1) / 2) return;
+    ix0 = (int)((sqrt(8.0 * (double)orb + 1.0) - 1.0) * 0.5);
+    while ((long long)(ix0 + 1) * (ix0 + 2) / 2 <= orb) ++ix0;
+    while ((long long)ix0 * (ix0 + 1) / 2 > orb) --ix0;
+    iy0 = (int)(orb - (long long)ix0 * (ix0 + 1) / 2);
+  }
+  const bool diag = G == 8 && ix0 == iy0;
+  const int n_mem = (G == 4 || diag) ? 4 : 8;
   const long long nxy = (long long)n * g.n_y;
-  const int rpa = g.rows_per_angle, q = g.n_angles / 4;
+  const int rpa = g.rows_per_angle;
   const int hy = g.n_det_y / 2, hz = g.n_det_z / 2;
   for (int zb0 = 0; zb0 < g.n_z; zb0 += 32 * kZcS) {
     const int nzb = min(32 * kZcS, g.n_z - zb0);
     const int zc = (nzb + 31) / 32;
     const int z0 = zb0 + lane * zc, z1 = min(z0 + zc, zb0 + nzb);
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < G; ++j)
       for (int t = 0; t < zc; ++t) sacc[warp][j][t][lane] = 0.0;
     for (int kk = 0; kk < n_base; ++kk) {
       const int i = base[kk];
       const AngleCS a = cs[kk];
-      const T* yb[4];
+      const bool full = G == 4 || ((i != 0) && (8 * i != g.n_angles));
+      const T* yb[G];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) yb[k] = in + (long long)((i + k * q) % g.n_angles) * rpa;
+      for (int e = 0; e < G; ++e)
+        yb[e] = in + (long long)d4_angle(g.n_angles, i, e) * rpa;
 #pragma unroll 1
-      for (int j = 0; j < 4; ++j) {
+      for (int hm = 0; hm < n_mem; ++hm) {
+        int cx, cy;
+        d4_pixel(n, ix0, iy0, hm, cx, cy);
         __syncwarp();
-        const bool ok = fast::plan_column(g, a.C, a.S, cx[j], cy[j], status, sh[warp], sp[warp], lane);
+        const bool ok = fast::plan_column(g, a.C, a.S, cx, cy, status, sh[warp], sp[warp], lane);
         __syncwarp();
         if (!ok) continue;
+        int slot[G];
+#pragma unroll
+        for (int e = 0; e < G; ++e) slot[e] = d4_compose(e, hm);
         fast::chunk_weights(g, sh[warp], sp[warp], z0, z1, [&](int iz, int my, int mz, double w) {
           const long long r = (long long)(mz + hz) * g.n_det_y + (my + hy);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) sacc[warp][(j + k) & 3][iz - z0][lane] += w * ld(&yb[k][r]);
+          for (int e = 0; e < 4; ++e) sacc[warp][slot[e]][iz - z0][lane] += w * ld(&yb[e][r]);
+          if (G == 8 && full) {
+            const long long rr = r + g.n_det_y - 1 - 2 * (my + hy);
+#pragma unroll
+            for (int e = 4; e < G; ++e) sacc[warp][slot[e]][iz - z0][lane] += w * ld(&yb[e][rr]);
+          }
         });
       }
     }
-    for (int j = 0; j < 4; ++j) {
-      const long long c = (long long)cy[j] * n + cx[j];
-      for (int iz = z0; iz < z1; ++iz) xout[iz * nxy + c] = (T)sacc[warp][j][iz - z0][lane];
+    for (int e = 0; e < (diag ? 4 : G); ++e) {
+      int cx, cy;
+      d4_pixel(n, ix0, iy0, e, cx, cy);
+      const long long c = (long long)cy * n + cx;
+      const int e2 = d4_compose(e, 5);  // diagonal: e c == (e o 5) c
+      for (int iz = z0; iz < z1; ++iz) {
+        double v = sacc[warp][e][iz - z0][lane];
+        if (diag) v += sacc[warp][e2][iz - z0][lane];
+        xout[iz * nxy + c] = (T)v;
+      }
     }
   }
 }
@@ -871,33 +926,44 @@ cudaError_t fwd_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int
 
 cudaError_t fwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                          int n_base, const void* x, unsigned long long* yacc, double scale,
-                         unsigned long long* n_upd, int* status, cudaStream_t st) {
+                         unsigned long long* n_upd, int* status, cudaStream_t st, int order) {
   if (n_base <= 0) return cudaSuccess;
   const long long nxy = (long long)g.n_x * g.n_y;
   const unsigned blocks = (unsigned)((nxy + kWarps3 - 1) / kWarps3);
-  if (dtype == CTSM_F64)
-    fwd3d_sym_kernel<double><<<blocks, kWarps3 * 32, 0, st>>>(g, cs, base, n_base,
-                                                             (const double*)x, yacc, scale,
-                                                             n_upd, status);
-  else
-    fwd3d_sym_kernel<float><<<blocks, kWarps3 * 32, 0, st>>>(g, cs, base, n_base,
-                                                            (const float*)x, yacc, scale, n_upd,
-                                                            status);
+#define CTSM_LAUNCH(T, G)                                                                    \
+  do {                                                                                       \
+    constexpr size_t smem = fwd3d_sym_dyn_smem<T, G>();                                      \
+    cudaFuncSetAttribute(fwd3d_sym_kernel<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         (int)smem);                                                         \
+    fwd3d_sym_kernel<T, G><<<blocks, kWarps3 * 32, smem, st>>>(g, cs, base, n_base,           \
+                                                               (const T*)x, yacc, scale,      \
+                                                               n_upd, status);               \
+  } while (0)
+  if (dtype == CTSM_F64) {
+    if (order == 8) CTSM_LAUNCH(double, 8); else CTSM_LAUNCH(double, 4);
+  } else {
+    if (order == 8) CTSM_LAUNCH(float, 8); else CTSM_LAUNCH(float, 4);
+  }
+#undef CTSM_LAUNCH
   count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
-                         int n_base, const void* y, void* x, int* status, cudaStream_t st) {
+                         int n_base, const void* y, void* x, int* status, cudaStream_t st,
+                         int order) {
   const long long h = g.n_x / 2;
-  const unsigned blocks = (unsigned)((h * h + kWarpsS - 1) / kWarpsS);
-  if (dtype == CTSM_F64)
-    bwd3d_sym_kernel<double><<<blocks, kWarpsS * 32, 0, st>>>(g, cs, base, n_base,
-                                                             (const double*)y, (double*)x,
-                                                             status);
-  else
-    bwd3d_sym_kernel<float><<<blocks, kWarpsS * 32, 0, st>>>(g, cs, base, n_base,
-                                                            (const float*)y, (float*)x, status);
+  const long long n_orb = order == 8 ? h * (h + 1) / 2 : h * h;
+  const unsigned blocks = (unsigned)((n_orb + kWarpsS - 1) / kWarpsS);
+#define CTSM_LAUNCH(T, G)                                                                  \
+  bwd3d_sym_kernel<T, G><<<blocks, kWarpsS * 32, 0, st>>>(g, cs, base, n_base, (const T*)y, \
+                                                          (T*)x, status)
+  if (dtype == CTSM_F64) {
+    if (order == 8) CTSM_LAUNCH(double, 8); else CTSM_LAUNCH(double, 4);
+  } else {
+    if (order == 8) CTSM_LAUNCH(float, 8); else CTSM_LAUNCH(float, 4);
+  }
+#undef CTSM_LAUNCH
   count_launch();
   return cudaGetLastError();
 }

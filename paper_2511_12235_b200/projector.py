@@ -145,8 +145,8 @@ def quarter_symmetric(g: ScanGeometry) -> bool:
 
 
 def symmetry_order(g: ScanGeometry) -> int:
-    """8 (dihedral: quarter turns and the reflection phi -> -phi; 2D scans
-    starting at angle 0 with n_angles % 8 == 0), 4 (quarter turns) or 1: the
+    """8 (dihedral: quarter turns and the reflection phi -> -phi, y -> -y;
+    scans starting at angle 0 with n_angles % 8 == 0), 4 (quarter turns) or 1: the
     number of (pixel, angle) pairs each weight evaluation of the matrix-free
     kernels serves."""
     return int(_lib.lib().ctsm_symmetry_order(ctypes.byref(g.to_c())))

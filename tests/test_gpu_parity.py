@@ -250,7 +250,7 @@ def test_symmetric_path_matches_general(name, monkeypatch):
 
 
 # ---- dihedral (8-fold) symmetric 2D path ----------------------------------------
-@pytest.mark.parametrize("name", ["c1", "wide24", "odd_det", "fine_det"])
+@pytest.mark.parametrize("name", ["c1", "wide24", "odd_det", "fine_det", "cone16", "c2"])
 def test_dihedral_path_matches_quarter_and_general(name, monkeypatch):
     """The dihedral kernels (8x weight reuse: quarter turns + reflection)
     reproduce the quarter-turn and the general kernels to rounding; orbit
@@ -260,6 +260,10 @@ def test_dihedral_path_matches_quarter_and_general(name, monkeypatch):
         g = CONFIGS["c1"]
     elif name == "wide24":
         g = TEST_GEOMETRIES["wide2d"].with_(n_angles=24)
+    elif name == "cone16":  # 3D, 16 angles: base angles 0, 1, 2 (1 has all 8 images)
+        g = TEST_GEOMETRIES["cone3d"].with_(n_angles=16)
+    elif name == "c2":
+        g = CONFIGS["c2"]
     elif name == "odd_det":  # fewer detector cells than the shadow: clipped cells
         g = TEST_GEOMETRIES["wide2d"].with_(n_angles=16, n_det_y=60)
     else:  # tile shadows wider than the forward kernel's shared-memory window

@@ -19,12 +19,15 @@ n_ang = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 g = CONFIGS[cfg]
 x = torch.from_numpy(phantom_for(cfg, g, dtype=np.float32)).cuda()
 y = torch.rand(g.n_measurements, dtype=torch.float32, device="cuda")
-from paper_2511_12235_b200.projector import quarter_symmetric  # noqa: E402
+from paper_2511_12235_b200.dist import shard_angles  # noqa: E402
+from paper_2511_12235_b200.projector import symmetry_order  # noqa: E402
 
-if quarter_symmetric(g) and not os.environ.get("CTSM_NO_SYMMETRY"):
-    base_step = max(1, (g.n_angles // 4) // max(1, n_ang // 4))
-    shard = ("orbits", 0, base_step)  # base angles + their quarter-turn images
-    n_sel = 4 * len(range(0, g.n_angles // 4, base_step))
+order = symmetry_order(g)
+if order > 1:
+    n_base = g.n_angles // 8 + 1 if order == 8 else g.n_angles // 4
+    base_step = max(1, n_base // max(1, n_ang // order))
+    shard = ("orbits", 0, base_step)  # base angles + their images under the group
+    n_sel = len(shard_angles(g, shard, order))
 else:
     step = max(1, g.n_angles // n_ang)
     shard = (0, g.n_angles, step)
