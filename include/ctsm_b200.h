@@ -155,6 +155,47 @@ int ctsm_sirt_update(ctsm_ctx* ctx, int dtype, uint64_t n, const void* cinv_dev,
 int ctsm_sirt(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, const void* y_dev,
               void* x_inout_dev, int iters, void* stream);
 
+/* ---- reconstruction protocol on device -----------
+ * The solvers take a linear operator W: a device CSR matrix (K3/K4 appliers)
+ * or the fp64 matrix-free projector of a scan (K5/K6) times `scale` (the
+ * matrix-free analogue of scale_values). All vectors are fp64 device arrays;
+ * reductions are deterministic (fixed-order), so results repeat bit for bit.
+ */
+enum { CTSM_OP_CSR = 0, CTSM_OP_MATRIX_FREE = 1 };
+typedef struct ctsm_operator {
+  int kind;
+  int pad0;
+  uint64_t n_rows, n_cols;          /* CSR (ignored for matrix-free) */
+  const uint64_t* row_start;        /* CSR, device */
+  const uint32_t* col;              /* CSR, device */
+  const double* val;                /* CSR, device */
+  const ctsm_geometry* geom;        /* matrix-free */
+  double scale;                     /* matrix-free: W = scale * A (CSR: must be 1) */
+} ctsm_operator;
+
+/* spectral_norm_power (projector.cpp:262-280): v_inout holds the start vector
+ * (the caller's normal_samples(n_cols, seed)); it is normalised, then `iters`
+ * times v <- W^T W v / ||W^T W v||; *norm_out = sqrt(||W^T W v||) of the
+ * last iteration. ZeroMatrix for an empty matrix or a collapsed iteration. */
+int ctsm_spectral_norm_power(ctsm_ctx* ctx, const ctsm_operator* op, int iters,
+                             double* v_inout_dev, double* norm_out, void* stream);
+/* nag_tikhonov (solver.hpp:32-35, solver.cpp:17-75): minimises
+ * 0.5 ||W u - p||^2 + 0.5 lambda ||u||^2 by Nesterov's method with the fixed
+ * step 1 / (1 + lambda) (W scaled to unit spectral norm by the caller);
+ * stops when ||W^T (W u - p) + lambda u||^2 < tol. u_dev receives the
+ * iterate (starts at 0). trace_host, if not NULL, receives 3 doubles per
+ * iteration: {iter, objective, grad_norm_sq} (SolveTraceRow). InvalidConfig
+ * for negative lambda/tol/max_iter; NonFinite when the iterate diverges. */
+int ctsm_nag_tikhonov(ctsm_ctx* ctx, const ctsm_operator* op, const double* p_dev,
+                      double lambda, int max_iter, double tol, double* u_dev,
+                      double* trace_host, int* iterations, int* converged, void* stream);
+/* normal_samples (phantoms.cpp:78-87; host): mt19937_64(seed), Box-Muller
+ * cosine branch -- the start vector of spectral_norm_power. */
+void ctsm_normal_samples(uint64_t n, uint64_t seed, double* out_host);
+/* scale_values (projector.cpp:282-286) on a device value array. */
+int ctsm_scale_values(ctsm_ctx* ctx, uint64_t nnz, double* val_dev, double factor,
+                      void* stream);
+
 /* ---- host-buffer entry points (the reference's value-semantics calls,
  * used for end-to-end timing; copies in/out of pinned staging inside) ---- */
 int ctsm_forward_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,

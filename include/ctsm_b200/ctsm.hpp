@@ -114,6 +114,26 @@ double spectral_norm_power(const SparseSystemMatrix& w, int iters = 100, std::ui
 void scale_values(SparseSystemMatrix* w, double factor);
 std::vector<double> angle_column_sums(const ScanGeometry& g, MatrixMode mode, int k,
                                       int angle_index);
+// solver.hpp:10-35: Nesterov-accelerated Tikhonov least squares; the iteration
+// runs on the device (ctsm_nag_tikhonov).
+struct SolveOptions {
+  double lambda = 1e-4;
+  int max_iter = 1000;
+  double tol = 1e-9;
+};
+struct SolveTraceRow {
+  int iter;
+  double objective;
+  double grad_norm_sq;
+};
+struct SolveResult {
+  std::vector<double> u;
+  int iterations = 0;
+  bool converged = false;
+  std::vector<SolveTraceRow> trace;
+};
+SolveResult nag_tikhonov(const SparseSystemMatrix& w, const std::vector<double>& p,
+                         const SolveOptions& opt, bool keep_trace = false);
 // Addition: SIRT (BASELINE.json configs[4]) on one device.
 std::vector<double> sirt(const ScanGeometry& g, const std::vector<double>& y,
                          const std::vector<double>& x0, int iters);

@@ -140,6 +140,22 @@ class Oracle:
                                                       ctypes.c_int]
             L.ref_angle_block_entries_par.restype = ctypes.c_long
         L.ref_angle_column_sums.argtypes = [_P, ctypes.c_int, _P]
+        # reference-only entry points (solver / io / phantoms), absent in the ports
+        self.has_solver = hasattr(L, "ref_nag_tikhonov")
+        if self.has_solver:
+            L.ref_spectral_norm_power.argtypes = [_P, ctypes.c_int, ctypes.c_uint64, _P]
+            L.ref_scale_values.argtypes = [_P, ctypes.c_double]
+            L.ref_nag_tikhonov.argtypes = [_P, _P, ctypes.c_double, ctypes.c_int, ctypes.c_double,
+                                           _P, _P, _P, _P]
+            L.ref_write_matrix.argtypes = [_P, ctypes.c_char_p]
+            L.ref_read_matrix.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int)]
+            L.ref_read_matrix.restype = _P
+            L.ref_csr_cols.argtypes = [_P]
+            L.ref_csr_cols.restype = ctypes.c_uint64
+            L.ref_csr_meta.argtypes = [_P, _P, ctypes.c_uint64]
+            L.ref_csr_meta.restype = ctypes.c_uint64
+            L.ref_write_tensor.argtypes = [ctypes.c_char_p, _P, ctypes.c_int, _P]
+            L.ref_normal_samples.argtypes = [ctypes.c_uint64, ctypes.c_uint64, _P]
 
     # -- helpers -----------------------------------------------------------
     def _check(self, st: int):
@@ -264,6 +280,89 @@ class Oracle:
         self._check(self.lib.ref_sirt(p, _ptr(y), _ptr(x), iters, threads))
         return x
 
+    # -- reference solver / io (ref_* variants only) -------------------------
+    def _with_matrix(self, g, fn, budget: int = 5 << 30, threads: int = 1):
+        og, p = self._g(g)
+        st = ctypes.c_int(0)
+        h = self.lib.ref_build_system_matrix(p, threads, budget, ctypes.byref(st))
+        self._check(st.value)
+        try:
+            return fn(h)
+        finally:
+            self.lib.ref_csr_free(h)
+
+    def spectral_norm_power(self, g, iters: int = 100, seed: int = 7, scale: float = 1.0,
+                            threads: int = 1) -> float:
+        """build_system_matrix + (scale_values) + spectral_norm_power."""
+        def run(h):
+            if scale != 1.0:
+                self._check(self.lib.ref_scale_values(h, scale))
+            out = ctypes.c_double(0.0)
+            self._check(self.lib.ref_spectral_norm_power(h, iters, seed, ctypes.byref(out)))
+            return out.value
+        return self._with_matrix(g, run, threads=threads)
+
+    def nag_tikhonov(self, g, p, lam: float, max_iter: int, tol: float, scale: float = 1.0,
+                     keep_trace: bool = False, threads: int = 1):
+        """build_system_matrix + scale_values(scale) + nag_tikhonov ->
+        (u, iterations, converged, trace[n, 3] or None)."""
+        p = np.ascontiguousarray(p, np.float64)
+
+        def run(h):
+            if scale != 1.0:
+                self._check(self.lib.ref_scale_values(h, scale))
+            u = np.zeros(self.lib.ref_csr_cols(h), np.float64)
+            its, conv = ctypes.c_int(0), ctypes.c_int(0)
+            tr = np.zeros(3 * max(max_iter, 1)) if keep_trace else None
+            self._check(self.lib.ref_nag_tikhonov(h, _ptr(p), lam, max_iter, tol, _ptr(u),
+                                                  ctypes.byref(its), ctypes.byref(conv),
+                                                  _ptr(tr) if keep_trace else None))
+            trace = tr[:3 * its.value].reshape(-1, 3) if keep_trace else None
+            return u, its.value, bool(conv.value), trace
+        return self._with_matrix(g, run, threads=threads)
+
+    def back_project_csr(self, g, y, threads: int = 1) -> np.ndarray:
+        """build_system_matrix + back_project (projector.cpp:219-233)."""
+        y = np.ascontiguousarray(y, np.float64)
+        x = np.zeros(g.n_x * g.n_y * g.n_z, np.float64)
+        self._with_matrix(g, lambda h: self._check(self.lib.ref_back_project(h, _ptr(y), _ptr(x))),
+                          threads=threads)
+        return x
+
+    def write_matrix(self, g, path: str, threads: int = 1) -> None:
+        """build_system_matrix + write_matrix (CSM1, io.cpp:153-177)."""
+        self._with_matrix(g, lambda h: self._check(self.lib.ref_write_matrix(h, path.encode())),
+                          threads=threads)
+
+    def read_matrix(self, path: str):
+        """read_matrix (io.cpp:179-227) -> (Csr, n_cols, meta)."""
+        st = ctypes.c_int(0)
+        h = self.lib.ref_read_matrix(path.encode(), ctypes.byref(st))
+        self._check(st.value)
+        try:
+            nnz = self.lib.ref_csr_nnz(h)
+            rows = self.lib.ref_csr_rows(h)
+            rs = np.empty(rows + 1, np.uint64)
+            col = np.empty(nnz, np.uint32)
+            val = np.empty(nnz, np.float64)
+            self.lib.ref_csr_copy(h, _ptr(rs), _ptr(col), _ptr(val))
+            n = self.lib.ref_csr_meta(h, None, 0)
+            buf = ctypes.create_string_buffer(int(n))
+            self.lib.ref_csr_meta(h, ctypes.cast(buf, _P), n)
+            return Csr(rs, col, val), int(self.lib.ref_csr_cols(h)), buf.raw.decode()
+        finally:
+            self.lib.ref_csr_free(h)
+
+    def write_tensor(self, path: str, dims, data) -> None:
+        d = np.ascontiguousarray(dims, np.uint64)
+        x = np.ascontiguousarray(data, np.float64)
+        self._check(self.lib.ref_write_tensor(path.encode(), _ptr(d), int(d.size), _ptr(x)))
+
+    def normal_samples(self, n: int, seed: int) -> np.ndarray:
+        out = np.empty(n, np.float64)
+        self.lib.ref_normal_samples(n, seed, _ptr(out))
+        return out
+
     def angle_column_sums(self, g, ip: int) -> np.ndarray:
         og, p = self._g(g)
         s = np.zeros(g.n_x * g.n_y * g.n_z, np.float64)
@@ -278,3 +377,69 @@ def csr_forward(c: Csr, x: np.ndarray) -> np.ndarray:
     y = np.zeros(c.row_start.size - 1)
     np.add.at(y, rows, c.val * x[c.col])
     return y
+
+
+def csr_back(c: Csr, y: np.ndarray, n_cols: int) -> np.ndarray:
+    """Transpose scatter in row order, skipping y_r == 0 (projector.cpp:219-233):
+    np.add.at applies the adds in input order, i.e. the reference's order."""
+    rows = np.repeat(np.arange(c.row_start.size - 1), np.diff(c.row_start).astype(np.int64))
+    keep = y[rows] != 0.0
+    x = np.zeros(n_cols)
+    np.add.at(x, c.col[keep], c.val[keep] * y[rows[keep]])
+    return x
+
+
+def _seq_sum(a: np.ndarray) -> float:
+    """Left-to-right sum (the reference's accumulation loops)."""
+    return float(np.cumsum(a)[-1]) if a.size else 0.0
+
+
+def nag_tikhonov_np(c: Csr, n_cols: int, p: np.ndarray, lam: float, max_iter: int, tol: float,
+                    keep_trace: bool = False):
+    """numpy restatement of solver.cpp:17-75 (same expressions, sequential
+    sums) -> (u, iterations, converged, trace[n, 3] or None)."""
+    L = 1.0 + lam
+    q = csr_back(c, p, n_cols)
+    u = np.zeros(n_cols)
+    u_prev = np.zeros(n_cols)
+    h = np.zeros(n_cols)
+    h_prev = np.zeros(n_cols)
+    t = 1.0
+    its, conv, trace = 0, False, []
+    for it in range(max_iter):
+        t_next = (1.0 + np.sqrt(1.0 + 4.0 * t * t)) / 2.0
+        m = (t - 1.0) / t_next
+        y = (1.0 + m) * u - m * u_prev
+        grad = (1.0 + m) * (h + lam * u) - m * (h_prev + lam * u_prev) - q
+        u_prev = u
+        h_prev = h
+        u = y - grad / L
+        t = t_next
+        v = csr_forward(c, u)
+        h = csr_back(c, v, n_cols)
+        gi = h + lam * u - q
+        grad_sq = _seq_sum(gi * gi)
+        its = it + 1
+        if keep_trace:
+            r = v - p
+            trace.append((it + 1, 0.5 * _seq_sum(r * r) + 0.5 * lam * _seq_sum(u * u), grad_sq))
+        if not np.isfinite(grad_sq):
+            raise OracleError(6, "solver iterate diverged")
+        if grad_sq < tol:
+            conv = True
+            break
+    return u, its, conv, (np.array(trace) if keep_trace else None)
+
+
+def spectral_norm_power_np(c: Csr, n_cols: int, v0: np.ndarray, iters: int) -> float:
+    """numpy restatement of projector.cpp:262-280 from the start vector v0
+    (normal_samples(n_cols, seed))."""
+    v = v0 / np.sqrt(_seq_sum(v0 * v0))
+    lam = 0.0
+    for _ in range(iters):
+        u = csr_back(c, csr_forward(c, v), n_cols)
+        lam = np.sqrt(_seq_sum(u * u))
+        if lam == 0.0:
+            raise OracleError(7, "power iteration collapsed")
+        v = u / lam
+    return float(np.sqrt(lam))

@@ -24,7 +24,10 @@
 #include <vector>
 
 #include "ctsm/geometry.hpp"
+#include "ctsm/io.hpp"
+#include "ctsm/phantoms.hpp"
 #include "ctsm/projector.hpp"
+#include "ctsm/solver.hpp"
 #include "ctsm/weights2d.hpp"
 #include "ctsm/weights3d.hpp"
 
@@ -276,6 +279,77 @@ int ref_sirt(const RefGeom* rg, const double* y, double* x, int iters, int threa
     for (uint64_t i = 0; i < nv; ++i) x[i] += C[i] * bp[i];
   }
   return 0;
+}
+
+// spectral_norm_power (projector.cpp:262-280) and nag_tikhonov (solver.cpp:17-75)
+// on a reference CSR handle; scale_values (282-286).
+int ref_spectral_norm_power(void* h, int iters, uint64_t seed, double* out) {
+  auto* m = static_cast<ctsm::SparseSystemMatrix*>(h);
+  REF_GUARD(*out = ctsm::spectral_norm_power(*m, iters, seed); return 0;)
+}
+
+int ref_scale_values(void* h, double factor) {
+  auto* m = static_cast<ctsm::SparseSystemMatrix*>(h);
+  REF_GUARD(ctsm::scale_values(m, factor); return 0;)
+}
+
+// trace (optional): 3 doubles per iteration {iter, objective, grad_norm_sq}
+int ref_nag_tikhonov(void* h, const double* p, double lambda, int max_iter, double tol,
+                     double* u, int* iterations, int* converged, double* trace) {
+  auto* m = static_cast<ctsm::SparseSystemMatrix*>(h);
+  REF_GUARD(const std::vector<double> pv(p, p + m->n_rows);
+            ctsm::SolveOptions opt;
+            opt.lambda = lambda; opt.max_iter = max_iter; opt.tol = tol;
+            const auto r = ctsm::nag_tikhonov(*m, pv, opt, trace != nullptr);
+            std::copy(r.u.begin(), r.u.end(), u);
+            *iterations = r.iterations; *converged = r.converged ? 1 : 0;
+            if (trace) for (std::size_t i = 0; i < r.trace.size(); ++i) {
+              trace[3 * i] = r.trace[i].iter;
+              trace[3 * i + 1] = r.trace[i].objective;
+              trace[3 * i + 2] = r.trace[i].grad_norm_sq;
+            }
+            return 0;)
+}
+
+// normal_samples (phantoms.cpp:78-87).
+void ref_normal_samples(uint64_t n, uint64_t seed, double* out) {
+  const auto v = ctsm::normal_samples(n, seed);
+  std::copy(v.begin(), v.end(), out);
+}
+
+// CSM1 / CTT1 writers and readers (io.cpp:153-270).
+int ref_write_matrix(void* h, const char* path) {
+  auto* m = static_cast<ctsm::SparseSystemMatrix*>(h);
+  REF_GUARD(ctsm::write_matrix(path, *m); return 0;)
+}
+
+void* ref_read_matrix(const char* path, int* status) {
+  try {
+    auto* m = new ctsm::SparseSystemMatrix(ctsm::read_matrix(path));
+    *status = 0;
+    return m;
+  } catch (const ctsm::Error& e) {
+    *status = fail_code(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    *status = -100;
+  }
+  return nullptr;
+}
+
+uint64_t ref_csr_cols(void* h) { return static_cast<ctsm::SparseSystemMatrix*>(h)->n_cols; }
+
+// meta string (size query with buf == NULL)
+uint64_t ref_csr_meta(void* h, char* buf, uint64_t cap) {
+  const std::string& s = static_cast<ctsm::SparseSystemMatrix*>(h)->meta;
+  if (buf) std::memcpy(buf, s.data(), std::min<uint64_t>(cap, s.size()));
+  return s.size();
+}
+
+int ref_write_tensor(const char* path, const uint64_t* dims, int rank, const double* data) {
+  REF_GUARD(const std::vector<uint64_t> d(dims, dims + rank);
+            uint64_t n = 1; for (auto v : d) n *= v;
+            ctsm::write_tensor(path, d, std::vector<double>(data, data + n)); return 0;)
 }
 
 // angle_column_sums (projector.cpp:288-295).

@@ -20,6 +20,21 @@ _P = ctypes.c_void_p
 _I = ctypes.c_int
 _U64 = ctypes.c_uint64
 _GP = ctypes.POINTER(CGeometry)
+_D = ctypes.c_double
+
+CTSM_OP_CSR = 0
+CTSM_OP_MATRIX_FREE = 1
+
+
+class COperator(ctypes.Structure):
+    """ctsm_operator (include/ctsm_b200.h)."""
+    _fields_ = [("kind", ctypes.c_int), ("pad0", ctypes.c_int),
+                ("n_rows", ctypes.c_uint64), ("n_cols", ctypes.c_uint64),
+                ("row_start", ctypes.c_void_p), ("col", ctypes.c_void_p), ("val", ctypes.c_void_p),
+                ("geom", _GP), ("scale", ctypes.c_double)]
+
+
+_OP = ctypes.POINTER(COperator)
 
 # name -> (restype, argtypes); mirrors include/ctsm_b200.h
 SIGNATURES = {
@@ -46,6 +61,11 @@ SIGNATURES = {
     "ctsm_sirt": (_I, [_P, _GP, _I, _P, _P, _I, _P]),
     "ctsm_forward_project_matrix_free_host": (_I, [_P, _GP, _P, _P]),
     "ctsm_back_project_matrix_free_host": (_I, [_P, _GP, _P, _P]),
+    "ctsm_spectral_norm_power": (_I, [_P, _OP, _I, _P, ctypes.POINTER(_D), _P]),
+    "ctsm_nag_tikhonov": (_I, [_P, _OP, _P, _D, _I, _D, _P, _P, ctypes.POINTER(_I),
+                               ctypes.POINTER(_I), _P]),
+    "ctsm_scale_values": (_I, [_P, _U64, _P, _D, _P]),
+    "ctsm_normal_samples": (None, [_U64, _U64, _P]),
 }
 
 _lib = None

@@ -21,6 +21,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
 UNITS = {
     "csr.cu": ["-fmad=false"],
     "mf.cu": [],
+    "solver.cu": ["-fmad=false"],
     "capi.cu": [],
     "api.cpp": [],
 }

@@ -3,6 +3,7 @@
 // in, host vectors out; device buffers are allocated per call.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <mutex>
 #include <random>
@@ -246,27 +247,53 @@ std::vector<double> back_project_matrix_free(const ScanGeometry& g, MatrixMode m
 
 double spectral_norm_power(const SparseSystemMatrix& w, int iters, std::uint64_t seed) {
   if (w.nnz() == 0) throw Error(ErrorCode::ZeroMatrix, "matrix has no entries");
-  std::vector<double> v = normal_samples(w.n_cols, seed);
-  double nrm = 0.0;
-  for (double x : v) nrm += x * x;
-  nrm = std::sqrt(nrm);
-  for (double& x : v) x /= nrm;
+  const std::vector<double> v = normal_samples(w.n_cols, seed);
   DevCsr m(w);
-  DevBuf<double> vd(w.n_cols), yd(w.n_rows), ud(w.n_cols);
-  std::vector<double> u(w.n_cols);
-  double lam = 0.0;
-  for (int it = 0; it < iters; ++it) {
-    h2d(vd.p, v.data(), v.size());
-    check(ctsm_spmv(ctx(), w.n_rows, w.n_cols, m.rs.p, m.col.p, m.val.p, vd.p, yd.p, nullptr));
-    check(ctsm_spmv_t(ctx(), w.n_rows, w.n_cols, m.rs.p, m.col.p, m.val.p, yd.p, ud.p, nullptr));
-    d2h(u.data(), ud.p, u.size());
-    lam = 0.0;
-    for (double x : u) lam += x * x;
-    lam = std::sqrt(lam);
-    if (lam == 0.0) throw Error(ErrorCode::ZeroMatrix, "power iteration collapsed");
-    for (std::uint64_t i = 0; i < w.n_cols; ++i) v[i] = u[i] / lam;
-  }
-  return std::sqrt(lam);
+  DevBuf<double> vd(w.n_cols);
+  h2d(vd.p, v.data(), v.size());
+  ctsm_operator op{};
+  op.kind = CTSM_OP_CSR;
+  op.n_rows = w.n_rows;
+  op.n_cols = w.n_cols;
+  op.row_start = m.rs.p;
+  op.col = m.col.p;
+  op.val = m.val.p;
+  op.scale = 1.0;
+  double out = 0.0;
+  check(ctsm_spectral_norm_power(ctx(), &op, iters, vd.p, &out, nullptr));
+  return out;
+}
+
+SolveResult nag_tikhonov(const SparseSystemMatrix& w, const std::vector<double>& p,
+                         const SolveOptions& opt, bool keep_trace) {
+  if (p.size() != w.n_rows)
+    throw Error(ErrorCode::DimensionMismatch, "data size does not match matrix rows");
+  if (!(opt.lambda >= 0.0) || !(opt.tol >= 0.0) || opt.max_iter < 0)
+    throw Error(ErrorCode::InvalidConfig, "solver options must be nonnegative");
+  SolveResult res;
+  res.u.assign(w.n_cols, 0.0);
+  if (w.nnz() == 0) throw Error(ErrorCode::ZeroMatrix, "matrix has no entries");
+  DevCsr m(w);
+  DevBuf<double> pd(w.n_rows), ud(w.n_cols);
+  h2d(pd.p, p.data(), p.size());
+  ctsm_operator op{};
+  op.kind = CTSM_OP_CSR;
+  op.n_rows = w.n_rows;
+  op.n_cols = w.n_cols;
+  op.row_start = m.rs.p;
+  op.col = m.col.p;
+  op.val = m.val.p;
+  op.scale = 1.0;
+  std::vector<double> tr(keep_trace ? 3 * (size_t)std::max(opt.max_iter, 1) : 0);
+  int its = 0, conv = 0;
+  check(ctsm_nag_tikhonov(ctx(), &op, pd.p, opt.lambda, opt.max_iter, opt.tol, ud.p,
+                          keep_trace ? tr.data() : nullptr, &its, &conv, nullptr));
+  d2h(res.u.data(), ud.p, res.u.size());
+  res.iterations = its;
+  res.converged = conv != 0;
+  for (int i = 0; keep_trace && i < its; ++i)
+    res.trace.push_back({(int)tr[3 * i], tr[3 * i + 1], tr[3 * i + 2]});
+  return res;
 }
 
 void scale_values(SparseSystemMatrix* w, double factor) {
@@ -304,3 +331,8 @@ std::vector<double> sirt(const ScanGeometry& g, const std::vector<double>& y,
 }
 
 }  // namespace ctsm
+
+extern "C" void ctsm_normal_samples(uint64_t n, uint64_t seed, double* out) {
+  const std::vector<double> v = ctsm::normal_samples((std::size_t)n, seed);
+  std::copy(v.begin(), v.end(), out);
+}

@@ -70,7 +70,8 @@ struct ctsm_ctx {
   unsigned long long* h_upd = nullptr;    // pinned mirror
   uint64_t last_updates = 0;
   double* h_red = nullptr;      // pinned
-  Buf angles, edges, cs, counts, scan, longrows, acc, part, base, alist, tmp_a, tmp_b, tmp_c, tmp_d,
+  Buf angles, edges, cs, counts, scan, longrows, acc, part, base, alist, sv_up, sv_h, sv_hp,
+      sv_q, sv_v, sv_part, sv_scal, tmp_a, tmp_b, tmp_c, tmp_d,
       tmp_e, tmp_f;
 };
 
@@ -229,7 +230,8 @@ int ctsm_destroy(ctsm_ctx* ctx) {
   if (!ctx) return 0;
   cudaSetDevice(ctx->device);
   Buf* bufs[] = {&ctx->angles, &ctx->edges, &ctx->cs,    &ctx->counts, &ctx->scan,
-                 &ctx->longrows, &ctx->acc, &ctx->part, &ctx->base, &ctx->alist, &ctx->tmp_a, &ctx->tmp_b,  &ctx->tmp_c,
+                 &ctx->longrows, &ctx->acc, &ctx->part, &ctx->base, &ctx->alist, &ctx->sv_up, &ctx->sv_h, &ctx->sv_hp, &ctx->sv_q,
+                 &ctx->sv_v, &ctx->sv_part, &ctx->sv_scal, &ctx->tmp_a, &ctx->tmp_b,  &ctx->tmp_c,
                  &ctx->tmp_d, &ctx->tmp_e, &ctx->tmp_f};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
@@ -739,6 +741,200 @@ int ctsm_sirt(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, const void* y_de
     CT_CUDA(sirt_update(dtype, nv, ctx->tmp_d.p, ctx->tmp_f.p, x_inout_dev, st));
   }
   return check_status(ctx, st, "sirt");
+}
+
+// ---- solvers ------------------------------------------
+namespace {
+
+struct OpRun {
+  const ctsm_operator* op;
+  uint64_t n_rows = 0, n_cols = 0;
+  double mcol = 0.0;  // CSR: max column |sum| (fixed-point bound of W^T)
+  double s = 1.0;     // operator scale
+};
+
+int op_prepare(ctsm_ctx* ctx, const ctsm_operator* op, cudaStream_t st, OpRun* r) {
+  if (!op) return fail(CTSM_ERR_INVALID_SPEC, "null operator");
+  r->op = op;
+  if (op->kind == CTSM_OP_CSR) {
+    if (op->scale != 1.0)
+      return fail(CTSM_ERR_INVALID_SPEC, "CSR operators are scaled with ctsm_scale_values");
+    r->n_rows = op->n_rows;
+    r->n_cols = op->n_cols;
+    uint64_t nnz = 0;
+    if (r->n_rows > 0)
+      CT_CUDA(cudaMemcpy(&nnz, op->row_start + r->n_rows, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    if (nnz == 0) return fail(CTSM_ERR_ZERO_MATRIX, "matrix has no entries");
+    CT_TRY(ensure(ctx, ctx->tmp_a, r->n_cols * sizeof(double)));
+    CT_CUDA(cudaMemsetAsync(ctx->tmp_a.p, 0, r->n_cols * sizeof(double), st));
+    CT_CUDA(colsum_abs(r->n_rows, op->row_start, op->col, op->val, (double*)ctx->tmp_a.p, st));
+    CT_TRY(fetch_max_abs(ctx, CTSM_F64, r->n_cols, ctx->tmp_a.p, st, &r->mcol));
+    if (!std::isfinite(r->mcol)) return fail(CTSM_ERR_NON_FINITE, "matrix not finite");
+  } else if (op->kind == CTSM_OP_MATRIX_FREE) {
+    DevGeom d;
+    CT_TRY(dev_geom(op->geom, &d));
+    r->n_rows = (uint64_t)d.rows_per_angle * op->geom->n_angles;
+    r->n_cols = (uint64_t)d.n_vox;
+    r->s = op->scale;
+    if (!std::isfinite(r->s)) return fail(CTSM_ERR_NON_FINITE, "operator scale must be finite");
+  } else {
+    return fail(CTSM_ERR_INVALID_SPEC, "unknown operator kind");
+  }
+  return 0;
+}
+
+// y = A x (unscaled)
+int op_fwd(ctsm_ctx* ctx, const OpRun& r, const double* x, double* y, cudaStream_t st) {
+  const ctsm_operator* op = r.op;
+  if (op->kind == CTSM_OP_CSR) {
+    CT_CUDA(spmv_csr(r.n_rows, op->row_start, op->col, op->val, x, y, ctx->status, st));
+    return 0;
+  }
+  return fwd_impl(ctx, op->geom, CTSM_F64, 0, op->geom->n_angles, 1, x, y, st);
+}
+
+// x = A^T y (unscaled), deterministic
+int op_bwd(ctsm_ctx* ctx, const OpRun& r, const double* y, double* x, cudaStream_t st) {
+  const ctsm_operator* op = r.op;
+  if (op->kind == CTSM_OP_CSR) {
+    double my = 0.0;
+    CT_TRY(fetch_max_abs(ctx, CTSM_F64, r.n_rows, y, st, &my));
+    if (!std::isfinite(my)) return fail(CTSM_ERR_NON_FINITE, "back projection not finite");
+    const double B = r.mcol * my * (1.0 + 1e-6);
+    if (!(B > 0.0)) {
+      CT_CUDA(cudaMemsetAsync(x, 0, r.n_cols * sizeof(double), st));
+      return 0;
+    }
+    const double scale = std::ldexp(1.0, 61) / B;
+    CT_TRY(ensure(ctx, ctx->tmp_b, r.n_cols * sizeof(unsigned long long)));
+    CT_CUDA(cudaMemsetAsync(ctx->tmp_b.p, 0, r.n_cols * sizeof(unsigned long long), st));
+    CT_CUDA(spmvt_csr_fixed(r.n_rows, op->row_start, op->col, op->val, y,
+                            (unsigned long long*)ctx->tmp_b.p, scale, st));
+    CT_CUDA(fixed_to_double(r.n_cols, (const unsigned long long*)ctx->tmp_b.p, scale, x, st));
+    return 0;
+  }
+  return bwd_impl(ctx, op->geom, CTSM_F64, 0, op->geom->n_angles, 1, y, x, st);
+}
+
+int read_scalars(ctsm_ctx* ctx, int n, double* out, cudaStream_t st) {
+  CT_CUDA(cudaMemcpyAsync(out, ctx->sv_scal.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CT_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+}  // namespace
+
+int ctsm_scale_values(ctsm_ctx* ctx, uint64_t nnz, double* val_dev, double factor, void* stream) {
+  CT_TRY(set_device(ctx));
+  if (!std::isfinite(factor)) return fail(CTSM_ERR_NON_FINITE, "scale factor must be finite");
+  CT_CUDA(scale_in_place(nnz, val_dev, factor, (cudaStream_t)stream));
+  return 0;
+}
+
+int ctsm_spectral_norm_power(ctsm_ctx* ctx, const ctsm_operator* op, int iters,
+                             double* v_dev, double* norm_out, void* stream) {
+  CT_TRY(set_device(ctx));
+  cudaStream_t st = (cudaStream_t)stream;
+  OpRun r;
+  CT_TRY(op_prepare(ctx, op, st, &r));
+  CT_TRY(ensure(ctx, ctx->sv_v, r.n_rows * sizeof(double)));
+  CT_TRY(ensure(ctx, ctx->sv_h, r.n_cols * sizeof(double)));
+  CT_TRY(ensure(ctx, ctx->sv_part, solver_partial_doubles() * sizeof(double)));
+  CT_TRY(ensure(ctx, ctx->sv_scal, 4 * sizeof(double)));
+  double* u = (double*)ctx->sv_h.p;
+  double* y = (double*)ctx->sv_v.p;
+  double* part = (double*)ctx->sv_part.p;
+  double* lam = (double*)ctx->sv_scal.p;
+  // v /= ||v|| (projector.cpp:268-271)
+  CT_CUDA(norm2(r.n_cols, v_dev, 1.0, part, lam, st));
+  CT_CUDA(normalize_by(r.n_cols, v_dev, 1.0, lam, v_dev, ctx->status, st));
+  const double s2 = r.s * r.s;
+  for (int it = 0; it < iters; ++it) {
+    CT_TRY(op_fwd(ctx, r, v_dev, y, st));
+    CT_TRY(op_bwd(ctx, r, y, u, st));
+    // lam = ||W^T W v|| = s^2 ||A^T A v||; v = W^T W v / lam
+    CT_CUDA(norm2(r.n_cols, u, s2, part, lam, st));
+    CT_CUDA(normalize_by(r.n_cols, u, s2, lam, v_dev, ctx->status, st));
+  }
+  double h = 0.0;
+  CT_TRY(read_scalars(ctx, 1, &h, st));
+  const int s = check_status(ctx, st, "spectral_norm_power");
+  if (s == CTSM_ERR_ZERO_MATRIX) return fail(s, "power iteration collapsed");
+  if (s) return s;
+  *norm_out = iters > 0 ? std::sqrt(h) : 0.0;
+  return 0;
+}
+
+int ctsm_nag_tikhonov(ctsm_ctx* ctx, const ctsm_operator* op, const double* p_dev,
+                      double lambda, int max_iter, double tol, double* u_dev,
+                      double* trace_host, int* iterations, int* converged, void* stream) {
+  CT_TRY(set_device(ctx));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!(lambda >= 0.0) || !(tol >= 0.0) || max_iter < 0)
+    return fail(CTSM_ERR_INVALID_CONFIG, "solver options must be nonnegative");
+  OpRun r;
+  CT_TRY(op_prepare(ctx, op, st, &r));
+  const uint64_t n = r.n_cols, nr = r.n_rows;
+  CT_TRY(ensure(ctx, ctx->sv_up, n * sizeof(double)));
+  CT_TRY(ensure(ctx, ctx->sv_h, n * sizeof(double)));
+  CT_TRY(ensure(ctx, ctx->sv_hp, n * sizeof(double)));
+  CT_TRY(ensure(ctx, ctx->sv_q, n * sizeof(double)));
+  CT_TRY(ensure(ctx, ctx->sv_v, nr * sizeof(double)));
+  CT_TRY(ensure(ctx, ctx->sv_part, solver_partial_doubles() * sizeof(double)));
+  CT_TRY(ensure(ctx, ctx->sv_scal, 4 * sizeof(double)));
+  double* up = (double*)ctx->sv_up.p;
+  double* h = (double*)ctx->sv_h.p;
+  double* hp = (double*)ctx->sv_hp.p;
+  double* q = (double*)ctx->sv_q.p;
+  double* v = (double*)ctx->sv_v.p;
+  double* part = (double*)ctx->sv_part.p;
+  double* scal = (double*)ctx->sv_scal.p;
+  const double lam = lambda, L = 1.0 + lam, s = r.s, s2 = s * s;
+  // q = W^T p (solver.cpp:28)
+  CT_TRY(op_bwd(ctx, r, p_dev, q, st));
+  if (s != 1.0) CT_CUDA(scale_in_place(n, q, s, st));
+  CT_CUDA(cudaMemsetAsync(u_dev, 0, n * sizeof(double), st));
+  CT_CUDA(cudaMemsetAsync(up, 0, n * sizeof(double), st));
+  CT_CUDA(cudaMemsetAsync(h, 0, n * sizeof(double), st));
+  CT_CUDA(cudaMemsetAsync(hp, 0, n * sizeof(double), st));
+  double t = 1.0;
+  int iters = 0, conv = 0;
+  for (int it = 0; it < max_iter; ++it) {
+    const double t_next = (1.0 + std::sqrt(1.0 + 4.0 * t * t)) / 2.0;
+    const double m = (t - 1.0) / t_next;
+    CT_CUDA(nag_step(n, m, lam, L, u_dev, up, h, hp, q, st));
+    t = t_next;
+    // v = W u, h = W^T v (solver.cpp:52-53)
+    CT_TRY(op_fwd(ctx, r, u_dev, v, st));
+    CT_TRY(op_bwd(ctx, r, v, h, st));
+    CT_CUDA(nag_grad_sq(n, s2, lam, h, u_dev, q, part, scal, st));
+    double vals[3] = {0.0, 0.0, 0.0};
+    if (trace_host) {
+      CT_CUDA(nag_trace_sums(nr, n, s, v, p_dev, u_dev, part, scal + 1, st));
+      CT_TRY(read_scalars(ctx, 3, vals, st));
+    } else {
+      CT_TRY(read_scalars(ctx, 1, vals, st));
+    }
+    CT_TRY(check_status(ctx, st, "nag_tikhonov"));
+    const double grad_sq = vals[0];
+    iters = it + 1;
+    if (trace_host) {
+      trace_host[3 * it] = (double)(it + 1);
+      trace_host[3 * it + 1] = 0.5 * vals[1] + 0.5 * lam * vals[2];
+      trace_host[3 * it + 2] = grad_sq;
+    }
+    if (!std::isfinite(grad_sq)) {
+      if (iterations) *iterations = iters;
+      return fail(CTSM_ERR_NON_FINITE, "solver iterate diverged");
+    }
+    if (grad_sq < tol) {
+      conv = 1;
+      break;
+    }
+  }
+  if (iterations) *iterations = iters;
+  if (converged) *converged = conv;
+  return 0;
 }
 
 // ---- host-buffer entry points ------------------------------------------------

@@ -114,4 +114,19 @@ cudaError_t fill_value(int dtype, uint64_t n, double v, void* out, cudaStream_t 
 namespace ctsmb {
 // Measured FP64 FMA throughput of the device in TFLOP/s (FMA = 2 flops).
 double bench_dfma_tflops(int device);
+// ---- solver.cu (deterministic vector kernels of the solvers) --------------
+size_t solver_partial_doubles();
+cudaError_t nag_step(uint64_t n, double m, double lam, double L, double* u, double* u_prev,
+                     double* h, double* h_prev, const double* q, cudaStream_t st);
+cudaError_t nag_grad_sq(uint64_t n, double hs, double lam, double* h, const double* u,
+                        const double* q, double* partial, double* out_dev, cudaStream_t st);
+cudaError_t nag_trace_sums(uint64_t n_rows, uint64_t n_cols, double vs, double* v,
+                           const double* p, const double* u, double* partial, double* out_dev,
+                           cudaStream_t st);
+cudaError_t norm2(uint64_t n, const double* a, double scale, double* partial, double* out_dev,
+                  cudaStream_t st);
+cudaError_t normalize_by(uint64_t n, const double* u, double us, const double* lam_dev,
+                         double* v, int* status, cudaStream_t st);
+cudaError_t scale_in_place(uint64_t n, double* v, double f, cudaStream_t st);
+
 }  // namespace ctsmb

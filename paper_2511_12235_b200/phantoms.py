@@ -11,6 +11,7 @@ generated once on the host and fed identically to the CPU oracle and the GPU.
 """
 from __future__ import annotations
 
+import ctypes
 import math
 
 import numpy as np
@@ -70,11 +71,13 @@ class MT19937_64:
 
 
 def normal_samples(n: int, seed: int) -> np.ndarray:
-    """phantoms.cpp:78-87."""
-    raw = MT19937_64(seed).draw(2 * n).reshape(n, 2) >> np.uint64(11)
-    u1 = (raw[:, 0].astype(np.float64) + 1.0) * 2.0 ** -53
-    u2 = raw[:, 1].astype(np.float64) * 2.0 ** -53
-    return np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * math.pi * u2)
+    """phantoms.cpp:78-87, computed by the library's host code
+    (ctsm_normal_samples: std::mt19937_64 + the C library's log/cos, so the
+    samples equal the reference's bit for bit)."""
+    from . import _lib
+    out = np.empty(n, np.float64)
+    _lib.lib().ctsm_normal_samples(n, seed, out.ctypes.data_as(ctypes.c_void_p))
+    return out
 
 
 def uniform_sinogram(n: int, seed: int) -> np.ndarray:

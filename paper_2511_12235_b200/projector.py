@@ -260,28 +260,62 @@ def back_project(w: SparseSystemMatrix, y):
 
 
 def scale_values(w: SparseSystemMatrix, factor: float) -> None:
-    """projector.cpp:282-286."""
+    """projector.cpp:282-286 (device kernel)."""
     if not math.isfinite(factor):
         raise CtsmError("NonFinite", "scale factor must be finite")
-    w.val.mul_(factor)
+    ctx = Context.get(w.device)
+    _lib.check(_lib.lib().ctsm_scale_values(ctx.handle, w.nnz(), _dev_ptr(w.val), float(factor),
+                                            _stream(ctx.device)))
+
+
+def csr_operator(w: SparseSystemMatrix):
+    """ctsm_operator of a device CSR matrix (solvers)."""
+    op = _lib.COperator()
+    op.kind = _lib.CTSM_OP_CSR
+    op.n_rows, op.n_cols = w.n_rows, w.n_cols
+    op.row_start, op.col, op.val = w.row_start.data_ptr(), w.col.data_ptr(), w.val.data_ptr()
+    op.scale = 1.0
+    return op, None
+
+
+def mf_operator(g: ScanGeometry, scale: float = 1.0):
+    """ctsm_operator of the fp64 matrix-free projector of a scan, times scale."""
+    g.validate()
+    cg = g.to_c()
+    op = _lib.COperator()
+    op.kind = _lib.CTSM_OP_MATRIX_FREE
+    op.geom = ctypes.pointer(cg)
+    op.scale = float(scale)
+    return op, cg  # keep cg alive with op
+
+
+def _spectral_norm(op, n_cols: int, device: int, iters: int, seed: int) -> float:
+    from .phantoms import normal_samples
+
+    ctx = Context.get(device)
+    v = torch.from_numpy(normal_samples(n_cols, seed)).to(f"cuda:{ctx.device}")
+    out = ctypes.c_double(0.0)
+    _lib.check(_lib.lib().ctsm_spectral_norm_power(ctx.handle, ctypes.byref(op), int(iters),
+                                                   _dev_ptr(v), ctypes.byref(out),
+                                                   _stream(ctx.device)))
+    return float(out.value)
 
 
 def spectral_norm_power(w: SparseSystemMatrix, iters: int = 100, seed: int = 7) -> float:
-    """projector.cpp:262-280 on K3/K4 (normal_samples, phantoms.cpp:78-87)."""
-    from .phantoms import normal_samples
-
+    """projector.cpp:262-280 on the device (K3/K4 + deterministic reductions);
+    the start vector is normal_samples(n_cols, seed) (phantoms.cpp:78-87)."""
     if w.nnz() == 0:
         raise CtsmError("ZeroMatrix", "matrix has no entries")
-    v = torch.from_numpy(normal_samples(w.n_cols, seed)).to(f"cuda:{w.device}")
-    v = v / torch.sqrt((v * v).sum())
-    lam = 0.0
-    for _ in range(iters):
-        u = back_project(w, forward_project(w, v))
-        lam = float(torch.sqrt((u * u).sum()))
-        if lam == 0.0:
-            raise CtsmError("ZeroMatrix", "power iteration collapsed")
-        v = u / lam
-    return math.sqrt(lam)
+    op, _keep = csr_operator(w)
+    return _spectral_norm(op, w.n_cols, w.device, iters, seed)
+
+
+def spectral_norm_power_matrix_free(g: ScanGeometry, iters: int = 100, seed: int = 7,
+                                    device: Optional[int] = None) -> float:
+    """spectral_norm_power on the matrix-free projector (K5/K6): the paper's
+    normalisation step for scans whose matrix is too large to store."""
+    op, _keep = mf_operator(g)
+    return _spectral_norm(op, g.n_voxels, device if device is not None else 0, iters, seed)
 
 
 # ---- matrix-free projectors (K5/K6) ---------------------------------------
