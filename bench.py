@@ -428,7 +428,7 @@ def run_sirt(args):
     import torch.distributed as dist
 
     from paper_2511_12235_b200 import CONFIGS, Context, _lib
-    from paper_2511_12235_b200.dist import angle_shard, shard_rows
+    from paper_2511_12235_b200.dist import angle_shard
     from paper_2511_12235_b200.phantoms import phantom_for
     from paper_2511_12235_b200.projector import (back_project_matrix_free,
                                                  forward_project_matrix_free)
@@ -444,7 +444,6 @@ def run_sirt(args):
     tdt = torch.float64 if args.dtype == "f64" else torch.float32
     ctx = Context.get(local)
     shard = angle_shard(g, rank, world)
-    rows = shard_rows(g, shard).to(dev)
     t_setup0 = time.perf_counter()
     x_true = torch.from_numpy(phantom_for(cfg, g, dtype=np.float32)).to(tdt).to(dev)
     y = torch.zeros(g.n_measurements, dtype=tdt, device=dev)
@@ -452,11 +451,12 @@ def run_sirt(args):
     ymax = y.abs().max()
     if world > 1:
         dist.all_reduce(ymax, op=dist.ReduceOp.MAX)
+    # noise on every row (a rank reads only its own rows: R is zero elsewhere)
     gen = torch.Generator(device=dev).manual_seed(12347 + rank)
-    y[rows] += 0.01 * ymax * torch.randn(rows.numel(), dtype=tdt, device=dev, generator=gen)
+    y += 0.01 * ymax * torch.randn(y.numel(), dtype=tdt, device=dev, generator=gen)
     R = torch.zeros_like(y)
     forward_project_matrix_free(g, "consistent", 1, torch.ones_like(x_true), angles=shard, out=R)
-    R[rows] = torch.where(R[rows] != 0, 1.0 / R[rows], torch.zeros_like(R[rows]))
+    R = torch.where(R != 0, 1.0 / R, torch.zeros_like(R))  # rows of other ranks stay 0
     Cc = back_project_matrix_free(g, "consistent", 1, torch.ones_like(y), angles=shard)
     if world > 1:
         dist.all_reduce(Cc)
@@ -471,7 +471,7 @@ def run_sirt(args):
 
     def iteration():
         forward_project_matrix_free(g, "consistent", 1, x, angles=shard, out=ax)
-        r[rows] = R[rows] * (y[rows] - ax[rows])
+        torch.mul(R, y - ax, out=r)  # R = 0 on rows of other ranks
         back_project_matrix_free(g, "consistent", 1, r, angles=shard, out=bp)
         if world > 1:
             dist.all_reduce(bp)
@@ -507,7 +507,8 @@ def run_sirt(args):
         cnt = torch.cat([upd, msx])
     nnz_live, ms = int(cnt[0].item()), float(cnt[1].item())
     if rank == 0:
-        resid = float(((y[rows] - ax[rows]) ** 2).sum().sqrt())
+        # residual over the rows rank 0 solves for (R != 0; empty rows excluded)
+        resid = float((torch.where(R != 0, y - ax, torch.zeros_like(ax)) ** 2).sum().sqrt())
         line = {
             "metric": "voxel-ray updates/s (SIRT iterations)",
             "value": 2.0 * nnz_live / (ms * 1e-3),

@@ -130,7 +130,7 @@ template <typename T, bool kFwd>
 __global__ void __launch_bounds__(kWarps3 * 32, 4) proj3d_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, int angle_begin, int angle_step, int n_sel,
     const T* __restrict__ in, T* __restrict__ xout, unsigned long long* __restrict__ yacc,
-    double scale, unsigned long long* n_upd, int* status) {
+    double scale, unsigned long long* n_upd, int accumulate, int* status) {
   __shared__ fast::ColumnHead sh[kWarps3];
   __shared__ fast::PieceCoef sp[kWarps3][fast::kMaxPieces];
   __shared__ double sacc[kWarps3][kZcMax][32];
@@ -186,7 +186,11 @@ __global__ void __launch_bounds__(kWarps3 * 32, 4) proj3d_kernel(
       }
     }
     if (!kFwd)
-      for (int iz = z0; iz < z1; ++iz) xout[iz * plane + col] = (T)sacc[warp][iz - z0][lane];
+      for (int iz = z0; iz < z1; ++iz) {
+        double v = sacc[warp][iz - z0][lane];
+        if (accumulate) v += (double)xout[iz * plane + col];
+        xout[iz * plane + col] = (T)v;
+      }
   }
   if (kFwd) count_updates(n_upd, cnt);
 }
@@ -650,7 +654,7 @@ constexpr int kZcS = 8;
 template <typename T, int G>
 __global__ void __launch_bounds__(kWarpsS * 32, 8) bwd3d_sym_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
-    const T* __restrict__ in, T* __restrict__ xout, int* status) {
+    const T* __restrict__ in, T* __restrict__ xout, int accumulate, int* status) {
   __shared__ fast::ColumnHead sh[kWarpsS];
   __shared__ fast::PieceCoef sp[kWarpsS][fast::kMaxPieces];
   __shared__ double sacc[kWarpsS][G][kZcS][32];
@@ -719,6 +723,7 @@ __global__ void __launch_bounds__(kWarpsS * 32, 8) bwd3d_sym_kernel(
       for (int iz = z0; iz < z1; ++iz) {
         double v = sacc[warp][e][iz - z0][lane];
         if (diag) v += sacc[warp][e2][iz - z0][lane];
+        if (accumulate) v += (double)xout[iz * nxy + c];
         xout[iz * nxy + c] = (T)v;
       }
     }
@@ -829,6 +834,13 @@ static dim3 tile_grid(const DevGeom& g, unsigned ydim) {
   return dim3(tiles, ydim);
 }
 
+// Angles per launch of the general 3D kernel: the rows of one launch's angles
+// should stay L2-resident (~64 MB of the 126 MB L2), see sym3d_chunk below.
+static int gen3d_chunk(const DevGeom& g, size_t elem_bytes) {
+  const int c = (int)((64.0 * (1 << 20)) / ((double)g.rows_per_angle * (double)elem_bytes));
+  return c < 1 ? 1 : c;
+}
+
 cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
                    int angle_step, int n_sel, const void* x, unsigned long long* yacc,
                    double scale, unsigned long long* n_upd, int* status, cudaStream_t st) {
@@ -842,19 +854,25 @@ cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_beg
     else
       fwd2d_kernel<float><<<grid, 128, 0, st>>>(g, cs, angle_begin, angle_step, n_sel,
                                                 (const float*)x, yacc, scale, n_upd, status);
+    count_launch();
   } else {
     const long long nxy = (long long)g.n_x * g.n_y;
     const unsigned blocks = (unsigned)((nxy + kWarps3 - 1) / kWarps3);
-    if (dtype == CTSM_F64)
-      proj3d_kernel<double, true><<<blocks, kWarps3 * 32, 0, st>>>(
-          g, cs, angle_begin, angle_step, n_sel, (const double*)x, nullptr, yacc, scale, n_upd,
-          status);
-    else
-      proj3d_kernel<float, true><<<blocks, kWarps3 * 32, 0, st>>>(
-          g, cs, angle_begin, angle_step, n_sel, (const float*)x, nullptr, yacc, scale, n_upd,
-          status);
+    const int chunk = gen3d_chunk(g, sizeof(unsigned long long));
+    for (int k0 = 0; k0 < n_sel; k0 += chunk) {
+      const int nk = n_sel - k0 < chunk ? n_sel - k0 : chunk;
+      const int a0 = angle_begin + k0 * angle_step;
+      if (dtype == CTSM_F64)
+        proj3d_kernel<double, true><<<blocks, kWarps3 * 32, 0, st>>>(
+            g, cs + k0, a0, angle_step, nk, (const double*)x, nullptr, yacc, scale, n_upd, 0,
+            status);
+      else
+        proj3d_kernel<float, true><<<blocks, kWarps3 * 32, 0, st>>>(
+            g, cs + k0, a0, angle_step, nk, (const float*)x, nullptr, yacc, scale, n_upd, 0,
+            status);
+      count_launch();
+    }
   }
-  count_launch();
   return cudaGetLastError();
 }
 
@@ -896,15 +914,21 @@ cudaError_t bwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_beg
   } else {
     const long long nxy = (long long)g.n_x * g.n_y;
     const unsigned blocks = (unsigned)((nxy + kWarps3 - 1) / kWarps3);
-    if (dtype == CTSM_F64)
-      proj3d_kernel<double, false><<<blocks, kWarps3 * 32, 0, st>>>(
-          g, cs, angle_begin, angle_step, n_sel, (const double*)y, (double*)x, nullptr, 1.0,
-          nullptr, status);
-    else
-      proj3d_kernel<float, false><<<blocks, kWarps3 * 32, 0, st>>>(
-          g, cs, angle_begin, angle_step, n_sel, (const float*)y, (float*)x, nullptr, 1.0,
-          nullptr, status);
-    count_launch();
+    // angle chunks accumulate into x in ascending order (deterministic)
+    const int chunk = gen3d_chunk(g, dtype == CTSM_F64 ? 8 : 4);
+    for (int k0 = 0; k0 < (n_sel > 0 ? n_sel : 1); k0 += chunk) {
+      const int nk = n_sel - k0 < chunk ? n_sel - k0 : chunk;
+      const int a0 = angle_begin + k0 * angle_step;
+      if (dtype == CTSM_F64)
+        proj3d_kernel<double, false><<<blocks, kWarps3 * 32, 0, st>>>(
+            g, cs + k0, a0, angle_step, nk, (const double*)y, (double*)x, nullptr, 1.0, nullptr,
+            k0 > 0, status);
+      else
+        proj3d_kernel<float, false><<<blocks, kWarps3 * 32, 0, st>>>(
+            g, cs + k0, a0, angle_step, nk, (const float*)y, (float*)x, nullptr, 1.0, nullptr,
+            k0 > 0, status);
+      count_launch();
+    }
   }
   return cudaGetLastError();
 }
@@ -924,28 +948,43 @@ cudaError_t fwd_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int
   return cudaGetLastError();
 }
 
+// Base angles per launch of the symmetric 3D kernels: every warp touches the
+// rows of all image angles of the launch's base angles, so a launch covering
+// the whole scan streams the sinogram (fixed-point accumulator / input) from
+// HBM with scattered accesses; chunks whose rows fit in ~64 MB of the 126 MB
+// L2 keep the atomics and gathers on chip.
+static int sym3d_chunk(const DevGeom& g, int order, size_t elem_bytes) {
+  const double per_base = (double)order * g.rows_per_angle * (double)elem_bytes;
+  const int c = (int)((64.0 * (1 << 20)) / per_base);
+  return c < 1 ? 1 : c;
+}
+
 cudaError_t fwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                          int n_base, const void* x, unsigned long long* yacc, double scale,
                          unsigned long long* n_upd, int* status, cudaStream_t st, int order) {
   if (n_base <= 0) return cudaSuccess;
   const long long nxy = (long long)g.n_x * g.n_y;
   const unsigned blocks = (unsigned)((nxy + kWarps3 - 1) / kWarps3);
-#define CTSM_LAUNCH(T, G)                                                                    \
-  do {                                                                                       \
-    constexpr size_t smem = fwd3d_sym_dyn_smem<T, G>();                                      \
-    cudaFuncSetAttribute(fwd3d_sym_kernel<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                         (int)smem);                                                         \
-    fwd3d_sym_kernel<T, G><<<blocks, kWarps3 * 32, smem, st>>>(g, cs, base, n_base,           \
-                                                               (const T*)x, yacc, scale,      \
-                                                               n_upd, status);               \
+  const int chunk = sym3d_chunk(g, order, sizeof(unsigned long long));
+  for (int k0 = 0; k0 < n_base; k0 += chunk) {
+    const int nk = n_base - k0 < chunk ? n_base - k0 : chunk;
+#define CTSM_LAUNCH(T, G)                                                                     \
+  do {                                                                                        \
+    constexpr size_t smem = fwd3d_sym_dyn_smem<T, G>();                                       \
+    cudaFuncSetAttribute(fwd3d_sym_kernel<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                         (int)smem);                                                          \
+    fwd3d_sym_kernel<T, G><<<blocks, kWarps3 * 32, smem, st>>>(g, cs + k0, base + k0, nk,      \
+                                                               (const T*)x, yacc, scale,       \
+                                                               n_upd, status);                \
   } while (0)
-  if (dtype == CTSM_F64) {
-    if (order == 8) CTSM_LAUNCH(double, 8); else CTSM_LAUNCH(double, 4);
-  } else {
-    if (order == 8) CTSM_LAUNCH(float, 8); else CTSM_LAUNCH(float, 4);
-  }
+    if (dtype == CTSM_F64) {
+      if (order == 8) CTSM_LAUNCH(double, 8); else CTSM_LAUNCH(double, 4);
+    } else {
+      if (order == 8) CTSM_LAUNCH(float, 8); else CTSM_LAUNCH(float, 4);
+    }
 #undef CTSM_LAUNCH
-  count_launch();
+    count_launch();
+  }
   return cudaGetLastError();
 }
 
@@ -955,16 +994,21 @@ cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const i
   const long long h = g.n_x / 2;
   const long long n_orb = order == 8 ? h * (h + 1) / 2 : h * h;
   const unsigned blocks = (unsigned)((n_orb + kWarpsS - 1) / kWarpsS);
-#define CTSM_LAUNCH(T, G)                                                                  \
-  bwd3d_sym_kernel<T, G><<<blocks, kWarpsS * 32, 0, st>>>(g, cs, base, n_base, (const T*)y, \
-                                                          (T*)x, status)
-  if (dtype == CTSM_F64) {
-    if (order == 8) CTSM_LAUNCH(double, 8); else CTSM_LAUNCH(double, 4);
-  } else {
-    if (order == 8) CTSM_LAUNCH(float, 8); else CTSM_LAUNCH(float, 4);
-  }
+  const int chunk = sym3d_chunk(g, order, dtype == CTSM_F64 ? 8 : 4);
+  // chunks accumulate into x in ascending order (deterministic)
+  for (int k0 = 0; k0 < (n_base > 0 ? n_base : 1); k0 += chunk) {
+    const int nk = n_base - k0 < chunk ? n_base - k0 : chunk;
+#define CTSM_LAUNCH(T, G)                                                                     \
+  bwd3d_sym_kernel<T, G><<<blocks, kWarpsS * 32, 0, st>>>(g, cs + k0, base + k0, nk,           \
+                                                          (const T*)y, (T*)x, k0 > 0, status)
+    if (dtype == CTSM_F64) {
+      if (order == 8) CTSM_LAUNCH(double, 8); else CTSM_LAUNCH(double, 4);
+    } else {
+      if (order == 8) CTSM_LAUNCH(float, 8); else CTSM_LAUNCH(float, 4);
+    }
 #undef CTSM_LAUNCH
-  count_launch();
+    count_launch();
+  }
   return cudaGetLastError();
 }
 
