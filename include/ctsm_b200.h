@@ -196,6 +196,27 @@ void ctsm_normal_samples(uint64_t n, uint64_t seed, double* out_host);
 int ctsm_scale_values(ctsm_ctx* ctx, uint64_t nnz, double* val_dev, double factor,
                       void* stream);
 
+/* ---- CSM1 / CTT1 containers (io.hpp:31-48) -------
+ * CSM1 (write_matrix / read_matrix, io.cpp:153-227): "CSM1", u64 n_rows,
+ * n_cols, nnz, meta_len, meta, row_start[n_rows+1] u64, col[nnz] as u64,
+ * val[nnz] f64 -- byte-identical to the reference writer. The device variants
+ * stream a device CSR through pinned staging (no host copy of the matrix).
+ * Reading: ctsm_csm1_header gives the sizes to allocate; the reader applies
+ * the reference's checks (IoFailure: bad magic, short file, inconsistent or
+ * decreasing row offsets, column out of range; TooLarge: n_cols >= 2^32). */
+int ctsm_write_csm1_device(ctsm_ctx* ctx, const char* path, uint64_t n_rows, uint64_t n_cols,
+                           const uint64_t* row_start_dev, const uint32_t* col_dev,
+                           const double* val_dev, const char* meta, uint64_t meta_len,
+                           void* stream);
+int ctsm_csm1_header(const char* path, uint64_t* n_rows, uint64_t* n_cols, uint64_t* nnz,
+                     uint64_t* meta_len);
+int ctsm_read_csm1_device(ctsm_ctx* ctx, const char* path, uint64_t* row_start_dev,
+                          uint32_t* col_dev, double* val_dev, char* meta_out, void* stream);
+/* CTT1 (write_tensor / read_tensor, io.cpp:229-270), host buffers. */
+int ctsm_write_ctt1(const char* path, const uint64_t* dims, int rank, const double* data_host);
+int ctsm_ctt1_header(const char* path, uint64_t* dims_out /* [8] */, int* rank_out);
+int ctsm_read_ctt1(const char* path, double* data_host, uint64_t count);
+
 /* ---- host-buffer entry points (the reference's value-semantics calls,
  * used for end-to-end timing; copies in/out of pinned staging inside) ---- */
 int ctsm_forward_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,

@@ -134,6 +134,12 @@ struct SolveResult {
 };
 SolveResult nag_tikhonov(const SparseSystemMatrix& w, const std::vector<double>& p,
                          const SolveOptions& opt, bool keep_trace = false);
+// io.hpp:31-48: CSM1 matrices and CTT1 tensors (byte-identical containers).
+void write_matrix(const std::string& path, const SparseSystemMatrix& w);
+SparseSystemMatrix read_matrix(const std::string& path);
+void write_tensor(const std::string& path, const std::vector<std::uint64_t>& dims,
+                  const std::vector<double>& data);
+std::vector<double> read_tensor(const std::string& path, std::vector<std::uint64_t>* dims);
 // Addition: SIRT (BASELINE.json configs[4]) on one device.
 std::vector<double> sirt(const ScanGeometry& g, const std::vector<double>& y,
                          const std::vector<double>& x0, int iters);

@@ -66,6 +66,14 @@ SIGNATURES = {
                                ctypes.POINTER(_I), _P]),
     "ctsm_scale_values": (_I, [_P, _U64, _P, _D, _P]),
     "ctsm_normal_samples": (None, [_U64, _U64, _P]),
+    "ctsm_write_csm1_device": (_I, [_P, ctypes.c_char_p, _U64, _U64, _P, _P, _P, ctypes.c_char_p,
+                                    _U64, _P]),
+    "ctsm_csm1_header": (_I, [ctypes.c_char_p, ctypes.POINTER(_U64), ctypes.POINTER(_U64),
+                              ctypes.POINTER(_U64), ctypes.POINTER(_U64)]),
+    "ctsm_read_csm1_device": (_I, [_P, ctypes.c_char_p, _P, _P, _P, _P, _P]),
+    "ctsm_write_ctt1": (_I, [ctypes.c_char_p, _P, _I, _P]),
+    "ctsm_ctt1_header": (_I, [ctypes.c_char_p, _P, ctypes.POINTER(_I)]),
+    "ctsm_read_ctt1": (_I, [ctypes.c_char_p, _P, _U64]),
 }
 
 _lib = None

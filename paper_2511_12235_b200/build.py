@@ -23,6 +23,7 @@ UNITS = {
     "mf.cu": [],
     "solver.cu": ["-fmad=false"],
     "capi.cu": [],
+    "io.cu": [],
     "api.cpp": [],
 }
 

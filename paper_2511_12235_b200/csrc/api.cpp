@@ -245,6 +245,59 @@ std::vector<double> back_project_matrix_free(const ScanGeometry& g, MatrixMode m
   return x;
 }
 
+// ---- io (CSM1 through the device streaming writer/reader; CTT1 host) ----
+void write_matrix(const std::string& path, const SparseSystemMatrix& w) {
+  if (w.row_start.size() != w.n_rows + 1)
+    throw Error(ErrorCode::DimensionMismatch, "row offsets do not match the row count");
+  DevCsr m(w);
+  check(ctsm_write_csm1_device(ctx(), path.c_str(), w.n_rows, w.n_cols, m.rs.p, m.col.p,
+                               m.val.p, w.meta.data(), w.meta.size(), nullptr));
+}
+
+SparseSystemMatrix read_matrix(const std::string& path) {
+  std::uint64_t n_rows = 0, n_cols = 0, nnz = 0, meta_len = 0;
+  check(ctsm_csm1_header(path.c_str(), &n_rows, &n_cols, &nnz, &meta_len));
+  SparseSystemMatrix w;
+  w.n_rows = n_rows;
+  w.n_cols = n_cols;
+  w.meta.assign(meta_len, '\0');
+  DevBuf<std::uint64_t> rs(n_rows + 1);
+  DevBuf<std::uint32_t> col(nnz);
+  DevBuf<double> val(nnz);
+  check(ctsm_read_csm1_device(ctx(), path.c_str(), rs.p, col.p, val.p,
+                              meta_len ? &w.meta[0] : nullptr, nullptr));
+  w.row_start.resize(n_rows + 1);
+  w.col.resize(nnz);
+  w.val.resize(nnz);
+  d2h(w.row_start.data(), rs.p, w.row_start.size());
+  d2h(w.col.data(), col.p, w.col.size());
+  d2h(w.val.data(), val.p, w.val.size());
+  return w;
+}
+
+void write_tensor(const std::string& path, const std::vector<std::uint64_t>& dims,
+                  const std::vector<double>& data) {
+  if (dims.empty() || dims.size() > 8)
+    throw Error(ErrorCode::InvalidSpec, "tensor rank must be between 1 and 8");
+  std::uint64_t count = 1;
+  for (std::uint64_t d : dims) count *= d;
+  if (count != data.size())
+    throw Error(ErrorCode::DimensionMismatch, "tensor dims do not match payload size");
+  check(ctsm_write_ctt1(path.c_str(), dims.data(), (int)dims.size(), data.data()));
+}
+
+std::vector<double> read_tensor(const std::string& path, std::vector<std::uint64_t>* dims) {
+  std::uint64_t d[8];
+  int rank = 0;
+  check(ctsm_ctt1_header(path.c_str(), d, &rank));
+  dims->assign(d, d + rank);
+  std::uint64_t count = 1;
+  for (int i = 0; i < rank; ++i) count *= d[i];
+  std::vector<double> out(count);
+  check(ctsm_read_ctt1(path.c_str(), out.data(), count));
+  return out;
+}
+
 double spectral_norm_power(const SparseSystemMatrix& w, int iters, std::uint64_t seed) {
   if (w.nnz() == 0) throw Error(ErrorCode::ZeroMatrix, "matrix has no entries");
   const std::vector<double> v = normal_samples(w.n_cols, seed);

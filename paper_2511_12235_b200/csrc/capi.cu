@@ -205,6 +205,9 @@ int fetch_max_abs(ctsm_ctx* ctx, int dtype, uint64_t n, const void* v, cudaStrea
 
 }  // namespace
 
+int ctsmb::set_error(int code, const char* msg) { return fail(code, msg); }
+int ctsmb::select_device(ctsm_ctx* ctx) { return ctx ? set_device(ctx) : 0; }
+
 extern "C" {
 
 int ctsm_create(int device, ctsm_ctx** out) {

@@ -5,7 +5,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
+
 #include "common.cuh"
+
+struct ctsm_ctx;
 
 namespace ctsmb {
 
@@ -16,6 +20,11 @@ struct EdgeAngle;
 
 // Global launch counter (reported by ctsm_launch_count).
 void count_launch(int n = 1);
+// Sets the thread-local last-error message (ctsm_last_error) and returns code.
+int set_error(int code, const char* msg);
+inline int set_error(int code, const std::string& msg) { return set_error(code, msg.c_str()); }
+// cudaSetDevice(ctx's device) (capi.cu); 0 or an error code.
+int select_device(::ctsm_ctx* ctx);
 
 // ---- csr.cu --------------------------------------------------------------
 size_t exact_angle_bytes();

@@ -122,6 +122,36 @@ int main() {
     scale_values(&w, 1.0 / nrm);
     EXPECT(std::abs(spectral_norm_power(w, 150, 7) - 1.0) <= 1e-8);
   }
+  // NAG-Tikhonov (solver.cpp:17-75): converges on the normalised matrix and
+  // decreases the objective; option validation
+  {
+    const ScanGeometry g = small_scan(false);
+    SparseSystemMatrix w = build_system_matrix(g, MatrixMode::consistent);
+    scale_values(&w, 1.0 / spectral_norm_power(w, 100, 7));
+    std::vector<double> u0(w.n_cols, 0.01);
+    const std::vector<double> p = forward_project(w, u0);
+    SolveOptions opt;
+    opt.lambda = 1e-2;
+    opt.max_iter = 400;
+    opt.tol = 1e-8;
+    const SolveResult r = nag_tikhonov(w, p, opt, true);
+    EXPECT(r.converged && r.iterations < 400 && (int)r.trace.size() == r.iterations);
+    EXPECT(r.trace.back().objective < r.trace.front().objective);
+    SolveOptions bad;
+    bad.lambda = -1.0;
+    EXPECT(code_of([&] { nag_tikhonov(w, p, bad); }) == (int)ErrorCode::InvalidConfig);
+    // CSM1 round trip (io.cpp:153-227) and CTT1
+    write_matrix("/tmp/ctsm_cpp_api_test.csm", w);
+    const SparseSystemMatrix r2 = read_matrix("/tmp/ctsm_cpp_api_test.csm");
+    EXPECT(r2.row_start == w.row_start && r2.col == w.col && r2.val == w.val &&
+           r2.meta == w.meta && r2.n_cols == w.n_cols);
+    write_tensor("/tmp/ctsm_cpp_api_test.ctt", {2, 3}, {1, 2, 3, 4, 5, 6});
+    std::vector<std::uint64_t> dims;
+    const auto t = read_tensor("/tmp/ctsm_cpp_api_test.ctt", &dims);
+    EXPECT(dims.size() == 2 && dims[1] == 3 && t.size() == 6 && t[5] == 6.0);
+    EXPECT(code_of([&] { read_matrix("/tmp/ctsm_no_such_file.csm"); }) ==
+           (int)ErrorCode::IoFailure);
+  }
   // memory budget and size limits (test_projector.cpp:144-155)
   {
     const ScanGeometry g = small_scan(true);
