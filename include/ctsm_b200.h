@@ -217,6 +217,35 @@ int ctsm_write_ctt1(const char* path, const uint64_t* dims, int rank, const doub
 int ctsm_ctt1_header(const char* path, uint64_t* dims_out /* [8] */, int* rank_out);
 int ctsm_read_ctt1(const char* path, double* data_host, uint64_t count);
 
+/* ---- line / multiline(k) modes -------------------
+ * The paper's comparison method (baseline.cpp:13-128): the exact intersection
+ * lengths of the ray to the centre of each detector cell (line) or the average
+ * over k (2D) / k*k (3D) uniformly placed rays (multiline), one device thread
+ * per detector cell. mode = MatrixMode ordinal (projector.hpp:12-16); for
+ * CTSM_MODE_CONSISTENT the calls forward to the entry points above (k ignored).
+ *   ctsm_csr_count_mode / ctsm_csr_fill_mode: build_system_matrix(g, mode, k)
+ *     rows of angles [angle_begin, angle_end), same protocol and errors as
+ *     ctsm_csr_count / ctsm_csr_fill; bit-identical to the reference with a
+ *     correctly rounded libm (merge_hits order and stable column sort kept).
+ *     Rows longer than 8192 traced hits (before merging) raise TooLarge.
+ *   ctsm_fwd_mf_mode / ctsm_bwd_mf_mode: forward_project_matrix_free(g, mode,
+ *     k, x) (projector.cpp:235-260) and its adjoint on a strided angle shard,
+ *     deterministic (gather / int64 fixed-point scatter). InvalidSpec for an
+ *     unknown mode or k <= 0 in multiline mode. */
+enum { CTSM_MODE_CONSISTENT = 0, CTSM_MODE_LINE = 1, CTSM_MODE_MULTILINE = 2 };
+int ctsm_csr_count_mode(ctsm_ctx* ctx, const ctsm_geometry* g, int mode, int k, int angle_begin,
+                        int angle_end, uint64_t memory_budget_bytes, uint64_t* row_start_dev,
+                        uint64_t* nnz_out, void* stream);
+int ctsm_csr_fill_mode(ctsm_ctx* ctx, const ctsm_geometry* g, int mode, int k, int angle_begin,
+                       int angle_end, const uint64_t* row_start_dev, uint32_t* col_dev,
+                       double* val_dev, void* stream);
+int ctsm_fwd_mf_mode(ctsm_ctx* ctx, const ctsm_geometry* g, int mode, int k, int dtype,
+                     int angle_begin, int angle_end, int angle_step, const void* x_dev,
+                     void* y_dev, void* stream);
+int ctsm_bwd_mf_mode(ctsm_ctx* ctx, const ctsm_geometry* g, int mode, int k, int dtype,
+                     int angle_begin, int angle_end, int angle_step, const void* y_dev,
+                     void* x_dev, void* stream);
+
 /* ---- host-buffer entry points (the reference's value-semantics calls,
  * used for end-to-end timing; copies in/out of pinned staging inside) ---- */
 int ctsm_forward_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,

@@ -99,7 +99,7 @@ struct SparseSystemMatrix {
 };
 
 // projector.hpp:41-70 (threads is accepted and ignored: the work runs on the
-// GPU; only MatrixMode::consistent is provided on the device path).
+// GPU; line / multiline(k) run the device ray tracer of baseline.cpp:13-128).
 SparseSystemMatrix build_system_matrix(const ScanGeometry& g, MatrixMode mode, int k = 1,
                                        int threads = 1,
                                        std::uint64_t memory_budget_bytes = 5ull << 30);

@@ -800,6 +800,211 @@ long ref_angle_block_entries_par(const o_geom* g, int ip, uint32_t* row, uint32_
   return st != 0 ? st : n;
 }
 
+/* ---- line / multiline baselines (baseline.cpp:13-128) --------------------
+ * The paper's comparison method: exact intersection
+ * lengths of one (line) or k resp. k*k (multiline) rays per detector cell. */
+typedef struct {
+  uint32_t col;
+  double len;
+  long seq; /* emission index: makes the column sort stable (merge_hits) */
+} ray_hit;
+typedef struct {
+  ray_hit* h;
+  long n, cap;
+} hit_vec;
+static void hit_push(hit_vec* v, uint32_t col, double len) {
+  if (v->n == v->cap) {
+    long nc = v->cap ? 2 * v->cap : 1024;
+    v->h = (ray_hit*)realloc(v->h, nc * sizeof(ray_hit));
+    if (!v->h) o_fail(E_OutOfMemory, "host allocation failed");
+    v->cap = nc;
+  }
+  v->h[v->n].col = col;
+  v->h[v->n].len = len;
+  v->h[v->n].seq = v->n;
+  v->n++;
+}
+
+/* trace_ray (baseline.cpp:13-67): incremental grid traversal from the origin
+ * along a unit direction; (column, length * scale) for every crossed voxel. */
+static void trace_ray(double ox, double oy, double oz, double ux, double uy, double uz,
+                      const o_geom* g, double scale, hit_vec* out) {
+  const double lo[3] = {face_x(g, 0), face_y(g, 0), face_z(g, 0)};
+  const double hi[3] = {face_x(g, g->n_x), face_y(g, g->n_y), face_z(g, g->n_z)};
+  const double org[3] = {ox, oy, oz};
+  const double dir[3] = {ux, uy, uz};
+  const double pitch[3] = {g->a, g->b, g->c};
+  const int dims[3] = {g->n_x, g->n_y, g->n_z};
+  double tmin = 0.0, tmax = INFINITY;
+  for (int ax = 0; ax < 3; ++ax) {
+    if (fabs(dir[ax]) < 1e-15) {
+      if (org[ax] < lo[ax] || org[ax] > hi[ax]) return;
+      continue;
+    }
+    double ta = (lo[ax] - org[ax]) / dir[ax];
+    double tb = (hi[ax] - org[ax]) / dir[ax];
+    if (ta > tb) {
+      const double t = ta;
+      ta = tb;
+      tb = t;
+    }
+    tmin = dmax(tmin, ta);
+    tmax = dmin(tmax, tb);
+  }
+  if (tmax <= tmin) return;
+  const double eps = 1e-12 * dmin(dmin(g->a, g->b), g->c);
+  int idx[3];
+  for (int ax = 0; ax < 3; ++ax) {
+    const double p = org[ax] + (tmin + eps) * dir[ax];
+    idx[ax] = (int)floor((p - lo[ax]) / pitch[ax]);
+  }
+  double t = tmin;
+  while (t < tmax - eps) {
+    int inside = 1;
+    for (int ax = 0; ax < 3; ++ax) inside = inside && idx[ax] >= 0 && idx[ax] < dims[ax];
+    if (!inside) break;
+    double tn = tmax;
+    int step_ax = -1;
+    for (int ax = 0; ax < 3; ++ax) {
+      if (dir[ax] == 0.0) continue;
+      const int f = idx[ax] + (dir[ax] > 0 ? 1 : 0);
+      const double tc = (lo[ax] + f * pitch[ax] - org[ax]) / dir[ax];
+      if (tc < tn) {
+        tn = tc;
+        step_ax = ax;
+      }
+    }
+    if (tn > t)
+      hit_push(out, (uint32_t)(((uint64_t)idx[2] * g->n_y + idx[1]) * g->n_x + idx[0]),
+               (tn - t) * scale);
+    if (step_ax < 0 || tn >= tmax) break;
+    idx[step_ax] += dir[step_ax] > 0 ? 1 : -1;
+    t = tn;
+  }
+}
+
+/* cell_ray (baseline.cpp:69-79) with detector_point (geometry.hpp:108-113). */
+static void cell_ray(double e_y, double e_z, int ip, const o_geom* g, double scale,
+                     hit_vec* out) {
+  const double phi = g_angle(g, ip);
+  const double ox = g->s * O_COS(phi), oy = g->s * O_SIN(phi);
+  const double cp = O_COS(phi), sp = O_SIN(phi);
+  const double dx = -g->d * cp - e_y * g->d_y * sp, dy = -g->d * sp + e_y * g->d_y * cp,
+               dz = e_z * g->d_z;
+  double ux = dx - ox, uy = dy - oy, uz = dz;
+  const double nrm = sqrt(ux * ux + uy * uy + uz * uz);
+  ux /= nrm;
+  uy /= nrm;
+  uz /= nrm;
+  trace_ray(ox, oy, 0.0, ux, uy, uz, g, scale, out);
+}
+
+static int hit_cmp(const void* a, const void* b) {
+  const ray_hit* x = (const ray_hit*)a;
+  const ray_hit* y = (const ray_hit*)b;
+  if (x->col != y->col) return x->col < y->col ? -1 : 1;
+  return x->seq < y->seq ? -1 : (x->seq > y->seq);
+}
+/* merge_hits (baseline.cpp:81-94): stable sort by column, lengths of equal
+ * columns summed in emission order. */
+static void merge_hits(hit_vec* v) {
+  qsort(v->h, v->n, sizeof(ray_hit), hit_cmp);
+  long m = 0;
+  for (long i = 0; i < v->n; ++i) {
+    if (m > 0 && v->h[m - 1].col == v->h[i].col)
+      v->h[m - 1].len += v->h[i].len;
+    else
+      v->h[m++] = v->h[i];
+  }
+  v->n = m;
+}
+
+/* line_weights / multiline_weights (baseline.cpp:98-128). mode 1 = line,
+ * 2 = multiline (MatrixMode order, projector.hpp:12-16). */
+static void ray_weights(const o_geom* g, int mode, int k, int m_y, int m_z, int ip,
+                        hit_vec* out) {
+  out->n = 0;
+  if (mode == 2 && k <= 0) o_fail(E_InvalidSpec, "multiline ray count must be > 0");
+  if (m_y < -g->n_det_y / 2 || m_y >= g->n_det_y / 2)
+    o_fail(E_InvalidSpec, "detector cell m_y out of range");
+  if (is_2d(g) && m_z != 0) o_fail(E_InvalidSpec, "m_z must be 0 for a 2D scan");
+  if (!is_2d(g) && (m_z < -g->n_det_z / 2 || m_z >= g->n_det_z / 2))
+    o_fail(E_InvalidSpec, "detector cell m_z out of range");
+  if (mode == 1 || k == 1) {
+    cell_ray(m_y + 0.5, is_2d(g) ? 0.0 : (m_z + 0.5), ip, g, 1.0, out);
+    if (mode == 2) merge_hits(out);
+    return;
+  }
+  if (is_2d(g)) {
+    for (int i = 0; i < k; ++i) cell_ray(m_y + (i + 0.5) / k, 0.0, ip, g, 1.0 / k, out);
+  } else {
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j)
+        cell_ray(m_y + (i + 0.5) / k, m_z + (j + 0.5) / k, ip, g, 1.0 / ((double)k * k), out);
+  }
+  merge_hits(out);
+}
+
+long ref_line_weights(const o_geom* g, int mode, int k, int m_y, int m_z, int ip, uint32_t* col,
+                      double* len, long cap) {
+  hit_vec v = {0};
+  long n = 0;
+  int st = 0;
+  {
+    jmp_buf jb;
+    jmp_buf* prev = t_jmp;
+    t_jmp = &jb;
+    if (setjmp(jb) == 0) {
+      ray_weights(g, mode, k, m_y, m_z, ip, &v);
+      t_jmp = prev;
+    } else {
+      t_jmp = prev;
+      st = -(t_code + 1);
+    }
+  }
+  if (st == 0) {
+    n = v.n;
+    for (long i = 0; i < v.n && i < cap; ++i) {
+      col[i] = v.h[i].col;
+      len[i] = v.h[i].len;
+    }
+  }
+  free(v.h);
+  return st != 0 ? st : n;
+}
+
+/* angle_block_entries for the ray modes (projector.cpp:72-83): rows in raster
+ * order (m_z outer, m_y inner), hits of each row in the ray's order. */
+static void angle_block_entries_rays(const o_geom* g, int mode, int k, int ip, emit_fn emit,
+                                     void* ctx) {
+  const int mz_lo = is_2d(g) ? 0 : -g->n_det_z / 2;
+  const int mz_hi = is_2d(g) ? 0 : g->n_det_z / 2 - 1;
+  hit_vec v = {0};
+  for (int m_z = mz_lo; m_z <= mz_hi; ++m_z)
+    for (int m_y = -g->n_det_y / 2; m_y < g->n_det_y / 2; ++m_y) {
+      ray_weights(g, mode, k, m_y, m_z, ip, &v);
+      const uint32_t row =
+          (uint32_t)((m_z + g->n_det_z / 2) * g->n_det_y + (m_y + g->n_det_y / 2));
+      for (long i = 0; i < v.n; ++i) emit(ctx, row, v.h[i].col, v.h[i].len);
+    }
+  free(v.h);
+}
+
+static void angle_block_entries_mode(const o_geom* g, int mode, int k, int ip, emit_fn emit,
+                                     void* ctx) {
+  if (mode == 0)
+    angle_block_entries(g, ip, emit, ctx);
+  else
+    angle_block_entries_rays(g, mode, k, ip, emit, ctx);
+}
+
+long ref_angle_block_entries_mode(const o_geom* g, int mode, int k, int ip, uint32_t* row,
+                                  uint32_t* col, double* w, long cap) {
+  entry_sink s = {row, col, w, 0, cap};
+  O_TRY(validate(g); angle_block_entries_mode(g, mode, k, ip, sink_emit, &s););
+  return s.n;
+}
+
 /* ---- build_system_matrix (projector.cpp:144-201) -------------------------- */
 typedef struct {
   uint64_t n_rows, n_cols;
@@ -814,7 +1019,7 @@ typedef struct {
  * are visited in column order and emit at most once per row), so a stable
  * counting sort by row reproduces the reference's stable_sort result. */
 static void bucket_by_row(const entry_vec* v, uint64_t rpa, uint64_t* counts, uint32_t* col_out,
-                          double* val_out) {
+                          double* val_out, int sort_rows) {
   uint64_t* pos = (uint64_t*)calloc(rpa + 1, sizeof(uint64_t));
   for (long i = 0; i < v->n; ++i) pos[v->row[i] + 1]++;
   for (uint64_t r = 0; r < rpa; ++r) {
@@ -827,18 +1032,40 @@ static void bucket_by_row(const entry_vec* v, uint64_t rpa, uint64_t* counts, ui
     val_out[p] = v->w[i];
   }
   free(pos);
+  if (!sort_rows) return;
+  /* ray modes: a row's hits come in ray order -> stable_sort by column
+   * (projector.cpp:100-102) */
+  hit_vec tmp = {0};
+  uint64_t off = 0;
+  for (uint64_t r = 0; r < rpa; ++r) {
+    tmp.n = 0;
+    for (uint64_t j = off; j < off + counts[r]; ++j) hit_push(&tmp, col_out[j], val_out[j]);
+    qsort(tmp.h, tmp.n, sizeof(ray_hit), hit_cmp);
+    for (long j = 0; j < tmp.n; ++j) {
+      col_out[off + j] = tmp.h[j].col;
+      val_out[off + j] = tmp.h[j].len;
+    }
+    off += counts[r];
+  }
+  free(tmp.h);
 }
 
 typedef struct {
   entry_vec* blocks;
+  int mode, k;
 } build_user;
 static void build_task(task* t, int item, int worker) {
   (void)worker;
   build_user* u = (build_user*)t->user;
-  angle_block_entries(t->g, item, vec_emit, &u->blocks[item]);
+  angle_block_entries_mode(t->g, u->mode, u->k, item, vec_emit, &u->blocks[item]);
 }
 
 void* ref_build_system_matrix(const o_geom* g, int threads, uint64_t budget, int* status) {
+  return ref_build_system_matrix_mode(g, 0, 1, threads, budget, status);
+}
+
+void* ref_build_system_matrix_mode(const o_geom* g, int mode, int k, int threads, uint64_t budget,
+                                   int* status) {
   *status = 0;
   csr* m = NULL;
   entry_vec first = {0};
@@ -856,7 +1083,7 @@ void* ref_build_system_matrix(const o_geom* g, int threads, uint64_t budget, int
     const uint64_t nvox = (uint64_t)g->n_x * g->n_y * g->n_z;
     if (nvox > 0xffffffffull) o_fail(E_TooLarge, "grid exceeds 2^32 voxel columns");
     const uint64_t n_rows = (uint64_t)g->n_angles * g->n_det_y * g->n_det_z;
-    angle_block_entries(g, 0, vec_emit, &first);
+    angle_block_entries_mode(g, mode, k, 0, vec_emit, &first);
     const uint64_t est_nnz = (uint64_t)first.n * (uint64_t)g->n_angles;
     const uint64_t est_bytes = est_nnz * (4 + 8) + (n_rows + 1) * 8;
     if (est_bytes > budget) {
@@ -871,7 +1098,7 @@ void* ref_build_system_matrix(const o_geom* g, int threads, uint64_t budget, int
   }
   const uint64_t rpa = (uint64_t)g->n_det_y * g->n_det_z;
   entry_vec* blocks = (entry_vec*)calloc(g->n_angles, sizeof(entry_vec));
-  build_user u = {blocks};
+  build_user u = {blocks, mode, k};
   task t;
   memset(&t, 0, sizeof t);
   t.fn = build_task;
@@ -906,7 +1133,7 @@ void* ref_build_system_matrix(const o_geom* g, int threads, uint64_t budget, int
   uint64_t off = 0;
   m->row_start[0] = 0;
   for (int ip = 0; ip < g->n_angles; ++ip) {
-    bucket_by_row(&blocks[ip], rpa, counts, m->col + off, m->val + off);
+    bucket_by_row(&blocks[ip], rpa, counts, m->col + off, m->val + off, mode != 0);
     for (uint64_t r = 0; r < rpa; ++r) {
       const uint64_t row = (uint64_t)ip * rpa + r;
       m->row_start[row + 1] = m->row_start[row] + counts[r];
@@ -978,6 +1205,7 @@ typedef struct {
   double* parts; /* n_sel * n_parts blocks of rpa */
   int n_parts;
   uint64_t rpa;
+  int mode, k;
 } fwd_user;
 typedef struct {
   double* block;
@@ -996,19 +1224,23 @@ static void fwd_task(task* t, int item, int worker) {
   double* block = u->parts + (uint64_t)item * u->rpa;
   memset(block, 0, u->rpa * sizeof(double));
   fwd_ctx c = {block, u->x};
-  angle_block_entries_slab(t->g, u->angles[k], lo, hi, fwd_emit, &c);
+  if (u->mode != 0)
+    angle_block_entries_rays(t->g, u->mode, u->k, u->angles[k], fwd_emit, &c);
+  else
+    angle_block_entries_slab(t->g, u->angles[k], lo, hi, fwd_emit, &c);
 }
 
 static int forward_mf_angles_impl(const o_geom* g, const int32_t* angles, int n_sel,
-                                  const double* x, double* y_sel, int threads, int split) {
+                                  const double* x, double* y_sel, int threads, int split,
+                                  int mode, int k) {
   O_TRY(validate(g););
   const uint64_t rpa = (uint64_t)g->n_det_y * g->n_det_z;
   int n_parts = 1;
-  if (split && n_sel > 0 && n_sel < threads) n_parts = (threads + n_sel - 1) / n_sel;
+  if (split && mode == 0 && n_sel > 0 && n_sel < threads) n_parts = (threads + n_sel - 1) / n_sel;
   if (n_parts > slab_extent(g)) n_parts = slab_extent(g);
   double* parts = y_sel;
   if (n_parts > 1) parts = (double*)malloc((uint64_t)n_sel * n_parts * rpa * sizeof(double));
-  fwd_user u = {angles, x, parts, n_parts, rpa};
+  fwd_user u = {angles, x, parts, n_parts, rpa, mode, k};
   task t;
   memset(&t, 0, sizeof t);
   t.fn = fwd_task;
@@ -1036,13 +1268,13 @@ static int forward_mf_angles_impl(const o_geom* g, const int32_t* angles, int n_
  * accumulation). */
 int ref_forward_mf_angles(const o_geom* g, const int32_t* angles, int n_sel, const double* x,
                           double* y_sel, int threads) {
-  return forward_mf_angles_impl(g, angles, n_sel, x, y_sel, threads, 0);
+  return forward_mf_angles_impl(g, angles, n_sel, x, y_sel, threads, 0, 0, 1);
 }
 /* Same values up to summation order; angles split into slabs so that a few
  * large angle blocks use all threads (tolerance checks at C3/C4 scale). */
 int ref_forward_mf_angles_par(const o_geom* g, const int32_t* angles, int n_sel, const double* x,
                               double* y_sel, int threads) {
-  return forward_mf_angles_impl(g, angles, n_sel, x, y_sel, threads, 1);
+  return forward_mf_angles_impl(g, angles, n_sel, x, y_sel, threads, 1, 0, 1);
 }
 
 int ref_forward_project_matrix_free(const o_geom* g, const double* x, double* y, int threads) {
@@ -1062,6 +1294,7 @@ typedef struct {
   double** part; /* per chunk slot */
   int base, n_parts;
   uint64_t rpa, nv;
+  int mode, k;
 } bwd_user;
 typedef struct {
   double* xpart;
@@ -1083,15 +1316,19 @@ static void bwd_task(task* t, int item, int worker) {
   memset(p + (uint64_t)lo * plane, 0, (uint64_t)(hi - lo) * plane * sizeof(double));
   const int ang = u->angles[u->base + k];
   bwd_ctx c = {p, u->y + (uint64_t)ang * u->rpa};
-  angle_block_entries_slab(t->g, ang, lo, hi, bwd_emit, &c);
+  if (u->mode != 0)
+    angle_block_entries_rays(t->g, u->mode, u->k, ang, bwd_emit, &c);
+  else
+    angle_block_entries_slab(t->g, ang, lo, hi, bwd_emit, &c);
 }
 
 static int back_mf_angles_impl(const o_geom* g, const int32_t* angles, int n_sel,
-                               const double* y, double* x, int threads, int split) {
+                               const double* y, double* x, int threads, int split, int mode,
+                               int k) {
   O_TRY(validate(g););
   const uint64_t nv = (uint64_t)g->n_x * g->n_y * g->n_z;
   int n_parts = 1;
-  if (split && n_sel > 0 && n_sel < threads) n_parts = (threads + n_sel - 1) / n_sel;
+  if (split && mode == 0 && n_sel > 0 && n_sel < threads) n_parts = (threads + n_sel - 1) / n_sel;
   if (n_parts > slab_extent(g)) n_parts = slab_extent(g);
   const int chunk = n_parts > 1 ? n_sel : (threads < 1 ? 1 : threads);
   double** part = (double**)malloc(sizeof(double*) * (chunk > 0 ? chunk : 1));
@@ -1100,7 +1337,7 @@ static int back_mf_angles_impl(const o_geom* g, const int32_t* angles, int n_sel
   int st = 0;
   for (int k0 = 0; k0 < n_sel && st == 0; k0 += chunk) {
     const int n = (n_sel - k0) < chunk ? (n_sel - k0) : chunk;
-    bwd_user u = {angles, y, part, k0, n_parts, (uint64_t)g->n_det_y * g->n_det_z, nv};
+    bwd_user u = {angles, y, part, k0, n_parts, (uint64_t)g->n_det_y * g->n_det_z, nv, mode, k};
     task t;
     memset(&t, 0, sizeof t);
     t.fn = bwd_task;
@@ -1120,17 +1357,37 @@ static int back_mf_angles_impl(const o_geom* g, const int32_t* angles, int n_sel
 
 int ref_back_mf_angles(const o_geom* g, const int32_t* angles, int n_sel, const double* y,
                        double* x, int threads) {
-  return back_mf_angles_impl(g, angles, n_sel, y, x, threads, 0);
+  return back_mf_angles_impl(g, angles, n_sel, y, x, threads, 0, 0, 1);
 }
 int ref_back_mf_angles_par(const o_geom* g, const int32_t* angles, int n_sel, const double* y,
                            double* x, int threads) {
-  return back_mf_angles_impl(g, angles, n_sel, y, x, threads, 1);
+  return back_mf_angles_impl(g, angles, n_sel, y, x, threads, 1, 0, 1);
 }
 
 int ref_back_project_matrix_free(const o_geom* g, const double* y, double* x, int threads) {
   int32_t* all = (int32_t*)malloc(sizeof(int32_t) * (g->n_angles > 0 ? g->n_angles : 1));
   for (int i = 0; i < g->n_angles; ++i) all[i] = i;
   const int st = ref_back_mf_angles(g, all, g->n_angles, y, x, threads);
+  free(all);
+  return st;
+}
+
+/* forward_project_matrix_free / the a16 adjoint for any MatrixMode. */
+static int32_t* all_angles(const o_geom* g) {
+  int32_t* all = (int32_t*)malloc(sizeof(int32_t) * (g->n_angles > 0 ? g->n_angles : 1));
+  for (int i = 0; i < g->n_angles; ++i) all[i] = i;
+  return all;
+}
+int ref_forward_mf_mode(const o_geom* g, int mode, int k, const double* x, double* y,
+                        int threads) {
+  int32_t* all = all_angles(g);
+  const int st = forward_mf_angles_impl(g, all, g->n_angles, x, y, threads, 0, mode, k);
+  free(all);
+  return st;
+}
+int ref_back_mf_mode(const o_geom* g, int mode, int k, const double* y, double* x, int threads) {
+  int32_t* all = all_angles(g);
+  const int st = back_mf_angles_impl(g, all, g->n_angles, y, x, threads, 0, mode, k);
   free(all);
   return st;
 }

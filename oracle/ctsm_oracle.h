@@ -1,8 +1,9 @@
 /* ctsm_oracle.h -- TEST INFRASTRUCTURE ONLY.
  *
- * Plain-C restatement of the reference hot path (consistent mode only). It
- * exports the same extern "C" entry points as ref_shim.cpp, so tests can drive
- * the restatement and the compiled reference interchangeably. Only tests/,
+ * Plain-C restatement of the reference hot path (consistent, line and
+ * multiline modes). It exports the same extern "C" entry points as
+ * ref_shim.cpp, so tests can drive the restatement and the compiled reference
+ * interchangeably. Only tests/,
  * __graft_entry__.smoke() and bench.py's cpu_baseline leg may load it; the
  * product never links or calls it.
  *
@@ -58,6 +59,16 @@ long ref_angle_block_entries_par(const o_geom* g, int ip, uint32_t* row, uint32_
                                  long cap, int threads);
 int ref_sirt(const o_geom* g, const double* y, double* x, int iters, int threads);
 int ref_angle_column_sums(const o_geom* g, int ip, double* sums);
+/* line / multiline modes (baseline.cpp:13-128; mode 1 = line, 2 = multiline,
+ * 0 = consistent as above). */
+long ref_line_weights(const o_geom* g, int mode, int k, int m_y, int m_z, int ip, uint32_t* col,
+                      double* len, long cap);
+long ref_angle_block_entries_mode(const o_geom* g, int mode, int k, int ip, uint32_t* row,
+                                  uint32_t* col, double* w, long cap);
+void* ref_build_system_matrix_mode(const o_geom* g, int mode, int k, int threads, uint64_t budget,
+                                   int* status);
+int ref_forward_mf_mode(const o_geom* g, int mode, int k, const double* x, double* y, int threads);
+int ref_back_mf_mode(const o_geom* g, int mode, int k, const double* y, double* x, int threads);
 
 #ifdef __cplusplus
 }

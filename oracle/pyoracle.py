@@ -42,6 +42,10 @@ ERROR_NAMES = [
 ]
 
 
+# MatrixMode ordinals (projector.hpp:12-16)
+MODES = {"consistent": 0, "line": 1, "multiline": 2}
+
+
 class OGeom(ctypes.Structure):
     """Mirror of ScanGeometry (geometry.hpp:29-44) == ctsm_geometry."""
 
@@ -140,6 +144,17 @@ class Oracle:
                                                       ctypes.c_int]
             L.ref_angle_block_entries_par.restype = ctypes.c_long
         L.ref_angle_column_sums.argtypes = [_P, ctypes.c_int, _P]
+        L.ref_line_weights.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, _P, _P, ctypes.c_long]
+        L.ref_line_weights.restype = ctypes.c_long
+        L.ref_build_system_matrix_mode.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                   ctypes.c_uint64, ctypes.POINTER(ctypes.c_int)]
+        L.ref_build_system_matrix_mode.restype = _P
+        L.ref_angle_block_entries_mode.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                   _P, _P, _P, ctypes.c_long]
+        L.ref_angle_block_entries_mode.restype = ctypes.c_long
+        L.ref_forward_mf_mode.argtypes = [_P, ctypes.c_int, ctypes.c_int, _P, _P, ctypes.c_int]
+        L.ref_back_mf_mode.argtypes = [_P, ctypes.c_int, ctypes.c_int, _P, _P, ctypes.c_int]
         # reference-only entry points (solver / io / phantoms), absent in the ports
         self.has_solver = hasattr(L, "ref_nag_tikhonov")
         if self.has_solver:
@@ -194,11 +209,21 @@ class Oracle:
         self._check(n)
         return my[:n].copy(), mz[:n].copy(), w[:n].copy()
 
-    def angle_block_entries(self, g, ip: int, threads: int = 1):
+    def angle_block_entries(self, g, ip: int, threads: int = 1, mode: str = "consistent",
+                            k: int = 1):
         """(row_raster u32, col u32, w f64) in emission order (projector.cpp:44-84).
         threads > 1 (restatement only) computes slabs in parallel; the result is
         identical."""
         og, p = self._g(g)
+        if mode != "consistent":
+            f = self.lib.ref_angle_block_entries_mode
+            n = f(p, MODES[mode], k, ip, None, None, None, 0)
+            self._check(n)
+            row = np.empty(n, np.uint32)
+            col = np.empty(n, np.uint32)
+            w = np.empty(n, np.float64)
+            self._check(f(p, MODES[mode], k, ip, _ptr(row), _ptr(col), _ptr(w), n))
+            return row, col, w
         if threads > 1 and self.has_par:
             f = self.lib.ref_angle_block_entries_par
             n = int(1.3 * 12 * g.n_x * g.n_y * g.n_z) + 1024
@@ -220,10 +245,12 @@ class Oracle:
         self._check(n2)
         return row, col, w
 
-    def build_system_matrix(self, g, threads: int = 1, budget: int = 5 << 30) -> Csr:
+    def build_system_matrix(self, g, threads: int = 1, budget: int = 5 << 30,
+                            mode: str = "consistent", k: int = 1) -> Csr:
         og, p = self._g(g)
         st = ctypes.c_int(0)
-        h = self.lib.ref_build_system_matrix(p, threads, budget, ctypes.byref(st))
+        h = self.lib.ref_build_system_matrix_mode(p, MODES[mode], k, threads, budget,
+                                                  ctypes.byref(st))
         self._check(st.value)
         try:
             nnz = self.lib.ref_csr_nnz(h)
@@ -236,19 +263,41 @@ class Oracle:
             self.lib.ref_csr_free(h)
         return Csr(rs, col, val)
 
-    def forward_project_matrix_free(self, g, x: np.ndarray, threads: int = 1) -> np.ndarray:
+    def forward_project_matrix_free(self, g, x: np.ndarray, threads: int = 1,
+                                    mode: str = "consistent", k: int = 1) -> np.ndarray:
         og, p = self._g(g)
         x = np.ascontiguousarray(x, np.float64)
         y = np.zeros(g.n_angles * g.n_det_y * g.n_det_z, np.float64)
-        self._check(self.lib.ref_forward_project_matrix_free(p, _ptr(x), _ptr(y), threads))
+        if mode == "consistent":
+            self._check(self.lib.ref_forward_project_matrix_free(p, _ptr(x), _ptr(y), threads))
+        else:
+            self._check(self.lib.ref_forward_mf_mode(p, MODES[mode], k, _ptr(x), _ptr(y), threads))
         return y
 
-    def back_project_matrix_free(self, g, y: np.ndarray, threads: int = 1) -> np.ndarray:
+    def back_project_matrix_free(self, g, y: np.ndarray, threads: int = 1,
+                                 mode: str = "consistent", k: int = 1) -> np.ndarray:
         og, p = self._g(g)
         y = np.ascontiguousarray(y, np.float64)
         x = np.zeros(g.n_x * g.n_y * g.n_z, np.float64)
-        self._check(self.lib.ref_back_project_matrix_free(p, _ptr(y), _ptr(x), threads))
+        if mode == "consistent":
+            self._check(self.lib.ref_back_project_matrix_free(p, _ptr(y), _ptr(x), threads))
+        else:
+            self._check(self.lib.ref_back_mf_mode(p, MODES[mode], k, _ptr(y), _ptr(x), threads))
         return x
+
+    def line_weights(self, g, m_y: int, m_z: int, ip: int, mode: str = "line", k: int = 1):
+        """line_weights / multiline_weights (baseline.cpp:98-128): (col, len)."""
+        og, p = self._g(g)
+        n = 4096
+        for _ in range(2):
+            col = np.empty(n, np.uint32)
+            ln = np.empty(n, np.float64)
+            m = self.lib.ref_line_weights(p, MODES[mode], k, m_y, m_z, ip, _ptr(col), _ptr(ln), n)
+            self._check(m)
+            if m <= n:
+                return col[:m].copy(), ln[:m].copy()
+            n = m
+        raise AssertionError("unreachable")
 
     def forward_mf_angles(self, g, angles, x: np.ndarray, threads: int = 1,
                           split: bool = False) -> np.ndarray:

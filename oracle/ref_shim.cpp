@@ -23,6 +23,7 @@
 #include <thread>
 #include <vector>
 
+#include "ctsm/baseline.hpp"
 #include "ctsm/geometry.hpp"
 #include "ctsm/io.hpp"
 #include "ctsm/phantoms.hpp"
@@ -358,4 +359,89 @@ int ref_angle_column_sums(const RefGeom* rg, int ip, double* sums) {
             std::copy(v.begin(), v.end(), sums); return 0;)
 }
 
+// ---- line / multiline modes ------------------------
+// mode: 0 consistent, 1 line, 2 multiline (MatrixMode order, projector.hpp:12-16).
+static ctsm::MatrixMode to_mode(int m) {
+  return m == 1 ? ctsm::MatrixMode::line
+                : (m == 2 ? ctsm::MatrixMode::multiline : ctsm::MatrixMode::consistent);
+}
+
+// line_weights / multiline_weights (baseline.cpp:99-128): hits of one
+// detector cell in the reference's order; returns the count (<= cap stored).
+long ref_line_weights(const RefGeom* rg, int mode, int k, int m_y, int m_z, int ip, uint32_t* col,
+                      double* len, long cap) {
+  REF_GUARD(const ctsm::ScanGeometry g = to_g(rg);
+            const auto hits = mode == 1 ? ctsm::line_weights(m_y, m_z, ip, g)
+                                        : ctsm::multiline_weights(m_y, m_z, ip, g, k);
+            for (long i = 0; i < (long)hits.size() && i < cap; ++i) {
+              col[i] = hits[i].col;
+              len[i] = hits[i].len;
+            } return (long)hits.size();)
+}
+
+// detail::angle_block_entries (projector.cpp:44-84) for any mode.
+long ref_angle_block_entries_mode(const RefGeom* rg, int mode, int k, int ip, uint32_t* row,
+                                  uint32_t* col, double* w, long cap) {
+  REF_GUARD(long n = 0; ctsm::detail::angle_block_entries(
+                to_g(rg), to_mode(mode), k, ip,
+                [&](uint32_t r, uint32_t c, double v) {
+                  if (n < cap) {
+                    row[n] = r;
+                    col[n] = c;
+                    w[n] = v;
+                  }
+                  ++n;
+                });
+            return n;)
+}
+
+void* ref_build_system_matrix_mode(const RefGeom* rg, int mode, int k, int threads,
+                                   uint64_t budget, int* status) {
+  try {
+    auto* m = new ctsm::SparseSystemMatrix(
+        ctsm::build_system_matrix(to_g(rg), to_mode(mode), k, threads, budget));
+    *status = 0;
+    return m;
+  } catch (const ctsm::Error& e) {
+    *status = fail_code(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    *status = -100;
+  }
+  return nullptr;
+}
+
+int ref_forward_mf_mode(const RefGeom* rg, int mode, int k, const double* x, double* y,
+                        int threads) {
+  REF_GUARD(const ctsm::ScanGeometry g = to_g(rg);
+            const std::vector<double> xv(x, x + g.n_voxels());
+            const auto yv = ctsm::forward_project_matrix_free(g, to_mode(mode), k, xv, threads);
+            std::copy(yv.begin(), yv.end(), y); return 0;)
+}
+
+// matrix-free A^T y for any mode: the a16 restatement through
+// detail::angle_block_entries(mode, k), per-angle partials summed in angle order.
+int ref_back_mf_mode(const RefGeom* rg, int mode, int k, const double* y, double* x,
+                     int threads) {
+  REF_GUARD(const ctsm::ScanGeometry g = to_g(rg); g.validate();
+            const uint64_t rpa = (uint64_t)g.n_det_y * g.n_det_z;
+            const uint64_t nv = g.n_voxels(); std::fill(x, x + nv, 0.0);
+            const int chunk = std::max(1, threads);
+            std::vector<std::vector<double>> part(chunk);
+            for (int k0 = 0; k0 < g.n_angles; k0 += chunk) {
+              const int n = std::min(chunk, g.n_angles - k0);
+              parallel_range(n, threads, [&](int t) {
+                auto& p = part[t];
+                p.assign(nv, 0.0);
+                const double* yb = y + (uint64_t)(k0 + t) * rpa;
+                ctsm::detail::angle_block_entries(
+                    g, to_mode(mode), k, k0 + t,
+                    [&](uint32_t r, uint32_t c, double wv) { p[c] += wv * yb[r]; });
+              });
+              for (int t = 0; t < n; ++t)
+                for (uint64_t i = 0; i < nv; ++i) x[i] += part[t][i];
+            } return 0;)
+}
+
 }  // extern "C"
+

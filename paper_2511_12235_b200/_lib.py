@@ -59,6 +59,10 @@ SIGNATURES = {
     "ctsm_sirt_residual": (_I, [_P, _GP, _I, _I, _I, _I, _P, _P, _P, _P]),
     "ctsm_sirt_update": (_I, [_P, _I, _U64, _P, _P, _P, _P]),
     "ctsm_sirt": (_I, [_P, _GP, _I, _P, _P, _I, _P]),
+    "ctsm_csr_count_mode": (_I, [_P, _GP, _I, _I, _I, _I, _U64, _P, ctypes.POINTER(_U64), _P]),
+    "ctsm_csr_fill_mode": (_I, [_P, _GP, _I, _I, _I, _I, _P, _P, _P, _P]),
+    "ctsm_fwd_mf_mode": (_I, [_P, _GP, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
+    "ctsm_bwd_mf_mode": (_I, [_P, _GP, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
     "ctsm_forward_project_matrix_free_host": (_I, [_P, _GP, _P, _P]),
     "ctsm_back_project_matrix_free_host": (_I, [_P, _GP, _P, _P]),
     "ctsm_spectral_norm_power": (_I, [_P, _OP, _I, _P, ctypes.POINTER(_D), _P]),

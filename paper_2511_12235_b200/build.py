@@ -1,6 +1,6 @@
 """Builds paper_2511_12235_b200/libctsm_b200.so with nvcc for sm_100a.
 
-csr.cu (bit-exact CSR emission) is compiled with -fmad=false so that no FMA
+csr.cu and line.cu (bit-exact CSR emission) are compiled with -fmad=false so that no FMA
 contraction changes the reference's rounding; the
 matrix-free kernels (mf.cu) keep contraction on.
 """
@@ -20,6 +20,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
           "-I" + CSRC, "-I" + os.path.join(HERE, "..", "include")] + ARCH
 UNITS = {
     "csr.cu": ["-fmad=false"],
+    "line.cu": ["-fmad=false"],
     "mf.cu": [],
     "solver.cu": ["-fmad=false"],
     "capi.cu": [],

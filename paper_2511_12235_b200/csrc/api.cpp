@@ -97,11 +97,8 @@ void d2h(T* h, const T* d, size_t n) {
     throw std::runtime_error("cudaMemcpy D2H failed");
 }
 
-void require_consistent(MatrixMode mode) {
-  if (mode != MatrixMode::consistent)
-    throw Error(ErrorCode::InvalidSpec,
-                "only the consistent matrix mode is provided on the device path");
-}
+// MatrixMode ordinal for the C-ABI (CTSM_MODE_*; projector.hpp:12-16).
+int mode_code(MatrixMode mode) { return static_cast<int>(mode); }
 
 // phantoms.cpp:78-87 convention (mt19937_64, Box-Muller cosine branch)
 std::vector<double> normal_samples(std::size_t n, std::uint64_t seed) {
@@ -150,7 +147,6 @@ std::string matrix_mode_name(MatrixMode mode, int k) {
 SparseSystemMatrix build_system_matrix(const ScanGeometry& g, MatrixMode mode, int k, int threads,
                                        std::uint64_t memory_budget_bytes) {
   (void)threads;
-  require_consistent(mode);
   const ctsm_geometry c = to_c(g);
   check(ctsm_validate_geometry(&c));
   SparseSystemMatrix w;
@@ -158,10 +154,12 @@ SparseSystemMatrix build_system_matrix(const ScanGeometry& g, MatrixMode mode, i
   w.n_cols = g.n_voxels();
   DevBuf<std::uint64_t> rs(w.n_rows + 1);
   std::uint64_t nnz = 0;
-  check(ctsm_csr_count(ctx(), &c, 0, g.n_angles, memory_budget_bytes, rs.p, &nnz, nullptr));
+  check(ctsm_csr_count_mode(ctx(), &c, mode_code(mode), k, 0, g.n_angles, memory_budget_bytes,
+                            rs.p, &nnz, nullptr));
   DevBuf<std::uint32_t> col(nnz);
   DevBuf<double> val(nnz);
-  check(ctsm_csr_fill(ctx(), &c, 0, g.n_angles, rs.p, col.p, val.p, nullptr));
+  check(ctsm_csr_fill_mode(ctx(), &c, mode_code(mode), k, 0, g.n_angles, rs.p, col.p, val.p,
+                           nullptr));
   w.row_start.resize(w.n_rows + 1);
   w.col.resize(nnz);
   w.val.resize(nnz);
@@ -219,29 +217,41 @@ std::vector<double> back_project(const SparseSystemMatrix& w, const std::vector<
 
 std::vector<double> forward_project_matrix_free(const ScanGeometry& g, MatrixMode mode, int k,
                                                 const std::vector<double>& x, int threads) {
-  (void)k;
   (void)threads;
-  require_consistent(mode);
   g.validate();
   if (x.size() != g.n_voxels())
     throw Error(ErrorCode::DimensionMismatch, "image size does not match the grid");
   const ctsm_geometry c = to_c(g);
   std::vector<double> y(g.n_measurements());
-  check(ctsm_forward_project_matrix_free_host(ctx(), &c, x.data(), y.data()));
+  if (mode == MatrixMode::consistent) {
+    check(ctsm_forward_project_matrix_free_host(ctx(), &c, x.data(), y.data()));
+    return y;
+  }
+  DevBuf<double> xd(x.size()), yd(y.size());
+  h2d(xd.p, x.data(), x.size());
+  check(ctsm_fwd_mf_mode(ctx(), &c, mode_code(mode), k, CTSM_F64, 0, g.n_angles, 1, xd.p, yd.p,
+                         nullptr));
+  d2h(y.data(), yd.p, y.size());
   return y;
 }
 
 std::vector<double> back_project_matrix_free(const ScanGeometry& g, MatrixMode mode, int k,
                                              const std::vector<double>& y, int threads) {
-  (void)k;
   (void)threads;
-  require_consistent(mode);
   g.validate();
   if (y.size() != g.n_measurements())
     throw Error(ErrorCode::DimensionMismatch, "sinogram size does not match the scan");
   const ctsm_geometry c = to_c(g);
   std::vector<double> x(g.n_voxels());
-  check(ctsm_back_project_matrix_free_host(ctx(), &c, y.data(), x.data()));
+  if (mode == MatrixMode::consistent) {
+    check(ctsm_back_project_matrix_free_host(ctx(), &c, y.data(), x.data()));
+    return x;
+  }
+  DevBuf<double> yd(y.size()), xd(x.size());
+  h2d(yd.p, y.data(), y.size());
+  check(ctsm_bwd_mf_mode(ctx(), &c, mode_code(mode), k, CTSM_F64, 0, g.n_angles, 1, yd.p, xd.p,
+                         nullptr));
+  d2h(x.data(), xd.p, x.size());
   return x;
 }
 
@@ -356,14 +366,13 @@ void scale_values(SparseSystemMatrix* w, double factor) {
 
 std::vector<double> angle_column_sums(const ScanGeometry& g, MatrixMode mode, int k,
                                       int angle_index) {
-  (void)k;
-  require_consistent(mode);
   g.validate();
   const ctsm_geometry c = to_c(g);
   DevBuf<double> yd(g.n_measurements()), xd(g.n_voxels());
   std::vector<double> ones(g.n_measurements(), 1.0), x(g.n_voxels());
   h2d(yd.p, ones.data(), ones.size());
-  check(ctsm_bwd_mf(ctx(), &c, CTSM_F64, angle_index, angle_index + 1, 1, yd.p, xd.p, nullptr));
+  check(ctsm_bwd_mf_mode(ctx(), &c, mode_code(mode), k, CTSM_F64, angle_index, angle_index + 1,
+                         1, yd.p, xd.p, nullptr));
   d2h(x.data(), xd.p, x.size());
   return x;
 }

@@ -72,7 +72,7 @@ struct ctsm_ctx {
   double* h_red = nullptr;      // pinned
   Buf angles, edges, cs, counts, scan, longrows, acc, part, base, alist, sv_up, sv_h, sv_hp,
       sv_q, sv_v, sv_part, sv_scal, tmp_a, tmp_b, tmp_c, tmp_d,
-      tmp_e, tmp_f;
+      tmp_e, tmp_f, lraw_start, lraw_col, lraw_val, lacc;
 };
 
 namespace {
@@ -235,7 +235,8 @@ int ctsm_destroy(ctsm_ctx* ctx) {
   Buf* bufs[] = {&ctx->angles, &ctx->edges, &ctx->cs,    &ctx->counts, &ctx->scan,
                  &ctx->longrows, &ctx->acc, &ctx->part, &ctx->base, &ctx->alist, &ctx->sv_up, &ctx->sv_h, &ctx->sv_hp, &ctx->sv_q,
                  &ctx->sv_v, &ctx->sv_part, &ctx->sv_scal, &ctx->tmp_a, &ctx->tmp_b,  &ctx->tmp_c,
-                 &ctx->tmp_d, &ctx->tmp_e, &ctx->tmp_f};
+                 &ctx->tmp_d, &ctx->tmp_e, &ctx->tmp_f, &ctx->lraw_start, &ctx->lraw_col,
+                 &ctx->lraw_val, &ctx->lacc};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   cudaFree(ctx->status);
@@ -680,6 +681,205 @@ int ctsm_bwd_mf(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begi
   CT_TRY(set_device(ctx));
   cudaStream_t st = (cudaStream_t)stream;
   CT_TRY(bwd_impl(ctx, g, dtype, angle_begin, angle_end, angle_step, y_dev, x_dev, st));
+  return check_status(ctx, st, "back_project_matrix_free");
+}
+
+// ---- line / multiline modes (baseline.cpp:13-128) ----
+static int check_mode(int mode, int k) {
+  if (mode != CTSM_MODE_CONSISTENT && mode != CTSM_MODE_LINE && mode != CTSM_MODE_MULTILINE)
+    return fail(CTSM_ERR_INVALID_SPEC, "unknown matrix mode");
+  if (mode == CTSM_MODE_MULTILINE && k <= 0)
+    return fail(CTSM_ERR_INVALID_SPEC, "multiline ray count must be > 0");
+  return 0;
+}
+
+// Final (merged) entry counts of the ray-mode rows of angles [angle_begin,
+// angle_begin + n_sel) into ctx->counts. Multiline rows are traced into
+// ctx->lraw_* (offsets ctx->lraw_start) and merged there in place
+// (merge_hits, baseline.cpp:81-94); line rows have distinct columns already.
+static int ray_rows(ctsm_ctx* ctx, const DevGeom& d, int mode, int k, int angle_begin, int n_sel,
+                    cudaStream_t st) {
+  const uint64_t n_rows = (uint64_t)d.rows_per_angle * n_sel;
+  CT_TRY(ensure(ctx, ctx->angles, (size_t)(n_sel > 0 ? n_sel : 1) * ray_angle_bytes()));
+  CT_CUDA(ray_angle_table(d, angle_begin, 1, n_sel, ctx->angles.p, st));
+  CT_TRY(ensure(ctx, ctx->counts, (n_rows ? n_rows : 1) * sizeof(unsigned)));
+  CT_CUDA(ray_count(d, ctx->angles.p, mode, k, n_rows, (unsigned*)ctx->counts.p, st));
+  if (mode == CTSM_MODE_LINE || k == 1) return 0;
+  CT_TRY(ensure(ctx, ctx->lraw_start, (n_rows + 1) * sizeof(uint64_t)));
+  CT_TRY(ensure(ctx, ctx->scan, scan_scratch_bytes(n_rows)));
+  CT_CUDA(exclusive_scan_u32_u64((const unsigned*)ctx->counts.p, n_rows,
+                                 (uint64_t*)ctx->lraw_start.p, ctx->scan.p, st));
+  uint64_t raw = 0;
+  CT_CUDA(cudaMemcpyAsync(&raw, (uint64_t*)ctx->lraw_start.p + n_rows, sizeof(uint64_t),
+                          cudaMemcpyDeviceToHost, st));
+  CT_CUDA(cudaStreamSynchronize(st));
+  CT_TRY(ensure(ctx, ctx->lraw_col, (raw ? raw : 1) * sizeof(uint32_t)));
+  CT_TRY(ensure(ctx, ctx->lraw_val, (raw ? raw : 1) * sizeof(double)));
+  CT_CUDA(ray_fill(d, ctx->angles.p, mode, k, n_rows, (const uint64_t*)ctx->lraw_start.p,
+                   (uint32_t*)ctx->lraw_col.p, (double*)ctx->lraw_val.p, st));
+  CT_TRY(ensure(ctx, ctx->longrows, (n_rows + 1) * sizeof(unsigned)));
+  CT_CUDA(ray_sort_merge(n_rows, (const uint64_t*)ctx->lraw_start.p, (unsigned*)ctx->counts.p,
+                         (uint32_t*)ctx->lraw_col.p, (double*)ctx->lraw_val.p,
+                         (unsigned*)ctx->longrows.p, (unsigned*)ctx->longrows.p + n_rows,
+                         ctx->status, st));
+  return 0;
+}
+
+// Bound on any column sum of a line / multiline matrix over one angle: the
+// (sub-)rays through a voxel land in its detector footprint, whose width is
+// at most W = diag * sdd / D (1 + U / D) per axis (D >= s - R_xy the least
+// depth, U the largest lateral offset); at most k W / pitch + 1 sub-rays of
+// weight <= diag / k (k^2 W_y W_z / pitch^2 .. in 3D) cross it.
+static double ray_colsum_bound(const ctsm_geometry* g) {
+  const bool two_d = g->n_z == 1 && g->n_det_z == 1;
+  const double rxy = std::hypot(g->n_x * g->a / 2.0, g->n_y * g->b / 2.0);
+  const double zmax = g->n_z * g->c / 2.0;
+  const double diag = two_d ? std::hypot(g->a, g->b)
+                            : std::sqrt(g->a * g->a + g->b * g->b + g->c * g->c);
+  const double dmin = g->s - rxy, sdd = g->s + g->d;
+  const double wy = diag * sdd / dmin * (1.0 + rxy / dmin);
+  double b = diag * (wy / g->d_y + 2.0);
+  if (!two_d) b *= diag * sdd / dmin * (1.0 + zmax / dmin) / g->d_z + 2.0;
+  return 2.0 * b;
+}
+
+int ctsm_csr_count_mode(ctsm_ctx* ctx, const ctsm_geometry* g, int mode, int k, int angle_begin,
+                        int angle_end, uint64_t memory_budget_bytes, uint64_t* row_start_dev,
+                        uint64_t* nnz_out, void* stream) {
+  CT_TRY(check_mode(mode, k));
+  if (mode == CTSM_MODE_CONSISTENT)
+    return ctsm_csr_count(ctx, g, angle_begin, angle_end, memory_budget_bytes, row_start_dev,
+                          nnz_out, stream);
+  CT_TRY(set_device(ctx));
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  if ((uint64_t)g->n_x * g->n_y * g->n_z > 0xffffffffull)
+    return fail(CTSM_ERR_TOO_LARGE, "grid exceeds 2^32 voxel columns");
+  CT_TRY(check_shard(g, angle_begin, angle_end, 1));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_sel = angle_end - angle_begin;
+  const uint64_t rpa = (uint64_t)d.rows_per_angle;
+  const uint64_t n_rows = rpa * n_sel;
+  const uint64_t n_meas = rpa * (uint64_t)g->n_angles;
+  {  // budget estimate from angle 0 (projector.cpp:155-169)
+    CT_TRY(ray_rows(ctx, d, mode, k, 0, 1, st));
+    CT_TRY(ensure(ctx, ctx->tmp_a, (rpa + 1) * sizeof(uint64_t)));
+    CT_TRY(ensure(ctx, ctx->scan, scan_scratch_bytes(rpa)));
+    CT_CUDA(exclusive_scan_u32_u64((const unsigned*)ctx->counts.p, rpa, (uint64_t*)ctx->tmp_a.p,
+                                   ctx->scan.p, st));
+    uint64_t nnz0 = 0;
+    CT_CUDA(cudaMemcpyAsync(&nnz0, (uint64_t*)ctx->tmp_a.p + rpa, sizeof(uint64_t),
+                            cudaMemcpyDeviceToHost, st));
+    CT_TRY(check_status(ctx, st, "build_system_matrix"));
+    const uint64_t est_nnz = nnz0 * (uint64_t)g->n_angles;
+    const uint64_t est_bytes = est_nnz * (sizeof(uint32_t) + sizeof(double)) +
+                               (n_meas + 1) * sizeof(uint64_t);
+    if (est_bytes > memory_budget_bytes) {
+      char msg[256];
+      snprintf(msg, sizeof msg, "estimated %llu entries (%llu MiB) exceed the budget of %llu MiB",
+               (unsigned long long)est_nnz, (unsigned long long)(est_bytes >> 20),
+               (unsigned long long)(memory_budget_bytes >> 20));
+      return fail(CTSM_ERR_OUT_OF_MEMORY, msg);
+    }
+  }
+  CT_TRY(ray_rows(ctx, d, mode, k, angle_begin, n_sel, st));
+  CT_TRY(ensure(ctx, ctx->scan, scan_scratch_bytes(n_rows)));
+  CT_CUDA(exclusive_scan_u32_u64((const unsigned*)ctx->counts.p, n_rows, row_start_dev,
+                                 ctx->scan.p, st));
+  uint64_t nnz = 0;
+  CT_CUDA(cudaMemcpyAsync(&nnz, row_start_dev + n_rows, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                          st));
+  CT_TRY(check_status(ctx, st, "build_system_matrix"));
+  if (angle_begin == 0 && angle_end == g->n_angles && nnz == 0)
+    return fail(CTSM_ERR_ZERO_MATRIX, "system matrix has no entries");
+  *nnz_out = nnz;
+  return 0;
+}
+
+int ctsm_csr_fill_mode(ctsm_ctx* ctx, const ctsm_geometry* g, int mode, int k, int angle_begin,
+                       int angle_end, const uint64_t* row_start_dev, uint32_t* col_dev,
+                       double* val_dev, void* stream) {
+  CT_TRY(check_mode(mode, k));
+  if (mode == CTSM_MODE_CONSISTENT)
+    return ctsm_csr_fill(ctx, g, angle_begin, angle_end, row_start_dev, col_dev, val_dev, stream);
+  CT_TRY(set_device(ctx));
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  CT_TRY(check_shard(g, angle_begin, angle_end, 1));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_sel = angle_end - angle_begin;
+  const uint64_t n_rows = (uint64_t)d.rows_per_angle * n_sel;
+  if (mode == CTSM_MODE_LINE || k == 1) {
+    // rays traced straight into the caller's rows, then the stable column sort
+    CT_TRY(ensure(ctx, ctx->angles, (size_t)(n_sel > 0 ? n_sel : 1) * ray_angle_bytes()));
+    CT_CUDA(ray_angle_table(d, angle_begin, 1, n_sel, ctx->angles.p, st));
+    CT_CUDA(ray_fill(d, ctx->angles.p, mode, k, n_rows, row_start_dev, col_dev, val_dev, st));
+    CT_TRY(ensure(ctx, ctx->counts, (n_rows ? n_rows : 1) * sizeof(unsigned)));
+    CT_TRY(ensure(ctx, ctx->longrows, (n_rows + 1) * sizeof(unsigned)));
+    CT_CUDA(ray_sort_merge(n_rows, row_start_dev, (unsigned*)ctx->counts.p, col_dev, val_dev,
+                           (unsigned*)ctx->longrows.p, (unsigned*)ctx->longrows.p + n_rows,
+                           ctx->status, st));
+  } else {
+    CT_TRY(ray_rows(ctx, d, mode, k, angle_begin, n_sel, st));
+    CT_CUDA(ray_compact(n_rows, (const uint64_t*)ctx->lraw_start.p, row_start_dev,
+                        (const uint32_t*)ctx->lraw_col.p, (const double*)ctx->lraw_val.p, col_dev,
+                        val_dev, st));
+  }
+  return check_status(ctx, st, "build_system_matrix");
+}
+
+int ctsm_fwd_mf_mode(ctsm_ctx* ctx, const ctsm_geometry* g, int mode, int k, int dtype,
+                     int angle_begin, int angle_end, int angle_step, const void* x_dev,
+                     void* y_dev, void* stream) {
+  CT_TRY(check_mode(mode, k));
+  if (mode == CTSM_MODE_CONSISTENT)
+    return ctsm_fwd_mf(ctx, g, dtype, angle_begin, angle_end, angle_step, x_dev, y_dev, stream);
+  CT_TRY(set_device(ctx));
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  CT_TRY(check_dtype(dtype));
+  CT_TRY(check_shard(g, angle_begin, angle_end, angle_step));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_sel = n_in_shard(angle_begin, angle_end, angle_step);
+  CT_TRY(ensure(ctx, ctx->angles, (size_t)(n_sel > 0 ? n_sel : 1) * ray_angle_bytes()));
+  CT_CUDA(ray_angle_table(d, angle_begin, angle_step, n_sel, ctx->angles.p, st));
+  CT_CUDA(cudaMemsetAsync(ctx->n_upd, 0, sizeof(unsigned long long), st));
+  CT_CUDA(ray_fwd_mf(d, dtype, ctx->angles.p, mode, k, angle_begin, angle_step, n_sel, x_dev,
+                     y_dev, ctx->n_upd, ctx->status, st));
+  CT_CUDA(cudaMemcpyAsync(ctx->h_upd, ctx->n_upd, sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, st));
+  CT_TRY(check_status(ctx, st, "forward_project_matrix_free"));
+  ctx->last_updates = *ctx->h_upd;
+  return 0;
+}
+
+int ctsm_bwd_mf_mode(ctsm_ctx* ctx, const ctsm_geometry* g, int mode, int k, int dtype,
+                     int angle_begin, int angle_end, int angle_step, const void* y_dev,
+                     void* x_dev, void* stream) {
+  CT_TRY(check_mode(mode, k));
+  if (mode == CTSM_MODE_CONSISTENT)
+    return ctsm_bwd_mf(ctx, g, dtype, angle_begin, angle_end, angle_step, y_dev, x_dev, stream);
+  CT_TRY(set_device(ctx));
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  CT_TRY(check_dtype(dtype));
+  CT_TRY(check_shard(g, angle_begin, angle_end, angle_step));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_sel = n_in_shard(angle_begin, angle_end, angle_step);
+  const uint64_t n_meas = (uint64_t)d.rows_per_angle * g->n_angles;
+  double my = 0.0;
+  CT_TRY(fetch_max_abs(ctx, dtype, n_meas, y_dev, st, &my));
+  if (!std::isfinite(my)) return fail(CTSM_ERR_NON_FINITE, "sinogram not finite");
+  // fixed-point scale: a power of two with max |x_c| * scale < 2^61
+  const double B = my * (double)n_sel * ray_colsum_bound(g);
+  int e = 0;
+  std::frexp(B, &e);
+  const double scale = B > 0.0 ? std::ldexp(1.0, 61 - e) : 1.0;
+  CT_TRY(ensure(ctx, ctx->angles, (size_t)(n_sel > 0 ? n_sel : 1) * ray_angle_bytes()));
+  CT_CUDA(ray_angle_table(d, angle_begin, angle_step, n_sel, ctx->angles.p, st));
+  CT_TRY(ensure(ctx, ctx->lacc, (size_t)d.n_vox * sizeof(unsigned long long)));
+  CT_CUDA(ray_bwd_mf(d, dtype, ctx->angles.p, mode, k, angle_begin, angle_step, n_sel, y_dev,
+                     (unsigned long long*)ctx->lacc.p, scale, x_dev, st));
   return check_status(ctx, st, "back_project_matrix_free");
 }
 

@@ -118,6 +118,27 @@ cudaError_t sirt_update(int dtype, uint64_t n, const void* cinv, const void* bp,
                         cudaStream_t st);
 cudaError_t fill_value(int dtype, uint64_t n, double v, void* out, cudaStream_t st);
 
+// ---- line.cu: line / multiline(k) rays (baseline.cpp:13-128) --------------
+size_t ray_angle_bytes();
+cudaError_t ray_angle_table(const DevGeom& g, int angle_begin, int angle_step, int n_sel,
+                            void* angles_dev, cudaStream_t st);
+cudaError_t ray_count(const DevGeom& g, const void* angles_dev, int mode, int k, uint64_t n_rows,
+                      unsigned* counts, cudaStream_t st);
+cudaError_t ray_fill(const DevGeom& g, const void* angles_dev, int mode, int k, uint64_t n_rows,
+                     const uint64_t* start, uint32_t* col, double* val, cudaStream_t st);
+cudaError_t ray_sort_merge(uint64_t n_rows, const uint64_t* start, unsigned* counts, uint32_t* col,
+                           double* val, unsigned* long_rows, unsigned* n_long, int* status,
+                           cudaStream_t st);
+cudaError_t ray_compact(uint64_t n_rows, const uint64_t* raw_start, const uint64_t* row_start,
+                        const uint32_t* rcol, const double* rval, uint32_t* col, double* val,
+                        cudaStream_t st);
+cudaError_t ray_fwd_mf(const DevGeom& g, int dtype, const void* angles_dev, int mode, int k,
+                       int angle_begin, int angle_step, int n_sel, const void* x, void* y,
+                       unsigned long long* n_upd, int* status, cudaStream_t st);
+cudaError_t ray_bwd_mf(const DevGeom& g, int dtype, const void* angles_dev, int mode, int k,
+                       int angle_begin, int angle_step, int n_sel, const void* y,
+                       unsigned long long* acc, double scale, void* x, cudaStream_t st);
+
 }  // namespace ctsmb
 
 namespace ctsmb {

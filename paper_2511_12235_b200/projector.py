@@ -70,11 +70,17 @@ def matrix_mode_name(mode: str, k: int = 1) -> str:
     return f"multiline:{k}" if mode == MatrixMode.multiline else mode
 
 
-def _require_consistent(mode: str) -> None:
-    if mode != MatrixMode.consistent:
-        raise CtsmError("InvalidSpec",
-                        f"matrix mode '{mode}' is not provided on the device path "
-                        "(consistent weights only; line/multiline are out of scope)")
+_MODE_CODES = {MatrixMode.consistent: 0, MatrixMode.line: 1, MatrixMode.multiline: 2}
+
+
+def _mode_code(mode: str, k: int) -> int:
+    """MatrixMode ordinal (projector.hpp:12-16) for the C-ABI; line and
+    multiline(k) run the device ray tracer (baseline.cpp:13-128)."""
+    if mode not in _MODE_CODES:
+        raise CtsmError("InvalidSpec", f"unknown matrix mode '{mode}'")
+    if mode == MatrixMode.multiline and k <= 0:
+        raise CtsmError("InvalidSpec", "multiline ray count must be > 0")
+    return _MODE_CODES[mode]
 
 
 # ---- device context -----------------------------------------------------
@@ -204,10 +210,11 @@ def build_system_matrix(g: ScanGeometry, mode: str = MatrixMode.consistent, k: i
                         threads: int = 1, memory_budget_bytes: int = DEFAULT_BUDGET,
                         device: Optional[int] = None, angle_range: Optional[tuple] = None
                         ) -> SparseSystemMatrix:
-    """projector.cpp:144-201 on the GPU (K1 2D / K2 3D). ``threads`` is accepted
-    for API compatibility and ignored. ``angle_range=(a0, a1)`` builds one
-    contiguous angle shard (rows a0*rpa .. a1*rpa)."""
-    _require_consistent(mode)
+    """projector.cpp:144-201 on the GPU (K1 2D / K2 3D; line / multiline(k)
+    by the device ray tracer, K9). ``threads`` is accepted for API
+    compatibility and ignored. ``angle_range=(a0, a1)`` builds one contiguous
+    angle shard (rows a0*rpa .. a1*rpa)."""
+    mc = _mode_code(mode, k)
     g.validate()
     if g.n_voxels > 0xFFFFFFFF:
         raise CtsmError("TooLarge", "grid exceeds 2^32 voxel columns")
@@ -220,12 +227,13 @@ def build_system_matrix(g: ScanGeometry, mode: str = MatrixMode.consistent, k: i
     nnz = ctypes.c_uint64(0)
     st = _stream(dev)
     L = _lib.lib()
-    _lib.check(L.ctsm_csr_count(ctx.handle, ctypes.byref(cg), a0, a1, memory_budget_bytes,
-                                _dev_ptr(row_start), ctypes.byref(nnz), st))
+    _lib.check(L.ctsm_csr_count_mode(ctx.handle, ctypes.byref(cg), mc, k, a0, a1,
+                                     memory_budget_bytes, _dev_ptr(row_start),
+                                     ctypes.byref(nnz), st))
     col = torch.empty(nnz.value, dtype=torch.int32, device=f"cuda:{dev}")
     val = torch.empty(nnz.value, dtype=torch.float64, device=f"cuda:{dev}")
-    _lib.check(L.ctsm_csr_fill(ctx.handle, ctypes.byref(cg), a0, a1, _dev_ptr(row_start),
-                               _dev_ptr(col), _dev_ptr(val), st))
+    _lib.check(L.ctsm_csr_fill_mode(ctx.handle, ctypes.byref(cg), mc, k, a0, a1,
+                                    _dev_ptr(row_start), _dev_ptr(col), _dev_ptr(val), st))
     return SparseSystemMatrix(n_rows=n_rows, n_cols=g.n_voxels, row_start=row_start, col=col,
                               val=val, meta=_meta(g, mode, k), device=dev,
                               row_offset=a0 * g.rows_per_angle)
@@ -326,8 +334,9 @@ def forward_project_matrix_free(g: ScanGeometry, mode: str = MatrixMode.consiste
     projection to an angle shard (rows of other angles are left untouched in
     ``out``, zero in a fresh output); ("orbits", b0, bstep) selects the base
     angles b0 + k bstep < n/4 of a quarter-turn symmetric scan together with
-    their quarter-turn images. dtype follows x (float64 / float32)."""
-    _require_consistent(mode)
+    their quarter-turn images. dtype follows x (float64 / float32). Line /
+    multiline(k) modes trace the detector rays on the device (K9)."""
+    mc = _mode_code(mode, k)
     g.validate()
     n = int(x.numel()) if (torch is not None and isinstance(x, torch.Tensor)) else int(np.size(x))
     if n != g.n_voxels:
@@ -340,13 +349,16 @@ def forward_project_matrix_free(g: ScanGeometry, mode: str = MatrixMode.consiste
     y = out if out is not None else torch.zeros(g.n_measurements, dtype=xt.dtype, device=xt.device)
     cg = g.to_c()
     if sh[0] == "orbits":
+        if mc != 0:
+            raise CtsmError("InvalidSpec", "orbit shards exist for the consistent mode only")
         _lib.check(_lib.lib().ctsm_fwd_mf_orbits(ctx.handle, ctypes.byref(cg), _dtype_code(xt),
                                                  sh[1], sh[2], _dev_ptr(xt), _dev_ptr(y),
                                                  _stream(ctx.device)))
     else:
         a0, a1, st = sh
-        _lib.check(_lib.lib().ctsm_fwd_mf(ctx.handle, ctypes.byref(cg), _dtype_code(xt), a0, a1,
-                                          st, _dev_ptr(xt), _dev_ptr(y), _stream(ctx.device)))
+        _lib.check(_lib.lib().ctsm_fwd_mf_mode(ctx.handle, ctypes.byref(cg), mc, k,
+                                               _dtype_code(xt), a0, a1, st, _dev_ptr(xt),
+                                               _dev_ptr(y), _stream(ctx.device)))
     return y if (was_t or out is not None) else y.cpu().numpy()
 
 
@@ -356,7 +368,7 @@ def back_project_matrix_free(g: ScanGeometry, mode: str = MatrixMode.consistent,
     """Matrix-free A^T y (K6; the reference only has CSR back_project,
     projector.cpp:219-233). With ``angles`` the result is the partial volume
     of that angle shard (summed across ranks by the multi-GPU driver)."""
-    _require_consistent(mode)
+    mc = _mode_code(mode, k)
     g.validate()
     n = int(y.numel()) if (torch is not None and isinstance(y, torch.Tensor)) else int(np.size(y))
     if n != g.n_measurements:
@@ -369,20 +381,23 @@ def back_project_matrix_free(g: ScanGeometry, mode: str = MatrixMode.consistent,
     x = out if out is not None else torch.empty(g.n_voxels, dtype=yt.dtype, device=yt.device)
     cg = g.to_c()
     if sh[0] == "orbits":
+        if mc != 0:
+            raise CtsmError("InvalidSpec", "orbit shards exist for the consistent mode only")
         _lib.check(_lib.lib().ctsm_bwd_mf_orbits(ctx.handle, ctypes.byref(cg), _dtype_code(yt),
                                                  sh[1], sh[2], _dev_ptr(yt), _dev_ptr(x),
                                                  _stream(ctx.device)))
     else:
         a0, a1, st = sh
-        _lib.check(_lib.lib().ctsm_bwd_mf(ctx.handle, ctypes.byref(cg), _dtype_code(yt), a0, a1,
-                                          st, _dev_ptr(yt), _dev_ptr(x), _stream(ctx.device)))
+        _lib.check(_lib.lib().ctsm_bwd_mf_mode(ctx.handle, ctypes.byref(cg), mc, k,
+                                               _dtype_code(yt), a0, a1, st, _dev_ptr(yt),
+                                               _dev_ptr(x), _stream(ctx.device)))
     return x if (was_t or out is not None) else x.cpu().numpy()
 
 
 def angle_column_sums(g: ScanGeometry, mode: str = MatrixMode.consistent, k: int = 1,
                       angle_index: int = 0, device: Optional[int] = None):
     """projector.cpp:288-295: per-voxel sums of one angle block (A^T 1 on one angle)."""
-    _require_consistent(mode)
+    _mode_code(mode, k)
     ctx = Context.get(device)
     ones = torch.ones(g.n_measurements, dtype=torch.float64, device=f"cuda:{ctx.device}")
     return back_project_matrix_free(g, mode, k, ones, angles=(angle_index, angle_index + 1, 1),

@@ -1,7 +1,8 @@
 """Generates the golden fixtures in tests/golden/ from the REFERENCE itself.
 
 Run in the build container (needs oracle/_ref, i.e. /root/reference compiled by
-oracle/Makefile):   python tests/golden/make_golden.py
+oracle/Makefile):   python tests/golden/make_golden.py [--rays]
+(--rays regenerates only the line / multiline fixtures rays_*.npz, c0_rays_*.npz)
 
 Each fixture is produced twice: with the reference linked against glibc's libm
 (`*_glibc.npz`, the reference exactly as shipped) and against the correctly
@@ -59,6 +60,38 @@ def weight_samples(orc, g, n, seed, angles=None, zslab=None):
                 mz=arr[:, 5].astype(np.int32), w=arr[:, 6])
 
 
+RAY_CASES = [("proj2d", "line", 1), ("proj2d", "multiline", 3), ("proj3d", "line", 1),
+             ("proj3d", "multiline", 2)]
+
+
+def ray_fixture(orc, g, mode, k, seed):
+    """line / multiline(k) matrices (baseline.cpp:13-128) of a test geometry."""
+    m = orc.build_system_matrix(g, threads=THREADS, mode=mode, k=k)
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(g.n_voxels)
+    y = rng.uniform(0, 1, g.n_measurements)
+    return dict(row_start=m.row_start, col=m.col, val=m.val, x=x, y=y,
+                fwd=orc.forward_project_matrix_free(g, x, THREADS, mode, k),
+                bwd=orc.back_project_matrix_free(g, y, THREADS, mode, k))
+
+
+def main_rays():
+    for variant in ("ref_glibc", "ref_cr"):
+        orc = pyoracle.load(variant)
+        tag = variant.split("_")[1]
+        for name, mode, k in RAY_CASES:
+            np.savez_compressed(os.path.join(HERE, f"rays_{name}_{mode}{k}_{tag}.npz"),
+                                **ray_fixture(orc, TEST_GEOMETRIES[name], mode, k, 13))
+        # C0 (BASELINE configs[0]) line / multiline:4 angle blocks
+        g = CONFIGS["c0"]
+        blocks = {}
+        for mode, k, ip in (("line", 1, 17), ("multiline", 4, 45), ("line", 1, 90)):
+            r, c, w = orc.angle_block_entries(g, ip, mode=mode, k=k)
+            key = f"{mode}{k}_{ip}"
+            blocks[f"row_{key}"], blocks[f"col_{key}"], blocks[f"w_{key}"] = r, c, w
+        np.savez_compressed(os.path.join(HERE, f"c0_rays_{tag}.npz"), **blocks)
+
+
 def main():
     for variant in ("ref_glibc", "ref_cr"):
         orc = pyoracle.load(variant)
@@ -89,4 +122,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--rays" in sys.argv:
+        main_rays()
+    else:
+        main()
+        main_rays()

@@ -149,3 +149,91 @@ def test_parallel_angle_block_is_identical():
     ya = port.forward_mf_angles(g, [1, 5], x, 4)
     yb = port.forward_mf_angles(g, [1, 5], x, 4, split=True)
     assert np.max(np.abs(ya - yb)) <= 1e-13 * max(1.0, np.max(np.abs(ya)))
+
+
+# ---- line / multiline modes (baseline.cpp:13-128) ----
+RAY_CASES = [("proj2d", "line", 1), ("proj2d", "multiline", 3), ("proj3d", "line", 1),
+             ("proj3d", "multiline", 2)]
+
+
+@pytest.mark.parametrize("name,mode,k", RAY_CASES)
+@pytest.mark.parametrize("tag", ["cr", "glibc"])
+def test_ray_modes_against_golden(name, mode, k, tag):
+    orc = pyoracle.load(f"port_{tag}")
+    g = TEST_GEOMETRIES[name]
+    gold = load(f"rays_{name}_{mode}{k}_{tag}.npz")
+    m = orc.build_system_matrix(g, threads=THREADS, mode=mode, k=k)
+    assert np.array_equal(m.row_start, gold["row_start"])
+    assert np.array_equal(m.col, gold["col"])
+    fwd = orc.forward_project_matrix_free(g, gold["x"], THREADS, mode, k)
+    bwd = orc.back_project_matrix_free(g, gold["y"], THREADS, mode, k)
+    if tag == "cr":
+        assert same_bits(m.val, gold["val"])
+        assert same_bits(fwd, gold["fwd"])
+        assert same_bits(bwd, gold["bwd"])
+    else:
+        assert np.max(np.abs(m.val - gold["val"])) <= 1e-10
+        assert np.max(np.abs(fwd - gold["fwd"])) <= 1e-10 * max(1.0, np.max(np.abs(gold["fwd"])))
+        assert np.max(np.abs(bwd - gold["bwd"])) <= 1e-10 * max(1.0, np.max(np.abs(gold["bwd"])))
+
+
+@pytest.mark.parametrize("tag", ["cr", "glibc"])
+def test_c0_ray_blocks_against_golden(tag):
+    orc = pyoracle.load(f"port_{tag}")
+    g = CONFIGS["c0"]
+    gold = load(f"c0_rays_{tag}.npz")
+    for mode, k, ip in (("line", 1, 17), ("multiline", 4, 45), ("line", 1, 90)):
+        key = f"{mode}{k}_{ip}"
+        r, c, w = orc.angle_block_entries(g, ip, mode=mode, k=k)
+        assert np.array_equal(r, gold[f"row_{key}"]) and np.array_equal(c, gold[f"col_{key}"])
+        if tag == "cr":
+            assert same_bits(w, gold[f"w_{key}"])
+        else:
+            assert np.max(np.abs(w - gold[f"w_{key}"])) <= 1e-10
+
+
+def test_line_weights_properties():
+    """line_weights: lengths sum to the in-grid chord (baseline.hpp:15-20);
+    multiline(k) averages k rays so its lengths sum to the mean chord."""
+    orc = pyoracle.load("port_cr")
+    g = TEST_GEOMETRIES["proj2d"]
+    col, ln = orc.line_weights(g, 0, 0, 1, "line")
+    assert len(col) > 0 and np.all(ln > 0)
+    assert len(set(col.tolist())) == len(col)
+    # the central ray at angle 0 crosses the whole grid along x: chord = n_x a
+    col0, ln0 = orc.line_weights(g, -1, 0, 0, "line")
+    col1, ln1 = orc.line_weights(g, 0, 0, 0, "line")
+    assert abs(ln0.sum() - g.n_x * g.a) < 1e-2 and abs(ln1.sum() - g.n_x * g.a) < 1e-2
+    colm, lnm = orc.line_weights(g, 3, 0, 2, "multiline", 4)
+    assert np.all(np.diff(colm.astype(np.int64)) > 0)  # merged + sorted by column
+    with pytest.raises(pyoracle.OracleError) as e:
+        orc.line_weights(g, 0, 0, 0, "multiline", 0)
+    assert e.value.code == "InvalidSpec"
+    with pytest.raises(pyoracle.OracleError) as e:
+        orc.line_weights(g, g.n_det_y, 0, 0, "line")
+    assert e.value.code == "InvalidSpec"
+
+
+@needs_ref
+@pytest.mark.parametrize("tag", ["cr", "glibc"])
+def test_port_equals_reference_ray_modes(tag):
+    port = pyoracle.load(f"port_{tag}")
+    ref = pyoracle.load(f"ref_{tag}")
+    for name in ("wide2d", "cone3d"):
+        g = TEST_GEOMETRIES[name]
+        for mode, k in (("line", 1), ("multiline", 3)):
+            a = port.build_system_matrix(g, threads=THREADS, mode=mode, k=k)
+            b = ref.build_system_matrix(g, threads=THREADS, mode=mode, k=k)
+            assert np.array_equal(a.row_start, b.row_start) and np.array_equal(a.col, b.col)
+            assert same_bits(a.val, b.val)
+    g = CONFIGS["c2"]
+    for mode, k, ip in (("line", 1, 37), ("multiline", 2, 90)):
+        a = port.angle_block_entries(g, ip, mode=mode, k=k)
+        b = ref.angle_block_entries(g, ip, mode=mode, k=k)
+        assert all(np.array_equal(u, v) for u, v in zip(a[:2], b[:2]))
+        assert same_bits(a[2], b[2])
+    for m_y, m_z, ip in ((0, 0, 3), (-7, 5, 100), (120, -60, 359)):
+        for mode, k in (("line", 1), ("multiline", 3)):
+            a = port.line_weights(g, m_y, m_z, ip, mode, k)
+            b = ref.line_weights(g, m_y, m_z, ip, mode, k)
+            assert np.array_equal(a[0], b[0]) and same_bits(a[1], b[1])
