@@ -18,6 +18,8 @@ NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
           "-I" + CSRC, "-I" + os.path.join(HERE, "..", "include")] + ARCH
+# tuning experiments only (tools/sweep3d.sh): extra nvcc flags, e.g. -DCTSM_KZCS=4
+COMMON += os.environ.get("CTSM_NVCC_EXTRA", "").split()
 UNITS = {
     "csr.cu": ["-fmad=false"],
     "line.cu": ["-fmad=false"],

@@ -72,7 +72,7 @@ struct ctsm_ctx {
   double* h_red = nullptr;      // pinned
   Buf angles, edges, cs, counts, scan, longrows, acc, part, base, alist, sv_up, sv_h, sv_hp,
       sv_q, sv_v, sv_part, sv_scal, tmp_a, tmp_b, tmp_c, tmp_d,
-      tmp_e, tmp_f, lraw_start, lraw_col, lraw_val, lacc;
+      tmp_e, tmp_f, lraw_start, lraw_col, lraw_val, lacc, bwd_t;
 };
 
 namespace {
@@ -236,7 +236,7 @@ int ctsm_destroy(ctsm_ctx* ctx) {
                  &ctx->longrows, &ctx->acc, &ctx->part, &ctx->base, &ctx->alist, &ctx->sv_up, &ctx->sv_h, &ctx->sv_hp, &ctx->sv_q,
                  &ctx->sv_v, &ctx->sv_part, &ctx->sv_scal, &ctx->tmp_a, &ctx->tmp_b,  &ctx->tmp_c,
                  &ctx->tmp_d, &ctx->tmp_e, &ctx->tmp_f, &ctx->lraw_start, &ctx->lraw_col,
-                 &ctx->lraw_val, &ctx->lacc};
+                 &ctx->lraw_val, &ctx->lacc, &ctx->bwd_t};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   cudaFree(ctx->status);
@@ -544,8 +544,10 @@ static int bwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d,
   const int nb = (int)base.size();
   const bool two_d = (g->n_z == 1 && g->n_det_z == 1);
   if (!two_d) {
+    const size_t ne = bwd3d_scratch_elems(d, symmetry_order(g), dtype);
+    if (ne) CT_TRY(ensure(ctx, ctx->bwd_t, ne * (dtype == CTSM_F64 ? 8 : 4)));
     CT_CUDA(bwd3d_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, y, x,
-                         ctx->status, st, symmetry_order(g)));
+                         ctx->status, st, symmetry_order(g), ne ? ctx->bwd_t.p : nullptr));
   } else if (symmetry_order(g) == 8) {
     const int nc = bwd_d8_chunks(d, nb);
     if (nc > 1) CT_TRY(ensure(ctx, ctx->part, (size_t)nc * g->n_x * g->n_y * sizeof(double)));

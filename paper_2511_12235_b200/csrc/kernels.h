@@ -88,9 +88,12 @@ cudaError_t rows_list(const DevGeom& g, int dtype, const int* angles, int n_list
 cudaError_t fwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                          int n_base, const void* x, unsigned long long* yacc, double scale,
                          unsigned long long* n_upd, int* status, cudaStream_t st, int order);
+// scratch: bwd3d_scratch_elems(...) elements of the dtype (transposed image
+// rows of one L2 chunk), or NULL for the untransposed gather.
+size_t bwd3d_scratch_elems(const DevGeom& g, int order, int dtype);
 cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                          int n_base, const void* y, void* x, int* status, cudaStream_t st,
-                         int order);
+                         int order, void* scratch);
 cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
                    int angle_step, int n_sel, const void* x, unsigned long long* yacc,
                    double scale, unsigned long long* n_upd, int* status, cudaStream_t st);

@@ -560,13 +560,19 @@ __global__ void __launch_bounds__(128, 6) bwd2d_d8_kernel(
 // per z-block ([image][slot][lane], conflict-free) and reused for all base
 // angles: the per-weight reads are shared-memory hits instead of G scattered
 // global loads.
-constexpr int kZcF = 8;  // z-block of 256 voxels for the staged values
+#ifndef CTSM_KZCF
+#define CTSM_KZCF 8
+#endif
+#ifndef CTSM_FWD3_MINB
+#define CTSM_FWD3_MINB 3
+#endif
+constexpr int kZcF = CTSM_KZCF;  // z-block of 32 * kZcF voxels for the staged values
 
 template <typename T, int G>
 constexpr size_t fwd3d_sym_dyn_smem() { return sizeof(T) * kWarps3 * G * kZcF * 32; }
 
 template <typename T, int G>
-__global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? 3 : 4) fwd3d_sym_kernel(
+__global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd3d_sym_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
     const T* __restrict__ in, unsigned long long* __restrict__ yacc, double scale,
     unsigned long long* n_upd, int* status) {
@@ -608,17 +614,20 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? 3 : 4) fwd3d_sym_kernel
       if (!ok) continue;
       // pending merge of consecutive emits to one row (see proj3d_kernel):
       // row pr = (mz + hz) ndy + py, py = my + hy; reflections write -1-my
-      long long pr = -1, pv[G];
+      // the run of one row is summed in FP64 (fixed lane order: deterministic)
+      // and converted to fixed point once, at the flush
+      long long pr = -1;
+      double pv[G];
       int py = 0;
 #pragma unroll
-      for (int e = 0; e < G; ++e) pv[e] = 0;
+      for (int e = 0; e < G; ++e) pv[e] = 0.0;
       auto flush = [&]() {
 #pragma unroll
         for (int e = 0; e < G; ++e)
-          if (e < ne && pv[e] != 0) {
+          if (e < ne && pv[e] != 0.0) {
             const long long r = (e < 4) ? pr : pr + ndy - 1 - 2 * py;
             atomicAdd(yacc + (long long)d4_angle(g.n_angles, i, e) * rpa + r,
-                      (unsigned long long)pv[e]);
+                      (unsigned long long)__double2ll_rn(pv[e] * scale));
           }
       };
       fast::chunk_weights(g, sh[warp], sp[warp], z0, z1, [&](int iz, int my, int mz, double w) {
@@ -629,12 +638,11 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? 3 : 4) fwd3d_sym_kernel
           pr = r;
           py = my + hy;
 #pragma unroll
-          for (int e = 0; e < G; ++e) pv[e] = 0;
+          for (int e = 0; e < G; ++e) pv[e] = 0.0;
         }
-        const double ws = w * scale;
 #pragma unroll
         for (int e = 0; e < G; ++e)
-          if (e < ne) pv[e] += __double2ll_rn(ws * (double)xsm[warp][e][iz - z0][lane]);
+          if (e < ne) pv[e] += w * (double)xsm[warp][e][iz - z0][lane];
       });
       if (pr >= 0) flush();
     }
@@ -648,11 +656,21 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? 3 : 4) fwd3d_sym_kernel
 // members are planned in turn and every weight set of member h is gathered
 // against the image angles e i into the shared-memory accumulator of member
 // e o h (fixed order: deterministic).
+#ifndef CTSM_KZCS
+#define CTSM_KZCS 8
+#endif
+#ifndef CTSM_BWD3_MINB
+#define CTSM_BWD3_MINB 8
+#endif
 constexpr int kWarpsS = 2;
-constexpr int kZcS = 8;
+constexpr int kZcS = CTSM_KZCS;
 
-template <typename T, int G>
-__global__ void __launch_bounds__(kWarpsS * 32, 8) bwd3d_sym_kernel(
+// TR: `in` is the launch's image rows transposed per (base slot, image) into
+// [k * G + e][my][mz] (mz fastest, transpose_images below): a lane walking up
+// its z-chunk then reads consecutive addresses (shared sectors / L1 hits)
+// instead of one 2 KB-strided sector per row.
+template <typename T, int G, bool TR>
+__global__ void __launch_bounds__(kWarpsS * 32, CTSM_BWD3_MINB) bwd3d_sym_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
     const T* __restrict__ in, T* __restrict__ xout, int accumulate, int* status) {
   __shared__ fast::ColumnHead sh[kWarpsS];
@@ -691,7 +709,8 @@ __global__ void __launch_bounds__(kWarpsS * 32, 8) bwd3d_sym_kernel(
       const T* yb[G];
 #pragma unroll
       for (int e = 0; e < G; ++e)
-        yb[e] = in + (long long)d4_angle(g.n_angles, i, e) * rpa;
+        yb[e] = TR ? in + (long long)(kk * G + e) * rpa
+                   : in + (long long)d4_angle(g.n_angles, i, e) * rpa;
 #pragma unroll 1
       for (int hm = 0; hm < n_mem; ++hm) {
         int cx, cy;
@@ -703,16 +722,20 @@ __global__ void __launch_bounds__(kWarpsS * 32, 8) bwd3d_sym_kernel(
         int slot[G];
 #pragma unroll
         for (int e = 0; e < G; ++e) slot[e] = d4_compose(e, hm);
-        fast::chunk_weights(g, sh[warp], sp[warp], z0, z1, [&](int iz, int my, int mz, double w) {
-          const long long r = (long long)(mz + hz) * g.n_det_y + (my + hy);
+        auto gather = [&](int t, int my, int mz, double w) {
+          const long long r = TR ? (long long)(my + hy) * g.n_det_z + (mz + hz)
+                                 : (long long)(mz + hz) * g.n_det_y + (my + hy);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) sacc[warp][slot[e]][iz - z0][lane] += w * ld(&yb[e][r]);
+          for (int e = 0; e < 4; ++e) sacc[warp][slot[e]][t][lane] += w * ld(&yb[e][r]);
           if (G == 8 && full) {
-            const long long rr = r + g.n_det_y - 1 - 2 * (my + hy);
+            const long long rr = TR ? (long long)(g.n_det_y - 1 - (my + hy)) * g.n_det_z + (mz + hz)
+                                    : r + g.n_det_y - 1 - 2 * (my + hy);
 #pragma unroll
-            for (int e = 4; e < G; ++e) sacc[warp][slot[e]][iz - z0][lane] += w * ld(&yb[e][rr]);
+            for (int e = 4; e < G; ++e) sacc[warp][slot[e]][t][lane] += w * ld(&yb[e][rr]);
           }
-        });
+        };
+        fast::chunk_weights(g, sh[warp], sp[warp], z0, z1,
+                            [&](int iz, int my, int mz, double w) { gather(iz - z0, my, mz, w); });
       }
     }
     for (int e = 0; e < (diag ? 4 : G); ++e) {
@@ -720,9 +743,11 @@ __global__ void __launch_bounds__(kWarpsS * 32, 8) bwd3d_sym_kernel(
       d4_pixel(n, ix0, iy0, e, cx, cy);
       const long long c = (long long)cy * n + cx;
       const int e2 = d4_compose(e, 5);  // diagonal: e c == (e o 5) c
-      for (int iz = z0; iz < z1; ++iz) {
-        double v = sacc[warp][e][iz - z0][lane];
-        if (diag) v += sacc[warp][e2][iz - z0][lane];
+      for (int t = 0; t < zc; ++t) {
+        const int iz = z0 + t;
+        if (iz >= z1) break;
+        double v = sacc[warp][e][t][lane];
+        if (diag) v += sacc[warp][e2][t][lane];
         if (accumulate) v += (double)xout[iz * nxy + c];
         xout[iz * nxy + c] = (T)v;
       }
@@ -988,19 +1013,63 @@ cudaError_t fwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const i
   return cudaGetLastError();
 }
 
+// Image rows of base slots [0, nk) -> yt[(k * G + e)][my][mz] (tiled transpose).
+template <typename T>
+__global__ void transpose_images_kernel(const T* __restrict__ y, const int* __restrict__ base,
+                                        int G, int n_angles, int ndy, int ndz,
+                                        T* __restrict__ yt) {
+  __shared__ T tile[32][33];
+  const int slab = blockIdx.z;
+  const int a = d4_angle(n_angles, base[slab / G], slab % G);
+  const long long rpa = (long long)ndy * ndz;
+  const T* src = y + (long long)a * rpa;
+  T* dst = yt + (long long)slab * rpa;
+  const int cx = blockIdx.x * 32 + threadIdx.x;  // my
+  const int rz = blockIdx.y * 32 + threadIdx.y;  // mz
+  for (int j = 0; j < 32; j += 8)
+    if (cx < ndy && rz + j < ndz) tile[threadIdx.y + j][threadIdx.x] = src[(long long)(rz + j) * ndy + cx];
+  __syncthreads();
+  const int oz = blockIdx.y * 32 + threadIdx.x;  // mz
+  const int oy = blockIdx.x * 32 + threadIdx.y;  // my
+  for (int j = 0; j < 32; j += 8)
+    if (oz < ndz && oy + j < ndy) dst[(long long)(oy + j) * ndz + oz] = tile[threadIdx.x][threadIdx.y + j];
+}
+
+size_t bwd3d_scratch_elems(const DevGeom& g, int order, int dtype) {
+  if (getenv("CTSM_BWD3_PLAIN")) return 0;
+  return (size_t)sym3d_chunk(g, order, dtype == CTSM_F64 ? 8 : 4) * order * g.rows_per_angle;
+}
+
 cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                          int n_base, const void* y, void* x, int* status, cudaStream_t st,
-                         int order) {
+                         int order, void* scratch) {
   const long long h = g.n_x / 2;
   const long long n_orb = order == 8 ? h * (h + 1) / 2 : h * h;
   const unsigned blocks = (unsigned)((n_orb + kWarpsS - 1) / kWarpsS);
   const int chunk = sym3d_chunk(g, order, dtype == CTSM_F64 ? 8 : 4);
+  const bool tr = scratch != nullptr && n_base > 0;
   // chunks accumulate into x in ascending order (deterministic)
   for (int k0 = 0; k0 < (n_base > 0 ? n_base : 1); k0 += chunk) {
     const int nk = n_base - k0 < chunk ? n_base - k0 : chunk;
-#define CTSM_LAUNCH(T, G)                                                                     \
-  bwd3d_sym_kernel<T, G><<<blocks, kWarpsS * 32, 0, st>>>(g, cs + k0, base + k0, nk,           \
-                                                          (const T*)y, (T*)x, k0 > 0, status)
+    if (tr) {
+      const dim3 tg((g.n_det_y + 31) / 32, (g.n_det_z + 31) / 32, (unsigned)(nk * order));
+      if (dtype == CTSM_F64)
+        transpose_images_kernel<double><<<tg, dim3(32, 8), 0, st>>>(
+            (const double*)y, base + k0, order, g.n_angles, g.n_det_y, g.n_det_z, (double*)scratch);
+      else
+        transpose_images_kernel<float><<<tg, dim3(32, 8), 0, st>>>(
+            (const float*)y, base + k0, order, g.n_angles, g.n_det_y, g.n_det_z, (float*)scratch);
+      count_launch();
+    }
+#define CTSM_LAUNCH(T, G)                                                                      \
+  do {                                                                                         \
+    if (tr)                                                                                    \
+      bwd3d_sym_kernel<T, G, true><<<blocks, kWarpsS * 32, 0, st>>>(                           \
+          g, cs + k0, base + k0, nk, (const T*)scratch, (T*)x, k0 > 0, status);                \
+    else                                                                                       \
+      bwd3d_sym_kernel<T, G, false><<<blocks, kWarpsS * 32, 0, st>>>(                          \
+          g, cs + k0, base + k0, nk, (const T*)y, (T*)x, k0 > 0, status);                      \
+  } while (0)
     if (dtype == CTSM_F64) {
       if (order == 8) CTSM_LAUNCH(double, 8); else CTSM_LAUNCH(double, 4);
     } else {
