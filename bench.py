@@ -347,9 +347,23 @@ def run_ours(args):
     kname = ("fwd2d" if ms_f >= ms_b else "bwd2d") + suffix
     if not g.is_2d():
         kname = kname.replace("2d", "3d")
+    # DRAM traffic of the same kernel and workload from one committed
+    # `ncu --set full` capture (profiles/ncu_kernels.json, tools/ncu_kernels.py)
+    traffic, ncu_pipe = None, None
+    try:
+        ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_kernels.json")))
+        tname = "double" if args.dtype == "f64" else "float"
+        key = f"{cfg}_{args.dtype}:{kname}_kernel<{tname}>"
+        if key in ncu:
+            traffic = ncu[key]["dram_bytes"]
+            ncu_pipe = ncu[key].get("fp64_pipe_pct")
+    except (OSError, ValueError, KeyError):
+        pass
     roof = {"bound": "fp64", "kernel": kname,
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": (achieved / peak) if peak else None, "traffic": None,
+            "frac": (achieved / peak) if peak else None, "traffic": traffic,
+            "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/ncu_kernels.json)",
+            "ncu_fp64_pipe_active_pct": ncu_pipe,
             "peak_source": "measured DFMA microkernel (MEASURED_PEAKS.json has no FP64 entry)",
             "work_per_unit": f"{per_unit:g} FP64 flops per weight evaluation (reference op count, SURVEY.md §8(d))",
             "units_per_launch": units, "symmetry_reuse": reuse,

@@ -347,6 +347,12 @@ __host__ __device__ constexpr int d4_compose(int g, int h) {
 // holds 32-bit limbs: the low 24 bits and the signed rest (f64), or one signed
 // limb (f32). With <= 128 adds per cell (one per tile pixel) no limb
 // overflows; the flush recombines them exactly into the 64-bit accumulator.
+#ifndef CTSM_D8F_MINB
+#define CTSM_D8F_MINB 7
+#endif
+#ifndef CTSM_D8B_MINB
+#define CTSM_D8B_MINB 7
+#endif
 constexpr int kD8Angles = 8;
 constexpr int kD8Win = 64;
 // w * xs rounded to the nearest integer (|.| < 2^47) by the 1.5 * 2^52 shift:
@@ -366,7 +372,7 @@ __device__ __forceinline__ void limb_add(unsigned* w, double wv, double xsv) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(128, 6) fwd2d_d8_kernel(
+__global__ void __launch_bounds__(128, CTSM_D8F_MINB) fwd2d_d8_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
     const T* __restrict__ x, unsigned long long* __restrict__ yacc, double scale,
     unsigned long long* n_upd, int* status) {
@@ -471,7 +477,7 @@ __global__ void __launch_bounds__(128, 6) fwd2d_d8_kernel(
 // of member h at base angle i is gathered against angle g i, cell g m for
 // every group element g into the accumulator of pixel (g o h) p0.
 template <typename T>
-__global__ void __launch_bounds__(128, 6) bwd2d_d8_kernel(
+__global__ void __launch_bounds__(128, CTSM_D8B_MINB) bwd2d_d8_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
     int chunk, const T* __restrict__ y, T* __restrict__ x, double* __restrict__ part,
     int* status) {
