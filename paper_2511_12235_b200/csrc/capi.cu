@@ -72,7 +72,7 @@ struct ctsm_ctx {
   double* h_red = nullptr;      // pinned
   Buf angles, edges, cs, counts, scan, longrows, acc, part, base, alist, sv_up, sv_h, sv_hp,
       sv_q, sv_v, sv_part, sv_scal, tmp_a, tmp_b, tmp_c, tmp_d,
-      tmp_e, tmp_f, lraw_start, lraw_col, lraw_val, lacc, bwd_t;
+      tmp_e, tmp_f, lraw_start, lraw_col, lraw_val, lacc, bwd_t, vol_t;
 };
 
 namespace {
@@ -494,12 +494,14 @@ static int fwd_d8_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d, 
   if (two_d && mx > 0.0)
     scale = std::min(scale, std::ldexp(1.0, dtype == CTSM_F64 ? 47 : 23) / (mx * 1.001));
   CT_CUDA(cudaMemsetAsync(ctx->n_upd, 0, sizeof(unsigned long long), st));
-  if (two_d)
+  if (two_d) {
     CT_CUDA(fwd_mf_d8(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, x, acc,
                       scale, ctx->n_upd, ctx->status, st));
-  else
+  } else {
+    CT_TRY(ensure(ctx, ctx->vol_t, (size_t)d.n_vox * (dtype == CTSM_F64 ? 8 : 4)));
     CT_CUDA(fwd3d_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, x,
-                         acc, scale, ctx->n_upd, ctx->status, st, 8));
+                         acc, scale, ctx->n_upd, ctx->status, st, 8, ctx->vol_t.p));
+  }
   CT_CUDA(rows_list(d, dtype, al, nl, acc, scale, y, 1, st));
   CT_CUDA(cudaMemcpyAsync(ctx->h_upd, ctx->n_upd, sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, st));
@@ -525,12 +527,14 @@ static int fwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d,
   const double scale = B > 0.0 ? std::ldexp(1.0, 61) / B : 1.0;
   CT_CUDA(cudaMemsetAsync(ctx->n_upd, 0, sizeof(unsigned long long), st));
   const bool two_d = (g->n_z == 1 && g->n_det_z == 1);
-  if (two_d)
+  if (two_d) {
     CT_CUDA(fwd_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, x, acc,
                        scale, ctx->n_upd, ctx->status, st));
-  else
+  } else {
+    CT_TRY(ensure(ctx, ctx->vol_t, (size_t)d.n_vox * (dtype == CTSM_F64 ? 8 : 4)));
     CT_CUDA(fwd3d_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, x,
-                         acc, scale, ctx->n_upd, ctx->status, st, 4));
+                         acc, scale, ctx->n_upd, ctx->status, st, 4, ctx->vol_t.p));
+  }
   for (int k = 0; k < 4; ++k)
     CT_CUDA(fixed_to_float_rows(d, dtype, base[0] + k * q, base_step, nb, acc, scale, y, st));
   CT_CUDA(cudaMemcpyAsync(ctx->h_upd, ctx->n_upd, sizeof(unsigned long long),
@@ -546,8 +550,10 @@ static int bwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d,
   if (!two_d) {
     const size_t ne = bwd3d_scratch_elems(d, symmetry_order(g), dtype);
     if (ne) CT_TRY(ensure(ctx, ctx->bwd_t, ne * (dtype == CTSM_F64 ? 8 : 4)));
+    CT_TRY(ensure(ctx, ctx->vol_t, (size_t)d.n_vox * (dtype == CTSM_F64 ? 8 : 4)));
     CT_CUDA(bwd3d_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, y, x,
-                         ctx->status, st, symmetry_order(g), ne ? ctx->bwd_t.p : nullptr));
+                         ctx->status, st, symmetry_order(g), ne ? ctx->bwd_t.p : nullptr,
+                         ctx->vol_t.p));
   } else if (symmetry_order(g) == 8) {
     const int nc = bwd_d8_chunks(d, nb);
     if (nc > 1) CT_TRY(ensure(ctx, ctx->part, (size_t)nc * g->n_x * g->n_y * sizeof(double)));

@@ -85,15 +85,20 @@ cudaError_t bwd_mf_d8(const DevGeom& g, int dtype, const AngleCS* cs, const int*
 // mode 0: zero the fixed-point rows of the listed angles; mode 1: convert them
 cudaError_t rows_list(const DevGeom& g, int dtype, const int* angles, int n_list,
                       unsigned long long* acc, double scale, void* y, int mode, cudaStream_t st);
+// The symmetric 3D kernels read / write the volume in the z-fastest layout
+// [n_y][n_x][n_z] (a lane's z-chunk is contiguous): vol_t is an n_vox scratch
+// of the dtype; fwd transposes x into it, bwd accumulates into it and
+// transposes the result into x.
 cudaError_t fwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                          int n_base, const void* x, unsigned long long* yacc, double scale,
-                         unsigned long long* n_upd, int* status, cudaStream_t st, int order);
+                         unsigned long long* n_upd, int* status, cudaStream_t st, int order,
+                         void* vol_t);
 // scratch: bwd3d_scratch_elems(...) elements of the dtype (transposed image
 // rows of one L2 chunk), or NULL for the untransposed gather.
 size_t bwd3d_scratch_elems(const DevGeom& g, int order, int dtype);
 cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                          int n_base, const void* y, void* x, int* status, cudaStream_t st,
-                         int order, void* scratch);
+                         int order, void* scratch, void* vol_t);
 cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
                    int angle_step, int n_sel, const void* x, unsigned long long* yacc,
                    double scale, unsigned long long* n_upd, int* status, cudaStream_t st);

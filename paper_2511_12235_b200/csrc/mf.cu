@@ -604,9 +604,10 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd
     for (int e = 0; e < G; ++e) {
       int rx, ry;
       d4_pixel(n, ix, iy, e, rx, ry);
-      const T* src = in + (long long)ry * n + rx;
-      for (int t = 0; t < zc; ++t)
-        xsm[warp][e][t][lane] = (z0 + t < z1) ? src[(long long)(z0 + t) * nxy] : (T)0;
+      // z-fastest volume: the lane's z-chunk is contiguous (its sectors are
+      // re-hit in L1 across t), instead of one sector per voxel
+      const T* src = in + ((long long)ry * n + rx) * g.n_z;
+      for (int t = 0; t < zc; ++t) xsm[warp][e][t][lane] = (z0 + t < z1) ? src[z0 + t] : (T)0;
     }
     __syncwarp();
     for (int kk = 0; kk < n_base; ++kk) {
@@ -618,6 +619,9 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd
       const bool ok = fast::plan_column(g, a.C, a.S, ix, iy, status, sh[warp], sp[warp], lane);
       __syncwarp();
       if (!ok) continue;
+#ifdef CTSM_EXP_PLAN_ONLY
+      continue;  // timing experiment: planning cost alone
+#endif
       // pending merge of consecutive emits to one row (see proj3d_kernel):
       // row pr = (mz + hz) ndy + py, py = my + hy; reflections write -1-my
       // the run of one row is summed in FP64 (fixed lane order: deterministic)
@@ -668,7 +672,20 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd
 #ifndef CTSM_BWD3_MINB
 #define CTSM_BWD3_MINB 8
 #endif
-constexpr int kWarpsS = 2;
+#ifndef CTSM_KWS
+#define CTSM_KWS 2
+#endif
+constexpr int kWarpsS = CTSM_KWS;
+template <typename T>
+struct BwdAcc {
+  using type = double;
+};
+#ifndef CTSM_BWD3_ACC64
+template <>
+struct BwdAcc<float> {
+  using type = float;
+};
+#endif
 constexpr int kZcS = CTSM_KZCS;
 
 // TR: `in` is the launch's image rows transposed per (base slot, image) into
@@ -681,7 +698,11 @@ __global__ void __launch_bounds__(kWarpsS * 32, CTSM_BWD3_MINB) bwd3d_sym_kernel
     const T* __restrict__ in, T* __restrict__ xout, int accumulate, int* status) {
   __shared__ fast::ColumnHead sh[kWarpsS];
   __shared__ fast::PieceCoef sp[kWarpsS][fast::kMaxPieces];
-  __shared__ double sacc[kWarpsS][G][kZcS][32];
+  // fp32 volumes accumulate their per-launch sums in fp32 (fixed order, so
+  // still deterministic): at most ~chunk * 12 terms per slot, an error far
+  // below the fp32 tolerance, and half the shared memory -> more warps/SM
+  using AccT = typename BwdAcc<T>::type;
+  __shared__ AccT sacc[kWarpsS][G][kZcS][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = g.n_x, h = n / 2;
   const long long orb = (long long)blockIdx.x * kWarpsS + warp;
@@ -699,7 +720,6 @@ __global__ void __launch_bounds__(kWarpsS * 32, CTSM_BWD3_MINB) bwd3d_sym_kernel
   }
   const bool diag = G == 8 && ix0 == iy0;
   const int n_mem = (G == 4 || diag) ? 4 : 8;
-  const long long nxy = (long long)n * g.n_y;
   const int rpa = g.rows_per_angle;
   const int hy = g.n_det_y / 2, hz = g.n_det_z / 2;
   for (int zb0 = 0; zb0 < g.n_z; zb0 += 32 * kZcS) {
@@ -725,6 +745,9 @@ __global__ void __launch_bounds__(kWarpsS * 32, CTSM_BWD3_MINB) bwd3d_sym_kernel
         const bool ok = fast::plan_column(g, a.C, a.S, cx, cy, status, sh[warp], sp[warp], lane);
         __syncwarp();
         if (!ok) continue;
+#ifdef CTSM_EXP_PLAN_ONLY
+        continue;  // timing experiment: planning cost alone
+#endif
         int slot[G];
 #pragma unroll
         for (int e = 0; e < G; ++e) slot[e] = d4_compose(e, hm);
@@ -732,12 +755,12 @@ __global__ void __launch_bounds__(kWarpsS * 32, CTSM_BWD3_MINB) bwd3d_sym_kernel
           const long long r = TR ? (long long)(my + hy) * g.n_det_z + (mz + hz)
                                  : (long long)(mz + hz) * g.n_det_y + (my + hy);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) sacc[warp][slot[e]][t][lane] += w * ld(&yb[e][r]);
+          for (int e = 0; e < 4; ++e) sacc[warp][slot[e]][t][lane] += (AccT)(w * ld(&yb[e][r]));
           if (G == 8 && full) {
             const long long rr = TR ? (long long)(g.n_det_y - 1 - (my + hy)) * g.n_det_z + (mz + hz)
                                     : r + g.n_det_y - 1 - 2 * (my + hy);
 #pragma unroll
-            for (int e = 4; e < G; ++e) sacc[warp][slot[e]][t][lane] += w * ld(&yb[e][rr]);
+            for (int e = 4; e < G; ++e) sacc[warp][slot[e]][t][lane] += (AccT)(w * ld(&yb[e][rr]));
           }
         };
         fast::chunk_weights(g, sh[warp], sp[warp], z0, z1,
@@ -752,10 +775,11 @@ __global__ void __launch_bounds__(kWarpsS * 32, CTSM_BWD3_MINB) bwd3d_sym_kernel
       for (int t = 0; t < zc; ++t) {
         const int iz = z0 + t;
         if (iz >= z1) break;
-        double v = sacc[warp][e][t][lane];
-        if (diag) v += sacc[warp][e2][t][lane];
-        if (accumulate) v += (double)xout[iz * nxy + c];
-        xout[iz * nxy + c] = (T)v;
+        double v = (double)sacc[warp][e][t][lane];
+        if (diag) v += (double)sacc[warp][e2][t][lane];
+        T* dst = xout + c * g.n_z + iz;  // z-fastest volume
+        if (accumulate) v += (double)*dst;
+        *dst = (T)v;
       }
     }
   }
@@ -986,14 +1010,52 @@ cudaError_t fwd_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int
 // L2 keep the atomics and gathers on chip.
 static int sym3d_chunk(const DevGeom& g, int order, size_t elem_bytes) {
   const double per_base = (double)order * g.rows_per_angle * (double)elem_bytes;
-  const int c = (int)((64.0 * (1 << 20)) / per_base);
+  static const double mb = getenv("CTSM_SYM3D_CHUNK_MB") ? atof(getenv("CTSM_SYM3D_CHUNK_MB")) : 64.0;
+  const int c = (int)((mb * (1 << 20)) / per_base);
   return c < 1 ? 1 : c;
 }
 
+// out[c][r] = in[r][c] for a rows x cols matrix (volume layout changes
+// [n_z][n_y n_x] <-> [n_y n_x][n_z]); 32x32 tiles through shared memory.
+template <typename T>
+__global__ void transpose2d_kernel(const T* __restrict__ in, T* __restrict__ out, long long rows,
+                                   long long cols) {
+  __shared__ T tile[32][33];
+  const long long c0 = (long long)blockIdx.x * 32, r0 = (long long)blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const long long r = r0 + j, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[j][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const long long c = c0 + j, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][j];
+  }
+}
+
+static cudaError_t transpose2d(int dtype, const void* in, void* out, long long rows,
+                               long long cols, cudaStream_t st) {
+  const dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  if (dtype == CTSM_F64)
+    transpose2d_kernel<double><<<grid, dim3(32, 8), 0, st>>>((const double*)in, (double*)out,
+                                                             rows, cols);
+  else
+    transpose2d_kernel<float><<<grid, dim3(32, 8), 0, st>>>((const float*)in, (float*)out, rows,
+                                                            cols);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t fwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
-                         int n_base, const void* x, unsigned long long* yacc, double scale,
-                         unsigned long long* n_upd, int* status, cudaStream_t st, int order) {
+                         int n_base, const void* x_in, unsigned long long* yacc, double scale,
+                         unsigned long long* n_upd, int* status, cudaStream_t st, int order,
+                         void* vol_t) {
   if (n_base <= 0) return cudaSuccess;
+  {
+    const cudaError_t e = transpose2d(dtype, x_in, vol_t, g.n_z, (long long)g.n_x * g.n_y, st);
+    if (e != cudaSuccess) return e;
+  }
+  const void* x = vol_t;
   const long long nxy = (long long)g.n_x * g.n_y;
   const unsigned blocks = (unsigned)((nxy + kWarps3 - 1) / kWarps3);
   const int chunk = sym3d_chunk(g, order, sizeof(unsigned long long));
@@ -1047,8 +1109,9 @@ size_t bwd3d_scratch_elems(const DevGeom& g, int order, int dtype) {
 }
 
 cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
-                         int n_base, const void* y, void* x, int* status, cudaStream_t st,
-                         int order, void* scratch) {
+                         int n_base, const void* y, void* x_out, int* status, cudaStream_t st,
+                         int order, void* scratch, void* vol_t) {
+  void* x = vol_t;  // z-fastest accumulator, transposed into x_out at the end
   const long long h = g.n_x / 2;
   const long long n_orb = order == 8 ? h * (h + 1) / 2 : h * h;
   const unsigned blocks = (unsigned)((n_orb + kWarpsS - 1) / kWarpsS);
@@ -1084,7 +1147,7 @@ cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const i
 #undef CTSM_LAUNCH
     count_launch();
   }
-  return cudaGetLastError();
+  return transpose2d(dtype, vol_t, x_out, (long long)g.n_x * g.n_y, g.n_z, st);
 }
 
 cudaError_t fwd_mf_d8(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
