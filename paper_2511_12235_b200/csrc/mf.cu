@@ -675,7 +675,17 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd
 #ifndef CTSM_KWS
 #define CTSM_KWS 2
 #endif
-constexpr int kWarpsS = CTSM_KWS;
+#ifndef CTSM_KWS_F
+#define CTSM_KWS_F 2
+#endif
+#ifndef CTSM_BWD3_MINB_F
+#define CTSM_BWD3_MINB_F CTSM_BWD3_MINB
+#endif
+// warps (orbits) per block and min blocks per SM of the fp64 / fp32 variants
+template <typename T>
+__host__ __device__ constexpr int bwd3_warps() { return sizeof(T) == 4 ? CTSM_KWS_F : CTSM_KWS; }
+template <typename T>
+__host__ __device__ constexpr int bwd3_minb() { return sizeof(T) == 4 ? CTSM_BWD3_MINB_F : CTSM_BWD3_MINB; }
 template <typename T>
 struct BwdAcc {
   using type = double;
@@ -693,9 +703,10 @@ constexpr int kZcS = CTSM_KZCS;
 // its z-chunk then reads consecutive addresses (shared sectors / L1 hits)
 // instead of one 2 KB-strided sector per row.
 template <typename T, int G, bool TR>
-__global__ void __launch_bounds__(kWarpsS * 32, CTSM_BWD3_MINB) bwd3d_sym_kernel(
+__global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sym_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
     const T* __restrict__ in, T* __restrict__ xout, int accumulate, int* status) {
+  constexpr int kWarpsS = bwd3_warps<T>();
   __shared__ fast::ColumnHead sh[kWarpsS];
   __shared__ fast::PieceCoef sp[kWarpsS][fast::kMaxPieces];
   // fp32 volumes accumulate their per-launch sums in fp32 (fixed order, so
@@ -754,13 +765,14 @@ __global__ void __launch_bounds__(kWarpsS * 32, CTSM_BWD3_MINB) bwd3d_sym_kernel
         auto gather = [&](int t, int my, int mz, double w) {
           const long long r = TR ? (long long)(my + hy) * g.n_det_z + (mz + hz)
                                  : (long long)(mz + hz) * g.n_det_y + (my + hy);
+          const AccT wa = (AccT)w;  // fp32 volumes: FFMA in fp32
 #pragma unroll
-          for (int e = 0; e < 4; ++e) sacc[warp][slot[e]][t][lane] += (AccT)(w * ld(&yb[e][r]));
+          for (int e = 0; e < 4; ++e) sacc[warp][slot[e]][t][lane] += wa * (AccT)__ldg(&yb[e][r]);
           if (G == 8 && full) {
             const long long rr = TR ? (long long)(g.n_det_y - 1 - (my + hy)) * g.n_det_z + (mz + hz)
                                     : r + g.n_det_y - 1 - 2 * (my + hy);
 #pragma unroll
-            for (int e = 4; e < G; ++e) sacc[warp][slot[e]][t][lane] += (AccT)(w * ld(&yb[e][rr]));
+            for (int e = 4; e < G; ++e) sacc[warp][slot[e]][t][lane] += wa * (AccT)__ldg(&yb[e][rr]);
           }
         };
         fast::chunk_weights(g, sh[warp], sp[warp], z0, z1,
@@ -1114,7 +1126,8 @@ cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const i
   void* x = vol_t;  // z-fastest accumulator, transposed into x_out at the end
   const long long h = g.n_x / 2;
   const long long n_orb = order == 8 ? h * (h + 1) / 2 : h * h;
-  const unsigned blocks = (unsigned)((n_orb + kWarpsS - 1) / kWarpsS);
+  const int kWS = dtype == CTSM_F64 ? bwd3_warps<double>() : bwd3_warps<float>();
+  const unsigned blocks = (unsigned)((n_orb + kWS - 1) / kWS);
   const int chunk = sym3d_chunk(g, order, dtype == CTSM_F64 ? 8 : 4);
   const bool tr = scratch != nullptr && n_base > 0;
   // chunks accumulate into x in ascending order (deterministic)
@@ -1133,10 +1146,10 @@ cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const i
 #define CTSM_LAUNCH(T, G)                                                                      \
   do {                                                                                         \
     if (tr)                                                                                    \
-      bwd3d_sym_kernel<T, G, true><<<blocks, kWarpsS * 32, 0, st>>>(                           \
+      bwd3d_sym_kernel<T, G, true><<<blocks, bwd3_warps<T>() * 32, 0, st>>>(                           \
           g, cs + k0, base + k0, nk, (const T*)scratch, (T*)x, k0 > 0, status);                \
     else                                                                                       \
-      bwd3d_sym_kernel<T, G, false><<<blocks, kWarpsS * 32, 0, st>>>(                          \
+      bwd3d_sym_kernel<T, G, false><<<blocks, bwd3_warps<T>() * 32, 0, st>>>(                          \
           g, cs + k0, base + k0, nk, (const T*)y, (T*)x, k0 > 0, status);                      \
   } while (0)
     if (dtype == CTSM_F64) {
