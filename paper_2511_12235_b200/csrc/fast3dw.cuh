@@ -346,6 +346,192 @@ __device__ __forceinline__ double atom_sum3(const ColumnHead& H, const PieceCoef
   return H.kappa * tan_a * v;
 }
 
+// ---- per-group piecewise-cubic tables -------------------------------------
+// For a cell group q the un-scaled atom sum f_q(G) (atom_sum3 without the
+// kappa tan_a factor) is the integral over the group's 2D region of a ramp
+// max(0, G - depth/a'): a piecewise cubic in G whose knots are the atoms' flag
+// thresholds (the depths of the region's vertices). Zero for G <= gmin and
+// the exact linear galpha G - gbeta for G > gmax. Between consecutive knots
+// it is one cubic, so it is recovered exactly (in real arithmetic) from the
+// reference atoms at 4 nodes of the interval: s = -1, -1/3, 1/3, 1 on the
+// interval mapped to [-1, 1], stored as b0 + b1 s + b2 s^2 + b3 s^3 (|s| <= 1:
+// rounding stays at a few ulps of max|f|). Knots closer than ~1e-9 of the
+// group's G range are merged; the sliver they bound then carries the cubic
+// of its neighbour, an error of order jump(f''') w^3 (negligible).
+// Per voxel a group evaluation is then a knot count and one Horner cubic
+// instead of the per-piece flag logic of atom_sum3. A (column, angle) whose
+// knots or intervals exceed the capacity falls back to atom_sum3.
+constexpr int kMaxKnots = 48;
+constexpr int kMaxIntervals = 64;
+struct GroupTable {
+  int ok;
+  unsigned char kbeg[kMaxPieces], kcnt[kMaxPieces], ibeg[kMaxPieces];
+  double kn[kMaxKnots];
+  double2 iv[kMaxIntervals][3];  // (mid, 2/w), (b0, b1), (b2, b3)
+};
+
+// Un-scaled atom sum of group q (the inner loop of atom_sum3).
+__device__ __forceinline__ double group_raw(const ColumnHead& H, const PieceCoef* P, int q,
+                                            double G) {
+  double v = 0.0;
+  for (int k = H.gbeg[q]; k < H.gend[q]; ++k) {
+    const double* c = P[k].c;
+    double tt;
+    switch (H.pkind[k]) {
+      case 0: tt = tri_abs(H, c + 7, c + kLin + 4, G) - tri_abs(H, c, c + kLin, G); break;
+      case 1: tt = trap_abs(H, c, G); break;
+      default: tt = tri_abs(H, c, c + kLin, G) - tri_abs(H, c + 7, c + kLin + 4, G); break;
+    }
+    v += tt;
+  }
+  return v;
+}
+
+// Builds the tables of a planned (column, angle); all lanes, after the
+// __syncwarp() that follows plan_column. Ends with __syncwarp().
+__device__ __forceinline__ void build_group_tables(const ColumnHead& H, const PieceCoef* P,
+                                                   GroupTable& T, int lane) {
+  const int ng = H.ng;
+  // (1) knots, lane q for group q: thresholds in (gmin, gmax) plus both ends,
+  // insertion-sorted in place into the group's slot of T.kn, close ones merged.
+  // Slots are provisional (18 per group) and compacted in (2).
+  constexpr int kRaw = 20;
+  double* raw = &T.iv[0][0].x;  // scratch: kMaxIntervals * 6 doubles >= kMaxPieces * kRaw
+  int cnt = 0;
+  bool bad = false;
+  if (lane < ng) {
+    const int q = lane;
+    const double lo = H.gmin[q], hi = H.gmax[q];
+    double* r = raw + q * kRaw;
+    r[0] = lo;
+    cnt = 1;
+    auto add = [&](double v) {
+      if (!(v > lo && v < hi)) return;
+      if (cnt >= kRaw - 1) {  // cannot happen (<= 3 pieces per cell): be safe
+        bad = true;
+        return;
+      }
+      int i = cnt++;
+      while (i > 0 && r[i - 1] > v) {
+        r[i] = r[i - 1];
+        --i;
+      }
+      r[i] = v;
+    };
+    for (int k = H.gbeg[q]; k < H.gend[q]; ++k) {
+      const double* c = P[k].c;
+      // every threshold any branch of the atom tests (a superset of the
+      // knots is harmless: the cubic just spans a split interval)
+      if (H.pkind[k] == 1) {
+        add(c[0]); add(c[1]); add(c[2]); add(c[3]);
+        if (H.flat) {
+          add(c[11]);
+          add(c[12]);
+        }
+      } else {
+        for (int e = 0; e < 2; ++e) {
+          add(c[7 * e]);
+          add(c[7 * e + 1]);
+          add(c[7 * e + 2]);
+        }
+      }
+    }
+    if (hi > lo) r[cnt++] = hi;
+    // merge knots closer than tol; the ends stay gmin and gmax exactly (a
+    // range below tol keeps gmin only: zero below, linear above)
+    const double tol = 1e-9 * (hi - lo) + 4e-16 * fabs(hi);
+    int m = 1;
+    for (int i = 1; i < cnt; ++i)
+      if (r[i] - r[m - 1] > tol) r[m++] = r[i];
+    if (m > 1) r[m - 1] = hi;
+    cnt = m;
+  }
+  // (2) offsets (warp prefix over groups) and capacity check
+  int kb = cnt, ib = cnt + 1;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, kb, o), b = __shfl_up_sync(0xffffffffu, ib, o);
+    if (lane >= o) {
+      kb += a;
+      ib += b;
+    }
+  }
+  const int kt = __shfl_sync(0xffffffffu, kb, 31), it = __shfl_sync(0xffffffffu, ib, 31);
+  kb -= cnt;
+  ib -= cnt + 1;
+  const bool fits = kt <= kMaxKnots && it <= kMaxIntervals && !__any_sync(0xffffffffu, bad);
+  if (fits && lane < ng) {
+    const double* r = raw + lane * kRaw;
+    for (int i = 0; i < cnt; ++i) T.kn[kb + i] = r[i];
+    T.kbeg[lane] = (unsigned char)kb;
+    T.kcnt[lane] = (unsigned char)cnt;
+    T.ibeg[lane] = (unsigned char)ib;
+  }
+  if (lane == 0) T.ok = fits;
+  __syncwarp();
+  if (!fits) return;
+  // (3) node values of the cubic intervals: item = (group, interval, node);
+  // the interval slots of group q are ibeg+1 .. ibeg+cnt-1 (slot ibeg: zero,
+  // ibeg+cnt: linear); node values go to the (b0,b1),(b2,b3) slots first.
+  int tot = 0;
+  for (int q = 0; q < ng; ++q) tot += 4 * (T.kcnt[q] - 1);
+  for (int it0 = lane; it0 < tot; it0 += 32) {
+    int q = 0, rem = it0;
+    while (rem >= 4 * (T.kcnt[q] - 1)) {
+      rem -= 4 * (T.kcnt[q] - 1);
+      ++q;
+    }
+    const int j = rem >> 2, nd = rem & 3;
+    const double k0 = T.kn[T.kbeg[q] + j], k1 = T.kn[T.kbeg[q] + j + 1];
+    const double mid = 0.5 * (k0 + k1), hw = 0.5 * (k1 - k0);
+    const double G = nd == 0 ? k0 : (nd == 3 ? k1 : mid + hw * (nd == 1 ? -1.0 / 3.0 : 1.0 / 3.0));
+    double* dst = &T.iv[T.ibeg[q] + 1 + j][1].x;
+    dst[nd] = group_raw(H, P, q, G);
+  }
+  __syncwarp();
+  // (4) coefficients, one lane per interval slot
+  for (int s = lane; s < it; s += 32) {
+    int q = 0;
+    while (q + 1 < ng && T.ibeg[q + 1] <= s) ++q;
+    const int j = s - T.ibeg[q], m = T.kcnt[q];
+    double2* e = T.iv[s];
+    if (j == 0) {
+      e[0] = make_double2(0.0, 0.0);
+      e[1] = make_double2(0.0, 0.0);
+      e[2] = make_double2(0.0, 0.0);
+    } else if (j == m) {
+      const double gm = H.gmax[q], al = H.galpha[q];
+      e[0] = make_double2(gm, 1.0);
+      e[1] = make_double2(al * gm - H.gbeta[q], al);
+      e[2] = make_double2(0.0, 0.0);
+    } else {
+      const double k0 = T.kn[T.kbeg[q] + j - 1], k1 = T.kn[T.kbeg[q] + j];
+      const double f0 = e[1].x, f1 = e[1].y, f2 = e[2].x, f3 = e[2].y;
+      const double E1 = 0.5 * (f0 + f3), E2 = 0.5 * (f1 + f2);
+      const double O1 = 0.5 * (f3 - f0), O2 = 0.5 * (f2 - f1);
+      const double b2 = 1.125 * (E1 - E2);
+      const double b0 = E2 - b2 * (1.0 / 9.0);
+      const double b1 = 0.125 * (27.0 * O2 - O1);
+      const double b3 = O1 - b1;
+      e[0] = make_double2(0.5 * (k0 + k1), 2.0 / (k1 - k0));
+      e[1] = make_double2(b0, b1);
+      e[2] = make_double2(b2, b3);
+    }
+  }
+  __syncwarp();
+}
+
+// f_q(G) from the table (see above).
+__device__ __forceinline__ double group_table(const GroupTable& T, int q, double G) {
+  const double* kn = T.kn + T.kbeg[q];
+  const int m = T.kcnt[q];
+  int j = 0;
+  for (int i = 0; i < m; ++i) j += kn[i] < G;
+  const double2* e = T.iv[T.ibeg[q] + j];
+  const double2 h = e[0], b01 = e[1], b23 = e[2];
+  const double s = (G - h.x) * h.y;
+  return fma(fma(fma(b23.y, s, b23.x), s, b01.y), s, b01.x);
+}
+
 // Weights of voxel iz of a planned column: emit(cell m_y, row m_z, w) for every
 // w > 1e-16 inside the detector (weights3d.cpp:426-458).
 template <typename Emit>
@@ -396,9 +582,20 @@ __device__ __forceinline__ void voxel_weights(const DevGeom& g, const ColumnHead
 // top face of voxel iz is the bottom face of voxel iz+1, so the atom sums
 // F(L, zt) computed for voxel iz are exactly F(L, zb) of voxel iz+1 and are
 // reused (up to 4 row edges cached). emit(iz, cell, row, w).
+__device__ __noinline__ double atom_sum3_slow(const ColumnHead& H, const PieceCoef* P, int q,
+                                              double tan_a, double gs, double zref) {
+  return atom_sum3(H, P, q, tan_a, gs, zref);
+}
+
 template <typename Emit>
 __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead& H,
-                                              const PieceCoef* P, int z0, int z1, Emit&& emit) {
+                                              const PieceCoef* P, int z0, int z1, Emit&& emit,
+                                              const GroupTable* T = nullptr) {
+  const bool tab = T != nullptr && T->ok;
+  auto Fq = [&](int q, double tan_a, double gs, double zref) -> double {
+    if (tab) return H.kappa * tan_a * group_table(*T, q, zref * gs);
+    return T != nullptr ? atom_sum3_slow(H, P, q, tan_a, gs, zref) : atom_sum3(H, P, q, tan_a, gs, zref);
+  };
   const int row_lo = -g.n_det_z / 2, row_hi = g.n_det_z / 2 - 1;
   const double dz_sdd = g.dz_sdd, sdd_dz = g.sdd_dz;
   const double c_mn = sdd_dz * H.dmin_inv, c_mx = sdd_dz * H.dmax_inv;
@@ -439,8 +636,8 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
         else if (L == cL1) Fb = cF1;
         else if (L == cL2) Fb = cF2;
         else if (L == cL3) Fb = cF3;
-        else Fb = atom_sum3(H, P, q, tan_a, gs, zb_s);
-        const double Ft = atom_sum3(H, P, q, tan_a, gs, zt_s);
+        else Fb = Fq(q, tan_a, gs, zb_s);
+        const double Ft = Fq(q, tan_a, gs, zt_s);
         switch (nn) {
           case 0: nL0 = L; nF0 = Ft; break;
           case 1: nL1 = L; nF1 = Ft; break;

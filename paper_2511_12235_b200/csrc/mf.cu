@@ -123,6 +123,28 @@ __global__ void bwd_reduce_kernel(long long n, int n_chunks, const double* __res
 // memory, fast3dw.cuh) and its lanes evaluate contiguous z-chunks of voxels.
 // Forward scatters w*x into the fixed-point sinogram accumulator; backward
 // accumulates w*y per voxel in shared memory in a fixed order (deterministic).
+// Per-group piecewise-cubic tables of a planned (column, angle)
+// (fast3dw.cuh), opt-in with CTSM_TABLE3D: measured slower than the per-piece
+// atom evaluation with its linear / zero short cuts at C3 (fwd 402 vs 332 ms,
+// bwd 344 vs 290 ms per projection, r1o), so the default keeps the atoms.
+#ifdef CTSM_TABLE3D
+#define CTSM_TABLE_DECL(n) __shared__ fast::GroupTable stab[n]
+#define CTSM_TABLE_PTR (&stab[warp])
+#else
+#define CTSM_TABLE_PTR nullptr
+#define CTSM_TABLE_DECL(n)
+#endif
+__device__ __forceinline__ const fast::GroupTable* table3d(const fast::ColumnHead& H,
+                                                           const fast::PieceCoef* P,
+                                                           fast::GroupTable* T, int lane) {
+#ifdef CTSM_TABLE3D
+  fast::build_group_tables(H, P, *T, lane);
+  return T;
+#else
+  return nullptr;
+#endif
+}
+
 constexpr int kWarps3 = 4;
 constexpr int kZcMax = 16;  // voxels per lane per z-block (z-block = 512 voxels)
 
@@ -134,6 +156,7 @@ __global__ void __launch_bounds__(kWarps3 * 32, 4) proj3d_kernel(
   __shared__ fast::ColumnHead sh[kWarps3];
   __shared__ fast::PieceCoef sp[kWarps3][fast::kMaxPieces];
   __shared__ double sacc[kWarps3][kZcMax][32];
+  CTSM_TABLE_DECL(kWarps3);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long nxy = (long long)g.n_x * g.n_y;
   const long long col = (long long)blockIdx.x * kWarps3 + warp;
@@ -158,6 +181,7 @@ __global__ void __launch_bounds__(kWarps3 * 32, 4) proj3d_kernel(
       if (!ok) continue;
       const fast::ColumnHead& H = sh[warp];
       const fast::PieceCoef* P = sp[warp];
+      const fast::GroupTable* TB = table3d(H, P, CTSM_TABLE_PTR, lane);
       if (kFwd) {
         unsigned long long* yb = yacc + (long long)ip * rpa;
         // consecutive emits of a lane often hit the same (row, cell) as z
@@ -176,13 +200,13 @@ __global__ void __launch_bounds__(kWarps3 * 32, 4) proj3d_kernel(
             pr = r;
             pv = v;
           }
-        });
+        }, TB);
         if (pr >= 0 && pv != 0) atomicAdd(&yb[pr], (unsigned long long)pv);
       } else {
         const T* yb = in + (long long)ip * rpa;
         fast::chunk_weights(g, H, P, z0, z1, [&](int iz, int my, int mz, double w) {
           sacc[warp][iz - z0][lane] += w * ld(&yb[(long long)(mz + hz) * g.n_det_y + (my + hy)]);
-        });
+        }, TB);
       }
     }
     if (!kFwd)
@@ -585,7 +609,13 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd
   __shared__ fast::ColumnHead sh[kWarps3];
   __shared__ fast::PieceCoef sp[kWarps3][fast::kMaxPieces];
   extern __shared__ __align__(16) unsigned char dyn_smem[];
-  T(*xsm)[G][kZcF][32] = reinterpret_cast<T(*)[G][kZcF][32]>(dyn_smem);
+  // [warp][t][chunk][lane][V]: the G image values of (t, lane) as NC 16-byte
+  // vectors, each chunk conflict-free across the lanes (one LDS.128 each)
+  constexpr int V = 16 / sizeof(T), NC = G / V;
+  T* xsm = reinterpret_cast<T*>(dyn_smem) + (size_t)(threadIdx.x >> 5) * kZcF * G * 32;
+  auto xidx = [&](int t, int e, int ln) { return ((t * NC + e / V) * 32 + ln) * V + e % V; };
+  __shared__ long long sab[kWarps3][G];  // row base of every image angle of the base angle
+  CTSM_TABLE_DECL(kWarps3);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = g.n_x;
   const long long nxy = (long long)n * g.n_y;
@@ -607,7 +637,7 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd
       // z-fastest volume: the lane's z-chunk is contiguous (its sectors are
       // re-hit in L1 across t), instead of one sector per voxel
       const T* src = in + ((long long)ry * n + rx) * g.n_z;
-      for (int t = 0; t < zc; ++t) xsm[warp][e][t][lane] = (z0 + t < z1) ? src[z0 + t] : (T)0;
+      for (int t = 0; t < zc; ++t) xsm[xidx(t, e, lane)] = (z0 + t < z1) ? src[z0 + t] : (T)0;
     }
     __syncwarp();
     for (int kk = 0; kk < n_base; ++kk) {
@@ -616,9 +646,11 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd
       const bool full = G == 4 || ((i != 0) && (8 * i != g.n_angles));
       const int ne = full ? G : 4;
       __syncwarp();
+      if (lane < G) sab[warp][lane] = (long long)d4_angle(g.n_angles, i, lane) * rpa;
       const bool ok = fast::plan_column(g, a.C, a.S, ix, iy, status, sh[warp], sp[warp], lane);
       __syncwarp();
       if (!ok) continue;
+      const fast::GroupTable* TB = table3d(sh[warp], sp[warp], CTSM_TABLE_PTR, lane);
 #ifdef CTSM_EXP_PLAN_ONLY
       continue;  // timing experiment: planning cost alone
 #endif
@@ -626,18 +658,25 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd
       // row pr = (mz + hz) ndy + py, py = my + hy; reflections write -1-my
       // the run of one row is summed in FP64 (fixed lane order: deterministic)
       // and converted to fixed point once, at the flush
+      // fp32 volumes sum a row run in fp32 (1-3 terms; converted to fixed
+      // point at the flush), fp64 volumes in fp64
+      using PT = T;
       long long pr = -1;
-      double pv[G];
+      PT pv[G];
       int py = 0;
 #pragma unroll
-      for (int e = 0; e < G; ++e) pv[e] = 0.0;
+      for (int e = 0; e < G; ++e) pv[e] = (PT)0;
       auto flush = [&]() {
 #pragma unroll
         for (int e = 0; e < G; ++e)
-          if (e < ne && pv[e] != 0.0) {
+          if (e < ne && pv[e] != (PT)0) {
             const long long r = (e < 4) ? pr : pr + ndy - 1 - 2 * py;
-            atomicAdd(yacc + (long long)d4_angle(g.n_angles, i, e) * rpa + r,
-                      (unsigned long long)__double2ll_rn(pv[e] * scale));
+#ifdef CTSM_EXP_NO_SCATTER
+            if (pv[e] == (PT)1.2345) yacc[r] = 1;  // timing experiment: no atomics
+#else
+            atomicAdd(yacc + sab[warp][e] + r,
+                      (unsigned long long)__double2ll_rn((double)pv[e] * scale));
+#endif
           }
       };
       fast::chunk_weights(g, sh[warp], sp[warp], z0, z1, [&](int iz, int my, int mz, double w) {
@@ -648,12 +687,25 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd
           pr = r;
           py = my + hy;
 #pragma unroll
-          for (int e = 0; e < G; ++e) pv[e] = 0.0;
+          for (int e = 0; e < G; ++e) pv[e] = (PT)0;
         }
+        const PT wp = (PT)w;
+        const T* xv = xsm + xidx(iz - z0, 0, lane);
 #pragma unroll
-        for (int e = 0; e < G; ++e)
-          if (e < ne) pv[e] += w * (double)xsm[warp][e][iz - z0][lane];
-      });
+        for (int c = 0; c < NC; ++c) {
+          T v[V];
+          if constexpr (sizeof(T) == 4) {
+            const float4 q = reinterpret_cast<const float4*>(xv)[c * 32];
+            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+          } else {
+            const double2 q = reinterpret_cast<const double2*>(xv)[c * 32];
+            v[0] = q.x; v[1] = q.y;
+          }
+#pragma unroll
+          for (int u = 0; u < V; ++u)
+            if (c * V + u < ne) pv[c * V + u] += wp * v[u];
+        }
+      }, TB);
       if (pr >= 0) flush();
     }
   }
@@ -698,6 +750,22 @@ struct BwdAcc<float> {
 #endif
 constexpr int kZcS = CTSM_KZCS;
 
+// G consecutive values (16-byte aligned) with 128-bit read-only loads.
+template <typename T, int G>
+__device__ __forceinline__ void load_vec(const T* p, T (&v)[G]) {
+  constexpr int per = 16 / sizeof(T);
+#pragma unroll
+  for (int c = 0; c < G / per; ++c) {
+    if constexpr (sizeof(T) == 4) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(p) + c);
+      v[4 * c] = q.x; v[4 * c + 1] = q.y; v[4 * c + 2] = q.z; v[4 * c + 3] = q.w;
+    } else {
+      const double2 q = __ldg(reinterpret_cast<const double2*>(p) + c);
+      v[2 * c] = q.x; v[2 * c + 1] = q.y;
+    }
+  }
+}
+
 // TR: `in` is the launch's image rows transposed per (base slot, image) into
 // [k * G + e][my][mz] (mz fastest, transpose_images below): a lane walking up
 // its z-chunk then reads consecutive addresses (shared sectors / L1 hits)
@@ -714,6 +782,7 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
   // below the fp32 tolerance, and half the shared memory -> more warps/SM
   using AccT = typename BwdAcc<T>::type;
   __shared__ AccT sacc[kWarpsS][G][kZcS][32];
+  CTSM_TABLE_DECL(kWarpsS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = g.n_x, h = n / 2;
   const long long orb = (long long)blockIdx.x * kWarpsS + warp;
@@ -743,11 +812,13 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
       const int i = base[kk];
       const AngleCS a = cs[kk];
       const bool full = G == 4 || ((i != 0) && (8 * i != g.n_angles));
-      const T* yb[G];
+      const T* yb[TR ? 1 : G];
+      if (TR) {
+        yb[0] = in + (long long)kk * G * rpa;
+      } else {
 #pragma unroll
-      for (int e = 0; e < G; ++e)
-        yb[e] = TR ? in + (long long)(kk * G + e) * rpa
-                   : in + (long long)d4_angle(g.n_angles, i, e) * rpa;
+        for (int e = 0; e < (TR ? 1 : G); ++e) yb[e] = in + (long long)d4_angle(g.n_angles, i, e) * rpa;
+      }
 #pragma unroll 1
       for (int hm = 0; hm < n_mem; ++hm) {
         int cx, cy;
@@ -756,27 +827,42 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
         const bool ok = fast::plan_column(g, a.C, a.S, cx, cy, status, sh[warp], sp[warp], lane);
         __syncwarp();
         if (!ok) continue;
+        const fast::GroupTable* TB = table3d(sh[warp], sp[warp], CTSM_TABLE_PTR, lane);
 #ifdef CTSM_EXP_PLAN_ONLY
         continue;  // timing experiment: planning cost alone
 #endif
-        int slot[G];
+        // accumulator slots of the images, 3 bits each (one register: kept
+        // live through the gathers instead of re-derived per weight)
+        unsigned pk = 0;
 #pragma unroll
-        for (int e = 0; e < G; ++e) slot[e] = d4_compose(e, hm);
+        for (int e = 0; e < G; ++e) pk |= (unsigned)d4_compose(e, hm) << (3 * e);
+#ifdef CTSM_EXP_NO_GATHER
+#define CTSM_LDY(p) ((AccT)1)
+#else
+#define CTSM_LDY(p) ((AccT)__ldg(p))
+#endif
         auto gather = [&](int t, int my, int mz, double w) {
-          const long long r = TR ? (long long)(my + hy) * g.n_det_z + (mz + hz)
-                                 : (long long)(mz + hz) * g.n_det_y + (my + hy);
           const AccT wa = (AccT)w;  // fp32 volumes: FFMA in fp32
+          if (TR) {
+            // the G image values of (my, mz): one contiguous vector
+            T v[G];
+            load_vec<T, G>(yb[0] + ((long long)(my + hy) * g.n_det_z + (mz + hz)) * G, v);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) sacc[warp][slot[e]][t][lane] += wa * (AccT)__ldg(&yb[e][r]);
-          if (G == 8 && full) {
-            const long long rr = TR ? (long long)(g.n_det_y - 1 - (my + hy)) * g.n_det_z + (mz + hz)
-                                    : r + g.n_det_y - 1 - 2 * (my + hy);
+            for (int e = 0; e < G; ++e)
+              if (e < 4 || full) sacc[warp][(pk >> (3 * e)) & 7][t][lane] += wa * (AccT)v[e];
+          } else {
+            const long long r = (long long)(mz + hz) * g.n_det_y + (my + hy);
 #pragma unroll
-            for (int e = 4; e < G; ++e) sacc[warp][slot[e]][t][lane] += wa * (AccT)__ldg(&yb[e][rr]);
+            for (int e = 0; e < 4; ++e) sacc[warp][(pk >> (3 * e)) & 7][t][lane] += wa * CTSM_LDY(&yb[e][r]);
+            if (G == 8 && full) {
+              const long long rr = r + g.n_det_y - 1 - 2 * (my + hy);
+#pragma unroll
+              for (int e = 4; e < G; ++e) sacc[warp][(pk >> (3 * e)) & 7][t][lane] += wa * CTSM_LDY(&yb[e][rr]);
+            }
           }
         };
         fast::chunk_weights(g, sh[warp], sp[warp], z0, z1,
-                            [&](int iz, int my, int mz, double w) { gather(iz - z0, my, mz, w); });
+                            [&](int iz, int my, int mz, double w) { gather(iz - z0, my, mz, w); }, TB);
       }
     }
     for (int e = 0; e < (diag ? 4 : G); ++e) {
@@ -1093,17 +1179,21 @@ cudaError_t fwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const i
   return cudaGetLastError();
 }
 
-// Image rows of base slots [0, nk) -> yt[(k * G + e)][my][mz] (tiled transpose).
+// Image rows of base slots [0, nk) -> yt[k][my][mz][e] (tiled transpose, the
+// G images of a base slot interleaved): image e >= 4 (a reflection) is stored
+// at the mirrored detector column ndy-1-my, so one (my, mz) of the base angle
+// reads the values of all its images as one contiguous G-vector.
 template <typename T>
 __global__ void transpose_images_kernel(const T* __restrict__ y, const int* __restrict__ base,
                                         int G, int n_angles, int ndy, int ndz,
                                         T* __restrict__ yt) {
   __shared__ T tile[32][33];
   const int slab = blockIdx.z;
-  const int a = d4_angle(n_angles, base[slab / G], slab % G);
+  const int e = slab % G;
+  const int a = d4_angle(n_angles, base[slab / G], e);
   const long long rpa = (long long)ndy * ndz;
   const T* src = y + (long long)a * rpa;
-  T* dst = yt + (long long)slab * rpa;
+  T* dst = yt + (long long)(slab / G) * G * rpa + e;
   const int cx = blockIdx.x * 32 + threadIdx.x;  // my
   const int rz = blockIdx.y * 32 + threadIdx.y;  // mz
   for (int j = 0; j < 32; j += 8)
@@ -1112,7 +1202,10 @@ __global__ void transpose_images_kernel(const T* __restrict__ y, const int* __re
   const int oz = blockIdx.y * 32 + threadIdx.x;  // mz
   const int oy = blockIdx.x * 32 + threadIdx.y;  // my
   for (int j = 0; j < 32; j += 8)
-    if (oz < ndz && oy + j < ndy) dst[(long long)(oy + j) * ndz + oz] = tile[threadIdx.x][threadIdx.y + j];
+    if (oz < ndz && oy + j < ndy) {
+      const int myc = e < 4 ? oy + j : ndy - 1 - (oy + j);
+      dst[((long long)myc * ndz + oz) * G] = tile[threadIdx.x][threadIdx.y + j];
+    }
 }
 
 size_t bwd3d_scratch_elems(const DevGeom& g, int order, int dtype) {
