@@ -557,8 +557,10 @@ static int bwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d,
   } else if (symmetry_order(g) == 8) {
     const int nc = bwd_d8_chunks(d, nb);
     if (nc > 1) CT_TRY(ensure(ctx, ctx->part, (size_t)nc * g->n_x * g->n_y * sizeof(double)));
+    const size_t ne = bwd_d8_scratch_elems(d, nb, dtype);
+    if (ne) CT_TRY(ensure(ctx, ctx->bwd_t, ne * (dtype == CTSM_F64 ? 8 : 4)));
     CT_CUDA(bwd_mf_d8(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, y, x,
-                      (double*)ctx->part.p, nc, ctx->status, st));
+                      (double*)ctx->part.p, nc, ctx->status, st, ne ? ctx->bwd_t.p : nullptr));
   } else {
     const int nc = bwd_sym_chunks(d, nb);
     if (nc > 1) CT_TRY(ensure(ctx, ctx->part, (size_t)nc * g->n_x * g->n_y * sizeof(double)));

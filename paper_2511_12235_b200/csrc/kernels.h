@@ -79,9 +79,12 @@ cudaError_t fwd_mf_d8(const DevGeom& g, int dtype, const AngleCS* cs, const int*
                       int n_base, const void* x, unsigned long long* yacc, double scale,
                       unsigned long long* n_upd, int* status, cudaStream_t st);
 int bwd_d8_chunks(const DevGeom& g, int n_base);
+// yt: scratch of bwd_d8_scratch_elems() elements of the dtype (the base
+// angles' rows with their 8 images interleaved), or null (direct gathers)
+size_t bwd_d8_scratch_elems(const DevGeom& g, int n_base, int dtype);
 cudaError_t bwd_mf_d8(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                       int n_base, const void* y, void* x, double* part, int n_chunks,
-                      int* status, cudaStream_t st);
+                      int* status, cudaStream_t st, void* yt);
 // mode 0: zero the fixed-point rows of the listed angles; mode 1: convert them
 cudaError_t rows_list(const DevGeom& g, int dtype, const int* angles, int n_list,
                       unsigned long long* acc, double scale, void* y, int mode, cudaStream_t st);

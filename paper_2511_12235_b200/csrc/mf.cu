@@ -40,6 +40,21 @@ __device__ __forceinline__ void count_updates(unsigned long long* n_upd, unsigne
 }
 
 // 2D pixel tile per block: 16 x 8 pixels, 128 threads.
+// G consecutive values (16-byte aligned) with 128-bit read-only loads.
+template <typename T, int G>
+__device__ __forceinline__ void load_vec(const T* p, T (&v)[G]) {
+  constexpr int per = 16 / sizeof(T);
+#pragma unroll
+  for (int c = 0; c < G / per; ++c) {
+    if constexpr (sizeof(T) == 4) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(p) + c);
+      v[4 * c] = q.x; v[4 * c + 1] = q.y; v[4 * c + 2] = q.z; v[4 * c + 3] = q.w;
+    } else {
+      const double2 q = __ldg(reinterpret_cast<const double2*>(p) + c);
+      v[2 * c] = q.x; v[2 * c + 1] = q.y;
+    }
+  }
+}
 constexpr int kTx = 16, kTy = 8;
 
 // Forward 2D: block = 16x8 pixel tile x a chunk of kFwdAngles angles; each
@@ -500,7 +515,11 @@ __global__ void __launch_bounds__(128, CTSM_D8F_MINB) fwd2d_d8_kernel(
 // on the diagonal, whose reflections coincide with rotations). The weight set
 // of member h at base angle i is gathered against angle g i, cell g m for
 // every group element g into the accumulator of pixel (g o h) p0.
-template <typename T>
+//
+// TR: y is the base angles' image rows interleaved, yt[k][m][e] (image e >= 4
+// at the mirrored cell, transpose_images_kernel): a weight reads the 8 image
+// values with vector loads instead of 8 scattered ones.
+template <typename T, bool TR>
 __global__ void __launch_bounds__(128, CTSM_D8B_MINB) bwd2d_d8_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
     int chunk, const T* __restrict__ y, T* __restrict__ x, double* __restrict__ part,
@@ -531,7 +550,7 @@ __global__ void __launch_bounds__(128, CTSM_D8B_MINB) bwd2d_d8_kernel(
     int rows[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e)
-      rows[e] = d4_angle(g.n_angles, i, e) * g.rows_per_angle + g.n_det_y / 2;
+      rows[e] = TR ? 0 : d4_angle(g.n_angles, i, e) * g.rows_per_angle + g.n_det_y / 2;
     // one inlined sweep for all members (small code: the member loop is not
     // unrolled); tsum[ge] collects member hm's sums per group element and is
     // folded into acc[ge o hm] by a static permutation per member.
@@ -543,12 +562,21 @@ __global__ void __launch_bounds__(128, CTSM_D8B_MINB) bwd2d_d8_kernel(
       double tsum[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) tsum[e] = 0.0;
+      const T* yk = y + ((long long)kk * g.n_det_y + g.n_det_y / 2) * 8;
       fast::pixel_weights(g, a.C, a.S, mx, my, status, [&](int m, double w) {
+        if (TR) {
+          T v[8];
+          load_vec<T, 8>(yk + (long long)m * 8, v);
 #pragma unroll
-        for (int ge = 0; ge < 4; ++ge) tsum[ge] += w * ld(&y[rows[ge] + m]);
-        if (full) {
+          for (int ge = 0; ge < 8; ++ge)
+            if (ge < 4 || full) tsum[ge] += w * (double)v[ge];
+        } else {
 #pragma unroll
-          for (int ge = 4; ge < 8; ++ge) tsum[ge] += w * ld(&y[rows[ge] - 1 - m]);
+          for (int ge = 0; ge < 4; ++ge) tsum[ge] += w * ld(&y[rows[ge] + m]);
+          if (full) {
+#pragma unroll
+            for (int ge = 4; ge < 8; ++ge) tsum[ge] += w * ld(&y[rows[ge] - 1 - m]);
+          }
         }
       });
       switch (hm) {
@@ -750,21 +778,7 @@ struct BwdAcc<float> {
 #endif
 constexpr int kZcS = CTSM_KZCS;
 
-// G consecutive values (16-byte aligned) with 128-bit read-only loads.
-template <typename T, int G>
-__device__ __forceinline__ void load_vec(const T* p, T (&v)[G]) {
-  constexpr int per = 16 / sizeof(T);
-#pragma unroll
-  for (int c = 0; c < G / per; ++c) {
-    if constexpr (sizeof(T) == 4) {
-      const float4 q = __ldg(reinterpret_cast<const float4*>(p) + c);
-      v[4 * c] = q.x; v[4 * c + 1] = q.y; v[4 * c + 2] = q.z; v[4 * c + 3] = q.w;
-    } else {
-      const double2 q = __ldg(reinterpret_cast<const double2*>(p) + c);
-      v[2 * c] = q.x; v[2 * c + 1] = q.y;
-    }
-  }
-}
+
 
 // TR: `in` is the launch's image rows transposed per (base slot, image) into
 // [k * G + e][my][mz] (mz fastest, transpose_images below): a lane walking up
@@ -1280,21 +1294,61 @@ int bwd_d8_chunks(const DevGeom& g, int n_base) {
   return (int)(c < 1 ? 1 : c);
 }
 
+// 2D rows of the base angles -> yt[k][m][e] (8 images interleaved, e >= 4 at
+// the mirrored cell): one thread per output element, coalesced writes.
+template <typename T>
+__global__ void interleave2d_kernel(const T* __restrict__ y, const int* __restrict__ base,
+                                    int n_base, int n_angles, int ndy, T* __restrict__ yt) {
+  const long long n = (long long)n_base * ndy * 8;
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < n;
+       o += (long long)gridDim.x * blockDim.x) {
+    const int e = (int)(o & 7);
+    const long long km = o >> 3;
+    const int k = (int)(km / ndy), m = (int)(km % ndy);
+    const int a = d4_angle(n_angles, base[k], e);
+    yt[o] = y[(long long)a * ndy + (e < 4 ? m : ndy - 1 - m)];
+  }
+}
+
+// fp32 only: measured at C1, the interleaved rows speed up the fp32 gathers
+// (0.81 -> 0.74 ms) but slow the fp64 ones (0.77 -> 0.92 ms; 64-byte vectors
+// spread over more L1 sectors than the 8 nearly coalesced direct rows)
+size_t bwd_d8_scratch_elems(const DevGeom& g, int n_base, int dtype) {
+  if (dtype == CTSM_F64 || getenv("CTSM_BWD2_PLAIN")) return 0;
+  return (size_t)n_base * 8 * g.rows_per_angle;
+}
+
 cudaError_t bwd_mf_d8(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                       int n_base, const void* y, void* x, double* part, int n_chunks,
-                      int* status, cudaStream_t st) {
+                      int* status, cudaStream_t st, void* yt) {
   const long long h = g.n_x / 2;
   const unsigned blocks = (unsigned)((h * (h + 1) / 2 + 127) / 128);
   const int chunk = (n_base + n_chunks - 1) / (n_chunks > 0 ? n_chunks : 1);
   const int nc = chunk > 0 ? (n_base + chunk - 1) / chunk : 1;
   double* p = nc > 1 ? part : nullptr;
   const dim3 grid(blocks, (unsigned)(nc > 0 ? nc : 1));
-  if (dtype == CTSM_F64)
-    bwd2d_d8_kernel<double><<<grid, 128, 0, st>>>(g, cs, base, n_base, chunk, (const double*)y,
-                                                  (double*)x, p, status);
-  else
-    bwd2d_d8_kernel<float><<<grid, 128, 0, st>>>(g, cs, base, n_base, chunk, (const float*)y,
-                                                 (float*)x, p, status);
+  const bool tr = yt != nullptr && n_base > 0;
+  if (tr) {
+    const unsigned gb = grid_for((uint64_t)n_base * g.n_det_y * 8);
+    if (dtype == CTSM_F64)
+      interleave2d_kernel<double><<<gb, 256, 0, st>>>((const double*)y, base, n_base, g.n_angles,
+                                                      g.n_det_y, (double*)yt);
+    else
+      interleave2d_kernel<float><<<gb, 256, 0, st>>>((const float*)y, base, n_base, g.n_angles,
+                                                     g.n_det_y, (float*)yt);
+    count_launch();
+  }
+#define CTSM_LAUNCH(T)                                                                        \
+  do {                                                                                        \
+    if (tr)                                                                                   \
+      bwd2d_d8_kernel<T, true><<<grid, 128, 0, st>>>(g, cs, base, n_base, chunk, (const T*)yt, \
+                                                     (T*)x, p, status);                       \
+    else                                                                                      \
+      bwd2d_d8_kernel<T, false><<<grid, 128, 0, st>>>(g, cs, base, n_base, chunk,             \
+                                                      (const T*)y, (T*)x, p, status);         \
+  } while (0)
+  if (dtype == CTSM_F64) CTSM_LAUNCH(double); else CTSM_LAUNCH(float);
+#undef CTSM_LAUNCH
   count_launch();
   if (nc > 1) {
     const long long np = (long long)g.n_x * g.n_y;
