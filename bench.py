@@ -353,10 +353,14 @@ def run_ours(args):
     try:
         ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_kernels.json")))
         tname = "double" if args.dtype == "f64" else "float"
-        key = f"{cfg}_{args.dtype}:{kname}_kernel<{tname}>"
-        if key in ncu:
-            traffic = ncu[key]["dram_bytes"]
-            ncu_pipe = ncu[key].get("fp64_pipe_pct")
+        # kernel names as ncu prints them: fwd2d_d8_kernel<double>,
+        # bwd2d_d8_kernel<float, 1>, fwd3d_sym_kernel<float, 8>, ...
+        kbase = kname.replace("3d_d8", "3d_sym")
+        prefix = f"{cfg}_{args.dtype}:{kbase}_kernel<{tname}"
+        hits = [k for k in sorted(ncu) if k == prefix + ">" or k.startswith(prefix + ",")]
+        if hits:
+            traffic = ncu[hits[0]]["dram_bytes"]
+            ncu_pipe = ncu[hits[0]].get("fp64_pipe_pct")
     except (OSError, ValueError, KeyError):
         pass
     roof = {"bound": "fp64", "kernel": kname,
