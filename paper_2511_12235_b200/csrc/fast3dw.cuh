@@ -592,10 +592,6 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
                                               const PieceCoef* P, int z0, int z1, Emit&& emit,
                                               const GroupTable* T = nullptr) {
   const bool tab = T != nullptr && T->ok;
-  auto Fq = [&](int q, double tan_a, double gs, double zref) -> double {
-    if (tab) return H.kappa * tan_a * group_table(*T, q, zref * gs);
-    return T != nullptr ? atom_sum3_slow(H, P, q, tan_a, gs, zref) : atom_sum3(H, P, q, tan_a, gs, zref);
-  };
   const int row_lo = -g.n_det_z / 2, row_hi = g.n_det_z / 2 - 1;
   const double dz_sdd = g.dz_sdd, sdd_dz = g.sdd_dz;
   const double c_mn = sdd_dz * H.dmin_inv, c_mx = sdd_dz * H.dmax_inv;
@@ -603,6 +599,21 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
   for (int q = 0; q < H.ng; ++q) {
     const double w2d = H.gw2d[q];
     const int cell = H.gcell[q];
+    // the group's short cuts in registers, division-free: with u = zref ga,
+    // G <= gmin  <=>  u <= gmin |L|  (F = 0), and G > gmax  <=>  u > gmax |L|,
+    // where F = kappa tan_a (galpha G - gbeta) = l1 zref - l2 |L|
+    // (tan_a = |L| dz/sdd, tan_a G = zref ga dz/sdd)
+    const double gmn = H.gmin[q], gmx = H.gmax[q];
+    const double l1 = H.kappa * H.galpha[q] * ga * dz_sdd, l2 = H.kappa * H.gbeta[q] * dz_sdd;
+    auto Fq = [&](double aL, double zref) -> double {
+      const double u = zref * ga;
+      if (u <= gmn * aL) return 0.0;
+      if (u > gmx * aL) return l1 * zref - l2 * aL;
+      const double tan_a = aL * dz_sdd;
+      const double G = u * frcp(aL);
+      if (tab) return H.kappa * tan_a * group_table(*T, q, G);
+      return H.kappa * tan_a * group_raw(H, P, q, G);
+    };
     // cache of F(L, z) at the current voxel's bottom face (signed L key)
     int cL0 = INT_MIN, cL1 = INT_MIN, cL2 = INT_MIN, cL3 = INT_MIN;
     double cF0 = 0.0, cF1 = 0.0, cF2 = 0.0, cF3 = 0.0;
@@ -628,16 +639,14 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
           return w2d * zt / (zt - zb);
         }
         const double aL = fabs(kk);
-        const double tan_a = aL * dz_sdd;
-        const double gs = ga * frcp(aL);  // 1 / (a' tan_a)
         const double zt_s = L > 0 ? zt : -zt, zb_s = L > 0 ? zb : -zb;
         double Fb;
         if (L == cL0) Fb = cF0;
         else if (L == cL1) Fb = cF1;
         else if (L == cL2) Fb = cF2;
         else if (L == cL3) Fb = cF3;
-        else Fb = Fq(q, tan_a, gs, zb_s);
-        const double Ft = Fq(q, tan_a, gs, zt_s);
+        else Fb = Fq(aL, zb_s);
+        const double Ft = Fq(aL, zt_s);
         switch (nn) {
           case 0: nL0 = L; nF0 = Ft; break;
           case 1: nL1 = L; nF1 = Ft; break;

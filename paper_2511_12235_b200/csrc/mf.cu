@@ -624,10 +624,15 @@ __global__ void __launch_bounds__(128, CTSM_D8B_MINB) bwd2d_d8_kernel(
 #ifndef CTSM_FWD3_MINB
 #define CTSM_FWD3_MINB 3
 #endif
-constexpr int kZcF = CTSM_KZCF;  // z-block of 32 * kZcF voxels for the staged values
+#ifndef CTSM_KZCF_F
+#define CTSM_KZCF_F CTSM_KZCF
+#endif
+// z-block of 32 * zc voxels for the staged values (per dtype)
+template <typename T>
+__host__ __device__ constexpr int fwd3_zc() { return sizeof(T) == 4 ? CTSM_KZCF_F : CTSM_KZCF; }
 
 template <typename T, int G>
-constexpr size_t fwd3d_sym_dyn_smem() { return sizeof(T) * kWarps3 * G * kZcF * 32; }
+constexpr size_t fwd3d_sym_dyn_smem() { return sizeof(T) * kWarps3 * G * fwd3_zc<T>() * 32; }
 
 template <typename T, int G>
 __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd3d_sym_kernel(
@@ -640,6 +645,7 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd
   // [warp][t][chunk][lane][V]: the G image values of (t, lane) as NC 16-byte
   // vectors, each chunk conflict-free across the lanes (one LDS.128 each)
   constexpr int V = 16 / sizeof(T), NC = G / V;
+  constexpr int kZcF = fwd3_zc<T>();
   T* xsm = reinterpret_cast<T*>(dyn_smem) + (size_t)(threadIdx.x >> 5) * kZcF * G * 32;
   auto xidx = [&](int t, int e, int ln) { return ((t * NC + e / V) * 32 + ln) * V + e % V; };
   __shared__ long long sab[kWarps3][G];  // row base of every image angle of the base angle
@@ -689,6 +695,7 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd
       // fp32 volumes sum a row run in fp32 (1-3 terms; converted to fixed
       // point at the flush), fp64 volumes in fp64
       using PT = T;
+      const float scale_f = (float)scale;
       long long pr = -1;
       PT pv[G];
       int py = 0;
@@ -702,8 +709,11 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd
 #ifdef CTSM_EXP_NO_SCATTER
             if (pv[e] == (PT)1.2345) yacc[r] = 1;  // timing experiment: no atomics
 #else
-            atomicAdd(yacc + sab[warp][e] + r,
-                      (unsigned long long)__double2ll_rn((double)pv[e] * scale));
+            // fp32 runs convert in fp32 (2^-24 of the fixed-point range:
+            // far below the fp32 output rounding)
+            const long long iv = sizeof(T) == 4 ? __float2ll_rn((float)pv[e] * scale_f)
+                                                : __double2ll_rn((double)pv[e] * scale);
+            atomicAdd(yacc + sab[warp][e] + r, (unsigned long long)iv);
 #endif
           }
       };
@@ -776,7 +786,11 @@ struct BwdAcc<float> {
   using type = float;
 };
 #endif
-constexpr int kZcS = CTSM_KZCS;
+#ifndef CTSM_KZCS_F
+#define CTSM_KZCS_F CTSM_KZCS
+#endif
+template <typename T>
+__host__ __device__ constexpr int bwd3_zc() { return sizeof(T) == 4 ? CTSM_KZCS_F : CTSM_KZCS; }
 
 
 
@@ -795,6 +809,7 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
   // still deterministic): at most ~chunk * 12 terms per slot, an error far
   // below the fp32 tolerance, and half the shared memory -> more warps/SM
   using AccT = typename BwdAcc<T>::type;
+  constexpr int kZcS = bwd3_zc<T>();
   __shared__ AccT sacc[kWarpsS][G][kZcS][32];
   CTSM_TABLE_DECL(kWarpsS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
