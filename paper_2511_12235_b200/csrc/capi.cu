@@ -476,6 +476,20 @@ static int fwd_d8_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d, 
   const uint64_t n_meas = (uint64_t)d.rows_per_angle * g->n_angles;
   const int nb = (int)base.size();
   if (nb == 0) return 0;
+  const bool two_d = (g->n_z == 1 && g->n_det_z == 1);
+  const size_t nf = (!two_d && dtype == CTSM_F32) ? fwd3d_f32_scratch_elems(d, 8) : 0;
+  if (nf) {  // fp32 3D: vector float reductions, no fixed-point rows
+    CT_TRY(upload_base(ctx, d, base, st));
+    CT_TRY(ensure(ctx, ctx->bwd_t, nf * sizeof(float)));
+    CT_TRY(ensure(ctx, ctx->vol_t, (size_t)d.n_vox * sizeof(float)));
+    CT_CUDA(cudaMemsetAsync(ctx->n_upd, 0, sizeof(unsigned long long), st));
+    CT_CUDA(fwd3d_mf_d8_f32(d, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb,
+                            (const float*)x, (float*)y, ctx->n_upd, ctx->status, st, ctx->vol_t.p,
+                            (float*)ctx->bwd_t.p));
+    CT_CUDA(cudaMemcpyAsync(ctx->h_upd, ctx->n_upd, sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));
+    return 0;
+  }
   const std::vector<int> rows = orbit_angles(g, 8, base);
   CT_TRY(ensure(ctx, ctx->alist, rows.size() * sizeof(int)));
   CT_CUDA(cudaMemcpyAsync(ctx->alist.p, rows.data(), rows.size() * sizeof(int),
@@ -490,7 +504,6 @@ static int fwd_d8_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d, 
   double scale = B > 0.0 ? std::ldexp(1.0, 61) / B : 1.0;
   // the kernel's shared-memory limbs need every contribution |w x| scale
   // below 2^47 (f64) / 2^23 (f32); weights are area fractions <= 1
-  const bool two_d = (g->n_z == 1 && g->n_det_z == 1);
   if (two_d && mx > 0.0)
     scale = std::min(scale, std::ldexp(1.0, dtype == CTSM_F64 ? 47 : 23) / (mx * 1.001));
   CT_CUDA(cudaMemsetAsync(ctx->n_upd, 0, sizeof(unsigned long long), st));

@@ -92,6 +92,13 @@ cudaError_t rows_list(const DevGeom& g, int dtype, const int* angles, int n_list
 // [n_y][n_x][n_z] (a lane's z-chunk is contiguous): vol_t is an n_vox scratch
 // of the dtype; fwd transposes x into it, bwd accumulates into it and
 // transposes the result into x.
+// fp32 dihedral 3D forward with vector float reductions into an interleaved
+// scratch yt of fwd3d_f32_scratch_elems() floats (0: use fwd3d_mf_sym);
+// writes y (fp32) directly for every image angle of the base angles.
+size_t fwd3d_f32_scratch_elems(const DevGeom& g, int order);
+cudaError_t fwd3d_mf_d8_f32(const DevGeom& g, const AngleCS* cs, const int* base, int n_base,
+                            const float* x_in, float* y, unsigned long long* n_upd, int* status,
+                            cudaStream_t st, void* vol_t, float* yt);
 cudaError_t fwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                          int n_base, const void* x, unsigned long long* yacc, double scale,
                          unsigned long long* n_upd, int* status, cudaStream_t st, int order,

@@ -634,11 +634,18 @@ __host__ __device__ constexpr int fwd3_zc() { return sizeof(T) == 4 ? CTSM_KZCF_
 template <typename T, int G>
 constexpr size_t fwd3d_sym_dyn_smem() { return sizeof(T) * kWarps3 * G * fwd3_zc<T>() * 32; }
 
-template <typename T, int G>
+//
+// FA (fp32 volumes, G = 8): the row runs go with two 16-byte vector float
+// reductions (red.global.add.v4.f32) into the launch's image-interleaved rows
+// yt[k][my][mz][e] (the layout of the back-projection's transposed input)
+// instead of 8 scalar 64-bit fixed-point atomics; fwd3d_uninterleave then
+// writes the sinogram rows. The fp32 sums are order-dependent at the fp32
+// rounding level (the fp64 path stays fixed point and bit-reproducible).
+template <typename T, int G, bool FA = false>
 __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd3d_sym_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
     const T* __restrict__ in, unsigned long long* __restrict__ yacc, double scale,
-    unsigned long long* n_upd, int* status) {
+    unsigned long long* n_upd, int* status, float* __restrict__ yt = nullptr) {
   __shared__ fast::ColumnHead sh[kWarps3];
   __shared__ fast::PieceCoef sp[kWarps3][fast::kMaxPieces];
   extern __shared__ __align__(16) unsigned char dyn_smem[];
@@ -702,6 +709,18 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd
 #pragma unroll
       for (int e = 0; e < G; ++e) pv[e] = (PT)0;
       auto flush = [&]() {
+        if constexpr (FA) {
+          // interleaved row (my, mz) of slot kk: all G images in one vector
+          const long long pz = pr / ndy;
+          float* dst = yt + (((long long)kk * ndy + py) * g.n_det_z + pz) * G;
+#pragma unroll
+          for (int c = 0; c < G / 4; ++c)
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * c),
+                         "f"((float)pv[4 * c]), "f"((float)pv[4 * c + 1]), "f"((float)pv[4 * c + 2]),
+                         "f"((float)pv[4 * c + 3])
+                         : "memory");
+          return;
+        }
 #pragma unroll
         for (int e = 0; e < G; ++e)
           if (e < ne && pv[e] != (PT)0) {
@@ -1170,6 +1189,83 @@ static cudaError_t transpose2d(int dtype, const void* in, void* out, long long r
     transpose2d_kernel<float><<<grid, dim3(32, 8), 0, st>>>((const float*)in, (float*)out, rows,
                                                             cols);
   count_launch();
+  return cudaGetLastError();
+}
+
+// yt[k][myc][mz][e] (slot k of the launch) -> sinogram rows of the image
+// angles: y[angle(k, e)][mz][my], myc = my (e < 4) or ndy-1-my (reflections).
+// Block = 32 (my) x 32 (mz) tile of one slot, all G images: the interleaved
+// rows are read as contiguous G*32-float runs, the sinogram rows written
+// coalesced. Slots of the self-symmetric base angles (i = 0, 8i = n) have
+// only the 4 rotations.
+template <int G>
+__global__ void fwd3d_uninterleave(const float* __restrict__ yt, const int* __restrict__ base,
+                                   int n_angles, int ndy, int ndz, float* __restrict__ y) {
+  __shared__ float tile[G][32][33];
+  const int k = blockIdx.z;
+  const int my0 = blockIdx.x * 32, mz0 = blockIdx.y * 32;
+  const int i = base[k];
+  const bool full = G == 4 || ((i != 0) && (8 * i != n_angles));
+  const long long rpa = (long long)ndy * ndz;
+  const float* src = yt + (long long)k * G * rpa;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  // rows my0..my0+31: for image e the interleaved row is my (e < 4) or
+  // ndy-1-my (e >= 4); each row run is G*32 contiguous floats
+  for (int half = 0; half < (G == 8 ? 2 : 1); ++half)
+    for (int j = 0; j < 32; ++j) {
+      const int my = my0 + j;
+      if (my >= ndy) break;
+      const int myc = half == 0 ? my : ndy - 1 - my;
+      const float* row = src + ((long long)myc * ndz + mz0) * G;
+      for (int t = tid; t < 32 * G; t += 256) {
+        const int mz = t / G, e = t % G;
+        if ((e < 4) == (half == 0) && mz0 + mz < ndz) tile[e][j][mz] = row[t];
+      }
+    }
+  __syncthreads();
+  for (int e = 0; e < (full ? G : 4); ++e) {
+    const int a = d4_angle(n_angles, i, e);
+    float* dst = y + (long long)a * rpa;
+    for (int j = threadIdx.y; j < 32; j += 8) {
+      const int mz = mz0 + j, my = my0 + threadIdx.x;
+      if (mz < ndz && my < ndy) dst[(long long)mz * ndy + my] = tile[e][threadIdx.x][j];
+    }
+  }
+}
+
+size_t fwd3d_f32_scratch_elems(const DevGeom& g, int order) {
+  if (order != 8 || getenv("CTSM_FWD3_FIXED")) return 0;
+  return (size_t)sym3d_chunk(g, order, 4) * order * g.rows_per_angle;
+}
+
+// fp32 dihedral forward with vector float reductions (see fwd3d_sym_kernel,
+// FA): writes the image rows of every base angle into y (fp32).
+cudaError_t fwd3d_mf_d8_f32(const DevGeom& g, const AngleCS* cs, const int* base, int n_base,
+                            const float* x_in, float* y, unsigned long long* n_upd, int* status,
+                            cudaStream_t st, void* vol_t, float* yt) {
+  if (n_base <= 0) return cudaSuccess;
+  {
+    const cudaError_t e = transpose2d(CTSM_F32, x_in, vol_t, g.n_z, (long long)g.n_x * g.n_y, st);
+    if (e != cudaSuccess) return e;
+  }
+  const long long nxy = (long long)g.n_x * g.n_y;
+  const unsigned blocks = (unsigned)((nxy + kWarps3 - 1) / kWarps3);
+  const int chunk = sym3d_chunk(g, 8, 4);
+  constexpr size_t smem = fwd3d_sym_dyn_smem<float, 8>();
+  cudaFuncSetAttribute(fwd3d_sym_kernel<float, 8, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  for (int k0 = 0; k0 < n_base; k0 += chunk) {
+    const int nk = n_base - k0 < chunk ? n_base - k0 : chunk;
+    cudaError_t e = cudaMemsetAsync(yt, 0, (size_t)nk * 8 * g.rows_per_angle * sizeof(float), st);
+    if (e != cudaSuccess) return e;
+    fwd3d_sym_kernel<float, 8, true><<<blocks, kWarps3 * 32, smem, st>>>(
+        g, cs + k0, base + k0, nk, (const float*)vol_t, nullptr, 1.0, n_upd, status, yt);
+    count_launch();
+    const dim3 ug((g.n_det_y + 31) / 32, (g.n_det_z + 31) / 32, (unsigned)nk);
+    fwd3d_uninterleave<8><<<ug, dim3(32, 8), 0, st>>>(yt, base + k0, g.n_angles, g.n_det_y,
+                                                       g.n_det_z, y);
+    count_launch();
+  }
   return cudaGetLastError();
 }
 

@@ -298,3 +298,27 @@ def test_dihedral_path_matches_quarter_and_general(name, monkeypatch):
         xo += back_project_matrix_free(g, "consistent", 1, y, angles=("orbits", r, 3))
     assert rel_err(yo.cpu().numpy(), res["d8"][0]) <= 1e-12
     assert rel_err(xo.cpu().numpy(), res["d8"][1]) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["cone16", "c3_slab"])
+def test_f32_3d_vector_reduction_forward(name, monkeypatch):
+    """fp32 dihedral 3D forward (vector float reductions into interleaved
+    rows, then un-interleaved): matches the fixed-point fp32 path and the fp64
+    general kernels within the fp32 bar, and orbit shards tile the scan."""
+    if name == "cone16":
+        g = TEST_GEOMETRIES["cone3d"].with_(n_angles=16)
+    else:  # C3 detector / grid pitch on a thin slab of angles' orbits
+        g = CONFIGS["c3"].with_(n_x=64, n_y=64, n_z=32, n_det_z=96, n_angles=64)
+    gen = torch.Generator().manual_seed(5)
+    x = torch.rand(g.n_voxels, generator=gen, dtype=torch.float64).cuda()
+    yf = forward_project_matrix_free(g, "consistent", 1, x.float())
+    monkeypatch.setenv("CTSM_FWD3_FIXED", "1")
+    yx = forward_project_matrix_free(g, "consistent", 1, x.float())
+    monkeypatch.delenv("CTSM_FWD3_FIXED")
+    y64 = forward_project_matrix_free(g, "consistent", 1, x)
+    assert rel_err(yf.cpu().numpy(), yx.cpu().numpy()) <= 1e-5
+    assert rel_err(yf.cpu().numpy(), y64.cpu().numpy()) <= 1e-5
+    yo = torch.zeros_like(yf)
+    for r in range(3):
+        forward_project_matrix_free(g, "consistent", 1, x.float(), angles=("orbits", r, 3), out=yo)
+    assert rel_err(yo.cpu().numpy(), yf.cpu().numpy()) <= 1e-6
