@@ -285,6 +285,7 @@ __device__ __forceinline__ bool plan_column(const DevGeom& g, double C, double S
   if (lane < ng) {  // group aggregates (lane q handles group q)
     const int q = lane;
     double mn = 1e300, mx = -1e300, al = 0.0, be = 0.0;
+#pragma unroll 1
     for (int k = H.gbeg[q]; k < H.gend[q]; ++k) {
       const double* c = P[k].c;
       const double* l = c + kLin;
@@ -640,13 +641,24 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
         }
         const double aL = fabs(kk);
         const double zt_s = L > 0 ? zt : -zt, zb_s = L > 0 ? zb : -zb;
-        double Fb;
-        if (L == cL0) Fb = cF0;
-        else if (L == cL1) Fb = cF1;
-        else if (L == cL2) Fb = cF2;
-        else if (L == cL3) Fb = cF3;
-        else Fb = Fq(aL, zb_s);
-        const double Ft = Fq(aL, zt_s);
+        double Fb = 0.0, Ft = 0.0;
+        bool need_b = true;
+        if (L == cL0) { Fb = cF0; need_b = false; }
+        else if (L == cL1) { Fb = cF1; need_b = false; }
+        else if (L == cL2) { Fb = cF2; need_b = false; }
+        else if (L == cL3) { Fb = cF3; need_b = false; }
+        // one call site of Fq (the cubic path is large: code size / icache)
+#pragma unroll 1
+        for (;;) {
+          const double f = Fq(aL, need_b ? zb_s : zt_s);
+          if (need_b) {
+            Fb = f;
+            need_b = false;
+          } else {
+            Ft = f;
+            break;
+          }
+        }
         switch (nn) {
           case 0: nL0 = L; nF0 = Ft; break;
           case 1: nL1 = L; nF1 = Ft; break;
@@ -657,14 +669,16 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
         ++nn;
         return L > 0 ? Ft - Fb : w2d - (Fb - Ft);
       };
-      if (k_hi >= k_lo) {
-        double prev = above(k_lo);
-        for (int L = k_lo; L <= k_hi; ++L) {
-          const double next = above(L + 1);
-          const double v = prev - next;
-          if (v > kEpsWeight) emit(iz, cell, L, v);
-          prev = next;
+      // edges k_lo .. k_hi+1 with one call site each of above() and emit()
+      double prev = 0.0;
+#pragma unroll 1
+      for (int L = k_lo; L <= k_hi + 1; ++L) {
+        const double cur = above(L);
+        if (L > k_lo) {
+          const double v = prev - cur;
+          if (v > kEpsWeight) emit(iz, cell, L - 1, v);
         }
+        prev = cur;
       }
       cL0 = nL0; cL1 = nL1; cL2 = nL2; cL3 = nL3;
       cF0 = nF0; cF1 = nF1; cF2 = nF2; cF3 = nF3;

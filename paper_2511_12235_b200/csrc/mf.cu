@@ -678,6 +678,7 @@ __global__ void __launch_bounds__(kWarps3 * 32, G == 8 ? CTSM_FWD3_MINB : 4) fwd
       // z-fastest volume: the lane's z-chunk is contiguous (its sectors are
       // re-hit in L1 across t), instead of one sector per voxel
       const T* src = in + ((long long)ry * n + rx) * g.n_z;
+#pragma unroll 1
       for (int t = 0; t < zc; ++t) xsm[xidx(t, e, lane)] = (z0 + t < z1) ? src[z0 + t] : (T)0;
     }
     __syncwarp();
