@@ -372,8 +372,12 @@ struct GroupTable {
 };
 
 // Un-scaled atom sum of group q (the inner loop of atom_sum3).
-__device__ __forceinline__ double group_raw(const ColumnHead& H, const PieceCoef* P, int q,
-                                            double G) {
+#ifdef CTSM_GROUP_RAW_NOINLINE
+__device__ __noinline__ double group_raw(
+#else
+__device__ __forceinline__ double group_raw(
+#endif
+    const ColumnHead& H, const PieceCoef* P, int q, double G) {
   double v = 0.0;
   for (int k = H.gbeg[q]; k < H.gend[q]; ++k) {
     const double* c = P[k].c;
