@@ -209,12 +209,14 @@ __device__ __forceinline__ bool plan_column(const DevGeom& g, double C, double S
     H.ng = ng;
   }
   if (lane < np) {
+    // constant divisors as reciprocal multiplies (tolerance-checked path)
+    const double ica = 1.0 / ca;
     double* c = P[lane].c;
     if (my_kind == 1) {
       // trap_flags_at / trap_atom_flags (weights3d.cpp:63-107)
       const double t1 = my_lo, t2 = my_hi;
       const double cr1 = Cp + Sp * t1, cr2 = Cp + Sp * t2;
-      const double Pg = (s * Cp - fx1) / ca, Pf = (s * Cp - fx0) / ca;
+      const double Pg = (s * Cp - fx1) * ica, Pf = (s * Cp - fx0) * ica;
       const double i1 = 1.0 / cr1, i2 = 1.0 / cr2, i12 = i1 * i2;
       c[0] = Pg * i1;
       c[1] = Pg * i2;
@@ -242,17 +244,17 @@ __device__ __forceinline__ bool plan_column(const DevGeom& g, double C, double S
       seg(fx0, l0, d0);
       seg(0.5 * (fx0 + fx1), lm, dm);
       seg(fx1, l1, d1);
-      const double area = ca * (l0 + 4.0 * lm + l1) / 6.0;
-      const double mom = ca * (l0 * d0 + 4.0 * lm * dm + l1 * d1) / 6.0;
+      const double area = ca * (l0 + 4.0 * lm + l1) * (1.0 / 6.0);
+      const double mom = ca * (l0 * d0 + 4.0 * lm * dm + l1 * d1) * (1.0 / 6.0);
       double* l = c + kLin;
       l[0] = fmin(fmin(c[0], c[1]), fmin(c[2], c[3]));
       l[1] = fmax(fmax(c[0], c[1]), fmax(c[2], c[3]));
-      l[2] = 6.0 * area / (ca * ca);
-      l[3] = area > 0.0 ? mom / area / ca : 0.0;
+      l[2] = 6.0 * area * ica * ica;
+      l[3] = area > 0.0 ? mom / area * ica : 0.0;
     } else {
       // tri_flags_at / tri_atom_flags (weights3d.cpp:115-168) at both ends
       const double xa = my_kind == 0 ? ax1 : ax4, ya = my_kind == 0 ? ay1 : ay4;
-      const double Pq = (s * Cp - xa) / ca, Qq = (s * Sp - ya) / ca;
+      const double Pq = (s * Cp - xa) * ica, Qq = (s * Sp - ya) * ica;
       const double thgg = Pq * Cp + Qq * Sp;
       const double Da = s - xa * Cp - ya * Sp;       // apex depth (= a' thgg)
       const double ta = my_kind == 0 ? sw.T1 : sw.T4;  // apex ray parameter
@@ -272,12 +274,12 @@ __device__ __forceinline__ bool plan_column(const DevGeom& g, double C, double S
         const double k = Da * (t - ta);
         const double dx = k / (t * Cp - Sp), dy = k / crg;
         const double area = 0.5 * fabs(dx * dy);
-        const double dcen = Da - (dx * Cp + dy * Sp) / 3.0;
+        const double dcen = Da - (dx * Cp + dy * Sp) * (1.0 / 3.0);
         double* l = c + kLin + 4 * e;
         l[0] = fmin(fmin(q[0], q[1]), q[2]);
         l[1] = fmax(fmax(q[0], q[1]), q[2]);
-        l[2] = 6.0 * area / (ca * ca);
-        l[3] = dcen / ca;
+        l[2] = 6.0 * area * ica * ica;
+        l[3] = dcen * ica;
       }
     }
   }
