@@ -711,13 +711,12 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
       const float scale_f = (float)scale;
       long long pr = -1;
       PT pv[G];
-      int py = 0;
+      int py = 0, pz = 0;
 #pragma unroll
       for (int e = 0; e < G; ++e) pv[e] = (PT)0;
       auto flush = [&]() {
         if constexpr (FA) {
           // interleaved row (my, mz) of slot kk: all G images in one vector
-          const long long pz = pr / ndy;
           float* dst = yt + (((long long)kk * ndy + py) * g.n_det_z + pz) * G;
 #pragma unroll
           for (int c = 0; c < G / 4; ++c)
@@ -749,6 +748,7 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
           if (pr >= 0) flush();
           pr = r;
           py = my + hy;
+          pz = mz + hz;
 #pragma unroll
           for (int e = 0; e < G; ++e) pv[e] = (PT)0;
         }
