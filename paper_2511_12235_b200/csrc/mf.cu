@@ -901,9 +901,19 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
             // the G image values of (my, mz): one contiguous vector
             T v[G];
             load_vec<T, G>(yb[0] + ((long long)(my + hy) * g.n_det_z + (mz + hz)) * G, v);
+            // the G slots are distinct (pk is a permutation): all loads, then
+            // all adds, then all stores -- written as one read-modify-write
+            // per slot the compiler must assume aliasing and serialise them
+            AccT* base = &sacc[warp][0][t][lane];
+            constexpr int kSlot = kZcS * 32;
+            AccT cur[G];
+#pragma unroll
+            for (int e = 0; e < G; ++e) cur[e] = base[((pk >> (3 * e)) & 7) * kSlot];
 #pragma unroll
             for (int e = 0; e < G; ++e)
-              if (e < 4 || full) sacc[warp][(pk >> (3 * e)) & 7][t][lane] += wa * (AccT)v[e];
+              if (e < 4 || full) cur[e] += wa * (AccT)v[e];
+#pragma unroll
+            for (int e = 0; e < G; ++e) base[((pk >> (3 * e)) & 7) * kSlot] = cur[e];
           } else {
             const long long r = (long long)(mz + hz) * g.n_det_y + (my + hy);
 #pragma unroll
