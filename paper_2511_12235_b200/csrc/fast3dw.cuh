@@ -612,12 +612,21 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
     // (tan_a = |L| dz/sdd, tan_a G = zref ga dz/sdd)
     const double gmn = H.gmin[q], gmx = H.gmax[q];
     const double l1 = H.kappa * H.galpha[q] * ga * dz_sdd, l2 = H.kappa * H.gbeta[q] * dz_sdd;
-    auto Fq = [&](double aL, double zref) -> double {
+    auto cheap = [&](double aL, double zref, double& f) -> bool {
       const double u = zref * ga;
-      if (u <= gmn * aL) return 0.0;
-      if (u > gmx * aL) return l1 * zref - l2 * aL;
+      if (u <= gmn * aL) {
+        f = 0.0;
+        return true;
+      }
+      if (u > gmx * aL) {
+        f = l1 * zref - l2 * aL;
+        return true;
+      }
+      return false;
+    };
+    auto Fcubic = [&](double aL, double zref) -> double {
       const double tan_a = aL * dz_sdd;
-      const double G = u * frcp(aL);
+      const double G = zref * ga * frcp(aL);
       if (tab) return H.kappa * tan_a * group_table(*T, q, G);
       return H.kappa * tan_a * group_raw(H, P, q, G);
     };
@@ -647,32 +656,40 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
         }
         const double aL = fabs(kk);
         const double zt_s = L > 0 ? zt : -zt, zb_s = L > 0 ? zb : -zb;
+        // zero / linear faces first (the common case, no cache traffic);
+        // only a cubic bottom face consults the cache of the previous
+        // voxel's cubic top faces, and only a cubic top face is cached
         double Fb = 0.0, Ft = 0.0;
-        bool need_b = true;
-        if (L == cL0) { Fb = cF0; need_b = false; }
-        else if (L == cL1) { Fb = cF1; need_b = false; }
-        else if (L == cL2) { Fb = cF2; need_b = false; }
-        else if (L == cL3) { Fb = cF3; need_b = false; }
-        // one call site of Fq (the cubic path is large: code size / icache)
+        bool need_b = !cheap(aL, zb_s, Fb), need_t = !cheap(aL, zt_s, Ft);
+        if (need_b) {
+          if (L == cL0) { Fb = cF0; need_b = false; }
+          else if (L == cL1) { Fb = cF1; need_b = false; }
+          else if (L == cL2) { Fb = cF2; need_b = false; }
+          else if (L == cL3) { Fb = cF3; need_b = false; }
+        }
+        if (need_b || need_t) {
+          // one call site of the cubic path (large: code size / icache)
 #pragma unroll 1
-        for (;;) {
-          const double f = Fq(aL, need_b ? zb_s : zt_s);
-          if (need_b) {
-            Fb = f;
-            need_b = false;
-          } else {
-            Ft = f;
-            break;
+          for (;;) {
+            const double f = Fcubic(aL, need_b ? zb_s : zt_s);
+            if (need_b) {
+              Fb = f;
+              need_b = false;
+              if (!need_t) break;
+            } else {
+              Ft = f;
+              switch (nn) {
+                case 0: nL0 = L; nF0 = Ft; break;
+                case 1: nL1 = L; nF1 = Ft; break;
+                case 2: nL2 = L; nF2 = Ft; break;
+                case 3: nL3 = L; nF3 = Ft; break;
+                default: break;
+              }
+              ++nn;
+              break;
+            }
           }
         }
-        switch (nn) {
-          case 0: nL0 = L; nF0 = Ft; break;
-          case 1: nL1 = L; nF1 = Ft; break;
-          case 2: nL2 = L; nF2 = Ft; break;
-          case 3: nL3 = L; nF3 = Ft; break;
-          default: break;
-        }
-        ++nn;
         return L > 0 ? Ft - Fb : w2d - (Fb - Ft);
       };
       // edges k_lo .. k_hi+1 with one call site each of above() and emit()
