@@ -594,10 +594,27 @@ __device__ __noinline__ double atom_sum3_slow(const ColumnHead& H, const PieceCo
   return atom_sum3(H, P, q, tan_a, gs, zref);
 }
 
+// Warp-batched cubic faces (chunk_weights with a CubicBatch): the cubic path
+// (group_raw: mixed-flag atoms) is needed by a few lanes at a time, at
+// different voxels, so evaluated where it arises it runs nearly every step
+// with 1-3 active lanes. Per cell group the lanes first list their cubic
+// faces (pass 1: the same zero / linear classification, no weights), the
+// warp evaluates the whole list with every lane busy (pass 2, a warp prefix
+// sum over the per-lane counts), and the row loop (pass 3) takes the values
+// in the order pass 1 listed them. Faces beyond a lane's kRq slots are
+// evaluated in place. The classification is the same products and compares
+// in both passes, so the two passes agree face by face.
+constexpr int kRq = 8;
+struct CubicBatch {
+  double rq[kRq][32];  // [slot][lane]: G in pass 1, the raw atom sum after pass 2
+  int roff[32];
+};
+
 template <typename Emit>
 __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead& H,
                                               const PieceCoef* P, int z0, int z1, Emit&& emit,
-                                              const GroupTable* T = nullptr) {
+                                              const GroupTable* T = nullptr,
+                                              CubicBatch* B = nullptr, int lane = 0) {
   const bool tab = T != nullptr && T->ok;
   const int row_lo = -g.n_det_z / 2, row_hi = g.n_det_z / 2 - 1;
   const double dz_sdd = g.dz_sdd, sdd_dz = g.sdd_dz;
@@ -625,12 +642,75 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
       return false;
     };
     auto Fcubic = [&](double aL, double zref) -> double {
+#ifdef CTSM_EXP_NO_CUBIC
+      return l1 * zref - l2 * aL;  // timing experiment only (wrong weights)
+#endif
       const double tan_a = aL * dz_sdd;
       const double G = zref * ga * frcp(aL);
       if (tab) return H.kappa * tan_a * group_table(*T, q, G);
       return H.kappa * tan_a * group_raw(H, P, q, G);
     };
-    // cache of F(L, z) at the current voxel's bottom face (signed L key)
+    int nl = 0, used = 0;
+    if (B != nullptr) {
+      // pass 1: list the cubic faces (same walk and tests as pass 3)
+      int nreq = 0;
+#pragma unroll 1
+      for (int iz = z0; iz < z1; ++iz) {
+        const double zb = (iz - g.n_z / 2.0) * g.c, zt = zb + g.c;
+        const double mb1 = zb * c_mn, mb2 = zb * c_mx, mt1 = zt * c_mn, mt2 = zt * c_mx;
+        const double m_min = fmin(fmin(mb1, mb2), fmin(mt1, mt2));
+        const double m_max = fmax(fmax(mb1, mb2), fmax(mt1, mt2));
+        const int fl = (int)floor(m_min);
+        const int k_lo = (fl < row_lo) ? row_lo : fl;
+        const int chi = (int)ceil(m_max) - 1;
+        const int k_hi = (chi < row_hi) ? chi : row_hi;
+#pragma unroll 1
+        for (int L = k_lo; L <= k_hi + 1; ++L) {
+          const double kk = (double)L;
+          if (kk <= m_min || kk >= m_max || L == 0) continue;
+          const double aL = fabs(kk);
+          const double zt_s = L > 0 ? zt : -zt, zb_s = L > 0 ? zb : -zb;
+          double f;
+          if (!cheap(aL, zb_s, f)) {
+            if (nreq < kRq) B->rq[nreq][lane] = zb_s * ga * frcp(aL);
+            ++nreq;
+          }
+          if (!cheap(aL, zt_s, f)) {
+            if (nreq < kRq) B->rq[nreq][lane] = zt_s * ga * frcp(aL);
+            ++nreq;
+          }
+        }
+      }
+      // pass 2: the warp evaluates all listed faces
+      nl = nreq < kRq ? nreq : kRq;
+      int incl = nl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      if (total > 0) {
+        B->roff[lane] = incl - nl;
+        __syncwarp();
+#pragma unroll 1
+        for (int f = lane; f < total; f += 32) {
+          int o = 0;
+#pragma unroll
+          for (int st = 16; st >= 1; st >>= 1)
+            if (o + st < 32 && B->roff[o + st] <= f) o += st;
+          const int k = f - B->roff[o];
+#ifdef CTSM_EXP_NO_CUBIC
+          B->rq[k][o] = 0.0;
+#else
+          B->rq[k][o] = group_raw(H, P, q, B->rq[k][o]);
+#endif
+        }
+        __syncwarp();
+      }
+    }
+    // cache of F(L, z) at the current voxel's bottom face (signed L key);
+    // unused when batched (pass 1 lists both faces)
     int cL0 = INT_MIN, cL1 = INT_MIN, cL2 = INT_MIN, cL3 = INT_MIN;
     double cF0 = 0.0, cF1 = 0.0, cF2 = 0.0, cF3 = 0.0;
     for (int iz = z0; iz < z1; ++iz) {
@@ -661,7 +741,7 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
         // voxel's cubic top faces, and only a cubic top face is cached
         double Fb = 0.0, Ft = 0.0;
         bool need_b = !cheap(aL, zb_s, Fb), need_t = !cheap(aL, zt_s, Ft);
-        if (need_b) {
+        if (need_b && B == nullptr) {
           if (L == cL0) { Fb = cF0; need_b = false; }
           else if (L == cL1) { Fb = cF1; need_b = false; }
           else if (L == cL2) { Fb = cF2; need_b = false; }
@@ -671,7 +751,12 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
           // one call site of the cubic path (large: code size / icache)
 #pragma unroll 1
           for (;;) {
-            const double f = Fcubic(aL, need_b ? zb_s : zt_s);
+            double f;
+            const int k = used++;
+            if (B != nullptr && k < nl)
+              f = H.kappa * (aL * dz_sdd) * B->rq[k][lane];
+            else
+              f = Fcubic(aL, need_b ? zb_s : zt_s);
             if (need_b) {
               Fb = f;
               need_b = false;

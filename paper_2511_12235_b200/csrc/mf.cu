@@ -160,6 +160,15 @@ __device__ __forceinline__ const fast::GroupTable* table3d(const fast::ColumnHea
 #endif
 }
 
+// warp-batched cubic faces (fast3dw.cuh CubicBatch); CTSM_NO_BATCH: in place
+#ifndef CTSM_NO_BATCH
+#define CTSM_BATCH_DECL(n) __shared__ fast::CubicBatch sbat[n]
+#define CTSM_BATCH_PTR (&sbat[warp])
+#else
+#define CTSM_BATCH_DECL(n)
+#define CTSM_BATCH_PTR nullptr
+#endif
+
 constexpr int kWarps3 = 4;
 constexpr int kZcMax = 16;  // voxels per lane per z-block (z-block = 512 voxels)
 
@@ -661,6 +670,7 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
   T* xsm = reinterpret_cast<T*>(dyn_smem) + (size_t)(threadIdx.x >> 5) * kZcF * G * 32;
   auto xidx = [&](int t, int e, int ln) { return ((t * NC + e / V) * 32 + ln) * V + e % V; };
   __shared__ long long sab[kWarps3][G];  // row base of every image angle of the base angle
+  CTSM_BATCH_DECL(kWarps3);
   CTSM_TABLE_DECL(kWarps3);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = g.n_x;
@@ -768,7 +778,7 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
           for (int u = 0; u < V; ++u)
             if (c * V + u < ne) pv[c * V + u] += wp * v[u];
         }
-      }, TB);
+      }, TB, CTSM_BATCH_PTR, lane);
       if (pr >= 0) flush();
     }
   }
@@ -837,6 +847,12 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
   constexpr int kZcS = bwd3_zc<T>();
   __shared__ AccT sacc[kWarpsS][G][kZcS][32];
   CTSM_TABLE_DECL(kWarpsS);
+#ifdef CTSM_BWD3_BATCH  // measured neutral / slightly slower in the back-projection (C3 190 vs 194 ms)
+  CTSM_BATCH_DECL(kWarpsS);
+#define CTSM_BATCH_PTR_B CTSM_BATCH_PTR
+#else
+#define CTSM_BATCH_PTR_B nullptr
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = g.n_x, h = n / 2;
   const long long orb = (long long)blockIdx.x * kWarpsS + warp;
@@ -926,7 +942,8 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
           }
         };
         fast::chunk_weights(g, sh[warp], sp[warp], z0, z1,
-                            [&](int iz, int my, int mz, double w) { gather(iz - z0, my, mz, w); }, TB);
+                            [&](int iz, int my, int mz, double w) { gather(iz - z0, my, mz, w); }, TB,
+                            CTSM_BATCH_PTR_B, lane);
       }
     }
     for (int e = 0; e < (diag ? 4 : G); ++e) {
