@@ -1,3 +1,4 @@
+#include <climits>
 // csr.cu -- K1/K2 consistent system-matrix CSR emission (bit-exact) and the
 // K3/K4 CSR appliers. Compiled with -fmad=false (see exact.cuh).
 //
@@ -154,60 +155,99 @@ __global__ void __launch_bounds__(128) csr3d_kernel(DevGeom g, const ExactAngle*
   if (ng == 0) return;
   const uint64_t row_base = (uint64_t)k * g.rows_per_angle;
   const double sdd_dz = sdd / g.d_z;
-  for (int iz = 0; iz < g.n_z; ++iz) {
-    const double zb = face(iz, g.n_z, g.c), zt = face(iz + 1, g.n_z, g.c);
-    const double cz = zt - zb;
-    double m_min = 0.0, m_max = 0.0;
-    bool first = true;
-    for (int q = 0; q < 4; ++q) {
-      const double depth = dep[q];
-      const double vz[2] = {zb, zt};
-      for (int r = 0; r < 2; ++r) {
-        const double m = sdd_dz * vz[r] / depth;
-        m_min = first ? m : exact::dmin(m_min, m);
-        m_max = first ? m : exact::dmax(m_max, m);
-        first = false;
+  // Cell group outer, voxel inner (the emission order within a row does not
+  // matter: rows are sorted by column afterwards). Along z the top face of
+  // voxel iz is the bottom face of voxel iz+1: atom_sum(..., cz, tan_a, zt)
+  // of voxel iz and atom_sum(..., cz', tan_a, zb') of voxel iz+1 are the same
+  // operation on the same operands whenever cz' == cz bitwise (zb' is
+  // face(iz+1) in both), so the value is reused -- bit-identical to
+  // recomputing it. Up to 4 row edges are cached per voxel.
+  for (int q = 0; q < ng; ++q) {
+    const int pi = gbeg[q], pj = gend[q];
+    const double w2d = gw2d[q];
+    int cL[4] = {INT_MIN, INT_MIN, INT_MIN, INT_MIN};
+    double cF[4] = {0.0, 0.0, 0.0, 0.0};
+    double ccz = -1.0;  // cz of the cached faces
+    for (int iz = 0; iz < g.n_z; ++iz) {
+      const double zb = face(iz, g.n_z, g.c), zt = face(iz + 1, g.n_z, g.c);
+      const double cz = zt - zb;
+      double m_min = 0.0, m_max = 0.0;
+      bool first = true;
+      for (int qq = 0; qq < 4; ++qq) {
+        const double depth = dep[qq];
+        const double vz[2] = {zb, zt};
+        for (int r = 0; r < 2; ++r) {
+          const double m = sdd_dz * vz[r] / depth;
+          m_min = first ? m : exact::dmin(m_min, m);
+          m_max = first ? m : exact::dmax(m_max, m);
+          first = false;
+        }
       }
-    }
-    const uint32_t column = (uint32_t)(((uint64_t)iz * g.n_y + iy) * g.n_x + ix);
-    const int fl = (int)floor(m_min);
-    const int k_lo = (fl < row_lo) ? row_lo : fl;
-    const int ch = (int)ceil(m_max) - 1;
-    const int k_hi = (ch < row_hi) ? ch : row_hi;
-    if (k_hi < k_lo) continue;
-    for (int q = 0; q < ng; ++q) {
-      const int pi = gbeg[q], pj = gend[q];
-      const double w2d = gw2d[q];
-      // above(k) lambda (weights3d.cpp:426-440)
-      auto above = [&](double kk) -> double {
-        if (kk <= m_min) return w2d;
-        if (kk >= m_max) return 0.0;
-        if (kk == 0.0) {
-          if (zb >= 0.0) return w2d;
-          if (zt <= 0.0) return 0.0;
-          return w2d * zt / (zt - zb);
+      const uint32_t column = (uint32_t)(((uint64_t)iz * g.n_y + iy) * g.n_x + ix);
+      const int fl = (int)floor(m_min);
+      const int k_lo = (fl < row_lo) ? row_lo : fl;
+      const int ch = (int)ceil(m_max) - 1;
+      const int k_hi = (ch < row_hi) ? ch : row_hi;
+      const bool reuse = (cz == ccz);
+      int nL[4] = {INT_MIN, INT_MIN, INT_MIN, INT_MIN};
+      double nF[4] = {0.0, 0.0, 0.0, 0.0};
+      int nn = 0;
+      if (k_hi >= k_lo) {
+        // above(k) lambda (weights3d.cpp:426-440); F(L, z) is atom_sum at
+        // zref = z (L > 0) or -z (L < 0); the bottom-face value of edge L
+        // comes from the cache when voxel iz-1 computed it as its top face
+        auto above = [&](double kk) -> double {
+          if (kk <= m_min) return w2d;
+          if (kk >= m_max) return 0.0;
+          if (kk == 0.0) {
+            if (zb >= 0.0) return w2d;
+            if (zt <= 0.0) return 0.0;
+            return w2d * zt / (zt - zb);
+          }
+          const int L = (int)kk;
+          const double tan_a = kk > 0.0 ? kk * g.d_z / sdd : -kk * g.d_z / sdd;
+          const double zt_s = kk > 0.0 ? zt : -zt, zb_s = kk > 0.0 ? zb : -zb;
+          double Fb;
+          bool hit = false;
+          if (reuse) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (!hit && cL[c] == L) {
+                Fb = cF[c];
+                hit = true;
+              }
+          }
+          const double Ft = exact::atom_sum(sw, pi, pj, s, a, b, cz, tan_a, zt_s);
+          if (!hit) Fb = exact::atom_sum(sw, pi, pj, s, a, b, cz, tan_a, zb_s);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (c == nn) {
+              nL[c] = L;
+              nF[c] = Ft;
+            }
+          ++nn;
+          // weights3d.cpp:432-438: k > 0 -> F(zt) - F(zb); k < 0 -> w2d - (F(-zb) - F(-zt))
+          return kk > 0.0 ? Ft - Fb : w2d - (Fb - Ft);
+        };
+        double prev = above((double)k_lo);
+        for (int L = k_lo; L <= k_hi; ++L) {
+          const double next = above((double)(L + 1));
+          const double v = prev - next;
+          if (v > kEpsWeight) {
+            em(row_base + (uint64_t)(L + g.n_det_z / 2) * g.n_det_y + (gcell[q] + g.n_det_y / 2),
+               column, v);
+          } else if (v < kNegClamp3D) {
+            raise_status(status, CTSM_ERR_NON_FINITE);
+          }
+          prev = next;
         }
-        if (kk > 0.0) {
-          const double tan_a = kk * g.d_z / sdd;
-          return exact::atom_sum(sw, pi, pj, s, a, b, cz, tan_a, zt) -
-                 exact::atom_sum(sw, pi, pj, s, a, b, cz, tan_a, zb);
-        }
-        const double tan_a = -kk * g.d_z / sdd;
-        return w2d - (exact::atom_sum(sw, pi, pj, s, a, b, cz, tan_a, -zb) -
-                      exact::atom_sum(sw, pi, pj, s, a, b, cz, tan_a, -zt));
-      };
-      double prev = above((double)k_lo);
-      for (int L = k_lo; L <= k_hi; ++L) {
-        const double next = above((double)(L + 1));
-        const double v = prev - next;
-        if (v > kEpsWeight) {
-          em(row_base + (uint64_t)(L + g.n_det_z / 2) * g.n_det_y + (gcell[q] + g.n_det_y / 2),
-             column, v);
-        } else if (v < kNegClamp3D) {
-          raise_status(status, CTSM_ERR_NON_FINITE);
-        }
-        prev = next;
       }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        cL[c] = nL[c];
+        cF[c] = nF[c];
+      }
+      ccz = cz;
     }
   }
 }
