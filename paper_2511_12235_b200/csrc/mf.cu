@@ -43,6 +43,28 @@ __device__ __forceinline__ void count_updates(unsigned long long* n_upd, unsigne
 // G consecutive values (16-byte aligned) with 128-bit read-only loads.
 template <typename T, int G>
 __device__ __forceinline__ void load_vec(const T* p, T (&v)[G]) {
+#ifndef CTSM_NO_LDG256
+  // 32-byte aligned vectors: sm_100 256-bit loads (LDG.E.ENL2.256), one per
+  // 8 floats / 4 doubles
+  if constexpr (G % (32 / sizeof(T)) == 0) {
+#pragma unroll
+    for (int c = 0; c < G / (32 / (int)sizeof(T)); ++c) {
+      if constexpr (sizeof(T) == 4) {
+        float* o = reinterpret_cast<float*>(v) + 8 * c;
+        asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3]), "=f"(o[4]), "=f"(o[5]), "=f"(o[6]),
+              "=f"(o[7])
+            : "l"(reinterpret_cast<const float*>(p) + 8 * c));
+      } else {
+        double* o = reinterpret_cast<double*>(v) + 4 * c;
+        asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+            : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3])
+            : "l"(reinterpret_cast<const double*>(p) + 4 * c));
+      }
+    }
+    return;
+  }
+#endif
   constexpr int per = 16 / sizeof(T);
 #pragma unroll
   for (int c = 0; c < G / per; ++c) {
