@@ -77,6 +77,15 @@ __device__ __forceinline__ void load_vec(const T* p, T (&v)[G]) {
     }
   }
 }
+// z-mirror reuse in the 3D symmetric kernels (CTSM_NO_ZMIRROR: off)
+__device__ __forceinline__ bool zmirror_on() {
+#ifdef CTSM_NO_ZMIRROR
+  return false;
+#else
+  return true;
+#endif
+}
+
 constexpr int kTx = 16, kTy = 8;
 
 // Forward 2D: block = 16x8 pixel tile x a chunk of kFwdAngles angles; each
@@ -703,8 +712,15 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
   const int rpa = g.rows_per_angle, ndy = g.n_det_y;
   const int hy = g.n_det_y / 2, hz = g.n_det_z / 2;
   unsigned cnt = 0;
-  for (int zb0 = 0; zb0 < g.n_z; zb0 += 32 * kZcF) {
-    const int nzb = min(32 * kZcF, g.n_z - zb0);
+  // z mirror (even n_z): only the lower half of the column is evaluated;
+  // each weight of voxel iz at row m_z also applies to voxel n_z-1-iz at row
+  // -1-m_z, whose values are staged in the upper half of the slots
+  const bool zmir = zmirror_on() && (g.n_z % 2 == 0);
+  constexpr int kMF = kZcF / 2;
+  const int zspan = zmir ? g.n_z / 2 : g.n_z;
+  const int zbs = 32 * (zmir ? kMF : kZcF);
+  for (int zb0 = 0; zb0 < zspan; zb0 += zbs) {
+    const int nzb = min(zbs, zspan - zb0);
     const int zc = (nzb + 31) / 32;
     const int z0 = zb0 + lane * zc, z1 = min(z0 + zc, zb0 + nzb);
     __syncwarp();
@@ -716,7 +732,10 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
       // re-hit in L1 across t), instead of one sector per voxel
       const T* src = in + ((long long)ry * n + rx) * g.n_z;
 #pragma unroll 1
-      for (int t = 0; t < zc; ++t) xsm[xidx(t, e, lane)] = (z0 + t < z1) ? src[z0 + t] : (T)0;
+      for (int t = 0; t < zc; ++t) {
+        xsm[xidx(t, e, lane)] = (z0 + t < z1) ? src[z0 + t] : (T)0;
+        if (zmir) xsm[xidx(kMF + t, e, lane)] = (z0 + t < z1) ? src[g.n_z - 1 - (z0 + t)] : (T)0;
+      }
     }
     __syncwarp();
     for (int kk = 0; kk < n_base; ++kk) {
@@ -742,39 +761,44 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
       using PT = T;
       const float scale_f = (float)scale;
       long long pr = -1;
-      PT pv[G];
+      PT pv[G], pm[G];  // run sums of the lower voxel and of its z mirror
       int py = 0, pz = 0;
 #pragma unroll
-      for (int e = 0; e < G; ++e) pv[e] = (PT)0;
+      for (int e = 0; e < G; ++e) pv[e] = pm[e] = (PT)0;
       auto flush = [&]() {
-        if constexpr (FA) {
-          // interleaved row (my, mz) of slot kk: all G images in one vector
-          float* dst = yt + (((long long)kk * ndy + py) * g.n_det_z + pz) * G;
+#pragma unroll 1
+        for (int side = 0; side < (zmir ? 2 : 1); ++side) {
+          const PT* q = side == 0 ? pv : pm;
+          const int rz = side == 0 ? pz : g.n_det_z - 1 - pz;  // mirror row -1-mz
+          if constexpr (FA) {
+            // interleaved row (my, mz) of slot kk: all G images in one vector
+            float* dst = yt + (((long long)kk * ndy + py) * g.n_det_z + rz) * G;
 #pragma unroll
-          for (int c = 0; c < G / 4; ++c)
-            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * c),
-                         "f"((float)pv[4 * c]), "f"((float)pv[4 * c + 1]), "f"((float)pv[4 * c + 2]),
-                         "f"((float)pv[4 * c + 3])
-                         : "memory");
-        } else {
+            for (int c = 0; c < G / 4; ++c)
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * c),
+                           "f"((float)q[4 * c]), "f"((float)q[4 * c + 1]), "f"((float)q[4 * c + 2]),
+                           "f"((float)q[4 * c + 3])
+                           : "memory");
+          } else {
 #pragma unroll
-        for (int e = 0; e < G; ++e)
-          if (e < ne && pv[e] != (PT)0) {
-            const long long r = (e < 4) ? pr : pr + ndy - 1 - 2 * py;
+            for (int e = 0; e < G; ++e)
+              if (e < ne && q[e] != (PT)0) {
+                const long long r = (long long)rz * ndy + ((e < 4) ? py : ndy - 1 - py);
 #ifdef CTSM_EXP_NO_SCATTER
-            if (pv[e] == (PT)1.2345) yacc[r] = 1;  // timing experiment: no atomics
+                if (q[e] == (PT)1.2345) yacc[r] = 1;  // timing experiment: no atomics
 #else
-            // fp32 runs convert in fp32 (2^-24 of the fixed-point range:
-            // far below the fp32 output rounding)
-            const long long iv = sizeof(T) == 4 ? __float2ll_rn((float)pv[e] * scale_f)
-                                                : __double2ll_rn((double)pv[e] * scale);
-            atomicAdd(yacc + sab[warp][e] + r, (unsigned long long)iv);
+                // fp32 runs convert in fp32 (2^-24 of the fixed-point range:
+                // far below the fp32 output rounding)
+                const long long iv = sizeof(T) == 4 ? __float2ll_rn((float)q[e] * scale_f)
+                                                    : __double2ll_rn((double)q[e] * scale);
+                atomicAdd(yacc + sab[warp][e] + r, (unsigned long long)iv);
 #endif
+              }
           }
         }
       };
       fast::chunk_weights(g, sh[warp], sp[warp], z0, z1, [&](int iz, int my, int mz, double w) {
-        cnt += ne;
+        cnt += zmir ? 2 * ne : ne;
         const long long r = (long long)(mz + hz) * ndy + (my + hy);
         if (r != pr) {
           if (pr >= 0) flush();
@@ -782,23 +806,27 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
           py = my + hy;
           pz = mz + hz;
 #pragma unroll
-          for (int e = 0; e < G; ++e) pv[e] = (PT)0;
+          for (int e = 0; e < G; ++e) pv[e] = pm[e] = (PT)0;
         }
         const PT wp = (PT)w;
-        const T* xv = xsm + xidx(iz - z0, 0, lane);
+#pragma unroll 1
+        for (int side = 0; side < (zmir ? 2 : 1); ++side) {
+          const T* xv = xsm + xidx((side == 0 ? 0 : kMF) + iz - z0, 0, lane);
+          PT* acc = side == 0 ? pv : pm;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          T v[V];
-          if constexpr (sizeof(T) == 4) {
-            const float4 q = reinterpret_cast<const float4*>(xv)[c * 32];
-            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-          } else {
-            const double2 q = reinterpret_cast<const double2*>(xv)[c * 32];
-            v[0] = q.x; v[1] = q.y;
+          for (int c = 0; c < NC; ++c) {
+            T v[V];
+            if constexpr (sizeof(T) == 4) {
+              const float4 q = reinterpret_cast<const float4*>(xv)[c * 32];
+              v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+            } else {
+              const double2 q = reinterpret_cast<const double2*>(xv)[c * 32];
+              v[0] = q.x; v[1] = q.y;
+            }
+#pragma unroll
+            for (int u = 0; u < V; ++u)
+              if (c * V + u < ne) acc[c * V + u] += wp * v[u];
           }
-#pragma unroll
-          for (int u = 0; u < V; ++u)
-            if (c * V + u < ne) pv[c * V + u] += wp * v[u];
         }
       }, TB, CTSM_BATCH_PTR, lane);
       if (pr >= 0) flush();
@@ -894,12 +922,23 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
   const int n_mem = (G == 4 || diag) ? 4 : 8;
   const int rpa = g.rows_per_angle;
   const int hy = g.n_det_y / 2, hz = g.n_det_z / 2;
-  for (int zb0 = 0; zb0 < g.n_z; zb0 += 32 * kZcS) {
-    const int nzb = min(32 * kZcS, g.n_z - zb0);
+  // z mirror (even n_z, TR): voxel iz at row m_z has the weight of voxel
+  // n_z-1-iz at row -1-m_z (source and detector centred on z = 0), so only
+  // the lower half of the column is evaluated and every weight is gathered
+  // twice; the mirrored voxels use the upper half of the slots
+  const bool zmir = TR && zmirror_on() && (g.n_z % 2 == 0);
+  constexpr int kM = kZcS / 2;
+  const int zspan = zmir ? g.n_z / 2 : g.n_z;
+  const int zbs = 32 * (zmir ? kM : kZcS);
+  for (int zb0 = 0; zb0 < zspan; zb0 += zbs) {
+    const int nzb = min(zbs, zspan - zb0);
     const int zc = (nzb + 31) / 32;
     const int z0 = zb0 + lane * zc, z1 = min(z0 + zc, zb0 + nzb);
     for (int j = 0; j < G; ++j)
-      for (int t = 0; t < zc; ++t) sacc[warp][j][t][lane] = 0.0;
+      for (int t = 0; t < zc; ++t) {
+        sacc[warp][j][t][lane] = 0.0;
+        if (zmir) sacc[warp][j][kM + t][lane] = 0.0;
+      }
     for (int kk = 0; kk < n_base; ++kk) {
       const int i = base[kk];
       const AngleCS a = cs[kk];
@@ -936,22 +975,27 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
         auto gather = [&](int t, int my, int mz, double w) {
           const AccT wa = (AccT)w;  // fp32 volumes: FFMA in fp32
           if (TR) {
-            // the G image values of (my, mz): one contiguous vector
-            T v[G];
-            load_vec<T, G>(yb[0] + ((long long)(my + hy) * g.n_det_z + (mz + hz)) * G, v);
-            // the G slots are distinct (pk is a permutation): all loads, then
-            // all adds, then all stores -- written as one read-modify-write
-            // per slot the compiler must assume aliasing and serialise them
-            AccT* base = &sacc[warp][0][t][lane];
-            constexpr int kSlot = kZcS * 32;
-            AccT cur[G];
+            // the G image values of (my, mz): one contiguous vector; with
+            // the z mirror also those of row -1-mz for voxel n_z-1-iz
+            const T* rowp = yb[0] + (long long)(my + hy) * g.n_det_z * G;
+#pragma unroll 1
+            for (int side = 0; side < (zmir ? 2 : 1); ++side) {
+              T v[G];
+              load_vec<T, G>(rowp + (long long)(side == 0 ? mz + hz : g.n_det_z - 1 - (mz + hz)) * G, v);
+              // the G slots are distinct (pk is a permutation): all loads,
+              // then all adds, then all stores -- as one read-modify-write per
+              // slot the compiler must assume aliasing and serialise them
+              AccT* base = &sacc[warp][0][side == 0 ? t : kM + t][lane];
+              constexpr int kSlot = kZcS * 32;
+              AccT cur[G];
 #pragma unroll
-            for (int e = 0; e < G; ++e) cur[e] = base[((pk >> (3 * e)) & 7) * kSlot];
+              for (int e = 0; e < G; ++e) cur[e] = base[((pk >> (3 * e)) & 7) * kSlot];
 #pragma unroll
-            for (int e = 0; e < G; ++e)
-              if (e < 4 || full) cur[e] += wa * (AccT)v[e];
+              for (int e = 0; e < G; ++e)
+                if (e < 4 || full) cur[e] += wa * (AccT)v[e];
 #pragma unroll
-            for (int e = 0; e < G; ++e) base[((pk >> (3 * e)) & 7) * kSlot] = cur[e];
+              for (int e = 0; e < G; ++e) base[((pk >> (3 * e)) & 7) * kSlot] = cur[e];
+            }
           } else {
             const long long r = (long long)(mz + hz) * g.n_det_y + (my + hy);
 #pragma unroll
@@ -976,11 +1020,14 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
       for (int t = 0; t < zc; ++t) {
         const int iz = z0 + t;
         if (iz >= z1) break;
-        double v = (double)sacc[warp][e][t][lane];
-        if (diag) v += (double)sacc[warp][e2][t][lane];
-        T* dst = xout + c * g.n_z + iz;  // z-fastest volume
-        if (accumulate) v += (double)*dst;
-        *dst = (T)v;
+        for (int side = 0; side < (zmir ? 2 : 1); ++side) {
+          const int sl = side == 0 ? t : kM + t;
+          double v = (double)sacc[warp][e][sl][lane];
+          if (diag) v += (double)sacc[warp][e2][sl][lane];
+          T* dst = xout + c * g.n_z + (side == 0 ? iz : g.n_z - 1 - iz);  // z-fastest volume
+          if (accumulate) v += (double)*dst;
+          *dst = (T)v;
+        }
       }
     }
   }
