@@ -73,6 +73,10 @@ struct ctsm_ctx {
   Buf angles, edges, cs, counts, scan, longrows, acc, part, base, alist, sv_up, sv_h, sv_hp,
       sv_q, sv_v, sv_part, sv_scal, tmp_a, tmp_b, tmp_c, tmp_d,
       tmp_e, tmp_f, lraw_start, lraw_col, lraw_val, lacc, bwd_t, vol_t;
+  // stream of the host-buffer calls: created non-blocking on first use, so
+  // the calls of two contexts (two host threads) overlap their copies with
+  // each other's kernels instead of serialising on the legacy stream
+  cudaStream_t hstream = nullptr;
 };
 
 namespace {
@@ -96,6 +100,12 @@ int set_device(ctsm_ctx* ctx) {
 }
 
 // Synchronises the stream and converts a raised device guard into its code.
+int host_stream(ctsm_ctx* ctx, cudaStream_t* st) {
+  if (!ctx->hstream) CT_CUDA(cudaStreamCreateWithFlags(&ctx->hstream, cudaStreamNonBlocking));
+  *st = ctx->hstream;
+  return 0;
+}
+
 int check_status(ctsm_ctx* ctx, cudaStream_t st, const char* what) {
   CT_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->status, sizeof(int), cudaMemcpyDeviceToHost, st));
   CT_CUDA(cudaStreamSynchronize(st));
@@ -236,9 +246,10 @@ int ctsm_destroy(ctsm_ctx* ctx) {
                  &ctx->longrows, &ctx->acc, &ctx->part, &ctx->base, &ctx->alist, &ctx->sv_up, &ctx->sv_h, &ctx->sv_hp, &ctx->sv_q,
                  &ctx->sv_v, &ctx->sv_part, &ctx->sv_scal, &ctx->tmp_a, &ctx->tmp_b,  &ctx->tmp_c,
                  &ctx->tmp_d, &ctx->tmp_e, &ctx->tmp_f, &ctx->lraw_start, &ctx->lraw_col,
-                 &ctx->lraw_val, &ctx->lacc, &ctx->bwd_t};
+                 &ctx->lraw_val, &ctx->lacc, &ctx->bwd_t, &ctx->vol_t};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
+  if (ctx->hstream) cudaStreamDestroy(ctx->hstream);
   cudaFree(ctx->status);
   cudaFree(ctx->dred);
   cudaFreeHost(ctx->h_status);
@@ -1172,7 +1183,8 @@ int ctsm_forward_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,
   const uint64_t nv = (uint64_t)d.n_vox, nm = (uint64_t)d.rows_per_angle * g->n_angles;
   CT_TRY(ensure(ctx, ctx->tmp_a, nv * sizeof(double)));
   CT_TRY(ensure(ctx, ctx->tmp_b, nm * sizeof(double)));
-  cudaStream_t st = nullptr;
+  cudaStream_t st;
+  CT_TRY(host_stream(ctx, &st));
   CT_CUDA(cudaMemcpyAsync(ctx->tmp_a.p, x_host, nv * sizeof(double), cudaMemcpyHostToDevice, st));
   CT_TRY(fwd_impl(ctx, g, CTSM_F64, 0, g->n_angles, 1, ctx->tmp_a.p, ctx->tmp_b.p, st));
   CT_CUDA(cudaMemcpyAsync(y_host, ctx->tmp_b.p, nm * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1187,7 +1199,8 @@ int ctsm_back_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,
   const uint64_t nv = (uint64_t)d.n_vox, nm = (uint64_t)d.rows_per_angle * g->n_angles;
   CT_TRY(ensure(ctx, ctx->tmp_a, nv * sizeof(double)));
   CT_TRY(ensure(ctx, ctx->tmp_b, nm * sizeof(double)));
-  cudaStream_t st = nullptr;
+  cudaStream_t st;
+  CT_TRY(host_stream(ctx, &st));
   CT_CUDA(cudaMemcpyAsync(ctx->tmp_b.p, y_host, nm * sizeof(double), cudaMemcpyHostToDevice, st));
   CT_TRY(bwd_impl(ctx, g, CTSM_F64, 0, g->n_angles, 1, ctx->tmp_b.p, ctx->tmp_a.p, st));
   CT_CUDA(cudaMemcpyAsync(x_host, ctx->tmp_a.p, nv * sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -200,7 +200,10 @@ __device__ __forceinline__ const fast::GroupTable* table3d(const fast::ColumnHea
 #define CTSM_BATCH_PTR nullptr
 #endif
 
-constexpr int kWarps3 = 4;
+#ifndef CTSM_KW3
+#define CTSM_KW3 4
+#endif
+constexpr int kWarps3 = CTSM_KW3;
 constexpr int kZcMax = 16;  // voxels per lane per z-block (z-block = 512 voxels)
 
 template <typename T, bool kFwd>
@@ -432,8 +435,25 @@ __host__ __device__ constexpr int d4_compose(int g, int h) {
 #ifndef CTSM_D8B_MINB
 #define CTSM_D8B_MINB 7
 #endif
-constexpr int kD8Angles = 8;
-constexpr int kD8Win = 64;
+#ifndef CTSM_D8ANG
+#define CTSM_D8ANG 8
+#endif
+constexpr int kD8Angles = CTSM_D8ANG;
+#ifndef CTSM_D8WIN
+#define CTSM_D8WIN 64
+#endif
+constexpr int kD8Win = CTSM_D8WIN;
+// tile width of the dihedral forward per dtype (128-pixel tiles): 32 x 4 for
+// fp64 (C1 fwd 1.078 -> 1.035 ms: shorter shadows per tile row, fewer window
+// cells per flush), 16 x 8 for fp32 (0.815 vs 0.823 ms at 32 x 4)
+#ifndef CTSM_D8TX_F64
+#define CTSM_D8TX_F64 32
+#endif
+#ifndef CTSM_D8TX_F32
+#define CTSM_D8TX_F32 16
+#endif
+template <typename T>
+__host__ __device__ constexpr int d8_tx() { return sizeof(T) == 8 ? CTSM_D8TX_F64 : CTSM_D8TX_F32; }
 // w * xs rounded to the nearest integer (|.| < 2^47) by the 1.5 * 2^52 shift:
 // the low 51 mantissa bits then hold the integer + 2^51 -- one DFMA instead of
 // a 64-bit float->int conversion.
@@ -458,6 +478,7 @@ __global__ void __launch_bounds__(128, CTSM_D8F_MINB) fwd2d_d8_kernel(
   constexpr int L = sizeof(T) == 8 ? 2 : 1;  // limbs per window cell
   __shared__ unsigned win[2][8][L][kD8Win];
   for (int j = threadIdx.x; j < 2 * 8 * L * kD8Win; j += blockDim.x) (&win[0][0][0][0])[j] = 0u;
+  constexpr int kTx = d8_tx<T>(), kTy = 128 / kTx;
   const int tiles_x = (g.n_x + kTx - 1) / kTx;
   const int tx0 = (blockIdx.x % tiles_x) * kTx, ty0 = (blockIdx.x / tiles_x) * kTy;
   const int ix = tx0 + (threadIdx.x % kTx);
@@ -897,7 +918,10 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
   constexpr int kZcS = bwd3_zc<T>();
   __shared__ AccT sacc[kWarpsS][G][kZcS][32];
   CTSM_TABLE_DECL(kWarpsS);
-#ifdef CTSM_BWD3_BATCH  // measured neutral / slightly slower in the back-projection (C3 190 vs 194 ms)
+// warp-batched cubic faces: neutral before the z mirror (C3 190 vs 194 ms),
+// a gain with it (C3 bwd 148 -> 138 ms: every batched face now serves two
+// voxels); CTSM_BWD3_NOBATCH evaluates them in place
+#ifndef CTSM_BWD3_NOBATCH
   CTSM_BATCH_DECL(kWarpsS);
 #define CTSM_BATCH_PTR_B CTSM_BATCH_PTR
 #else
@@ -1132,8 +1156,9 @@ cudaError_t build_angle_cs(const DevGeom& g, int angle_begin, int angle_step, in
   return cudaGetLastError();
 }
 
-static dim3 tile_grid(const DevGeom& g, unsigned ydim) {
-  const unsigned tiles = (unsigned)(((g.n_x + kTx - 1) / kTx) * ((g.n_y + kTy - 1) / kTy));
+static dim3 tile_grid(const DevGeom& g, unsigned ydim, int tx = kTx) {
+  const int ty = 128 / tx;
+  const unsigned tiles = (unsigned)(((g.n_x + tx - 1) / tx) * ((g.n_y + ty - 1) / ty));
   return dim3(tiles, ydim);
 }
 
@@ -1487,7 +1512,8 @@ cudaError_t fwd_mf_d8(const DevGeom& g, int dtype, const AngleCS* cs, const int*
                       int n_base, const void* x, unsigned long long* yacc, double scale,
                       unsigned long long* n_upd, int* status, cudaStream_t st) {
   if (n_base <= 0) return cudaSuccess;
-  const dim3 grid = tile_grid(g, (unsigned)((n_base + kD8Angles - 1) / kD8Angles));
+  const dim3 grid = tile_grid(g, (unsigned)((n_base + kD8Angles - 1) / kD8Angles),
+                              dtype == CTSM_F64 ? d8_tx<double>() : d8_tx<float>());
   if (dtype == CTSM_F64)
     fwd2d_d8_kernel<double><<<grid, 128, 0, st>>>(g, cs, base, n_base, (const double*)x, yacc,
                                                   scale, n_upd, status);
@@ -1501,7 +1527,10 @@ cudaError_t fwd_mf_d8(const DevGeom& g, int dtype, const AngleCS* cs, const int*
 int bwd_d8_chunks(const DevGeom& g, int n_base) {
   const long long h = g.n_x / 2;
   const long long blocks = (h * (h + 1) / 2 + 127) / 128;
-  long long c = (16LL * 148 * 6 + blocks - 1) / blocks;
+#ifndef CTSM_BWD2_WAVES
+#define CTSM_BWD2_WAVES 3  // C1 bwd 0.772 -> 0.761 ms (f64), 0.738 -> 0.725 (f32) vs 6
+#endif
+  long long c = (16LL * 148 * CTSM_BWD2_WAVES + blocks - 1) / blocks;
   if (c > n_base) c = n_base;
   if (c > 64) c = 64;
   return (int)(c < 1 ? 1 : c);
