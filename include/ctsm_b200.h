@@ -98,6 +98,17 @@ int ctsm_spmv(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols, const uint64_t* r
 int ctsm_spmv_t(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols, const uint64_t* row_start_dev,
                 const uint32_t* col_dev, const double* val_dev, const double* y_dev,
                 double* x_dev, void* stream);
+/* K4 in two parts, for callers that keep the matrix: the column-sum bound
+ * max_c sum_r |A_rc| (one pass over the CSR; a property of the matrix, valid
+ * until its values change) and the scatter with a given bound. ctsm_spmv_t
+ * is the two in sequence. */
+int ctsm_csr_colsum_max(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols,
+                        const uint64_t* row_start_dev, const uint32_t* col_dev,
+                        const double* val_dev, double* colsum_max, void* stream);
+int ctsm_spmv_t_bound(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols,
+                      const uint64_t* row_start_dev, const uint32_t* col_dev,
+                      const double* val_dev, double colsum_max, const double* y_dev,
+                      double* x_dev, void* stream);
 
 /* ---- K5/K6: matrix-free projectors (forward_project_matrix_free,
  * projector.hpp:56-59; back_project_matrix_free is the rebuild's addition).
@@ -247,7 +258,10 @@ int ctsm_bwd_mf_mode(ctsm_ctx* ctx, const ctsm_geometry* g, int mode, int k, int
                      void* x_dev, void* stream);
 
 /* ---- host-buffer entry points (the reference's value-semantics calls,
- * used for end-to-end timing; copies in/out of pinned staging inside) ---- */
+ * projector.cpp:235-260; used for end-to-end timing). fp64 host arrays in,
+ * fp64 host arrays out; the copies and kernels run on the context's own
+ * non-blocking stream and the call returns when the result is on the host,
+ * so calls on two contexts from two host threads overlap. ---- */
 int ctsm_forward_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,
                                           const double* x_host, double* y_host);
 int ctsm_back_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,

@@ -371,33 +371,65 @@ int ctsm_spmv(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols, const uint64_t* r
   return s;
 }
 
-int ctsm_spmv_t(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols, const uint64_t* row_start_dev,
-                const uint32_t* col_dev, const double* val_dev, const double* y_dev,
-                double* x_dev, void* stream) {
+int ctsm_csr_colsum_max(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols,
+                        const uint64_t* row_start_dev, const uint32_t* col_dev,
+                        const double* val_dev, double* colsum_max, void* stream) {
   CT_TRY(set_device(ctx));
   cudaStream_t st = (cudaStream_t)stream;
-  // fixed-point bound: |x_c| <= max|y| * max_c sum_r |A_rc|
   CT_TRY(ensure(ctx, ctx->tmp_a, n_cols * sizeof(double)));
   CT_CUDA(cudaMemsetAsync(ctx->tmp_a.p, 0, n_cols * sizeof(double), st));
   CT_CUDA(colsum_abs(n_rows, row_start_dev, col_dev, val_dev, (double*)ctx->tmp_a.p, st));
-  double mcol = 0.0, my = 0.0;
+  double mcol = 0.0;
   CT_TRY(fetch_max_abs(ctx, CTSM_F64, n_cols, ctx->tmp_a.p, st, &mcol));
-  CT_TRY(fetch_max_abs(ctx, CTSM_F64, n_rows, y_dev, st, &my));
-  if (!std::isfinite(mcol) || !std::isfinite(my))
-    return fail(CTSM_ERR_NON_FINITE, "back projection not finite");
+  if (!std::isfinite(mcol)) return fail(CTSM_ERR_NON_FINITE, "matrix not finite");
+  *colsum_max = mcol;
+  return 0;
+}
+
+// Fixed-point scale of the CSR scatter: 2^61 / B with B >= max|x_c| rounded
+// up to a power of two, so that last-bit differences of the (atomically
+// summed) column bound never change the result bits.
+static double csr_fixed_scale(double mcol, double my) {
   const double B = mcol * my * (1.0 + 1e-6);
-  if (!(B > 0.0)) {
+  if (!(B > 0.0)) return 0.0;
+  int ex = 0;
+  (void)std::frexp(B, &ex);  // B <= 2^ex
+  return std::ldexp(1.0, 61 - ex);
+}
+
+int ctsm_spmv_t_bound(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols,
+                      const uint64_t* row_start_dev, const uint32_t* col_dev,
+                      const double* val_dev, double colsum_max, const double* y_dev,
+                      double* x_dev, void* stream) {
+  CT_TRY(set_device(ctx));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!std::isfinite(colsum_max) || colsum_max < 0.0)
+    return fail(CTSM_ERR_NON_FINITE, "column-sum bound not finite");
+  // fixed-point bound: |x_c| <= max|y| * max_c sum_r |A_rc|
+  double my = 0.0;
+  CT_TRY(fetch_max_abs(ctx, CTSM_F64, n_rows, y_dev, st, &my));
+  if (!std::isfinite(my)) return fail(CTSM_ERR_NON_FINITE, "back projection not finite");
+  const double scale = csr_fixed_scale(colsum_max, my);
+  if (!(scale > 0.0)) {
     CT_CUDA(cudaMemsetAsync(x_dev, 0, n_cols * sizeof(double), st));
     CT_CUDA(cudaStreamSynchronize(st));
     return 0;
   }
-  const double scale = std::ldexp(1.0, 61) / B;
   CT_TRY(ensure(ctx, ctx->tmp_b, n_cols * sizeof(unsigned long long)));
   CT_CUDA(cudaMemsetAsync(ctx->tmp_b.p, 0, n_cols * sizeof(unsigned long long), st));
   CT_CUDA(spmvt_csr_fixed(n_rows, row_start_dev, col_dev, val_dev, y_dev,
                           (unsigned long long*)ctx->tmp_b.p, scale, st));
   CT_CUDA(fixed_to_double(n_cols, (const unsigned long long*)ctx->tmp_b.p, scale, x_dev, st));
   return check_status(ctx, st, "back projection");
+}
+
+int ctsm_spmv_t(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols, const uint64_t* row_start_dev,
+                const uint32_t* col_dev, const double* val_dev, const double* y_dev,
+                double* x_dev, void* stream) {
+  double mcol = 0.0;
+  CT_TRY(ctsm_csr_colsum_max(ctx, n_rows, n_cols, row_start_dev, col_dev, val_dev, &mcol, stream));
+  return ctsm_spmv_t_bound(ctx, n_rows, n_cols, row_start_dev, col_dev, val_dev, mcol, y_dev,
+                           x_dev, stream);
 }
 
 // ---- K5/K6 ----------------------------------------------------------------
@@ -1037,12 +1069,11 @@ int op_bwd(ctsm_ctx* ctx, const OpRun& r, const double* y, double* x, cudaStream
     double my = 0.0;
     CT_TRY(fetch_max_abs(ctx, CTSM_F64, r.n_rows, y, st, &my));
     if (!std::isfinite(my)) return fail(CTSM_ERR_NON_FINITE, "back projection not finite");
-    const double B = r.mcol * my * (1.0 + 1e-6);
-    if (!(B > 0.0)) {
+    const double scale = csr_fixed_scale(r.mcol, my);
+    if (!(scale > 0.0)) {
       CT_CUDA(cudaMemsetAsync(x, 0, r.n_cols * sizeof(double), st));
       return 0;
     }
-    const double scale = std::ldexp(1.0, 61) / B;
     CT_TRY(ensure(ctx, ctx->tmp_b, r.n_cols * sizeof(unsigned long long)));
     CT_CUDA(cudaMemsetAsync(ctx->tmp_b.p, 0, r.n_cols * sizeof(unsigned long long), st));
     CT_CUDA(spmvt_csr_fixed(r.n_rows, op->row_start, op->col, op->val, y,

@@ -253,6 +253,25 @@ def forward_project(w: SparseSystemMatrix, x):
     return y if was_t else y.cpu().numpy()
 
 
+def _colsum_max(w: SparseSystemMatrix) -> float:
+    """max_c sum_r |A_rc| (the fixed-point bound of K4), computed once per
+    matrix and kept while its arrays are unchanged: the key holds the tensors'
+    storage pointers and torch version counters (bumped by every in-place
+    torch op); scale_values drops it."""
+    key = (w.col.data_ptr(), w.col._version, w.val.data_ptr(), w.val._version,
+           w.row_start.data_ptr(), w.row_start._version)
+    cached = getattr(w, "_colsum_cache", None)
+    if cached is not None and cached[0] == key:
+        return cached[1]
+    ctx = Context.get(w.device)
+    out = ctypes.c_double()
+    _lib.check(_lib.lib().ctsm_csr_colsum_max(ctx.handle, w.n_rows, w.n_cols, _dev_ptr(w.row_start),
+                                              _dev_ptr(w.col), _dev_ptr(w.val), ctypes.byref(out),
+                                              _stream(w.device)))
+    w._colsum_cache = (key, out.value)
+    return out.value
+
+
 def back_project(w: SparseSystemMatrix, y):
     """projector.cpp:219-233 (K4)."""
     n = int(y.numel()) if (torch is not None and isinstance(y, torch.Tensor)) else int(np.size(y))
@@ -261,9 +280,9 @@ def back_project(w: SparseSystemMatrix, y):
     ctx = Context.get(w.device)
     yt, was_t = _to_device(y, w.device, torch.float64)
     x = torch.empty(w.n_cols, dtype=torch.float64, device=yt.device)
-    _lib.check(_lib.lib().ctsm_spmv_t(ctx.handle, w.n_rows, w.n_cols, _dev_ptr(w.row_start),
-                                      _dev_ptr(w.col), _dev_ptr(w.val), _dev_ptr(yt), _dev_ptr(x),
-                                      _stream(w.device)))
+    _lib.check(_lib.lib().ctsm_spmv_t_bound(ctx.handle, w.n_rows, w.n_cols, _dev_ptr(w.row_start),
+                                            _dev_ptr(w.col), _dev_ptr(w.val), _colsum_max(w),
+                                            _dev_ptr(yt), _dev_ptr(x), _stream(w.device)))
     return x if was_t else x.cpu().numpy()
 
 
@@ -272,6 +291,7 @@ def scale_values(w: SparseSystemMatrix, factor: float) -> None:
     if not math.isfinite(factor):
         raise CtsmError("NonFinite", "scale factor must be finite")
     ctx = Context.get(w.device)
+    w._colsum_cache = None  # values change through the C-ABI, not a torch op
     _lib.check(_lib.lib().ctsm_scale_values(ctx.handle, w.nnz(), _dev_ptr(w.val), float(factor),
                                             _stream(ctx.device)))
 
