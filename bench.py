@@ -83,14 +83,16 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     x = phantom_for(cfg, g)
     y = uniform_sinogram(g.n_measurements, 12346)
-    # bounded sample: strided angles sized to ~10 s of CPU work per step
+    # bounded sample: strided angles sized so that the whole --warmup W
+    # --steps K run stays within ~2 minutes (<= 10 s of CPU work per step)
+    step_budget = min(10.0, 120.0 / max(1, args.warmup + args.steps))
     probe = np.array([0, g.n_angles // 2], np.int32)
     t0 = time.perf_counter()
     orc.forward_mf_angles(g, probe, x, cores)
     orc.back_mf_angles(g, probe, y, cores)
     tau = time.perf_counter() - t0  # ~ one angle's fwd+bwd (the 2 probes run in parallel)
     # the reference parallelises over angles: use >= one angle per core
-    n_sample = int(min(g.n_angles, cores * max(1, int(10.0 / max(tau, 1e-6)))))
+    n_sample = int(min(g.n_angles, cores * max(1, int(step_budget / max(tau, 1e-6)))))
     angles = np.linspace(0, g.n_angles, n_sample, endpoint=False).astype(np.int32)
     times = []
     for it in range(args.warmup + args.steps):
