@@ -349,7 +349,7 @@ def spectral_norm_power_matrix_free(g: ScanGeometry, iters: int = 100, seed: int
 # ---- matrix-free projectors (K5/K6) ---------------------------------------
 def forward_project_matrix_free(g: ScanGeometry, mode: str = MatrixMode.consistent, k: int = 1,
                                 x=None, threads: int = 1, *, angles=None, out=None,
-                                device: Optional[int] = None):
+                                device: Optional[int] = None, context: Optional["Context"] = None):
     """projector.cpp:235-260 (K5). ``angles`` = (begin, end, step) restricts the
     projection to an angle shard (rows of other angles are left untouched in
     ``out``, zero in a fresh output); ("orbits", b0, bstep) selects the base
@@ -361,9 +361,11 @@ def forward_project_matrix_free(g: ScanGeometry, mode: str = MatrixMode.consiste
     n = int(x.numel()) if (torch is not None and isinstance(x, torch.Tensor)) else int(np.size(x))
     if n != g.n_voxels:
         raise CtsmError("DimensionMismatch", "image size does not match the grid")
-    ctx = Context.get(device if device is not None else
-                      (x.device.index if (torch is not None and isinstance(x, torch.Tensor)
-                                          and x.is_cuda) else None))
+    # context: an explicit Context (own scratch and status word) lets two
+    # host threads or two streams run projections concurrently
+    ctx = context if context is not None else Context.get(
+        device if device is not None else
+        (x.device.index if (torch is not None and isinstance(x, torch.Tensor) and x.is_cuda) else None))
     xt, was_t = _to_device(x, ctx.device)
     sh = _angle_shard(g, angles)
     y = out if out is not None else torch.zeros(g.n_measurements, dtype=xt.dtype, device=xt.device)
@@ -384,7 +386,7 @@ def forward_project_matrix_free(g: ScanGeometry, mode: str = MatrixMode.consiste
 
 def back_project_matrix_free(g: ScanGeometry, mode: str = MatrixMode.consistent, k: int = 1,
                              y=None, threads: int = 1, *, angles=None, out=None,
-                             device: Optional[int] = None):
+                             device: Optional[int] = None, context: Optional["Context"] = None):
     """Matrix-free A^T y (K6; the reference only has CSR back_project,
     projector.cpp:219-233). With ``angles`` the result is the partial volume
     of that angle shard (summed across ranks by the multi-GPU driver)."""
@@ -393,9 +395,9 @@ def back_project_matrix_free(g: ScanGeometry, mode: str = MatrixMode.consistent,
     n = int(y.numel()) if (torch is not None and isinstance(y, torch.Tensor)) else int(np.size(y))
     if n != g.n_measurements:
         raise CtsmError("DimensionMismatch", "sinogram size does not match the scan")
-    ctx = Context.get(device if device is not None else
-                      (y.device.index if (torch is not None and isinstance(y, torch.Tensor)
-                                          and y.is_cuda) else None))
+    ctx = context if context is not None else Context.get(
+        device if device is not None else
+        (y.device.index if (torch is not None and isinstance(y, torch.Tensor) and y.is_cuda) else None))
     yt, was_t = _to_device(y, ctx.device)
     sh = _angle_shard(g, angles)
     x = out if out is not None else torch.empty(g.n_voxels, dtype=yt.dtype, device=yt.device)
