@@ -619,6 +619,10 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
   const int row_lo = -g.n_det_z / 2, row_hi = g.n_det_z / 2 - 1;
   const double dz_sdd = g.dz_sdd, sdd_dz = g.sdd_dz;
   const double c_mn = sdd_dz * H.dmin_inv, c_mx = sdd_dz * H.dmax_inv;
+  // row magnification range of a voxel [zb, zt]: the extremes of the four
+  // products z * c (c > 0, rounding monotone) picked by the signs of zb, zt,
+  // bit-identical to min / max over all four
+  const double c_lo = fmin(c_mn, c_mx), c_hi = fmax(c_mn, c_mx);
   const double ga = H.inv_a * sdd_dz;  // G = zref * ga / |L|
   for (int q = 0; q < H.ng; ++q) {
     const double w2d = H.gw2d[q];
@@ -657,9 +661,8 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
 #pragma unroll 1
       for (int iz = z0; iz < z1; ++iz) {
         const double zb = (iz - g.n_z / 2.0) * g.c, zt = zb + g.c;
-        const double mb1 = zb * c_mn, mb2 = zb * c_mx, mt1 = zt * c_mn, mt2 = zt * c_mx;
-        const double m_min = fmin(fmin(mb1, mb2), fmin(mt1, mt2));
-        const double m_max = fmax(fmax(mb1, mb2), fmax(mt1, mt2));
+        const double m_min = zb * (zb >= 0.0 ? c_lo : c_hi);
+        const double m_max = zt * (zt <= 0.0 ? c_lo : c_hi);
         const int fl = (int)floor(m_min);
         const int k_lo = (fl < row_lo) ? row_lo : fl;
         const int chi = (int)ceil(m_max) - 1;
@@ -715,9 +718,8 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
     double cF0 = 0.0, cF1 = 0.0, cF2 = 0.0, cF3 = 0.0;
     for (int iz = z0; iz < z1; ++iz) {
       const double zb = (iz - g.n_z / 2.0) * g.c, zt = zb + g.c;
-      const double mb1 = zb * c_mn, mb2 = zb * c_mx, mt1 = zt * c_mn, mt2 = zt * c_mx;
-      const double m_min = fmin(fmin(mb1, mb2), fmin(mt1, mt2));
-      const double m_max = fmax(fmax(mb1, mb2), fmax(mt1, mt2));
+      const double m_min = zb * (zb >= 0.0 ? c_lo : c_hi);
+      const double m_max = zt * (zt <= 0.0 ? c_lo : c_hi);
       const int fl = (int)floor(m_min);
       const int k_lo = (fl < row_lo) ? row_lo : fl;
       const int chi = (int)ceil(m_max) - 1;
