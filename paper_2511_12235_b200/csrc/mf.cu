@@ -516,25 +516,34 @@ __global__ void __launch_bounds__(128, CTSM_D8F_MINB) fwd2d_d8_kernel(
   __syncthreads();
   const int k0 = blockIdx.y * kD8Angles;
   const int k1 = min(k0 + kD8Angles, n_base);
-  for (int kk = k0; kk < k1; ++kk) {
-    const int buf = (kk - k0) & 1;
-    const AngleCS a = cs[kk];
-    const int i = base[kk];
-    const bool full = (i != 0) && (8 * i != g.n_angles);
-    // shadow of the tile: t over the 4 corners (depths checked by the sweeps)
-    double tmin, tmax;
-    {
+  // shadow of the tile (t over the 4 corners; depths checked by the sweeps)
+  // per angle of the chunk: uniform across the block, so lane j of every
+  // warp computes angle k0 + j once and the loop reads it by shuffle
+  static_assert(kD8Angles <= 32, "one lane per angle of the chunk");
+  int sh_clo = 0, sh_w = 0;
+  {
+    const int kk = k0 + (int)(threadIdx.x & 31);
+    if ((threadIdx.x & 31) < kD8Angles && kk < k1) {
+      const AngleCS a = cs[kk];
       const double s = g.s;
       const double t0 = (Y0 * a.C - X0 * a.S) * fast::frcp(s - X0 * a.C - Y0 * a.S);
       const double t1 = (Y0 * a.C - X1 * a.S) * fast::frcp(s - X1 * a.C - Y0 * a.S);
       const double t2 = (Y1 * a.C - X1 * a.S) * fast::frcp(s - X1 * a.C - Y1 * a.S);
       const double t3 = (Y1 * a.C - X0 * a.S) * fast::frcp(s - X0 * a.C - Y1 * a.S);
-      tmin = fmin(fmin(t0, t1), fmin(t2, t3));
-      tmax = fmax(fmax(t0, t1), fmax(t2, t3));
+      const double tmin = fmin(fmin(t0, t1), fmin(t2, t3));
+      const double tmax = fmax(fmax(t0, t1), fmax(t2, t3));
+      sh_clo = max((int)floor(tmin * g.u_scale) - 1, cell_lo);
+      const int chi = min((int)ceil(tmax * g.u_scale) + 1, cell_hi);
+      sh_w = chi - sh_clo + 1;
     }
-    const int clo = max((int)floor(tmin * g.u_scale) - 1, cell_lo);
-    const int chi = min((int)ceil(tmax * g.u_scale) + 1, cell_hi);
-    const int W = chi - clo + 1;
+  }
+  for (int kk = k0; kk < k1; ++kk) {
+    const int buf = (kk - k0) & 1;
+    const AngleCS a = cs[kk];
+    const int i = base[kk];
+    const bool full = (i != 0) && (8 * i != g.n_angles);
+    const int clo = __shfl_sync(0xffffffffu, sh_clo, kk - k0);
+    const int W = __shfl_sync(0xffffffffu, sh_w, kk - k0);
     const bool use_win = W <= kD8Win;
     if (inside) {
       unsigned* wb = &win[buf][0][0][0] - clo;
