@@ -667,8 +667,10 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
         const int k_lo = (fl < row_lo) ? row_lo : fl;
         const int chi = (int)ceil(m_max) - 1;
         const int k_hi = (chi < row_hi) ? chi : row_hi;
+        // unclamped ends are always skipped below (floor(m_min) <= m_min,
+        // ceil(m_max) >= m_max): leave them out of the walk
 #pragma unroll 1
-        for (int L = k_lo; L <= k_hi + 1; ++L) {
+        for (int L = k_lo + (fl >= row_lo), Le = k_hi + (chi >= row_hi); L <= Le; ++L) {
           const double kk = (double)L;
           if (kk <= m_min || kk >= m_max || L == 0) continue;
           const double aL = fabs(kk);
@@ -780,9 +782,12 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
         return L > 0 ? Ft - Fb : w2d - (Fb - Ft);
       };
       // edges k_lo .. k_hi+1 with one call site each of above() and emit()
-      double prev = 0.0;
+      // unclamped lower end: above(k_lo) = w2d (floor(m_min) <= m_min, an
+      // early return before any cache traffic), so the walk starts after it
+      const bool lo_free = fl >= row_lo;
+      double prev = lo_free ? w2d : 0.0;
 #pragma unroll 1
-      for (int L = k_lo; L <= k_hi + 1; ++L) {
+      for (int L = k_lo + (lo_free ? 1 : 0); L <= k_hi + 1; ++L) {
         const double cur = above(L);
         if (L > k_lo) {
           const double v = prev - cur;
