@@ -430,13 +430,13 @@ __host__ __device__ constexpr int d4_compose(int g, int h) {
 // limb (f32). With <= 128 adds per cell (one per tile pixel) no limb
 // overflows; the flush recombines them exactly into the 64-bit accumulator.
 #ifndef CTSM_D8F_MINB
-#define CTSM_D8F_MINB 7
+#define CTSM_D8F_MINB 8  // with 16-angle chunks: C1 fwd 1.003 -> 0.975 ms (f64), 0.747 -> 0.727 (f32)
 #endif
 #ifndef CTSM_D8B_MINB
 #define CTSM_D8B_MINB 7
 #endif
 #ifndef CTSM_D8ANG
-#define CTSM_D8ANG 8
+#define CTSM_D8ANG 16  // base angles per block (<= 32: one lane per angle computes the shadow)
 #endif
 constexpr int kD8Angles = CTSM_D8ANG;
 #ifndef CTSM_D8WIN
