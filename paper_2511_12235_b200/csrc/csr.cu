@@ -217,8 +217,19 @@ __global__ void __launch_bounds__(128) csr3d_kernel(DevGeom g, const ExactAngle*
                 hit = true;
               }
           }
+#ifdef CTSM_CSR3_TWO_SITES
           const double Ft = exact::atom_sum(sw, pi, pj, s, a, b, cz, tan_a, zt_s);
           if (!hit) Fb = exact::atom_sum(sw, pi, pj, s, a, b, cz, tan_a, zb_s);
+#else
+          // one call site of the (large) atom sum: instruction-cache bound
+          // kernel; the same calls on the same operands as two sites
+          double Ft = 0.0;
+#pragma unroll 1
+          for (int f = hit ? 1 : 0; f < 2; ++f) {
+            const double r = exact::atom_sum(sw, pi, pj, s, a, b, cz, tan_a, f == 0 ? zb_s : zt_s);
+            if (f == 0) Fb = r; else Ft = r;
+          }
+#endif
 #pragma unroll
           for (int c = 0; c < 4; ++c)
             if (c == nn) {
@@ -229,9 +240,22 @@ __global__ void __launch_bounds__(128) csr3d_kernel(DevGeom g, const ExactAngle*
           // weights3d.cpp:432-438: k > 0 -> F(zt) - F(zb); k < 0 -> w2d - (F(-zb) - F(-zt))
           return kk > 0.0 ? Ft - Fb : w2d - (Fb - Ft);
         };
+#ifdef CTSM_CSR3_TWO_SITES
         double prev = above((double)k_lo);
         for (int L = k_lo; L <= k_hi; ++L) {
           const double next = above((double)(L + 1));
+#else
+        // one call site of above(): edges k_lo .. k_hi+1 in order (the same
+        // calls as above(k_lo) followed by above(L+1) per row)
+        double prev = 0.0;
+#pragma unroll 1
+        for (int L = k_lo - 1; L <= k_hi; ++L) {
+          const double next = above((double)(L + 1));
+          if (L < k_lo) {
+            prev = next;
+            continue;
+          }
+#endif
           const double v = prev - next;
           if (v > kEpsWeight) {
             em(row_base + (uint64_t)(L + g.n_det_z / 2) * g.n_det_y + (gcell[q] + g.n_det_y / 2),
