@@ -149,6 +149,18 @@ int ctsm_bwd_mf_orbits(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int bas
  * A) counted live by the last successful ctsm_fwd_mf call on ctx. */
 uint64_t ctsm_last_update_count(ctsm_ctx* ctx);
 
+/* Kernel family of the last matrix-free call on ctx (CTSM_PATH_* bits):
+ * GENERAL = per-angle kernels; QUARTER / DIHEDRAL = the symmetric production
+ * kernels (4 / 8 (pixel, angle) pairs per weight evaluation); ZMIRROR = the
+ * 3D z-mirror reuse (even n_z); F32_VECRED = the fp32 3D forward with
+ * red.global.add.v4.f32 row runs. Lets tests assert which kernel ran. */
+#define CTSM_PATH_GENERAL 1
+#define CTSM_PATH_QUARTER 4
+#define CTSM_PATH_DIHEDRAL 8
+#define CTSM_PATH_ZMIRROR 16
+#define CTSM_PATH_F32_VECRED 32
+int ctsm_last_kernel_path(ctsm_ctx* ctx);
+
 /* ---- K7/K8: SIRT pieces (BASELINE.json configs[4]) ----------------------
  * x <- x + C .* A^T (R .* (y - A x)), R = 1/(A 1), C = 1/(A^T 1), zero sums -> 0.
  * ctsm_sirt_residual: r = R .* (y - ax) over the shard's rows, with R
@@ -266,6 +278,12 @@ int ctsm_forward_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,
                                           const double* x_host, double* y_host);
 int ctsm_back_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,
                                        const double* y_host, double* x_host);
+/* fp32 overloads: fp32 host arrays (BASELINE configs 3/4);
+ * the weights are still evaluated in FP64. */
+int ctsm_forward_project_matrix_free_host_f32(ctsm_ctx* ctx, const ctsm_geometry* g,
+                                              const float* x_host, float* y_host);
+int ctsm_back_project_matrix_free_host_f32(ctsm_ctx* ctx, const ctsm_geometry* g,
+                                           const float* y_host, float* x_host);
 
 /* ---- diagnostics ---------------------------------------------------------
  * Measured FP64 FMA throughput of `device` in TFLOP/s (FMA = 2 flops): the

@@ -1206,6 +1206,7 @@ typedef struct {
   int n_parts;
   uint64_t rpa;
   int mode, k;
+  int zlo, zhi; /* slab range evaluated (whole grid by default) */
 } fwd_user;
 typedef struct {
   double* block;
@@ -1219,8 +1220,9 @@ static void fwd_task(task* t, int item, int worker) {
   (void)worker;
   fwd_user* u = (fwd_user*)t->user;
   const int k = item / u->n_parts, part = item % u->n_parts;
-  const int n = slab_extent(t->g);
-  const int lo = (int)((int64_t)n * part / u->n_parts), hi = (int)((int64_t)n * (part + 1) / u->n_parts);
+  const int n = u->zhi - u->zlo;
+  const int lo = u->zlo + (int)((int64_t)n * part / u->n_parts),
+            hi = u->zlo + (int)((int64_t)n * (part + 1) / u->n_parts);
   double* block = u->parts + (uint64_t)item * u->rpa;
   memset(block, 0, u->rpa * sizeof(double));
   fwd_ctx c = {block, u->x};
@@ -1232,15 +1234,18 @@ static void fwd_task(task* t, int item, int worker) {
 
 static int forward_mf_angles_impl(const o_geom* g, const int32_t* angles, int n_sel,
                                   const double* x, double* y_sel, int threads, int split,
-                                  int mode, int k) {
+                                  int mode, int k, int zlo, int zhi) {
   O_TRY(validate(g););
   const uint64_t rpa = (uint64_t)g->n_det_y * g->n_det_z;
+  const int z0 = zlo < 0 ? 0 : zlo;
+  const int z1r = (zhi < 0 || zhi > slab_extent(g)) ? slab_extent(g) : zhi;
+  const int z1 = z1r < z0 ? z0 : z1r;
   int n_parts = 1;
   if (split && mode == 0 && n_sel > 0 && n_sel < threads) n_parts = (threads + n_sel - 1) / n_sel;
-  if (n_parts > slab_extent(g)) n_parts = slab_extent(g);
+  if (n_parts > z1 - z0) n_parts = z1 - z0 > 0 ? z1 - z0 : 1;
   double* parts = y_sel;
   if (n_parts > 1) parts = (double*)malloc((uint64_t)n_sel * n_parts * rpa * sizeof(double));
-  fwd_user u = {angles, x, parts, n_parts, rpa, mode, k};
+  fwd_user u = {angles, x, parts, n_parts, rpa, mode, k, z0, z1};
   task t;
   memset(&t, 0, sizeof t);
   t.fn = fwd_task;
@@ -1268,13 +1273,20 @@ static int forward_mf_angles_impl(const o_geom* g, const int32_t* angles, int n_
  * accumulation). */
 int ref_forward_mf_angles(const o_geom* g, const int32_t* angles, int n_sel, const double* x,
                           double* y_sel, int threads) {
-  return forward_mf_angles_impl(g, angles, n_sel, x, y_sel, threads, 0, 0, 1);
+  return forward_mf_angles_impl(g, angles, n_sel, x, y_sel, threads, 0, 0, 1, 0, -1);
 }
 /* Same values up to summation order; angles split into slabs so that a few
  * large angle blocks use all threads (tolerance checks at C3/C4 scale). */
 int ref_forward_mf_angles_par(const o_geom* g, const int32_t* angles, int n_sel, const double* x,
                               double* y_sel, int threads) {
-  return forward_mf_angles_impl(g, angles, n_sel, x, y_sel, threads, 1, 0, 1);
+  return forward_mf_angles_impl(g, angles, n_sel, x, y_sel, threads, 1, 0, 1, 0, -1);
+}
+/* A x rows of the listed angles from the voxels of z slabs [zlo, zhi) only
+ * (x restricted to those slabs; 2D: pixel rows): BASELINE-scale parity checks
+ * of the outer / central slabs without evaluating the whole grid. */
+int ref_forward_mf_angles_slabs(const o_geom* g, const int32_t* angles, int n_sel, int zlo,
+                                int zhi, const double* x, double* y_sel, int threads) {
+  return forward_mf_angles_impl(g, angles, n_sel, x, y_sel, threads, 1, 0, 1, zlo, zhi);
 }
 
 int ref_forward_project_matrix_free(const o_geom* g, const double* x, double* y, int threads) {
@@ -1295,6 +1307,8 @@ typedef struct {
   int base, n_parts;
   uint64_t rpa, nv;
   int mode, k;
+  int zlo, zhi;
+  int compact; /* y holds only the rows of the listed angles, in list order */
 } bwd_user;
 typedef struct {
   double* xpart;
@@ -1308,14 +1322,15 @@ static void bwd_task(task* t, int item, int worker) {
   (void)worker;
   bwd_user* u = (bwd_user*)t->user;
   const int k = item / u->n_parts, part = item % u->n_parts;
-  const int n = slab_extent(t->g);
-  const int lo = (int)((int64_t)n * part / u->n_parts), hi = (int)((int64_t)n * (part + 1) / u->n_parts);
+  const int n = u->zhi - u->zlo;
+  const int lo = u->zlo + (int)((int64_t)n * part / u->n_parts),
+            hi = u->zlo + (int)((int64_t)n * (part + 1) / u->n_parts);
   const uint64_t plane = t->g->n_z > 1 || t->g->n_det_z > 1 ? (uint64_t)t->g->n_x * t->g->n_y
                                                               : (uint64_t)t->g->n_x;
   double* p = u->part[k];
   memset(p + (uint64_t)lo * plane, 0, (uint64_t)(hi - lo) * plane * sizeof(double));
   const int ang = u->angles[u->base + k];
-  bwd_ctx c = {p, u->y + (uint64_t)ang * u->rpa};
+  bwd_ctx c = {p, u->y + (uint64_t)(u->compact ? u->base + k : ang) * u->rpa};
   if (u->mode != 0)
     angle_block_entries_rays(t->g, u->mode, u->k, ang, bwd_emit, &c);
   else
@@ -1324,12 +1339,16 @@ static void bwd_task(task* t, int item, int worker) {
 
 static int back_mf_angles_impl(const o_geom* g, const int32_t* angles, int n_sel,
                                const double* y, double* x, int threads, int split, int mode,
-                               int k) {
+                               int k, int zlo, int zhi, int compact) {
   O_TRY(validate(g););
   const uint64_t nv = (uint64_t)g->n_x * g->n_y * g->n_z;
+  const int z0 = zlo < 0 ? 0 : zlo;
+  const int z1r = (zhi < 0 || zhi > slab_extent(g)) ? slab_extent(g) : zhi;
+  const int z1 = z1r < z0 ? z0 : z1r;
   int n_parts = 1;
   if (split && mode == 0 && n_sel > 0 && n_sel < threads) n_parts = (threads + n_sel - 1) / n_sel;
-  if (n_parts > slab_extent(g)) n_parts = slab_extent(g);
+  if (n_parts > z1 - z0) n_parts = z1 - z0 > 0 ? z1 - z0 : 1;
+  const uint64_t plane = g->n_z > 1 || g->n_det_z > 1 ? (uint64_t)g->n_x * g->n_y : (uint64_t)g->n_x;
   const int chunk = n_parts > 1 ? n_sel : (threads < 1 ? 1 : threads);
   double** part = (double**)malloc(sizeof(double*) * (chunk > 0 ? chunk : 1));
   for (int i = 0; i < chunk; ++i) part[i] = (double*)malloc(nv * sizeof(double));
@@ -1337,7 +1356,8 @@ static int back_mf_angles_impl(const o_geom* g, const int32_t* angles, int n_sel
   int st = 0;
   for (int k0 = 0; k0 < n_sel && st == 0; k0 += chunk) {
     const int n = (n_sel - k0) < chunk ? (n_sel - k0) : chunk;
-    bwd_user u = {angles, y, part, k0, n_parts, (uint64_t)g->n_det_y * g->n_det_z, nv, mode, k};
+    bwd_user u = {angles, y, part, k0, n_parts, (uint64_t)g->n_det_y * g->n_det_z, nv, mode, k,
+                  z0, z1, compact};
     task t;
     memset(&t, 0, sizeof t);
     t.fn = bwd_task;
@@ -1348,7 +1368,7 @@ static int back_mf_angles_impl(const o_geom* g, const int32_t* angles, int n_sel
     st = run_tasks(&t);
     if (st == 0)
       for (int k = 0; k < n; ++k)
-        for (uint64_t i = 0; i < nv; ++i) x[i] += part[k][i];
+        for (uint64_t i = (uint64_t)z0 * plane; i < (uint64_t)z1 * plane; ++i) x[i] += part[k][i];
   }
   for (int i = 0; i < chunk; ++i) free(part[i]);
   free(part);
@@ -1357,11 +1377,17 @@ static int back_mf_angles_impl(const o_geom* g, const int32_t* angles, int n_sel
 
 int ref_back_mf_angles(const o_geom* g, const int32_t* angles, int n_sel, const double* y,
                        double* x, int threads) {
-  return back_mf_angles_impl(g, angles, n_sel, y, x, threads, 0, 0, 1);
+  return back_mf_angles_impl(g, angles, n_sel, y, x, threads, 0, 0, 1, 0, -1, 0);
 }
 int ref_back_mf_angles_par(const o_geom* g, const int32_t* angles, int n_sel, const double* y,
                            double* x, int threads) {
-  return back_mf_angles_impl(g, angles, n_sel, y, x, threads, 1, 0, 1);
+  return back_mf_angles_impl(g, angles, n_sel, y, x, threads, 1, 0, 1, 0, -1, 0);
+}
+/* A^T y of the listed angles on the voxels of z slabs [zlo, zhi) (other
+ * voxels 0); y_rows holds only the rows of the listed angles, in list order. */
+int ref_back_mf_angles_slabs(const o_geom* g, const int32_t* angles, int n_sel, int zlo, int zhi,
+                             const double* y_rows, double* x, int threads) {
+  return back_mf_angles_impl(g, angles, n_sel, y_rows, x, threads, 1, 0, 1, zlo, zhi, 1);
 }
 
 int ref_back_project_matrix_free(const o_geom* g, const double* y, double* x, int threads) {
@@ -1381,13 +1407,13 @@ static int32_t* all_angles(const o_geom* g) {
 int ref_forward_mf_mode(const o_geom* g, int mode, int k, const double* x, double* y,
                         int threads) {
   int32_t* all = all_angles(g);
-  const int st = forward_mf_angles_impl(g, all, g->n_angles, x, y, threads, 0, mode, k);
+  const int st = forward_mf_angles_impl(g, all, g->n_angles, x, y, threads, 0, mode, k, 0, -1);
   free(all);
   return st;
 }
 int ref_back_mf_mode(const o_geom* g, int mode, int k, const double* y, double* x, int threads) {
   int32_t* all = all_angles(g);
-  const int st = back_mf_angles_impl(g, all, g->n_angles, y, x, threads, 0, mode, k);
+  const int st = back_mf_angles_impl(g, all, g->n_angles, y, x, threads, 0, mode, k, 0, -1, 0);
   free(all);
   return st;
 }

@@ -55,6 +55,13 @@ int ref_forward_mf_angles_par(const o_geom* g, const int32_t* angles, int n_sel,
                               double* y_sel, int threads);
 int ref_back_mf_angles_par(const o_geom* g, const int32_t* angles, int n_sel, const double* y,
                            double* x, int threads);
+/* slab-restricted variants (z slabs [zlo, zhi); 2D: pixel rows): forward from
+ * the voxels of those slabs only; back-projection onto those voxels only, from
+ * y_rows = the rows of the listed angles in list order */
+int ref_forward_mf_angles_slabs(const o_geom* g, const int32_t* angles, int n_sel, int zlo,
+                                int zhi, const double* x, double* y_sel, int threads);
+int ref_back_mf_angles_slabs(const o_geom* g, const int32_t* angles, int n_sel, int zlo, int zhi,
+                             const double* y_rows, double* x, int threads);
 long ref_angle_block_entries_par(const o_geom* g, int ip, uint32_t* row, uint32_t* col, double* w,
                                  long cap, int threads);
 int ref_sirt(const o_geom* g, const double* y, double* x, int iters, int threads);

@@ -140,9 +140,19 @@ class Oracle:
         if self.has_par:
             L.ref_forward_mf_angles_par.argtypes = [_P, _P, ctypes.c_int, _P, _P, ctypes.c_int]
             L.ref_back_mf_angles_par.argtypes = [_P, _P, ctypes.c_int, _P, _P, ctypes.c_int]
+        # slab-parallel angle blocks: the restatement, and the reference's own
+        # voxel_volume_factors / pixel_area_factors per slab (ref_shim.cpp)
+        self.has_entries_par = hasattr(L, "ref_angle_block_entries_par")
+        if self.has_entries_par:
             L.ref_angle_block_entries_par.argtypes = [_P, ctypes.c_int, _P, _P, _P, ctypes.c_long,
                                                       ctypes.c_int]
             L.ref_angle_block_entries_par.restype = ctypes.c_long
+        self.has_slabs = hasattr(L, "ref_forward_mf_angles_slabs")
+        if self.has_slabs:
+            L.ref_forward_mf_angles_slabs.argtypes = [_P, _P, ctypes.c_int, ctypes.c_int,
+                                                      ctypes.c_int, _P, _P, ctypes.c_int]
+            L.ref_back_mf_angles_slabs.argtypes = [_P, _P, ctypes.c_int, ctypes.c_int,
+                                                   ctypes.c_int, _P, _P, ctypes.c_int]
         L.ref_angle_column_sums.argtypes = [_P, ctypes.c_int, _P]
         L.ref_line_weights.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_int, _P, _P, ctypes.c_long]
@@ -224,7 +234,7 @@ class Oracle:
             w = np.empty(n, np.float64)
             self._check(f(p, MODES[mode], k, ip, _ptr(row), _ptr(col), _ptr(w), n))
             return row, col, w
-        if threads > 1 and self.has_par:
+        if threads > 1 and self.has_entries_par:
             f = self.lib.ref_angle_block_entries_par
             n = int(1.3 * 12 * g.n_x * g.n_y * g.n_z) + 1024
             for _ in range(2):
@@ -320,6 +330,31 @@ class Oracle:
         x = np.zeros(g.n_x * g.n_y * g.n_z, np.float64)
         f = self.lib.ref_back_mf_angles_par if (split and self.has_par) else self.lib.ref_back_mf_angles
         self._check(f(p, _ptr(a), a.size, _ptr(y), _ptr(x), threads))
+        return x
+
+    def forward_mf_angles_slabs(self, g, angles, zlo: int, zhi: int, x: np.ndarray,
+                                threads: int = 1) -> np.ndarray:
+        """A x rows of the listed angles from the voxels of z slabs [zlo, zhi)
+        only (restatement only): BASELINE-scale parity of chosen slabs."""
+        og, p = self._g(g)
+        a = np.ascontiguousarray(angles, np.int32)
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros(a.size * g.n_det_y * g.n_det_z, np.float64)
+        self._check(self.lib.ref_forward_mf_angles_slabs(p, _ptr(a), a.size, zlo, zhi, _ptr(x),
+                                                         _ptr(y), threads))
+        return y
+
+    def back_mf_angles_slabs(self, g, angles, zlo: int, zhi: int, y_rows: np.ndarray,
+                             threads: int = 1) -> np.ndarray:
+        """A^T y of the listed angles on the voxels of z slabs [zlo, zhi)
+        (others 0); y_rows = the rows of the listed angles, in list order."""
+        og, p = self._g(g)
+        a = np.ascontiguousarray(angles, np.int32)
+        yr = np.ascontiguousarray(y_rows, np.float64)
+        assert yr.size == a.size * g.n_det_y * g.n_det_z
+        x = np.zeros(g.n_x * g.n_y * g.n_z, np.float64)
+        self._check(self.lib.ref_back_mf_angles_slabs(p, _ptr(a), a.size, zlo, zhi, _ptr(yr),
+                                                      _ptr(x), threads))
         return x
 
     def sirt(self, g, y: np.ndarray, x0: np.ndarray, iters: int, threads: int = 1) -> np.ndarray:

@@ -158,6 +158,54 @@ long ref_angle_block_entries(const RefGeom* rg, int ip, uint32_t* row, uint32_t*
             return n;)
 }
 
+// detail::angle_block_entries (projector.cpp:44-84, consistent mode) with the
+// z slabs (2D: pixel rows) spread over `threads` workers: each slab calls the
+// reference's public voxel_volume_factors / pixel_area_factors for its voxels
+// in the reference's z -> y -> x order with the reference's raster and column
+// maps, and the slabs are concatenated in slab order, so the entries (and
+// their order) are identical to ref_angle_block_entries. Used by the flip
+// tests against the reference as shipped (glibc libm) at BASELINE size.
+long ref_angle_block_entries_par(const RefGeom* rg, int ip, uint32_t* row, uint32_t* col,
+                                 double* w, long cap, int threads) {
+  REF_GUARD(
+      const ctsm::ScanGeometry g = to_g(rg); g.validate(); const double phi = g.angle(ip);
+      const bool two_d = g.is_2d(); const int n_slab = two_d ? g.n_y : g.n_z;
+      struct Ent { uint32_t r, c; double w; };
+      std::vector<std::vector<Ent>> slabs(n_slab);
+      const auto raster = [&](int m_y, int m_z) {
+        return (uint32_t)((m_z + g.n_det_z / 2) * g.n_det_y + (m_y + g.n_det_y / 2));
+      };
+      parallel_range(n_slab, threads, [&](int sl) {
+        auto& out = slabs[sl];
+        if (two_d) {
+          for (int ix = 0; ix < g.n_x; ++ix) {
+            const ctsm::VoxelIndex n{ix, sl, 0};
+            const uint32_t c = (uint32_t)ctsm::voxel_column(g, n);
+            for (const auto& cw : ctsm::pixel_area_factors(n, phi, g))
+              out.push_back({raster(cw.m_y, 0), c, cw.w});
+          }
+          return;
+        }
+        for (int iy = 0; iy < g.n_y; ++iy)
+          for (int ix = 0; ix < g.n_x; ++ix) {
+            const ctsm::VoxelIndex n{ix, iy, sl};
+            const uint32_t c = (uint32_t)ctsm::voxel_column(g, n);
+            for (const auto& vw : ctsm::voxel_volume_factors(n, phi, g))
+              out.push_back({raster(vw.m_y, vw.m_z), c, vw.w});
+          }
+      });
+      long n = 0;
+      for (const auto& sv : slabs) for (const Ent& e : sv) {
+        if (n < cap) {
+          row[n] = e.r;
+          col[n] = e.c;
+          w[n] = e.w;
+        }
+        ++n;
+      }
+      return n;)
+}
+
 // build_system_matrix (projector.cpp:144-201) -> opaque handle.
 void* ref_build_system_matrix(const RefGeom* rg, int threads, uint64_t budget, int* status) {
   try {
@@ -251,6 +299,78 @@ int ref_back_mf_angles(const RefGeom* rg, const int32_t* angles, int n_sel, cons
               for (int t = 0; t < n; ++t)
                 for (uint64_t i = 0; i < nv; ++i) x[i] += part[t][i];
             } return 0;)
+}
+
+// Bounded sample of one A x + A^T y step for bench.py's reference arm: work
+// items are (listed angle, z-slab band) pairs spread over `threads` workers;
+// each item walks the voxels of its band with the reference's own
+// voxel_volume_factors / pixel_area_factors (weights3d.hpp:90,
+// weights2d.hpp:31) in projector.cpp:53-69's order and applies every weight
+// twice: y[r] += w x[c] into the item's angle block (forward_project_matrix_free,
+// projector.cpp:249-252) and x_out[c] += w y[r] (the a16 adjoint). Slab bands
+// are disjoint, so the reference's per-angle parallelism (ordered_parallel_for,
+// projector.cpp:114-140) is kept while a few angles still use every core.
+// *updates = weights applied (one per weight and direction).
+int ref_mf_pair_sample(const RefGeom* rg, const int32_t* angles, int n_sel, int zlo, int zhi,
+                       int bands, const double* x, const double* y, double* checksum,
+                       uint64_t* updates, int threads) {
+  REF_GUARD(
+      const ctsm::ScanGeometry g = to_g(rg); g.validate();
+      const bool two_d = g.is_2d(); const int n_slab = two_d ? g.n_y : g.n_z;
+      zlo = std::max(0, zlo); zhi = std::min(n_slab, zhi); bands = std::max(1, bands);
+      const uint64_t rpa = (uint64_t)g.n_det_y * g.n_det_z;
+      const int items = n_sel * bands;
+      std::vector<double> sums(items, 0.0);
+      std::vector<uint64_t> counts(items, 0);
+      const auto raster = [&](int m_y, int m_z) {
+        return (uint32_t)((m_z + g.n_det_z / 2) * g.n_det_y + (m_y + g.n_det_y / 2));
+      };
+      parallel_range(items, threads, [&](int it) {
+        const int k = it / bands, b = it % bands;
+        const int lo = zlo + (int)((int64_t)(zhi - zlo) * b / bands);
+        const int hi = zlo + (int)((int64_t)(zhi - zlo) * (b + 1) / bands);
+        const double phi = g.angle(angles[k]);
+        const double* yb = y + (uint64_t)angles[k] * rpa;
+        std::vector<double> block(rpa, 0.0);
+        const uint64_t plane = two_d ? (uint64_t)g.n_x : (uint64_t)g.n_x * g.n_y;
+        const uint64_t base = (uint64_t)lo * plane;
+        std::vector<double> xp((uint64_t)(hi - lo) * plane, 0.0);  // the angle's partial volume
+        uint64_t n = 0;
+        for (int sl = lo; sl < hi; ++sl) {
+          if (two_d) {
+            for (int ix = 0; ix < g.n_x; ++ix) {
+              const ctsm::VoxelIndex v{ix, sl, 0};
+              const uint32_t c = (uint32_t)ctsm::voxel_column(g, v);
+              for (const auto& cw : ctsm::pixel_area_factors(v, phi, g)) {
+                const uint32_t r = raster(cw.m_y, 0);
+                block[r] += cw.w * x[c];
+                xp[c - base] += cw.w * yb[r];
+                ++n;
+              }
+            }
+            continue;
+          }
+          for (int iy = 0; iy < g.n_y; ++iy)
+            for (int ix = 0; ix < g.n_x; ++ix) {
+              const ctsm::VoxelIndex v{ix, iy, sl};
+              const uint32_t c = (uint32_t)ctsm::voxel_column(g, v);
+              for (const auto& vw : ctsm::voxel_volume_factors(v, phi, g)) {
+                const uint32_t r = raster(vw.m_y, vw.m_z);
+                block[r] += vw.w * x[c];
+                xp[c - base] += vw.w * yb[r];
+                ++n;
+              }
+            }
+        }
+        double bs = 0.0;
+        for (double v : block) bs += v;
+        for (double v : xp) bs += v;
+        sums[it] = bs;
+        counts[it] = 2 * n;
+      });
+      double cs = 0.0; uint64_t nu = 0;
+      for (int i = 0; i < items; ++i) { cs += sums[i]; nu += counts[i]; }
+      *checksum = cs; *updates = nu; return 0;)
 }
 
 int ref_back_project_matrix_free(const RefGeom* rg, const double* y, double* x, int threads) {

@@ -53,6 +53,7 @@ SIGNATURES = {
     "ctsm_fwd_mf": (_I, [_P, _GP, _I, _I, _I, _I, _P, _P, _P]),
     "ctsm_bwd_mf": (_I, [_P, _GP, _I, _I, _I, _I, _P, _P, _P]),
     "ctsm_last_update_count": (_U64, [_P]),
+    "ctsm_last_kernel_path": (_I, [_P]),
     "ctsm_quarter_symmetric": (_I, [_GP]),
     "ctsm_symmetry_order": (_I, [_GP]),
     "ctsm_fwd_mf_orbits": (_I, [_P, _GP, _I, _I, _I, _P, _P, _P]),
@@ -67,6 +68,8 @@ SIGNATURES = {
     "ctsm_bwd_mf_mode": (_I, [_P, _GP, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
     "ctsm_forward_project_matrix_free_host": (_I, [_P, _GP, _P, _P]),
     "ctsm_back_project_matrix_free_host": (_I, [_P, _GP, _P, _P]),
+    "ctsm_forward_project_matrix_free_host_f32": (_I, [_P, _GP, _P, _P]),
+    "ctsm_back_project_matrix_free_host_f32": (_I, [_P, _GP, _P, _P]),
     "ctsm_spectral_norm_power": (_I, [_P, _OP, _I, _P, ctypes.POINTER(_D), _P]),
     "ctsm_nag_tikhonov": (_I, [_P, _OP, _P, _D, _I, _D, _P, _P, ctypes.POINTER(_I),
                                ctypes.POINTER(_I), _P]),

@@ -69,6 +69,9 @@ struct ctsm_ctx {
   unsigned long long* n_upd = nullptr;    // device: voxel-ray updates of the last forward call
   unsigned long long* h_upd = nullptr;    // pinned mirror
   uint64_t last_updates = 0;
+  // kernel family of the last matrix-free call (ctsm_last_kernel_path):
+  // CTSM_PATH_* bits, so tests can assert which production kernel ran
+  int last_path = 0;
   double* h_red = nullptr;      // pinned
   Buf angles, edges, cs, counts, scan, longrows, acc, part, base, alist, sv_up, sv_h, sv_hp,
       sv_q, sv_v, sv_part, sv_scal, tmp_a, tmp_b, tmp_c, tmp_d,
@@ -465,6 +468,15 @@ static int symmetry_order(const ctsm_geometry* g) {
     return 8;
   return 4;
 }
+// CTSM_PATH_* bits of a symmetric call (include/ctsm_b200.h).
+static int sym_path_bits(const ctsm_geometry* g) {
+  const bool two_d = (g->n_z == 1 && g->n_det_z == 1);
+  int p = symmetry_order(g) == 8 ? CTSM_PATH_DIHEDRAL : CTSM_PATH_QUARTER;
+#ifndef CTSM_NO_ZMIRROR
+  if (!two_d && g->n_z % 2 == 0) p |= CTSM_PATH_ZMIRROR;
+#endif
+  return p;
+}
 // Base angle set of a symmetry order: [0, n/4) for 4, [0, n/8] for 8.
 static int base_limit(const ctsm_geometry* g, int order) {
   return order == 8 ? g->n_angles / 8 + 1 : g->n_angles / 4;
@@ -522,6 +534,7 @@ static int fwd_d8_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d, 
   const bool two_d = (g->n_z == 1 && g->n_det_z == 1);
   const size_t nf = (!two_d && dtype == CTSM_F32) ? fwd3d_f32_scratch_elems(d, 8) : 0;
   if (nf) {  // fp32 3D: vector float reductions, no fixed-point rows
+    ctx->last_path |= CTSM_PATH_F32_VECRED;
     CT_TRY(upload_base(ctx, d, base, st));
     CT_TRY(ensure(ctx, ctx->bwd_t, nf * sizeof(float)));
     CT_TRY(ensure(ctx, ctx->vol_t, (size_t)d.n_vox * sizeof(float)));
@@ -572,6 +585,7 @@ static int fwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d,
   double mx = 0.0;
   CT_TRY(fetch_max_abs(ctx, dtype, (uint64_t)d.n_vox, x, st, &mx));
   if (!std::isfinite(mx)) return fail(CTSM_ERR_NON_FINITE, "image not finite");
+  ctx->last_path = sym_path_bits(g);
   if (symmetry_order(g) == 8) return fwd_d8_impl(ctx, g, d, dtype, base, mx, x, y, st);
   CT_TRY(upload_base(ctx, d, base, st));
   CT_TRY(ensure(ctx, ctx->acc, n_meas * sizeof(unsigned long long)));
@@ -600,11 +614,13 @@ static int fwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d,
 
 static int bwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d, int dtype,
                         const std::vector<int>& base, const void* y, void* x, cudaStream_t st) {
+  ctx->last_path = sym_path_bits(g);
   CT_TRY(upload_base(ctx, d, base, st));
   const int nb = (int)base.size();
   const bool two_d = (g->n_z == 1 && g->n_det_z == 1);
   if (!two_d) {
     const size_t ne = bwd3d_scratch_elems(d, symmetry_order(g), dtype);
+    if (!ne) ctx->last_path &= ~CTSM_PATH_ZMIRROR;  // the plain-gather variant has no mirror
     if (ne) CT_TRY(ensure(ctx, ctx->bwd_t, ne * (dtype == CTSM_F64 ? 8 : 4)));
     CT_TRY(ensure(ctx, ctx->vol_t, (size_t)d.n_vox * (dtype == CTSM_F64 ? 8 : 4)));
     CT_CUDA(bwd3d_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, y, x,
@@ -641,6 +657,7 @@ static int fwd_impl(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int begin,
   double mx = 0.0;
   CT_TRY(fetch_max_abs(ctx, dtype, (uint64_t)d.n_vox, x, st, &mx));
   if (!std::isfinite(mx)) return fail(CTSM_ERR_NON_FINITE, "image not finite");
+  ctx->last_path = CTSM_PATH_GENERAL;
   CT_TRY(prepare_cs(ctx, d, begin, step, n_sel, st));
   CT_TRY(ensure(ctx, ctx->acc, n_meas * sizeof(unsigned long long)));
   unsigned long long* acc = (unsigned long long*)ctx->acc.p;
@@ -666,6 +683,7 @@ static int bwd_impl(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int begin,
   std::vector<int> base;
   if (n_sel > 0 && quarter_symmetric(g) && sym_base_of_shard(g, begin, end, step, &base))
     return bwd_sym_impl(ctx, g, d, dtype, base, y, x, st);
+  ctx->last_path = CTSM_PATH_GENERAL;
   CT_TRY(prepare_cs(ctx, d, begin, step, n_sel, st));
   const int nc = bwd_chunks(d, n_sel);
   if (nc > 1) CT_TRY(ensure(ctx, ctx->part, (size_t)nc * g->n_x * g->n_y * sizeof(double)));
@@ -685,6 +703,8 @@ int ctsm_fwd_mf(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int angle_begi
 }
 
 uint64_t ctsm_last_update_count(ctsm_ctx* ctx) { return ctx ? ctx->last_updates : 0; }
+
+int ctsm_last_kernel_path(ctsm_ctx* ctx) { return ctx ? ctx->last_path : 0; }
 
 int ctsm_quarter_symmetric(const ctsm_geometry* g) {
   DevGeom d;
@@ -1206,36 +1226,64 @@ int ctsm_nag_tikhonov(ctsm_ctx* ctx, const ctsm_operator* op, const double* p_de
 }
 
 // ---- host-buffer entry points ------------------------------------------------
-int ctsm_forward_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,
-                                          const double* x_host, double* y_host) {
+// The reference's value-semantics calls (projector.hpp:56-59 and the a16
+// adjoint): host x / y in, host y / x out, copies and kernels on the
+// context's own non-blocking stream. f64, and the fp32 overloads (SURVEY.md
+// §8(b) "fp32 overloads") whose weights are still evaluated in FP64.
+static int fwd_host(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, const void* x_host,
+                    void* y_host) {
   CT_TRY(set_device(ctx));
   DevGeom d;
   CT_TRY(dev_geom(g, &d));
+  const size_t es = dtype == CTSM_F64 ? 8 : 4;
   const uint64_t nv = (uint64_t)d.n_vox, nm = (uint64_t)d.rows_per_angle * g->n_angles;
-  CT_TRY(ensure(ctx, ctx->tmp_a, nv * sizeof(double)));
-  CT_TRY(ensure(ctx, ctx->tmp_b, nm * sizeof(double)));
+  CT_TRY(ensure(ctx, ctx->tmp_a, nv * es));
+  CT_TRY(ensure(ctx, ctx->tmp_b, nm * es));
   cudaStream_t st;
   CT_TRY(host_stream(ctx, &st));
-  CT_CUDA(cudaMemcpyAsync(ctx->tmp_a.p, x_host, nv * sizeof(double), cudaMemcpyHostToDevice, st));
-  CT_TRY(fwd_impl(ctx, g, CTSM_F64, 0, g->n_angles, 1, ctx->tmp_a.p, ctx->tmp_b.p, st));
-  CT_CUDA(cudaMemcpyAsync(y_host, ctx->tmp_b.p, nm * sizeof(double), cudaMemcpyDeviceToHost, st));
-  return check_status(ctx, st, "forward_project_matrix_free");
+  CT_CUDA(cudaMemcpyAsync(ctx->tmp_a.p, x_host, nv * es, cudaMemcpyHostToDevice, st));
+  CT_TRY(fwd_impl(ctx, g, dtype, 0, g->n_angles, 1, ctx->tmp_a.p, ctx->tmp_b.p, st));
+  CT_CUDA(cudaMemcpyAsync(y_host, ctx->tmp_b.p, nm * es, cudaMemcpyDeviceToHost, st));
+  CT_TRY(check_status(ctx, st, "forward_project_matrix_free"));
+  ctx->last_updates = *ctx->h_upd;
+  return 0;
+}
+
+static int bwd_host(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, const void* y_host,
+                    void* x_host) {
+  CT_TRY(set_device(ctx));
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  const size_t es = dtype == CTSM_F64 ? 8 : 4;
+  const uint64_t nv = (uint64_t)d.n_vox, nm = (uint64_t)d.rows_per_angle * g->n_angles;
+  CT_TRY(ensure(ctx, ctx->tmp_a, nv * es));
+  CT_TRY(ensure(ctx, ctx->tmp_b, nm * es));
+  cudaStream_t st;
+  CT_TRY(host_stream(ctx, &st));
+  CT_CUDA(cudaMemcpyAsync(ctx->tmp_b.p, y_host, nm * es, cudaMemcpyHostToDevice, st));
+  CT_TRY(bwd_impl(ctx, g, dtype, 0, g->n_angles, 1, ctx->tmp_b.p, ctx->tmp_a.p, st));
+  CT_CUDA(cudaMemcpyAsync(x_host, ctx->tmp_a.p, nv * es, cudaMemcpyDeviceToHost, st));
+  return check_status(ctx, st, "back_project_matrix_free");
+}
+
+int ctsm_forward_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,
+                                          const double* x_host, double* y_host) {
+  return fwd_host(ctx, g, CTSM_F64, x_host, y_host);
 }
 
 int ctsm_back_project_matrix_free_host(ctsm_ctx* ctx, const ctsm_geometry* g,
                                        const double* y_host, double* x_host) {
-  CT_TRY(set_device(ctx));
-  DevGeom d;
-  CT_TRY(dev_geom(g, &d));
-  const uint64_t nv = (uint64_t)d.n_vox, nm = (uint64_t)d.rows_per_angle * g->n_angles;
-  CT_TRY(ensure(ctx, ctx->tmp_a, nv * sizeof(double)));
-  CT_TRY(ensure(ctx, ctx->tmp_b, nm * sizeof(double)));
-  cudaStream_t st;
-  CT_TRY(host_stream(ctx, &st));
-  CT_CUDA(cudaMemcpyAsync(ctx->tmp_b.p, y_host, nm * sizeof(double), cudaMemcpyHostToDevice, st));
-  CT_TRY(bwd_impl(ctx, g, CTSM_F64, 0, g->n_angles, 1, ctx->tmp_b.p, ctx->tmp_a.p, st));
-  CT_CUDA(cudaMemcpyAsync(x_host, ctx->tmp_a.p, nv * sizeof(double), cudaMemcpyDeviceToHost, st));
-  return check_status(ctx, st, "back_project_matrix_free");
+  return bwd_host(ctx, g, CTSM_F64, y_host, x_host);
+}
+
+int ctsm_forward_project_matrix_free_host_f32(ctsm_ctx* ctx, const ctsm_geometry* g,
+                                              const float* x_host, float* y_host) {
+  return fwd_host(ctx, g, CTSM_F32, x_host, y_host);
+}
+
+int ctsm_back_project_matrix_free_host_f32(ctsm_ctx* ctx, const ctsm_geometry* g,
+                                           const float* y_host, float* x_host) {
+  return bwd_host(ctx, g, CTSM_F32, y_host, x_host);
 }
 
 }  // extern "C"

@@ -416,6 +416,14 @@ def back_project_matrix_free(g: ScanGeometry, mode: str = MatrixMode.consistent,
     return x if (was_t or out is not None) else x.cpu().numpy()
 
 
+def last_kernel_path(context: Optional["Context"] = None, device: Optional[int] = None) -> int:
+    """CTSM_PATH_* bits of the last matrix-free call on a context
+    (include/ctsm_b200.h): 1 general, 4 quarter-turn, 8 dihedral, +16 z mirror,
+    +32 fp32 vector-reduction forward."""
+    ctx = context if context is not None else Context.get(device)
+    return int(_lib.lib().ctsm_last_kernel_path(ctx.handle))
+
+
 def angle_column_sums(g: ScanGeometry, mode: str = MatrixMode.consistent, k: int = 1,
                       angle_index: int = 0, device: Optional[int] = None):
     """projector.cpp:288-295: per-voxel sums of one angle block (A^T 1 on one angle)."""

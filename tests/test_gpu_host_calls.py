@@ -59,3 +59,41 @@ def test_host_calls_concurrent_bitequal(name):
     finally:
         ca.close()
         cb.close()
+
+
+def _host_f32(ctx, g, fn, src, n_out):
+    out = np.empty(n_out, np.float32)
+    cg = g.to_c()
+    _lib.check(getattr(_lib.lib(), fn)(ctx.handle, ctypes.byref(cg),
+                                       ctypes.c_void_p(src.ctypes.data),
+                                       ctypes.c_void_p(out.ctypes.data)))
+    return out
+
+
+@pytest.mark.parametrize("name", ["cone16", "c3_slab"])
+def test_host_calls_f32(name):
+    """fp32 overloads (ctsm_*_project_matrix_free_host_f32) =
+    the device-resident fp32 calls: A^T y bit-equal (fixed-order gathers), A x
+    within 1e-6 (the fp32 3D forward's vector reductions are order-dependent
+    at fp32 rounding)."""
+    if name == "cone16":
+        g = TEST_GEOMETRIES["cone3d"].with_(n_angles=16)
+    else:
+        g = CONFIGS["c3"].with_(n_x=64, n_y=64, n_z=32, n_det_z=96, n_angles=64)
+    rng = np.random.default_rng(9)
+    x = rng.random(g.n_voxels).astype(np.float32)
+    y = rng.random(g.n_measurements).astype(np.float32)
+    dev_y = forward_project_matrix_free(g, "consistent", 1, torch.from_numpy(x).cuda()).cpu().numpy()
+    dev_x = back_project_matrix_free(g, "consistent", 1, torch.from_numpy(y).cuda()).cpu().numpy()
+    ca, cb = Context(0), Context(0)
+    try:
+        with ThreadPoolExecutor(max_workers=1) as pool:
+            fut = pool.submit(_host_f32, cb, g, "ctsm_back_project_matrix_free_host_f32", y,
+                              g.n_voxels)
+            yf = _host_f32(ca, g, "ctsm_forward_project_matrix_free_host_f32", x, g.n_measurements)
+            xb = fut.result()
+        assert np.max(np.abs(yf - dev_y)) <= 1e-6 * max(1.0, float(np.max(np.abs(dev_y))))
+        assert np.array_equal(xb, dev_x)
+    finally:
+        ca.close()
+        cb.close()
