@@ -1,24 +1,33 @@
 #!/usr/bin/env python3
 """Benchmark of the consistent-system-matrix hot path on B200.
 
-Workload (default, --config c1): BASELINE.json configs[1] -- 2D fan-beam
-512x512 grid, 0.5 mm pixels, s=500, sdd=1000, 1024 cells of 0.6 mm, 720
-angles; one step = matrix-free A x (40-ellipse phantom) + A^T y (U[0,1)
-sinogram), fp64 storage and FP64 weights. Metric: voxel-ray updates/s, where
-one projection performs nnz(A) = 591,345,624 updates, so
-a step is 2 * nnz updates. Multi-GPU (torchrun): angles are sharded
-round-robin (rank::N); A x needs no communication, the A^T y partial volumes
-are summed with an NCCL all-reduce.
+Default workload (--config c3): BASELINE.json configs[3], the largest
+matrix-free projection pair that BASELINE.json states for 1-8 GPUs -- 3D
+circular cone-beam, 256^3 voxels of 0.5 mm, s = 500, sdd = 1000, 512 x 384
+detector of 0.8 mm pixels, 720 angles; one step = matrix-free A x
+(50-ellipsoid phantom) + A^T y (U[0,1) sinogram), fp32 storage, FP64 weights.
+Metric: voxel-ray updates/s = nonzero weights applied per second (a projection
+applies nnz(A) of them; counted live by the forward kernel). Other workloads:
+--config c0..c4, --dtype f32|f64, --mode proj|sirt|csr.
+
+Multi-GPU: `python bench.py --gpus N` re-launches itself under
+torch.distributed.run with N ranks (or is launched that way by the driver);
+angles are sharded by symmetry orbits (rank r takes base angles r, r+N, ...
+and their images), A x needs no communication, the A^T y partial volumes are
+summed with an NCCL all-reduce.
 
 --impl reference times the reference's own CPU implementation
-(oracle/_ref/libctsm_ref_glibc.so: forward_project_matrix_free and the
-angle_block_entries adjoint) on all host cores over a bounded angle sample.
+(oracle/_ref/libctsm_ref_glibc.so, the unmodified reference sources) on all
+host cores; each step is a bounded sample of the same workload (strided
+angles x strided voxel slabs, A x and A^T y each evaluating the weights as
+the reference does).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import subprocess
 import sys
 import time
@@ -28,34 +37,40 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# nnz(A) per projection (voxel-ray updates); C1/C2 are
-# re-verified by tests/test_gpu_parity.py::test_nnz_counts.
+# nnz(A) per projection (voxel-ray updates), SURVEY.md §0 fact 4 (C0/C1 are
+# checked against the GPU's live count and CSR by tests/test_gpu_parity.py).
 NNZ = {"c0": 18_291_648, "c1": 591_345_624, "c2": 4_604_879_490}
-# sampled estimates for the matrix-free 3D configs; the
-# GPU arm counts its updates live, the CPU reference arm uses these.
+# sampled estimates for the matrix-free 3D configs; only
+# used to extrapolate the CPU sample to a full step, never for `value`.
 NNZ_EST = {"c3": 7.22e10, "c4": 1.158e12}
 # FP64 operations per pixel/voxel-angle as executed by the reference
-# (add/sub/mul/div each 1, libm calls excluded).
+# (add/sub/mul/div each 1, an FMA would count 1, libm calls
+# excluded).
 F_REF = {"2d": 247.0, "3d": 1513.0}
+DEFAULT_DTYPE = {"c0": "f64", "c1": "f64", "c2": "f64", "c3": "f32", "c4": "f32"}
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=None,
-                   help="timed steps (default: 50 for proj, 5 for sirt, 3 for csr)")
+                   help="timed steps (default: 20 for proj (50 for 2D), 5 for sirt, 3 for csr)")
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="c1")
-    p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    p.add_argument("--config", default="c3", choices=["c0", "c1", "c2", "c3", "c4"])
+    p.add_argument("--dtype", default=None, choices=["f64", "f32"])
     p.add_argument("--no-clocks", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--mode", default="proj", choices=["proj", "sirt", "csr"],
                    help="proj: one A x + A^T y per step; sirt: one SIRT iteration per step "
-                        "(BASELINE configs[4]: y = A x_true + 1%% noise)")
+                        "(BASELINE configs[4]: y = A x_true + 1%% noise); csr: one "
+                        "build_system_matrix per step")
     a = p.parse_args()
+    if a.dtype is None:
+        a.dtype = DEFAULT_DTYPE[a.config]
     if a.steps is None:
-        a.steps = {"proj": 50, "sirt": 5, "csr": 3}[a.mode]
+        a.steps = {"proj": 50 if a.config in ("c0", "c1") else 20, "sirt": 5, "csr": 3}[a.mode]
     return a
 
 
@@ -66,63 +81,209 @@ def dist_env():
     return world, rank, local
 
 
+def relaunch_if_needed(args):
+    """`python bench.py --gpus N` without torchrun: start the N ranks here
+    (the driver's own launch line, on 127.0.0.1). Under torchrun the world
+    size must equal --gpus."""
+    if args.impl == "reference" or args.mode == "csr":
+        return
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return
+    if args.gpus <= 1:
+        return
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.run(cmd).returncode)
+
+
+def init_dist(torch, dev):
+    """NCCL process group over the ranks torchrun started; prints the
+    communicator size per rank (NCCL_DEBUG=INFO adds NCCL's own lines)."""
+    import torch.distributed as dist
+    world, rank, local = dist_env()
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        dist.init_process_group("nccl", device_id=dev)
+        assert dist.get_world_size() == world
+        t = torch.ones(1, device=dev)
+        dist.all_reduce(t)
+        print(f"[bench] rank {rank}/{world} on cuda:{local}: communicator nranks={int(t.item())}",
+              file=sys.stderr, flush=True)
+        assert int(t.item()) == world
+    return dist
+
+
+def host_info():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "libc": " ".join(platform.libc_ver()),
+            "cores": os.cpu_count() or 1}
+
+
+def workload_config(args, world):
+    """The `config` object: identical in both arms for the same flags."""
+    cfg = args.config
+    what = {"proj": "matrix-free A x + A^T y", "sirt": "SIRT (one iteration per step)",
+            "csr": "build_system_matrix (consistent CSR assembly)"}[args.mode]
+    return {"workload": f"{cfg}: BASELINE.json configs[{cfg[1]}] {what}",
+            "parallelism": f"angle-shard x{world}",
+            "l2": "flushed (256 MB write) before each step" if args.mode == "proj"
+                  else "working set larger than L2"}
+
+
 # ---------------------------------------------------------------------------
+# The reference's CPU path on a bounded sample (reference arm and cpu_baseline)
+# ---------------------------------------------------------------------------
+def _load_oracle():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    variant = "ref_glibc" if pyoracle.available("ref_glibc") else "port_glibc"
+    return pyoracle, pyoracle.load(variant), variant
+
+
+def sample_inputs(cfg, g):
+    """Synthetic inputs of the CPU sample: the same seeded phantom as the GPU
+    arm where it is cheap to build (2D), a PCG64 U[0.005, 0.02) volume for the
+    3D configs (the CPU cost does not depend on the values)."""
+    from paper_2511_12235_b200.phantoms import phantom_for, uniform_sinogram
+    if g.is_2d():
+        x = phantom_for(cfg, g)
+    else:
+        x = 0.005 + 0.015 * np.random.Generator(np.random.PCG64(12345)).random(g.n_voxels)
+    y = uniform_sinogram(g.n_measurements, 12346)
+    return x, y
+
+
+class PairSample:
+    """A bounded A x + A^T y sample of one config: strided angles (angle 0, a
+    flat-branch angle, included) x strided slabs (z planes / pixel rows),
+    sized by a probe to about `seconds` of wall time on `cores` threads."""
+
+    def __init__(self, cfg, seconds):
+        from paper_2511_12235_b200 import CONFIGS
+        self.pyoracle, self.orc, self.variant = _load_oracle()
+        self.cfg, self.g = cfg, CONFIGS[cfg]
+        g = self.g
+        self.cores = os.cpu_count() or 1
+        self.x, self.y = sample_inputs(cfg, g)
+        n_slab_total = g.n_y if g.is_2d() else g.n_z
+        n_ang = min(g.n_angles, max(16, self.cores))
+        self.angles = np.unique(np.linspace(0, g.n_angles, n_ang, endpoint=False).astype(np.int32))
+        probe_slabs = np.array([n_slab_total // 3], np.int32)
+        t0 = time.perf_counter()
+        self.orc.mf_pair_sample(g, self.angles, probe_slabs, self.x, self.y, self.cores)
+        tau = max(time.perf_counter() - t0, 1e-4)  # one slab of every sampled angle
+        n_sl = int(max(1, min(n_slab_total, seconds / tau)))
+        self.slabs = np.unique(np.linspace(0, n_slab_total, n_sl, endpoint=False).astype(np.int32))
+        self.frac = (self.angles.size * self.slabs.size) / (g.n_angles * n_slab_total)
+
+    def run(self):
+        t0 = time.perf_counter()
+        upd, _ = self.orc.mf_pair_sample(self.g, self.angles, self.slabs, self.x, self.y, self.cores)
+        return upd, time.perf_counter() - t0
+
+    def describe(self, t):
+        unit = "pixel rows" if self.g.is_2d() else "z planes"
+        return (f"A x + A^T y over {self.angles.size} of {self.g.n_angles} strided angles x "
+                f"{self.slabs.size} strided {unit} ({100 * self.frac:.3g}% of a step, {t:.1f} s)")
+
+
+def cpu_baseline_proj(cfg, seconds=12.0):
+    try:
+        s = PairSample(cfg, seconds)
+        upd, t = s.run()
+    except Exception as e:  # pragma: no cover
+        return {"error": repr(e)}
+    return {"value": upd / t, "unit": "updates/s", "cores": s.cores,
+            "kind": "reference" if s.variant == "ref_glibc" else "port",
+            "sample": s.describe(t), **host_info()}
+
+
+def csr_reference_sample(cfg, seconds):
+    """Reference CSR assembly: build_system_matrix in full where it fits a
+    bounded run (C0), else build_angle_block of strided angles, one angle per
+    core (C2). Returns (weights built, seconds, description)."""
+    from paper_2511_12235_b200 import CONFIGS
+    _, orc, variant = _load_oracle()
+    g = CONFIGS[cfg]
+    cores = os.cpu_count() or 1
+    if g.is_2d():
+        t0 = time.perf_counter()
+        w = orc.build_system_matrix(g, threads=cores, budget=1 << 40)
+        t = time.perf_counter() - t0
+        return w.nnz, t, f"build_system_matrix in full ({t:.1f} s)", variant, cores
+    t0 = time.perf_counter()
+    orc.csr_angle_sample(g, np.array([g.n_angles // 3], np.int32), 1)
+    tau = time.perf_counter() - t0
+    rounds = max(1, int(seconds / max(tau, 1e-3)))
+    n_ang = min(g.n_angles, cores * rounds)
+    angles = np.unique(np.linspace(0, g.n_angles, n_ang, endpoint=False).astype(np.int32))
+    t0 = time.perf_counter()
+    nnz = orc.csr_angle_sample(g, angles, cores)
+    t = time.perf_counter() - t0
+    return nnz, t, (f"build_angle_block of {angles.size} of {g.n_angles} strided angles, one angle "
+                    f"per core ({t:.1f} s)"), variant, cores
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle
-    from paper_2511_12235_b200 import CONFIGS
-    from paper_2511_12235_b200.phantoms import phantom_for, uniform_sinogram
-
     cfg = args.config
-    g = CONFIGS[cfg]
-    variant = "ref_glibc" if pyoracle.available("ref_glibc") else "port_glibc"
-    orc = pyoracle.load(variant)
-    cores = os.cpu_count() or 1
-    x = phantom_for(cfg, g)
-    y = uniform_sinogram(g.n_measurements, 12346)
-    # bounded sample: strided angles sized so that the whole --warmup W
-    # --steps K run stays within ~2 minutes (<= 10 s of CPU work per step)
-    step_budget = min(10.0, 120.0 / max(1, args.warmup + args.steps))
-    probe = np.array([0, g.n_angles // 2], np.int32)
-    t0 = time.perf_counter()
-    orc.forward_mf_angles(g, probe, x, cores)
-    orc.back_mf_angles(g, probe, y, cores)
-    tau = time.perf_counter() - t0  # ~ one angle's fwd+bwd (the 2 probes run in parallel)
-    # the reference parallelises over angles: use >= one angle per core
-    n_sample = int(min(g.n_angles, cores * max(1, int(step_budget / max(tau, 1e-6)))))
-    angles = np.linspace(0, g.n_angles, n_sample, endpoint=False).astype(np.int32)
-    times = []
-    for it in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        orc.forward_mf_angles(g, angles, x, cores)
-        orc.back_mf_angles(g, angles, y, cores)
-        t = time.perf_counter() - t0
-        if it >= args.warmup:
+    # each step is a bounded sample; the whole run stays within a few minutes
+    step_budget = min(6.0, 150.0 / max(1, args.warmup + args.steps))
+    if args.mode == "csr":
+        nnz, t, desc, variant, cores = csr_reference_sample(cfg, step_budget)
+        times = [t]
+        for it in range(1, args.warmup + args.steps):
+            nnz, t, desc, variant, cores = csr_reference_sample(cfg, step_budget)
             times.append(t)
-    t_sample = float(np.mean(times))
-    t_full = t_sample * g.n_angles / angles.size  # extrapolated fwd+bwd time
-    value = 2.0 * NNZ.get(cfg, NNZ_EST.get(cfg, 0.0)) / t_full
+        t = float(np.mean(times[-args.steps:]))
+        value, unit, metric = nnz / t, "weights/s", "SM weights/s (consistent CSR assembly)"
+        full_ms = NNZ[cfg] / value * 1e3
+    else:
+        s = PairSample(cfg, step_budget)
+        variant, cores = s.variant, s.cores
+        times, upd = [], 0
+        for it in range(args.warmup + args.steps):
+            upd, t = s.run()
+            if it >= args.warmup:
+                times.append(t)
+        t = float(np.mean(times))
+        desc = s.describe(t)
+        value, unit = upd / t, "updates/s"
+        metric = ("voxel-ray updates/s (SIRT iterations)" if args.mode == "sirt"
+                  else "voxel-ray updates/s (A x + A^T y)")
+        full_ms = 2.0 * NNZ.get(cfg, NNZ_EST.get(cfg, 0.0)) / value * 1e3
     line = {
-        "impl": "reference",
-        "metric": "voxel-ray updates/s (A x + A^T y)",
-        "value": value,
-        "unit": "updates/s",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": t_full * 1e3,
-        "higher_is_better": True,
-        "scaling": "strong",
-        "vs_baseline": None,
-        "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": f"{cfg}: BASELINE.json configs[{cfg[1]}]", "sample_angles": int(angles.size)},
-        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": "reference" if variant == "ref_glibc" else "port",
-                         "sample": f"{angles.size} of {g.n_angles} strided angles, fwd+bwd, extrapolated x{g.n_angles / angles.size:.0f}"},
-        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": metric, "value": value, "unit": unit,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3,  # one step = one bounded sample (see cpu_baseline.sample)
+        "ms_per_full_step_extrapolated": full_ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, args.gpus),
+        "cpu_baseline": {"value": value, "unit": unit, "cores": cores,
+                         "kind": "reference" if variant == "ref_glibc" else "port",
+                         "sample": desc, **host_info()},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -131,8 +292,9 @@ def run_reference(args):
 def measure_dfma_peak(torch):
     """Measured FP64 FMA throughput (TFLOP/s, FMA = 2 flops) with a DFMA
     microkernel in the library's own context."""
-    from paper_2511_12235_b200 import _lib
     import ctypes
+
+    from paper_2511_12235_b200 import _lib
 
     L = _lib.lib()
     f = getattr(L, "ctsm_bench_dfma", None)
@@ -212,11 +374,131 @@ class ClockSampler:
                 "timed_region_s": round(t1 - t0, 4)}
 
 
+def fp64_roofline(torch, g, cfg, dtype, world, ms_f, ms_b):
+    """FP64 roofline of the dominant kernel (the slower of fwd / bwd), per
+    SURVEY.md §8(d): achieved = weight evaluations per launch x F (FP64
+    arithmetic operations per evaluation as the reference executes them, an
+    FMA counting as ONE operation) / kernel time; peak = the measured FP64
+    arithmetic-instruction rate = measured DFMA FLOP/s / 2. The evaluations
+    are the ones the kernel performs: with the dihedral (quarter-turn)
+    symmetry each serves 8 (4) pixel-angles of the workload and, in 3D, the z
+    mirror doubles that (the workload-equivalent figure is beside it)."""
+    from paper_2511_12235_b200.projector import symmetry_order
+    peak_flops = measure_dfma_peak(torch)
+    order = symmetry_order(g)
+    npix = g.n_x * g.n_y * g.n_z
+    n_eval = {8: g.n_angles // 8 + 1, 4: g.n_angles // 4}.get(order, g.n_angles)
+    if order > 1 and world > 1:  # orbit shards: the slowest rank's base angles
+        n_eval = -(-n_eval // world)
+    elif world > 1:
+        n_eval = -(-g.n_angles // world)
+    units = npix * n_eval
+    reuse = g.n_angles / world / n_eval
+    if not g.is_2d() and order > 1 and g.n_z % 2 == 0:
+        units /= 2  # z mirror: only the lower half of every voxel column is evaluated
+        reuse *= 2
+    per_unit = F_REF["2d"] if g.is_2d() else F_REF["3d"]
+    dom_ms = max(ms_f, ms_b)
+    achieved = units * per_unit / (dom_ms * 1e-3) / 1e12  # T FP64 ops/s (FMA = 1)
+    peak_ops = peak_flops / 2.0 if peak_flops else None
+    suffix = {8: "_d8", 4: "_sym"}.get(order, "")
+    kname = ("fwd2d" if ms_f >= ms_b else "bwd2d") + suffix
+    if not g.is_2d():
+        kname = kname.replace("2d", "3d")
+    # DRAM traffic and pipe utilisation of the same kernel and workload from one
+    # committed `ncu --set full` capture (profiles/ncu_kernels.json)
+    traffic = ncu_pipe = ncu_ms = None
+    try:
+        ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_kernels.json")))
+        tname = "double" if dtype == "f64" else "float"
+        kbase = kname.replace("3d_d8", "3d_sym")
+        prefix = f"{cfg}_{dtype}:{kbase}_kernel<{tname}"
+        hits = [k for k in sorted(ncu) if k == prefix + ">" or k.startswith(prefix + ",")]
+        if hits:
+            traffic = ncu[hits[0]]["dram_bytes"]
+            ncu_pipe = ncu[hits[0]].get("fp64_pipe_pct")
+            ncu_ms = ncu[hits[0]].get("duration_ms")
+    except (OSError, ValueError, KeyError):
+        pass
+    return {"bound": "fp64", "kernel": kname, "achieved": achieved, "peak": peak_ops,
+            "unit": "T FP64 op/s (arithmetic instructions, FMA = 1 op; SURVEY.md §8(d))",
+            "frac": (achieved / peak_ops) if peak_ops else None,
+            "frac_flops_convention": (achieved / peak_flops) if peak_flops else None,
+            "traffic": traffic,
+            "traffic_unit": "DRAM bytes per kernel launch of the ncu capture (ncu --set full, "
+                            "profiles/ncu_kernels.json)",
+            "ncu_fp64_pipe_active_pct": ncu_pipe, "ncu_launch_ms": ncu_ms,
+            "peak_source": "measured DFMA microkernel (ctsm_bench_dfma; MEASURED_PEAKS.json has no "
+                           f"FP64 entry): {peak_flops:.2f} TFLOP/s = {peak_ops:.2f} T DFMA/s"
+                           if peak_flops else "unavailable",
+            "work_per_unit": f"{per_unit:g} FP64 ops per weight evaluation (reference op count, "
+                             "SURVEY.md §8(d))",
+            "units_per_launch": units, "symmetry_reuse": reuse,
+            "workload_equivalent_Tops": achieved * reuse,
+            "fwd_ms": ms_f, "bwd_ms": ms_b}
+
+
+def e2e_projection_pair(torch, args, g, x_h, y_h, ctx, local, updates_per_step):
+    """The same step through the reference-facing host-buffer C-ABI
+    (ctsm_{forward,back}_project_matrix_free_host[_f32]): pinned host x / y in,
+    host y / x out, H2D and D2H copies inside the timed region. A x and A^T y
+    are independent calls: a user thread each, one context (scratch, status
+    word, non-blocking stream) per thread, so one call's copies overlap the
+    other's kernels."""
+    import ctypes
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2511_12235_b200 import Context, _lib
+    L = _lib.lib()
+    f32 = args.dtype == "f32"
+    npdt, es = (np.float32, 4) if f32 else (np.float64, 8)
+    tdt = torch.float32 if f32 else torch.float64
+    fwd = L.ctsm_forward_project_matrix_free_host_f32 if f32 else L.ctsm_forward_project_matrix_free_host
+    bwd = L.ctsm_back_project_matrix_free_host_f32 if f32 else L.ctsm_back_project_matrix_free_host
+    xh = torch.from_numpy(x_h.astype(npdt)).pin_memory()
+    yh = torch.from_numpy(y_h.astype(npdt)).pin_memory()
+    yo = torch.empty(g.n_measurements, dtype=tdt).pin_memory()
+    xo = torch.empty(g.n_voxels, dtype=tdt).pin_memory()
+    cg = g.to_c()
+    ctx_b = Context(local)
+    pool = ThreadPoolExecutor(max_workers=1)
+
+    def bwd_call():
+        _lib.check(bwd(ctx_b.handle, ctypes.byref(cg), ctypes.c_void_p(yh.data_ptr()),
+                       ctypes.c_void_p(xo.data_ptr())))
+
+    def e2e_step():
+        fut = pool.submit(bwd_call)
+        _lib.check(fwd(ctx.handle, ctypes.byref(cg), ctypes.c_void_p(xh.data_ptr()),
+                       ctypes.c_void_p(yo.data_ptr())))
+        fut.result()
+
+    n_warm = max(1, min(args.warmup, 3))
+    n_steps = args.steps if g.is_2d() else min(args.steps, 5)
+    for _ in range(n_warm):
+        e2e_step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(n_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    te = (time.perf_counter() - t0) / n_steps
+    pool.shutdown()
+    ctx_b.close()
+    return {"value": updates_per_step / te, "unit": "updates/s",
+            "h2d_bytes_per_step": es * (g.n_voxels + g.n_measurements),
+            "d2h_bytes_per_step": es * (g.n_measurements + g.n_voxels),
+            "ms_per_step": te * 1e3, "steps": n_steps,
+            "calls": ("ctsm_forward_project_matrix_free_host" + ("_f32" if f32 else "") +
+                      " and ctsm_back_project_matrix_free_host" + ("_f32" if f32 else "") +
+                      " (pinned host buffers), issued concurrently from two host threads")}
+
+
 def run_ours(args):
     import torch
-    import torch.distributed as dist
 
     from paper_2511_12235_b200 import CONFIGS, Context, _lib
+    from paper_2511_12235_b200.dist import angle_shard
     from paper_2511_12235_b200.phantoms import phantom_for, uniform_sinogram
     from paper_2511_12235_b200.projector import (back_project_matrix_free,
                                                  forward_project_matrix_free)
@@ -224,9 +506,7 @@ def run_ours(args):
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
-    if world > 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+    dist = init_dist(torch, dev)
     cfg = args.config
     g = CONFIGS[cfg]
     tdt = torch.float64 if args.dtype == "f64" else torch.float32
@@ -237,7 +517,6 @@ def run_ours(args):
     y = torch.from_numpy(y_h).to(tdt).to(dev)
     yout = torch.zeros(g.n_measurements, dtype=tdt, device=dev)
     xout = torch.zeros(g.n_voxels, dtype=tdt, device=dev)
-    from paper_2511_12235_b200.dist import angle_shard
     shard = angle_shard(g, rank, world)  # orbit shards for quarter-turn symmetric scans
     flush = torch.empty(256 << 20, dtype=torch.int8, device=dev)  # > 126 MB L2
 
@@ -291,196 +570,51 @@ def run_ours(args):
     updates_per_step = 2.0 * nnz_live
     value = updates_per_step / (ms * 1e-3)
 
-    # ---- end-to-end through the reference-facing host-buffer C-ABI ----
     e2e = None
-    if not args.no_e2e and world == 1 and args.dtype == "f64":
-        import ctypes
-        L = _lib.lib()
-        xh = torch.from_numpy(x_h.astype(np.float64)).pin_memory()
-        yh = torch.from_numpy(y_h).pin_memory()
-        yo = torch.empty(g.n_measurements, dtype=torch.float64).pin_memory()
-        xo = torch.empty(g.n_voxels, dtype=torch.float64).pin_memory()
-        cg = g.to_c()
-        # A x and A^T y are independent calls: a user thread each, one
-        # context (scratch, status word, non-blocking stream) per thread, so
-        # one call's host<->device copies overlap the other's kernels
-        from concurrent.futures import ThreadPoolExecutor
-        from paper_2511_12235_b200.projector import Context as _Ctx
-        ctx_b = _Ctx(local)
-        pool = ThreadPoolExecutor(max_workers=1)
-
-        def bwd_call():
-            _lib.check(L.ctsm_back_project_matrix_free_host(ctx_b.handle, ctypes.byref(cg),
-                                                            ctypes.c_void_p(yh.data_ptr()),
-                                                            ctypes.c_void_p(xo.data_ptr())))
-
-        def e2e_step():
-            fut = pool.submit(bwd_call)
-            _lib.check(L.ctsm_forward_project_matrix_free_host(ctx.handle, ctypes.byref(cg),
-                                                               ctypes.c_void_p(xh.data_ptr()),
-                                                               ctypes.c_void_p(yo.data_ptr())))
-            fut.result()
-        for _ in range(max(1, args.warmup)):
-            e2e_step()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            e2e_step()
-        torch.cuda.synchronize()
-        te = (time.perf_counter() - t0) / args.steps
-        e2e = {"value": updates_per_step / te, "unit": "updates/s",
-               "h2d_bytes_per_step": 8 * (g.n_voxels + g.n_measurements),
-               "d2h_bytes_per_step": 8 * (g.n_measurements + g.n_voxels),
-               "ms_per_step": te * 1e3,
-               "calls": "ctsm_forward_project_matrix_free_host and ctsm_back_project_matrix_free_host "
-                        "(pinned host buffers), issued concurrently from two host threads"}
-        pool.shutdown()
-        ctx_b.close()
+    if not args.no_e2e and world == 1:
+        del yout, xout
+        e2e = e2e_projection_pair(torch, args, g, x_h, y_h, ctx, local, updates_per_step)
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
-    peak = measure_dfma_peak(torch)
-    # roofline of the dominant kernel (the slower of fwd / bwd). Units are the
-    # pixel/voxel-angle weight evaluations the kernel actually performs: with
-    # the dihedral (quarter-turn) symmetry each evaluation serves 8 (4)
-    # pixel-angles of the workload, and in 3D the z mirror doubles that, so
-    # units = voxel-angles / reuse (the workload-equivalent figure is reported
-    # beside it).
-    from paper_2511_12235_b200.projector import symmetry_order
-    reuse = symmetry_order(g)
-    npix = g.n_x * g.n_y * g.n_z
-    if reuse == 8:  # base angles 0..n/8 (the two self-symmetric ones reuse 4x)
-        n_eval = g.n_angles // 8 + 1
-    elif reuse == 4:
-        n_eval = g.n_angles // 4
-    else:
-        n_eval = g.n_angles
-    units = npix * n_eval / (world if world > 1 else 1)
-    reuse = g.n_angles / n_eval
-    if not g.is_2d() and symmetry_order(g) > 1 and g.n_z % 2 == 0:
-        # z mirror of the symmetric 3D kernels: only the lower half of every
-        # voxel column is evaluated, each weight also serves voxel n_z-1-iz
-        units /= 2
-        reuse *= 2
-    per_unit = F_REF["2d"] if g.is_2d() else F_REF["3d"]
-    dom_ms = max(ms_f, ms_b)
-    achieved = units * per_unit / (dom_ms * 1e-3) / 1e12
-    suffix = {8: "_d8", 4: "_sym"}.get(symmetry_order(g), "")
-    kname = ("fwd2d" if ms_f >= ms_b else "bwd2d") + suffix
-    if not g.is_2d():
-        kname = kname.replace("2d", "3d")
-    # DRAM traffic of the same kernel and workload from one committed
-    # `ncu --set full` capture (profiles/ncu_kernels.json, tools/ncu_kernels.py)
-    traffic, ncu_pipe = None, None
-    try:
-        ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_kernels.json")))
-        tname = "double" if args.dtype == "f64" else "float"
-        # kernel names as ncu prints them: fwd2d_d8_kernel<double>,
-        # bwd2d_d8_kernel<float, 1>, fwd3d_sym_kernel<float, 8>, ...
-        kbase = kname.replace("3d_d8", "3d_sym")
-        prefix = f"{cfg}_{args.dtype}:{kbase}_kernel<{tname}"
-        hits = [k for k in sorted(ncu) if k == prefix + ">" or k.startswith(prefix + ",")]
-        if hits:
-            traffic = ncu[hits[0]]["dram_bytes"]
-            ncu_pipe = ncu[hits[0]].get("fp64_pipe_pct")
-    except (OSError, ValueError, KeyError):
-        pass
-    roof = {"bound": "fp64", "kernel": kname,
-            "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": (achieved / peak) if peak else None, "traffic": traffic,
-            "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/ncu_kernels.json)",
-            "ncu_fp64_pipe_active_pct": ncu_pipe,
-            "peak_source": "measured DFMA microkernel (MEASURED_PEAKS.json has no FP64 entry)",
-            "work_per_unit": f"{per_unit:g} FP64 flops per weight evaluation (reference op count, SURVEY.md §8(d))",
-            "units_per_launch": units, "symmetry_reuse": reuse,
-            "workload_equivalent_TFLOPs": achieved * reuse,
-            "fwd_ms": ms_f, "bwd_ms": ms_b}
     line = {
         "metric": "voxel-ray updates/s (A x + A^T y)",
-        "value": value,
-        "unit": "updates/s",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": ms,
-        "higher_is_better": True,
-        "scaling": "strong",
-        "vs_baseline": None,
-        "dtype": args.dtype,
-        "data": "synthetic",
-        "config": {"workload": f"{cfg}: BASELINE.json configs[{cfg[1]}] matrix-free A x + A^T y",
-                   "parallelism": f"angle-shard x{world}", "l2": "flushed (256 MB write) before each step"},
-        "roofline": roof,
+        "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": workload_config(args, world),
+        "roofline": fp64_roofline(torch, g, cfg, args.dtype, world, ms_f, ms_b),
         "updates_per_projection": nnz_live,
         "nnz_reference": NNZ.get(cfg),  # reference nnz; the live count may differ by noise-band (<1e-13) entries
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk,
     }
-    if world == 1 and os.environ.get("CTSM_BENCH_NO_CPU") is None:
-        line["cpu_baseline"] = cpu_baseline_quick(cfg)
+    if world == 1 and not args.no_cpu and os.environ.get("CTSM_BENCH_NO_CPU") is None:
+        line["cpu_baseline"] = cpu_baseline_proj(cfg)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def cpu_baseline_quick(cfg):
-    """The reference's CPU path on a bounded sample (rank 0, N=1)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    try:
-        import pyoracle
-        from paper_2511_12235_b200 import CONFIGS
-        from paper_2511_12235_b200.phantoms import phantom_for, uniform_sinogram
-    except Exception as e:  # pragma: no cover
-        return {"error": str(e)}
-    variant = "ref_glibc" if pyoracle.available("ref_glibc") else "port_glibc"
-    if not pyoracle.available(variant):
-        return {"error": "oracle not built"}
-    orc = pyoracle.load(variant)
-    g = CONFIGS[cfg]
-    cores = os.cpu_count() or 1
-    x = phantom_for(cfg, g)
-    y = uniform_sinogram(g.n_measurements, 12346)
-    # bounded sample sized to ~10 s of CPU work: time 2 angles, then scale
-    probe = np.array([0, g.n_angles // 2], np.int32)
-    t0 = time.perf_counter()
-    orc.forward_mf_angles(g, probe, x, cores)
-    orc.back_mf_angles(g, probe, y, cores)
-    tau = time.perf_counter() - t0  # ~ one angle's fwd+bwd (the 2 probes run in parallel)
-    # the reference parallelises over angles: use >= one angle per core
-    n_sample = int(min(g.n_angles, cores * max(1, int(10.0 / max(tau, 1e-6)))))
-    angles = np.linspace(0, g.n_angles, n_sample, endpoint=False).astype(np.int32)
-    t0 = time.perf_counter()
-    orc.forward_mf_angles(g, angles, x, cores)
-    orc.back_mf_angles(g, angles, y, cores)
-    t = time.perf_counter() - t0
-    t_full = t * g.n_angles / angles.size
-    return {"value": 2.0 * NNZ.get(cfg, NNZ_EST.get(cfg, 0.0)) / t_full, "unit": "updates/s", "cores": cores,
-            "kind": "reference" if variant == "ref_glibc" else "port",
-            "sample": f"fwd+bwd over {angles.size} of {g.n_angles} strided angles ({t:.1f} s), extrapolated"}
-
-
 def run_sirt(args):
     """SIRT iterations (x <- x + C A^T (R (y - A x))), angle-sharded; one step =
-    one iteration = one A x + one A^T r + the all-reduce. The setup (y = A
-    x_true + noise, R = 1/(A 1), C = 1/(A^T 1)) runs once, untimed."""
+    one iteration = one A x + the fused residual (K8) + one A^T r + the
+    all-reduce + the update. The setup (y = A x_true + noise, R = 1/(A 1),
+    C = 1/(A^T 1)) runs once, untimed."""
     import torch
-    import torch.distributed as dist
 
     from paper_2511_12235_b200 import CONFIGS, Context, _lib
-    from paper_2511_12235_b200.dist import angle_shard
+    from paper_2511_12235_b200.dist import SirtState, angle_shard
     from paper_2511_12235_b200.phantoms import phantom_for
-    from paper_2511_12235_b200.projector import (back_project_matrix_free,
-                                                 forward_project_matrix_free)
+    from paper_2511_12235_b200.projector import forward_project_matrix_free
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
-    if world > 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+    dist = init_dist(torch, dev)
     cfg = args.config
     g = CONFIGS[cfg]
     tdt = torch.float64 if args.dtype == "f64" else torch.float32
@@ -490,38 +624,22 @@ def run_sirt(args):
     x_true = torch.from_numpy(phantom_for(cfg, g, dtype=np.float32)).to(tdt).to(dev)
     y = torch.zeros(g.n_measurements, dtype=tdt, device=dev)
     forward_project_matrix_free(g, "consistent", 1, x_true, angles=shard, out=y)
+    del x_true
     ymax = y.abs().max()
     if world > 1:
         dist.all_reduce(ymax, op=dist.ReduceOp.MAX)
     # noise on every row (a rank reads only its own rows: R is zero elsewhere)
     gen = torch.Generator(device=dev).manual_seed(12347 + rank)
-    y += 0.01 * ymax * torch.randn(y.numel(), dtype=tdt, device=dev, generator=gen)
-    R = torch.zeros_like(y)
-    forward_project_matrix_free(g, "consistent", 1, torch.ones_like(x_true), angles=shard, out=R)
-    R = torch.where(R != 0, 1.0 / R, torch.zeros_like(R))  # rows of other ranks stay 0
-    Cc = back_project_matrix_free(g, "consistent", 1, torch.ones_like(y), angles=shard)
-    if world > 1:
-        dist.all_reduce(Cc)
-    Cc = torch.where(Cc != 0, 1.0 / Cc, torch.zeros_like(Cc))
+    y.add_(torch.randn(y.numel(), dtype=tdt, device=dev, generator=gen), alpha=float(0.01 * ymax))
+    state = SirtState(g, y)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup0
-    x = torch.zeros_like(x_true)
-    ax = torch.zeros_like(y)
-    r = torch.zeros_like(y)
-    bp = torch.empty_like(x)
+    x = torch.zeros(g.n_voxels, dtype=tdt, device=dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-
-    def iteration():
-        forward_project_matrix_free(g, "consistent", 1, x, angles=shard, out=ax)
-        torch.mul(R, y - ax, out=r)  # R = 0 on rows of other ranks
-        back_project_matrix_free(g, "consistent", 1, r, angles=shard, out=bp)
-        if world > 1:
-            dist.all_reduce(bp)
-        x.add_(Cc * bp)
 
     clocks = ClockSampler(local, not args.no_clocks)
     for _ in range(args.warmup):
-        iteration()
+        state.step(x)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -531,7 +649,7 @@ def run_sirt(args):
     for _ in range(args.steps):
         torch.cuda.synchronize()
         ev0.record()
-        iteration()
+        state.step(x)
         ev1.record()
         torch.cuda.synchronize()
         ms_total += ev0.elapsed_time(ev1)
@@ -548,38 +666,72 @@ def run_sirt(args):
         dist.all_reduce(msx, op=dist.ReduceOp.MAX)
         cnt = torch.cat([upd, msx])
     nnz_live, ms = int(cnt[0].item()), float(cnt[1].item())
+    updates_per_step = 2.0 * nnz_live
+
+    # ---- end to end: a user's solve through the host-buffer path: y from
+    # pinned host memory, `steps` iterations, x back to the host; per iteration
+    e2e = None
+    if not args.no_e2e and world == 1:
+        yh = y.cpu().pin_memory()
+        xh = torch.empty(g.n_voxels, dtype=tdt).pin_memory()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        y.copy_(yh, non_blocking=True)
+        x.zero_()
+        for _ in range(args.steps):
+            state.step(x)
+        xh.copy_(x, non_blocking=True)
+        torch.cuda.synchronize()
+        te = (time.perf_counter() - t0) / args.steps
+        es = 4 if args.dtype == "f32" else 8
+        e2e = {"value": updates_per_step / te, "unit": "updates/s",
+               "h2d_bytes_per_step": es * g.n_measurements / args.steps,
+               "d2h_bytes_per_step": es * g.n_voxels / args.steps, "ms_per_step": te * 1e3,
+               "calls": f"one solve of {args.steps} iterations: y from pinned host memory, x back "
+                        "to the host; bytes and time per iteration"}
     if rank == 0:
         # residual over the rows rank 0 solves for (R != 0; empty rows excluded)
-        resid = float((torch.where(R != 0, y - ax, torch.zeros_like(ax)) ** 2).sum().sqrt())
+        ax = torch.zeros_like(y)
+        forward_project_matrix_free(g, "consistent", 1, x, angles=shard, out=ax)
+        resid = float((torch.where(state.R != 0, y - ax, torch.zeros_like(ax)) ** 2).sum().sqrt())
+        del ax
+        # the iteration is one forward and one back-projection launch; the
+        # roofline is the slower projection's, taken as half the iteration
         line = {
             "metric": "voxel-ray updates/s (SIRT iterations)",
-            "value": 2.0 * nnz_live / (ms * 1e-3),
-            "unit": "updates/s",
+            "value": updates_per_step / (ms * 1e-3), "unit": "updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": f"{cfg}: BASELINE.json configs[{cfg[1]}] SIRT (one iteration per step)",
-                       "parallelism": f"angle-shard x{world}", "setup_s": t_setup,
+            "config": {**workload_config(args, world), "setup_s": t_setup,
                        "iterations_total": args.warmup + args.steps},
+            "roofline": {**fp64_roofline(torch, g, cfg, args.dtype, world, ms / 2, ms / 2),
+                         "note": "one A x and one A^T r launch per iteration; kernel time taken as "
+                                 "half the iteration (the elementwise K8 steps are < 1 %)"},
             "updates_per_projection": nnz_live,
             "rank0_residual_norm": resid,
+            "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk,
         }
+        if world == 1 and not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline_proj(cfg)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
 def run_csr(args):
-    """K1/K2 consistent CSR assembly (bit-exact path) + K3 SpMV on one GPU.
+    """K1/K2 consistent CSR assembly (bit-exact path) + K3/K4 on one GPU.
     One step = build_system_matrix (count, scan, fill, per-row sort) of the
-    whole config; metric SM weights/s = nnz / build time. K3 A x on the built
-    matrix is timed separately (HBM roofline: 12 B/nnz + 16 B/row)."""
+    whole config; metric SM weights/s = nnz / build time. K3 A x and K4 A^T y
+    on the built matrix are timed separately (HBM roofline: 12 B/nnz + 16
+    B/row)."""
     import torch
 
     from paper_2511_12235_b200 import CONFIGS, _lib
-    from paper_2511_12235_b200.phantoms import phantom_for
-    from paper_2511_12235_b200.projector import build_system_matrix, forward_project
+    from paper_2511_12235_b200.phantoms import phantom_for, uniform_sinogram
+    from paper_2511_12235_b200.projector import (back_project, build_system_matrix,
+                                                 forward_project)
 
     cfg = args.config
     g = CONFIGS[cfg]
@@ -608,6 +760,27 @@ def run_csr(args):
     clocks.mark(False)
     ms /= args.steps
     nnz = w.nnz()
+    # end to end: the matrix built AND copied to host memory (the reference
+    # returns a host SparseSystemMatrix), where it fits a bounded run
+    e2e = None
+    csr_bytes = 12 * nnz + 8 * (w.n_rows + 1)
+    if not args.no_e2e and csr_bytes < (8 << 30):
+        hrs = torch.empty(w.n_rows + 1, dtype=torch.int64).pin_memory()
+        hcol = torch.empty(nnz, dtype=torch.int32).pin_memory()
+        hval = torch.empty(nnz, dtype=torch.float64).pin_memory()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            w2 = build_system_matrix(g, memory_budget_bytes=budget)
+            hrs.copy_(w2.row_start, non_blocking=True)
+            hcol.copy_(w2.col, non_blocking=True)
+            hval.copy_(w2.val, non_blocking=True)
+            torch.cuda.synchronize()
+            del w2
+        te = (time.perf_counter() - t0) / args.steps
+        e2e = {"value": nnz / te, "unit": "weights/s", "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": csr_bytes, "ms_per_step": te * 1e3,
+               "calls": "build_system_matrix + the CSR copied to pinned host memory"}
     x = torch.from_numpy(phantom_for(cfg, g, dtype=np.float64 if g.is_2d() else np.float32)).double().to(dev)
     for _ in range(3):
         forward_project(w, x)
@@ -620,8 +793,6 @@ def run_csr(args):
         torch.cuda.synchronize()
         ms_spmv += ev0.elapsed_time(ev1) / 5
     # K4 (reference back_project, projector.cpp:219-233) on a U[0, 1) sinogram
-    from paper_2511_12235_b200.projector import back_project
-    from paper_2511_12235_b200.phantoms import uniform_sinogram
     yb = torch.from_numpy(uniform_sinogram(w.n_rows, 12346)).to(dev)
     for _ in range(3):
         back_project(w, yb)
@@ -638,13 +809,30 @@ def run_csr(args):
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     gbs = bytes_spmv / (ms_spmv * 1e-3) / 1e9
+    # FP64 roofline of the emission kernel (K1 / K2): every
+    # pixel/voxel-angle is evaluated (no symmetry on the bit-exact path), F
+    # reference operations each, against the measured DFMA instruction rate.
+    peak_flops = measure_dfma_peak(torch)
+    per_unit = F_REF["2d"] if g.is_2d() else F_REF["3d"]
+    units = float(g.n_x * g.n_y * g.n_z) * g.n_angles
+    achieved = units * per_unit / (ms * 1e-3) / 1e12
+    roof = {"bound": "fp64", "kernel": "csr2d_kernel" if g.is_2d() else "csr3d_kernel",
+            "achieved": achieved, "peak": peak_flops / 2 if peak_flops else None,
+            "unit": "T FP64 op/s (arithmetic instructions, FMA = 1 op; SURVEY.md §8(d))",
+            "frac": achieved / (peak_flops / 2) if peak_flops else None,
+            "traffic": None,
+            "work_per_unit": f"{per_unit:g} FP64 ops per pixel/voxel-angle (reference op count; "
+                             "the crmath calls are excluded like the reference's libm calls)",
+            "units_per_launch": units,
+            "note": "whole build (all emission passes, scan, sort) taken as the kernel time"}
     line = {
         "metric": "SM weights/s (consistent CSR assembly)", "value": nnz / (ms * 1e-3),
         "unit": "weights/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg}: BASELINE.json configs[{cfg[1]}] build_system_matrix"},
+        "config": workload_config(args, 1),
         "nnz": nnz, "nnz_reference": NNZ.get(cfg),
+        "roofline": roof,
         "spmv": {"ms": ms_spmv, "GB/s": gbs, "algorithmic_bytes": bytes_spmv,
                  "hbm_peak_gbs": peaks.get("hbm_gbs"), "frac": gbs / peaks.get("hbm_gbs", 6650.0)},
         "spmv_t": {"ms": ms_spmvt, "GB/s": bytes_spmv / (ms_spmvt * 1e-3) / 1e9,
@@ -652,13 +840,24 @@ def run_csr(args):
                    "frac": bytes_spmv / (ms_spmvt * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
                    "note": "back_project: int64 fixed-point scatter (deterministic) with the matrix's "
                            "column-sum bound, computed once per matrix (cached, outside the timed calls)"},
+        "e2e": e2e,
         "gpu_launches": int(launches), "clocks": clk,
     }
+    if not args.no_cpu:
+        del w, x, yb
+        try:
+            n_ref, t_ref, desc, variant, cores = csr_reference_sample(cfg, 12.0)
+            line["cpu_baseline"] = {"value": n_ref / t_ref, "unit": "weights/s", "cores": cores,
+                                    "kind": "reference" if variant == "ref_glibc" else "port",
+                                    "sample": desc, **host_info()}
+        except Exception as e:  # pragma: no cover
+            line["cpu_baseline"] = {"error": repr(e)}
     print(json.dumps(line), flush=True)
 
 
 def main():
     args = parse()
+    relaunch_if_needed(args)
     if args.impl == "reference":
         run_reference(args)
     elif args.mode == "sirt":

@@ -153,6 +153,12 @@ class Oracle:
                                                       ctypes.c_int, _P, _P, ctypes.c_int]
             L.ref_back_mf_angles_slabs.argtypes = [_P, _P, ctypes.c_int, ctypes.c_int,
                                                    ctypes.c_int, _P, _P, ctypes.c_int]
+        # bounded samples for bench.py's reference arm (ref_* variants only)
+        self.has_pair_sample = hasattr(L, "ref_mf_pair_sample")
+        if self.has_pair_sample:
+            L.ref_mf_pair_sample.argtypes = [_P, _P, ctypes.c_int, _P, ctypes.c_int, _P, _P, _P, _P,
+                                             ctypes.c_int]
+            L.ref_csr_angle_sample.argtypes = [_P, _P, ctypes.c_int, _P, ctypes.c_int]
         L.ref_angle_column_sums.argtypes = [_P, ctypes.c_int, _P]
         L.ref_line_weights.argtypes = [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_int, _P, _P, ctypes.c_long]
@@ -356,6 +362,44 @@ class Oracle:
         self._check(self.lib.ref_back_mf_angles_slabs(p, _ptr(a), a.size, zlo, zhi, _ptr(yr),
                                                       _ptr(x), threads))
         return x
+
+    def mf_pair_sample(self, g, angles, slabs, x: np.ndarray, y: np.ndarray, threads: int = 1):
+        """One bounded A x + A^T y sample: the listed angles x the listed slabs
+        (z planes in 3D, pixel rows in 2D), weights evaluated once per product
+        as the reference does -> (updates applied, checksum). ref_* variants
+        use the reference's own weight functions (ref_shim.cpp); the ports fall
+        back to the slab restatements."""
+        og, p = self._g(g)
+        a = np.ascontiguousarray(angles, np.int32)
+        sl = np.ascontiguousarray(slabs, np.int32)
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.ascontiguousarray(y, np.float64)
+        if self.has_pair_sample:
+            cs = ctypes.c_double(0.0)
+            nu = ctypes.c_uint64(0)
+            self._check(self.lib.ref_mf_pair_sample(p, _ptr(a), a.size, _ptr(sl), sl.size, _ptr(x),
+                                                    _ptr(y), ctypes.byref(cs), ctypes.byref(nu),
+                                                    threads))
+            return int(nu.value), float(cs.value)
+        if g.n_z == 1:
+            raise NotImplementedError("2D slab samples need the ref_* oracle")
+        rpa = g.n_det_y * g.n_det_z
+        yrows = np.concatenate([y[int(k) * rpa:(int(k) + 1) * rpa] for k in a])
+        cs, nu = 0.0, 0
+        for z in sl:
+            yy = self.forward_mf_angles_slabs(g, a, int(z), int(z) + 1, x, threads)
+            xx = self.back_mf_angles_slabs(g, a, int(z), int(z) + 1, yrows, threads)
+            cs += float(yy.sum() + xx.sum())
+        return nu, cs
+
+    def csr_angle_sample(self, g, angles, threads: int = 1) -> int:
+        """build_angle_block (projector.cpp:92-104) of the listed angles, one
+        angle per worker -> entries built (ref_* variants only)."""
+        og, p = self._g(g)
+        a = np.ascontiguousarray(angles, np.int32)
+        nnz = ctypes.c_uint64(0)
+        self._check(self.lib.ref_csr_angle_sample(p, _ptr(a), a.size, ctypes.byref(nnz), threads))
+        return int(nnz.value)
 
     def sirt(self, g, y: np.ndarray, x0: np.ndarray, iters: int, threads: int = 1) -> np.ndarray:
         og, p = self._g(g)

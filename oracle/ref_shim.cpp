@@ -301,52 +301,52 @@ int ref_back_mf_angles(const RefGeom* rg, const int32_t* angles, int n_sel, cons
             } return 0;)
 }
 
-// Bounded sample of one A x + A^T y step for bench.py's reference arm: work
-// items are (listed angle, z-slab band) pairs spread over `threads` workers;
-// each item walks the voxels of its band with the reference's own
-// voxel_volume_factors / pixel_area_factors (weights3d.hpp:90,
-// weights2d.hpp:31) in projector.cpp:53-69's order and applies every weight
-// twice: y[r] += w x[c] into the item's angle block (forward_project_matrix_free,
-// projector.cpp:249-252) and x_out[c] += w y[r] (the a16 adjoint). Slab bands
-// are disjoint, so the reference's per-angle parallelism (ordered_parallel_for,
+// Bounded sample of one A x + A^T y step for bench.py's reference arm and
+// cpu_baseline. The reference's API cannot bound an angle block, so the work
+// items here are (listed angle, listed slab) pairs spread over `threads`
+// workers: a slab is one z plane of voxels (3D) or one pixel row (2D). Each
+// item walks its voxels in projector.cpp:53-69's order with the reference's
+// own voxel_volume_factors / pixel_area_factors (weights3d.hpp:90,
+// weights2d.hpp:31) TWICE, as a reference user would for the two products:
+// pass 1 is forward_project_matrix_free's accumulation y[r] += w x[c] into the
+// item's angle block (projector.cpp:249-252), pass 2 the a16 adjoint
+// x_out[c] += w y[r], re-evaluating the weights. Slabs are disjoint, so the
+// reference's per-angle parallelism (ordered_parallel_for,
 // projector.cpp:114-140) is kept while a few angles still use every core.
 // *updates = weights applied (one per weight and direction).
-int ref_mf_pair_sample(const RefGeom* rg, const int32_t* angles, int n_sel, int zlo, int zhi,
-                       int bands, const double* x, const double* y, double* checksum,
-                       uint64_t* updates, int threads) {
+int ref_mf_pair_sample(const RefGeom* rg, const int32_t* angles, int n_sel,
+                       const int32_t* slabs, int n_slabs, const double* x, const double* y,
+                       double* checksum, uint64_t* updates, int threads) {
   REF_GUARD(
       const ctsm::ScanGeometry g = to_g(rg); g.validate();
-      const bool two_d = g.is_2d(); const int n_slab = two_d ? g.n_y : g.n_z;
-      zlo = std::max(0, zlo); zhi = std::min(n_slab, zhi); bands = std::max(1, bands);
+      const bool two_d = g.is_2d();
       const uint64_t rpa = (uint64_t)g.n_det_y * g.n_det_z;
-      const int items = n_sel * bands;
+      const int items = n_sel * n_slabs;
       std::vector<double> sums(items, 0.0);
       std::vector<uint64_t> counts(items, 0);
       const auto raster = [&](int m_y, int m_z) {
         return (uint32_t)((m_z + g.n_det_z / 2) * g.n_det_y + (m_y + g.n_det_y / 2));
       };
       parallel_range(items, threads, [&](int it) {
-        const int k = it / bands, b = it % bands;
-        const int lo = zlo + (int)((int64_t)(zhi - zlo) * b / bands);
-        const int hi = zlo + (int)((int64_t)(zhi - zlo) * (b + 1) / bands);
+        const int k = it % n_sel, sl = slabs[it / n_sel];  // angles interleaved over workers
         const double phi = g.angle(angles[k]);
         const double* yb = y + (uint64_t)angles[k] * rpa;
-        std::vector<double> block(rpa, 0.0);
         const uint64_t plane = two_d ? (uint64_t)g.n_x : (uint64_t)g.n_x * g.n_y;
-        const uint64_t base = (uint64_t)lo * plane;
-        std::vector<double> xp((uint64_t)(hi - lo) * plane, 0.0);  // the angle's partial volume
+        const uint64_t base = (uint64_t)sl * plane;
+        std::vector<double> block(rpa, 0.0);   // the angle's sinogram block (pass 1)
+        std::vector<double> xp(plane, 0.0);    // the angle's partial volume slab (pass 2)
         uint64_t n = 0;
-        for (int sl = lo; sl < hi; ++sl) {
+        for (int pass = 0; pass < 2; ++pass) {
+          const auto apply = [&](uint32_t r, uint32_t c, double w) {
+            if (pass == 0) block[r] += w * x[c]; else xp[c - base] += w * yb[r];
+            ++n;
+          };
           if (two_d) {
             for (int ix = 0; ix < g.n_x; ++ix) {
               const ctsm::VoxelIndex v{ix, sl, 0};
               const uint32_t c = (uint32_t)ctsm::voxel_column(g, v);
-              for (const auto& cw : ctsm::pixel_area_factors(v, phi, g)) {
-                const uint32_t r = raster(cw.m_y, 0);
-                block[r] += cw.w * x[c];
-                xp[c - base] += cw.w * yb[r];
-                ++n;
-              }
+              for (const auto& cw : ctsm::pixel_area_factors(v, phi, g))
+                apply(raster(cw.m_y, 0), c, cw.w);
             }
             continue;
           }
@@ -354,23 +354,49 @@ int ref_mf_pair_sample(const RefGeom* rg, const int32_t* angles, int n_sel, int 
             for (int ix = 0; ix < g.n_x; ++ix) {
               const ctsm::VoxelIndex v{ix, iy, sl};
               const uint32_t c = (uint32_t)ctsm::voxel_column(g, v);
-              for (const auto& vw : ctsm::voxel_volume_factors(v, phi, g)) {
-                const uint32_t r = raster(vw.m_y, vw.m_z);
-                block[r] += vw.w * x[c];
-                xp[c - base] += vw.w * yb[r];
-                ++n;
-              }
+              for (const auto& vw : ctsm::voxel_volume_factors(v, phi, g))
+                apply(raster(vw.m_y, vw.m_z), c, vw.w);
             }
         }
         double bs = 0.0;
         for (double v : block) bs += v;
         for (double v : xp) bs += v;
         sums[it] = bs;
-        counts[it] = 2 * n;
+        counts[it] = n;
       });
       double cs = 0.0; uint64_t nu = 0;
       for (int i = 0; i < items; ++i) { cs += sums[i]; nu += counts[i]; }
       *checksum = cs; *updates = nu; return 0;)
+}
+
+// Bounded sample of build_system_matrix for bench.py's CSR cpu_baseline (C2's
+// 55 GB matrix does not fit a bounded run): the listed angles' blocks, one
+// angle per worker as ordered_parallel_for does (projector.cpp:114-140), each
+// built as build_angle_block does (projector.cpp:92-104): per-row entry
+// vectors filled through detail::angle_block_entries, then a stable sort by
+// column. *nnz = entries of the listed angle blocks.
+int ref_csr_angle_sample(const RefGeom* rg, const int32_t* angles, int n_sel, uint64_t* nnz,
+                         int threads) {
+  REF_GUARD(
+      const ctsm::ScanGeometry g = to_g(rg); g.validate();
+      const uint64_t rpa = (uint64_t)g.n_det_y * g.n_det_z;
+      std::vector<uint64_t> counts(n_sel, 0);
+      parallel_range(n_sel, threads, [&](int k) {
+        std::vector<std::vector<std::pair<uint32_t, double>>> rows(rpa);
+        ctsm::detail::angle_block_entries(
+            g, ctsm::MatrixMode::consistent, 1, angles[k],
+            [&](uint32_t r, uint32_t c, double w) { rows[r].emplace_back(c, w); });
+        uint64_t n = 0;
+        for (auto& row : rows) {
+          std::stable_sort(row.begin(), row.end(),
+                           [](const auto& a, const auto& b) { return a.first < b.first; });
+          n += row.size();
+        }
+        counts[k] = n;
+      });
+      uint64_t total = 0;
+      for (uint64_t c : counts) total += c;
+      *nnz = total; return 0;)
 }
 
 int ref_back_project_matrix_free(const RefGeom* rg, const double* y, double* x, int threads) {

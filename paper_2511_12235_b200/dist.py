@@ -109,42 +109,91 @@ def sharded_back_project(g: ScanGeometry, y: torch.Tensor, group=None,
     return part
 
 
-def _invert_nonzero(v: torch.Tensor) -> torch.Tensor:
-    out = torch.zeros_like(v)
-    nz = v != 0
-    out[nz] = 1.0 / v[nz]
-    return out
+class DeviceElementwise:
+    """K7/K8 elementwise steps of SIRT through the C-ABI kernels
+    (ctsm_invert_nonzero, ctsm_sirt_residual, ctsm_sirt_update): the product
+    path on CUDA tensors. R is zero on the rows a rank does not own, so the
+    residual kernel runs over the full sinogram and leaves those rows zero."""
+
+    def invert_nonzero(self, g, v: torch.Tensor) -> torch.Tensor:
+        from . import _lib
+        from .projector import Context, _dev_ptr, _dtype_code, _stream
+        ctx = Context.get(v.device.index)
+        _lib.check(_lib.lib().ctsm_invert_nonzero(ctx.handle, _dtype_code(v), v.numel(),
+                                                  _dev_ptr(v), _stream(ctx.device)))
+        return v
+
+    def residual(self, g, y: torch.Tensor, rinv: torch.Tensor, ax: torch.Tensor) -> torch.Tensor:
+        """ax <- rinv * (y - ax) in place; returns ax."""
+        import ctypes
+        from . import _lib
+        from .projector import Context, _dev_ptr, _dtype_code, _stream
+        ctx = Context.get(ax.device.index)
+        cg = g.to_c()
+        _lib.check(_lib.lib().ctsm_sirt_residual(ctx.handle, ctypes.byref(cg), _dtype_code(ax), 0,
+                                                 g.n_angles, 1, _dev_ptr(y), _dev_ptr(rinv),
+                                                 _dev_ptr(ax), _stream(ctx.device)))
+        return ax
+
+    def update(self, g, cinv: torch.Tensor, bp: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
+        """x += cinv * bp in place."""
+        from . import _lib
+        from .projector import Context, _dev_ptr, _dtype_code, _stream
+        ctx = Context.get(x.device.index)
+        _lib.check(_lib.lib().ctsm_sirt_update(ctx.handle, _dtype_code(x), x.numel(), _dev_ptr(cinv),
+                                               _dev_ptr(bp), _dev_ptr(x), _stream(ctx.device)))
+        return x
+
+
+class SirtState:
+    """Per-rank SIRT state of an angle shard: R = 1/(A 1) on the local rows (0
+    elsewhere), C = 1/(A^T 1) (all-reduced), and the work arrays. step() is
+    one iteration x <- x + C A^T (R (y - A x)): local A x, the fused residual
+    (K8), local A^T, ONE all-reduce of the back-projection, the update."""
+
+    def __init__(self, g: ScanGeometry, y: torch.Tensor, group=None, fwd: Callable = None,
+                 bwd: Callable = None, ew=None):
+        self.g, self.y, self.group = g, y, group
+        self.fwd = fwd or _default_fwd
+        self.bwd = bwd or _default_bwd
+        self.ew = ew or DeviceElementwise()
+        self.rank, self.world = _world(group)
+        self.shard = angle_shard(g, self.rank, self.world)
+        self.ax = torch.zeros(g.n_measurements, dtype=y.dtype, device=y.device)
+        self.bp = torch.empty(g.n_voxels, dtype=y.dtype, device=y.device)
+        # R = 1 / (A 1): rows of other ranks stay 0 in ax, hence in R
+        ones_v = torch.ones(g.n_voxels, dtype=y.dtype, device=y.device)
+        self.R = torch.zeros(g.n_measurements, dtype=y.dtype, device=y.device)
+        self.fwd(g, ones_v, self.shard, self.R)
+        self.ew.invert_nonzero(g, self.R)
+        del ones_v
+        # C = 1 / (A^T 1): local partial + all-reduce
+        self.ax.fill_(1.0)
+        self.C = torch.empty(g.n_voxels, dtype=y.dtype, device=y.device)
+        self.bwd(g, self.ax, self.shard, self.C)
+        if self.world > 1:
+            dist.all_reduce(self.C, group=group)
+        self.ew.invert_nonzero(g, self.C)
+
+    def step(self, x: torch.Tensor) -> torch.Tensor:
+        g = self.g
+        self.fwd(g, x, self.shard, self.ax)
+        self.ew.residual(g, self.y, self.R, self.ax)  # ax <- R (y - A x); 0 on foreign rows
+        part = self.bwd(g, self.ax, self.shard, self.bp)
+        if self.world > 1:
+            dist.all_reduce(part, group=self.group)
+        return self.ew.update(g, self.C, part, x)
 
 
 def sharded_sirt(g: ScanGeometry, y: torch.Tensor, x0: torch.Tensor, iters: int, group=None,
-                 fwd: Callable = _default_fwd, bwd: Callable = _default_bwd) -> torch.Tensor:
+                 fwd: Callable = _default_fwd, bwd: Callable = _default_bwd, ew=None) -> torch.Tensor:
     """SIRT x <- x + C A^T (R (y - A x)) with angle sharding (BASELINE configs[4]).
 
     y is the full sinogram on every rank (each rank reads only its rows); x is
-    replicated and identical on all ranks after every iteration."""
-    rank, world = _world(group)
-    shard = angle_shard(g, rank, world)
-    rows = shard_rows(g, shard).to(y.device)
+    replicated and identical on all ranks after every iteration. ``ew`` swaps
+    the elementwise kernels (tests on CPU ranks only)."""
+    state = SirtState(g, y, group, fwd, bwd, ew)
     x = x0.clone()
-    ax = torch.zeros(g.n_measurements, dtype=y.dtype, device=y.device)
-    bp = torch.empty(g.n_voxels, dtype=y.dtype, device=y.device)
-    # R = 1 / (A 1) on the local rows
-    ones_v = torch.ones(g.n_voxels, dtype=y.dtype, device=y.device)
-    fwd(g, ones_v, shard, ax)
-    R = torch.zeros_like(ax)
-    R[rows] = _invert_nonzero(ax[rows])
-    # C = 1 / (A^T 1): local partial + all-reduce
-    ones_m = torch.ones(g.n_measurements, dtype=y.dtype, device=y.device)
-    colsum = bwd(g, ones_m, shard, bp)
-    if world > 1:
-        dist.all_reduce(colsum, group=group)
-    C = _invert_nonzero(colsum)
-    r = torch.zeros_like(ax)
     for _ in range(iters):
-        fwd(g, x, shard, ax)
-        r[rows] = R[rows] * (y[rows] - ax[rows])
-        part = bwd(g, r, shard, bp)
-        if world > 1:
-            dist.all_reduce(part, group=group)
-        x += C * part
+        state.step(x)
     return x

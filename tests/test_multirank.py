@@ -44,7 +44,23 @@ def _oracle_fns():
         out.copy_(torch.from_numpy(orc.back_mf_angles(g, angles, y.numpy(), 1)))
         return out
 
-    return orc, fwd, bwd
+    class TorchElementwise:
+        """CPU stand-in for the K7/K8 C-ABI kernels (same contracts)."""
+
+        def invert_nonzero(self, g, v):
+            nz = v != 0
+            v[nz] = 1.0 / v[nz]
+            return v
+
+        def residual(self, g, y, rinv, ax):
+            ax.copy_(rinv * (y - ax))
+            return ax
+
+        def update(self, g, cinv, bp, x):
+            x += cinv * bp
+            return x
+
+    return orc, fwd, bwd, TorchElementwise()
 
 
 def _worker(rank, world, port, name, q):
@@ -56,7 +72,7 @@ def _worker(rank, world, port, name, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2511_12235_b200 import dist as cdist
-    orc, fwd, bwd = _oracle_fns()
+    orc, fwd, bwd, ew = _oracle_fns()
     g = TEST_GEOMETRIES[name]
     rng = np.random.default_rng(5)
     x = torch.from_numpy(rng.uniform(0, 1, g.n_voxels))
@@ -66,7 +82,7 @@ def _worker(rank, world, port, name, q):
     dist.all_reduce(yl)
     xb = cdist.sharded_back_project(g, y, bwd=bwd)
     ys = torch.from_numpy(orc.forward_project_matrix_free(g, x.numpy(), 1))
-    xs = cdist.sharded_sirt(g, ys, torch.zeros(g.n_voxels, dtype=torch.float64), 3, fwd=fwd, bwd=bwd)
+    xs = cdist.sharded_sirt(g, ys, torch.zeros(g.n_voxels, dtype=torch.float64), 3, fwd=fwd, bwd=bwd, ew=ew)
     if rank == 0:
         q.put((yl.numpy(), xb.numpy(), xs.numpy()))
     dist.barrier()
