@@ -90,6 +90,22 @@ int ctsm_csr_fill(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int an
                   const uint64_t* row_start_dev, uint32_t* col_dev, double* val_dev,
                   void* stream);
 
+/* Single-evaluation build of the same rows: every weight is evaluated once.
+ * Per chunk of angles the kernel appends 16-byte records {row, col, val} and
+ * counts the rows; after the row scan the records are scattered into
+ * row-grouped scratch and each row is radix-sorted by column into the
+ * caller's arrays. row_start_dev as ctsm_csr_count; col_dev / val_dev hold
+ * `capacity` entries (ctsm_csr_angle_nnz(angle 0) * angles * 1.2 is a good
+ * size). *nnz_out receives the shard's entry count; the arrays are complete
+ * only if *nnz_out <= capacity (otherwise call again with larger arrays).
+ * Errors as ctsm_csr_count. ctsm_csr_angle_nnz counts one angle's entries
+ * (the reference's budget estimate uses angle 0, projector.cpp:155-169). */
+int ctsm_csr_angle_nnz(ctsm_ctx* ctx, const ctsm_geometry* g, int angle, uint64_t* nnz_out,
+                       void* stream);
+int ctsm_csr_build(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int angle_end,
+                   uint64_t memory_budget_bytes, uint64_t* row_start_dev, uint32_t* col_dev,
+                   double* val_dev, uint64_t capacity, uint64_t* nnz_out, void* stream);
+
 /* ---- K3/K4: CSR appliers (forward_project / back_project,
  * projector.cpp:203-233). Deterministic; NonFinite check as the reference. */
 int ctsm_spmv(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols, const uint64_t* row_start_dev,

@@ -82,6 +82,14 @@ struct DevBuf {
   ~DevBuf() {
     if (p) cudaFree(p);
   }
+  void reset(size_t n) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    if (n && cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(ErrorCode::OutOfMemory, "device allocation failed");
+    }
+  }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
 };
@@ -154,12 +162,30 @@ SparseSystemMatrix build_system_matrix(const ScanGeometry& g, MatrixMode mode, i
   w.n_cols = g.n_voxels();
   DevBuf<std::uint64_t> rs(w.n_rows + 1);
   std::uint64_t nnz = 0;
-  check(ctsm_csr_count_mode(ctx(), &c, mode_code(mode), k, 0, g.n_angles, memory_budget_bytes,
-                            rs.p, &nnz, nullptr));
-  DevBuf<std::uint32_t> col(nnz);
-  DevBuf<double> val(nnz);
-  check(ctsm_csr_fill_mode(ctx(), &c, mode_code(mode), k, 0, g.n_angles, rs.p, col.p, val.p,
-                           nullptr));
+  DevBuf<std::uint32_t> col(0);
+  DevBuf<double> val(0);
+  if (mode == MatrixMode::consistent) {
+    // single evaluation: arrays sized from the angle-0 estimate
+    std::uint64_t nnz0 = 0;
+    check(ctsm_csr_angle_nnz(ctx(), &c, 0, &nnz0, nullptr));
+    std::uint64_t cap = (std::uint64_t)((double)nnz0 * g.n_angles * 1.2) + 65536;
+    if (12 * nnz0 * (std::uint64_t)g.n_angles + 8 * (w.n_rows + 1) > memory_budget_bytes) cap = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      col.reset(cap);
+      val.reset(cap);
+      check(ctsm_csr_build(ctx(), &c, 0, g.n_angles, memory_budget_bytes, rs.p, col.p, val.p, cap,
+                           &nnz, nullptr));
+      if (nnz <= cap) break;
+      cap = nnz;
+    }
+  } else {
+    check(ctsm_csr_count_mode(ctx(), &c, mode_code(mode), k, 0, g.n_angles, memory_budget_bytes,
+                              rs.p, &nnz, nullptr));
+    col.reset(nnz);
+    val.reset(nnz);
+    check(ctsm_csr_fill_mode(ctx(), &c, mode_code(mode), k, 0, g.n_angles, rs.p, col.p, val.p,
+                             nullptr));
+  }
   w.row_start.resize(w.n_rows + 1);
   w.col.resize(nnz);
   w.val.resize(nnz);

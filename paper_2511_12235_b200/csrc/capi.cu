@@ -1,6 +1,7 @@
 // capi.cu -- the extern "C" boundary (include/ctsm_b200.h): context, geometry
 // validation, buffer management and the orchestration of the kernels in
 // csr.cu / mf.cu. Host code only.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -75,7 +76,8 @@ struct ctsm_ctx {
   double* h_red = nullptr;      // pinned
   Buf angles, edges, cs, counts, scan, longrows, acc, part, base, alist, sv_up, sv_h, sv_hp,
       sv_q, sv_v, sv_part, sv_scal, tmp_a, tmp_b, tmp_c, tmp_d,
-      tmp_e, tmp_f, lraw_start, lraw_col, lraw_val, lacc, bwd_t, vol_t;
+      tmp_e, tmp_f, lraw_start, lraw_col, lraw_val, lacc, bwd_t, vol_t, plans, rec, grp_col,
+      grp_val, cursor;
   // stream of the host-buffer calls: created non-blocking on first use, so
   // the calls of two contexts (two host threads) overlap their copies with
   // each other's kernels instead of serialising on the legacy stream
@@ -249,7 +251,8 @@ int ctsm_destroy(ctsm_ctx* ctx) {
                  &ctx->longrows, &ctx->acc, &ctx->part, &ctx->base, &ctx->alist, &ctx->sv_up, &ctx->sv_h, &ctx->sv_hp, &ctx->sv_q,
                  &ctx->sv_v, &ctx->sv_part, &ctx->sv_scal, &ctx->tmp_a, &ctx->tmp_b,  &ctx->tmp_c,
                  &ctx->tmp_d, &ctx->tmp_e, &ctx->tmp_f, &ctx->lraw_start, &ctx->lraw_col,
-                 &ctx->lraw_val, &ctx->lacc, &ctx->bwd_t, &ctx->vol_t};
+                 &ctx->lraw_val, &ctx->lacc, &ctx->bwd_t, &ctx->vol_t, &ctx->plans, &ctx->rec,
+                 &ctx->grp_col, &ctx->grp_val, &ctx->cursor};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->hstream) cudaStreamDestroy(ctx->hstream);
@@ -281,52 +284,93 @@ static int prepare_exact(ctsm_ctx* ctx, const DevGeom& d, int angle_begin, int n
   return 0;
 }
 
+// Angles per emission chunk: bounds the per-chunk scratch (plans, records,
+// row-grouped arrays) and keeps chunk-local rows and entries below 2^31.
+static int csr_chunk_angles(const DevGeom& d, int n_sel, uint64_t per_angle_entries) {
+  const uint64_t rec_budget = 2ull << 30, plan_budget = 1ull << 30;
+  uint64_t a = rec_budget / (16ull * (per_angle_entries + 1));
+  const size_t plan1 = csr_plan_bytes(d, 1);
+  if (plan1) a = std::min<uint64_t>(a, plan_budget / plan1);
+  a = std::min<uint64_t>(a, (1ull << 31) / (uint64_t)d.rows_per_angle);
+  a = std::min<uint64_t>(a, (uint64_t)n_sel);
+  return (int)std::max<uint64_t>(a, 1);
+}
+
+// Angle-0 entry count (the reference's budget estimate, projector.cpp:155-169).
+static int csr_angle_count(ctsm_ctx* ctx, const DevGeom& d, int angle, uint64_t* nnz,
+                           cudaStream_t st) {
+  const uint64_t rpa = (uint64_t)d.rows_per_angle;
+  CT_TRY(ensure(ctx, ctx->counts, rpa * sizeof(unsigned)));
+  CT_TRY(ensure(ctx, ctx->tmp_a, (rpa + 1) * sizeof(uint64_t)));
+  CT_TRY(ensure(ctx, ctx->scan, scan_scratch_bytes(rpa)));
+  CT_TRY(ensure(ctx, ctx->plans, csr_plan_bytes(d, 1)));
+  CT_TRY(prepare_exact(ctx, d, angle, 1, st));
+  CT_CUDA(cudaMemsetAsync(ctx->counts.p, 0, rpa * sizeof(unsigned), st));
+  CsrSink sk{0, (unsigned*)ctx->counts.p, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0};
+  CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, 1, sk, ctx->plans.p, ctx->status, st));
+  CT_CUDA(exclusive_scan_u32_u64((const unsigned*)ctx->counts.p, rpa, (uint64_t*)ctx->tmp_a.p,
+                                 ctx->scan.p, st));
+  CT_CUDA(cudaMemcpyAsync(nnz, (uint64_t*)ctx->tmp_a.p + rpa, sizeof(uint64_t),
+                          cudaMemcpyDeviceToHost, st));
+  return check_status(ctx, st, "build_system_matrix");
+}
+
+static int csr_budget_check(const ctsm_geometry* g, const DevGeom& d, uint64_t nnz0,
+                            uint64_t memory_budget_bytes) {
+  const uint64_t n_meas = (uint64_t)d.rows_per_angle * (uint64_t)g->n_angles;
+  const uint64_t est_nnz = nnz0 * (uint64_t)g->n_angles;
+  const uint64_t est_bytes =
+      est_nnz * (sizeof(uint32_t) + sizeof(double)) + (n_meas + 1) * sizeof(uint64_t);
+  if (est_bytes > memory_budget_bytes) {
+    char msg[256];
+    snprintf(msg, sizeof msg, "estimated %llu entries (%llu MiB) exceed the budget of %llu MiB",
+             (unsigned long long)est_nnz, (unsigned long long)(est_bytes >> 20),
+             (unsigned long long)(memory_budget_bytes >> 20));
+    return fail(CTSM_ERR_OUT_OF_MEMORY, msg);
+  }
+  return 0;
+}
+
+static int csr_prologue(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int angle_end,
+                        DevGeom* d) {
+  CT_TRY(set_device(ctx));
+  CT_TRY(dev_geom(g, d));
+  if ((uint64_t)g->n_x * g->n_y * g->n_z > 0xffffffffull)
+    return fail(CTSM_ERR_TOO_LARGE, "grid exceeds 2^32 voxel columns");
+  return check_shard(g, angle_begin, angle_end, 1);
+}
+
+int ctsm_csr_angle_nnz(ctsm_ctx* ctx, const ctsm_geometry* g, int angle, uint64_t* nnz_out,
+                       void* stream) {
+  DevGeom d;
+  CT_TRY(csr_prologue(ctx, g, angle, angle + 1, &d));
+  return csr_angle_count(ctx, d, angle, nnz_out, (cudaStream_t)stream);
+}
+
+// Two-evaluation protocol: count (this call), the caller allocates, fill.
 int ctsm_csr_count(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int angle_end,
                    uint64_t memory_budget_bytes, uint64_t* row_start_dev, uint64_t* nnz_out,
                    void* stream) {
-  CT_TRY(set_device(ctx));
   DevGeom d;
-  CT_TRY(dev_geom(g, &d));
-  if ((uint64_t)g->n_x * g->n_y * g->n_z > 0xffffffffull)
-    return fail(CTSM_ERR_TOO_LARGE, "grid exceeds 2^32 voxel columns");
-  CT_TRY(check_shard(g, angle_begin, angle_end, 1));
+  CT_TRY(csr_prologue(ctx, g, angle_begin, angle_end, &d));
   cudaStream_t st = (cudaStream_t)stream;
   const int n_sel = angle_end - angle_begin;
-  const uint64_t rpa = (uint64_t)d.rows_per_angle;
-  const uint64_t n_rows = rpa * n_sel;
-  const uint64_t n_meas = rpa * (uint64_t)g->n_angles;
-  // memory-budget estimate from angle 0, as the reference (projector.cpp:155-169)
+  const uint64_t n_rows = (uint64_t)d.rows_per_angle * n_sel;
   uint64_t nnz0 = 0;
-  {
-    CT_TRY(prepare_exact(ctx, d, 0, 1, st));
-    CT_TRY(ensure(ctx, ctx->counts, rpa * sizeof(unsigned)));
-    CT_TRY(ensure(ctx, ctx->tmp_a, (rpa + 1) * sizeof(uint64_t)));
-    CT_TRY(ensure(ctx, ctx->scan, scan_scratch_bytes(rpa)));
-    CT_CUDA(cudaMemsetAsync(ctx->counts.p, 0, rpa * sizeof(unsigned), st));
-    CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, 0, 1, 0, (unsigned*)ctx->counts.p, nullptr,
-                     nullptr, nullptr, ctx->status, st));
-    CT_CUDA(exclusive_scan_u32_u64((const unsigned*)ctx->counts.p, rpa, (uint64_t*)ctx->tmp_a.p,
-                                   ctx->scan.p, st));
-    CT_CUDA(cudaMemcpyAsync(&nnz0, (uint64_t*)ctx->tmp_a.p + rpa, sizeof(uint64_t),
-                            cudaMemcpyDeviceToHost, st));
-    CT_TRY(check_status(ctx, st, "build_system_matrix"));
-    const uint64_t est_nnz = nnz0 * (uint64_t)g->n_angles;
-    const uint64_t est_bytes = est_nnz * (sizeof(uint32_t) + sizeof(double)) +
-                               (n_meas + 1) * sizeof(uint64_t);
-    if (est_bytes > memory_budget_bytes) {
-      char msg[256];
-      snprintf(msg, sizeof msg, "estimated %llu entries (%llu MiB) exceed the budget of %llu MiB",
-               (unsigned long long)est_nnz, (unsigned long long)(est_bytes >> 20),
-               (unsigned long long)(memory_budget_bytes >> 20));
-      return fail(CTSM_ERR_OUT_OF_MEMORY, msg);
-    }
-  }
-  CT_TRY(prepare_exact(ctx, d, angle_begin, n_sel, st));
+  CT_TRY(csr_angle_count(ctx, d, 0, &nnz0, st));
+  CT_TRY(csr_budget_check(g, d, nnz0, memory_budget_bytes));
+  const int A = csr_chunk_angles(d, n_sel, nnz0);
+  CT_TRY(ensure(ctx, ctx->plans, csr_plan_bytes(d, A)));
   CT_TRY(ensure(ctx, ctx->counts, n_rows * sizeof(unsigned)));
   CT_TRY(ensure(ctx, ctx->scan, scan_scratch_bytes(n_rows)));
   CT_CUDA(cudaMemsetAsync(ctx->counts.p, 0, n_rows * sizeof(unsigned), st));
-  CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, angle_begin, n_sel, 0,
-                   (unsigned*)ctx->counts.p, nullptr, nullptr, nullptr, ctx->status, st));
+  for (int c0 = 0; c0 < n_sel; c0 += A) {
+    const int na = std::min(A, n_sel - c0);
+    CT_TRY(prepare_exact(ctx, d, angle_begin + c0, na, st));
+    CsrSink sk{0, (unsigned*)ctx->counts.p + (uint64_t)c0 * d.rows_per_angle, nullptr, nullptr,
+               nullptr, nullptr, nullptr, 0, 0};
+    CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, na, sk, ctx->plans.p, ctx->status, st));
+  }
   CT_CUDA(exclusive_scan_u32_u64((const unsigned*)ctx->counts.p, n_rows, row_start_dev,
                                  ctx->scan.p, st));
   uint64_t nnz = 0;
@@ -339,26 +383,126 @@ int ctsm_csr_count(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int a
   return 0;
 }
 
+// Fill: each chunk is emitted into row-grouped scratch (slots from per-row
+// cursors), then radix-sorted by column into the caller's arrays.
 int ctsm_csr_fill(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int angle_end,
                   const uint64_t* row_start_dev, uint32_t* col_dev, double* val_dev,
                   void* stream) {
-  CT_TRY(set_device(ctx));
   DevGeom d;
-  CT_TRY(dev_geom(g, &d));
-  CT_TRY(check_shard(g, angle_begin, angle_end, 1));
+  CT_TRY(csr_prologue(ctx, g, angle_begin, angle_end, &d));
   cudaStream_t st = (cudaStream_t)stream;
   const int n_sel = angle_end - angle_begin;
-  const uint64_t n_rows = (uint64_t)d.rows_per_angle * n_sel;
-  CT_TRY(prepare_exact(ctx, d, angle_begin, n_sel, st));
-  CT_TRY(ensure(ctx, ctx->counts, n_rows * sizeof(unsigned)));
-  CT_TRY(ensure(ctx, ctx->longrows, (n_rows + 1) * sizeof(unsigned)));
-  CT_CUDA(cudaMemsetAsync(ctx->counts.p, 0, n_rows * sizeof(unsigned), st));
-  CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, angle_begin, n_sel, 1,
-                   (unsigned*)ctx->counts.p, row_start_dev, col_dev, val_dev, ctx->status, st));
-  unsigned* nlong = (unsigned*)ctx->longrows.p + n_rows;
-  CT_CUDA(csr_sort_rows(n_rows, row_start_dev, col_dev, val_dev, (unsigned*)ctx->longrows.p, nlong,
-                        ctx->status, st));
+  const uint64_t rpa = (uint64_t)d.rows_per_angle;
+  // chunk bounds from the row offsets: two D2H reads per chunk boundary
+  uint64_t total = 0;
+  CT_CUDA(cudaMemcpyAsync(&total, row_start_dev + rpa * n_sel, sizeof total,
+                          cudaMemcpyDeviceToHost, st));
+  CT_CUDA(cudaStreamSynchronize(st));
+  const int A = csr_chunk_angles(d, n_sel, n_sel ? total / n_sel + 1 : 1);
+  const int n_chunks = (n_sel + A - 1) / A;
+  std::vector<uint64_t> bounds((size_t)n_chunks + 1, 0);
+  for (int i = 0; i < n_chunks; ++i)
+    CT_CUDA(cudaMemcpyAsync(&bounds[i], row_start_dev + rpa * (uint64_t)(i * A), sizeof(uint64_t),
+                            cudaMemcpyDeviceToHost, st));
+  CT_CUDA(cudaStreamSynchronize(st));
+  bounds[n_chunks] = total;
+  CT_TRY(ensure(ctx, ctx->plans, csr_plan_bytes(d, A)));
+  CT_TRY(ensure(ctx, ctx->counts, (size_t)A * rpa * sizeof(unsigned)));
+  CT_TRY(ensure(ctx, ctx->longrows, ((size_t)A * rpa + 2) * sizeof(unsigned)));
+  size_t ci = 0;
+  for (int c0 = 0; c0 < n_sel; c0 += A, ++ci) {
+    const int na = std::min(A, n_sel - c0);
+    const uint64_t nr = (uint64_t)na * rpa, row_off = (uint64_t)c0 * rpa;
+    const uint64_t base = bounds[ci], nnz_c = bounds[ci + 1] - bounds[ci];
+    if (nnz_c == 0) continue;
+    CT_TRY(ensure(ctx, ctx->grp_col, nnz_c * sizeof(uint32_t)));
+    CT_TRY(ensure(ctx, ctx->grp_val, nnz_c * sizeof(double)));
+    CT_TRY(prepare_exact(ctx, d, angle_begin + c0, na, st));
+    CT_CUDA(cudaMemsetAsync(ctx->counts.p, 0, nr * sizeof(unsigned), st));
+    CsrSink sk{1, (unsigned*)ctx->counts.p, row_start_dev + row_off, (uint32_t*)ctx->grp_col.p,
+               (double*)ctx->grp_val.p, nullptr, nullptr, 0, base};
+    CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, na, sk, ctx->plans.p, ctx->status, st));
+    unsigned* lr = (unsigned*)ctx->longrows.p;
+    CT_CUDA(csr_sort_rows_radix(nr, row_start_dev + row_off, base, (const uint32_t*)ctx->grp_col.p,
+                                (const double*)ctx->grp_val.p, col_dev + base, val_dev + base, lr,
+                                lr + nr + 1, st));
+  }
   return check_status(ctx, st, "build_system_matrix");
+}
+
+// Single-evaluation build: every weight is evaluated once. Per angle chunk:
+// mode-2 emission (row counts + 16-byte records), row scan, records scattered
+// into row-grouped scratch, per-row radix sort by column into the caller's
+// arrays. col_dev / val_dev hold `capacity` entries; *nnz_out receives the
+// shard's entry count, and the arrays are complete only if it is <= capacity
+// (otherwise the remaining chunks are only counted: call again with arrays of
+// *nnz_out entries).
+int ctsm_csr_build(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int angle_end,
+                   uint64_t memory_budget_bytes, uint64_t* row_start_dev, uint32_t* col_dev,
+                   double* val_dev, uint64_t capacity, uint64_t* nnz_out, void* stream) {
+  DevGeom d;
+  CT_TRY(csr_prologue(ctx, g, angle_begin, angle_end, &d));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_sel = angle_end - angle_begin;
+  const uint64_t rpa = (uint64_t)d.rows_per_angle;
+  uint64_t nnz0 = 0;
+  CT_TRY(csr_angle_count(ctx, d, 0, &nnz0, st));
+  CT_TRY(csr_budget_check(g, d, nnz0, memory_budget_bytes));
+  const uint64_t per_angle = nnz0 + nnz0 / 2 + 4096;  // angle 0 is a flat (sparser) angle
+  const int A = csr_chunk_angles(d, n_sel, per_angle);
+  const unsigned long long seg_slack = 148ull * 8 * 4 * 256;
+  unsigned long long cap = (unsigned long long)A * per_angle + seg_slack;
+  CT_TRY(ensure(ctx, ctx->plans, csr_plan_bytes(d, A)));
+  CT_TRY(ensure(ctx, ctx->counts, (size_t)A * rpa * sizeof(unsigned)));
+  CT_TRY(ensure(ctx, ctx->scan, scan_scratch_bytes((uint64_t)A * rpa)));
+  CT_TRY(ensure(ctx, ctx->longrows, ((size_t)A * rpa + 2) * sizeof(unsigned)));
+  CT_TRY(ensure(ctx, ctx->cursor, 2 * sizeof(unsigned long long)));
+  uint64_t base = 0;
+  for (int c0 = 0; c0 < n_sel; c0 += A) {
+    const int na = std::min(A, n_sel - c0);
+    const uint64_t nr = (uint64_t)na * rpa, row_off = (uint64_t)c0 * rpa;
+    CT_TRY(prepare_exact(ctx, d, angle_begin + c0, na, st));
+    unsigned long long cur_h = 0;
+    uint64_t end_h = 0;
+    const bool counting_only = base > capacity;
+    for (int attempt = 0;; ++attempt) {
+      if (!counting_only) CT_TRY(ensure(ctx, ctx->rec, (size_t)cap * 16));
+      CT_CUDA(cudaMemsetAsync(ctx->counts.p, 0, nr * sizeof(unsigned), st));
+      CT_CUDA(cudaMemsetAsync(ctx->cursor.p, 0, sizeof(unsigned long long), st));
+      CsrSink sk{counting_only ? 0 : 2, (unsigned*)ctx->counts.p, nullptr, nullptr, nullptr,
+                 ctx->rec.p, (unsigned long long*)ctx->cursor.p, cap, 0};
+      CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, na, sk, ctx->plans.p, ctx->status, st));
+      CT_CUDA(exclusive_scan_u32_u64((const unsigned*)ctx->counts.p, nr, row_start_dev + row_off,
+                                     ctx->scan.p, st, base));
+      CT_CUDA(cudaMemcpyAsync(&cur_h, ctx->cursor.p, sizeof cur_h, cudaMemcpyDeviceToHost, st));
+      CT_CUDA(cudaMemcpyAsync(&end_h, row_start_dev + row_off + nr, sizeof end_h,
+                              cudaMemcpyDeviceToHost, st));
+      CT_TRY(check_status(ctx, st, "build_system_matrix"));
+      if (cur_h <= cap) break;
+      if (attempt >= 4) return fail(CTSM_ERR_OUT_OF_MEMORY, "record buffer keeps overflowing");
+      cap = cur_h + cur_h / 4 + seg_slack;  // records were dropped: redo the chunk
+    }
+    const uint64_t nnz_c = end_h - base;
+    if (!counting_only && end_h <= capacity && nnz_c) {
+      CT_TRY(ensure(ctx, ctx->grp_col, nnz_c * sizeof(uint32_t)));
+      CT_TRY(ensure(ctx, ctx->grp_val, nnz_c * sizeof(double)));
+      CT_CUDA(cudaMemsetAsync(ctx->counts.p, 0, nr * sizeof(unsigned), st));
+      CT_CUDA(csr_scatter_records(ctx->rec.p, cur_h, row_start_dev + row_off, base,
+                                  (unsigned*)ctx->counts.p, (uint32_t*)ctx->grp_col.p,
+                                  (double*)ctx->grp_val.p, st));
+      unsigned* lr = (unsigned*)ctx->longrows.p;
+      CT_CUDA(csr_sort_rows_radix(nr, row_start_dev + row_off, base,
+                                  (const uint32_t*)ctx->grp_col.p, (const double*)ctx->grp_val.p,
+                                  col_dev + base, val_dev + base, lr, lr + nr + 1, st));
+    }
+    base = end_h;
+    if (base > capacity) capacity = 0;  // the later chunks are only counted
+  }
+  CT_CUDA(cudaStreamSynchronize(st));
+  if (angle_begin == 0 && angle_end == g->n_angles && base == 0)
+    return fail(CTSM_ERR_ZERO_MATRIX, "system matrix has no entries");
+  *nnz_out = base;
+  return 0;
 }
 
 // ---- K3/K4 ----------------------------------------------------------------

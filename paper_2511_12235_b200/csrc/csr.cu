@@ -8,6 +8,7 @@
 // scatters (col, w) into per-row slots, and a per-row sort restores the
 // reference's strictly ascending column order (projector.cpp:100-102).
 #include "exact.cuh"
+#include "csr3d.cuh"
 #include "kernels.h"
 
 namespace ctsmb {
@@ -35,23 +36,7 @@ cudaError_t build_exact_tables(const DevGeom& g, int angle_begin, int n_sel, voi
 
 namespace {
 
-struct Emitter {
-  int mode;
-  unsigned* row_counter;
-  const uint64_t* row_start;
-  uint32_t* col;
-  double* val;
-  __device__ __forceinline__ void operator()(uint64_t row_local, uint32_t column, double w) const {
-    if (mode == 0) {
-      atomicAdd(&row_counter[row_local], 1u);
-    } else {
-      const unsigned slot = atomicAdd(&row_counter[row_local], 1u);
-      const uint64_t pos = row_start[row_local] + slot;
-      col[pos] = column;
-      val[pos] = w;
-    }
-  }
-};
+using k2::Sink;
 
 // One thread per (pixel, angle): pixel_area_factors (weights2d.cpp:105-129)
 // -> emit (projector.cpp:53-60).
@@ -60,7 +45,7 @@ struct Emitter {
 #endif
 __global__ void __launch_bounds__(128, CTSM_CSR2_MINB) csr2d_kernel(DevGeom g, const ExactAngle* __restrict__ angs,
                                                     const EdgeAngle* __restrict__ edges,
-                                                    Emitter em, int* status) {
+                                                    Sink em, int* status) {
   const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (pix >= (long long)g.n_x * g.n_y) return;
   const int k = blockIdx.y;
@@ -87,220 +72,57 @@ __global__ void __launch_bounds__(128, CTSM_CSR2_MINB) csr2d_kernel(DevGeom g, c
     if (have && cur == cell) {
       cw += w;
     } else {
-      if (have && !(cw <= kEpsWeight)) em(row_base + (cur + g.n_det_y / 2), column, cw);
+      if (have && !(cw <= kEpsWeight)) k2::emit_any(em, row_base + (cur + g.n_det_y / 2), column, cw);
       cur = cell;
       cw = w;
       have = true;
     }
   }
-  if (have && !(cw <= kEpsWeight)) em(row_base + (cur + g.n_det_y / 2), column, cw);
-}
-
-// One thread per (voxel column (ix, iy), angle); walks iz. The xy sweep, the
-// per-cell 2D weights and the corner depths are shared along the column
-// (identical computations), then voxel_volume_factors (weights3d.cpp:354-462)
-// runs per voxel.
-#ifndef CTSM_CSR3_MINB
-#define CTSM_CSR3_MINB 4  // 128 registers (small spills): C2 assembly 2.73 -> 2.51 s
-#endif
-__global__ void __launch_bounds__(128, CTSM_CSR3_MINB) csr3d_kernel(DevGeom g, const ExactAngle* __restrict__ angs,
-                                                    const EdgeAngle* __restrict__ edges,
-                                                    Emitter em, int* status) {
-  const long long colxy = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (colxy >= (long long)g.n_x * g.n_y) return;
-  const int k = blockIdx.y;
-  const int ix = (int)(colxy % g.n_x), iy = (int)(colxy / g.n_x);
-  const ExactAngle A = angs[k];
-  const double s = g.s;
-  Sweep sw;
-  if (!exact::strip_sweep(g, A, edges, face(ix, g.n_x, g.a), face(ix + 1, g.n_x, g.a),
-                          face(iy, g.n_y, g.b), face(iy + 1, g.n_y, g.b), sw, status))
-    return;
-  const double a = sw.x1 - sw.x0, b = sw.y1 - sw.y0;
-  const double sdd = g.s + g.d;
-  // depths of the four xy corners (weights3d.cpp:367-371), order x0y0,x0y1,x1y0,x1y1
-  double dep[4];
-  {
-    const double vx[2] = {sw.x0, sw.x1}, vy[2] = {sw.y0, sw.y1};
-    for (int i = 0; i < 2; ++i)
-      for (int j = 0; j < 2; ++j) {
-        const double depth = s - vx[i] * sw.C - vy[j] * sw.S;
-        if (depth <= kEpsDenRel * s) {
-          raise_status(status, CTSM_ERR_DEGENERATE_GEOMETRY);
-          return;
-        }
-        dep[2 * i + j] = depth;
-      }
-  }
-  // cell groups with their 2D weight (weights3d.cpp:385-397)
-  const int cell_lo = -g.n_det_y / 2, cell_hi = g.n_det_y / 2 - 1;
-  const int row_lo = -g.n_det_z / 2, row_hi = g.n_det_z / 2 - 1;
-  int ng = 0;
-  unsigned char gbeg[kMaxBrk], gend[kMaxBrk];
-  int gcell[kMaxBrk];
-  double gw2d[kMaxBrk];
-  {
-    int i = 0;
-    while (i < sw.np) {
-      int j = i;
-      while (j < sw.np && sw.pcell[j] == sw.pcell[i]) ++j;
-      const int cell = sw.pcell[i];
-      if (cell >= cell_lo && cell <= cell_hi) {
-        double w2d = 0.0;
-        for (int p = i; p < j; ++p) w2d += exact::piece_area(sw, p, s, status);
-        if (w2d < 0.0) w2d = 0.0;
-        gbeg[ng] = (unsigned char)i;
-        gend[ng] = (unsigned char)j;
-        gcell[ng] = cell;
-        gw2d[ng] = w2d;
-        ++ng;
-      }
-      i = j;
-    }
-  }
-  if (ng == 0) return;
-  const uint64_t row_base = (uint64_t)k * g.rows_per_angle;
-  const double sdd_dz = sdd / g.d_z;
-  // Cell group outer, voxel inner (the emission order within a row does not
-  // matter: rows are sorted by column afterwards). Along z the top face of
-  // voxel iz is the bottom face of voxel iz+1: atom_sum(..., cz, tan_a, zt)
-  // of voxel iz and atom_sum(..., cz', tan_a, zb') of voxel iz+1 are the same
-  // operation on the same operands whenever cz' == cz bitwise (zb' is
-  // face(iz+1) in both), so the value is reused -- bit-identical to
-  // recomputing it. Up to 4 row edges are cached per voxel.
-  for (int q = 0; q < ng; ++q) {
-    const int pi = gbeg[q], pj = gend[q];
-    const double w2d = gw2d[q];
-    int cL[4] = {INT_MIN, INT_MIN, INT_MIN, INT_MIN};
-    double cF[4] = {0.0, 0.0, 0.0, 0.0};
-    double ccz = -1.0;  // cz of the cached faces
-    for (int iz = 0; iz < g.n_z; ++iz) {
-      const double zb = face(iz, g.n_z, g.c), zt = face(iz + 1, g.n_z, g.c);
-      const double cz = zt - zb;
-      double m_min = 0.0, m_max = 0.0;
-      bool first = true;
-      for (int qq = 0; qq < 4; ++qq) {
-        const double depth = dep[qq];
-        const double vz[2] = {zb, zt};
-        for (int r = 0; r < 2; ++r) {
-          const double m = sdd_dz * vz[r] / depth;
-          m_min = first ? m : exact::dmin(m_min, m);
-          m_max = first ? m : exact::dmax(m_max, m);
-          first = false;
-        }
-      }
-      const uint32_t column = (uint32_t)(((uint64_t)iz * g.n_y + iy) * g.n_x + ix);
-      const int fl = (int)floor(m_min);
-      const int k_lo = (fl < row_lo) ? row_lo : fl;
-      const int ch = (int)ceil(m_max) - 1;
-      const int k_hi = (ch < row_hi) ? ch : row_hi;
-      const bool reuse = (cz == ccz);
-      int nL[4] = {INT_MIN, INT_MIN, INT_MIN, INT_MIN};
-      double nF[4] = {0.0, 0.0, 0.0, 0.0};
-      int nn = 0;
-      if (k_hi >= k_lo) {
-        // above(k) lambda (weights3d.cpp:426-440); F(L, z) is atom_sum at
-        // zref = z (L > 0) or -z (L < 0); the bottom-face value of edge L
-        // comes from the cache when voxel iz-1 computed it as its top face
-        auto above = [&](double kk) -> double {
-          if (kk <= m_min) return w2d;
-          if (kk >= m_max) return 0.0;
-          if (kk == 0.0) {
-            if (zb >= 0.0) return w2d;
-            if (zt <= 0.0) return 0.0;
-            return w2d * zt / (zt - zb);
-          }
-          const int L = (int)kk;
-          const double tan_a = kk > 0.0 ? kk * g.d_z / sdd : -kk * g.d_z / sdd;
-          const double zt_s = kk > 0.0 ? zt : -zt, zb_s = kk > 0.0 ? zb : -zb;
-          double Fb;
-          bool hit = false;
-          if (reuse) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-              if (!hit && cL[c] == L) {
-                Fb = cF[c];
-                hit = true;
-              }
-          }
-#ifdef CTSM_CSR3_TWO_SITES
-          const double Ft = exact::atom_sum(sw, pi, pj, s, a, b, cz, tan_a, zt_s);
-          if (!hit) Fb = exact::atom_sum(sw, pi, pj, s, a, b, cz, tan_a, zb_s);
-#else
-          // one call site of the (large) atom sum: instruction-cache bound
-          // kernel; the same calls on the same operands as two sites
-          double Ft = 0.0;
-#pragma unroll 1
-          for (int f = hit ? 1 : 0; f < 2; ++f) {
-            const double r = exact::atom_sum(sw, pi, pj, s, a, b, cz, tan_a, f == 0 ? zb_s : zt_s);
-            if (f == 0) Fb = r; else Ft = r;
-          }
-#endif
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (c == nn) {
-              nL[c] = L;
-              nF[c] = Ft;
-            }
-          ++nn;
-          // weights3d.cpp:432-438: k > 0 -> F(zt) - F(zb); k < 0 -> w2d - (F(-zb) - F(-zt))
-          return kk > 0.0 ? Ft - Fb : w2d - (Fb - Ft);
-        };
-#ifdef CTSM_CSR3_TWO_SITES
-        double prev = above((double)k_lo);
-        for (int L = k_lo; L <= k_hi; ++L) {
-          const double next = above((double)(L + 1));
-#else
-        // one call site of above(): edges k_lo .. k_hi+1 in order (the same
-        // calls as above(k_lo) followed by above(L+1) per row)
-        double prev = 0.0;
-#pragma unroll 1
-        for (int L = k_lo - 1; L <= k_hi; ++L) {
-          const double next = above((double)(L + 1));
-          if (L < k_lo) {
-            prev = next;
-            continue;
-          }
-#endif
-          const double v = prev - next;
-          if (v > kEpsWeight) {
-            em(row_base + (uint64_t)(L + g.n_det_z / 2) * g.n_det_y + (gcell[q] + g.n_det_y / 2),
-               column, v);
-          } else if (v < kNegClamp3D) {
-            raise_status(status, CTSM_ERR_NON_FINITE);
-          }
-          prev = next;
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        cL[c] = nL[c];
-        cF[c] = nF[c];
-      }
-      ccz = cz;
-    }
-  }
+  if (have && !(cw <= kEpsWeight)) k2::emit_any(em, row_base + (cur + g.n_det_y / 2), column, cw);
 }
 
 }  // namespace
 
-cudaError_t csr_emit(const DevGeom& g, const void* angles_dev, const void* edges_dev,
-                     int angle_begin, int n_sel, int mode, unsigned* row_counter,
-                     const uint64_t* row_start, uint32_t* col, double* val, int* status,
-                     cudaStream_t st) {
-  (void)angle_begin;
+size_t csr_plan_bytes(const DevGeom& g, int n_sel) {
+  if (g.n_z == 1 && g.n_det_z == 1) return 0;
+  return (size_t)g.n_x * g.n_y * (size_t)n_sel * sizeof(k2::ColPlan);
+}
+
+// Emission of angles [0, n_sel) of the prepared tables (rows local to the
+// shard). 3D: plan kernel + warp-per-column kernel (csr3d.cuh); `plans` needs
+// csr_plan_bytes(g, n_sel) bytes.
+cudaError_t csr_emit(const DevGeom& g, const void* angles_dev, const void* edges_dev, int n_sel,
+                     const CsrSink& out, void* plans, int* status, cudaStream_t st) {
   if (n_sel <= 0) return cudaSuccess;
-  Emitter em{mode, row_counter, row_start, col, val};
+  Sink em{out.mode, out.row_counter, out.row_start, out.col, out.val, (uint4*)out.rec,
+          out.cursor, out.cap, 0u, out.pos_base};
   const long long nxy = (long long)g.n_x * g.n_y;
-  dim3 grid((unsigned)((nxy + 127) / 128), (unsigned)n_sel);
   const bool two_d = (g.n_z == 1 && g.n_det_z == 1);
-  if (two_d)
-    csr2d_kernel<<<grid, 128, 0, st>>>(g, (const ExactAngle*)angles_dev,
-                                       (const EdgeAngle*)edges_dev, em, status);
-  else
-    csr3d_kernel<<<grid, 128, 0, st>>>(g, (const ExactAngle*)angles_dev,
-                                       (const EdgeAngle*)edges_dev, em, status);
-  count_launch();
+  const ExactAngle* angs = (const ExactAngle*)angles_dev;
+  const EdgeAngle* edges = (const EdgeAngle*)edges_dev;
+  // gridDim.y <= 65535: launch the angles in slices
+  for (int k0 = 0; k0 < n_sel; k0 += 32768) {
+    const int nk = n_sel - k0 < 32768 ? n_sel - k0 : 32768;
+    Sink e2 = em;
+    const uint64_t row_off = (uint64_t)k0 * g.rows_per_angle;
+    e2.row_counter = em.row_counter + row_off;
+    if (em.row_start) e2.row_start = em.row_start + row_off;
+    e2.row_bias = (unsigned)row_off;
+    dim3 grid((unsigned)((nxy + 127) / 128), (unsigned)nk);
+    if (two_d) {
+      csr2d_kernel<<<grid, 128, 0, st>>>(g, angs + k0, edges, e2, status);
+      count_launch();
+    } else {
+      k2::ColPlan* pl = (k2::ColPlan*)plans + (size_t)k0 * nxy;
+      k2::plan3d_kernel<<<grid, 128, 0, st>>>(g, angs + k0, edges, pl, status);
+      const long long items = nxy * nk;
+      const long long blocks = (items + k2::kEmitWarps - 1) / k2::kEmitWarps;
+      const long long cap = 148ll * CTSM_EMIT3_MINB;  // one resident wave, warps stride
+      k2::emit3d_kernel<<<(unsigned)(blocks < cap ? blocks : cap), k2::kEmitWarps * 32, 0, st>>>(
+          g, pl, nk, e2, status);
+      count_launch(2);
+    }
+  }
   return cudaGetLastError();
 }
 
@@ -366,7 +188,7 @@ __global__ void scan_tiles_kernel(uint64_t* tile_sums, uint64_t n_tiles) {
 }
 
 __global__ void scan_down_kernel(const unsigned* in, uint64_t n, const uint64_t* tile_offs,
-                                 uint64_t* out) {
+                                 uint64_t* out, uint64_t out_base) {
   __shared__ uint64_t smem[32];
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
   uint64_t vals[kScanItems];
@@ -377,7 +199,7 @@ __global__ void scan_down_kernel(const unsigned* in, uint64_t n, const uint64_t*
     s += vals[i];
   }
   uint64_t total;
-  uint64_t off = block_scan_excl(s, smem, &total) + tile_offs[blockIdx.x];
+  uint64_t off = block_scan_excl(s, smem, &total) + tile_offs[blockIdx.x] + out_base;
   for (int i = 0; i < kScanItems; ++i) {
     const uint64_t idx = base + (uint64_t)threadIdx.x * kScanItems + i;
     if (idx < n) out[idx] = off;
@@ -393,13 +215,13 @@ size_t scan_scratch_bytes(uint64_t n) {
 }
 
 cudaError_t exclusive_scan_u32_u64(const unsigned* counts, uint64_t n, uint64_t* row_start,
-                                   void* scratch, cudaStream_t st) {
-  if (n == 0) return cudaMemsetAsync(row_start, 0, sizeof(uint64_t), st);
+                                   void* scratch, cudaStream_t st, uint64_t base) {
+  if (n == 0) return cudaMemcpyAsync(row_start, &base, sizeof(uint64_t), cudaMemcpyHostToDevice, st);
   const uint64_t tiles = (n + kScanTile - 1) / kScanTile;
   uint64_t* ts = (uint64_t*)scratch;
   scan_reduce_kernel<<<(unsigned)tiles, kScanBlock, 0, st>>>(counts, n, ts);
   scan_tiles_kernel<<<1, kScanBlock, 0, st>>>(ts, tiles);
-  scan_down_kernel<<<(unsigned)tiles, kScanBlock, 0, st>>>(counts, n, ts, row_start);
+  scan_down_kernel<<<(unsigned)tiles, kScanBlock, 0, st>>>(counts, n, ts, row_start, base);
   count_launch(3);
   return cudaGetLastError();
 }
@@ -512,6 +334,244 @@ cudaError_t csr_sort_rows(uint64_t n_rows, const uint64_t* row_start, uint32_t* 
   const unsigned grid = (unsigned)(blocks < 148ull * 16 ? blocks : 148ull * 16);
   sort_rows_warp<<<grid, kSortWarps * 32, 0, st>>>(n_rows, row_start, col, val, long_rows, n_long);
   sort_rows_long<<<148, 32, 0, st>>>(long_rows, n_long, row_start, col, val);
+  count_launch(2);
+  return cudaGetLastError();
+}
+
+// ---- single-evaluation build: records -> rows -> sorted rows ---------------
+namespace {
+// Step P: each record goes to its row's range of the (unsorted) row-grouped
+// arrays; the slot within the row is taken from a per-row cursor.
+__global__ void __launch_bounds__(256) scatter_records_kernel(const uint4* __restrict__ rec,
+                                                              unsigned long long n,
+                                                              const uint64_t* __restrict__ rs,
+                                                              uint64_t base, unsigned* slot,
+                                                              uint32_t* col, double* val) {
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    const uint4 r = __ldcs(&rec[i]);
+    if (r.x == k2::kInvalidRow) continue;
+    const uint64_t pos = (rs[r.x] - base) + atomicAdd(&slot[r.x], 1u);
+    col[pos] = r.y;
+    val[pos] = __hiloint2double((int)r.w, (int)r.z);
+  }
+}
+
+// Step Q: per-row LSD radix sort by column, one warp per row, out of place
+// (grouped arrays -> final arrays). The digits that are equal in all keys of a
+// row are skipped; each 8-bit pass is histogram, scan, and a stable scatter
+// (32 keys at a time: match_any ranks equal digits within the chunk).
+constexpr int kRsWarps = 4;
+constexpr int kRsCap = 1024;  // longer rows go to sort_rows_block
+struct RsWarp {
+  uint32_t key[2][kRsCap];
+  uint16_t idx[2][kRsCap];
+  uint32_t hist[256];
+};
+
+__global__ void __launch_bounds__(kRsWarps * 32) sort_rows_radix(
+    uint64_t n_rows, const uint64_t* __restrict__ rs, uint64_t base,
+    const uint32_t* __restrict__ col_in, const double* __restrict__ val_in,
+    uint32_t* __restrict__ col_out, double* __restrict__ val_out, unsigned* long_rows,
+    unsigned* n_long) {
+  extern __shared__ __align__(16) unsigned char rs_smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  RsWarp& w = reinterpret_cast<RsWarp*>(rs_smem)[wid];
+  const unsigned full = 0xffffffffu;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint64_t warps_total = (uint64_t)gridDim.x * kRsWarps;
+  for (uint64_t r = (uint64_t)blockIdx.x * kRsWarps + wid; r < n_rows; r += warps_total) {
+    const uint64_t b = rs[r] - base;
+    const uint64_t n64 = rs[r + 1] - rs[r];
+    if (n64 == 0) continue;
+    if (n64 > (uint64_t)kRsCap) {
+      if (lane == 0) long_rows[atomicAdd(n_long, 1u)] = (unsigned)r;
+      continue;
+    }
+    const int n = (int)n64;
+    uint32_t kor = 0u, kand = ~0u;
+    for (int i = lane; i < n; i += 32) {
+      const uint32_t k = __ldcs(&col_in[b + i]);
+      w.key[0][i] = k;
+      w.idx[0][i] = (uint16_t)i;
+      kor |= k;
+      kand &= k;
+    }
+    __syncwarp();
+    bool sorted = true;
+    for (int i = lane; i + 1 < n; i += 32)
+      if (w.key[0][i] > w.key[0][i + 1]) sorted = false;
+    int cur = 0;
+    if (!__all_sync(full, sorted)) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        kor |= __shfl_xor_sync(full, kor, o);
+        kand &= __shfl_xor_sync(full, kand, o);
+      }
+      const uint32_t diff = kor ^ kand;
+      for (int shift = 0; shift < 32; shift += 8) {
+        if (((diff >> shift) & 0xffu) == 0u) continue;
+        for (int j = lane; j < 256; j += 32) w.hist[j] = 0u;
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) atomicAdd(&w.hist[(w.key[cur][i] >> shift) & 0xffu], 1u);
+        __syncwarp();
+        {
+          unsigned loc[8], sum = 0u;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            loc[j] = w.hist[lane * 8 + j];
+            sum += loc[j];
+          }
+          unsigned incl = sum;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(full, incl, o);
+            if (lane >= o) incl += y;
+          }
+          unsigned run = incl - sum;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            w.hist[lane * 8 + j] = run;
+            run += loc[j];
+          }
+        }
+        __syncwarp();
+        for (int c = 0; c < n; c += 32) {
+          const int i = c + lane;
+          const bool valid = i < n;
+          const uint32_t k = valid ? w.key[cur][i] : 0u;
+          const uint16_t id = valid ? w.idx[cur][i] : (uint16_t)0;
+          const unsigned d = valid ? ((k >> shift) & 0xffu) : (256u + (unsigned)lane);
+          const unsigned peers = __match_any_sync(full, d);
+          const unsigned rank = __popc(peers & lt);
+          if (valid) {
+            const unsigned pos = w.hist[d] + rank;
+            w.key[cur ^ 1][pos] = k;
+            w.idx[cur ^ 1][pos] = id;
+          }
+          __syncwarp();
+          if (valid && rank == 0u) w.hist[d] += __popc(peers);
+          __syncwarp();
+        }
+        cur ^= 1;
+      }
+    }
+    for (int i = lane; i < n; i += 32) {
+      col_out[b + i] = w.key[cur][i];
+      val_out[b + i] = val_in[b + w.idx[cur][i]];
+    }
+    __syncwarp();
+  }
+}
+
+// Rows longer than kRsCap: one block per row, bitonic sort of (column, index)
+// keys in shared memory up to kLongCap entries; beyond that a shell sort in
+// global memory by one thread (kept for completeness).
+constexpr int kLongCap = 16384;
+constexpr int kLongThreads = 512;
+__global__ void __launch_bounds__(kLongThreads) sort_rows_block(
+    const unsigned* __restrict__ long_rows, const unsigned* __restrict__ n_long,
+    const uint64_t* __restrict__ rs, uint64_t base, const uint32_t* __restrict__ col_in,
+    const double* __restrict__ val_in, uint32_t* __restrict__ col_out,
+    double* __restrict__ val_out) {
+  extern __shared__ __align__(16) unsigned char rs_smem[];
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(rs_smem);
+  const unsigned nl = *n_long;
+  for (unsigned q = blockIdx.x; q < nl; q += gridDim.x) {
+    const uint64_t r = long_rows[q];
+    const uint64_t b = rs[r] - base;
+    const uint64_t n = rs[r + 1] - rs[r];
+    if (n <= (uint64_t)kLongCap) {
+      int n2 = 1;
+      while ((uint64_t)n2 < n) n2 <<= 1;
+      for (int i = threadIdx.x; i < n2; i += kLongThreads)
+        key[i] = (uint64_t)i < n ? (((unsigned long long)col_in[b + i] << 32) | (unsigned)i) : ~0ull;
+      __syncthreads();
+      for (int k = 2; k <= n2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int i = threadIdx.x; i < n2; i += kLongThreads) {
+            const int p = i ^ j;
+            if (p > i) {
+              const unsigned long long x = key[i], y = key[p];
+              if ((x > y) == ((i & k) == 0)) {
+                key[i] = y;
+                key[p] = x;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      for (uint64_t i = threadIdx.x; i < n; i += kLongThreads) {
+        const unsigned long long kk = key[i];
+        col_out[b + i] = (uint32_t)(kk >> 32);
+        val_out[b + i] = val_in[b + (kk & 0xffffffffu)];
+      }
+      __syncthreads();
+    } else {
+      for (uint64_t i = threadIdx.x; i < n; i += kLongThreads) {
+        col_out[b + i] = col_in[b + i];
+        val_out[b + i] = val_in[b + i];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        long long gap = 1;
+        while (gap < (long long)n / 3) gap = 3 * gap + 1;
+        for (; gap > 0; gap /= 3)
+          for (long long i = gap; i < (long long)n; ++i) {
+            const uint32_t c = col_out[b + i];
+            const double v = val_out[b + i];
+            long long j = i;
+            while (j >= gap && col_out[b + j - gap] > c) {
+              col_out[b + j] = col_out[b + j - gap];
+              val_out[b + j] = val_out[b + j - gap];
+              j -= gap;
+            }
+            col_out[b + j] = c;
+            val_out[b + j] = v;
+          }
+      }
+      __syncthreads();
+    }
+  }
+}
+}  // namespace
+
+cudaError_t csr_scatter_records(const void* rec, unsigned long long n, const uint64_t* row_start,
+                                uint64_t base, unsigned* slot, uint32_t* col, double* val,
+                                cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const unsigned long long blocks = (n + 255) / 256;
+  const unsigned grid = (unsigned)(blocks < 148ull * 32 ? blocks : 148ull * 32);
+  scatter_records_kernel<<<grid, 256, 0, st>>>((const uint4*)rec, n, row_start, base, slot, col,
+                                               val);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t csr_sort_rows_radix(uint64_t n_rows, const uint64_t* row_start, uint64_t base,
+                                const uint32_t* col_in, const double* val_in, uint32_t* col_out,
+                                double* val_out, unsigned* long_rows, unsigned* n_long,
+                                cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(sort_rows_radix, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kRsWarps * sizeof(RsWarp)));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(sort_rows_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kLongCap * sizeof(unsigned long long)));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  cudaError_t e = cudaMemsetAsync(n_long, 0, sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
+  if (n_rows == 0) return cudaSuccess;
+  const uint64_t blocks = (n_rows + kRsWarps - 1) / kRsWarps;
+  const unsigned grid = (unsigned)(blocks < 148ull * 4 ? blocks : 148ull * 4);
+  sort_rows_radix<<<grid, kRsWarps * 32, kRsWarps * sizeof(RsWarp), st>>>(
+      n_rows, row_start, base, col_in, val_in, col_out, val_out, long_rows, n_long);
+  sort_rows_block<<<148, kLongThreads, kLongCap * sizeof(unsigned long long), st>>>(
+      long_rows, n_long, row_start, base, col_in, val_in, col_out, val_out);
   count_launch(2);
   return cudaGetLastError();
 }

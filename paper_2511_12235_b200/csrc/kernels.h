@@ -31,17 +31,46 @@ size_t exact_angle_bytes();
 size_t edge_angle_bytes();
 cudaError_t build_exact_tables(const DevGeom& g, int angle_begin, int n_sel, void* angles_dev,
                                void* edges_dev, cudaStream_t st);
-// mode 0: count entries per row into row_counter (u32, zeroed by caller);
-// mode 1: fill col/val using row_start and row_counter as slot cursors (zeroed).
-cudaError_t csr_emit(const DevGeom& g, const void* angles_dev, const void* edges_dev,
-                     int angle_begin, int n_sel, int mode, unsigned* row_counter,
-                     const uint64_t* row_start, uint32_t* col, double* val, int* status,
-                     cudaStream_t st);
+// Output sink of the CSR emission kernels (csr3d.cuh Sink):
+//   mode 0: count entries per row into row_counter (u32, zeroed by the caller);
+//   mode 1: fill col/val at row_start[row] - pos_base + slot, row_counter as
+//           slot cursors;
+//   mode 2: count and append 16-byte records {row, col, val} to rec[0..cap),
+//           allocated from *cursor (zeroed by the caller; cursor > cap means
+//           records were dropped: retry with a larger buffer).
+struct CsrSink {
+  int mode;
+  unsigned* row_counter;
+  const uint64_t* row_start;
+  uint32_t* col;
+  double* val;
+  void* rec;
+  unsigned long long* cursor;
+  unsigned long long cap;
+  uint64_t pos_base;
+};
+// Bytes of the per-(column, angle) plan scratch of the 3D emission (0 for 2D).
+size_t csr_plan_bytes(const DevGeom& g, int n_sel);
+// Emits the rows of the n_sel angles of the prepared tables (rows local to
+// the shard) into `out`.
+cudaError_t csr_emit(const DevGeom& g, const void* angles_dev, const void* edges_dev, int n_sel,
+                     const CsrSink& out, void* plans, int* status, cudaStream_t st);
+// Single-evaluation build, after a mode-2 emission and the row scan: records
+// -> row-grouped arrays (slot zeroed by the caller) -> per-row radix sort by
+// column into the final arrays. row_start holds global offsets; the arrays
+// passed here start at offset `base`.
+cudaError_t csr_scatter_records(const void* rec, unsigned long long n, const uint64_t* row_start,
+                                uint64_t base, unsigned* slot, uint32_t* col, double* val,
+                                cudaStream_t st);
+cudaError_t csr_sort_rows_radix(uint64_t n_rows, const uint64_t* row_start, uint64_t base,
+                                const uint32_t* col_in, const double* val_in, uint32_t* col_out,
+                                double* val_out, unsigned* long_rows, unsigned* n_long,
+                                cudaStream_t st);
 // row_start[0..n] = exclusive scan of counts[0..n-1] (u32 -> u64); scratch
 // needs scan_scratch_bytes(n).
 size_t scan_scratch_bytes(uint64_t n);
 cudaError_t exclusive_scan_u32_u64(const unsigned* counts, uint64_t n, uint64_t* row_start,
-                                   void* scratch, cudaStream_t st);
+                                   void* scratch, cudaStream_t st, uint64_t base = 0);
 // Sort each row's entries by column (in place).
 cudaError_t csr_sort_rows(uint64_t n_rows, const uint64_t* row_start, uint32_t* col,
                           double* val, unsigned* long_rows, unsigned* n_long, int* status,

@@ -208,12 +208,14 @@ def _meta(g: ScanGeometry, mode: str, k: int) -> str:
 
 def build_system_matrix(g: ScanGeometry, mode: str = MatrixMode.consistent, k: int = 1,
                         threads: int = 1, memory_budget_bytes: int = DEFAULT_BUDGET,
-                        device: Optional[int] = None, angle_range: Optional[tuple] = None
-                        ) -> SparseSystemMatrix:
+                        device: Optional[int] = None, angle_range: Optional[tuple] = None,
+                        two_pass: bool = False) -> SparseSystemMatrix:
     """projector.cpp:144-201 on the GPU (K1 2D / K2 3D; line / multiline(k)
     by the device ray tracer, K9). ``threads`` is accepted for API
     compatibility and ignored. ``angle_range=(a0, a1)`` builds one contiguous
-    angle shard (rows a0*rpa .. a1*rpa)."""
+    angle shard (rows a0*rpa .. a1*rpa). The consistent matrix is built by
+    ``ctsm_csr_build`` (each weight evaluated once); ``two_pass=True`` uses
+    the count / fill protocol instead (two evaluations, exact-size arrays)."""
     mc = _mode_code(mode, k)
     g.validate()
     if g.n_voxels > 0xFFFFFFFF:
@@ -227,6 +229,27 @@ def build_system_matrix(g: ScanGeometry, mode: str = MatrixMode.consistent, k: i
     nnz = ctypes.c_uint64(0)
     st = _stream(dev)
     L = _lib.lib()
+    if mc == 0 and not two_pass:
+        # single evaluation (ctsm_csr_build): arrays sized from the angle-0
+        # estimate; the views keep the (slightly larger) storage alive
+        nnz0 = ctypes.c_uint64(0)
+        _lib.check(L.ctsm_csr_angle_nnz(ctx.handle, ctypes.byref(cg), 0, ctypes.byref(nnz0), st))
+        cap = int(nnz0.value * (a1 - a0) * 1.2) + 65536
+        if 12 * nnz0.value * g.n_angles + 8 * (g.n_measurements + 1) > memory_budget_bytes:
+            cap = 0  # the call raises OutOfMemory (projector.cpp:155-169)
+        for _ in range(2):
+            col = torch.empty(cap, dtype=torch.int32, device=f"cuda:{dev}")
+            val = torch.empty(cap, dtype=torch.float64, device=f"cuda:{dev}")
+            _lib.check(L.ctsm_csr_build(ctx.handle, ctypes.byref(cg), a0, a1, memory_budget_bytes,
+                                        _dev_ptr(row_start), _dev_ptr(col), _dev_ptr(val), cap,
+                                        ctypes.byref(nnz), st))
+            if nnz.value <= cap:
+                break
+            cap = nnz.value
+        return SparseSystemMatrix(n_rows=n_rows, n_cols=g.n_voxels, row_start=row_start,
+                                  col=col[:nnz.value], val=val[:nnz.value],
+                                  meta=_meta(g, mode, k), device=dev,
+                                  row_offset=a0 * g.rows_per_angle)
     _lib.check(L.ctsm_csr_count_mode(ctx.handle, ctypes.byref(cg), mc, k, a0, a1,
                                      memory_budget_bytes, _dev_ptr(row_start),
                                      ctypes.byref(nnz), st))

@@ -90,6 +90,57 @@ def test_csr_c2_angle_blocks_bitexact(ip, oracle_cr):
     assert np.array_equal(val.view(np.uint64), ref[2].view(np.uint64))
 
 
+@pytest.mark.parametrize("name", ["proj2d", "cone3d"])
+def test_csr_two_pass_equals_single_evaluation(name):
+    """count / fill (two evaluations, exact-size arrays) and ctsm_csr_build
+    (one evaluation) give the same bits."""
+    g = TEST_GEOMETRIES[name]
+    a = build_system_matrix(g).to_host()
+    b = build_system_matrix(g, two_pass=True).to_host()
+    for x, y in zip(a, b):
+        assert np.array_equal(x.view(np.uint64) if x.dtype == np.float64 else x,
+                              y.view(np.uint64) if y.dtype == np.float64 else y)
+
+
+def test_csr_build_capacity_protocol(oracle_cr):
+    """ctsm_csr_build with too small arrays reports the needed entry count
+    and leaves the caller to retry; several angle chunks (C2, 9 angles: the
+    chunk holds 7) are stitched at the right offsets."""
+    import ctypes
+    import torch
+    from paper_2511_12235_b200 import _lib
+    from paper_2511_12235_b200.projector import Context, _dev_ptr, _stream
+    g = CONFIGS["c2"]
+    ctx = Context.get(None)
+    cg = g.to_c()
+    a0, a1 = 88, 97
+    n_rows = (a1 - a0) * g.rows_per_angle
+    rs = torch.empty(n_rows + 1, dtype=torch.int64, device="cuda")
+    nnz = ctypes.c_uint64(0)
+    small = torch.empty(1000, dtype=torch.int32, device="cuda")
+    smallv = torch.empty(1000, dtype=torch.float64, device="cuda")
+    L = _lib.lib()
+    _lib.check(L.ctsm_csr_build(ctx.handle, ctypes.byref(cg), a0, a1, 1 << 40, _dev_ptr(rs),
+                                _dev_ptr(small), _dev_ptr(smallv), 1000, ctypes.byref(nnz),
+                                _stream(ctx.device)))
+    need = nnz.value
+    assert need > 1000
+    w = build_system_matrix(g, angle_range=(a0, a1), memory_budget_bytes=1 << 40)
+    assert w.nnz() == need
+    assert int(rs[-1].item()) == need and torch.equal(rs, w.row_start)
+    rs_h, col, val = w.to_host()
+    rpa = g.rows_per_angle
+    for ip in (88, 94, 96):  # first chunk, last angle of it, second chunk
+        ref = entries_to_csr(g, *oracle_cr.angle_block_entries(g, ip, threads=NTHREADS))
+        lo, hi = int(rs_h[(ip - a0) * rpa]), int(rs_h[(ip - a0 + 1) * rpa])
+        assert np.array_equal(rs_h[(ip - a0) * rpa:(ip - a0 + 1) * rpa + 1] - np.uint64(lo), ref[0])
+        assert np.array_equal(col[lo:hi], ref[1])
+        assert np.array_equal(val[lo:hi].view(np.uint64), ref[2].view(np.uint64))
+    w2 = build_system_matrix(g, angle_range=(a0, a1), memory_budget_bytes=1 << 40, two_pass=True)
+    assert torch.equal(w2.row_start, w.row_start) and torch.equal(w2.col, w.col)
+    assert torch.equal(w2.val.view(torch.int64), w.val.view(torch.int64))
+
+
 def test_csr_budget_and_size_limits():
     g = TEST_GEOMETRIES["proj3d"]
     with pytest.raises(CtsmError) as e:
