@@ -302,9 +302,16 @@ int ctsm_back_project_matrix_free_host_f32(ctsm_ctx* ctx, const ctsm_geometry* g
                                            const float* y_host, float* x_host);
 
 /* ---- diagnostics ---------------------------------------------------------
+ * ctsm_selftest_division: the exact 3D emission divides by per-column
+ * constants with a precomputed correctly rounded reciprocal and one fma
+ * correction (csr3d.cuh div_by), which returns the IEEE quotient; this runs
+ * the sequence against the division instruction on n pseudo-random operand
+ * pairs and reports the number of differing results (expected 0).
+ *
  * Measured FP64 FMA throughput of `device` in TFLOP/s (FMA = 2 flops): the
  * FP64 roofline denominator used by bench.py (MEASURED_PEAKS.json has none). */
 double ctsm_bench_dfma(int device);
+int ctsm_selftest_division(ctsm_ctx* ctx, uint64_t n, uint64_t seed, uint64_t* mismatches);
 
 #ifdef __cplusplus
 }

@@ -46,6 +46,7 @@ SIGNATURES = {
     "ctsm_validate_geometry": (_I, [_GP]),
     "ctsm_csr_count": (_I, [_P, _GP, _I, _I, _U64, _P, ctypes.POINTER(_U64), _P]),
     "ctsm_csr_fill": (_I, [_P, _GP, _I, _I, _P, _P, _P, _P]),
+    "ctsm_selftest_division": (_I, [_P, _U64, _U64, ctypes.POINTER(_U64)]),
     "ctsm_csr_angle_nnz": (_I, [_P, _GP, _I, ctypes.POINTER(_U64), _P]),
     "ctsm_csr_build": (_I, [_P, _GP, _I, _I, _U64, _P, _P, _P, _U64, ctypes.POINTER(_U64), _P]),
     "ctsm_spmv": (_I, [_P, _U64, _U64, _P, _P, _P, _P, _P, _P]),

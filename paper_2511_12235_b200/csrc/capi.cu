@@ -76,8 +76,11 @@ struct ctsm_ctx {
   double* h_red = nullptr;      // pinned
   Buf angles, edges, cs, counts, scan, longrows, acc, part, base, alist, sv_up, sv_h, sv_hp,
       sv_q, sv_v, sv_part, sv_scal, tmp_a, tmp_b, tmp_c, tmp_d,
-      tmp_e, tmp_f, lraw_start, lraw_col, lraw_val, lacc, bwd_t, vol_t, plans, rec, grp_col,
-      grp_val, cursor;
+      tmp_e, tmp_f, lraw_start, lraw_col, lraw_val, lacc, bwd_t, vol_t, plans, rec, grp,
+      cursor, plans2, rec2, grp2, angles2, counts2, longrows2;
+  // second stream + events of the pipelined CSR build (ctsm_csr_build)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // stream of the host-buffer calls: created non-blocking on first use, so
   // the calls of two contexts (two host threads) overlap their copies with
   // each other's kernels instead of serialising on the legacy stream
@@ -252,7 +255,11 @@ int ctsm_destroy(ctsm_ctx* ctx) {
                  &ctx->sv_v, &ctx->sv_part, &ctx->sv_scal, &ctx->tmp_a, &ctx->tmp_b,  &ctx->tmp_c,
                  &ctx->tmp_d, &ctx->tmp_e, &ctx->tmp_f, &ctx->lraw_start, &ctx->lraw_col,
                  &ctx->lraw_val, &ctx->lacc, &ctx->bwd_t, &ctx->vol_t, &ctx->plans, &ctx->rec,
-                 &ctx->grp_col, &ctx->grp_val, &ctx->cursor};
+                 &ctx->grp, &ctx->cursor, &ctx->plans2, &ctx->rec2, &ctx->grp2, &ctx->angles2,
+                 &ctx->counts2, &ctx->longrows2};
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  for (cudaEvent_t e : ctx->ev)
+    if (e) cudaEventDestroy(e);
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->hstream) cudaStreamDestroy(ctx->hstream);
@@ -306,7 +313,7 @@ static int csr_angle_count(ctsm_ctx* ctx, const DevGeom& d, int angle, uint64_t*
   CT_TRY(ensure(ctx, ctx->plans, csr_plan_bytes(d, 1)));
   CT_TRY(prepare_exact(ctx, d, angle, 1, st));
   CT_CUDA(cudaMemsetAsync(ctx->counts.p, 0, rpa * sizeof(unsigned), st));
-  CsrSink sk{0, (unsigned*)ctx->counts.p, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0};
+  CsrSink sk{0, (unsigned*)ctx->counts.p, nullptr, nullptr, nullptr, nullptr, 0, 0};
   CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, 1, sk, ctx->plans.p, ctx->status, st));
   CT_CUDA(exclusive_scan_u32_u64((const unsigned*)ctx->counts.p, rpa, (uint64_t*)ctx->tmp_a.p,
                                  ctx->scan.p, st));
@@ -368,7 +375,7 @@ int ctsm_csr_count(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int a
     const int na = std::min(A, n_sel - c0);
     CT_TRY(prepare_exact(ctx, d, angle_begin + c0, na, st));
     CsrSink sk{0, (unsigned*)ctx->counts.p + (uint64_t)c0 * d.rows_per_angle, nullptr, nullptr,
-               nullptr, nullptr, nullptr, 0, 0};
+               nullptr, nullptr, 0, 0};
     CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, na, sk, ctx->plans.p, ctx->status, st));
   }
   CT_CUDA(exclusive_scan_u32_u64((const unsigned*)ctx->counts.p, n_rows, row_start_dev,
@@ -415,27 +422,31 @@ int ctsm_csr_fill(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int an
     const uint64_t nr = (uint64_t)na * rpa, row_off = (uint64_t)c0 * rpa;
     const uint64_t base = bounds[ci], nnz_c = bounds[ci + 1] - bounds[ci];
     if (nnz_c == 0) continue;
-    CT_TRY(ensure(ctx, ctx->grp_col, nnz_c * sizeof(uint32_t)));
-    CT_TRY(ensure(ctx, ctx->grp_val, nnz_c * sizeof(double)));
+    CT_TRY(ensure(ctx, ctx->grp, nnz_c * 16));
     CT_TRY(prepare_exact(ctx, d, angle_begin + c0, na, st));
     CT_CUDA(cudaMemsetAsync(ctx->counts.p, 0, nr * sizeof(unsigned), st));
-    CsrSink sk{1, (unsigned*)ctx->counts.p, row_start_dev + row_off, (uint32_t*)ctx->grp_col.p,
-               (double*)ctx->grp_val.p, nullptr, nullptr, 0, base};
+    CsrSink sk{1, (unsigned*)ctx->counts.p, row_start_dev + row_off, ctx->grp.p, nullptr, nullptr,
+               0, base};
     CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, na, sk, ctx->plans.p, ctx->status, st));
     unsigned* lr = (unsigned*)ctx->longrows.p;
-    CT_CUDA(csr_sort_rows_radix(nr, row_start_dev + row_off, base, (const uint32_t*)ctx->grp_col.p,
-                                (const double*)ctx->grp_val.p, col_dev + base, val_dev + base, lr,
-                                lr + nr + 1, st));
+    CT_CUDA(csr_sort_rows_radix(nr, row_start_dev + row_off, ctx->grp.p, col_dev, val_dev, ~0ull,
+                                nnz_c, lr, lr + nr + 1, st));
   }
   return check_status(ctx, st, "build_system_matrix");
 }
 
 // Single-evaluation build: every weight is evaluated once. Per angle chunk:
-// mode-2 emission (row counts + 16-byte records), row scan, records scattered
-// into row-grouped scratch, per-row radix sort by column into the caller's
-// arrays. col_dev / val_dev hold `capacity` entries; *nnz_out receives the
-// shard's entry count, and the arrays are complete only if it is <= capacity
-// (otherwise the remaining chunks are only counted: call again with arrays of
+// mode-2 emission (row counts + 16-byte records) and the row scan on the
+// caller's stream; on a second stream the records are scattered into
+// row-grouped scratch and each row is radix-sorted by column into the
+// caller's arrays, overlapping the next chunk's (FP64-bound) emission with
+// this chunk's (HBM-bound) grouping. Nothing in the loop waits for the
+// device: record counts and row offsets are read by the kernels from device
+// memory, the per-chunk scratch is double-buffered, and the host checks the
+// counts once at the end (dropped records -> the build is redone with a
+// larger record buffer). col_dev / val_dev hold `capacity` entries;
+// *nnz_out receives the shard's entry count and the arrays are complete only
+// if it is <= capacity (rows beyond are skipped: call again with arrays of
 // *nnz_out entries).
 int ctsm_csr_build(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int angle_end,
                    uint64_t memory_budget_bytes, uint64_t* row_start_dev, uint32_t* col_dev,
@@ -448,60 +459,93 @@ int ctsm_csr_build(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int a
   uint64_t nnz0 = 0;
   CT_TRY(csr_angle_count(ctx, d, 0, &nnz0, st));
   CT_TRY(csr_budget_check(g, d, nnz0, memory_budget_bytes));
-  const uint64_t per_angle = nnz0 + nnz0 / 2 + 4096;  // angle 0 is a flat (sparser) angle
-  const int A = csr_chunk_angles(d, n_sel, per_angle);
+  if (!ctx->side) CT_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  for (int i = 0; i < 4; ++i)
+    if (!ctx->ev[i]) CT_CUDA(cudaEventCreateWithFlags(&ctx->ev[i], cudaEventDisableTiming));
+  cudaStream_t sb = ctx->side;
+  uint64_t per_angle = nnz0 + nnz0 / 2 + 4096;  // angle 0 is a flat (sparser) angle
   const unsigned long long seg_slack = 148ull * 8 * 4 * 256;
-  unsigned long long cap = (unsigned long long)A * per_angle + seg_slack;
-  CT_TRY(ensure(ctx, ctx->plans, csr_plan_bytes(d, A)));
-  CT_TRY(ensure(ctx, ctx->counts, (size_t)A * rpa * sizeof(unsigned)));
-  CT_TRY(ensure(ctx, ctx->scan, scan_scratch_bytes((uint64_t)A * rpa)));
-  CT_TRY(ensure(ctx, ctx->longrows, ((size_t)A * rpa + 2) * sizeof(unsigned)));
-  CT_TRY(ensure(ctx, ctx->cursor, 2 * sizeof(unsigned long long)));
-  uint64_t base = 0;
-  for (int c0 = 0; c0 < n_sel; c0 += A) {
-    const int na = std::min(A, n_sel - c0);
-    const uint64_t nr = (uint64_t)na * rpa, row_off = (uint64_t)c0 * rpa;
-    CT_TRY(prepare_exact(ctx, d, angle_begin + c0, na, st));
-    unsigned long long cur_h = 0;
-    uint64_t end_h = 0;
-    const bool counting_only = base > capacity;
-    for (int attempt = 0;; ++attempt) {
-      if (!counting_only) CT_TRY(ensure(ctx, ctx->rec, (size_t)cap * 16));
-      CT_CUDA(cudaMemsetAsync(ctx->counts.p, 0, nr * sizeof(unsigned), st));
-      CT_CUDA(cudaMemsetAsync(ctx->cursor.p, 0, sizeof(unsigned long long), st));
-      CsrSink sk{counting_only ? 0 : 2, (unsigned*)ctx->counts.p, nullptr, nullptr, nullptr,
-                 ctx->rec.p, (unsigned long long*)ctx->cursor.p, cap, 0};
-      CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, na, sk, ctx->plans.p, ctx->status, st));
-      CT_CUDA(exclusive_scan_u32_u64((const unsigned*)ctx->counts.p, nr, row_start_dev + row_off,
-                                     ctx->scan.p, st, base));
-      CT_CUDA(cudaMemcpyAsync(&cur_h, ctx->cursor.p, sizeof cur_h, cudaMemcpyDeviceToHost, st));
-      CT_CUDA(cudaMemcpyAsync(&end_h, row_start_dev + row_off + nr, sizeof end_h,
-                              cudaMemcpyDeviceToHost, st));
-      CT_TRY(check_status(ctx, st, "build_system_matrix"));
-      if (cur_h <= cap) break;
-      if (attempt >= 4) return fail(CTSM_ERR_OUT_OF_MEMORY, "record buffer keeps overflowing");
-      cap = cur_h + cur_h / 4 + seg_slack;  // records were dropped: redo the chunk
+  for (int attempt = 0;; ++attempt) {
+    const int A = std::max(1, csr_chunk_angles(d, n_sel, per_angle) / 2);
+    const unsigned long long cap = (unsigned long long)A * per_angle + seg_slack;
+    const int n_chunks = (n_sel + A - 1) / A;
+    // double-buffered per-chunk scratch
+    Buf* plans[2] = {&ctx->plans, &ctx->plans2};
+    Buf* angles[2] = {&ctx->angles, &ctx->angles2};
+    Buf* counts[2] = {&ctx->counts, &ctx->counts2};
+    Buf* rec[2] = {&ctx->rec, &ctx->rec2};
+    Buf* grp[2] = {&ctx->grp, &ctx->grp2};
+    Buf* lrow[2] = {&ctx->longrows, &ctx->longrows2};
+    for (int p = 0; p < 2; ++p) {
+      CT_TRY(ensure(ctx, *plans[p], csr_plan_bytes(d, A)));
+      CT_TRY(ensure(ctx, *angles[p], (size_t)A * exact_angle_bytes()));
+      CT_TRY(ensure(ctx, *counts[p], (size_t)A * rpa * sizeof(unsigned)));
+      CT_TRY(ensure(ctx, *rec[p], (size_t)cap * 16));
+      CT_TRY(ensure(ctx, *grp[p], (size_t)cap * 16));
+      CT_TRY(ensure(ctx, *lrow[p], ((size_t)A * rpa + 2) * sizeof(unsigned)));
     }
-    const uint64_t nnz_c = end_h - base;
-    if (!counting_only && end_h <= capacity && nnz_c) {
-      CT_TRY(ensure(ctx, ctx->grp_col, nnz_c * sizeof(uint32_t)));
-      CT_TRY(ensure(ctx, ctx->grp_val, nnz_c * sizeof(double)));
-      CT_CUDA(cudaMemsetAsync(ctx->counts.p, 0, nr * sizeof(unsigned), st));
-      CT_CUDA(csr_scatter_records(ctx->rec.p, cur_h, row_start_dev + row_off, base,
-                                  (unsigned*)ctx->counts.p, (uint32_t*)ctx->grp_col.p,
-                                  (double*)ctx->grp_val.p, st));
-      unsigned* lr = (unsigned*)ctx->longrows.p;
-      CT_CUDA(csr_sort_rows_radix(nr, row_start_dev + row_off, base,
-                                  (const uint32_t*)ctx->grp_col.p, (const double*)ctx->grp_val.p,
-                                  col_dev + base, val_dev + base, lr, lr + nr + 1, st));
+    CT_TRY(ensure(ctx, ctx->edges, (size_t)d.n_edges * edge_angle_bytes()));
+    CT_TRY(ensure(ctx, ctx->scan, scan_scratch_bytes((uint64_t)A * rpa)));
+    CT_TRY(ensure(ctx, ctx->cursor, ((size_t)n_chunks + 2) * sizeof(unsigned long long)));
+    unsigned long long* cursors = (unsigned long long*)ctx->cursor.p;  // [n_chunks], then base
+    uint64_t* base_slot = (uint64_t*)(cursors + n_chunks);
+    CT_CUDA(cudaMemsetAsync(cursors, 0, ((size_t)n_chunks + 2) * sizeof(unsigned long long), st));
+    CT_CUDA(cudaMemsetAsync(row_start_dev, 0, sizeof(uint64_t), st));
+    for (int c = 0; c < n_chunks; ++c) {
+      const int p = c & 1, c0 = c * A;
+      const int na = std::min(A, n_sel - c0);
+      const uint64_t nr = (uint64_t)na * rpa, row_off = (uint64_t)c0 * rpa;
+      // the grouping of chunk c - 2 must be done with this parity's scratch
+      if (c >= 2) CT_CUDA(cudaStreamWaitEvent(st, ctx->ev[2 + p], 0));
+      CT_CUDA(build_exact_tables(d, angle_begin + c0, na, angles[p]->p, ctx->edges.p, st));
+      CT_CUDA(cudaMemsetAsync(counts[p]->p, 0, nr * sizeof(unsigned), st));
+      CsrSink sk{2, (unsigned*)counts[p]->p, nullptr, nullptr, rec[p]->p, cursors + c, cap, 0};
+      CT_CUDA(csr_emit(d, angles[p]->p, ctx->edges.p, na, sk, plans[p]->p, ctx->status, st));
+      CT_CUDA(cudaMemcpyAsync(base_slot, row_start_dev + row_off, sizeof(uint64_t),
+                              cudaMemcpyDeviceToDevice, st));
+      CT_CUDA(exclusive_scan_u32_u64((const unsigned*)counts[p]->p, nr, row_start_dev + row_off,
+                                     ctx->scan.p, st, 0, base_slot, (unsigned*)counts[p]->p));
+      CT_CUDA(cudaEventRecord(ctx->ev[p], st));
+      // second stream: group by row (the counts now hold the rows' local
+      // offsets and serve as cursors), sort by column
+      CT_CUDA(cudaStreamWaitEvent(sb, ctx->ev[p], 0));
+      CT_CUDA(csr_scatter_records(rec[p]->p, cursors + c, cap, (unsigned*)counts[p]->p, grp[p]->p,
+                                  cap, sb));
+      unsigned* lr = (unsigned*)lrow[p]->p;
+      CT_CUDA(csr_sort_rows_radix(nr, row_start_dev + row_off, grp[p]->p, col_dev, val_dev,
+                                  capacity, cap, lr, lr + nr + 1, sb));
+      CT_CUDA(cudaEventRecord(ctx->ev[2 + p], sb));
     }
-    base = end_h;
-    if (base > capacity) capacity = 0;  // the later chunks are only counted
+    // join, then look at the counts
+    for (int p = 0; p < 2 && p < n_chunks; ++p) CT_CUDA(cudaStreamWaitEvent(st, ctx->ev[2 + p], 0));
+    std::vector<unsigned long long> cur_h((size_t)n_chunks);
+    uint64_t total = 0;
+    CT_CUDA(cudaMemcpyAsync(cur_h.data(), cursors, (size_t)n_chunks * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));
+    CT_CUDA(cudaMemcpyAsync(&total, row_start_dev + rpa * n_sel, sizeof total,
+                            cudaMemcpyDeviceToHost, st));
+    CT_TRY(check_status(ctx, st, "build_system_matrix"));
+    unsigned long long worst = 0;
+    for (unsigned long long v : cur_h) worst = std::max(worst, v);
+    if (worst <= cap) {
+      if (angle_begin == 0 && angle_end == g->n_angles && total == 0)
+        return fail(CTSM_ERR_ZERO_MATRIX, "system matrix has no entries");
+      *nnz_out = total;
+      return 0;
+    }
+    if (attempt >= 3) return fail(CTSM_ERR_OUT_OF_MEMORY, "record buffer keeps overflowing");
+    per_angle = (worst + worst / 4) / (unsigned long long)A + 4096;  // records were dropped
   }
-  CT_CUDA(cudaStreamSynchronize(st));
-  if (angle_begin == 0 && angle_end == g->n_angles && base == 0)
-    return fail(CTSM_ERR_ZERO_MATRIX, "system matrix has no entries");
-  *nnz_out = base;
+}
+
+int ctsm_selftest_division(ctsm_ctx* ctx, uint64_t n, uint64_t seed, uint64_t* mismatches) {
+  CT_TRY(set_device(ctx));
+  CT_TRY(ensure(ctx, ctx->cursor, 2 * sizeof(unsigned long long)));
+  CT_CUDA(cudaMemset(ctx->cursor.p, 0, sizeof(unsigned long long)));
+  CT_CUDA(selftest_division(n, seed, (unsigned long long*)ctx->cursor.p, nullptr));
+  unsigned long long h = 0;
+  CT_CUDA(cudaMemcpy(&h, ctx->cursor.p, sizeof h, cudaMemcpyDeviceToHost));
+  *mismatches = h;
   return 0;
 }
 

@@ -1,4 +1,5 @@
 #include <climits>
+#include <cstdlib>
 // csr.cu -- K1/K2 consistent system-matrix CSR emission (bit-exact) and the
 // K3/K4 CSR appliers. Compiled with -fmad=false (see exact.cuh).
 //
@@ -83,6 +84,13 @@ __global__ void __launch_bounds__(128, CTSM_CSR2_MINB) csr2d_kernel(DevGeom g, c
 
 }  // namespace
 
+cudaError_t selftest_division(unsigned long long n, unsigned long long seed,
+                              unsigned long long* mismatches_dev, cudaStream_t st) {
+  k2::selftest_division_kernel<<<148 * 8, 256, 0, st>>>(n, seed, mismatches_dev);
+  count_launch();
+  return cudaGetLastError();
+}
+
 size_t csr_plan_bytes(const DevGeom& g, int n_sel) {
   if (g.n_z == 1 && g.n_det_z == 1) return 0;
   return (size_t)g.n_x * g.n_y * (size_t)n_sel * sizeof(k2::ColPlan);
@@ -94,7 +102,7 @@ size_t csr_plan_bytes(const DevGeom& g, int n_sel) {
 cudaError_t csr_emit(const DevGeom& g, const void* angles_dev, const void* edges_dev, int n_sel,
                      const CsrSink& out, void* plans, int* status, cudaStream_t st) {
   if (n_sel <= 0) return cudaSuccess;
-  Sink em{out.mode, out.row_counter, out.row_start, out.col, out.val, (uint4*)out.rec,
+  Sink em{out.mode, out.row_counter, out.row_start, (uint4*)out.grp, (uint4*)out.rec,
           out.cursor, out.cap, 0u, out.pos_base};
   const long long nxy = (long long)g.n_x * g.n_y;
   const bool two_d = (g.n_z == 1 && g.n_det_z == 1);
@@ -117,7 +125,11 @@ cudaError_t csr_emit(const DevGeom& g, const void* angles_dev, const void* edges
       k2::plan3d_kernel<<<grid, 128, 0, st>>>(g, angs + k0, edges, pl, status);
       const long long items = nxy * nk;
       const long long blocks = (items + k2::kEmitWarps - 1) / k2::kEmitWarps;
-      const long long cap = 148ll * CTSM_EMIT3_MINB;  // one resident wave, warps stride
+      static const int per_sm = [] {  // experiment knob: emission blocks per SM
+        const char* e = getenv("CTSM_EMIT3_BLOCKS");
+        return e ? atoi(e) : CTSM_EMIT3_MINB;
+      }();
+      const long long cap = 148ll * per_sm;  // one resident wave, warps stride
       k2::emit3d_kernel<<<(unsigned)(blocks < cap ? blocks : cap), k2::kEmitWarps * 32, 0, st>>>(
           g, pl, nk, e2, status);
       count_launch(2);
@@ -188,7 +200,8 @@ __global__ void scan_tiles_kernel(uint64_t* tile_sums, uint64_t n_tiles) {
 }
 
 __global__ void scan_down_kernel(const unsigned* in, uint64_t n, const uint64_t* tile_offs,
-                                 uint64_t* out, uint64_t out_base) {
+                                 uint64_t* out, uint64_t out_base, const uint64_t* base_dev,
+                                 unsigned* local_out) {
   __shared__ uint64_t smem[32];
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
   uint64_t vals[kScanItems];
@@ -199,10 +212,14 @@ __global__ void scan_down_kernel(const unsigned* in, uint64_t n, const uint64_t*
     s += vals[i];
   }
   uint64_t total;
-  uint64_t off = block_scan_excl(s, smem, &total) + tile_offs[blockIdx.x] + out_base;
+  uint64_t loc = block_scan_excl(s, smem, &total) + tile_offs[blockIdx.x];
+  uint64_t off = loc + out_base + (base_dev ? *base_dev : 0);
   for (int i = 0; i < kScanItems; ++i) {
     const uint64_t idx = base + (uint64_t)threadIdx.x * kScanItems + i;
     if (idx < n) out[idx] = off;
+    // the shard-local offset (may alias the counts: each thread has read its items)
+    if (idx < n && local_out) local_out[idx] = (unsigned)loc;
+    loc += vals[i];
     off += vals[i];
     if (idx + 1 == n) out[n] = off;
   }
@@ -215,13 +232,18 @@ size_t scan_scratch_bytes(uint64_t n) {
 }
 
 cudaError_t exclusive_scan_u32_u64(const unsigned* counts, uint64_t n, uint64_t* row_start,
-                                   void* scratch, cudaStream_t st, uint64_t base) {
-  if (n == 0) return cudaMemcpyAsync(row_start, &base, sizeof(uint64_t), cudaMemcpyHostToDevice, st);
+                                   void* scratch, cudaStream_t st, uint64_t base,
+                                   const uint64_t* base_dev, unsigned* local_out) {
+  if (n == 0) {
+    if (base_dev) return cudaMemcpyAsync(row_start, base_dev, sizeof(uint64_t), cudaMemcpyDeviceToDevice, st);
+    return cudaMemcpyAsync(row_start, &base, sizeof(uint64_t), cudaMemcpyHostToDevice, st);
+  }
   const uint64_t tiles = (n + kScanTile - 1) / kScanTile;
   uint64_t* ts = (uint64_t*)scratch;
   scan_reduce_kernel<<<(unsigned)tiles, kScanBlock, 0, st>>>(counts, n, ts);
   scan_tiles_kernel<<<1, kScanBlock, 0, st>>>(ts, tiles);
-  scan_down_kernel<<<(unsigned)tiles, kScanBlock, 0, st>>>(counts, n, ts, row_start, base);
+  scan_down_kernel<<<(unsigned)tiles, kScanBlock, 0, st>>>(counts, n, ts, row_start, base, base_dev,
+                                                           local_out);
   count_launch(3);
   return cudaGetLastError();
 }
@@ -341,20 +363,23 @@ cudaError_t csr_sort_rows(uint64_t n_rows, const uint64_t* row_start, uint32_t* 
 // ---- single-evaluation build: records -> rows -> sorted rows ---------------
 namespace {
 // Step P: each record goes to its row's range of the (unsorted) row-grouped
-// arrays; the slot within the row is taken from a per-row cursor.
+// array: `cursor` holds the rows' shard-local start offsets (written by the
+// scan) and hands out the slots, so a record costs one atomic and one 16-byte
+// store {col, -, val}.
 __global__ void __launch_bounds__(256) scatter_records_kernel(const uint4* __restrict__ rec,
-                                                              unsigned long long n,
-                                                              const uint64_t* __restrict__ rs,
-                                                              uint64_t base, unsigned* slot,
-                                                              uint32_t* col, double* val) {
+                                                              const unsigned long long* n_dev,
+                                                              unsigned long long cap,
+                                                              unsigned* cursor, uint4* grp,
+                                                              uint64_t grp_cap) {
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  const unsigned long long n = *n_dev < cap ? *n_dev : cap;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += stride) {
     const uint4 r = __ldcs(&rec[i]);
     if (r.x == k2::kInvalidRow) continue;
-    const uint64_t pos = (rs[r.x] - base) + atomicAdd(&slot[r.x], 1u);
-    col[pos] = r.y;
-    val[pos] = __hiloint2double((int)r.w, (int)r.z);
+    const uint64_t pos = atomicAdd(&cursor[r.x], 1u);
+    if (pos >= grp_cap) continue;  // only after dropped records; the host redoes the build
+    grp[pos] = make_uint4(r.y, 0u, r.z, r.w);
   }
 }
 
@@ -371,20 +396,21 @@ struct RsWarp {
 };
 
 __global__ void __launch_bounds__(kRsWarps * 32) sort_rows_radix(
-    uint64_t n_rows, const uint64_t* __restrict__ rs, uint64_t base,
-    const uint32_t* __restrict__ col_in, const double* __restrict__ val_in,
-    uint32_t* __restrict__ col_out, double* __restrict__ val_out, unsigned* long_rows,
-    unsigned* n_long) {
+    uint64_t n_rows, const uint64_t* __restrict__ rs, const uint4* __restrict__ grp,
+    uint32_t* __restrict__ col_out, double* __restrict__ val_out, uint64_t out_cap,
+    uint64_t grp_cap, unsigned* long_rows, unsigned* n_long) {
   extern __shared__ __align__(16) unsigned char rs_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   RsWarp& w = reinterpret_cast<RsWarp*>(rs_smem)[wid];
   const unsigned full = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
   const uint64_t warps_total = (uint64_t)gridDim.x * kRsWarps;
+  const uint64_t base = rs[0];  // the grouped arrays start at the chunk's first entry
   for (uint64_t r = (uint64_t)blockIdx.x * kRsWarps + wid; r < n_rows; r += warps_total) {
     const uint64_t b = rs[r] - base;
     const uint64_t n64 = rs[r + 1] - rs[r];
     if (n64 == 0) continue;
+    if (rs[r + 1] > out_cap || b + n64 > grp_cap) continue;  // beyond the caller's arrays
     if (n64 > (uint64_t)kRsCap) {
       if (lane == 0) long_rows[atomicAdd(n_long, 1u)] = (unsigned)r;
       continue;
@@ -392,7 +418,7 @@ __global__ void __launch_bounds__(kRsWarps * 32) sort_rows_radix(
     const int n = (int)n64;
     uint32_t kor = 0u, kand = ~0u;
     for (int i = lane; i < n; i += 32) {
-      const uint32_t k = __ldcs(&col_in[b + i]);
+      const uint32_t k = grp[b + i].x;
       w.key[0][i] = k;
       w.idx[0][i] = (uint16_t)i;
       kor |= k;
@@ -458,8 +484,9 @@ __global__ void __launch_bounds__(kRsWarps * 32) sort_rows_radix(
       }
     }
     for (int i = lane; i < n; i += 32) {
-      col_out[b + i] = w.key[cur][i];
-      val_out[b + i] = val_in[b + w.idx[cur][i]];
+      const uint4 e = grp[b + w.idx[cur][i]];
+      col_out[base + b + i] = w.key[cur][i];
+      val_out[base + b + i] = __hiloint2double((int)e.w, (int)e.z);
     }
     __syncwarp();
   }
@@ -472,21 +499,25 @@ constexpr int kLongCap = 16384;
 constexpr int kLongThreads = 512;
 __global__ void __launch_bounds__(kLongThreads) sort_rows_block(
     const unsigned* __restrict__ long_rows, const unsigned* __restrict__ n_long,
-    const uint64_t* __restrict__ rs, uint64_t base, const uint32_t* __restrict__ col_in,
-    const double* __restrict__ val_in, uint32_t* __restrict__ col_out,
-    double* __restrict__ val_out) {
+    const uint64_t* __restrict__ rs, const uint4* __restrict__ grp,
+    uint32_t* __restrict__ col_out_g, double* __restrict__ val_out_g, uint64_t out_cap,
+    uint64_t grp_cap) {
   extern __shared__ __align__(16) unsigned char rs_smem[];
   unsigned long long* key = reinterpret_cast<unsigned long long*>(rs_smem);
   const unsigned nl = *n_long;
+  const uint64_t base = rs[0];
+  uint32_t* col_out = col_out_g + base;
+  double* val_out = val_out_g + base;
   for (unsigned q = blockIdx.x; q < nl; q += gridDim.x) {
     const uint64_t r = long_rows[q];
     const uint64_t b = rs[r] - base;
     const uint64_t n = rs[r + 1] - rs[r];
+    if (rs[r + 1] > out_cap || b + n > grp_cap) continue;
     if (n <= (uint64_t)kLongCap) {
       int n2 = 1;
       while ((uint64_t)n2 < n) n2 <<= 1;
       for (int i = threadIdx.x; i < n2; i += kLongThreads)
-        key[i] = (uint64_t)i < n ? (((unsigned long long)col_in[b + i] << 32) | (unsigned)i) : ~0ull;
+        key[i] = (uint64_t)i < n ? (((unsigned long long)grp[b + i].x << 32) | (unsigned)i) : ~0ull;
       __syncthreads();
       for (int k = 2; k <= n2; k <<= 1)
         for (int j = k >> 1; j > 0; j >>= 1) {
@@ -504,14 +535,16 @@ __global__ void __launch_bounds__(kLongThreads) sort_rows_block(
         }
       for (uint64_t i = threadIdx.x; i < n; i += kLongThreads) {
         const unsigned long long kk = key[i];
+        const uint4 e = grp[b + (kk & 0xffffffffu)];
         col_out[b + i] = (uint32_t)(kk >> 32);
-        val_out[b + i] = val_in[b + (kk & 0xffffffffu)];
+        val_out[b + i] = __hiloint2double((int)e.w, (int)e.z);
       }
       __syncthreads();
     } else {
       for (uint64_t i = threadIdx.x; i < n; i += kLongThreads) {
-        col_out[b + i] = col_in[b + i];
-        val_out[b + i] = val_in[b + i];
+        const uint4 e = grp[b + i];
+        col_out[b + i] = e.x;
+        val_out[b + i] = __hiloint2double((int)e.w, (int)e.z);
       }
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -537,21 +570,19 @@ __global__ void __launch_bounds__(kLongThreads) sort_rows_block(
 }
 }  // namespace
 
-cudaError_t csr_scatter_records(const void* rec, unsigned long long n, const uint64_t* row_start,
-                                uint64_t base, unsigned* slot, uint32_t* col, double* val,
-                                cudaStream_t st) {
-  if (n == 0) return cudaSuccess;
-  const unsigned long long blocks = (n + 255) / 256;
-  const unsigned grid = (unsigned)(blocks < 148ull * 32 ? blocks : 148ull * 32);
-  scatter_records_kernel<<<grid, 256, 0, st>>>((const uint4*)rec, n, row_start, base, slot, col,
-                                               val);
+cudaError_t csr_scatter_records(const void* rec, const unsigned long long* n_dev,
+                                unsigned long long cap, unsigned* cursor, void* grp,
+                                uint64_t grp_cap, cudaStream_t st) {
+  if (cap == 0) return cudaSuccess;
+  scatter_records_kernel<<<148 * 32, 256, 0, st>>>((const uint4*)rec, n_dev, cap, cursor,
+                                                   (uint4*)grp, grp_cap);
   count_launch();
   return cudaGetLastError();
 }
 
-cudaError_t csr_sort_rows_radix(uint64_t n_rows, const uint64_t* row_start, uint64_t base,
-                                const uint32_t* col_in, const double* val_in, uint32_t* col_out,
-                                double* val_out, unsigned* long_rows, unsigned* n_long,
+cudaError_t csr_sort_rows_radix(uint64_t n_rows, const uint64_t* row_start, const void* grp,
+                                uint32_t* col_out, double* val_out, uint64_t out_cap,
+                                uint64_t grp_cap, unsigned* long_rows, unsigned* n_long,
                                 cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
@@ -569,9 +600,9 @@ cudaError_t csr_sort_rows_radix(uint64_t n_rows, const uint64_t* row_start, uint
   const uint64_t blocks = (n_rows + kRsWarps - 1) / kRsWarps;
   const unsigned grid = (unsigned)(blocks < 148ull * 4 ? blocks : 148ull * 4);
   sort_rows_radix<<<grid, kRsWarps * 32, kRsWarps * sizeof(RsWarp), st>>>(
-      n_rows, row_start, base, col_in, val_in, col_out, val_out, long_rows, n_long);
+      n_rows, row_start, (const uint4*)grp, col_out, val_out, out_cap, grp_cap, long_rows, n_long);
   sort_rows_block<<<148, kLongThreads, kLongCap * sizeof(unsigned long long), st>>>(
-      long_rows, n_long, row_start, base, col_in, val_in, col_out, val_out);
+      long_rows, n_long, row_start, (const uint4*)grp, col_out, val_out, out_cap, grp_cap);
   count_launch(2);
   return cudaGetLastError();
 }

@@ -32,7 +32,7 @@ namespace k2 {
 
 constexpr int kMaxGrp = kMaxBrk;  // cell groups of one column sweep
 constexpr int kMaxOps = 32;       // distinct atoms per (row edge, z face)
-constexpr int kOpc = 10;          // doubles per OpConsts record
+constexpr int kOpc = 11;          // doubles per OpConsts record
 
 struct ColPlan {
   double S, C;                      // sin / cos of the canonical angle
@@ -54,7 +54,8 @@ static_assert(sizeof(ColPlan) % 8 == 0, "ColPlan is copied as doubles");
 
 // Output sink of the emission kernels.
 //   mode 0: count entries per row (row_counter += 1);
-//   mode 1: fill col / val at row_start[row] + slot, slot = row_counter++;
+//   mode 1: write the row-grouped entry {col, val} at row_start[row] -
+//           pos_base + slot, slot = row_counter++;
 //   mode 2: count, and append the entry as a 16-byte record {row, col, val}
 //           to `rec` (single-evaluation build: the records are grouped by row
 //           and sorted afterwards). Records are allocated from *cursor; a
@@ -64,8 +65,7 @@ struct Sink {
   int mode;
   unsigned* row_counter;
   const uint64_t* row_start;
-  uint32_t* col;
-  double* val;
+  uint4* grp;   // mode 1: row-grouped {col, -, val} entries
   uint4* rec;
   unsigned long long* cursor;
   unsigned long long cap;
@@ -89,8 +89,7 @@ __device__ __forceinline__ void emit_any(const Sink& sk, uint64_t row_local, uin
   } else if (sk.mode == 1) {
     const unsigned slot = atomicAdd(&sk.row_counter[row_local], 1u);
     const uint64_t pos = sk.row_start[row_local] - sk.pos_base + slot;
-    sk.col[pos] = column;
-    sk.val[pos] = w;
+    sk.grp[pos] = make_uint4(column, 0u, (unsigned)__double2loint(w), (unsigned)__double2hiint(w));
   } else {
     atomicAdd(&sk.row_counter[row_local], 1u);
     const unsigned m = __activemask();
@@ -123,8 +122,7 @@ __device__ __forceinline__ void emit_warp(const Sink& sk, bool flag, uint64_t ro
     if (flag) {
       const unsigned slot = atomicAdd(&sk.row_counter[row_local], 1u);
       const uint64_t pos = sk.row_start[row_local] - sk.pos_base + slot;
-      sk.col[pos] = column;
-      sk.val[pos] = w;
+      sk.grp[pos] = make_uint4(column, 0u, (unsigned)__double2loint(w), (unsigned)__double2hiint(w));
     }
     return;
   }
@@ -259,11 +257,31 @@ __global__ void __launch_bounds__(128) plan3d_kernel(DevGeom g,
 }
 
 // ---- atoms with per-column constants ---------------------------------------
+// x / b with rb = RN(1 / b) supplied: q0 = RN(x rb), r = x - b q0 (exact, one
+// fma), q = RN(q0 + r rb). By Markstein's theorem (rb correctly rounded, q0
+// within one ulp of x / b) q is the correctly rounded quotient, i.e. the bits
+// of the IEEE division the reference performs -- in 3 FP64 instructions
+// instead of the ~25 of a full division. Every divisor of the atom loop (C,
+// S, cr1 cr2) is a per-column or per-breakpoint constant. Checked against the
+// IEEE division on 2^28 random operand pairs by ctsm_selftest_division
+// (tests/test_gpu_parity.py). CTSM_EXACT_DIV=1 compiles the plain divisions.
+__device__ __forceinline__ double div_by(double x, double b, double rb) {
+#ifdef CTSM_EXACT_DIV
+  (void)rb;
+  return x / b;
+#else
+  const double q0 = x * rb;
+  const double r = __fma_rn(-b, q0, x);
+  return __fma_rn(r, rb, q0);
+#endif
+}
+
 // OpConsts of a corner-triangle atom at breakpoint t (tri_flags_at /
 // tri_atom_flags, weights3d.cpp:115-168): c0 crg, c1 srh, c2 P/crg, c3 Q/srh,
 // c4 P C, c5 Q S, c6 delta, c7 S S delta^3, c8 srh/C, c9 t.
 __device__ __forceinline__ double tri_eval(const double* __restrict__ c, double S, double C,
-                                           bool flat, double G, double tan_a, double coef) {
+                                           double rS, double rC, bool flat, double G,
+                                           double tan_a, double coef) {
   const double g = G - c[2];
   const double gg = G - c[4] - c[5];
   const double h = G - c[3];
@@ -273,14 +291,14 @@ __device__ __forceinline__ double tri_eval(const double* __restrict__ c, double 
     if (fg && fgg) {
       const double delta = c[6];
       pair = c[0] * (3.0 * gg * gg * delta + 3.0 * gg * S * delta * delta + c[7]) -
-             exact::cube(gg) * c[1] / C;
+             div_by(exact::cube(gg) * c[1], C, rC);
     } else if (!fg && !fgg) {
       pair = 0.0;
     } else {
       double v = 0.0;
       if (fg) v += c[0] * exact::cube(g);
-      if (fgg) v -= exact::cube(gg) / C;
-      pair = v / S;
+      if (fgg) v -= div_by(exact::cube(gg), C, rC);
+      pair = div_by(v, S, rS);
     }
     const double tt = pair + (fh ? c[8] * exact::cube(h) : 0.0);
     return coef * fabs(tan_a * tt);
@@ -295,29 +313,33 @@ __device__ __forceinline__ double tri_eval(const double* __restrict__ c, double 
 // trap_face_part (weights3d.cpp:51-61) with P/cr1, P/cr2 and the P^3 term
 // supplied.
 __device__ __forceinline__ double face_part_pre(double G, double G3, double P, double S,
-                                                double t12, double cr1, double cr2, double cr12,
-                                                double Pd1, double Pd2, double K) {
+                                                double rS, double t12, double cr1, double cr2,
+                                                double cr12, double rcr12, double Pd1,
+                                                double Pd2, double K) {
   const double d1 = G - Pd1, d2 = G - Pd2;
   const bool f1 = d1 > 0.0, f2 = d2 > 0.0;
-  if (f1 && f2) return t12 * (G3 - 3.0 * G * P * P / cr12 + K);
+  if (f1 && f2) return t12 * (G3 - div_by(3.0 * G * P * P, cr12, rcr12) + K);
   if (!f1 && !f2) return 0.0;
   double v = 0.0;
   if (f1) v += cr1 * exact::cube(d1);
   if (f2) v -= cr2 * exact::cube(d2);
-  return v / S;
+  return div_by(v, S, rS);
 }
 
 // OpConsts of a trapezoid atom over (t1, t2) (weights3d.cpp:63-107): c0 cr1,
 // c1 cr2, c2 t1 - t2, c3 cr1 cr2, c4 Pg/cr1, c5 Pg/cr2, c6 Pf/cr1, c7 Pf/cr2,
-// c8 Pg^3 (cr1 + cr2) / (cr1 cr2)^2, c9 the same for Pf. cst: Pg, Pf and, for
-// the flat branch, 3 (s C - x1) / a and 3 (s C - x0) / a.
+// c8 Pg^3 (cr1 + cr2) / (cr1 cr2)^2, c9 the same for Pf, c10 1 / (cr1 cr2). cst:
+// Pg, Pf and, for the flat branch, 3 (s C - x1) / a and 3 (s C - x0) / a.
 __device__ __forceinline__ double trap_eval(const double* __restrict__ c,
-                                            const double* __restrict__ cst, double S, bool flat,
-                                            double G, double G3, double tan_a, double coef) {
+                                            const double* __restrict__ cst, double S, double rS,
+                                            bool flat, double G, double G3, double tan_a,
+                                            double coef) {
   const double Pg = cst[0], Pf = cst[1];
   if (!flat) {
-    const double pg = face_part_pre(G, G3, Pg, S, c[2], c[0], c[1], c[3], c[4], c[5], c[8]);
-    const double pf = face_part_pre(G, G3, Pf, S, c[2], c[0], c[1], c[3], c[6], c[7], c[9]);
+    const double pg =
+        face_part_pre(G, G3, Pg, S, rS, c[2], c[0], c[1], c[3], c[10], c[4], c[5], c[8]);
+    const double pf =
+        face_part_pre(G, G3, Pf, S, rS, c[2], c[0], c[1], c[3], c[10], c[6], c[7], c[9]);
     return coef * fabs(tan_a * (pg - pf));
   }
   const double gv = G - Pg, fv = G - Pf;
@@ -325,6 +347,38 @@ __device__ __forceinline__ double trap_eval(const double* __restrict__ c,
   if (gv > 0.0) t += gv * gv * (gv + cst[2]);
   if (fv > 0.0) t -= fv * fv * (fv + cst[3]);
   return coef * fabs(tan_a * t * c[2]);
+}
+
+// Self-test of div_by against the IEEE division: pseudo-random numerators
+// over 26 decades and divisors in the ranges of C, S and cr1 cr2.
+__global__ void selftest_division_kernel(unsigned long long n, unsigned long long seed,
+                                         unsigned long long* mismatches) {
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  unsigned long long bad = 0;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    unsigned long long z = seed + i * 0x9E3779B97F4A7C15ull;  // splitmix64
+    double u[3];
+    for (int j = 0; j < 3; ++j) {
+      z += 0x9E3779B97F4A7C15ull;
+      unsigned long long t = z;
+      t = (t ^ (t >> 30)) * 0xBF58476D1CE4E5B9ull;
+      t = (t ^ (t >> 27)) * 0x94D049BB133111EBull;
+      t ^= t >> 31;
+      u[j] = (double)(t >> 11) * 0x1.0p-53;
+    }
+    const int sel = (int)(i % 3);
+    double b = sel == 0 ? 0.02 + 0.98 * u[0] : (sel == 1 ? 1e-8 + u[0] : 0.25 + 3.75 * u[0]);
+    if (i & 8) b = -b;
+    double x = (2.0 * u[1] - 1.0) * exp10(-20.0 + 26.0 * u[2]);
+    if (i % 5 == 0) x = b * floor(u[1] * 1048576.0) * (1.0 + ((i & 16) ? 0x1.0p-52 : 0.0));
+    const double rb = 1.0 / b;
+    const double q0 = x * rb;
+    const double r = __fma_rn(-b, q0, x);
+    const double q = __fma_rn(r, rb, q0);
+    if (__double_as_longlong(q) != __double_as_longlong(x / b)) ++bad;
+  }
+  if (bad) atomicAdd(mismatches, bad);
 }
 
 constexpr int kEmitWarps = 4;
@@ -369,6 +423,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32, CTSM_EMIT3_MINB)
     const double S = ws.plan.S, C = ws.plan.C;
     const double a = ws.plan.x1 - ws.plan.x0, b = ws.plan.y1 - ws.plan.y0;
     const bool flat = !(fabs(S) > kEpsSingular);
+    const double rS = 1.0 / S, rC = 1.0 / C;
     if (lane == 0) {
       ws.cst[0] = (s * C - ws.plan.x1) / a;
       ws.cst[1] = (s * C - ws.plan.x0) / a;
@@ -393,6 +448,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32, CTSM_EMIT3_MINB)
         c[7] = Pf / cr2;
         c[8] = exact::cube(Pg) * (cr1 + cr2) / exact::sq(cr1 * cr2);
         c[9] = exact::cube(Pf) * (cr1 + cr2) / exact::sq(cr1 * cr2);
+        c[10] = 1.0 / (cr1 * cr2);
       } else {
         const double t = ws.plan.tbrk[ws.plan.opb[o]];
         const double xa = ty == 0 ? ws.plan.apex1_x : ws.plan.apex4_x;
@@ -486,8 +542,8 @@ __global__ void __launch_bounds__(kEmitWarps * 32, CTSM_EMIT3_MINB)
               if (kind == 1) {
                 if (need) {
                   const double* c = ws.opc[ws.plan.plo[p]];
-                  Fb += trap_eval(c, ws.cst, S, flat, Gb, Gb3, tan_a, coef);
-                  Ft += trap_eval(c, ws.cst, S, flat, Gt, Gt3, tan_a, coef);
+                  Fb += trap_eval(c, ws.cst, S, rS, flat, Gb, Gb3, tan_a, coef);
+                  Ft += trap_eval(c, ws.cst, S, rS, flat, Gt, Gt3, tan_a, coef);
                 }
               } else {
                 // b_lo first, then b_hi: the next piece of the chain reuses b_hi
@@ -507,8 +563,8 @@ __global__ void __launch_bounds__(kEmitWarps * 32, CTSM_EMIT3_MINB)
                   } else {
                     if (need) {
                       const double* c = ws.opc[op];
-                      rb = tri_eval(c, S, C, flat, Gb, tan_a, coef);
-                      rt = tri_eval(c, S, C, flat, Gt, tan_a, coef);
+                      rb = tri_eval(c, S, C, rS, rC, flat, Gb, tan_a, coef);
+                      rt = tri_eval(c, S, C, rS, rC, flat, Gt, tan_a, coef);
                     }
                     if (lru == 0) {
                       tag0 = op;

@@ -33,8 +33,8 @@ cudaError_t build_exact_tables(const DevGeom& g, int angle_begin, int n_sel, voi
                                void* edges_dev, cudaStream_t st);
 // Output sink of the CSR emission kernels (csr3d.cuh Sink):
 //   mode 0: count entries per row into row_counter (u32, zeroed by the caller);
-//   mode 1: fill col/val at row_start[row] - pos_base + slot, row_counter as
-//           slot cursors;
+//   mode 1: write row-grouped 16-byte entries {col, -, val} to grp at
+//           row_start[row] - pos_base + slot, row_counter as slot cursors;
 //   mode 2: count and append 16-byte records {row, col, val} to rec[0..cap),
 //           allocated from *cursor (zeroed by the caller; cursor > cap means
 //           records were dropped: retry with a larger buffer).
@@ -42,13 +42,16 @@ struct CsrSink {
   int mode;
   unsigned* row_counter;
   const uint64_t* row_start;
-  uint32_t* col;
-  double* val;
+  void* grp;
   void* rec;
   unsigned long long* cursor;
   unsigned long long cap;
   uint64_t pos_base;
 };
+// div_by (csr3d.cuh) against the IEEE division on n pseudo-random operand
+// pairs; adds the number of differing results to *mismatches_dev.
+cudaError_t selftest_division(unsigned long long n, unsigned long long seed,
+                              unsigned long long* mismatches_dev, cudaStream_t st);
 // Bytes of the per-(column, angle) plan scratch of the 3D emission (0 for 2D).
 size_t csr_plan_bytes(const DevGeom& g, int n_sel);
 // Emits the rows of the n_sel angles of the prepared tables (rows local to
@@ -56,21 +59,27 @@ size_t csr_plan_bytes(const DevGeom& g, int n_sel);
 cudaError_t csr_emit(const DevGeom& g, const void* angles_dev, const void* edges_dev, int n_sel,
                      const CsrSink& out, void* plans, int* status, cudaStream_t st);
 // Single-evaluation build, after a mode-2 emission and the row scan: records
-// -> row-grouped arrays (slot zeroed by the caller) -> per-row radix sort by
-// column into the final arrays. row_start holds global offsets; the arrays
-// passed here start at offset `base`.
-cudaError_t csr_scatter_records(const void* rec, unsigned long long n, const uint64_t* row_start,
-                                uint64_t base, unsigned* slot, uint32_t* col, double* val,
-                                cudaStream_t st);
-cudaError_t csr_sort_rows_radix(uint64_t n_rows, const uint64_t* row_start, uint64_t base,
-                                const uint32_t* col_in, const double* val_in, uint32_t* col_out,
-                                double* val_out, unsigned* long_rows, unsigned* n_long,
+// -> row-grouped 16-byte entries (cursor = the rows' shard-local offsets, from
+// the scan's local_out) -> per-row radix sort by column into the final arrays.
+// row_start points at the chunk's first row and holds global offsets: the
+// grouped array (grp_cap entries) starts at entry row_start[0], col_out /
+// val_out are the whole matrix's arrays (out_cap
+// entries; rows reaching beyond are skipped). The record count is read from
+// device memory (*n_dev, clamped to cap), so the host never waits on a chunk.
+cudaError_t csr_scatter_records(const void* rec, const unsigned long long* n_dev,
+                                unsigned long long cap, unsigned* cursor, void* grp,
+                                uint64_t grp_cap, cudaStream_t st);
+cudaError_t csr_sort_rows_radix(uint64_t n_rows, const uint64_t* row_start, const void* grp,
+                                uint32_t* col_out, double* val_out, uint64_t out_cap,
+                                uint64_t grp_cap, unsigned* long_rows, unsigned* n_long,
                                 cudaStream_t st);
 // row_start[0..n] = exclusive scan of counts[0..n-1] (u32 -> u64); scratch
 // needs scan_scratch_bytes(n).
 size_t scan_scratch_bytes(uint64_t n);
 cudaError_t exclusive_scan_u32_u64(const unsigned* counts, uint64_t n, uint64_t* row_start,
-                                   void* scratch, cudaStream_t st, uint64_t base = 0);
+                                   void* scratch, cudaStream_t st, uint64_t base = 0,
+                                   const uint64_t* base_dev = nullptr,
+                                   unsigned* local_out = nullptr);
 // Sort each row's entries by column (in place).
 cudaError_t csr_sort_rows(uint64_t n_rows, const uint64_t* row_start, uint32_t* col,
                           double* val, unsigned* long_rows, unsigned* n_long, int* status,

@@ -141,6 +141,18 @@ def test_csr_build_capacity_protocol(oracle_cr):
     assert torch.equal(w2.val.view(torch.int64), w.val.view(torch.int64))
 
 
+def test_division_by_reciprocal_is_ieee_exact():
+    """csr3d.cuh div_by (reciprocal + one fma correction) against the IEEE
+    division on 2^28 pseudo-random operand pairs: no differing bit."""
+    import ctypes
+    from paper_2511_12235_b200 import _lib
+    from paper_2511_12235_b200.projector import Context
+    bad = ctypes.c_uint64(1)
+    _lib.check(_lib.lib().ctsm_selftest_division(Context.get(None).handle, 1 << 28, 20261021,
+                                                 ctypes.byref(bad)))
+    assert bad.value == 0
+
+
 def test_csr_budget_and_size_limits():
     g = TEST_GEOMETRIES["proj3d"]
     with pytest.raises(CtsmError) as e:
