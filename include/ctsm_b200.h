@@ -106,6 +106,29 @@ int ctsm_csr_build(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int a
                    uint64_t memory_budget_bytes, uint64_t* row_start_dev, uint32_t* col_dev,
                    double* val_dev, uint64_t capacity, uint64_t* nnz_out, void* stream);
 
+/* ---- the reference's weight API -------------------------------------------
+ * ctsm_weights_batch: pixel_area_factors (weights2d.hpp:31-32,
+ * weights2d.cpp:105-129) / voxel_volume_factors (weights3d.hpp:90-91,
+ * weights3d.cpp:354-462) for n (voxel, phi) queries given as HOST arrays (iz
+ * may be NULL for 2D). Query q's weights are written, in the reference's
+ * order (ascending m_y, then m_z), to entries [q*cap, q*cap + count[q]) of
+ * the host arrays m_y, m_z (may be NULL for 2D) and w. Bit-identical to the
+ * reference with a correctly rounded libm. TooLarge if a query has more than
+ * cap weights; the reference's guards raise their codes.
+ * ctsm_angle_block_entries: detail::angle_block_entries (projector.hpp:72-78,
+ * projector.cpp:44-84): every (raster row, column, weight) entry of one angle
+ * block into DEVICE arrays of `capacity` entries, in the reference's emission
+ * order (consistent: voxels z -> y -> x, each voxel's weights by (m_y, m_z);
+ * line / multiline: row by row). *n_out receives the entry count; the arrays
+ * are complete only if it is <= capacity (ctsm_csr_angle_nnz gives the count
+ * of the consistent mode beforehand). */
+int ctsm_weights_batch(ctsm_ctx* ctx, const ctsm_geometry* g, uint64_t n, const int32_t* ix,
+                       const int32_t* iy, const int32_t* iz, const double* phi, int cap,
+                       int32_t* count, int32_t* m_y, int32_t* m_z, double* w);
+int ctsm_angle_block_entries(ctsm_ctx* ctx, const ctsm_geometry* g, int mode, int k, int angle,
+                             uint64_t capacity, uint32_t* raster_dev, uint32_t* col_dev,
+                             double* w_dev, uint64_t* n_out, void* stream);
+
 /* ---- K3/K4: CSR appliers (forward_project / back_project,
  * projector.cpp:203-233). Deterministic; NonFinite check as the reference. */
 int ctsm_spmv(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols, const uint64_t* row_start_dev,
@@ -300,6 +323,33 @@ int ctsm_forward_project_matrix_free_host_f32(ctsm_ctx* ctx, const ctsm_geometry
                                               const float* x_host, float* y_host);
 int ctsm_back_project_matrix_free_host_f32(ctsm_ctx* ctx, const ctsm_geometry* g,
                                            const float* y_host, float* x_host);
+
+/* ---- multi-GPU context --------------------------
+ * One process, n devices: each device gets its own ctsm_ctx and stream, the
+ * angles are sharded over the devices (ctsm_shard_angles: by symmetry orbits
+ * for quarter-turn / dihedral scans, else strided), A x needs no
+ * communication, and A^T y / SIRT sum the partial volumes with ncclAllReduce
+ * over the devices' communicators (ncclCommInitAll; NCCL is bound at run time
+ * from libnccl.so.2). Operands are HOST arrays of the dtype; x is replicated.
+ * With one device no NCCL call is made (unless CTSM_MULTI_FORCE_NCCL=1, which
+ * runs the one-rank communicator: used by the tests on single-GPU boxes).
+ * ctsm_shard_angles: the angles (ascending) of rank `rank` of `world`, their
+ * count, and whether the shard is an orbit shard (base angles rank, rank +
+ * world, ... with all their images) -- the partition torch.distributed
+ * callers (paper_2511_12235_b200/dist.py) and this context share. */
+typedef struct ctsm_multi ctsm_multi;
+int ctsm_shard_angles(const ctsm_geometry* g, int rank, int world, int* angles_out, int* n_out,
+                      int* orbits_out);
+int ctsm_multi_create(const int* devices, int n, ctsm_multi** out);
+int ctsm_multi_destroy(ctsm_multi* m);
+int ctsm_multi_size(const ctsm_multi* m);
+int ctsm_multi_nccl_version(const ctsm_multi* m); /* 0 if no communicator was created */
+int ctsm_multi_forward_project_matrix_free_host(ctsm_multi* m, const ctsm_geometry* g, int dtype,
+                                                const void* x_host, void* y_host);
+int ctsm_multi_back_project_matrix_free_host(ctsm_multi* m, const ctsm_geometry* g, int dtype,
+                                             const void* y_host, void* x_host);
+int ctsm_multi_sirt_host(ctsm_multi* m, const ctsm_geometry* g, int dtype, const void* y_host,
+                         void* x_inout_host, int iters);
 
 /* ---- diagnostics ---------------------------------------------------------
  * ctsm_selftest_division: the exact 3D emission divides by per-column

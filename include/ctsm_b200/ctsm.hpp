@@ -9,6 +9,8 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -81,6 +83,45 @@ struct ScanGeometry {
   }
 };
 
+// geometry.hpp:66-84
+struct VoxelIndex {
+  int ix = 0, iy = 0, iz = 0;
+};
+struct DetectorIndex {
+  int m_y = 0, m_z = 0;
+};
+inline std::uint64_t voxel_column(const ScanGeometry& g, const VoxelIndex& n) {
+  return (std::uint64_t(n.iz) * g.n_y + n.iy) * g.n_x + n.ix;
+}
+inline std::uint64_t measurement_row(const ScanGeometry& g, int angle_index,
+                                     const DetectorIndex& m) {
+  const std::uint64_t raster =
+      std::uint64_t(m.m_z + g.n_det_z / 2) * g.n_det_y + (m.m_y + g.n_det_y / 2);
+  return std::uint64_t(angle_index) * g.n_det_y * g.n_det_z + raster;
+}
+
+// weights2d.hpp:20-32 / weights3d.hpp:82-91: the consistent weights of one
+// pixel / voxel at fan angle phi, evaluated on the device (bit-identical to
+// the reference with a correctly rounded libm), in the reference's order.
+struct CellWeight {
+  int m_y = 0;
+  double w = 0;
+};
+struct VoxelWeight {
+  int m_y = 0, m_z = 0;
+  double w = 0;
+};
+std::vector<CellWeight> pixel_area_factors(const VoxelIndex& n, double phi, const ScanGeometry& g);
+std::vector<VoxelWeight> voxel_volume_factors(const VoxelIndex& n, double phi,
+                                              const ScanGeometry& g);
+// Additions: many (voxel, phi) queries in one device launch.
+std::vector<std::vector<CellWeight>> pixel_area_factors(const std::vector<VoxelIndex>& n,
+                                                        const std::vector<double>& phi,
+                                                        const ScanGeometry& g);
+std::vector<std::vector<VoxelWeight>> voxel_volume_factors(const std::vector<VoxelIndex>& n,
+                                                           const std::vector<double>& phi,
+                                                           const ScanGeometry& g);
+
 // projector.hpp:12-16
 enum class MatrixMode { consistent, line, multiline };
 
@@ -114,6 +155,66 @@ double spectral_norm_power(const SparseSystemMatrix& w, int iters = 100, std::ui
 void scale_values(SparseSystemMatrix* w, double factor);
 std::vector<double> angle_column_sums(const ScanGeometry& g, MatrixMode mode, int k,
                                       int angle_index);
+namespace detail {
+// projector.hpp:72-78: every (local row, column, weight) entry of one angle
+// block, emitted in the reference's order (projector.cpp:44-84); the entries
+// are evaluated and ordered on the device and streamed to the callback.
+void angle_block_entries(const ScanGeometry& g, MatrixMode mode, int k, int angle_index,
+                         const std::function<void(std::uint32_t, std::uint32_t, double)>& emit);
+}  // namespace detail
+
+// Additions: fp32 operands (BASELINE configs 3 and 4; the
+// weights are still evaluated in FP64).
+std::vector<float> forward_project_matrix_free(const ScanGeometry& g, MatrixMode mode, int k,
+                                               const std::vector<float>& x, int threads = 1);
+std::vector<float> back_project_matrix_free(const ScanGeometry& g, MatrixMode mode, int k,
+                                            const std::vector<float>& y, int threads = 1);
+
+// Addition: a system matrix resident on the device. The value-semantics calls
+// above upload the CSR on every call (as the reference's signatures demand);
+// a DeviceSystemMatrix is uploaded (or built in place) once and applied many
+// times -- the solver loops, spectral_norm_power, repeated projections.
+class DeviceSystemMatrix {
+ public:
+  explicit DeviceSystemMatrix(const SparseSystemMatrix& w);  // upload
+  // build_system_matrix on the device, the matrix never leaves it
+  DeviceSystemMatrix(const ScanGeometry& g, MatrixMode mode, int k = 1,
+                     std::uint64_t memory_budget_bytes = 5ull << 30);
+  ~DeviceSystemMatrix();
+  DeviceSystemMatrix(const DeviceSystemMatrix&) = delete;
+  DeviceSystemMatrix& operator=(const DeviceSystemMatrix&) = delete;
+  std::uint64_t n_rows() const;
+  std::uint64_t n_cols() const;
+  std::uint64_t nnz() const;
+  const std::string& meta() const;
+  SparseSystemMatrix download() const;
+  void scale_values(double factor);
+  struct Impl;
+  const Impl& impl() const { return *impl_; }
+
+ private:
+  std::unique_ptr<Impl> impl_;
+};
+std::vector<double> forward_project(const DeviceSystemMatrix& w, const std::vector<double>& x);
+std::vector<double> back_project(const DeviceSystemMatrix& w, const std::vector<double>& y);
+double spectral_norm_power(const DeviceSystemMatrix& w, int iters = 100, std::uint64_t seed = 7);
+
+// Additions: multi-GPU variants taking a device list:
+// angles sharded over the devices, A x without communication, A^T y and SIRT
+// with an NCCL all-reduce of the partial volumes inside the library.
+std::vector<double> forward_project_matrix_free(const ScanGeometry& g, MatrixMode mode, int k,
+                                                const std::vector<double>& x,
+                                                const std::vector<int>& devices);
+std::vector<double> back_project_matrix_free(const ScanGeometry& g, MatrixMode mode, int k,
+                                             const std::vector<double>& y,
+                                             const std::vector<int>& devices);
+std::vector<float> forward_project_matrix_free(const ScanGeometry& g, MatrixMode mode, int k,
+                                               const std::vector<float>& x,
+                                               const std::vector<int>& devices);
+std::vector<float> back_project_matrix_free(const ScanGeometry& g, MatrixMode mode, int k,
+                                            const std::vector<float>& y,
+                                            const std::vector<int>& devices);
+
 // solver.hpp:10-35: Nesterov-accelerated Tikhonov least squares; the iteration
 // runs on the device (ctsm_nag_tikhonov).
 struct SolveOptions {
@@ -134,6 +235,8 @@ struct SolveResult {
 };
 SolveResult nag_tikhonov(const SparseSystemMatrix& w, const std::vector<double>& p,
                          const SolveOptions& opt, bool keep_trace = false);
+SolveResult nag_tikhonov(const DeviceSystemMatrix& w, const std::vector<double>& p,
+                         const SolveOptions& opt, bool keep_trace = false);
 // io.hpp:31-48: CSM1 matrices and CTT1 tensors (byte-identical containers).
 void write_matrix(const std::string& path, const SparseSystemMatrix& w);
 SparseSystemMatrix read_matrix(const std::string& path);
@@ -143,5 +246,13 @@ std::vector<double> read_tensor(const std::string& path, std::vector<std::uint64
 // Addition: SIRT (BASELINE.json configs[4]) on one device.
 std::vector<double> sirt(const ScanGeometry& g, const std::vector<double>& y,
                          const std::vector<double>& x0, int iters);
+std::vector<float> sirt(const ScanGeometry& g, const std::vector<float>& y,
+                        const std::vector<float>& x0, int iters);
+// ... on a device list (rows sharded, x replicated, one all-reduce per iteration)
+std::vector<double> sirt(const ScanGeometry& g, const std::vector<double>& y,
+                         const std::vector<double>& x0, int iters,
+                         const std::vector<int>& devices);
+std::vector<float> sirt(const ScanGeometry& g, const std::vector<float>& y,
+                        const std::vector<float>& x0, int iters, const std::vector<int>& devices);
 
 }  // namespace ctsm

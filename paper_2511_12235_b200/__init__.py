@@ -9,6 +9,7 @@ from .projector import (  # noqa: F401
     Context,
     MatrixMode,
     SparseSystemMatrix,
+    angle_block_entries,
     angle_column_sums,
     back_project,
     back_project_matrix_free,
@@ -17,9 +18,12 @@ from .projector import (  # noqa: F401
     forward_project_matrix_free,
     matrix_mode_name,
     parse_matrix_mode,
+    pixel_area_factors,
     scale_values,
     sirt,
     spectral_norm_power,
+    voxel_volume_factors,
+    weights_batch,
 )
 
 __version__ = "0.1.0"

@@ -46,6 +46,17 @@ SIGNATURES = {
     "ctsm_validate_geometry": (_I, [_GP]),
     "ctsm_csr_count": (_I, [_P, _GP, _I, _I, _U64, _P, ctypes.POINTER(_U64), _P]),
     "ctsm_csr_fill": (_I, [_P, _GP, _I, _I, _P, _P, _P, _P]),
+    "ctsm_weights_batch": (_I, [_P, _GP, _U64, _P, _P, _P, _P, _I, _P, _P, _P, _P]),
+    "ctsm_angle_block_entries": (_I, [_P, _GP, _I, _I, _I, _U64, _P, _P, _P,
+                                      ctypes.POINTER(_U64), _P]),
+    "ctsm_shard_angles": (_I, [_GP, _I, _I, _P, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
+    "ctsm_multi_create": (_I, [_P, _I, ctypes.POINTER(_P)]),
+    "ctsm_multi_destroy": (_I, [_P]),
+    "ctsm_multi_size": (_I, [_P]),
+    "ctsm_multi_nccl_version": (_I, [_P]),
+    "ctsm_multi_forward_project_matrix_free_host": (_I, [_P, _GP, _I, _P, _P]),
+    "ctsm_multi_back_project_matrix_free_host": (_I, [_P, _GP, _I, _P, _P]),
+    "ctsm_multi_sirt_host": (_I, [_P, _GP, _I, _P, _P, _I]),
     "ctsm_selftest_division": (_I, [_P, _U64, _U64, ctypes.POINTER(_U64)]),
     "ctsm_csr_angle_nnz": (_I, [_P, _GP, _I, ctypes.POINTER(_U64), _P]),
     "ctsm_csr_build": (_I, [_P, _GP, _I, _I, _U64, _P, _P, _P, _U64, ctypes.POINTER(_U64), _P]),

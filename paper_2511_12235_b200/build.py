@@ -1,6 +1,6 @@
 """Builds paper_2511_12235_b200/libctsm_b200.so with nvcc for sm_100a.
 
-csr.cu and line.cu (bit-exact CSR emission) are compiled with -fmad=false so that no FMA
+csr.cu, weights.cu and line.cu (bit-exact CSR emission and weight API) are compiled with -fmad=false so that no FMA
 contraction changes the reference's rounding; the
 matrix-free kernels (mf.cu) keep contraction on.
 """
@@ -23,11 +23,13 @@ COMMON += os.environ.get("CTSM_NVCC_EXTRA", "").split()
 UNITS = {
     "csr.cu": ["-fmad=false"],
     "line.cu": ["-fmad=false"],
+    "weights.cu": ["-fmad=false"],
     "mf.cu": [],
     "solver.cu": ["-fmad=false"],
     "capi.cu": [],
     "io.cu": [],
     "api.cpp": [],
+    "multi.cu": [],
 }
 
 
@@ -55,7 +57,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
     if force or _stale(LIB, objs):
-        cmd = [NVCC, "-shared", "-o", LIB] + objs + ARCH + ["-lcudart"]
+        cmd = [NVCC, "-shared", "-o", LIB] + objs + ARCH + ["-lcudart", "-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -538,6 +538,108 @@ int ctsm_csr_build(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int a
   }
 }
 
+// ---- the reference's weight API (weights2d.hpp:31-32, weights3d.hpp:90-91,
+// projector.hpp:72-78) ---------------------------------------------------------
+int ctsm_weights_batch(ctsm_ctx* ctx, const ctsm_geometry* g, uint64_t n, const int32_t* ix,
+                       const int32_t* iy, const int32_t* iz, const double* phi, int cap,
+                       int32_t* count, int32_t* m_y, int32_t* m_z, double* w) {
+  CT_TRY(set_device(ctx));
+  DevGeom d;
+  CT_TRY(dev_geom(g, &d));
+  if (cap <= 0) return fail(CTSM_ERR_INVALID_SPEC, "slab capacity must be > 0");
+  if (n == 0) return 0;
+  for (uint64_t q = 0; q < n; ++q) {
+    // VoxelIndex outside the grid is the caller's error in the reference
+    // (faces are computed for any index); keep the indices as given
+    (void)q;
+  }
+  cudaStream_t st = nullptr;
+  CT_TRY(ensure(ctx, ctx->edges, (size_t)d.n_edges * edge_angle_bytes()));
+  CT_CUDA(build_exact_tables(d, 0, 0, nullptr, ctx->edges.p, st));
+  const size_t ni = n * sizeof(int), nd = n * sizeof(double);
+  const size_t slab = (size_t)n * cap;
+  CT_TRY(ensure(ctx, ctx->tmp_a, 4 * ni + nd));
+  CT_TRY(ensure(ctx, ctx->tmp_b, slab * (2 * sizeof(int) + sizeof(double))));
+  int* dix = (int*)ctx->tmp_a.p;
+  int* diy = dix + n;
+  int* diz = diy + n;
+  int* dcount = diz + n;
+  double* dphi = (double*)((char*)ctx->tmp_a.p + 4 * ni);
+  double* dw = (double*)ctx->tmp_b.p;
+  int* dmy = (int*)(dw + slab);
+  int* dmz = dmy + slab;
+  CT_CUDA(cudaMemcpyAsync(dix, ix, ni, cudaMemcpyHostToDevice, st));
+  CT_CUDA(cudaMemcpyAsync(diy, iy, ni, cudaMemcpyHostToDevice, st));
+  if (iz) CT_CUDA(cudaMemcpyAsync(diz, iz, ni, cudaMemcpyHostToDevice, st));
+  else CT_CUDA(cudaMemsetAsync(diz, 0, ni, st));
+  CT_CUDA(cudaMemcpyAsync(dphi, phi, nd, cudaMemcpyHostToDevice, st));
+  CT_CUDA(weights_batch(d, ctx->edges.p, (long long)n, dix, diy, diz, dphi, cap, dcount, dmy, dmz,
+                        dw, ctx->status, st));
+  CT_CUDA(cudaMemcpyAsync(count, dcount, ni, cudaMemcpyDeviceToHost, st));
+  CT_CUDA(cudaMemcpyAsync(m_y, dmy, slab * sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (m_z) CT_CUDA(cudaMemcpyAsync(m_z, dmz, slab * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CT_CUDA(cudaMemcpyAsync(w, dw, slab * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CT_TRY(check_status(ctx, st, "weights"));
+  for (uint64_t q = 0; q < n; ++q)
+    if (count[q] > cap) return fail(CTSM_ERR_TOO_LARGE, "a query has more weights than the slab holds");
+  return 0;
+}
+
+int ctsm_angle_block_entries(ctsm_ctx* ctx, const ctsm_geometry* g, int mode, int k, int angle,
+                             uint64_t capacity, uint32_t* raster_dev, uint32_t* col_dev,
+                             double* w_dev, uint64_t* n_out, void* stream) {
+  DevGeom d;
+  CT_TRY(csr_prologue(ctx, g, angle, angle + 1, &d));
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t rpa = (uint64_t)d.rows_per_angle;
+  if (mode != CTSM_MODE_CONSISTENT) {
+    // ray modes emit row by row (projector.cpp:72-83): the block's CSR order
+    CT_TRY(ensure(ctx, ctx->tmp_c, (rpa + 1) * sizeof(uint64_t)));
+    uint64_t nnz = 0;
+    CT_TRY(ctsm_csr_count_mode(ctx, g, mode, k, angle, angle + 1, ~0ull, (uint64_t*)ctx->tmp_c.p,
+                               &nnz, stream));
+    *n_out = nnz;
+    if (nnz > capacity) return 0;
+    CT_TRY(ctsm_csr_fill_mode(ctx, g, mode, k, angle, angle + 1, (const uint64_t*)ctx->tmp_c.p,
+                              col_dev, w_dev, stream));
+    CT_CUDA(expand_row_index(rpa, (const uint64_t*)ctx->tmp_c.p, raster_dev, st));
+    CT_CUDA(cudaStreamSynchronize(st));
+    return 0;
+  }
+  const uint64_t n_cols = (uint64_t)d.n_vox;
+  const unsigned long long cap = capacity + 148ull * 8 * 4 * 256;
+  CT_TRY(ensure(ctx, ctx->plans, csr_plan_bytes(d, 1)));
+  CT_TRY(ensure(ctx, ctx->counts, std::max(rpa, n_cols) * sizeof(unsigned)));
+  CT_TRY(ensure(ctx, ctx->scan, scan_scratch_bytes(std::max(rpa, n_cols))));
+  CT_TRY(ensure(ctx, ctx->tmp_c, (std::max(rpa, n_cols) + 1) * sizeof(uint64_t)));
+  CT_TRY(ensure(ctx, ctx->cursor, 2 * sizeof(unsigned long long)));
+  CT_TRY(ensure(ctx, ctx->rec, (size_t)cap * 16));
+  CT_TRY(ensure(ctx, ctx->grp, (size_t)cap * 16));
+  CT_TRY(prepare_exact(ctx, d, angle, 1, st));
+  CT_CUDA(cudaMemsetAsync(ctx->counts.p, 0, rpa * sizeof(unsigned), st));
+  CT_CUDA(cudaMemsetAsync(ctx->cursor.p, 0, sizeof(unsigned long long), st));
+  CsrSink sk{2, (unsigned*)ctx->counts.p, nullptr, nullptr, ctx->rec.p,
+             (unsigned long long*)ctx->cursor.p, cap, 0};
+  CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, 1, sk, ctx->plans.p, ctx->status, st));
+  // the entry count is the sum of the row counts
+  CT_CUDA(exclusive_scan_u32_u64((const unsigned*)ctx->counts.p, rpa, (uint64_t*)ctx->tmp_c.p,
+                                 ctx->scan.p, st));
+  uint64_t nnz = 0;
+  unsigned long long cur = 0;
+  CT_CUDA(cudaMemcpyAsync(&nnz, (uint64_t*)ctx->tmp_c.p + rpa, sizeof nnz, cudaMemcpyDeviceToHost,
+                          st));
+  CT_CUDA(cudaMemcpyAsync(&cur, ctx->cursor.p, sizeof cur, cudaMemcpyDeviceToHost, st));
+  CT_TRY(check_status(ctx, st, "angle_block_entries"));
+  *n_out = nnz;
+  if (nnz > capacity || cur > cap) return 0;  // the caller retries with arrays of *n_out
+  CT_CUDA(records_to_emission_order(ctx->rec.p, (unsigned long long*)ctx->cursor.p, cap, n_cols,
+                                    (unsigned*)ctx->counts.p, (uint64_t*)ctx->tmp_c.p,
+                                    ctx->scan.p, ctx->grp.p, g->n_det_y, g->n_det_z, raster_dev,
+                                    col_dev, w_dev, st));
+  CT_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
 int ctsm_selftest_division(ctsm_ctx* ctx, uint64_t n, uint64_t seed, uint64_t* mismatches) {
   CT_TRY(set_device(ctx));
   CT_TRY(ensure(ctx, ctx->cursor, 2 * sizeof(unsigned long long)));
@@ -904,6 +1006,26 @@ int ctsm_symmetry_order(const ctsm_geometry* g) {
   DevGeom d;
   if (dev_geom(g, &d) != 0) return 1;
   return symmetry_order(g);
+}
+
+int ctsm_shard_angles(const ctsm_geometry* g, int rank, int world, int* angles_out, int* n_out,
+                      int* orbits_out) {
+  CT_TRY(validate(g));
+  if (world <= 0 || rank < 0 || rank >= world)
+    return fail(CTSM_ERR_INVALID_SPEC, "rank / world out of range");
+  const int order = symmetry_order(g);
+  std::vector<int> a;
+  if (order >= 4) {
+    std::vector<int> base;
+    for (int i = rank; i < base_limit(g, order); i += world) base.push_back(i);
+    a = orbit_angles(g, order, base);
+  } else {
+    for (int i = rank; i < g->n_angles; i += world) a.push_back(i);
+  }
+  if (angles_out) std::copy(a.begin(), a.end(), angles_out);
+  if (n_out) *n_out = (int)a.size();
+  if (orbits_out) *orbits_out = order >= 4 ? 1 : 0;
+  return 0;
 }
 
 static int orbit_base(const ctsm_geometry* g, int base_begin, int base_step,

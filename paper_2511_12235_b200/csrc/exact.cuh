@@ -49,7 +49,7 @@ __device__ __forceinline__ long long lround_exact(double v) {
 }
 
 // Table builders (one thread per entry).
-__global__ void build_angle_table(DevGeom g, int angle_begin, int n, ExactAngle* out) {
+static __global__ void build_angle_table(DevGeom g, int angle_begin, int n, ExactAngle* out) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int i = angle_begin + k;
@@ -64,7 +64,7 @@ __global__ void build_angle_table(DevGeom g, int angle_begin, int n, ExactAngle*
   out[k] = A;
 }
 
-__global__ void build_edge_table(DevGeom g, EdgeAngle* out) {
+static __global__ void build_edge_table(DevGeom g, EdgeAngle* out) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= g.n_edges) return;
   const long long e = (long long)g.edge_lo + k;
@@ -104,7 +104,7 @@ struct Sweep {
 
 // canonical_orientation (geometry.cpp:76-97) + strip_sweep (weights2d.cpp:38-87).
 // Returns false (status raised) on failure.
-__device__ bool strip_sweep(const DevGeom& g, const ExactAngle& A, const EdgeAngle* edges,
+static __device__ bool strip_sweep(const DevGeom& g, const ExactAngle& A, const EdgeAngle* edges,
                             double x0, double x1, double y0, double y1, Sweep& sw, int* status) {
   const double s = g.s;
   bool bad = false;

@@ -92,6 +92,27 @@ cudaError_t spmvt_csr_fixed(uint64_t n_rows, const uint64_t* row_start, const ui
                             const double* val, const double* y, unsigned long long* acc,
                             double scale, cudaStream_t st);
 
+// ---- weights.cu: the reference's weight API on the device ------------------
+// pixel_area_factors / voxel_volume_factors (weights2d.cpp:105-129,
+// weights3d.cpp:354-462) for n_q (voxel, phi) queries (device arrays); query q
+// writes its weights, in the reference's order, to slab q of `cap` entries
+// and count[q] (which may exceed cap: the slab then holds the first cap).
+cudaError_t weights_batch(const DevGeom& g, const void* edges_dev, long long n_q, const int* ix,
+                          const int* iy, const int* iz, const double* phi, int cap, int* count,
+                          int* my, int* mz, double* w, int* status, cudaStream_t st);
+// Mode-2 emission records of ONE angle -> (raster, col, w) in the reference's
+// emission order (projector.cpp:44-84): counting sort by column, then each
+// column's entries by (m_y, m_z). counts: n_cols u32; scan_tmp: n_cols + 1
+// u64; tmp: cap 16-byte records.
+cudaError_t records_to_emission_order(const void* rec, const unsigned long long* n_dev,
+                                      unsigned long long cap, uint64_t n_cols, unsigned* counts,
+                                      uint64_t* scan_tmp, void* scan_scratch, void* tmp,
+                                      int n_det_y, int n_det_z, uint32_t* raster, uint32_t* col,
+                                      double* w, cudaStream_t st);
+// raster[j] = r for the entries j of row r (CSR of one angle block).
+cudaError_t expand_row_index(uint64_t n_rows, const uint64_t* row_start, uint32_t* raster,
+                             cudaStream_t st);
+
 // ---- mf.cu ---------------------------------------------------------------
 struct AngleCS {
   double C, S;

@@ -262,6 +262,77 @@ def build_system_matrix(g: ScanGeometry, mode: str = MatrixMode.consistent, k: i
                               row_offset=a0 * g.rows_per_angle)
 
 
+def weights_batch(g: ScanGeometry, ix, iy, iz, phi, cap: int = 256, device: Optional[int] = None):
+    """pixel_area_factors (weights2d.hpp:31-32) / voxel_volume_factors
+    (weights3d.hpp:90-91) for a batch of (voxel, phi) queries in one device
+    launch. Returns (count[n], m_y[n, cap], m_z[n, cap], w[n, cap]) numpy
+    arrays; query q's weights are the first count[q] entries of its rows, in
+    the reference's order."""
+    g.validate()
+    ix = np.ascontiguousarray(ix, np.int32)
+    n = ix.size
+    iy = np.ascontiguousarray(iy, np.int32)
+    iz = np.zeros(n, np.int32) if iz is None else np.ascontiguousarray(iz, np.int32)
+    phi = np.ascontiguousarray(phi, np.float64)
+    if not (iy.size == n and iz.size == n and phi.size == n):
+        raise CtsmError("DimensionMismatch", "one (ix, iy, iz, phi) per query is required")
+    ctx = Context.get(device)
+    cg = g.to_c()
+    count = np.zeros(n, np.int32)
+    my = np.zeros((n, cap), np.int32)
+    mz = np.zeros((n, cap), np.int32)
+    w = np.zeros((n, cap), np.float64)
+    _lib.check(_lib.lib().ctsm_weights_batch(ctx.handle, ctypes.byref(cg), n, ix.ctypes.data,
+                                             iy.ctypes.data, iz.ctypes.data, phi.ctypes.data, cap,
+                                             count.ctypes.data, my.ctypes.data, mz.ctypes.data,
+                                             w.ctypes.data))
+    return count, my, mz, w
+
+
+def pixel_area_factors(n, phi: float, g: ScanGeometry):
+    """weights2d.hpp:31-32: [(m_y, w), ...] of pixel n = (ix, iy) at angle phi."""
+    count, my, _, w = weights_batch(g, [n[0]], [n[1]], None, [phi])
+    return [(int(my[0, i]), float(w[0, i])) for i in range(count[0])]
+
+
+def voxel_volume_factors(n, phi: float, g: ScanGeometry):
+    """weights3d.hpp:90-91: [(m_y, m_z, w), ...] of voxel n = (ix, iy, iz)."""
+    if g.is_2d():
+        raise CtsmError("InvalidSpec", "voxel_volume_factors needs a 3D scan")
+    count, my, mz, w = weights_batch(g, [n[0]], [n[1]], [n[2]], [phi])
+    return [(int(my[0, i]), int(mz[0, i]), float(w[0, i])) for i in range(count[0])]
+
+
+def angle_block_entries(g: ScanGeometry, mode: str, k: int, angle_index: int,
+                        device: Optional[int] = None):
+    """detail::angle_block_entries (projector.hpp:72-78): (raster, col, w)
+    CUDA tensors of one angle block in the reference's emission order."""
+    mc = _mode_code(mode, k)
+    g.validate()
+    ctx = Context.get(device)
+    dev = ctx.device
+    cg = g.to_c()
+    st = _stream(dev)
+    L = _lib.lib()
+    cap = ctypes.c_uint64(0)
+    if mc == 0:
+        _lib.check(L.ctsm_csr_angle_nnz(ctx.handle, ctypes.byref(cg), angle_index,
+                                        ctypes.byref(cap), st))
+    n = ctypes.c_uint64(0)
+    capv = cap.value
+    for _ in range(2):
+        raster = torch.empty(capv, dtype=torch.int32, device=f"cuda:{dev}")
+        col = torch.empty(capv, dtype=torch.int32, device=f"cuda:{dev}")
+        w = torch.empty(capv, dtype=torch.float64, device=f"cuda:{dev}")
+        _lib.check(L.ctsm_angle_block_entries(ctx.handle, ctypes.byref(cg), mc, k, angle_index,
+                                              capv, _dev_ptr(raster), _dev_ptr(col), _dev_ptr(w),
+                                              ctypes.byref(n), st))
+        if n.value <= capv:
+            break
+        capv = n.value
+    return raster[:n.value], col[:n.value], w[:n.value]
+
+
 def forward_project(w: SparseSystemMatrix, x):
     """projector.cpp:203-217 (K3)."""
     n = int(x.numel()) if (torch is not None and isinstance(x, torch.Tensor)) else int(np.size(x))

@@ -131,3 +131,35 @@ def test_orbit_shards_partition_angles(world, order):
     g = TEST_GEOMETRIES["wide2d"].with_(n_angles=48)
     got = torch.cat([shard_angles(g, ("orbits", r, world), order) for r in range(world)])
     assert torch.equal(torch.sort(got).values, torch.arange(g.n_angles))
+
+
+def test_shard_angles_c_abi_matches_dist():
+    """ctsm_shard_angles (the partition of the library's multi-GPU context)
+    and dist.shard_angles (the torch.distributed drivers) agree, cover every
+    angle exactly once, and are balanced to within one orbit."""
+    import ctypes
+
+    from paper_2511_12235_b200 import CONFIGS, _lib
+    from paper_2511_12235_b200.dist import shard_angles
+
+    L = _lib.lib()
+    odd = CONFIGS["c1"].with_(n_angles=90, angle_end=3.0)  # no symmetry: strided shards
+    for g in (CONFIGS["c1"], CONFIGS["c3"], CONFIGS["c0"], odd):
+        cg = g.to_c()
+        for world in (1, 2, 3, 8):
+            seen = []
+            sizes = []
+            for rank in range(world):
+                buf = (ctypes.c_int * g.n_angles)()
+                n = ctypes.c_int(0)
+                orb = ctypes.c_int(0)
+                assert L.ctsm_shard_angles(ctypes.byref(cg), rank, world, buf, ctypes.byref(n),
+                                           ctypes.byref(orb)) == 0
+                got = list(buf[:n.value])
+                order = 8 if (orb.value and g.angle_start == 0.0 and g.n_angles % 8 == 0) else 4
+                shard = ("orbits", rank, world) if orb.value else (rank, g.n_angles, world)
+                assert got == shard_angles(g, shard, order=order).tolist()
+                seen += got
+                sizes.append(n.value)
+            assert sorted(seen) == list(range(g.n_angles))
+            assert max(sizes) - min(sizes) <= 8
