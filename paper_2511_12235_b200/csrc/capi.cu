@@ -165,10 +165,54 @@ int validate(const ctsm_geometry* g) {
   return 0;
 }
 
+// Upper bound of the detector cells one pixel's shadow spans: u = sdd L / D
+// (L lateral, D depth) moves by at most sdd / D * sqrt(1 + (L / D)^2) per
+// unit of displacement, D >= s - R, |L / D| <= R / (s - R), R the grid
+// half-diagonal.
+double shadow_cells_bound(const ctsm_geometry* g) {
+  const double R = std::hypot(g->n_x * g->a / 2.0, g->n_y * g->b / 2.0);
+  const double t = R / (g->s - R);
+  return std::hypot(g->a, g->b) * (g->s + g->d) / ((g->s - R) * g->d_y) * std::sqrt(1.0 + t * t);
+}
+
+// Device capacity of the exact sweep (common.cuh kMaxBrk breakpoints: the 4
+// corners and the detector edges inside the shadow). The reference has no
+// such limit (its sweep is a std::vector); a geometry beyond it is rejected
+// here, by name, instead of failing inside a kernel.
+int check_sweep_capacity(const ctsm_geometry* g) {
+  const double w = shadow_cells_bound(g);
+  if (!(std::floor(w) + 1.0 + 4.0 <= (double)kMaxBrk)) {
+    char msg[200];
+    snprintf(msg, sizeof msg,
+             "a pixel's shadow can span %.0f detector cells; the device sweep holds %d "
+             "(detector pitch too fine for the pixel size and magnification)",
+             std::floor(w) + 1.0, kMaxBrk - 5);
+    return fail(CTSM_ERR_TOO_LARGE, msg);
+  }
+  return 0;
+}
+
+// The 3D matrix-free kernels plan at most mf3d_max_pieces() pieces per column
+// sweep (cells of the shadow + 2 zone boundaries).
+int check_mf3d_capacity(const ctsm_geometry* g) {
+  if (g->n_z == 1 && g->n_det_z == 1) return 0;
+  const double w = shadow_cells_bound(g);
+  if (!(std::floor(w) + 2.0 + 2.0 <= (double)mf3d_max_pieces())) {
+    char msg[200];
+    snprintf(msg, sizeof msg,
+             "a voxel's shadow can span %.0f detector columns; the 3D matrix-free kernels hold "
+             "%d (build the CSR matrix instead, or coarsen the detector)",
+             std::floor(w) + 2.0, mf3d_max_pieces() - 2);
+    return fail(CTSM_ERR_TOO_LARGE, msg);
+  }
+  return 0;
+}
+
 // Derived device geometry incl. the edge-table extent: every fan angle of the
 // grid satisfies |tan| <= R / (s - R), R the grid half-diagonal.
 int dev_geom(const ctsm_geometry* g, DevGeom* out) {
   CT_TRY(validate(g));
+  CT_TRY(check_sweep_capacity(g));
   DevGeom d = make_dev_geom(*g);
   const double R = std::hypot(g->n_x * g->a / 2.0, g->n_y * g->b / 2.0);
   const double umax = R / (g->s - R) * (g->s + g->d) / g->d_y;
@@ -936,6 +980,7 @@ static int fwd_impl(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int begin,
                     int step, const void* x, void* y, cudaStream_t st) {
   DevGeom d;
   CT_TRY(dev_geom(g, &d));
+  CT_TRY(check_mf3d_capacity(g));
   CT_TRY(check_dtype(dtype));
   CT_TRY(check_shard(g, begin, end, step));
   const int n_sel = n_in_shard(begin, end, step);
@@ -967,6 +1012,7 @@ static int bwd_impl(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int begin,
                     int step, const void* y, void* x, cudaStream_t st) {
   DevGeom d;
   CT_TRY(dev_geom(g, &d));
+  CT_TRY(check_mf3d_capacity(g));
   CT_TRY(check_dtype(dtype));
   CT_TRY(check_shard(g, begin, end, step));
   const int n_sel = n_in_shard(begin, end, step);
@@ -1044,6 +1090,7 @@ int ctsm_fwd_mf_orbits(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int bas
   CT_TRY(set_device(ctx));
   DevGeom d;
   CT_TRY(dev_geom(g, &d));
+  CT_TRY(check_mf3d_capacity(g));
   CT_TRY(check_dtype(dtype));
   std::vector<int> base;
   CT_TRY(orbit_base(g, base_begin, base_step, &base));
@@ -1060,6 +1107,7 @@ int ctsm_bwd_mf_orbits(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int bas
   CT_TRY(set_device(ctx));
   DevGeom d;
   CT_TRY(dev_geom(g, &d));
+  CT_TRY(check_mf3d_capacity(g));
   CT_TRY(check_dtype(dtype));
   std::vector<int> base;
   CT_TRY(orbit_base(g, base_begin, base_step, &base));

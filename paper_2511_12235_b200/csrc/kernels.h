@@ -114,6 +114,8 @@ cudaError_t expand_row_index(uint64_t n_rows, const uint64_t* row_start, uint32_
                              cudaStream_t st);
 
 // ---- mf.cu ---------------------------------------------------------------
+// Pieces one column sweep of the 3D matrix-free kernels may hold (fast3dw.cuh).
+int mf3d_max_pieces();
 struct AngleCS {
   double C, S;
 };

@@ -14,6 +14,8 @@
 
 namespace ctsmb {
 
+int mf3d_max_pieces() { return fast::kMaxPieces; }
+
 namespace {
 
 __global__ void angle_cs_kernel(DevGeom g, int angle_begin, int angle_step, int n, AngleCS* out) {

@@ -54,3 +54,23 @@ def test_errors_without_gpu_are_loud():
     h = ctypes.c_void_p()
     st = _lib.lib().ctsm_create(0, ctypes.byref(h))
     assert st != 0
+
+
+def test_validate_rejects_sweeps_beyond_the_device_capacity():
+    """A detector pitch so fine that a pixel's shadow spans more cells than the
+    device sweep holds is rejected by name (TooLarge) at validation, not by a
+    kernel (the reference's sweep is a std::vector and has no such limit)."""
+    import ctypes
+
+    from paper_2511_12235_b200 import CONFIGS
+
+    L = _lib.lib()
+    g = CONFIGS["c0"]
+    cg = g.to_c()
+    assert L.ctsm_validate_geometry(ctypes.byref(cg)) == 0
+    fine = g.with_(d_y=g.d_y / 12, n_det_y=g.n_det_y * 12).to_c()
+    assert L.ctsm_validate_geometry(ctypes.byref(fine)) == 9  # TooLarge
+    assert b"shadow" in L.ctsm_last_error()
+    for name in ("c1", "c2", "c3", "c4"):  # every BASELINE config is within the limits
+        cg = CONFIGS[name].to_c()
+        assert L.ctsm_validate_geometry(ctypes.byref(cg)) == 0

@@ -153,6 +153,22 @@ def test_division_by_reciprocal_is_ieee_exact():
     assert bad.value == 0
 
 
+def test_wide_shadows_csr_exact_and_matrix_free_limit(oracle_cr):
+    """A detector 4x finer than cone3d's: a voxel's shadow spans ~18 cells.
+    The exact CSR path (24 breakpoints) still matches the oracle bit for bit;
+    the 3D matrix-free kernels (12 pieces per column) refuse by name instead
+    of failing inside a kernel."""
+    g0 = TEST_GEOMETRIES["cone3d"]
+    g = g0.with_(d_y=g0.d_y / 4, n_det_y=g0.n_det_y * 4)
+    w = build_system_matrix(g, memory_budget_bytes=1 << 34)
+    ref = oracle_cr.build_system_matrix(g, threads=NTHREADS, budget=1 << 34)
+    assert_csr_bitexact(w.to_host(), ref)
+    with pytest.raises(CtsmError) as e:
+        forward_project_matrix_free(g, "consistent", 1,
+                                    torch.zeros(g.n_voxels, dtype=torch.float64, device="cuda"))
+    assert e.value.code == "TooLarge" and "shadow" in str(e.value)
+
+
 def test_csr_budget_and_size_limits():
     g = TEST_GEOMETRIES["proj3d"]
     with pytest.raises(CtsmError) as e:
