@@ -722,8 +722,8 @@ def run_sirt(args):
 
 def run_csr(args):
     """K1/K2 consistent CSR assembly (bit-exact path) + K3/K4 on one GPU.
-    One step = build_system_matrix (count, scan, fill, per-row sort) of the
-    whole config; metric SM weights/s = nnz / build time. K3 A x and K4 A^T y
+    One step = build_system_matrix (ctsm_csr_build: single-evaluation emission,
+    row scan, record scatter, per-row radix sort) of the whole config; metric SM weights/s = nnz / build time. K3 A x and K4 A^T y
     on the built matrix are timed separately (HBM roofline: 12 B/nnz + 16
     B/row)."""
     import torch
@@ -816,15 +816,29 @@ def run_csr(args):
     per_unit = F_REF["2d"] if g.is_2d() else F_REF["3d"]
     units = float(g.n_x * g.n_y * g.n_z) * g.n_angles
     achieved = units * per_unit / (ms * 1e-3) / 1e12
-    roof = {"bound": "fp64", "kernel": "csr2d_kernel" if g.is_2d() else "csr3d_kernel",
+    kname = "csr2d_kernel" if g.is_2d() else "emit3d_kernel"
+    ncu = {}
+    try:
+        ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_kernels.json"))).get(
+            f"{cfg}_csr:{kname}", {})
+    except Exception:
+        pass
+    roof = {"bound": "fp64", "kernel": kname,
             "achieved": achieved, "peak": peak_flops / 2 if peak_flops else None,
             "unit": "T FP64 op/s (arithmetic instructions, FMA = 1 op; SURVEY.md §8(d))",
             "frac": achieved / (peak_flops / 2) if peak_flops else None,
-            "traffic": None,
+            "traffic": ncu.get("dram_bytes"),
+            "traffic_unit": "DRAM bytes per emission launch of the ncu capture (one chunk of "
+                            "angles; profiles/ncu_kernels.json)",
+            "ncu_fp64_pipe_active_pct": ncu.get("fp64_pipe_pct"),
+            "ncu_launch_ms": ncu.get("duration_ms"),
             "work_per_unit": f"{per_unit:g} FP64 ops per pixel/voxel-angle (reference op count; "
                              "the crmath calls are excluded like the reference's libm calls)",
             "units_per_launch": units,
-            "note": "whole build (all emission passes, scan, sort) taken as the kernel time"}
+            "algorithmic_output_bytes": 12.0 * nnz + 8.0 * (w.n_rows + 1),
+            "note": "whole build taken as the kernel time: per angle chunk the plan and emission "
+                    "kernels (each weight evaluated once), the row scan, the record scatter and "
+                    "the per-row radix sort (profiles/*_csr_c2_launches.csv gives the shares)"}
     line = {
         "metric": "SM weights/s (consistent CSR assembly)", "value": nnz / (ms * 1e-3),
         "unit": "weights/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,

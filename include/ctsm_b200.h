@@ -324,6 +324,26 @@ int ctsm_forward_project_matrix_free_host_f32(ctsm_ctx* ctx, const ctsm_geometry
 int ctsm_back_project_matrix_free_host_f32(ctsm_ctx* ctx, const ctsm_geometry* g,
                                            const float* y_host, float* x_host);
 
+/* ---- independent numerical oracles on the device (
+ * oracle.hpp:24-45, oracle.cpp:70-196) ----------------------------------------
+ * Batches of n cases given as HOST arrays: boxes[6n] = {x0, x1, y0, y1, zb, zt}
+ * per case, phi[n], and the detector cell (m_y[n], m_z[n]) of each case.
+ * ctsm_mc_volume_3d: McEstimate of mc_volume_3d -- the volume fraction of
+ *   the box inside the cone wedge of the cell by uniform point sampling with
+ *   the reference's 16 mt19937_64 sub-streams (seed + shard), so the estimate
+ *   is deterministic and the hit count is the reference's for the same libm;
+ *   value / std_err / hits (each may be NULL) receive n results.
+ * ctsm_multiline_volume_3d: the k x k Gauss-Legendre ray-grid integral.
+ * ctsm_gauss_legendre: nodes and weights on [-1, 1] (host). */
+int ctsm_mc_volume_3d(ctsm_ctx* ctx, uint64_t n, const double* boxes, const double* phi, double s,
+                      double d, double d_y, double d_z, const int32_t* m_y, const int32_t* m_z,
+                      uint64_t n_samples, uint64_t seed, double* value, double* std_err,
+                      uint64_t* hits);
+int ctsm_multiline_volume_3d(ctsm_ctx* ctx, uint64_t n, const double* boxes, const double* phi,
+                             double s, double d, double d_y, double d_z, const int32_t* m_y,
+                             const int32_t* m_z, int k, double* out);
+void ctsm_gauss_legendre(int k, double* x, double* w);
+
 /* ---- multi-GPU context --------------------------
  * One process, n devices: each device gets its own ctsm_ctx and stream, the
  * angles are sharded over the devices (ctsm_shard_angles: by symmetry orbits

@@ -13,6 +13,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace ctsm {
@@ -214,6 +215,30 @@ std::vector<float> forward_project_matrix_free(const ScanGeometry& g, MatrixMode
 std::vector<float> back_project_matrix_free(const ScanGeometry& g, MatrixMode mode, int k,
                                             const std::vector<float>& y,
                                             const std::vector<int>& devices);
+
+// oracle.hpp:24-45: the independent numerical oracles, evaluated on the device
+// (the dense Eigen helpers of oracle.hpp are out of scope). The batch forms
+// take n cases: boxes[6n] = {x0, x1, y0, y1, zb, zt} per case.
+struct McEstimate {
+  double value = 0;
+  double std_err = 0;
+};
+McEstimate mc_volume_3d(double x0, double x1, double y0, double y1, double zb, double zt,
+                        double phi, double s, double d, double d_y, double d_z, int m_y, int m_z,
+                        std::uint64_t n_samples, std::uint64_t seed);
+double multiline_volume_3d(double x0, double x1, double y0, double y1, double zb, double zt,
+                           double phi, double s, double d, double d_y, double d_z, int m_y,
+                           int m_z, int k = 200);
+std::pair<std::vector<double>, std::vector<double>> gauss_legendre(int k);
+std::vector<McEstimate> mc_volume_3d(const std::vector<double>& boxes,
+                                     const std::vector<double>& phi, double s, double d,
+                                     double d_y, double d_z, const std::vector<int>& m_y,
+                                     const std::vector<int>& m_z, std::uint64_t n_samples,
+                                     std::uint64_t seed);
+std::vector<double> multiline_volume_3d(const std::vector<double>& boxes,
+                                        const std::vector<double>& phi, double s, double d,
+                                        double d_y, double d_z, const std::vector<int>& m_y,
+                                        const std::vector<int>& m_z, int k = 200);
 
 // solver.hpp:10-35: Nesterov-accelerated Tikhonov least squares; the iteration
 // runs on the device (ctsm_nag_tikhonov).

@@ -1463,6 +1463,165 @@ int ref_angle_column_sums(const o_geom* g, int ip, double* sums) {
   return 0;
 }
 
+
+/* ---- independent numerical oracles (oracle.cpp:70-196) --------------------
+ * The reference's oracle.cpp includes <Eigen/Dense> (absent here), so it
+ * cannot be compiled where it lies; the Eigen-free bodies of mc_volume_3d,
+ * gauss_legendre and multiline_volume_3d are restated here. Pin: like the
+ * reference's own tests (test_weights3d.cpp:198-212; validate.cpp:167-293)
+ * they are checked against voxel_volume_factors (tests/test_oracle_pin.py):
+ * MC within 4 standard errors + 1e-6, Gauss-Legendre within 1e-6. */
+
+/* std::mt19937_64 (the 64-bit Mersenne Twister of Matsumoto & Nishimura). */
+typedef struct {
+  uint64_t mt[312];
+  int idx;
+} mt64;
+static void mt64_seed(mt64* r, uint64_t seed) {
+  r->mt[0] = seed;
+  for (int i = 1; i < 312; ++i)
+    r->mt[i] = 6364136223846793005ULL * (r->mt[i - 1] ^ (r->mt[i - 1] >> 62)) + (uint64_t)i;
+  r->idx = 312;
+}
+static uint64_t mt64_next(mt64* r) {
+  if (r->idx >= 312) {
+    for (int i = 0; i < 312; ++i) {
+      const uint64_t x = (r->mt[i] & 0xFFFFFFFF80000000ULL) | (r->mt[(i + 1) % 312] & 0x7FFFFFFFULL);
+      r->mt[i] = r->mt[(i + 156) % 312] ^ (x >> 1) ^ ((x & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+    }
+    r->idx = 0;
+  }
+  uint64_t x = r->mt[r->idx++];
+  x ^= (x >> 29) & 0x5555555555555555ULL;
+  x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+  x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+  x ^= x >> 43;
+  return x;
+}
+static double mt64_u01(mt64* r) { return (double)(mt64_next(r) >> 11) * 0x1.0p-53; } /* oracle.cpp:46-49 */
+
+/* mc_volume_3d (oracle.cpp:70-98): out[0] = value, out[1] = std_err, returns hits */
+uint64_t ref_mc_volume_3d(const double* box, double phi, double s, double d, double d_y, double d_z,
+                          int m_y, int m_z, uint64_t n_samples, uint64_t seed, double* out) {
+  const double x0 = box[0], x1 = box[1], y0 = box[2], y1 = box[3], zb = box[4], zt = box[5];
+  const double cp = O_COS(phi), sp = O_SIN(phi);
+  const int n_shards = 16;
+  uint64_t hits = 0, total = 0;
+  mt64 rng;
+  for (int shard = 0; shard < n_shards; ++shard) {
+    mt64_seed(&rng, seed + (uint64_t)shard);
+    const uint64_t count = n_samples / n_shards + (shard < (int)(n_samples % n_shards) ? 1 : 0);
+    for (uint64_t i = 0; i < count; ++i) {
+      const double x = x0 + (x1 - x0) * mt64_u01(&rng);
+      const double y = y0 + (y1 - y0) * mt64_u01(&rng);
+      const double z = zb + (zt - zb) * mt64_u01(&rng);
+      const double depth = s - x * cp - y * sp;
+      const double uy = (s + d) / depth * (y * cp - x * sp) / d_y;
+      const double uz = (s + d) / depth * z / d_z;
+      if (uy >= m_y && uy < m_y + 1 && uz >= m_z && uz < m_z + 1) ++hits;
+    }
+    total += count;
+  }
+  const double p = (double)hits / (double)total;
+  const double var = p * (1.0 - p), fl = 1.0 / (double)total;
+  out[0] = p;
+  out[1] = sqrt((var > fl ? var : fl) / (double)total);
+  return hits;
+}
+
+/* gauss_legendre (oracle.cpp:100-122) */
+void ref_gauss_legendre(int k, double* x, double* w) {
+  for (int i = 0; i < k; ++i) {
+    double t = cos(K_PI * (i + 0.75) / (k + 0.5));
+    double pp = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = 0.0;
+      for (int j = 0; j < k; ++j) {
+        const double p2 = p1;
+        p1 = p0;
+        p0 = ((2.0 * j + 1.0) * t * p1 - j * p2) / (j + 1.0);
+      }
+      pp = k * (t * p0 - p1) / (t * t - 1.0);
+      const double dt = p0 / pp;
+      t -= dt;
+      if (fabs(dt) < 1e-15) break;
+    }
+    x[i] = t;
+    w[i] = 2.0 / ((1.0 - t * t) * pp * pp);
+  }
+}
+
+/* multiline_volume_3d (oracle.cpp:124-196) */
+double ref_multiline_volume_3d(const double* box, double phi, double s, double d, double d_y,
+                               double d_z, int m_y, int m_z, int k) {
+  const double x0 = box[0], x1 = box[1], y0 = box[2], y1 = box[3], zb = box[4], zt = box[5];
+  const double cp = O_COS(phi), sp = O_SIN(phi);
+  const double sx = s * cp, sy = s * sp;
+  double u_min = 0, u_max = 0, v_min = 0, v_max = 0;
+  int first = 1;
+  const double vxs[2] = {x0, x1}, vys[2] = {y0, y1}, vzs[2] = {zb, zt};
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) {
+      const double vx = vxs[a], vy = vys[b];
+      const double depth = s - vx * cp - vy * sp;
+      const double u = (s + d) / depth * (vy * cp - vx * sp) / d_y;
+      u_min = first ? u : dmin(u_min, u);
+      u_max = first ? u : dmax(u_max, u);
+      for (int c = 0; c < 2; ++c) {
+        const double v = (s + d) / depth * vzs[c] / d_z;
+        if (first) {
+          v_min = v_max = v;
+        } else {
+          v_min = dmin(v_min, v);
+          v_max = dmax(v_max, v);
+        }
+        first = 0;
+      }
+    }
+  const double u_lo = dmax((double)m_y, u_min), u_hi = dmin((double)m_y + 1.0, u_max);
+  const double v_lo = dmax((double)m_z, v_min), v_hi = dmin((double)m_z + 1.0, v_max);
+  if (u_hi <= u_lo || v_hi <= v_lo) return 0.0;
+  double* nodes = (double*)malloc(2 * (size_t)k * sizeof(double));
+  double* wts = nodes + k;
+  ref_gauss_legendre(k, nodes, wts);
+  const double uc = 0.5 * (u_lo + u_hi), ur = 0.5 * (u_hi - u_lo);
+  const double vc = 0.5 * (v_lo + v_hi), vr = 0.5 * (v_hi - v_lo);
+  double total = 0.0;
+  for (int i = 0; i < k; ++i) {
+    const double ey = (uc + ur * nodes[i]) * d_y;
+    for (int j = 0; j < k; ++j) {
+      const double ez = (vc + vr * nodes[j]) * d_z;
+      const double dx = -d * cp - ey * sp, dy = -d * sp + ey * cp, dz = ez;
+      double t0 = 0.0, t1 = INFINITY;
+      const double org[3] = {sx, sy, 0.0};
+      const double dir[3] = {dx - sx, dy - sy, dz};
+      const double lo[3] = {x0, y0, zb}, hi[3] = {x1, y1, zt};
+      for (int ax = 0; ax < 3; ++ax) {
+        if (fabs(dir[ax]) < 1e-300) {
+          if (org[ax] < lo[ax] || org[ax] > hi[ax]) {
+            t0 = 1.0;
+            t1 = 0.0;
+            break;
+          }
+          continue;
+        }
+        double ta = (lo[ax] - org[ax]) / dir[ax];
+        double tb = (hi[ax] - org[ax]) / dir[ax];
+        if (ta > tb) {
+          const double tmp = ta;
+          ta = tb;
+          tb = tmp;
+        }
+        t0 = dmax(t0, ta);
+        t1 = dmin(t1, tb);
+      }
+      if (t1 > t0) total += wts[i] * wts[j] * (cube(t1) - cube(t0)) / 3.0;
+    }
+  }
+  free(nodes);
+  return d_y * d_z * (s + d) * total * ur * vr / ((x1 - x0) * (y1 - y0) * (zt - zb));
+}
+
 #ifdef CTSM_ORACLE_CRMATH
 /* crmath entry points for tests/test_crmath.py (correct-rounding checks). */
 void orc_crm_eval(int fn, const double* a, const double* b, double* out, long n) {

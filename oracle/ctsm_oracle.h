@@ -77,6 +77,14 @@ void* ref_build_system_matrix_mode(const o_geom* g, int mode, int k, int threads
 int ref_forward_mf_mode(const o_geom* g, int mode, int k, const double* x, double* y, int threads);
 int ref_back_mf_mode(const o_geom* g, int mode, int k, const double* y, double* x, int threads);
 
+/* Independent numerical oracles (oracle.cpp:70-196; restatement only: the
+ * reference's oracle.cpp needs Eigen). box = {x0, x1, y0, y1, zb, zt}. */
+uint64_t ref_mc_volume_3d(const double* box, double phi, double s, double d, double d_y, double d_z,
+                          int m_y, int m_z, uint64_t n_samples, uint64_t seed, double* out);
+void ref_gauss_legendre(int k, double* x, double* w);
+double ref_multiline_volume_3d(const double* box, double phi, double s, double d, double d_y,
+                               double d_z, int m_y, int m_z, int k);
+
 #ifdef __cplusplus
 }
 #endif

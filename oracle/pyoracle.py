@@ -142,6 +142,18 @@ class Oracle:
             L.ref_back_mf_angles_par.argtypes = [_P, _P, ctypes.c_int, _P, _P, ctypes.c_int]
         # slab-parallel angle blocks: the restatement, and the reference's own
         # voxel_volume_factors / pixel_area_factors per slab (ref_shim.cpp)
+        self.has_numeric = hasattr(L, "ref_mc_volume_3d")
+        if self.has_numeric:
+            L.ref_mc_volume_3d.argtypes = [_P, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                           ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                           ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, _P]
+            L.ref_mc_volume_3d.restype = ctypes.c_uint64
+            L.ref_gauss_legendre.argtypes = [ctypes.c_int, _P, _P]
+            L.ref_gauss_legendre.restype = None
+            L.ref_multiline_volume_3d.argtypes = [_P, ctypes.c_double, ctypes.c_double,
+                                                  ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                                  ctypes.c_int, ctypes.c_int, ctypes.c_int]
+            L.ref_multiline_volume_3d.restype = ctypes.c_double
         self.has_entries_par = hasattr(L, "ref_angle_block_entries_par")
         if self.has_entries_par:
             L.ref_angle_block_entries_par.argtypes = [_P, ctypes.c_int, _P, _P, _P, ctypes.c_long,
@@ -224,6 +236,32 @@ class Oracle:
         n = self.lib.ref_voxel_volume_factors(p, ix, iy, iz, phi, _ptr(my), _ptr(mz), _ptr(w), 256)
         self._check(n)
         return my[:n].copy(), mz[:n].copy(), w[:n].copy()
+
+    # -- independent numerical oracles (oracle.cpp:70-196; restatement only) --
+    @staticmethod
+    def voxel_box(g, ix: int, iy: int, iz: int) -> np.ndarray:
+        return np.array([(ix - g.n_x / 2.0) * g.a, (ix + 1 - g.n_x / 2.0) * g.a,
+                         (iy - g.n_y / 2.0) * g.b, (iy + 1 - g.n_y / 2.0) * g.b,
+                         (iz - g.n_z / 2.0) * g.c, (iz + 1 - g.n_z / 2.0) * g.c], np.float64)
+
+    def mc_volume_3d(self, g, box, phi: float, m_y: int, m_z: int, n_samples: int, seed: int):
+        """(value, std_err, hits) of oracle.cpp:70-98."""
+        box = np.ascontiguousarray(box, np.float64)
+        out = np.zeros(2, np.float64)
+        hits = self.lib.ref_mc_volume_3d(_ptr(box), phi, g.s, g.d, g.d_y, g.d_z, m_y, m_z,
+                                         n_samples, seed, _ptr(out))
+        return float(out[0]), float(out[1]), int(hits)
+
+    def gauss_legendre(self, k: int):
+        x = np.zeros(k, np.float64)
+        w = np.zeros(k, np.float64)
+        self.lib.ref_gauss_legendre(k, _ptr(x), _ptr(w))
+        return x, w
+
+    def multiline_volume_3d(self, g, box, phi: float, m_y: int, m_z: int, k: int = 200) -> float:
+        box = np.ascontiguousarray(box, np.float64)
+        return float(self.lib.ref_multiline_volume_3d(_ptr(box), phi, g.s, g.d, g.d_y, g.d_z, m_y,
+                                                      m_z, k))
 
     def angle_block_entries(self, g, ip: int, threads: int = 1, mode: str = "consistent",
                             k: int = 1):

@@ -57,6 +57,9 @@ SIGNATURES = {
     "ctsm_multi_forward_project_matrix_free_host": (_I, [_P, _GP, _I, _P, _P]),
     "ctsm_multi_back_project_matrix_free_host": (_I, [_P, _GP, _I, _P, _P]),
     "ctsm_multi_sirt_host": (_I, [_P, _GP, _I, _P, _P, _I]),
+    "ctsm_mc_volume_3d": (_I, [_P, _U64, _P, _P, _D, _D, _D, _D, _P, _P, _U64, _U64, _P, _P, _P]),
+    "ctsm_multiline_volume_3d": (_I, [_P, _U64, _P, _P, _D, _D, _D, _D, _P, _P, _I, _P]),
+    "ctsm_gauss_legendre": (None, [_I, _P, _P]),
     "ctsm_selftest_division": (_I, [_P, _U64, _U64, ctypes.POINTER(_U64)]),
     "ctsm_csr_angle_nnz": (_I, [_P, _GP, _I, ctypes.POINTER(_U64), _P]),
     "ctsm_csr_build": (_I, [_P, _GP, _I, _I, _U64, _P, _P, _P, _U64, ctypes.POINTER(_U64), _P]),

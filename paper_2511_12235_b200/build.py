@@ -24,6 +24,7 @@ UNITS = {
     "csr.cu": ["-fmad=false"],
     "line.cu": ["-fmad=false"],
     "weights.cu": ["-fmad=false"],
+    "oracles.cu": ["-fmad=false"],
     "mf.cu": [],
     "solver.cu": ["-fmad=false"],
     "capi.cu": [],

@@ -743,6 +743,57 @@ SolveResult nag_tikhonov(const DeviceSystemMatrix& w, const std::vector<double>&
   return res;
 }
 
+// ---- independent numerical oracles (oracle.hpp:24-45) -------------------------
+std::vector<McEstimate> mc_volume_3d(const std::vector<double>& boxes,
+                                     const std::vector<double>& phi, double s, double d,
+                                     double d_y, double d_z, const std::vector<int>& m_y,
+                                     const std::vector<int>& m_z, std::uint64_t n_samples,
+                                     std::uint64_t seed) {
+  const size_t n = phi.size();
+  if (boxes.size() != 6 * n || m_y.size() != n || m_z.size() != n)
+    throw Error(ErrorCode::DimensionMismatch, "one box, angle and cell per case is required");
+  std::vector<double> v(n), se(n);
+  check(ctsm_mc_volume_3d(ctx(), n, boxes.data(), phi.data(), s, d, d_y, d_z, m_y.data(),
+                          m_z.data(), n_samples, seed, v.data(), se.data(), nullptr));
+  std::vector<McEstimate> out(n);
+  for (size_t i = 0; i < n; ++i) out[i] = {v[i], se[i]};
+  return out;
+}
+
+std::vector<double> multiline_volume_3d(const std::vector<double>& boxes,
+                                        const std::vector<double>& phi, double s, double d,
+                                        double d_y, double d_z, const std::vector<int>& m_y,
+                                        const std::vector<int>& m_z, int k) {
+  const size_t n = phi.size();
+  if (boxes.size() != 6 * n || m_y.size() != n || m_z.size() != n)
+    throw Error(ErrorCode::DimensionMismatch, "one box, angle and cell per case is required");
+  std::vector<double> out(n);
+  check(ctsm_multiline_volume_3d(ctx(), n, boxes.data(), phi.data(), s, d, d_y, d_z, m_y.data(),
+                                 m_z.data(), k, out.data()));
+  return out;
+}
+
+McEstimate mc_volume_3d(double x0, double x1, double y0, double y1, double zb, double zt,
+                        double phi, double s, double d, double d_y, double d_z, int m_y, int m_z,
+                        std::uint64_t n_samples, std::uint64_t seed) {
+  return mc_volume_3d(std::vector<double>{x0, x1, y0, y1, zb, zt}, std::vector<double>{phi}, s, d,
+                      d_y, d_z, std::vector<int>{m_y}, std::vector<int>{m_z}, n_samples, seed)[0];
+}
+
+double multiline_volume_3d(double x0, double x1, double y0, double y1, double zb, double zt,
+                           double phi, double s, double d, double d_y, double d_z, int m_y,
+                           int m_z, int k) {
+  return multiline_volume_3d(std::vector<double>{x0, x1, y0, y1, zb, zt}, std::vector<double>{phi},
+                             s, d, d_y, d_z, std::vector<int>{m_y}, std::vector<int>{m_z}, k)[0];
+}
+
+std::pair<std::vector<double>, std::vector<double>> gauss_legendre(int k) {
+  if (k <= 0) throw Error(ErrorCode::InvalidSpec, "k must be > 0");
+  std::vector<double> x((size_t)k), w((size_t)k);
+  ctsm_gauss_legendre(k, x.data(), w.data());
+  return {x, w};
+}
+
 // ---- multi-GPU variants -----------------------------------------------------
 namespace {
 struct Multi {

@@ -212,7 +212,6 @@ int check_mf3d_capacity(const ctsm_geometry* g) {
 // grid satisfies |tan| <= R / (s - R), R the grid half-diagonal.
 int dev_geom(const ctsm_geometry* g, DevGeom* out) {
   CT_TRY(validate(g));
-  CT_TRY(check_sweep_capacity(g));
   DevGeom d = make_dev_geom(*g);
   const double R = std::hypot(g->n_x * g->a / 2.0, g->n_y * g->b / 2.0);
   const double umax = R / (g->s - R) * (g->s + g->d) / g->d_y;
@@ -384,8 +383,9 @@ static int csr_budget_check(const ctsm_geometry* g, const DevGeom& d, uint64_t n
 
 static int csr_prologue(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int angle_end,
                         DevGeom* d) {
-  CT_TRY(set_device(ctx));
   CT_TRY(dev_geom(g, d));
+  CT_TRY(check_sweep_capacity(g));  // before any device work: testable without a GPU
+  CT_TRY(set_device(ctx));
   if ((uint64_t)g->n_x * g->n_y * g->n_z > 0xffffffffull)
     return fail(CTSM_ERR_TOO_LARGE, "grid exceeds 2^32 voxel columns");
   return check_shard(g, angle_begin, angle_end, 1);
@@ -587,9 +587,10 @@ int ctsm_csr_build(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int a
 int ctsm_weights_batch(ctsm_ctx* ctx, const ctsm_geometry* g, uint64_t n, const int32_t* ix,
                        const int32_t* iy, const int32_t* iz, const double* phi, int cap,
                        int32_t* count, int32_t* m_y, int32_t* m_z, double* w) {
-  CT_TRY(set_device(ctx));
   DevGeom d;
   CT_TRY(dev_geom(g, &d));
+  CT_TRY(check_sweep_capacity(g));
+  CT_TRY(set_device(ctx));
   if (cap <= 0) return fail(CTSM_ERR_INVALID_SPEC, "slab capacity must be > 0");
   if (n == 0) return 0;
   for (uint64_t q = 0; q < n; ++q) {
@@ -682,6 +683,80 @@ int ctsm_angle_block_entries(ctsm_ctx* ctx, const ctsm_geometry* g, int mode, in
                                     col_dev, w_dev, st));
   CT_CUDA(cudaStreamSynchronize(st));
   return 0;
+}
+
+// ---- independent numerical oracles (oracle.cpp:70-196) -----------------------
+static int oracle_upload(ctsm_ctx* ctx, uint64_t n, const double* boxes, const double* phi,
+                         const int32_t* m_y, const int32_t* m_z, double** dbox, double** dphi,
+                         int** dmy, int** dmz, cudaStream_t st) {
+  CT_TRY(ensure(ctx, ctx->tmp_a, n * (7 * sizeof(double) + 2 * sizeof(int))));
+  *dbox = (double*)ctx->tmp_a.p;
+  *dphi = *dbox + 6 * n;
+  *dmy = (int*)(*dphi + n);
+  *dmz = *dmy + n;
+  CT_CUDA(cudaMemcpyAsync(*dbox, boxes, 6 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+  CT_CUDA(cudaMemcpyAsync(*dphi, phi, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  CT_CUDA(cudaMemcpyAsync(*dmy, m_y, n * sizeof(int), cudaMemcpyHostToDevice, st));
+  CT_CUDA(cudaMemcpyAsync(*dmz, m_z, n * sizeof(int), cudaMemcpyHostToDevice, st));
+  return 0;
+}
+
+int ctsm_mc_volume_3d(ctsm_ctx* ctx, uint64_t n, const double* boxes, const double* phi, double s,
+                      double d, double d_y, double d_z, const int32_t* m_y, const int32_t* m_z,
+                      uint64_t n_samples, uint64_t seed, double* value, double* std_err,
+                      uint64_t* hits) {
+  CT_TRY(set_device(ctx));
+  if (n_samples == 0) return fail(CTSM_ERR_INVALID_SPEC, "n_samples must be > 0");
+  if (n == 0) return 0;
+  cudaStream_t st = nullptr;
+  double *dbox, *dphi;
+  int *dmy, *dmz;
+  CT_TRY(oracle_upload(ctx, n, boxes, phi, m_y, m_z, &dbox, &dphi, &dmy, &dmz, st));
+  CT_TRY(ensure(ctx, ctx->tmp_b, n * sizeof(unsigned long long)));
+  CT_CUDA(cudaMemsetAsync(ctx->tmp_b.p, 0, n * sizeof(unsigned long long), st));
+  CT_CUDA(mc_volume_batch((long long)n, dbox, dphi, s, d, d_y, d_z, dmy, dmz, n_samples, seed,
+                          (unsigned long long*)ctx->tmp_b.p, st));
+  std::vector<unsigned long long> h(n);
+  CT_CUDA(cudaMemcpyAsync(h.data(), ctx->tmp_b.p, n * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, st));
+  CT_CUDA(cudaStreamSynchronize(st));
+  for (uint64_t i = 0; i < n; ++i) {
+    // oracle.cpp:92-97: binomial standard error, floored at one count's worth
+    const double p = (double)h[i] / (double)n_samples;
+    const double var = std::max(p * (1.0 - p), 1.0 / (double)n_samples);
+    if (value) value[i] = p;
+    if (std_err) std_err[i] = std::sqrt(var / (double)n_samples);
+    if (hits) hits[i] = h[i];
+  }
+  return 0;
+}
+
+int ctsm_multiline_volume_3d(ctsm_ctx* ctx, uint64_t n, const double* boxes, const double* phi,
+                             double s, double d, double d_y, double d_z, const int32_t* m_y,
+                             const int32_t* m_z, int k, double* out) {
+  CT_TRY(set_device(ctx));
+  if (k <= 0) return fail(CTSM_ERR_INVALID_SPEC, "ray grid size k must be > 0");
+  if (n == 0) return 0;
+  cudaStream_t st = nullptr;
+  double *dbox, *dphi;
+  int *dmy, *dmz;
+  CT_TRY(oracle_upload(ctx, n, boxes, phi, m_y, m_z, &dbox, &dphi, &dmy, &dmz, st));
+  std::vector<double> nodes((size_t)2 * k);
+  gauss_legendre_host(k, nodes.data(), nodes.data() + k);
+  CT_TRY(ensure(ctx, ctx->tmp_b, (n + 2 * (size_t)k) * sizeof(double)));
+  double* dout = (double*)ctx->tmp_b.p;
+  double* dnodes = dout + n;
+  CT_CUDA(cudaMemcpyAsync(dnodes, nodes.data(), 2 * (size_t)k * sizeof(double),
+                          cudaMemcpyHostToDevice, st));
+  CT_CUDA(multiline_volume_batch((long long)n, dbox, dphi, s, d, d_y, d_z, dmy, dmz, k, dnodes,
+                                 dnodes + k, dout, st));
+  CT_CUDA(cudaMemcpyAsync(out, dout, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CT_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+void ctsm_gauss_legendre(int k, double* x, double* w) {
+  if (k > 0) gauss_legendre_host(k, x, w);
 }
 
 int ctsm_selftest_division(ctsm_ctx* ctx, uint64_t n, uint64_t seed, uint64_t* mismatches) {

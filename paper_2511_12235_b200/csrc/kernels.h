@@ -113,6 +113,19 @@ cudaError_t records_to_emission_order(const void* rec, const unsigned long long*
 cudaError_t expand_row_index(uint64_t n_rows, const uint64_t* row_start, uint32_t* raster,
                              cudaStream_t st);
 
+// ---- oracles.cu: mc_volume_3d / multiline_volume_3d (oracle.cpp:70-196) -----
+// Batches of cases (device arrays: box[6n] = x0 x1 y0 y1 zb zt, phi[n], my[n],
+// mz[n]); hits[n] (zeroed by the caller) receives the MC hit counts.
+cudaError_t mc_volume_batch(long long n_cases, const double* box, const double* phi, double s,
+                            double d, double d_y, double d_z, const int* my, const int* mz,
+                            unsigned long long n_samples, unsigned long long seed,
+                            unsigned long long* hits, cudaStream_t st);
+cudaError_t multiline_volume_batch(long long n_cases, const double* box, const double* phi,
+                                   double s, double d, double d_y, double d_z, const int* my,
+                                   const int* mz, int k, const double* nodes, const double* wts,
+                                   double* out, cudaStream_t st);
+void gauss_legendre_host(int k, double* x, double* w);
+
 // ---- mf.cu ---------------------------------------------------------------
 // Pieces one column sweep of the 3D matrix-free kernels may hold (fast3dw.cuh).
 int mf3d_max_pieces();

@@ -342,6 +342,30 @@ int main() {
                                                      std::vector<int>{0, 0}); }) ==
            (int)ErrorCode::InvalidSpec);
   }
+  // ---- device MC / Gauss-Legendre oracles (oracle.hpp:24-45) ----------------
+  {
+    const ScanGeometry g = small_scan(true);
+    const VoxelIndex n{4, 7, 6};
+    const double phi = 0.7;
+    const auto ws = voxel_volume_factors(n, phi, g);
+    EXPECT(!ws.empty());
+    const VoxelWeight* best = &ws[0];
+    for (const auto& vw : ws)
+      if (vw.w > best->w) best = &vw;
+    const McEstimate mc =
+        mc_volume_3d(g.face_x(n.ix), g.face_x(n.ix + 1), g.face_y(n.iy), g.face_y(n.iy + 1),
+                     g.face_z(n.iz), g.face_z(n.iz + 1), phi, g.s, g.d, g.d_y, g.d_z, best->m_y,
+                     best->m_z, 400000, 99);
+    EXPECT(std::abs(best->w - mc.value) < 4 * mc.std_err + 1e-6);  // test_weights3d.cpp:198-212
+    const double gl = multiline_volume_3d(g.face_x(n.ix), g.face_x(n.ix + 1), g.face_y(n.iy),
+                                          g.face_y(n.iy + 1), g.face_z(n.iz), g.face_z(n.iz + 1),
+                                          phi, g.s, g.d, g.d_y, g.d_z, best->m_y, best->m_z, 100);
+    EXPECT(std::abs(gl - best->w) < 2e-5);  // k = 100 quadrature of a kinked integrand
+    const auto glw = gauss_legendre(16);
+    double sw = 0;
+    for (double v : glw.second) sw += v;
+    EXPECT(std::abs(sw - 2.0) < 1e-13);
+  }
   // ---- re-entrancy: concurrent calls from several host threads (each thread
   // gets its own context) give the single-thread result ----------------------
   {

@@ -56,10 +56,12 @@ def test_errors_without_gpu_are_loud():
     assert st != 0
 
 
-def test_validate_rejects_sweeps_beyond_the_device_capacity():
+def test_exact_paths_reject_sweeps_beyond_the_device_capacity():
     """A detector pitch so fine that a pixel's shadow spans more cells than the
-    device sweep holds is rejected by name (TooLarge) at validation, not by a
-    kernel (the reference's sweep is a std::vector and has no such limit)."""
+    device sweep holds is rejected by name (TooLarge) by the exact (CSR /
+    weight API) entry points before any device work, not by a kernel (the
+    reference's sweep is a std::vector and has no such limit). The 2D
+    matrix-free kernels have no such limit, so validation itself passes."""
     import ctypes
 
     from paper_2511_12235_b200 import CONFIGS
@@ -69,8 +71,11 @@ def test_validate_rejects_sweeps_beyond_the_device_capacity():
     cg = g.to_c()
     assert L.ctsm_validate_geometry(ctypes.byref(cg)) == 0
     fine = g.with_(d_y=g.d_y / 12, n_det_y=g.n_det_y * 12).to_c()
-    assert L.ctsm_validate_geometry(ctypes.byref(fine)) == 9  # TooLarge
+    assert L.ctsm_validate_geometry(ctypes.byref(fine)) == 0
+    nnz = ctypes.c_uint64(0)
+    assert L.ctsm_csr_angle_nnz(None, ctypes.byref(fine), 0, ctypes.byref(nnz), None) == 9  # TooLarge
     assert b"shadow" in L.ctsm_last_error()
-    for name in ("c1", "c2", "c3", "c4"):  # every BASELINE config is within the limits
+    for name in ("c0", "c1", "c2", "c3", "c4"):  # every BASELINE config is within the limits
         cg = CONFIGS[name].to_c()
-        assert L.ctsm_validate_geometry(ctypes.byref(cg)) == 0
+        st = L.ctsm_csr_angle_nnz(None, ctypes.byref(cg), 0, ctypes.byref(nnz), None)
+        assert st != 9, name  # (fails later: no context / no device here)

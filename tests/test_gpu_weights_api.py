@@ -150,3 +150,38 @@ def test_multi_context_rejects_bad_device_lists():
     assert L.ctsm_multi_create(arr, 0, ctypes.byref(h)) == 10
     arr = (ctypes.c_int * 1)(99)
     assert L.ctsm_multi_create(arr, 1, ctypes.byref(h)) == 10  # no such device
+
+
+# ---- device MC / Gauss-Legendre oracles -------------
+def test_device_numeric_oracles(oracle_cr):
+    """mc_volume_3d on the device reproduces the CPU oracle's hit counts (same
+    16 mt19937_64 sub-streams, same arithmetic); multiline_volume_3d agrees to
+    rounding; both agree with the closed-form weights by the reference's
+    criteria (test_weights3d.cpp:198-212)."""
+    from paper_2511_12235_b200.oracles import (mc_volume_3d, mc_volume_3d_batch,
+                                               multiline_volume_3d_batch, voxel_box)
+    g = TEST_GEOMETRIES["cone3d"]
+    rng = np.random.default_rng(8)
+    boxes, phis, mys, mzs, ws = [], [], [], [], []
+    for _ in range(24):
+        ix, iy, iz = (int(v) for v in rng.integers(0, 6, 3))
+        phi = float(rng.uniform(0, 6.28))
+        my, mz, w = oracle_cr.voxel_volume_factors(g, ix, iy, iz, phi)
+        i = int(np.argmax(w))
+        boxes.append(voxel_box(g, ix, iy, iz))
+        phis.append(phi)
+        mys.append(int(my[i]))
+        mzs.append(int(mz[i]))
+        ws.append(float(w[i]))
+    n_samples, seed = 100003, 99
+    v, se, hits = mc_volume_3d_batch(boxes, phis, g.s, g.d, g.d_y, g.d_z, mys, mzs, n_samples, seed)
+    gl = multiline_volume_3d_batch(boxes, phis, g.s, g.d, g.d_y, g.d_z, mys, mzs, 100)
+    for c in range(len(ws)):
+        rv, rse, rh = oracle_cr.mc_volume_3d(g, boxes[c], phis[c], mys[c], mzs[c], n_samples, seed)
+        assert int(hits[c]) == rh and v[c] == rv and se[c] == rse
+        assert abs(ws[c] - v[c]) < 4 * se[c] + 1e-6
+        rgl = oracle_cr.multiline_volume_3d(g, boxes[c], phis[c], mys[c], mzs[c], 100)
+        assert abs(gl[c] - rgl) <= 1e-12 * max(1.0, abs(rgl))
+        assert abs(gl[c] - ws[c]) < 2e-5  # k = 100 quadrature of a kinked integrand
+    one = mc_volume_3d(*boxes[0], phis[0], g.s, g.d, g.d_y, g.d_z, mys[0], mzs[0], n_samples, seed)
+    assert one.value == v[0] and one.std_err == se[0]

@@ -237,3 +237,42 @@ def test_port_equals_reference_ray_modes(tag):
             a = port.line_weights(g, m_y, m_z, ip, mode, k)
             b = ref.line_weights(g, m_y, m_z, ip, mode, k)
             assert np.array_equal(a[0], b[0]) and same_bits(a[1], b[1])
+
+
+def test_numeric_oracles_agree_with_the_closed_form():
+    """Pin of the restated MC / Gauss-Legendre oracles (oracle.cpp:70-196; the
+    reference file needs Eigen and cannot be compiled here): the reference's
+    own criteria -- MC within 4 standard errors + 1e-6 of the voxel weight
+    (test_weights3d.cpp:198-212), the ray-grid integral within 1e-6."""
+    import pyoracle
+    from paper_2511_12235_b200 import TEST_GEOMETRIES
+
+    o = pyoracle.load("port_cr")
+    g = TEST_GEOMETRIES["cone3d"]
+    for (ix, iy, iz, phi) in ((1, 2, 4, 0.7), (3, 0, 1, 2.9), (5, 5, 3, 5.1)):
+        my, mz, w = o.voxel_volume_factors(g, ix, iy, iz, phi)
+        box = o.voxel_box(g, ix, iy, iz)
+        tot = 0.0
+        for i in np.argsort(-w)[:3]:
+            v, se, hits = o.mc_volume_3d(g, box, phi, int(my[i]), int(mz[i]), 200000, 99)
+            assert abs(w[i] - v) < 4 * se + 1e-6
+            assert hits == round(v * 200000)
+            gl = o.multiline_volume_3d(g, box, phi, int(my[i]), int(mz[i]), 120)
+            assert abs(gl - w[i]) < 1e-6
+            tot += gl
+        assert tot <= 1.0 + 1e-6
+    x, wt = o.gauss_legendre(24)
+    xr, wr = np.polynomial.legendre.leggauss(24)
+    assert np.max(np.abs(np.sort(x) - xr)) < 1e-14 and np.max(np.abs(wt[np.argsort(x)] - wr)) < 1e-14
+
+
+def test_library_gauss_legendre_matches_the_oracle():
+    """ctsm_gauss_legendre is host code (no GPU): same Newton iteration."""
+    import pyoracle
+    from paper_2511_12235_b200.oracles import gauss_legendre
+
+    o = pyoracle.load("port_cr")
+    for k in (1, 2, 7, 200):
+        x, w = gauss_legendre(k)
+        xo, wo = o.gauss_legendre(k)
+        assert np.array_equal(x, xo) and np.array_equal(w, wo)
