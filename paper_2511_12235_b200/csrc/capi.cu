@@ -77,7 +77,7 @@ struct ctsm_ctx {
   Buf angles, edges, cs, counts, scan, longrows, acc, part, base, alist, sv_up, sv_h, sv_hp,
       sv_q, sv_v, sv_part, sv_scal, tmp_a, tmp_b, tmp_c, tmp_d,
       tmp_e, tmp_f, lraw_start, lraw_col, lraw_val, lacc, bwd_t, vol_t, plans, rec, grp,
-      cursor, plans2, rec2, grp2, angles2, counts2, longrows2;
+      cursor, plans2, rec2, grp2, angles2, counts2, longrows2, mfplans;
   // second stream + events of the pipelined CSR build (ctsm_csr_build)
   cudaStream_t side = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -299,7 +299,7 @@ int ctsm_destroy(ctsm_ctx* ctx) {
                  &ctx->tmp_d, &ctx->tmp_e, &ctx->tmp_f, &ctx->lraw_start, &ctx->lraw_col,
                  &ctx->lraw_val, &ctx->lacc, &ctx->bwd_t, &ctx->vol_t, &ctx->plans, &ctx->rec,
                  &ctx->grp, &ctx->cursor, &ctx->plans2, &ctx->rec2, &ctx->grp2, &ctx->angles2,
-                 &ctx->counts2, &ctx->longrows2};
+                 &ctx->counts2, &ctx->longrows2, &ctx->mfplans};
   if (ctx->side) cudaStreamDestroy(ctx->side);
   for (cudaEvent_t e : ctx->ev)
     if (e) cudaEventDestroy(e);
@@ -948,9 +948,10 @@ static int fwd_d8_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d, 
     CT_TRY(ensure(ctx, ctx->bwd_t, nf * sizeof(float)));
     CT_TRY(ensure(ctx, ctx->vol_t, (size_t)d.n_vox * sizeof(float)));
     CT_CUDA(cudaMemsetAsync(ctx->n_upd, 0, sizeof(unsigned long long), st));
+    CT_TRY(ensure(ctx, ctx->mfplans, mf3d_plan_bytes(d, 8)));
     CT_CUDA(fwd3d_mf_d8_f32(d, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb,
                             (const float*)x, (float*)y, ctx->n_upd, ctx->status, st, ctx->vol_t.p,
-                            (float*)ctx->bwd_t.p));
+                            (float*)ctx->bwd_t.p, ctx->mfplans.p));
     CT_CUDA(cudaMemcpyAsync(ctx->h_upd, ctx->n_upd, sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, st));
     return 0;
@@ -977,8 +978,10 @@ static int fwd_d8_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d, 
                       scale, ctx->n_upd, ctx->status, st));
   } else {
     CT_TRY(ensure(ctx, ctx->vol_t, (size_t)d.n_vox * (dtype == CTSM_F64 ? 8 : 4)));
+    CT_TRY(ensure(ctx, ctx->mfplans, mf3d_plan_bytes(d, 8)));
     CT_CUDA(fwd3d_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, x,
-                         acc, scale, ctx->n_upd, ctx->status, st, 8, ctx->vol_t.p));
+                         acc, scale, ctx->n_upd, ctx->status, st, 8, ctx->vol_t.p,
+                         ctx->mfplans.p));
   }
   CT_CUDA(rows_list(d, dtype, al, nl, acc, scale, y, 1, st));
   CT_CUDA(cudaMemcpyAsync(ctx->h_upd, ctx->n_upd, sizeof(unsigned long long),
@@ -1011,8 +1014,10 @@ static int fwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d,
                        scale, ctx->n_upd, ctx->status, st));
   } else {
     CT_TRY(ensure(ctx, ctx->vol_t, (size_t)d.n_vox * (dtype == CTSM_F64 ? 8 : 4)));
+    CT_TRY(ensure(ctx, ctx->mfplans, mf3d_plan_bytes(d, 4)));
     CT_CUDA(fwd3d_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, x,
-                         acc, scale, ctx->n_upd, ctx->status, st, 4, ctx->vol_t.p));
+                         acc, scale, ctx->n_upd, ctx->status, st, 4, ctx->vol_t.p,
+                         ctx->mfplans.p));
   }
   for (int k = 0; k < 4; ++k)
     CT_CUDA(fixed_to_float_rows(d, dtype, base[0] + k * q, base_step, nb, acc, scale, y, st));
@@ -1032,9 +1037,10 @@ static int bwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d,
     if (!ne) ctx->last_path &= ~CTSM_PATH_ZMIRROR;  // the plain-gather variant has no mirror
     if (ne) CT_TRY(ensure(ctx, ctx->bwd_t, ne * (dtype == CTSM_F64 ? 8 : 4)));
     CT_TRY(ensure(ctx, ctx->vol_t, (size_t)d.n_vox * (dtype == CTSM_F64 ? 8 : 4)));
+    CT_TRY(ensure(ctx, ctx->mfplans, mf3d_plan_bytes(d, symmetry_order(g))));
     CT_CUDA(bwd3d_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, y, x,
                          ctx->status, st, symmetry_order(g), ne ? ctx->bwd_t.p : nullptr,
-                         ctx->vol_t.p));
+                         ctx->vol_t.p, ctx->mfplans.p));
   } else if (symmetry_order(g) == 8) {
     const int nc = bwd_d8_chunks(d, nb);
     if (nc > 1) CT_TRY(ensure(ctx, ctx->part, (size_t)nc * g->n_x * g->n_y * sizeof(double)));

@@ -42,11 +42,11 @@ constexpr int kMaxPieces = 12;  // pieces of one column sweep inside the detecto
 // Only mixed flags need the reference's cubic forms.
 constexpr int kCoef = 24;
 constexpr int kLin = 14;
-struct PieceCoef {
+struct alignas(32) PieceCoef {
   double c[kCoef];
 };
 
-struct ColumnHead {
+struct alignas(32) ColumnHead {
   double S, C, invS, invC, kappa;  // canonical sin/cos of phi', 1/S, 1/C, a'^2/(6 b' c)
   double inv_a;                    // 1 / a' (G = zref / (a' tan_a))
   double dmin_inv, dmax_inv;       // extremes of 1/depth over the 4 xy corners
@@ -112,9 +112,14 @@ __device__ __forceinline__ double trap_tt(const ColumnHead& h, const double* c, 
   return t * c[6];
 }
 
-// Plans one (column, angle): every lane of the warp computes the sweep (cheap,
-// identical), lane j computes piece j's coefficients into P[j]; lane 0 writes
-// the head. Caller must __syncwarp() before reading H / P.
+// Plans one (column, angle). Warp-cooperative form (kSerial = false): every
+// lane of the warp computes the sweep (identical), lane j computes piece j's
+// coefficients into P[j]; lane 0 writes the head; the caller must
+// __syncwarp() before reading H / P. Serial form (kSerial = true, lane = 0):
+// one thread does all of it -- used by plan3d_fast_kernel, which plans a
+// whole launch's (column, base angle) pairs one per thread, so the sweep is
+// computed once instead of by all 32 lanes of the projection kernel's warp.
+template <bool kSerial = false>
 __device__ __forceinline__ bool plan_column(const DevGeom& g, double C, double S, int ix, int iy,
                                             int* status, ColumnHead& H, PieceCoef* P,
                                             int lane) {
@@ -150,6 +155,13 @@ __device__ __forceinline__ bool plan_column(const DevGeom& g, double C, double S
   int np = 0, ng = 0, last_end = 0;
   double my_lo = 0.0, my_hi = 0.0;
   int my_kind = -1;
+  // serial form: nothing is read back from H / P (global memory there): the
+  // piece bounds stay in thread-local arrays, kinds and group ends in packed
+  // registers, and the group aggregates are accumulated while the pieces are
+  // computed (same order as the warp form's per-group loop)
+  double all_lo[kSerial ? kMaxPieces : 1], all_hi[kSerial ? kMaxPieces : 1];
+  unsigned kinds = 0;             // 2 bits per piece
+  unsigned long long gends = 0;   // 4 bits per group
   bool overflow = false;
   sweep_walk(
       g, C, S, sw,
@@ -159,7 +171,11 @@ __device__ __forceinline__ bool plan_column(const DevGeom& g, double C, double S
           overflow = true;
           return;
         }
-        if (lane == np) {
+        if (kSerial) {
+          all_lo[np] = tlo;
+          all_hi[np] = thi;
+          kinds |= (unsigned)zone << (2 * np);
+        } else if (lane == np) {
           my_lo = tlo;
           my_hi = thi;
           my_kind = zone;
@@ -176,6 +192,7 @@ __device__ __forceinline__ bool plan_column(const DevGeom& g, double C, double S
             H.gcell[ng] = cell;
             H.gw2d[ng] = acc > 0.0 ? acc : 0.0;
           }
+          if (kSerial) gends |= (unsigned long long)np << (4 * ng);
           ++ng;
           last_end = np;
         }
@@ -208,10 +225,22 @@ __device__ __forceinline__ bool plan_column(const DevGeom& g, double C, double S
     H.np = np;
     H.ng = ng;
   }
-  if (lane < np) {
+  int qcur = 0;
+  double agg_mn = 1e300, agg_mx = -1e300, agg_al = 0.0, agg_be = 0.0;
+  for (int pj = kSerial ? 0 : lane; pj < np && (kSerial || pj == lane); ++pj) {
+    if (kSerial) {
+      my_lo = all_lo[pj];
+      my_hi = all_hi[pj];
+      my_kind = (int)((kinds >> (2 * pj)) & 3u);
+    }
     // constant divisors as reciprocal multiplies (tolerance-checked path)
     const double ica = 1.0 / ca;
-    double* c = P[lane].c;
+    double cl[kSerial ? kCoef : 1];
+    if (kSerial) {
+#pragma unroll
+      for (int i = 0; i < kCoef; ++i) cl[i] = 0.0;
+    }
+    double* c = kSerial ? cl : P[pj].c;
     if (my_kind == 1) {
       // trap_flags_at / trap_atom_flags (weights3d.cpp:63-107)
       const double t1 = my_lo, t2 = my_hi;
@@ -258,6 +287,7 @@ __device__ __forceinline__ bool plan_column(const DevGeom& g, double C, double S
       const double thgg = Pq * Cp + Qq * Sp;
       const double Da = s - xa * Cp - ya * Sp;       // apex depth (= a' thgg)
       const double ta = my_kind == 0 ? sw.T1 : sw.T4;  // apex ray parameter
+#pragma unroll
       for (int e = 0; e < 2; ++e) {
         const double t = e == 0 ? my_lo : my_hi;
         const double crg = Cp + Sp * t, srh = Sp - Cp * t;
@@ -282,10 +312,43 @@ __device__ __forceinline__ bool plan_column(const DevGeom& g, double C, double S
         l[3] = dcen * ica;
       }
     }
+    if (kSerial) {
+      const double* l = cl + kLin;
+      // the piece leaves as six 32-byte stores (whole sectors: no partial
+      // writes, 6 instead of 22 store instructions per piece)
+#pragma unroll
+      for (int i = 0; i < kCoef; i += 4)
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(P[pj].c + i), "d"(cl[i]),
+                     "d"(cl[i + 1]), "d"(cl[i + 2]), "d"(cl[i + 3])
+                     : "memory");
+      if (my_kind == 1) {
+        agg_mn = fmin(agg_mn, l[0]);
+        agg_mx = fmax(agg_mx, l[1]);
+        agg_al += l[2];
+        agg_be += l[2] * l[3];
+      } else {
+        const double sg = my_kind == 0 ? 1.0 : -1.0;
+        agg_mn = fmin(agg_mn, fmin(l[0], l[4]));
+        agg_mx = fmax(agg_mx, fmax(l[1], l[5]));
+        agg_al += sg * (l[6] - l[2]);
+        agg_be += sg * (l[6] * l[7] - l[2] * l[3]);
+      }
+      if (pj + 1 == (int)((gends >> (4 * qcur)) & 15ull)) {  // last piece of group qcur
+        H.gmin[qcur] = agg_mn;
+        H.gmax[qcur] = agg_mx;
+        H.galpha[qcur] = agg_al;
+        H.gbeta[qcur] = agg_be;
+        ++qcur;
+        agg_mn = 1e300;
+        agg_mx = -1e300;
+        agg_al = agg_be = 0.0;
+      }
+    }
   }
+  if (kSerial) return true;
   __syncwarp();
-  if (lane < ng) {  // group aggregates (lane q handles group q)
-    const int q = lane;
+  for (int q = kSerial ? 0 : lane; q < ng && (kSerial || q == lane); ++q) {
+    // group aggregates (warp form: lane q handles group q)
     double mn = 1e300, mx = -1e300, al = 0.0, be = 0.0;
 #pragma unroll 1
     for (int k = H.gbeg[q]; k < H.gend[q]; ++k) {

@@ -172,17 +172,21 @@ cudaError_t rows_list(const DevGeom& g, int dtype, const int* angles, int n_list
 size_t fwd3d_f32_scratch_elems(const DevGeom& g, int order);
 cudaError_t fwd3d_mf_d8_f32(const DevGeom& g, const AngleCS* cs, const int* base, int n_base,
                             const float* x_in, float* y, unsigned long long* n_upd, int* status,
-                            cudaStream_t st, void* vol_t, float* yt);
+                            cudaStream_t st, void* vol_t, float* yt, void* plans = nullptr);
 cudaError_t fwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                          int n_base, const void* x, unsigned long long* yacc, double scale,
                          unsigned long long* n_upd, int* status, cudaStream_t st, int order,
-                         void* vol_t);
+                         void* vol_t, void* plans = nullptr);
 // scratch: bwd3d_scratch_elems(...) elements of the dtype (transposed image
 // rows of one L2 chunk), or NULL for the untransposed gather.
 size_t bwd3d_scratch_elems(const DevGeom& g, int order, int dtype);
 cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                          int n_base, const void* y, void* x, int* status, cudaStream_t st,
-                         int order, void* scratch, void* vol_t);
+                         int order, void* scratch, void* vol_t, void* plans = nullptr);
+// Plan scratch of one launch of the symmetric 3D kernels (0: plan in-kernel):
+// the (column, base angle) plans of a launch are computed one per thread by a
+// plan pass instead of by every projection warp.
+size_t mf3d_plan_bytes(const DevGeom& g, int order);
 cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
                    int angle_step, int n_sel, const void* x, unsigned long long* yacc,
                    double scale, unsigned long long* n_upd, int* status, cudaStream_t st);

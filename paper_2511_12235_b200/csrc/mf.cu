@@ -705,6 +705,65 @@ __global__ void __launch_bounds__(128, CTSM_D8B_MINB) bwd2d_d8_kernel(
 // per z-block ([image][slot][lane], conflict-free) and reused for all base
 // angles: the per-weight reads are shared-memory hits instead of G scattered
 // global loads.
+// ---- plan pass of the symmetric 3D kernels --------------------------------
+// Planning a (column, base angle) -- the xy sweep, the pieces' G-independent
+// coefficients, the group short cuts -- does not depend on z. Inside the
+// projection kernels it was done by the whole warp (every lane computing the
+// same sweep), 26 % of a C3 projection. plan3d_fast_kernel plans all (column,
+// base angle) pairs of a launch with ONE THREAD each (full lanes instead of 32
+// redundant copies) into global memory; the projection kernels then load the
+// plan (coalesced, ~1-3 KB) into shared memory instead of computing it.
+struct FastPlan {
+  fast::ColumnHead H;
+  fast::PieceCoef P[fast::kMaxPieces];
+};
+static_assert(sizeof(fast::ColumnHead) % 32 == 0 && sizeof(fast::PieceCoef) % 32 == 0,
+              "plans are stored as 32-byte vectors and loaded as 16-byte vectors");
+
+__global__ void __launch_bounds__(128) plan3d_fast_kernel(DevGeom g, const AngleCS* __restrict__ cs,
+                                                          int n_base, FastPlan* __restrict__ plans,
+                                                          int* status) {
+  const long long nxy = (long long)g.n_x * g.n_y;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nxy * n_base) return;
+  const int kk = (int)(t / nxy);
+  const long long col = t - (long long)kk * nxy;
+  FastPlan* out = plans + t;
+  // the head is assembled in thread-local memory (small fields written all
+  // over it) and leaves as 32-byte stores; the pieces are stored from
+  // registers by plan_column
+  fast::ColumnHead Hl;
+  fast::plan_column<true>(g, cs[kk].C, cs[kk].S, (int)(col % g.n_x), (int)(col / g.n_x), status,
+                          Hl, out->P, 0);
+  const double* src = reinterpret_cast<const double*>(&Hl);
+  double* dst = reinterpret_cast<double*>(&out->H);
+#pragma unroll 1
+  for (int i = 0; i < (int)(sizeof(fast::ColumnHead) / 8); i += 4)
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst + i), "d"(src[i]),
+                 "d"(src[i + 1]), "d"(src[i + 2]), "d"(src[i + 3])
+                 : "memory");
+}
+
+// Loads the plan of (column, slot kk) into the warp's shared head / pieces.
+// Returns false for a column without work (failed sweep or no cell group).
+__device__ __forceinline__ bool load_plan(const FastPlan* __restrict__ plans, long long idx,
+                                          fast::ColumnHead& H, fast::PieceCoef* P, int lane) {
+  const FastPlan* src = plans + idx;
+  {
+    const double2* s2 = reinterpret_cast<const double2*>(&src->H);
+    double2* d2 = reinterpret_cast<double2*>(&H);
+    for (int i = lane; i < (int)(sizeof(fast::ColumnHead) / 16); i += 32) d2[i] = __ldg(&s2[i]);
+  }
+  __syncwarp();
+  const int np = H.np;
+  {
+    const double2* s2 = reinterpret_cast<const double2*>(src->P);
+    double2* d2 = reinterpret_cast<double2*>(P);
+    for (int i = lane; i < np * (int)(sizeof(fast::PieceCoef) / 16); i += 32) d2[i] = __ldg(&s2[i]);
+  }
+  return H.ng > 0;
+}
+
 #ifndef CTSM_KZCF
 #define CTSM_KZCF 8
 #endif
@@ -737,9 +796,10 @@ template <typename T, int G, bool FA = false>
 __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
     const T* __restrict__ in, unsigned long long* __restrict__ yacc, double scale,
-    unsigned long long* n_upd, int* status, float* __restrict__ yt = nullptr) {
-  __shared__ fast::ColumnHead sh[kWarps3];
-  __shared__ fast::PieceCoef sp[kWarps3][fast::kMaxPieces];
+    unsigned long long* n_upd, int* status, float* __restrict__ yt = nullptr,
+    const FastPlan* __restrict__ plans = nullptr) {
+  __shared__ __align__(16) fast::ColumnHead sh[kWarps3];
+  __shared__ __align__(16) fast::PieceCoef sp[kWarps3][fast::kMaxPieces];
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   // [warp][t][chunk][lane][V]: the G image values of (t, lane) as NC 16-byte
   // vectors, each chunk conflict-free across the lanes (one LDS.128 each)
@@ -792,7 +852,9 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
       const int ne = full ? G : 4;
       __syncwarp();
       if (lane < G) sab[warp][lane] = (long long)d4_angle(g.n_angles, i, lane) * rpa;
-      const bool ok = fast::plan_column(g, a.C, a.S, ix, iy, status, sh[warp], sp[warp], lane);
+      const bool ok = plans ? load_plan(plans, (long long)kk * nxy + col, sh[warp], sp[warp], lane)
+                            : fast::plan_column(g, a.C, a.S, ix, iy, status, sh[warp], sp[warp],
+                                                lane);
       __syncwarp();
       if (!ok) continue;
       const fast::GroupTable* TB = table3d(sh[warp], sp[warp], CTSM_TABLE_PTR, lane);
@@ -933,10 +995,11 @@ __host__ __device__ constexpr int bwd3_zc() { return sizeof(T) == 4 ? CTSM_KZCS_
 template <typename T, int G, bool TR>
 __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sym_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
-    const T* __restrict__ in, T* __restrict__ xout, int accumulate, int* status) {
+    const T* __restrict__ in, T* __restrict__ xout, int accumulate, int* status,
+    const FastPlan* __restrict__ plans = nullptr) {
   constexpr int kWarpsS = bwd3_warps<T>();
-  __shared__ fast::ColumnHead sh[kWarpsS];
-  __shared__ fast::PieceCoef sp[kWarpsS][fast::kMaxPieces];
+  __shared__ __align__(16) fast::ColumnHead sh[kWarpsS];
+  __shared__ __align__(16) fast::PieceCoef sp[kWarpsS][fast::kMaxPieces];
   // fp32 volumes accumulate their per-launch sums in fp32 (fixed order, so
   // still deterministic): at most ~chunk * 12 terms per slot, an error far
   // below the fp32 tolerance, and half the shared memory -> more warps/SM
@@ -1005,7 +1068,10 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
         int cx, cy;
         d4_pixel(n, ix0, iy0, hm, cx, cy);
         __syncwarp();
-        const bool ok = fast::plan_column(g, a.C, a.S, cx, cy, status, sh[warp], sp[warp], lane);
+        const bool ok =
+            plans ? load_plan(plans, (long long)kk * ((long long)n * g.n_y) + (long long)cy * n + cx,
+                              sh[warp], sp[warp], lane)
+                  : fast::plan_column(g, a.C, a.S, cx, cy, status, sh[warp], sp[warp], lane);
         __syncwarp();
         if (!ok) continue;
         const fast::GroupTable* TB = table3d(sh[warp], sp[warp], CTSM_TABLE_PTR, lane);
@@ -1386,6 +1452,24 @@ __global__ void fwd3d_uninterleave(const float* __restrict__ yt, const int* __re
   }
 }
 
+// Bytes of the plan scratch of one launch of the symmetric 3D kernels (the
+// fp32 chunking is the larger one).
+size_t mf3d_plan_bytes(const DevGeom& g, int order) {
+  static const bool off = getenv("CTSM_NO_PLAN_PASS") != nullptr;
+  if (off || (g.n_z == 1 && g.n_det_z == 1)) return 0;
+  return (size_t)g.n_x * g.n_y * (size_t)sym3d_chunk(g, order, 4) * sizeof(FastPlan);
+}
+
+static cudaError_t plan_pass(const DevGeom& g, const AngleCS* cs, int nk, void* plans, int* status,
+                             cudaStream_t st) {
+  if (!plans) return cudaSuccess;
+  const long long n = (long long)g.n_x * g.n_y * nk;
+  plan3d_fast_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(g, cs, nk, (FastPlan*)plans,
+                                                                  status);
+  count_launch();
+  return cudaGetLastError();
+}
+
 size_t fwd3d_f32_scratch_elems(const DevGeom& g, int order) {
   if (order != 8 || getenv("CTSM_FWD3_FIXED")) return 0;
   return (size_t)sym3d_chunk(g, order, 4) * order * g.rows_per_angle;
@@ -1395,7 +1479,7 @@ size_t fwd3d_f32_scratch_elems(const DevGeom& g, int order) {
 // FA): writes the image rows of every base angle into y (fp32).
 cudaError_t fwd3d_mf_d8_f32(const DevGeom& g, const AngleCS* cs, const int* base, int n_base,
                             const float* x_in, float* y, unsigned long long* n_upd, int* status,
-                            cudaStream_t st, void* vol_t, float* yt) {
+                            cudaStream_t st, void* vol_t, float* yt, void* plans) {
   if (n_base <= 0) return cudaSuccess;
   {
     const cudaError_t e = transpose2d(CTSM_F32, x_in, vol_t, g.n_z, (long long)g.n_x * g.n_y, st);
@@ -1411,8 +1495,11 @@ cudaError_t fwd3d_mf_d8_f32(const DevGeom& g, const AngleCS* cs, const int* base
     const int nk = n_base - k0 < chunk ? n_base - k0 : chunk;
     cudaError_t e = cudaMemsetAsync(yt, 0, (size_t)nk * 8 * g.rows_per_angle * sizeof(float), st);
     if (e != cudaSuccess) return e;
+    e = plan_pass(g, cs + k0, nk, plans, status, st);
+    if (e != cudaSuccess) return e;
     fwd3d_sym_kernel<float, 8, true><<<blocks, kWarps3 * 32, smem, st>>>(
-        g, cs + k0, base + k0, nk, (const float*)vol_t, nullptr, 1.0, n_upd, status, yt);
+        g, cs + k0, base + k0, nk, (const float*)vol_t, nullptr, 1.0, n_upd, status, yt,
+        (const FastPlan*)plans);
     count_launch();
     const dim3 ug((g.n_det_y + 31) / 32, (g.n_det_z + 31) / 32, (unsigned)nk);
     fwd3d_uninterleave<8><<<ug, dim3(32, 8), 0, st>>>(yt, base + k0, g.n_angles, g.n_det_y,
@@ -1425,7 +1512,7 @@ cudaError_t fwd3d_mf_d8_f32(const DevGeom& g, const AngleCS* cs, const int* base
 cudaError_t fwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                          int n_base, const void* x_in, unsigned long long* yacc, double scale,
                          unsigned long long* n_upd, int* status, cudaStream_t st, int order,
-                         void* vol_t) {
+                         void* vol_t, void* plans) {
   if (n_base <= 0) return cudaSuccess;
   {
     const cudaError_t e = transpose2d(dtype, x_in, vol_t, g.n_z, (long long)g.n_x * g.n_y, st);
@@ -1437,14 +1524,18 @@ cudaError_t fwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const i
   const int chunk = sym3d_chunk(g, order, sizeof(unsigned long long));
   for (int k0 = 0; k0 < n_base; k0 += chunk) {
     const int nk = n_base - k0 < chunk ? n_base - k0 : chunk;
+    {
+      const cudaError_t e = plan_pass(g, cs + k0, nk, plans, status, st);
+      if (e != cudaSuccess) return e;
+    }
 #define CTSM_LAUNCH(T, G)                                                                     \
   do {                                                                                        \
     constexpr size_t smem = fwd3d_sym_dyn_smem<T, G>();                                       \
     cudaFuncSetAttribute(fwd3d_sym_kernel<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                          (int)smem);                                                          \
-    fwd3d_sym_kernel<T, G><<<blocks, kWarps3 * 32, smem, st>>>(g, cs + k0, base + k0, nk,      \
-                                                               (const T*)x, yacc, scale,       \
-                                                               n_upd, status);                \
+    fwd3d_sym_kernel<T, G><<<blocks, kWarps3 * 32, smem, st>>>(                                \
+        g, cs + k0, base + k0, nk, (const T*)x, yacc, scale, n_upd, status, nullptr,           \
+        (const FastPlan*)plans);                                                              \
   } while (0)
     if (dtype == CTSM_F64) {
       if (order == 8) CTSM_LAUNCH(double, 8); else CTSM_LAUNCH(double, 4);
@@ -1493,7 +1584,7 @@ size_t bwd3d_scratch_elems(const DevGeom& g, int order, int dtype) {
 
 cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int* base,
                          int n_base, const void* y, void* x_out, int* status, cudaStream_t st,
-                         int order, void* scratch, void* vol_t) {
+                         int order, void* scratch, void* vol_t, void* plans) {
   void* x = vol_t;  // z-fastest accumulator, transposed into x_out at the end
   const long long h = g.n_x / 2;
   const long long n_orb = order == 8 ? h * (h + 1) / 2 : h * h;
@@ -1514,14 +1605,21 @@ cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const i
             (const float*)y, base + k0, order, g.n_angles, g.n_det_y, g.n_det_z, (float*)scratch);
       count_launch();
     }
+    // the fp64 chunking is the smaller one: the plan scratch holds it
+    void* pl = (n_base > 0) ? plans : nullptr;
+    {
+      const cudaError_t e = plan_pass(g, cs + k0, nk > 0 ? nk : 0, pl, status, st);
+      if (e != cudaSuccess) return e;
+    }
 #define CTSM_LAUNCH(T, G)                                                                      \
   do {                                                                                         \
     if (tr)                                                                                    \
       bwd3d_sym_kernel<T, G, true><<<blocks, bwd3_warps<T>() * 32, 0, st>>>(                           \
-          g, cs + k0, base + k0, nk, (const T*)scratch, (T*)x, k0 > 0, status);                \
+          g, cs + k0, base + k0, nk, (const T*)scratch, (T*)x, k0 > 0, status,                 \
+          (const FastPlan*)pl);                                                                \
     else                                                                                       \
       bwd3d_sym_kernel<T, G, false><<<blocks, bwd3_warps<T>() * 32, 0, st>>>(                          \
-          g, cs + k0, base + k0, nk, (const T*)y, (T*)x, k0 > 0, status);                      \
+          g, cs + k0, base + k0, nk, (const T*)y, (T*)x, k0 > 0, status, (const FastPlan*)pl); \
   } while (0)
     if (dtype == CTSM_F64) {
       if (order == 8) CTSM_LAUNCH(double, 8); else CTSM_LAUNCH(double, 4);
