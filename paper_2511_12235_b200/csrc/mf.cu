@@ -852,9 +852,14 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
       const int ne = full ? G : 4;
       __syncwarp();
       if (lane < G) sab[warp][lane] = (long long)d4_angle(g.n_angles, i, lane) * rpa;
+#ifdef CTSM_INKERNEL_PLAN
       const bool ok = plans ? load_plan(plans, (long long)kk * nxy + col, sh[warp], sp[warp], lane)
                             : fast::plan_column(g, a.C, a.S, ix, iy, status, sh[warp], sp[warp],
                                                 lane);
+#else
+      (void)a;
+      const bool ok = load_plan(plans, (long long)kk * nxy + col, sh[warp], sp[warp], lane);
+#endif
       __syncwarp();
       if (!ok) continue;
       const fast::GroupTable* TB = table3d(sh[warp], sp[warp], CTSM_TABLE_PTR, lane);
@@ -1068,10 +1073,17 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
         int cx, cy;
         d4_pixel(n, ix0, iy0, hm, cx, cy);
         __syncwarp();
+#ifdef CTSM_INKERNEL_PLAN
         const bool ok =
             plans ? load_plan(plans, (long long)kk * ((long long)n * g.n_y) + (long long)cy * n + cx,
                               sh[warp], sp[warp], lane)
                   : fast::plan_column(g, a.C, a.S, cx, cy, status, sh[warp], sp[warp], lane);
+#else
+        (void)a;
+        const bool ok = load_plan(
+            plans, (long long)kk * ((long long)n * g.n_y) + (long long)cy * n + cx, sh[warp],
+            sp[warp], lane);
+#endif
         __syncwarp();
         if (!ok) continue;
         const fast::GroupTable* TB = table3d(sh[warp], sp[warp], CTSM_TABLE_PTR, lane);
@@ -1455,8 +1467,11 @@ __global__ void fwd3d_uninterleave(const float* __restrict__ yt, const int* __re
 // Bytes of the plan scratch of one launch of the symmetric 3D kernels (the
 // fp32 chunking is the larger one).
 size_t mf3d_plan_bytes(const DevGeom& g, int order) {
+#ifdef CTSM_INKERNEL_PLAN
   static const bool off = getenv("CTSM_NO_PLAN_PASS") != nullptr;
-  if (off || (g.n_z == 1 && g.n_det_z == 1)) return 0;
+  if (off) return 0;
+#endif
+  if (g.n_z == 1 && g.n_det_z == 1) return 0;
   return (size_t)g.n_x * g.n_y * (size_t)sym3d_chunk(g, order, 4) * sizeof(FastPlan);
 }
 
