@@ -874,7 +874,7 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
       // point at the flush), fp64 volumes in fp64
       using PT = T;
       const float scale_f = (float)scale;
-      long long pr = -1;
+      int pr = -1;
       PT pv[G], pm[G];  // run sums of the lower voxel and of its z mirror
       int py = 0, pz = 0;
 #pragma unroll
@@ -886,7 +886,8 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
           const int rz = side == 0 ? pz : g.n_det_z - 1 - pz;  // mirror row -1-mz
           if constexpr (FA) {
             // interleaved row (my, mz) of slot kk: all G images in one vector
-            float* dst = yt + (((long long)kk * ndy + py) * g.n_det_z + rz) * G;
+            // (the launch's scratch holds < 2^31 floats: sym3d_chunk bounds it)
+            float* dst = yt + (unsigned)(((kk * ndy + py) * g.n_det_z + rz) * G);
 #pragma unroll
             for (int c = 0; c < G / 4; ++c)
               asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * c),
@@ -911,9 +912,10 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
           }
         }
       };
+      unsigned nw = 0;  // weights of this (column, angle); updates = nw * images * sides
       fast::chunk_weights(g, sh[warp], sp[warp], z0, z1, [&](int iz, int my, int mz, double w) {
-        cnt += zmir ? 2 * ne : ne;
-        const long long r = (long long)(mz + hz) * ndy + (my + hy);
+        ++nw;
+        const int r = (mz + hz) * ndy + (my + hy);  // < rows_per_angle < 2^31
         if (r != pr) {
           if (pr >= 0) flush();
           pr = r;
@@ -937,13 +939,17 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
               const double2 q = reinterpret_cast<const double2*>(xv)[c * 32];
               v[0] = q.x; v[1] = q.y;
             }
+            // FA: the interleaved scratch rows carry all G image slots and
+            // fwd3d_uninterleave reads only the first 4 of a self-symmetric
+            // base angle, so the other 4 may accumulate (unused) values
 #pragma unroll
             for (int u = 0; u < V; ++u)
-              if (c * V + u < ne) acc[c * V + u] += wp * v[u];
+              if (FA || c * V + u < ne) acc[c * V + u] += wp * v[u];
           }
         }
       }, TB, CTSM_BATCH_PTR, lane);
       if (pr >= 0) flush();
+      cnt += nw * (unsigned)(zmir ? 2 * ne : ne);
     }
   }
   count_updates(n_upd, cnt);
@@ -1100,16 +1106,28 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
 #else
 #define CTSM_LDY(p) ((AccT)__ldg(p))
 #endif
+        // consecutive weights of a lane often hit the same detector row (the
+        // row shared by voxels iz and iz + 1): its image vectors are kept in
+        // registers instead of being gathered again
+        int prow = -1;
+        T pv0[G], pv1[G];
         auto gather = [&](int t, int my, int mz, double w) {
           const AccT wa = (AccT)w;  // fp32 volumes: FFMA in fp32
           if (TR) {
             // the G image values of (my, mz): one contiguous vector; with
             // the z mirror also those of row -1-mz for voxel n_z-1-iz
-            const T* rowp = yb[0] + (long long)(my + hy) * g.n_det_z * G;
+            const int rowi = (my + hy) * g.n_det_z + (mz + hz);
+            if (rowi != prow) {
+              const T* rowp = yb[0] + (long long)(my + hy) * g.n_det_z * G;
+              load_vec<T, G>(rowp + (long long)(mz + hz) * G, pv0);
+              if (zmir) load_vec<T, G>(rowp + (long long)(g.n_det_z - 1 - (mz + hz)) * G, pv1);
+              prow = rowi;
+            }
 #pragma unroll 1
             for (int side = 0; side < (zmir ? 2 : 1); ++side) {
               T v[G];
-              load_vec<T, G>(rowp + (long long)(side == 0 ? mz + hz : g.n_det_z - 1 - (mz + hz)) * G, v);
+#pragma unroll
+              for (int e = 0; e < G; ++e) v[e] = side == 0 ? pv0[e] : pv1[e];
               // the G slots are distinct (pk is a permutation): all loads,
               // then all adds, then all stores -- as one read-modify-write per
               // slot the compiler must assume aliasing and serialise them
