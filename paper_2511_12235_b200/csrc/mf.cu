@@ -879,11 +879,9 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
       int py = 0, pz = 0;
 #pragma unroll
       for (int e = 0; e < G; ++e) pv[e] = pm[e] = (PT)0;
-      auto flush = [&]() {
-#pragma unroll 1
-        for (int side = 0; side < (zmir ? 2 : 1); ++side) {
-          const PT* q = side == 0 ? pv : pm;
-          const int rz = side == 0 ? pz : g.n_det_z - 1 - pz;  // mirror row -1-mz
+      // one call site per side (no loop over a register-array selector)
+      auto flush_side = [&](const PT* q, const int rz) {
+        {
           if constexpr (FA) {
             // interleaved row (my, mz) of slot kk: all G images in one vector
             // (the launch's scratch holds < 2^31 floats: sym3d_chunk bounds it)
@@ -912,6 +910,10 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
           }
         }
       };
+      auto flush = [&]() {
+        flush_side(pv, pz);
+        if (zmir) flush_side(pm, g.n_det_z - 1 - pz);  // mirror row -1-mz
+      };
       unsigned nw = 0;  // weights of this (column, angle); updates = nw * images * sides
       fast::chunk_weights(g, sh[warp], sp[warp], z0, z1, [&](int iz, int my, int mz, double w) {
         ++nw;
@@ -925,10 +927,8 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
           for (int e = 0; e < G; ++e) pv[e] = pm[e] = (PT)0;
         }
         const PT wp = (PT)w;
-#pragma unroll 1
-        for (int side = 0; side < (zmir ? 2 : 1); ++side) {
-          const T* xv = xsm + xidx((side == 0 ? 0 : kMF) + iz - z0, 0, lane);
-          PT* acc = side == 0 ? pv : pm;
+        auto acc_side = [&](PT* acc, const int slot) {
+          const T* xv = xsm + xidx(slot, 0, lane);
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
             T v[V];
@@ -946,7 +946,9 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
             for (int u = 0; u < V; ++u)
               if (FA || c * V + u < ne) acc[c * V + u] += wp * v[u];
           }
-        }
+        };
+        acc_side(pv, iz - z0);
+        if (zmir) acc_side(pm, kMF + iz - z0);
       }, TB, CTSM_BATCH_PTR, lane);
       if (pr >= 0) flush();
       cnt += nw * (unsigned)(zmir ? 2 * ne : ne);
@@ -1123,15 +1125,12 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
               if (zmir) load_vec<T, G>(rowp + (long long)(g.n_det_z - 1 - (mz + hz)) * G, pv1);
               prow = rowi;
             }
-#pragma unroll 1
-            for (int side = 0; side < (zmir ? 2 : 1); ++side) {
-              T v[G];
-#pragma unroll
-              for (int e = 0; e < G; ++e) v[e] = side == 0 ? pv0[e] : pv1[e];
+            // one call site per side (no loop over a register-array selector)
+            auto add_side = [&](const T* v, const int slot) {
               // the G slots are distinct (pk is a permutation): all loads,
               // then all adds, then all stores -- as one read-modify-write per
               // slot the compiler must assume aliasing and serialise them
-              AccT* base = &sacc[warp][0][side == 0 ? t : kM + t][lane];
+              AccT* base = &sacc[warp][0][slot][lane];
               constexpr int kSlot = kZcS * 32;
               AccT cur[G];
 #pragma unroll
@@ -1141,7 +1140,9 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
                 if (e < 4 || full) cur[e] += wa * (AccT)v[e];
 #pragma unroll
               for (int e = 0; e < G; ++e) base[((pk >> (3 * e)) & 7) * kSlot] = cur[e];
-            }
+            };
+            add_side(pv0, t);
+            if (zmir) add_side(pv1, kM + t);
           } else {
             const long long r = (long long)(mz + hz) * g.n_det_y + (my + hy);
 #pragma unroll
