@@ -1081,8 +1081,9 @@ static int fwd_impl(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int begin,
   const double B = mx * row_sum_bound(g) * 1.05;
   const double scale = B > 0.0 ? std::ldexp(1.0, 61) / B : 1.0;
   CT_CUDA(cudaMemsetAsync(ctx->n_upd, 0, sizeof(unsigned long long), st));
+  CT_TRY(ensure(ctx, ctx->mfplans, mf3d_plan_bytes_general(d)));
   CT_CUDA(fwd_mf(d, dtype, (const AngleCS*)ctx->cs.p, begin, step, n_sel, x, acc, scale,
-                 ctx->n_upd, ctx->status, st));
+                 ctx->n_upd, ctx->status, st, ctx->mfplans.p));
   CT_CUDA(fixed_to_float_rows(d, dtype, begin, step, n_sel, acc, scale, y, st));
   CT_CUDA(cudaMemcpyAsync(ctx->h_upd, ctx->n_upd, sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, st));
@@ -1104,8 +1105,9 @@ static int bwd_impl(ctsm_ctx* ctx, const ctsm_geometry* g, int dtype, int begin,
   CT_TRY(prepare_cs(ctx, d, begin, step, n_sel, st));
   const int nc = bwd_chunks(d, n_sel);
   if (nc > 1) CT_TRY(ensure(ctx, ctx->part, (size_t)nc * g->n_x * g->n_y * sizeof(double)));
+  CT_TRY(ensure(ctx, ctx->mfplans, mf3d_plan_bytes_general(d)));
   CT_CUDA(bwd_mf(d, dtype, (const AngleCS*)ctx->cs.p, begin, step, n_sel, y, x,
-                 (double*)ctx->part.p, nc, ctx->status, st));
+                 (double*)ctx->part.p, nc, ctx->status, st, ctx->mfplans.p));
   return 0;
 }
 

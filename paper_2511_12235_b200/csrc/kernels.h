@@ -187,15 +187,17 @@ cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const i
 // the (column, base angle) plans of a launch are computed one per thread by a
 // plan pass instead of by every projection warp.
 size_t mf3d_plan_bytes(const DevGeom& g, int order);
+size_t mf3d_plan_bytes_general(const DevGeom& g);  // the per-angle kernels (fwd_mf / bwd_mf)
 cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
                    int angle_step, int n_sel, const void* x, unsigned long long* yacc,
-                   double scale, unsigned long long* n_upd, int* status, cudaStream_t st);
+                   double scale, unsigned long long* n_upd, int* status, cudaStream_t st,
+                   void* plans = nullptr);
 // Backward uses n_chunks angle chunks (bwd_chunks) with a partial-sum buffer
 // part of n_chunks * n_x * n_y doubles when n_chunks > 1 (2D only).
 int bwd_chunks(const DevGeom& g, int n_sel);
 cudaError_t bwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
                    int angle_step, int n_sel, const void* y, void* x, double* part, int n_chunks,
-                   int* status, cudaStream_t st);
+                   int* status, cudaStream_t st, void* plans = nullptr);
 // y rows of the shard <- acc / scale (and acc rows zeroed for reuse)
 cudaError_t fixed_to_float_rows(const DevGeom& g, int dtype, int angle_begin, int angle_step,
                                 int n_sel, unsigned long long* acc, double scale, void* y,

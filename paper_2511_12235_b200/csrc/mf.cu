@@ -208,13 +208,83 @@ __device__ __forceinline__ const fast::GroupTable* table3d(const fast::ColumnHea
 constexpr int kWarps3 = CTSM_KW3;
 constexpr int kZcMax = 16;  // voxels per lane per z-block (z-block = 512 voxels)
 
+// ---- plan pass of the 3D kernels --------------------------------
+// Planning a (column, base angle) -- the xy sweep, the pieces' G-independent
+// coefficients, the group short cuts -- does not depend on z. Inside the
+// projection kernels it was done by the whole warp (every lane computing the
+// same sweep), 26 % of a C3 projection. plan3d_fast_kernel plans all (column,
+// base angle) pairs of a launch with ONE THREAD each (full lanes instead of 32
+// redundant copies) into global memory; the projection kernels then load the
+// plan (coalesced, ~1-3 KB) into shared memory instead of computing it.
+struct FastPlan {
+  fast::ColumnHead H;
+  fast::PieceCoef P[fast::kMaxPieces];
+};
+static_assert(sizeof(fast::ColumnHead) % 32 == 0 && sizeof(fast::PieceCoef) % 32 == 0,
+              "plans are stored as 32-byte vectors and loaded as 16-byte vectors");
+
+__global__ void __launch_bounds__(128) plan3d_fast_kernel(DevGeom g, const AngleCS* __restrict__ cs,
+                                                          int n_base, FastPlan* __restrict__ plans,
+                                                          int* status) {
+  const long long nxy = (long long)g.n_x * g.n_y;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nxy * n_base) return;
+  const int kk = (int)(t / nxy);
+  const long long col = t - (long long)kk * nxy;
+  FastPlan* out = plans + t;
+  // the head is assembled in thread-local memory (small fields written all
+  // over it) and leaves as 32-byte stores; the pieces are stored from
+  // registers by plan_column
+  fast::ColumnHead Hl;
+  fast::plan_column<true>(g, cs[kk].C, cs[kk].S, (int)(col % g.n_x), (int)(col / g.n_x), status,
+                          Hl, out->P, 0);
+  const double* src = reinterpret_cast<const double*>(&Hl);
+  double* dst = reinterpret_cast<double*>(&out->H);
+#pragma unroll 1
+  for (int i = 0; i < (int)(sizeof(fast::ColumnHead) / 8); i += 4)
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst + i), "d"(src[i]),
+                 "d"(src[i + 1]), "d"(src[i + 2]), "d"(src[i + 3])
+                 : "memory");
+}
+
+// Loads the plan of (column, slot kk) into the warp's shared head / pieces.
+// Returns false for a column without work (failed sweep or no cell group).
+__device__ __forceinline__ bool load_plan(const FastPlan* __restrict__ plans, long long idx,
+                                          fast::ColumnHead& H, fast::PieceCoef* P, int lane) {
+  const FastPlan* src = plans + idx;
+  {
+    const double2* s2 = reinterpret_cast<const double2*>(&src->H);
+    double2* d2 = reinterpret_cast<double2*>(&H);
+    for (int i = lane; i < (int)(sizeof(fast::ColumnHead) / 16); i += 32) d2[i] = __ldg(&s2[i]);
+  }
+  __syncwarp();
+  const int np = H.np;
+  {
+    const double2* s2 = reinterpret_cast<const double2*>(src->P);
+    double2* d2 = reinterpret_cast<double2*>(P);
+    for (int i = lane; i < np * (int)(sizeof(fast::PieceCoef) / 16); i += 32) d2[i] = __ldg(&s2[i]);
+  }
+  return H.ng > 0;
+}
+
+static cudaError_t plan_pass(const DevGeom& g, const AngleCS* cs, int nk, void* plans, int* status,
+                             cudaStream_t st) {
+  if (!plans) return cudaSuccess;
+  const long long n = (long long)g.n_x * g.n_y * nk;
+  plan3d_fast_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(g, cs, nk, (FastPlan*)plans,
+                                                                  status);
+  count_launch();
+  return cudaGetLastError();
+}
+
 template <typename T, bool kFwd>
 __global__ void __launch_bounds__(kWarps3 * 32, 4) proj3d_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, int angle_begin, int angle_step, int n_sel,
     const T* __restrict__ in, T* __restrict__ xout, unsigned long long* __restrict__ yacc,
-    double scale, unsigned long long* n_upd, int accumulate, int* status) {
-  __shared__ fast::ColumnHead sh[kWarps3];
-  __shared__ fast::PieceCoef sp[kWarps3][fast::kMaxPieces];
+    double scale, unsigned long long* n_upd, int accumulate, int* status,
+    const FastPlan* __restrict__ plans = nullptr) {
+  __shared__ __align__(32) fast::ColumnHead sh[kWarps3];
+  __shared__ __align__(32) fast::PieceCoef sp[kWarps3][fast::kMaxPieces];
   __shared__ double sacc[kWarps3][kZcMax][32];
   CTSM_TABLE_DECL(kWarps3);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -236,7 +306,9 @@ __global__ void __launch_bounds__(kWarps3 * 32, 4) proj3d_kernel(
       const int ip = angle_begin + k * angle_step;
       const AngleCS a = cs[k];
       __syncwarp();
-      const bool ok = fast::plan_column(g, a.C, a.S, ix, iy, status, sh[warp], sp[warp], lane);
+      const bool ok = plans ? load_plan(plans, (long long)k * nxy + col, sh[warp], sp[warp], lane)
+                            : fast::plan_column(g, a.C, a.S, ix, iy, status, sh[warp], sp[warp],
+                                                lane);
       __syncwarp();
       if (!ok) continue;
       const fast::ColumnHead& H = sh[warp];
@@ -705,65 +777,6 @@ __global__ void __launch_bounds__(128, CTSM_D8B_MINB) bwd2d_d8_kernel(
 // per z-block ([image][slot][lane], conflict-free) and reused for all base
 // angles: the per-weight reads are shared-memory hits instead of G scattered
 // global loads.
-// ---- plan pass of the symmetric 3D kernels --------------------------------
-// Planning a (column, base angle) -- the xy sweep, the pieces' G-independent
-// coefficients, the group short cuts -- does not depend on z. Inside the
-// projection kernels it was done by the whole warp (every lane computing the
-// same sweep), 26 % of a C3 projection. plan3d_fast_kernel plans all (column,
-// base angle) pairs of a launch with ONE THREAD each (full lanes instead of 32
-// redundant copies) into global memory; the projection kernels then load the
-// plan (coalesced, ~1-3 KB) into shared memory instead of computing it.
-struct FastPlan {
-  fast::ColumnHead H;
-  fast::PieceCoef P[fast::kMaxPieces];
-};
-static_assert(sizeof(fast::ColumnHead) % 32 == 0 && sizeof(fast::PieceCoef) % 32 == 0,
-              "plans are stored as 32-byte vectors and loaded as 16-byte vectors");
-
-__global__ void __launch_bounds__(128) plan3d_fast_kernel(DevGeom g, const AngleCS* __restrict__ cs,
-                                                          int n_base, FastPlan* __restrict__ plans,
-                                                          int* status) {
-  const long long nxy = (long long)g.n_x * g.n_y;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nxy * n_base) return;
-  const int kk = (int)(t / nxy);
-  const long long col = t - (long long)kk * nxy;
-  FastPlan* out = plans + t;
-  // the head is assembled in thread-local memory (small fields written all
-  // over it) and leaves as 32-byte stores; the pieces are stored from
-  // registers by plan_column
-  fast::ColumnHead Hl;
-  fast::plan_column<true>(g, cs[kk].C, cs[kk].S, (int)(col % g.n_x), (int)(col / g.n_x), status,
-                          Hl, out->P, 0);
-  const double* src = reinterpret_cast<const double*>(&Hl);
-  double* dst = reinterpret_cast<double*>(&out->H);
-#pragma unroll 1
-  for (int i = 0; i < (int)(sizeof(fast::ColumnHead) / 8); i += 4)
-    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst + i), "d"(src[i]),
-                 "d"(src[i + 1]), "d"(src[i + 2]), "d"(src[i + 3])
-                 : "memory");
-}
-
-// Loads the plan of (column, slot kk) into the warp's shared head / pieces.
-// Returns false for a column without work (failed sweep or no cell group).
-__device__ __forceinline__ bool load_plan(const FastPlan* __restrict__ plans, long long idx,
-                                          fast::ColumnHead& H, fast::PieceCoef* P, int lane) {
-  const FastPlan* src = plans + idx;
-  {
-    const double2* s2 = reinterpret_cast<const double2*>(&src->H);
-    double2* d2 = reinterpret_cast<double2*>(&H);
-    for (int i = lane; i < (int)(sizeof(fast::ColumnHead) / 16); i += 32) d2[i] = __ldg(&s2[i]);
-  }
-  __syncwarp();
-  const int np = H.np;
-  {
-    const double2* s2 = reinterpret_cast<const double2*>(src->P);
-    double2* d2 = reinterpret_cast<double2*>(P);
-    for (int i = lane; i < np * (int)(sizeof(fast::PieceCoef) / 16); i += 32) d2[i] = __ldg(&s2[i]);
-  }
-  return H.ng > 0;
-}
-
 #ifndef CTSM_KZCF
 #define CTSM_KZCF 8
 #endif
@@ -1288,13 +1301,18 @@ static dim3 tile_grid(const DevGeom& g, unsigned ydim, int tx = kTx) {
 // Angles per launch of the general 3D kernel: the rows of one launch's angles
 // should stay L2-resident (~64 MB of the 126 MB L2), see sym3d_chunk below.
 static int gen3d_chunk(const DevGeom& g, size_t elem_bytes) {
-  const int c = (int)((64.0 * (1 << 20)) / ((double)g.rows_per_angle * (double)elem_bytes));
+  int c = (int)((64.0 * (1 << 20)) / ((double)g.rows_per_angle * (double)elem_bytes));
+  // ... and the launch's plans (one per column and angle) within ~2 GB
+  const double plan_angle = (double)g.n_x * g.n_y * (double)sizeof(FastPlan);
+  const int cp = (int)((2048.0 * (1 << 20)) / plan_angle);
+  if (c > cp) c = cp;
   return c < 1 ? 1 : c;
 }
 
 cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
                    int angle_step, int n_sel, const void* x, unsigned long long* yacc,
-                   double scale, unsigned long long* n_upd, int* status, cudaStream_t st) {
+                   double scale, unsigned long long* n_upd, int* status, cudaStream_t st,
+                   void* plans) {
   if (n_sel <= 0) return cudaSuccess;
   const bool two_d = (g.n_z == 1 && g.n_det_z == 1);
   if (two_d) {
@@ -1313,14 +1331,18 @@ cudaError_t fwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_beg
     for (int k0 = 0; k0 < n_sel; k0 += chunk) {
       const int nk = n_sel - k0 < chunk ? n_sel - k0 : chunk;
       const int a0 = angle_begin + k0 * angle_step;
+      {
+        const cudaError_t e = plan_pass(g, cs + k0, nk, plans, status, st);
+        if (e != cudaSuccess) return e;
+      }
       if (dtype == CTSM_F64)
         proj3d_kernel<double, true><<<blocks, kWarps3 * 32, 0, st>>>(
             g, cs + k0, a0, angle_step, nk, (const double*)x, nullptr, yacc, scale, n_upd, 0,
-            status);
+            status, (const FastPlan*)plans);
       else
         proj3d_kernel<float, true><<<blocks, kWarps3 * 32, 0, st>>>(
             g, cs + k0, a0, angle_step, nk, (const float*)x, nullptr, yacc, scale, n_upd, 0,
-            status);
+            status, (const FastPlan*)plans);
       count_launch();
     }
   }
@@ -1340,7 +1362,7 @@ int bwd_chunks(const DevGeom& g, int n_sel) {
 
 cudaError_t bwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_begin,
                    int angle_step, int n_sel, const void* y, void* x, double* part, int n_chunks,
-                   int* status, cudaStream_t st) {
+                   int* status, cudaStream_t st, void* plans) {
   const bool two_d = (g.n_z == 1 && g.n_det_z == 1);
   if (two_d) {
     const int chunk = (n_sel + n_chunks - 1) / (n_chunks > 0 ? n_chunks : 1);
@@ -1370,14 +1392,19 @@ cudaError_t bwd_mf(const DevGeom& g, int dtype, const AngleCS* cs, int angle_beg
     for (int k0 = 0; k0 < (n_sel > 0 ? n_sel : 1); k0 += chunk) {
       const int nk = n_sel - k0 < chunk ? n_sel - k0 : chunk;
       const int a0 = angle_begin + k0 * angle_step;
+      void* pl = n_sel > 0 ? plans : nullptr;
+      {
+        const cudaError_t e = plan_pass(g, cs + k0, nk > 0 ? nk : 0, pl, status, st);
+        if (e != cudaSuccess) return e;
+      }
       if (dtype == CTSM_F64)
         proj3d_kernel<double, false><<<blocks, kWarps3 * 32, 0, st>>>(
             g, cs + k0, a0, angle_step, nk, (const double*)y, (double*)x, nullptr, 1.0, nullptr,
-            k0 > 0, status);
+            k0 > 0, status, (const FastPlan*)pl);
       else
         proj3d_kernel<float, false><<<blocks, kWarps3 * 32, 0, st>>>(
             g, cs + k0, a0, angle_step, nk, (const float*)y, (float*)x, nullptr, 1.0, nullptr,
-            k0 > 0, status);
+            k0 > 0, status, (const FastPlan*)pl);
       count_launch();
     }
   }
@@ -1494,14 +1521,10 @@ size_t mf3d_plan_bytes(const DevGeom& g, int order) {
   return (size_t)g.n_x * g.n_y * (size_t)sym3d_chunk(g, order, 4) * sizeof(FastPlan);
 }
 
-static cudaError_t plan_pass(const DevGeom& g, const AngleCS* cs, int nk, void* plans, int* status,
-                             cudaStream_t st) {
-  if (!plans) return cudaSuccess;
-  const long long n = (long long)g.n_x * g.n_y * nk;
-  plan3d_fast_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(g, cs, nk, (FastPlan*)plans,
-                                                                  status);
-  count_launch();
-  return cudaGetLastError();
+// ... and of one launch of the general (per-angle) 3D kernel.
+size_t mf3d_plan_bytes_general(const DevGeom& g) {
+  if (g.n_z == 1 && g.n_det_z == 1) return 0;
+  return (size_t)g.n_x * g.n_y * (size_t)gen3d_chunk(g, 4) * sizeof(FastPlan);
 }
 
 size_t fwd3d_f32_scratch_elems(const DevGeom& g, int order) {

@@ -228,6 +228,7 @@ int ctsm_multi_create(const int* devices, int n, ctsm_multi** out) {
 int ctsm_multi_destroy(ctsm_multi* m) {
   if (!m) return 0;
   for (DevSlot& d : m->dev) {
+    if (!d.ctx) continue;  // slot never came up (e.g. no such device): nothing to release
     cudaSetDevice(d.device);
     if (d.comm && m->nccl.CommDestroy) m->nccl.CommDestroy(d.comm);
     void* bufs[] = {d.x, d.y, d.r, d.c, d.bp};
