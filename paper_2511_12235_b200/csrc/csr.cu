@@ -1,13 +1,15 @@
-#include <climits>
-#include <cstdlib>
 // csr.cu -- K1/K2 consistent system-matrix CSR emission (bit-exact) and the
 // K3/K4 CSR appliers. Compiled with -fmad=false (see exact.cuh).
 //
-// Emission (build_system_matrix, projector.cpp:144-201) runs in two passes
-// over (voxel column, angle) work items, both evaluating exactly the same
-// weights: pass 1 counts entries per row, a scan yields row_start, pass 2
-// scatters (col, w) into per-row slots, and a per-row sort restores the
-// reference's strictly ascending column order (projector.cpp:100-102).
+// Emission (build_system_matrix, projector.cpp:144-201) either evaluates each
+// weight once into records that are then grouped by row (ctsm_csr_build), or
+// runs twice over the same weights (the count / fill protocol: pass 1 counts
+// entries per row, a scan yields row_start, pass 2 writes row-grouped
+// entries); in both cases a per-row radix sort restores the reference's
+// strictly ascending column order (projector.cpp:100-102).
+#include <climits>
+#include <cstdlib>
+
 #include "exact.cuh"
 #include "csr3d.cuh"
 #include "kernels.h"
@@ -245,118 +247,6 @@ cudaError_t exclusive_scan_u32_u64(const unsigned* counts, uint64_t n, uint64_t*
   scan_down_kernel<<<(unsigned)tiles, kScanBlock, 0, st>>>(counts, n, ts, row_start, base, base_dev,
                                                            local_out);
   count_launch(3);
-  return cudaGetLastError();
-}
-
-// ---- per-row sort by column ---------------------------------------------
-namespace {
-constexpr int kSortWarps = 2;
-constexpr int kWarpCap = 1024;  // rows up to this length are sorted by one warp
-
-__device__ __forceinline__ void bitonic_warp(unsigned long long* key, int n2) {
-  const int lane = threadIdx.x & 31;
-  for (int k = 2; k <= n2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = lane; i < n2; i += 32) {
-        const int p = i ^ j;
-        if (p > i) {
-          const unsigned long long a = key[i], b = key[p];
-          const bool up = ((i & k) == 0);
-          if ((a > b) == up) {
-            key[i] = b;
-            key[p] = a;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kSortWarps * 32) sort_rows_warp(uint64_t n_rows,
-                                                                  const uint64_t* __restrict__ rs,
-                                                                  uint32_t* col, double* val,
-                                                                  unsigned* long_rows,
-                                                                  unsigned* n_long) {
-  __shared__ unsigned long long skey[kSortWarps][kWarpCap];
-  __shared__ double sval[kSortWarps][kWarpCap];
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t warps_total = (uint64_t)gridDim.x * kSortWarps;
-  for (uint64_t r = (uint64_t)blockIdx.x * kSortWarps + wid; r < n_rows; r += warps_total) {
-    const uint64_t b = rs[r], e = rs[r + 1];
-    const int n = (int)(e - b);
-    if (n <= 1) continue;
-    if (n > kWarpCap) {
-      if (lane == 0) long_rows[atomicAdd(n_long, 1u)] = (unsigned)r;
-      continue;
-    }
-    // already sorted? (cheap check, common for rows from few columns)
-    bool sorted = true;
-    for (int i = lane; i + 1 < n; i += 32)
-      if (col[b + i] > col[b + i + 1]) sorted = false;
-    if (__all_sync(0xffffffffu, sorted)) continue;
-    int n2 = 1;
-    while (n2 < n) n2 <<= 1;
-    for (int i = lane; i < n2; i += 32) {
-      if (i < n) {
-        skey[wid][i] = ((unsigned long long)col[b + i] << 32) | (unsigned)i;
-        sval[wid][i] = val[b + i];
-      } else {
-        skey[wid][i] = ~0ull;
-      }
-    }
-    __syncwarp();
-    bitonic_warp(skey[wid], n2);
-    for (int i = lane; i < n; i += 32) {
-      const unsigned long long kk = skey[wid][i];
-      col[b + i] = (uint32_t)(kk >> 32);
-      val[b + i] = sval[wid][kk & 0xffffffffu];
-    }
-    __syncwarp();
-  }
-}
-
-// Long rows: one block each, shell-sort in global memory by a single thread
-// (rare; keeps correctness for any geometry).
-__global__ void sort_rows_long(const unsigned* long_rows, const unsigned* n_long,
-                               const uint64_t* __restrict__ rs, uint32_t* col, double* val) {
-  const unsigned nl = *n_long;
-  for (unsigned q = blockIdx.x; q < nl; q += gridDim.x) {
-    if (threadIdx.x != 0) continue;
-    const uint64_t r = long_rows[q];
-    const uint64_t b = rs[r];
-    const long long n = (long long)(rs[r + 1] - b);
-    long long gap = 1;
-    while (gap < n / 3) gap = 3 * gap + 1;
-    for (; gap > 0; gap /= 3)
-      for (long long i = gap; i < n; ++i) {
-        const uint32_t c = col[b + i];
-        const double v = val[b + i];
-        long long j = i;
-        while (j >= gap && col[b + j - gap] > c) {
-          col[b + j] = col[b + j - gap];
-          val[b + j] = val[b + j - gap];
-          j -= gap;
-        }
-        col[b + j] = c;
-        val[b + j] = v;
-      }
-  }
-}
-}  // namespace
-
-cudaError_t csr_sort_rows(uint64_t n_rows, const uint64_t* row_start, uint32_t* col,
-                          double* val, unsigned* long_rows, unsigned* n_long, int* status,
-                          cudaStream_t st) {
-  (void)status;
-  cudaError_t e = cudaMemsetAsync(n_long, 0, sizeof(unsigned), st);
-  if (e != cudaSuccess) return e;
-  if (n_rows == 0) return cudaSuccess;
-  const uint64_t blocks = (n_rows + kSortWarps - 1) / kSortWarps;
-  const unsigned grid = (unsigned)(blocks < 148ull * 16 ? blocks : 148ull * 16);
-  sort_rows_warp<<<grid, kSortWarps * 32, 0, st>>>(n_rows, row_start, col, val, long_rows, n_long);
-  sort_rows_long<<<148, 32, 0, st>>>(long_rows, n_long, row_start, col, val);
-  count_launch(2);
   return cudaGetLastError();
 }
 

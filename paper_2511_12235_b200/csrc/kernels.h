@@ -80,10 +80,6 @@ cudaError_t exclusive_scan_u32_u64(const unsigned* counts, uint64_t n, uint64_t*
                                    void* scratch, cudaStream_t st, uint64_t base = 0,
                                    const uint64_t* base_dev = nullptr,
                                    unsigned* local_out = nullptr);
-// Sort each row's entries by column (in place).
-cudaError_t csr_sort_rows(uint64_t n_rows, const uint64_t* row_start, uint32_t* col,
-                          double* val, unsigned* long_rows, unsigned* n_long, int* status,
-                          cudaStream_t st);
 cudaError_t spmv_csr(uint64_t n_rows, const uint64_t* row_start, const uint32_t* col,
                      const double* val, const double* x, double* y, int* status, cudaStream_t st);
 cudaError_t colsum_abs(uint64_t n_rows, const uint64_t* row_start, const uint32_t* col,

@@ -102,6 +102,26 @@ def test_csr_two_pass_equals_single_evaluation(name):
                               y.view(np.uint64) if y.dtype == np.float64 else y)
 
 
+def test_csr_long_rows_block_sort(oracle_cr):
+    """C1's grid (512^2 pixels) with a 3x coarser detector: rows hold ~2,400
+    entries, beyond the warp radix sort's 1,024, so they take the block-wide
+    sort. Three angle blocks (axis-aligned, oblique, diagonal), bit-identical
+    to the oracle."""
+    g = CONFIGS["c1"].with_(d_y=1.8, n_det_y=344)
+    for ip in (0, 37, 90):
+        w = build_system_matrix(g, angle_range=(ip, ip + 1), memory_budget_bytes=1 << 40)
+        ref = entries_to_csr(g, *oracle_cr.angle_block_entries(g, ip, threads=NTHREADS))
+        rs, col, val = w.to_host()
+        assert int(np.max(np.diff(rs.astype(np.int64)))) > 1024
+        assert np.array_equal(rs, ref[0])
+        assert np.array_equal(col, ref[1])
+        assert np.array_equal(val.view(np.uint64), ref[2].view(np.uint64))
+        w2 = build_system_matrix(g, angle_range=(ip, ip + 1), memory_budget_bytes=1 << 40,
+                                 two_pass=True)
+        assert torch.equal(w2.col, w.col) and torch.equal(w2.val.view(torch.int64),
+                                                          w.val.view(torch.int64))
+
+
 def test_csr_build_capacity_protocol(oracle_cr):
     """ctsm_csr_build with too small arrays reports the needed entry count
     and leaves the caller to retry; several angle chunks (C2, 9 angles: the
