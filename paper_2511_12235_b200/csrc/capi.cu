@@ -78,6 +78,11 @@ struct ctsm_ctx {
       sv_q, sv_v, sv_part, sv_scal, tmp_a, tmp_b, tmp_c, tmp_d,
       tmp_e, tmp_f, lraw_start, lraw_col, lraw_val, lacc, bwd_t, vol_t, plans, rec, grp,
       cursor, plans2, rec2, grp2, angles2, counts2, longrows2, mfplans;
+  // key of the base-angle tables currently in `base` / `cs` (upload_base)
+  bool base_valid = false;
+  std::vector<int> base_cached;
+  int base_n_angles = 0;
+  double base_a0 = 0.0, base_a1 = 0.0;
   // second stream + events of the pipelined CSR build (ctsm_csr_build)
   cudaStream_t side = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -847,6 +852,7 @@ int ctsm_spmv_t(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols, const uint64_t*
 // ---- K5/K6 ----------------------------------------------------------------
 static int prepare_cs(ctsm_ctx* ctx, const DevGeom& d, int begin, int step, int n_sel,
                       cudaStream_t st) {
+  ctx->base_valid = false;  // cs is shared with the symmetric kernels' base tables
   CT_TRY(ensure(ctx, ctx->cs, (size_t)(n_sel > 0 ? n_sel : 1) * sizeof(AngleCS)));
   CT_CUDA(build_angle_cs(d, begin, step, n_sel, (AngleCS*)ctx->cs.p, st));
   return 0;
@@ -924,12 +930,24 @@ static bool sym_base_of_shard(const ctsm_geometry* g, int begin, int end, int st
 static int upload_base(ctsm_ctx* ctx, const DevGeom& d, const std::vector<int>& base,
                        cudaStream_t st) {
   const size_t n = base.size();
+  // the base list and its (cos, sin) table depend only on the scan's angles:
+  // repeated projections of one scan (the common case) skip the upload, the
+  // table kernel and the host synchronisation
+  if (ctx->base_valid && ctx->base_cached == base && ctx->base_n_angles == d.n_angles &&
+      ctx->base_a0 == d.angle_start && ctx->base_a1 == d.angle_end && ctx->base.p && ctx->cs.p)
+    return 0;
+  ctx->base_valid = false;
   CT_TRY(ensure(ctx, ctx->base, (n ? n : 1) * sizeof(int)));
   if (n)
     CT_CUDA(cudaMemcpyAsync(ctx->base.p, base.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
   CT_TRY(ensure(ctx, ctx->cs, (n ? n : 1) * sizeof(AngleCS)));
   CT_CUDA(build_angle_cs_list(d, (const int*)ctx->base.p, (int)n, (AngleCS*)ctx->cs.p, st));
   CT_CUDA(cudaStreamSynchronize(st));  // base is pageable host memory
+  ctx->base_cached = base;
+  ctx->base_n_angles = d.n_angles;
+  ctx->base_a0 = d.angle_start;
+  ctx->base_a1 = d.angle_end;
+  ctx->base_valid = true;
   return 0;
 }
 
