@@ -474,15 +474,13 @@ cudaError_t csr_sort_rows_radix(uint64_t n_rows, const uint64_t* row_start, cons
                                 uint32_t* col_out, double* val_out, uint64_t out_cap,
                                 uint64_t grp_cap, unsigned* long_rows, unsigned* n_long,
                                 cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  {  // per device (function attributes are not shared between devices): set on every call
     cudaError_t e = cudaFuncSetAttribute(sort_rows_radix, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(kRsWarps * sizeof(RsWarp)));
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(sort_rows_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(kLongCap * sizeof(unsigned long long)));
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   cudaError_t e = cudaMemsetAsync(n_long, 0, sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
