@@ -74,10 +74,17 @@ def parse():
     return a
 
 
+def share_gpu():
+    """CTSM_BENCH_SHARE_GPU=1: every rank uses cuda:0 and the collectives go
+    through gloo. A functional check of the N-rank code path on a one-GPU box
+    (tests/test_gpu_host_calls.py); never a measurement."""
+    return os.environ.get("CTSM_BENCH_SHARE_GPU") == "1"
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if share_gpu() else int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
 
 
@@ -114,7 +121,10 @@ def init_dist(torch, dev):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=dev)
+        if share_gpu():
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         assert dist.get_world_size() == world
         t = torch.ones(1, device=dev)
         dist.all_reduce(t)
@@ -494,6 +504,71 @@ def e2e_projection_pair(torch, args, g, x_h, y_h, ctx, local, updates_per_step):
                       " (pinned host buffers), issued concurrently from two host threads")}
 
 
+def e2e_projection_pair_sharded(torch, dist, args, g, x_h, y_h, dev, world, rank,
+                                updates_per_step):
+    """N ranks: the step through the public sharded API (dist.sharded_forward
+    / sharded_back_project) with pinned host buffers. Per step and rank: x
+    host -> device, A x on the rank's angle shard, its sinogram rows device ->
+    host; its rows of y host -> device, A^T y on the shard, the NCCL
+    all-reduce of the volume, the volume device -> host. Timed between
+    barriers, max over ranks."""
+    from paper_2511_12235_b200.dist import (angle_shard, shard_angles, sharded_back_project,
+                                            sharded_forward)
+    f32 = args.dtype == "f32"
+    npdt, es = (np.float32, 4) if f32 else (np.float64, 8)
+    tdt = torch.float32 if f32 else torch.float64
+    rpa = g.rows_per_angle
+    angles = shard_angles(g, angle_shard(g, rank, world)).tolist()
+    xh = torch.from_numpy(x_h.astype(npdt)).pin_memory()
+    yh = torch.from_numpy(y_h.astype(npdt)).pin_memory().view(g.n_angles, rpa)
+    yo = torch.empty(g.n_angles, rpa, dtype=tdt).pin_memory()
+    xo = torch.empty(g.n_voxels, dtype=tdt).pin_memory()
+    xd = torch.empty(g.n_voxels, dtype=tdt, device=dev)
+    yd = torch.zeros(g.n_angles, rpa, dtype=tdt, device=dev)
+    yin = torch.zeros(g.n_angles, rpa, dtype=tdt, device=dev)
+    bp = torch.empty(g.n_voxels, dtype=tdt, device=dev)
+    idx = torch.tensor(angles, device=dev)
+    idx_h = torch.tensor(angles)
+    stage_d = torch.empty(len(angles), rpa, dtype=tdt, device=dev)
+    stage_h = torch.empty(len(angles), rpa, dtype=tdt).pin_memory()      # A x rows out
+    stage_in_h = torch.empty(len(angles), rpa, dtype=tdt).pin_memory()   # y rows in
+
+    def step():
+        xd.copy_(xh, non_blocking=True)
+        sharded_forward(g, xd, out=yd.view(-1))
+        torch.index_select(yd, 0, idx, out=stage_d)
+        stage_h.copy_(stage_d, non_blocking=True)
+        # this rank's rows of y: gathered on the host, one H2D copy, scattered on the device
+        torch.index_select(yh, 0, idx_h, out=stage_in_h)
+        stage_d.copy_(stage_in_h, non_blocking=True)
+        yin.index_copy_(0, idx, stage_d)
+        sharded_back_project(g, yin.view(-1), out=bp)
+        xo.copy_(bp, non_blocking=True)
+        torch.cuda.synchronize()
+
+    n_warm = max(1, min(args.warmup, 3))
+    n_steps = args.steps if g.is_2d() else min(args.steps, 5)
+    for _ in range(n_warm):
+        step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(n_steps):
+        step()
+    dist.barrier()
+    te = torch.tensor([(time.perf_counter() - t0) / n_steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    te = float(te.item())
+    rows = len(angles) * rpa
+    return {"value": updates_per_step / te, "unit": "updates/s",
+            "h2d_bytes_per_step": es * (g.n_voxels + rows),
+            "d2h_bytes_per_step": es * (rows + g.n_voxels),
+            "bytes_are": "per rank (x replicated, the rank's own sinogram rows)",
+            "ms_per_step": te * 1e3, "steps": n_steps,
+            "calls": "dist.sharded_forward / dist.sharded_back_project with pinned host buffers "
+                     "on every rank (max over ranks)"}
+
+
 def run_ours(args):
     import torch
 
@@ -574,6 +649,10 @@ def run_ours(args):
     if not args.no_e2e and world == 1:
         del yout, xout
         e2e = e2e_projection_pair(torch, args, g, x_h, y_h, ctx, local, updates_per_step)
+    elif not args.no_e2e:
+        del yout, xout
+        e2e = e2e_projection_pair_sharded(torch, dist, args, g, x_h, y_h, dev, world, rank,
+                                          updates_per_step)
 
     if rank != 0:
         if world > 1:

@@ -4,6 +4,7 @@ e2e leg): equal to the device-resident calls, also when A x and A^T y run
 concurrently from two host threads on two contexts (each context owns its
 scratch, status word and non-blocking stream)."""
 import ctypes
+import os
 from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
@@ -97,3 +98,30 @@ def test_host_calls_f32(name):
     finally:
         ca.close()
         cb.close()
+
+
+def test_bench_two_ranks_functional(tmp_path):
+    """bench.py --gpus 2 launches two ranks (orbit shards, all-reduce of the
+    A^T y volume, max-over-ranks timing, one JSON line from rank 0). On this
+    one-GPU box both ranks share cuda:0 and reduce through gloo
+    (CTSM_BENCH_SHARE_GPU=1): a check of the N-rank code path on the real
+    kernels, not a measurement."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CTSM_BENCH_SHARE_GPU="1")
+    for extra in (["--config", "c1", "--dtype", "f32"],
+                  ["--config", "c1", "--mode", "sirt", "--no-e2e"]):
+        r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps",
+                            "2", "--warmup", "1", "--no-cpu", "--no-clocks"] + extra,
+                           capture_output=True, text=True, timeout=900, env=env, cwd=root)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        assert len(lines) == 1, r.stdout
+        line = json.loads(lines[0])
+        assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
+        assert "x2" in line["config"]["parallelism"]
+        if "--no-e2e" not in extra:
+            assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
