@@ -479,7 +479,7 @@ int ctsm_csr_fill(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int an
     CT_CUDA(csr_emit(d, ctx->angles.p, ctx->edges.p, na, sk, ctx->plans.p, ctx->status, st));
     unsigned* lr = (unsigned*)ctx->longrows.p;
     CT_CUDA(csr_sort_rows_radix(nr, row_start_dev + row_off, ctx->grp.p, col_dev, val_dev, ~0ull,
-                                nnz_c, lr, lr + nr + 1, st));
+                                nnz_c, lr, lr + nr + 1, st, (uint64_t)d.n_vox));
   }
   return check_status(ctx, st, "build_system_matrix");
 }
@@ -562,7 +562,7 @@ int ctsm_csr_build(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int a
                                   cap, sb));
       unsigned* lr = (unsigned*)lrow[p]->p;
       CT_CUDA(csr_sort_rows_radix(nr, row_start_dev + row_off, grp[p]->p, col_dev, val_dev,
-                                  capacity, cap, lr, lr + nr + 1, sb));
+                                  capacity, cap, lr, lr + nr + 1, sb, (uint64_t)d.n_vox));
       CT_CUDA(cudaEventRecord(ctx->ev[2 + p], sb));
     }
     // join, then look at the counts

@@ -279,21 +279,28 @@ __global__ void __launch_bounds__(256) scatter_records_kernel(const uint4* __res
 // (32 keys at a time: match_any ranks equal digits within the chunk).
 constexpr int kRsWarps = 4;
 constexpr int kRsCap = 1024;  // longer rows go to sort_rows_block
+constexpr int kRsIdxBits = 10;
+// kPacked (columns below 2^22, e.g. C0 and C2): a key and its entry index
+// travel as one 32-bit word (column << 10 | index): one shared-memory array
+// pair instead of two, 9 instead of 13 KB per warp.
+template <bool kPacked>
 struct RsWarp {
   uint32_t key[2][kRsCap];
-  uint16_t idx[2][kRsCap];
+  uint16_t idx[kPacked ? 1 : 2][kPacked ? 1 : kRsCap];
   uint32_t hist[256];
 };
 
+template <bool kPacked>
 __global__ void __launch_bounds__(kRsWarps * 32) sort_rows_radix(
     uint64_t n_rows, const uint64_t* __restrict__ rs, const uint4* __restrict__ grp,
     uint32_t* __restrict__ col_out, double* __restrict__ val_out, uint64_t out_cap,
     uint64_t grp_cap, unsigned* long_rows, unsigned* n_long) {
   extern __shared__ __align__(16) unsigned char rs_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  RsWarp& w = reinterpret_cast<RsWarp*>(rs_smem)[wid];
+  RsWarp<kPacked>& w = reinterpret_cast<RsWarp<kPacked>*>(rs_smem)[wid];
   const unsigned full = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
+  constexpr int kS = kPacked ? kRsIdxBits : 0;  // the column starts at this bit of a key
   const uint64_t warps_total = (uint64_t)gridDim.x * kRsWarps;
   const uint64_t base = rs[0];  // the grouped arrays start at the chunk's first entry
   for (uint64_t r = (uint64_t)blockIdx.x * kRsWarps + wid; r < n_rows; r += warps_total) {
@@ -309,8 +316,8 @@ __global__ void __launch_bounds__(kRsWarps * 32) sort_rows_radix(
     uint32_t kor = 0u, kand = ~0u;
     for (int i = lane; i < n; i += 32) {
       const uint32_t k = grp[b + i].x;
-      w.key[0][i] = k;
-      w.idx[0][i] = (uint16_t)i;
+      w.key[0][i] = kPacked ? ((k << kRsIdxBits) | (uint32_t)i) : k;
+      if (!kPacked) w.idx[0][i] = (uint16_t)i;
       kor |= k;
       kand &= k;
     }
@@ -326,11 +333,12 @@ __global__ void __launch_bounds__(kRsWarps * 32) sort_rows_radix(
         kand &= __shfl_xor_sync(full, kand, o);
       }
       const uint32_t diff = kor ^ kand;
-      for (int shift = 0; shift < 32; shift += 8) {
+      for (int shift = 0; shift < 32 - kS; shift += 8) {
         if (((diff >> shift) & 0xffu) == 0u) continue;
         for (int j = lane; j < 256; j += 32) w.hist[j] = 0u;
         __syncwarp();
-        for (int i = lane; i < n; i += 32) atomicAdd(&w.hist[(w.key[cur][i] >> shift) & 0xffu], 1u);
+        for (int i = lane; i < n; i += 32)
+          atomicAdd(&w.hist[(w.key[cur][i] >> (shift + kS)) & 0xffu], 1u);
         __syncwarp();
         {
           unsigned loc[8], sum = 0u;
@@ -357,14 +365,15 @@ __global__ void __launch_bounds__(kRsWarps * 32) sort_rows_radix(
           const int i = c + lane;
           const bool valid = i < n;
           const uint32_t k = valid ? w.key[cur][i] : 0u;
-          const uint16_t id = valid ? w.idx[cur][i] : (uint16_t)0;
-          const unsigned d = valid ? ((k >> shift) & 0xffu) : (256u + (unsigned)lane);
+          uint16_t id = 0;
+          if (!kPacked) id = valid ? w.idx[cur][i] : (uint16_t)0;
+          const unsigned d = valid ? ((k >> (shift + kS)) & 0xffu) : (256u + (unsigned)lane);
           const unsigned peers = __match_any_sync(full, d);
           const unsigned rank = __popc(peers & lt);
           if (valid) {
             const unsigned pos = w.hist[d] + rank;
             w.key[cur ^ 1][pos] = k;
-            w.idx[cur ^ 1][pos] = id;
+            if (!kPacked) w.idx[cur ^ 1][pos] = id;
           }
           __syncwarp();
           if (valid && rank == 0u) w.hist[d] += __popc(peers);
@@ -374,8 +383,10 @@ __global__ void __launch_bounds__(kRsWarps * 32) sort_rows_radix(
       }
     }
     for (int i = lane; i < n; i += 32) {
-      const uint4 e = grp[b + w.idx[cur][i]];
-      col_out[base + b + i] = w.key[cur][i];
+      const uint32_t k = w.key[cur][i];
+      const unsigned src = kPacked ? (k & ((1u << kRsIdxBits) - 1u)) : (unsigned)w.idx[cur][i];
+      const uint4 e = grp[b + src];
+      col_out[base + b + i] = kPacked ? (k >> kRsIdxBits) : k;
       val_out[base + b + i] = __hiloint2double((int)e.w, (int)e.z);
     }
     __syncwarp();
@@ -464,7 +475,10 @@ cudaError_t csr_scatter_records(const void* rec, const unsigned long long* n_dev
                                 unsigned long long cap, unsigned* cursor, void* grp,
                                 uint64_t grp_cap, cudaStream_t st) {
   if (cap == 0) return cudaSuccess;
-  scatter_records_kernel<<<148 * 32, 256, 0, st>>>((const uint4*)rec, n_dev, cap, cursor,
+#ifndef CTSM_SCATTER_BLOCKS
+#define CTSM_SCATTER_BLOCKS 32
+#endif
+  scatter_records_kernel<<<148 * CTSM_SCATTER_BLOCKS, 256, 0, st>>>((const uint4*)rec, n_dev, cap, cursor,
                                                    (uint4*)grp, grp_cap);
   count_launch();
   return cudaGetLastError();
@@ -473,10 +487,16 @@ cudaError_t csr_scatter_records(const void* rec, const unsigned long long* n_dev
 cudaError_t csr_sort_rows_radix(uint64_t n_rows, const uint64_t* row_start, const void* grp,
                                 uint32_t* col_out, double* val_out, uint64_t out_cap,
                                 uint64_t grp_cap, unsigned* long_rows, unsigned* n_long,
-                                cudaStream_t st) {
+                                cudaStream_t st, uint64_t n_cols) {
+  const bool packed = n_cols != 0 && n_cols <= (1ull << (32 - kRsIdxBits));
   {  // per device (function attributes are not shared between devices): set on every call
-    cudaError_t e = cudaFuncSetAttribute(sort_rows_radix, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(kRsWarps * sizeof(RsWarp)));
+    cudaError_t e = packed
+                        ? cudaFuncSetAttribute(sort_rows_radix<true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)(kRsWarps * sizeof(RsWarp<true>)))
+                        : cudaFuncSetAttribute(sort_rows_radix<false>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)(kRsWarps * sizeof(RsWarp<false>)));
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(sort_rows_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(kLongCap * sizeof(unsigned long long)));
@@ -486,9 +506,20 @@ cudaError_t csr_sort_rows_radix(uint64_t n_rows, const uint64_t* row_start, cons
   if (e != cudaSuccess) return e;
   if (n_rows == 0) return cudaSuccess;
   const uint64_t blocks = (n_rows + kRsWarps - 1) / kRsWarps;
-  const unsigned grid = (unsigned)(blocks < 148ull * 4 ? blocks : 148ull * 4);
-  sort_rows_radix<<<grid, kRsWarps * 32, kRsWarps * sizeof(RsWarp), st>>>(
-      n_rows, row_start, (const uint4*)grp, col_out, val_out, out_cap, grp_cap, long_rows, n_long);
+#ifndef CTSM_SORT_BLOCKS
+#define CTSM_SORT_BLOCKS 0  // blocks per SM in the grid; 0: what the shared memory allows
+#endif
+  // 37 KB (packed) / 53 KB of shared memory per block
+  const uint64_t per_sm = CTSM_SORT_BLOCKS ? CTSM_SORT_BLOCKS : (packed ? 6 : 4);
+  const unsigned grid = (unsigned)(blocks < 148ull * per_sm ? blocks : 148ull * per_sm);
+  if (packed)
+    sort_rows_radix<true><<<grid, kRsWarps * 32, kRsWarps * sizeof(RsWarp<true>), st>>>(
+        n_rows, row_start, (const uint4*)grp, col_out, val_out, out_cap, grp_cap, long_rows,
+        n_long);
+  else
+    sort_rows_radix<false><<<grid, kRsWarps * 32, kRsWarps * sizeof(RsWarp<false>), st>>>(
+        n_rows, row_start, (const uint4*)grp, col_out, val_out, out_cap, grp_cap, long_rows,
+        n_long);
   sort_rows_block<<<148, kLongThreads, kLongCap * sizeof(unsigned long long), st>>>(
       long_rows, n_long, row_start, (const uint4*)grp, col_out, val_out, out_cap, grp_cap);
   count_launch(2);

@@ -66,13 +66,15 @@ cudaError_t csr_emit(const DevGeom& g, const void* angles_dev, const void* edges
 // val_out are the whole matrix's arrays (out_cap
 // entries; rows reaching beyond are skipped). The record count is read from
 // device memory (*n_dev, clamped to cap), so the host never waits on a chunk.
+// n_cols (if given and <= 2^22) lets the sort pack a key and its entry index
+// into one 32-bit word.
 cudaError_t csr_scatter_records(const void* rec, const unsigned long long* n_dev,
                                 unsigned long long cap, unsigned* cursor, void* grp,
                                 uint64_t grp_cap, cudaStream_t st);
 cudaError_t csr_sort_rows_radix(uint64_t n_rows, const uint64_t* row_start, const void* grp,
                                 uint32_t* col_out, double* val_out, uint64_t out_cap,
                                 uint64_t grp_cap, unsigned* long_rows, unsigned* n_long,
-                                cudaStream_t st);
+                                cudaStream_t st, uint64_t n_cols = 0);
 // row_start[0..n] = exclusive scan of counts[0..n-1] (u32 -> u64); scratch
 // needs scan_scratch_bytes(n).
 size_t scan_scratch_bytes(uint64_t n);
