@@ -342,7 +342,11 @@ static int prepare_exact(ctsm_ctx* ctx, const DevGeom& d, int angle_begin, int n
 // Angles per emission chunk: bounds the per-chunk scratch (plans, records,
 // row-grouped arrays) and keeps chunk-local rows and entries below 2^31.
 static int csr_chunk_angles(const DevGeom& d, int n_sel, uint64_t per_angle_entries) {
-  const uint64_t rec_budget = 2ull << 30, plan_budget = 1ull << 30;
+  static const uint64_t rec_budget = [] {  // experiment knob: CTSM_CSR_REC_MB
+    const char* e = getenv("CTSM_CSR_REC_MB");
+    return (uint64_t)(e ? atoll(e) : 2048) << 20;
+  }();
+  const uint64_t plan_budget = 1ull << 30;
   uint64_t a = rec_budget / (16ull * (per_angle_entries + 1));
   const size_t plan1 = csr_plan_bytes(d, 1);
   if (plan1) a = std::min<uint64_t>(a, plan_budget / plan1);
@@ -515,7 +519,8 @@ int ctsm_csr_build(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int a
   uint64_t per_angle = nnz0 + nnz0 / 2 + 4096;  // angle 0 is a flat (sparser) angle
   const unsigned long long seg_slack = 148ull * 8 * 4 * 256;
   for (int attempt = 0;; ++attempt) {
-    const int A = std::max(1, csr_chunk_angles(d, n_sel, per_angle) / 2);
+    // (the scratch is double-buffered: ~4 x the record budget in total)
+    const int A = csr_chunk_angles(d, n_sel, per_angle);
     const unsigned long long cap = (unsigned long long)A * per_angle + seg_slack;
     const int n_chunks = (n_sel + A - 1) / A;
     // double-buffered per-chunk scratch
