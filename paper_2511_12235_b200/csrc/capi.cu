@@ -515,7 +515,8 @@ int ctsm_csr_build(ctsm_ctx* ctx, const ctsm_geometry* g, int angle_begin, int a
   if (!ctx->side) CT_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
   for (int i = 0; i < 4; ++i)
     if (!ctx->ev[i]) CT_CUDA(cudaEventCreateWithFlags(&ctx->ev[i], cudaEventDisableTiming));
-  cudaStream_t sb = ctx->side;
+  static const bool one_stream = getenv("CTSM_CSR_ONE_STREAM") != nullptr;  // experiment knob
+  cudaStream_t sb = one_stream ? st : ctx->side;
   uint64_t per_angle = nnz0 + nnz0 / 2 + 4096;  // angle 0 is a flat (sparser) angle
   const unsigned long long seg_slack = 148ull * 8 * 4 * 256;
   for (int attempt = 0;; ++attempt) {
