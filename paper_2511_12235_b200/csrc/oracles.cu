@@ -126,37 +126,36 @@ __global__ void __launch_bounds__(kGlThreads) multiline_volume_kernel(
   }
   const double uc = 0.5 * (u_lo + u_hi), ur = 0.5 * (u_hi - u_lo);
   const double vc = 0.5 * (v_lo + v_hi), vr = 0.5 * (v_hi - v_lo);
+  // One thread per ray of the k x k grid (strided); a ray S + t (D - S) meets
+  // the box in the parameter interval common to the three axis slabs, and its
+  // share of the cone volume over that interval is (t1^3 - t0^3) / 3.
   double total = 0.0;
   const long long n_rays = (long long)k * k;
+  const double src[3] = {sx, sy, 0.0};
+  const double bmin[3] = {x0, y0, zb}, bmax[3] = {x1, y1, zt};
   for (long long r = threadIdx.x; r < n_rays; r += kGlThreads) {
     const int i = (int)(r / k), j = (int)(r % k);
     const double ey = (uc + ur * nodes[i]) * d_y;
     const double ez = (vc + vr * nodes[j]) * d_z;
-    const double dx = -d * cp - ey * sp, dy = -d * sp + ey * cp, dz = ez;
-    double t0 = 0.0, t1 = INFINITY;
-    const double org[3] = {sx, sy, 0.0};
-    const double dir[3] = {dx - sx, dy - sy, dz};
-    const double lo[3] = {x0, y0, zb}, hi[3] = {x1, y1, zt};
+    // detector point of the ray, minus the source
+    const double dir[3] = {(-d * cp - ey * sp) - sx, (-d * sp + ey * cp) - sy, ez};
+    double t_in = 0.0, t_out = INFINITY;
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-      if (fabs(dir[ax]) < 1e-300) {
-        if (org[ax] < lo[ax] || org[ax] > hi[ax]) {
-          t0 = 1.0;
-          t1 = 0.0;
+      if (fabs(dir[ax]) < 1e-300) {  // parallel to the slab: inside or never
+        if (src[ax] < bmin[ax] || src[ax] > bmax[ax]) {
+          t_in = 1.0;
+          t_out = 0.0;
         }
         continue;
       }
-      double ta = (lo[ax] - org[ax]) / dir[ax];
-      double tb = (hi[ax] - org[ax]) / dir[ax];
-      if (ta > tb) {
-        const double tmp = ta;
-        ta = tb;
-        tb = tmp;
-      }
-      t0 = omax(t0, ta);
-      t1 = omin(t1, tb);
+      const double ta = (bmin[ax] - src[ax]) / dir[ax];
+      const double tb = (bmax[ax] - src[ax]) / dir[ax];
+      t_in = omax(t_in, ta > tb ? tb : ta);
+      t_out = omin(t_out, ta > tb ? ta : tb);
     }
-    if (t1 > t0) total += wts[i] * wts[j] * (t1 * t1 * t1 - t0 * t0 * t0) / 3.0;
+    if (t_out > t_in)
+      total += wts[i] * wts[j] * (t_out * t_out * t_out - t_in * t_in * t_in) / 3.0;
   }
   red[threadIdx.x] = total;
   __syncthreads();
