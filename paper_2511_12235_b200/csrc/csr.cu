@@ -64,10 +64,11 @@ __global__ void __launch_bounds__(128, CTSM_CSR2_MINB) csr2d_kernel(DevGeom g, c
   bool have = false;
   int cur = 0;
   double cw = 0.0;
+  exact::AreaCache ac;
   for (int p = 0; p < sw.np; ++p) {
     const int cell = sw.pcell[p];
     if (cell < cell_lo || cell > cell_hi) continue;
-    double w = exact::piece_area(sw, p, g.s, status);
+    double w = exact::piece_area_cached(sw, p, g.s, status, ac);
     if (w < 0.0) {
       if (w < kNegClamp2D) raise_status(status, CTSM_ERR_NON_FINITE);
       w = 0.0;

@@ -188,13 +188,14 @@ __global__ void __launch_bounds__(128) plan3d_kernel(DevGeom g,
   const int cell_lo = -g.n_det_y / 2, cell_hi = g.n_det_y / 2 - 1;
   int ng = 0;
   int i = 0;
+  exact::AreaCache ac;
   while (i < sw.np) {
     int j = i;
     while (j < sw.np && sw.pcell[j] == sw.pcell[i]) ++j;
     const int cell = sw.pcell[i];
     if (cell >= cell_lo && cell <= cell_hi) {
       double w2d = 0.0;
-      for (int p = i; p < j; ++p) w2d += exact::piece_area(sw, p, s, status);
+      for (int p = i; p < j; ++p) w2d += exact::piece_area_cached(sw, p, s, status, ac);
       if (w2d < 0.0) w2d = 0.0;
       out->gbeg[ng] = (unsigned char)i;
       out->gend[ng] = (unsigned char)j;

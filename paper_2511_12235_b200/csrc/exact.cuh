@@ -283,6 +283,97 @@ __device__ __forceinline__ double piece_area(const Sweep& sw, int p, double s, i
   }
 }
 
+// piece_area with the identical sub-expressions of consecutive calls shared
+// (bit-preserving: same operations on the same operands, evaluated once):
+//   * sin(gamma_near - gamma_far) and sin(phi - gamma_near) depend only on
+//     the pixel and the piece kind; the reference evaluates them in every
+//     triangle_area_factor call (weights2d.cpp:10-14), twice per piece;
+//   * triangle_area_factor at a breakpoint is needed as b_hi of one piece and
+//     as b_lo of the next piece of the same kind (weights2d.cpp:93-99), and
+//     cos / tan(phi - beta) of band_area (weights2d.cpp:21-26) likewise.
+// A pixel's ~6 pieces then cost ~3 crmath calls each instead of 12.
+struct AreaCache {
+  int tag0 = -1, tag2 = -1, tagb = -1;  // breakpoint whose value is cached
+  double val0 = 0.0, val2 = 0.0;        // triangle factor at tag0 (kind 0) / tag2 (kind 2)
+  double cb = 0.0, tb = 0.0;            // cos / tan(phi - brk[tagb])
+  bool have0 = false, have2 = false;
+  double nf0 = 0.0, pn0 = 0.0, nf2 = 0.0, pn2 = 0.0;  // sin(gn - gf), sin(phi - gn) per kind
+};
+
+// triangle_area_factor(phi, gamma_far, gamma_near, brk[bi], a, b) for kind 0
+// (gamma_far = G1, gamma_near = G2) or kind 2 (G4, G3).
+__device__ __forceinline__ double tri_factor_at(const Sweep& sw, int kind, int bi, double a,
+                                                double b, AreaCache& c) {
+  const double gf = kind == 0 ? sw.G1 : sw.G4, gn = kind == 0 ? sw.G2 : sw.G3;
+  double nf, pn;
+  if (kind == 0) {
+    if (!c.have0) {
+      c.nf0 = crm_sin(gn - gf);
+      c.pn0 = crm_sin(sw.phi - gn);
+      c.have0 = true;
+    }
+    nf = c.nf0;
+    pn = c.pn0;
+  } else {
+    if (!c.have2) {
+      c.nf2 = crm_sin(gn - gf);
+      c.pn2 = crm_sin(sw.phi - gn);
+      c.have2 = true;
+    }
+    nf = c.nf2;
+    pn = c.pn2;
+  }
+  const double beta = sw.brk[bi];
+  if (fabs(nf) < kEpsAngle) return 0.0;
+  if (fabs(crm_sin(beta - sw.phi)) < kEpsAngle) return 0.0;
+  const double den = fabs(crm_sin(2.0 * (sw.phi - beta)));
+  const double r = pn * crm_sin(beta - gf) / nf;
+  return (a / (b * den)) * r * r;
+}
+
+__device__ __forceinline__ double piece_area_cached(const Sweep& sw, int p, double s, int* status,
+                                                    AreaCache& c) {
+  const double a = sw.x1 - sw.x0, b = sw.y1 - sw.y0;
+  const int lo = sw.pb[p], hi = lo + 1;
+  switch (sw.pkind[p]) {
+    case 0: {
+      const double tlo = c.tag0 == lo ? c.val0 : tri_factor_at(sw, 0, lo, a, b, c);
+      const double thi = tri_factor_at(sw, 0, hi, a, b, c);
+      c.tag0 = hi;
+      c.val0 = thi;
+      return thi - tlo;
+    }
+    case 1: {
+      double c1, t1;
+      if (c.tagb == lo) {
+        c1 = c.cb;
+        t1 = c.tb;
+      } else {
+        c1 = crm_cos(sw.phi - sw.brk[lo]);
+        t1 = crm_tan(sw.phi - sw.brk[lo]);
+      }
+      const double c2 = crm_cos(sw.phi - sw.brk[hi]);
+      const double t2 = crm_tan(sw.phi - sw.brk[hi]);
+      c.tagb = hi;
+      c.cb = c2;
+      c.tb = t2;
+      if (fabs(c1) < kEpsAngle || fabs(c2) < kEpsAngle) {
+        raise_status(status, CTSM_ERR_RAY_PARALLEL_TO_FACE);
+        return 0.0;
+      }
+      const double xm = 0.5 * (sw.x0 + sw.x1);
+      return (1.0 / b) * fabs(s * sw.C - xm) * fabs(t1 - t2);
+    }
+    default: {
+      const double tlo = c.tag2 == lo ? c.val2 : tri_factor_at(sw, 2, lo, a, b, c);
+      const double thi = tri_factor_at(sw, 2, hi, a, b, c);
+      c.tag2 = hi;
+      c.val2 = thi;
+      return tlo - thi;
+    }
+  }
+}
+
 // atom_sum lambda (weights3d.cpp:400-423) over pieces [i, j) of one cell.
 __device__ __forceinline__ double atom_sum(const Sweep& sw, int i, int j, double s, double a,
                                            double b, double cz, double tan_a, double zref) {

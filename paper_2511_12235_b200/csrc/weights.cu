@@ -73,10 +73,11 @@ __global__ void __launch_bounds__(64) weights_batch_kernel(DevGeom g,
     bool have = false;
     int cur = 0;
     double cw = 0.0;
+    exact::AreaCache ac;
     for (int p = 0; p < sw.np; ++p) {
       const int cell = sw.pcell[p];
       if (cell < cell_lo || cell > cell_hi) continue;
-      double w = exact::piece_area(sw, p, s, status);
+      double w = exact::piece_area_cached(sw, p, s, status, ac);
       if (w < 0.0) {
         if (w < kNegClamp2D) raise_status(status, CTSM_ERR_NON_FINITE);
         w = 0.0;
@@ -120,13 +121,14 @@ __global__ void __launch_bounds__(64) weights_batch_kernel(DevGeom g,
   }
   const int row_lo = -g.n_det_z / 2, row_hi = g.n_det_z / 2 - 1;
   int i = 0;
+  exact::AreaCache ac;
   while (i < sw.np) {
     int j = i;
     while (j < sw.np && sw.pcell[j] == sw.pcell[i]) ++j;
     const int cell = sw.pcell[i];
     if (cell >= cell_lo && cell <= cell_hi) {
       double w2d = 0.0;
-      for (int p = i; p < j; ++p) w2d += exact::piece_area(sw, p, s, status);
+      for (int p = i; p < j; ++p) w2d += exact::piece_area_cached(sw, p, s, status, ac);
       if (w2d < 0.0) w2d = 0.0;
       auto above = [&](double kk) -> double {
         if (kk <= m_min) return w2d;
