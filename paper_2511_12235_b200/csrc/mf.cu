@@ -955,9 +955,22 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
             // FA: the interleaved scratch rows carry all G image slots and
             // fwd3d_uninterleave reads only the first 4 of a self-symmetric
             // base angle, so the other 4 may accumulate (unused) values
+            if constexpr (FA && sizeof(T) == 4) {
+              // packed fp32 FMAs (FFMA2, sm_100): two images per instruction,
+              // each component rounded as the scalar FMA would
+              const float2 w2 = make_float2((float)wp, (float)wp);
 #pragma unroll
-            for (int u = 0; u < V; ++u)
-              if (FA || c * V + u < ne) acc[c * V + u] += wp * v[u];
+              for (int u = 0; u < V; u += 2) {
+                const float2 r = __ffma2_rn(w2, make_float2((float)v[u], (float)v[u + 1]),
+                                            make_float2((float)acc[c * V + u], (float)acc[c * V + u + 1]));
+                acc[c * V + u] = (PT)r.x;
+                acc[c * V + u + 1] = (PT)r.y;
+              }
+            } else {
+#pragma unroll
+              for (int u = 0; u < V; ++u)
+                if (FA || c * V + u < ne) acc[c * V + u] += wp * v[u];
+            }
           }
         };
         acc_side(pv, iz - z0);
