@@ -1442,12 +1442,22 @@ cudaError_t fwd_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const int
 // Base angles per launch of the symmetric 3D kernels: every warp touches the
 // rows of all image angles of the launch's base angles, so a launch covering
 // the whole scan streams the sinogram (fixed-point accumulator / input) from
-// HBM with scattered accesses; chunks whose rows fit in ~64 MB of the 126 MB
-// L2 keep the atomics and gathers on chip.
+// HBM with scattered accesses; chunks bound that working set (and the launch's
+// plan and scratch buffers).
 static int sym3d_chunk(const DevGeom& g, int order, size_t elem_bytes) {
   const double per_base = (double)order * g.rows_per_angle * (double)elem_bytes;
-  static const double mb = getenv("CTSM_SYM3D_CHUNK_MB") ? atof(getenv("CTSM_SYM3D_CHUNK_MB")) : 64.0;
-  const int c = (int)((mb * (1 << 20)) / per_base);
+  // r2: 192 MB of image rows per launch. Round 1 kept a launch's rows within
+  // ~64 MB of the L2; with the interleaved fp32 rows and the plan pass longer
+  // launches pay instead (fewer launch tails): C3 189.6 -> 183.5 ms, C4 SIRT
+  // 2.96 -> 2.74 s per iteration at 256 MB, flat beyond ~160 MB.
+  // (measured on the fp32 paths; the fp64 fixed-point rows keep 64 MB)
+  static const double mb_env = getenv("CTSM_SYM3D_CHUNK_MB") ? atof(getenv("CTSM_SYM3D_CHUNK_MB")) : 0.0;
+  const double mb = mb_env > 0.0 ? mb_env : (elem_bytes == 4 ? 192.0 : 64.0);
+  int c = (int)((mb * (1 << 20)) / per_base);
+  // ... and the launch's plans (one per column and base angle) within ~6 GB
+  const double plan_base = (double)g.n_x * g.n_y * (double)sizeof(FastPlan);
+  const int cp = (int)((6144.0 * (1 << 20)) / plan_base);
+  if (c > cp) c = cp;
   return c < 1 ? 1 : c;
 }
 

@@ -221,3 +221,46 @@ def test_csr_c2_flips_vs_reference_glibc(ip):
             fh.write(json.dumps(line) + "\n")
     assert line["max_flipped_w"] < 1e-11, line
     assert dw <= 1e-10, line
+
+
+def test_c2_full_matrix_hashes():
+    """The WHOLE C2 system matrix (360 angle blocks, 4.6 G entries) against the
+    unmodified reference compiled with the correctly rounded libm: entry count
+    and an order-independent 64-bit hash of (row, column, weight bits) of
+    every angle block (tests/golden/c2_block_hashes_ref_cr.npz, generated by
+    tests/golden/make_c2_hashes.py from oracle/_ref). One differing bit in any
+    of the 4.6 G weights, columns or row offsets changes a block hash."""
+    fx_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                           "c2_block_hashes_ref_cr.npz")
+    if not os.path.exists(fx_path):
+        pytest.skip("fixture not generated")
+    fx = np.load(fx_path)
+    g = CONFIGS["c2"]
+    w = build_system_matrix(g, memory_budget_bytes=1 << 40)
+    assert w.nnz() == int(fx["nnz"].sum())
+    rpa = g.rows_per_angle
+    rs = w.row_start
+    k1 = 0x9E3779B97F4A7C15 - (1 << 64)  # the fixture's constants as int64
+    k2 = 0xC2B2AE3D27D4EB4F - (1 << 64)
+    ar = torch.arange(rpa, device=rs.device, dtype=torch.int64)
+    bad = []
+    for ip in range(g.n_angles):
+        blk = rs[ip * rpa:(ip + 1) * rpa + 1]
+        lo, hi = int(blk[0].item()), int(blk[-1].item())
+        if hi - lo != int(fx["nnz"][ip]):
+            bad.append((ip, "nnz", hi - lo, int(fx["nnz"][ip])))
+            continue
+        raster = torch.repeat_interleave(ar, blk[1:] - blk[:-1])
+        key = (raster << 32) | (w.col[lo:hi].to(torch.int64) & 0xFFFFFFFF)
+        m = (w.val[lo:hi].view(torch.int64) * k1) ^ (key * k2)
+        h = int(m.sum().item()) & ((1 << 64) - 1)
+        if h != int(fx["hash"][ip]):
+            bad.append((ip, "hash", hex(h), hex(int(fx["hash"][ip]))))
+    line = {"case": "c2 full CSR vs ref_cr block hashes", "blocks": g.n_angles, "nnz": w.nnz(),
+            "mismatching_blocks": len(bad)}
+    print(json.dumps(line))
+    rep = os.environ.get("CTSM_PARITY_REPORT")
+    if rep:
+        with open(rep, "a") as fh:
+            fh.write(json.dumps(line) + "\n")
+    assert not bad, bad[:5]
