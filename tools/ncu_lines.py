@@ -17,10 +17,12 @@ def main():
     raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
                           "cuda,sass"], capture_output=True, text=True).stdout
     cur_file = cur_fn = hdr = None
-    agg = collections.defaultdict(lambda: [0, 0, ""])
+    agg = collections.defaultdict(lambda: [0, 0, "", 0])
     for r in csv.reader(io.StringIO(raw)):
         if not r:
             continue
+        if r[0] == "Line No" and "--header" in sys.argv:
+            print(list(enumerate(r)))
         if r[0] == "File Path":
             cur_file = r[1].split("/")[-1]
             continue
@@ -36,17 +38,25 @@ def main():
             s, ie = int(r[4] or 0), int(r[7] or 0)
         except ValueError:
             continue
+        # thread-level instruction count (active lanes per line), when present
+        ti_col = next((i for i, h in enumerate(hdr) if h.strip() == "Thread Instructions Executed"), None)
+        try:
+            te = int(r[ti_col] or 0) if ti_col is not None else 0
+        except ValueError:
+            te = 0
         key = (cur_fn[:60], cur_file, int(r[0]))
         agg[key][0] += s
         agg[key][1] += ie
         agg[key][2] = r[1][:90]
+        agg[key][3] += te
     for fn in sorted(set(k[0] for k in agg)):
         sub = [(k, v) for k, v in agg.items() if k[0] == fn]
         ts = sum(v[0] for _, v in sub) or 1
         ti = sum(v[1] for _, v in sub) or 1
         print(f"===== {fn}  samples={ts} warp_instr={ti}")
         for k, v in sorted(sub, key=lambda x: -x[1][0])[:top]:
-            print(f"{100 * v[0] / ts:5.1f}% samp {100 * v[1] / ti:5.1f}% inst  {k[1]}:{k[2]}  {v[2]}")
+            lanes = f"{v[3] / v[1]:5.1f} ln " if v[3] and v[1] else ""
+            print(f"{100 * v[0] / ts:5.1f}% samp {100 * v[1] / ti:5.1f}% inst {lanes} {k[1]}:{k[2]}  {v[2]}")
 
 
 if __name__ == "__main__":
