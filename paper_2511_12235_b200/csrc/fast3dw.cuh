@@ -864,5 +864,203 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
   }
 }
 
+
+// chunk_weights with the (voxel, row edge) walks of a lane flattened into one
+// loop (CTSM_FLAT, batched form only): in chunk_weights the lanes of a warp
+// step through their voxels in lockstep, so every voxel costs the warp the
+// longest edge walk among its 32 lanes (2 or 3 edges, whichever lane has the
+// most); flattened, a lane that finishes a voxel's edges moves on to its next
+// voxel while other lanes still work on theirs, and the warp pays the longest
+// *chunk total* instead of the sum of the per-voxel maxima. The per-lane
+// sequence of evaluations, their operands and the emission order are those
+// of chunk_weights (same lambdas, same products and compares), so the
+// weights are bit-identical.
+// pre(cell, row) is called before the weight of (cell, row) is evaluated (it
+// may turn out to be zero and not be emitted): the back-projection issues the
+// row's image-vector loads there, so that they are in flight during the
+// evaluation instead of being waited for right after it.
+// gend(cell) is called after the last weight of a cell group: the forward
+// flushes its pending row run there, so a run never crosses groups and its
+// detector cell is the group's (loop-invariant address arithmetic).
+struct NoPre {
+  __device__ __forceinline__ void operator()(int, int) const {}
+};
+struct NoGroupEnd {
+  __device__ __forceinline__ void operator()(int) const {}
+};
+template <typename Emit, typename Pre = NoPre, typename GEnd = NoGroupEnd>
+__device__ __forceinline__ void chunk_weights_flat(const DevGeom& g, const ColumnHead& H,
+                                                   const PieceCoef* P, int z0, int z1,
+                                                   Emit&& emit, CubicBatch* B, int lane,
+                                                   Pre&& pre = NoPre(),
+                                                   GEnd&& gend = NoGroupEnd()) {
+  const int row_lo = -g.n_det_z / 2, row_hi = g.n_det_z / 2 - 1;
+  const double dz_sdd = g.dz_sdd, sdd_dz = g.sdd_dz;
+  const double c_mn = sdd_dz * H.dmin_inv, c_mx = sdd_dz * H.dmax_inv;
+  const double c_lo = fmin(c_mn, c_mx), c_hi = fmax(c_mn, c_mx);
+  const double ga = H.inv_a * sdd_dz;  // G = zref * ga / |L|
+  const double hz = g.n_z / 2.0, vc = g.c;
+  for (int q = 0; q < H.ng; ++q) {
+    const double w2d = H.gw2d[q];
+    const int cell = H.gcell[q];
+    const double gmn = H.gmin[q], gmx = H.gmax[q];
+    const double l1 = H.kappa * H.galpha[q] * ga * dz_sdd, l2 = H.kappa * H.gbeta[q] * dz_sdd;
+    auto cheap = [&](double aL, double zref, double& f) -> bool {
+      const double u = zref * ga;
+      if (u <= gmn * aL) {
+        f = 0.0;
+        return true;
+      }
+      if (u > gmx * aL) {
+        f = l1 * zref - l2 * aL;
+        return true;
+      }
+      return false;
+    };
+    // walk state of the lane: voxel iz with faces zb / zt, its magnification
+    // range, the current edge L and the last edge Le of the voxel
+    int iz, L = 0, Le = -1, k_lo = 0;
+    double zb = 0.0, zt = 0.0, m_min = 0.0, m_max = 0.0;
+    // pass 1: list the cubic faces
+    auto setup1 = [&]() {
+      for (; iz < z1; ++iz) {
+        zb = ((double)iz - hz) * vc;
+        zt = zb + vc;
+        m_min = zb * (zb >= 0.0 ? c_lo : c_hi);
+        m_max = zt * (zt <= 0.0 ? c_lo : c_hi);
+        const int fl = (int)floor(m_min);
+        k_lo = (fl < row_lo) ? row_lo : fl;
+        const int chi = (int)ceil(m_max) - 1;
+        const int k_hi = (chi < row_hi) ? chi : row_hi;
+        L = k_lo + (fl >= row_lo);
+        Le = k_hi + (chi >= row_hi);
+        if (L <= Le) return;
+      }
+    };
+    int nreq = 0;
+    iz = z0;
+    setup1();
+#pragma unroll 1
+    while (iz < z1) {
+      const double kk = (double)L;
+      if (!(kk <= m_min || kk >= m_max || L == 0)) {
+        const double aL = fabs(kk);
+        const double zt_s = L > 0 ? zt : -zt, zb_s = L > 0 ? zb : -zb;
+        double f;
+        if (!cheap(aL, zb_s, f)) {
+          if (nreq < kRq) B->rq[nreq][lane] = zb_s * ga * frcp(aL);
+          ++nreq;
+        }
+        if (!cheap(aL, zt_s, f)) {
+          if (nreq < kRq) B->rq[nreq][lane] = zt_s * ga * frcp(aL);
+          ++nreq;
+        }
+      }
+      if (++L > Le) {
+        ++iz;
+        setup1();
+      }
+    }
+    // pass 2: the warp evaluates all listed faces
+    const int nl = nreq < kRq ? nreq : kRq;
+    int incl = nl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total > 0) {
+      B->roff[lane] = incl - nl;
+      __syncwarp();
+#pragma unroll 1
+      for (int f = lane; f < total; f += 32) {
+        int o = 0;
+#pragma unroll
+        for (int st = 16; st >= 1; st >>= 1)
+          if (o + st < 32 && B->roff[o + st] <= f) o += st;
+        const int k = f - B->roff[o];
+        B->rq[k][o] = group_raw(H, P, q, B->rq[k][o]);
+      }
+      __syncwarp();
+    }
+    // pass 3: the weights
+    int used = 0;
+    double prev = 0.0;
+    auto setup3 = [&]() {
+      for (; iz < z1; ++iz) {
+        zb = ((double)iz - hz) * vc;
+        zt = zb + vc;
+        m_min = zb * (zb >= 0.0 ? c_lo : c_hi);
+        m_max = zt * (zt <= 0.0 ? c_lo : c_hi);
+        const int fl = (int)floor(m_min);
+        k_lo = (fl < row_lo) ? row_lo : fl;
+        const int chi = (int)ceil(m_max) - 1;
+        const int k_hi = (chi < row_hi) ? chi : row_hi;
+        // unclamped lower end: above(k_lo) = w2d, the walk starts after it
+        const bool lo_free = fl >= row_lo;
+        prev = lo_free ? w2d : 0.0;
+        L = k_lo + (lo_free ? 1 : 0);
+        Le = k_hi + 1;
+        if (k_hi >= k_lo) return;
+      }
+    };
+    auto above = [&](int Lq) -> double {
+      const double kk = (double)Lq;
+      if (kk <= m_min) return w2d;
+      if (kk >= m_max) return 0.0;
+      if (Lq == 0) {
+        if (zb >= 0.0) return w2d;
+        if (zt <= 0.0) return 0.0;
+        return w2d * zt / (zt - zb);
+      }
+      const double aL = fabs(kk);
+      const double zt_s = Lq > 0 ? zt : -zt, zb_s = Lq > 0 ? zb : -zb;
+      double Fb = 0.0, Ft = 0.0;
+      bool need_b = !cheap(aL, zb_s, Fb), need_t = !cheap(aL, zt_s, Ft);
+      if (need_b || need_t) {
+        // one call site of the cubic path
+#pragma unroll 1
+        for (;;) {
+          double f;
+          const int k = used++;
+          if (k < nl) {
+            f = H.kappa * (aL * dz_sdd) * B->rq[k][lane];
+          } else {
+            const double zr = need_b ? zb_s : zt_s;
+            f = H.kappa * (aL * dz_sdd) * group_raw(H, P, q, zr * ga * frcp(aL));
+          }
+          if (need_b) {
+            Fb = f;
+            need_b = false;
+            if (!need_t) break;
+          } else {
+            Ft = f;
+            break;
+          }
+        }
+      }
+      return Lq > 0 ? Ft - Fb : w2d - (Fb - Ft);
+    };
+    iz = z0;
+    setup3();
+#pragma unroll 1
+    while (iz < z1) {
+      if (L > k_lo) pre(cell, L - 1);
+      const double cur = above(L);
+      if (L > k_lo) {
+        const double v = prev - cur;
+        if (v > kEpsWeight) emit(iz, cell, L - 1, v);
+      }
+      prev = cur;
+      if (++L > Le) {
+        ++iz;
+        setup3();
+      }
+    }
+    gend(cell);
+  }
+}
+
 }  // namespace fast
 }  // namespace ctsmb
