@@ -1077,7 +1077,7 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
 #define CTSM_KWS_F 2
 #endif
 #ifndef CTSM_BWD3_MINB_F
-#define CTSM_BWD3_MINB_F CTSM_BWD3_MINB
+#define CTSM_BWD3_MINB_F 7  // with the early row-vector loads: C3 bwd 45.9 -> 45.1 ms per half scan (8: 45.9, 6: 51.2, 9: 63.9)
 #endif
 // warps (orbits) per block and min blocks per SM of the fp64 / fp32 variants
 template <typename T>
