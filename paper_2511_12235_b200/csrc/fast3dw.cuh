@@ -882,6 +882,13 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
 // gend(cell) is called after the last weight of a cell group: the forward
 // flushes its pending row run there, so a run never crosses groups and its
 // detector cell is the group's (loop-invariant address arithmetic).
+#ifndef CTSM_FLAT_CUBIC2
+#define CTSM_FLAT_CUBIC2 0
+#endif
+__device__ __noinline__ double group_raw_ool(const ColumnHead& H, const PieceCoef* P, int q,
+                                             double G) {
+  return group_raw(H, P, q, G);
+}
 struct NoPre {
   __device__ __forceinline__ void operator()(int, int) const {}
 };
@@ -1032,6 +1039,21 @@ __device__ __forceinline__ void chunk_weights_flat(const DevGeom& g, const Colum
       const double zt_s = Lq > 0 ? zt : -zt, zb_s = Lq > 0 ? zb : -zb;
       double Fb = 0.0, Ft = 0.0;
       bool need_b = !cheap(aL, zb_s, Fb), need_t = !cheap(aL, zt_s, Ft);
+#if CTSM_FLAT_CUBIC2
+      if (need_b || need_t) {
+        // a listed face takes its value from the batch; a face beyond the
+        // lane's kRq slots (rare) goes through the out-of-line atom sum
+        const double kap = H.kappa * (aL * dz_sdd);
+        if (need_b) {
+          const int k = used++;
+          Fb = kap * (k < nl ? B->rq[k][lane] : group_raw_ool(H, P, q, zb_s * ga * frcp(aL)));
+        }
+        if (need_t) {
+          const int k = used++;
+          Ft = kap * (k < nl ? B->rq[k][lane] : group_raw_ool(H, P, q, zt_s * ga * frcp(aL)));
+        }
+      }
+#else
       if (need_b || need_t) {
         // one call site of the cubic path
 #pragma unroll 1
@@ -1054,6 +1076,7 @@ __device__ __forceinline__ void chunk_weights_flat(const DevGeom& g, const Colum
           }
         }
       }
+#endif
       return Lq > 0 ? Ft - Fb : w2d - (Fb - Ft);
     };
     iz = z0;
