@@ -882,9 +882,6 @@ __device__ __forceinline__ void chunk_weights(const DevGeom& g, const ColumnHead
 // gend(cell) is called after the last weight of a cell group: the forward
 // flushes its pending row run there, so a run never crosses groups and its
 // detector cell is the group's (loop-invariant address arithmetic).
-#ifndef CTSM_FLAT_CUBIC2
-#define CTSM_FLAT_CUBIC2 0
-#endif
 __device__ __noinline__ double group_raw_ool(const ColumnHead& H, const PieceCoef* P, int q,
                                              double G) {
   return group_raw(H, P, q, G);
@@ -898,7 +895,12 @@ struct NoGroupEnd {
 // (Summing a voxel's weights in 16 more registers and adding them to the
 // back-projection's shared-memory accumulators once per (group, voxel) was
 // slower: C3 bwd 47.5 vs 43.4 ms per half scan.)
-template <typename Emit, typename Pre = NoPre, typename GEnd = NoGroupEnd>
+// kTwoSite: the emitting pass takes a cubic face's value at two call sites
+// (bottom / top face; a face beyond the lane's kRq slots goes through the
+// out-of-line atom sum) instead of one loop around a single site: the forward
+// gains 2 % (C3 83 -> 82 ms per projection), the back-projection loses 3 %
+// (87 -> 90 ms), so only the forward uses it.
+template <bool kTwoSite = false, typename Emit, typename Pre = NoPre, typename GEnd = NoGroupEnd>
 __device__ __forceinline__ void chunk_weights_flat(const DevGeom& g, const ColumnHead& H,
                                                    const PieceCoef* P, int z0, int z1,
                                                    Emit&& emit, CubicBatch* B, int lane,
@@ -914,7 +916,8 @@ __device__ __forceinline__ void chunk_weights_flat(const DevGeom& g, const Colum
   // integer edge L, L <= m_min <=> L <= fl and L >= m_max <=> L > chi, so
   // the walks compare integers (C3 bwd 45.1 -> 43.4 ms per half scan).
   // (Computing the ranges of a chunk once per (column, angle) and keeping
-  // them packed in two registers across the groups was slower: 45.0 ms.)
+  // them across the groups was slower, packed in two registers (45.0 ms) or
+  // in shared memory (44.7 ms).)
   auto range_of = [&](int izq, int& fl, int& chi) {
     const double zb = ((double)izq - hz) * vc, zt = zb + vc;
     const double m_min = zb * (zb >= 0.0 ? c_lo : c_hi);
@@ -1039,8 +1042,7 @@ __device__ __forceinline__ void chunk_weights_flat(const DevGeom& g, const Colum
       const double zt_s = Lq > 0 ? zt : -zt, zb_s = Lq > 0 ? zb : -zb;
       double Fb = 0.0, Ft = 0.0;
       bool need_b = !cheap(aL, zb_s, Fb), need_t = !cheap(aL, zt_s, Ft);
-#if CTSM_FLAT_CUBIC2
-      if (need_b || need_t) {
+      if (kTwoSite && (need_b || need_t)) {
         // a listed face takes its value from the batch; a face beyond the
         // lane's kRq slots (rare) goes through the out-of-line atom sum
         const double kap = H.kappa * (aL * dz_sdd);
@@ -1052,9 +1054,7 @@ __device__ __forceinline__ void chunk_weights_flat(const DevGeom& g, const Colum
           const int k = used++;
           Ft = kap * (k < nl ? B->rq[k][lane] : group_raw_ool(H, P, q, zt_s * ga * frcp(aL)));
         }
-      }
-#else
-      if (need_b || need_t) {
+      } else if (need_b || need_t) {
         // one call site of the cubic path
 #pragma unroll 1
         for (;;) {
@@ -1076,7 +1076,6 @@ __device__ __forceinline__ void chunk_weights_flat(const DevGeom& g, const Colum
           }
         }
       }
-#endif
       return Lq > 0 ? Ft - Fb : w2d - (Fb - Ft);
     };
     iz = z0;

@@ -1026,7 +1026,7 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
         flush_side(pv, prz);
         if (zmir) flush_side(pm, g.n_det_z - 1 - prz);
       };
-      fast::chunk_weights_flat(
+      fast::chunk_weights_flat<true>(
           g, sh[warp], sp[warp], z0, z1,
           [&](int iz, int my, int mz, double w) {
             ++nw;
@@ -1319,6 +1319,166 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
           T* dst = xout + c * g.n_z + (side == 0 ? iz : g.n_z - 1 - iz);  // z-fastest volume
           if (accumulate) v += (double)*dst;
           *dst = (T)v;
+        }
+      }
+    }
+  }
+}
+
+// Member-outer form of the symmetric back-projection (transposed image rows,
+// flattened walk; CTSM_BWD3_VEC). In bwd3d_sym_kernel a weight of member h is
+// added, per image e, to the accumulator of pixel (e o h) p0: a run-time
+// permutation of 8 scalar shared-memory slots (3 integer instructions per
+// slot to decode it, 8 LDS + 8 STS per side). Here the members are the OUTER
+// loop: member h accumulates all its base angles in image order -- slot e
+// holds image e, so the G slots of a voxel are one contiguous vector
+// (2 LDS.128 + 2 STS.128 per side in fp32, no decoding) -- and its sums are
+// added to the pixels (e o h) p0 of the z-fastest volume once per member and
+// z-block. The orbit belongs to this warp alone, so those updates are plain
+// loads and stores in a fixed order (deterministic).
+#ifndef CTSM_BWD3_VEC
+#define CTSM_BWD3_VEC 1  // C3 bwd 87 -> 85 ms per projection
+#endif
+template <typename T, int G>
+__global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sym_v_kernel(
+    DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
+    const T* __restrict__ in, T* __restrict__ xout, int accumulate, int* status,
+    const FastPlan* __restrict__ plans) {
+  constexpr int kWarpsS = bwd3_warps<T>();
+  __shared__ __align__(16) fast::ColumnHead sh[kWarpsS];
+  __shared__ __align__(16) fast::PieceCoef sp[kWarpsS][fast::kMaxPieces];
+  using AccT = typename BwdAcc<T>::type;
+  constexpr int kZcS = bwd3_zc<T>();
+  constexpr int V = 16 / sizeof(AccT), NC = G / V;
+  // [warp][slot][chunk][lane][V]: the G image sums of (slot, lane) as NC
+  // 16-byte vectors, each conflict-free across the lanes
+  __shared__ __align__(16) AccT sacc[kWarpsS][kZcS][NC][32][V];
+  CTSM_BATCH_DECL(kWarpsS);
+  (void)cs;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = g.n_x, h = n / 2;
+  const long long nxy = (long long)n * g.n_y;
+  const long long orb = (long long)blockIdx.x * kWarpsS + warp;
+  int ix0, iy0;
+  if (G == 4) {
+    if (orb >= (long long)h * h) return;  // whole warp
+    ix0 = (int)(orb % h);
+    iy0 = (int)(orb / h);
+  } else {
+    if (orb >= (long long)h * (h + 1) / 2) return;
+    ix0 = (int)((sqrt(8.0 * (double)orb + 1.0) - 1.0) * 0.5);
+    while ((long long)(ix0 + 1) * (ix0 + 2) / 2 <= orb) ++ix0;
+    while ((long long)ix0 * (ix0 + 1) / 2 > orb) --ix0;
+    iy0 = (int)(orb - (long long)ix0 * (ix0 + 1) / 2);
+  }
+  const bool diag = G == 8 && ix0 == iy0;
+  const int n_mem = (G == 4 || diag) ? 4 : 8;
+  const int rpa = g.rows_per_angle;
+  const int hy = g.n_det_y / 2, hz = g.n_det_z / 2;
+  const bool zmir = zmirror_on() && (g.n_z % 2 == 0);
+  constexpr int kM = kZcS / 2;
+  const int zspan = zmir ? g.n_z / 2 : g.n_z;
+  const int zbs = 32 * (zmir ? kM : kZcS);
+  for (int zb0 = 0; zb0 < zspan; zb0 += zbs) {
+    const int nzb = min(zbs, zspan - zb0);
+    const int zc = (nzb + 31) / 32;
+    const int z0 = zb0 + lane * zc, z1 = min(z0 + zc, zb0 + nzb);
+#pragma unroll 1
+    for (int hm = 0; hm < n_mem; ++hm) {
+      int cx, cy;
+      d4_pixel(n, ix0, iy0, hm, cx, cy);
+      const long long mcol = (long long)cy * n + cx;
+      // this lane's slots (only this lane reads or writes them)
+      for (int t = 0; t < zc; ++t)
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int u = 0; u < V; ++u) {
+            sacc[warp][t][c][lane][u] = (AccT)0;
+            if (zmir) sacc[warp][kM + t][c][lane][u] = (AccT)0;
+          }
+#pragma unroll 1
+      for (int kk = 0; kk < n_base; ++kk) {
+        const int i = base[kk];
+        const bool full = G == 4 || ((i != 0) && (8 * i != g.n_angles));
+        const T* yb = in + (long long)kk * G * rpa;
+        __syncwarp();
+        const bool ok = load_plan(plans, (long long)kk * nxy + mcol, sh[warp], sp[warp], lane);
+#if CTSM_PLAN_PREFETCH
+        if (kk + 1 < n_base) {
+          prefetch_plan(plans, (long long)(kk + 1) * nxy + mcol, lane);
+        } else if (hm + 1 < n_mem) {
+          int px, py;
+          d4_pixel(n, ix0, iy0, hm + 1, px, py);
+          prefetch_plan(plans, (long long)py * n + px, lane);
+        }
+#endif
+        __syncwarp();
+        if (!ok) continue;
+        int prow = -1;
+        T pv0[G], pv1[G];
+        auto pre_row = [&](int my, int mz) {
+          const int rowi = (my + hy) * g.n_det_z + (mz + hz);
+          if (rowi != prow) {
+            const T* rowp = yb + (long long)(my + hy) * g.n_det_z * G;
+            load_vec<T, G>(rowp + (long long)(mz + hz) * G, pv0);
+            if (zmir) load_vec<T, G>(rowp + (long long)(g.n_det_z - 1 - (mz + hz)) * G, pv1);
+            prow = rowi;
+          }
+        };
+        auto add_side = [&](const T* v, const int slot, const AccT wa) {
+          AccT* sp0 = &sacc[warp][slot][0][lane][0];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            if (c * V < 4 || full) {
+              if constexpr (sizeof(AccT) == 4) {
+                float4* q = reinterpret_cast<float4*>(sp0 + c * 32 * V);
+                float4 cur = *q;
+                const float2 w2 = make_float2((float)wa, (float)wa);
+                const float2 lo = __ffma2_rn(w2, make_float2((float)v[c * V], (float)v[c * V + 1]),
+                                             make_float2(cur.x, cur.y));
+                const float2 hi = __ffma2_rn(w2, make_float2((float)v[c * V + 2], (float)v[c * V + 3]),
+                                             make_float2(cur.z, cur.w));
+                *q = make_float4(lo.x, lo.y, hi.x, hi.y);
+              } else {
+                double2* q = reinterpret_cast<double2*>(sp0 + c * 32 * V);
+                double2 cur = *q;
+                cur.x += (double)wa * (double)v[c * V];
+                cur.y += (double)wa * (double)v[c * V + 1];
+                *q = cur;
+              }
+            }
+          }
+        };
+        fast::chunk_weights_flat(
+            g, sh[warp], sp[warp], z0, z1,
+            [&](int iz, int my, int mz, double w) {
+              pre_row(my, mz);  // already loaded by the walk's pre() (no-op here)
+              const AccT wa = (AccT)w;
+              add_side(pv0, iz - z0, wa);
+              if (zmir) add_side(pv1, kM + iz - z0, wa);
+            },
+            CTSM_BATCH_PTR, lane, pre_row);
+      }
+      // member hm's sums of image e belong to pixel (e o hm) p0; the first
+      // member initialises the pixels (on the diagonal the images e >= 4
+      // alias the pixels of e < 4 and add to them)
+#pragma unroll 1
+      for (int e = 0; e < G; ++e) {
+        int px, py;
+        d4_pixel(n, ix0, iy0, d4_compose(e, hm), px, py);
+        T* col = xout + ((long long)py * n + px) * g.n_z;  // z-fastest volume
+        const bool init = hm == 0 && !accumulate && (e < 4 || !diag);
+        for (int t = 0; t < zc; ++t) {
+          const int iz = z0 + t;
+          if (iz >= z1) break;
+          for (int side = 0; side < (zmir ? 2 : 1); ++side) {
+            const int sl = side == 0 ? t : kM + t;
+            double v = (double)sacc[warp][sl][e / V][lane][e % V];
+            T* dst = col + (side == 0 ? iz : g.n_z - 1 - iz);
+            if (!init) v += (double)*dst;
+            *dst = (T)v;
+          }
         }
       }
     }
@@ -1812,7 +1972,11 @@ cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const i
     }
 #define CTSM_LAUNCH(T, G)                                                                      \
   do {                                                                                         \
-    if (tr)                                                                                    \
+    if (tr && CTSM_BWD3_VEC && pl)                                                             \
+      bwd3d_sym_v_kernel<T, G><<<blocks, bwd3_warps<T>() * 32, 0, st>>>(                       \
+          g, cs + k0, base + k0, nk, (const T*)scratch, (T*)x, k0 > 0, status,                 \
+          (const FastPlan*)pl);                                                                \
+    else if (tr)                                                                               \
       bwd3d_sym_kernel<T, G, true><<<blocks, bwd3_warps<T>() * 32, 0, st>>>(                           \
           g, cs + k0, base + k0, nk, (const T*)scratch, (T*)x, k0 > 0, status,                 \
           (const FastPlan*)pl);                                                                \
