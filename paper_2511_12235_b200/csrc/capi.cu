@@ -1060,7 +1060,8 @@ static int bwd_sym_impl(ctsm_ctx* ctx, const ctsm_geometry* g, const DevGeom& d,
     const size_t ne = bwd3d_scratch_elems(d, symmetry_order(g), dtype);
     if (!ne) ctx->last_path &= ~CTSM_PATH_ZMIRROR;  // the plain-gather variant has no mirror
     if (ne) CT_TRY(ensure(ctx, ctx->bwd_t, ne * (dtype == CTSM_F64 ? 8 : 4)));
-    CT_TRY(ensure(ctx, ctx->vol_t, (size_t)d.n_vox * (dtype == CTSM_F64 ? 8 : 4)));
+    // two partial volumes (the split symmetric back-projection, mf.cu)
+    CT_TRY(ensure(ctx, ctx->vol_t, 2 * (size_t)d.n_vox * (dtype == CTSM_F64 ? 8 : 4)));
     CT_TRY(ensure(ctx, ctx->mfplans, mf3d_plan_bytes(d, symmetry_order(g))));
     CT_CUDA(bwd3d_mf_sym(d, dtype, (const AngleCS*)ctx->cs.p, (const int*)ctx->base.p, nb, y, x,
                          ctx->status, st, symmetry_order(g), ne ? ctx->bwd_t.p : nullptr,

@@ -204,6 +204,10 @@ __device__ __forceinline__ const fast::GroupTable* table3d(const fast::ColumnHea
 #define CTSM_BWD3_EARLY_LOAD 1  // C3 bwd 97 -> 92 ms per projection
 #endif
 // flattened walk of the forward: row runs flushed at the end of their cell group
+// fp32 forward without row runs (every weight reduced to memory directly)
+#ifndef CTSM_FWD3_DIRECT
+#define CTSM_FWD3_DIRECT 0
+#endif
 #ifndef CTSM_FWD3_GEND
 #define CTSM_FWD3_GEND 1  // C3 fwd 85 -> 83 ms per projection
 #endif
@@ -1016,6 +1020,36 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
       };
 #if CTSM_FLAT && !defined(CTSM_NO_BATCH) && !defined(CTSM_TABLE3D)
       (void)TB;
+#if CTSM_FWD3_DIRECT
+      if constexpr (FA && sizeof(T) == 4) {
+        // no row runs: every weight goes straight to the interleaved rows (two
+        // vector reductions per side), no pending sums, no flush branch
+        fast::chunk_weights_flat<true>(
+            g, sh[warp], sp[warp], z0, z1,
+            [&](int iz, int my, int mz, double w) {
+              ++nw;
+              const float wf = (float)w;
+              const int rz = mz + hz;
+              float* cellp = yt + (unsigned)(((kk * ndy + (my + hy)) * g.n_det_z) * G);
+              auto side = [&](const int slot, const int row) {
+                const float4* xv = reinterpret_cast<const float4*>(xsm + xidx(slot, 0, lane));
+                float* dst = cellp + row * G;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                  const float4 q = xv[c * 32];
+                  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * c),
+                               "f"(wf * q.x), "f"(wf * q.y), "f"(wf * q.z), "f"(wf * q.w)
+                               : "memory");
+                }
+              };
+              side(iz - z0, rz);
+              if (zmir) side(kMF + iz - z0, g.n_det_z - 1 - rz);
+            },
+            CTSM_BATCH_PTR, lane);
+        pr = -1;
+      } else
+#endif
+      {
 #if CTSM_FWD3_GEND
       // runs end with their cell group: the pending run's cell is the group's
       // (py is loop-invariant in the walk; the flush address is rz * G off a
@@ -1048,6 +1082,7 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
 #else
       fast::chunk_weights_flat(g, sh[warp], sp[warp], z0, z1, on_weight, CTSM_BATCH_PTR, lane);
 #endif
+      }
 #else
       fast::chunk_weights(g, sh[warp], sp[warp], z0, z1, on_weight, TB, CTSM_BATCH_PTR, lane);
 #endif
@@ -1132,14 +1167,16 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
 #endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = g.n_x, h = n / 2;
+  // (dispatching the orbits from the centre of the grid outwards, most work
+  // first, changed nothing: 85 vs 85 ms)
+  const long long n_orb = G == 4 ? (long long)h * h : (long long)h * (h + 1) / 2;
   const long long orb = (long long)blockIdx.x * kWarpsS + warp;
+  if (orb >= n_orb) return;  // whole warp
   int ix0, iy0;
   if (G == 4) {
-    if (orb >= (long long)h * h) return;  // whole warp
     ix0 = (int)(orb % h);
     iy0 = (int)(orb / h);
   } else {
-    if (orb >= (long long)h * (h + 1) / 2) return;
     ix0 = (int)((sqrt(8.0 * (double)orb + 1.0) - 1.0) * 0.5);
     while ((long long)(ix0 + 1) * (ix0 + 2) / 2 <= orb) ++ix0;
     while ((long long)ix0 * (ix0 + 1) / 2 > orb) --ix0;
@@ -1339,6 +1376,9 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
 #ifndef CTSM_BWD3_VEC
 #define CTSM_BWD3_VEC 1  // C3 bwd 87 -> 85 ms per projection
 #endif
+#ifndef CTSM_BWD3_SPLIT
+#define CTSM_BWD3_SPLIT 1  // C3 bwd 86 -> 79 ms per projection
+#endif
 template <typename T, int G>
 __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sym_v_kernel(
     DevGeom g, const AngleCS* __restrict__ cs, const int* __restrict__ base, int n_base,
@@ -1358,14 +1398,25 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = g.n_x, h = n / 2;
   const long long nxy = (long long)n * g.n_y;
+  // CTSM_BWD3_SPLIT: an orbit is shared by the block's two warps, warp w
+  // taking half of the members and folding into its own partial volume
+  // (xout + w * n_vox; the host adds the two while transposing). A C3 launch
+  // is 8,256 orbits on 16 resident warps x 148 SMs = 3.49 rounds, i.e. 4 with
+  // the last one half empty (occupancy 14 of 16 warps, ncu); split, it is
+  // 6.97 rounds of half-length units.
+  const long long n_orb = G == 4 ? (long long)h * h : (long long)h * (h + 1) / 2;
+#if CTSM_BWD3_SPLIT
+  static_assert(kWarpsS == 2, "a warp pair per orbit");
+  const long long orb = (long long)blockIdx.x;
+#else
   const long long orb = (long long)blockIdx.x * kWarpsS + warp;
+#endif
+  if (orb >= n_orb) return;  // whole warp
   int ix0, iy0;
   if (G == 4) {
-    if (orb >= (long long)h * h) return;  // whole warp
     ix0 = (int)(orb % h);
     iy0 = (int)(orb / h);
   } else {
-    if (orb >= (long long)h * (h + 1) / 2) return;
     ix0 = (int)((sqrt(8.0 * (double)orb + 1.0) - 1.0) * 0.5);
     while ((long long)(ix0 + 1) * (ix0 + 2) / 2 <= orb) ++ix0;
     while ((long long)ix0 * (ix0 + 1) / 2 > orb) --ix0;
@@ -1383,8 +1434,15 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
     const int nzb = min(zbs, zspan - zb0);
     const int zc = (nzb + 31) / 32;
     const int z0 = zb0 + lane * zc, z1 = min(z0 + zc, zb0 + nzb);
+#if CTSM_BWD3_SPLIT
+    const int m_lo = warp * (n_mem / 2), m_hi = m_lo + n_mem / 2;
+    T* const xw = xout + (long long)warp * g.n_vox;
+#else
+    const int m_lo = 0, m_hi = n_mem;
+    T* const xw = xout;
+#endif
 #pragma unroll 1
-    for (int hm = 0; hm < n_mem; ++hm) {
+    for (int hm = m_lo; hm < m_hi; ++hm) {
       int cx, cy;
       d4_pixel(n, ix0, iy0, hm, cx, cy);
       const long long mcol = (long long)cy * n + cx;
@@ -1407,7 +1465,7 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
 #if CTSM_PLAN_PREFETCH
         if (kk + 1 < n_base) {
           prefetch_plan(plans, (long long)(kk + 1) * nxy + mcol, lane);
-        } else if (hm + 1 < n_mem) {
+        } else if (hm + 1 < m_hi) {
           int px, py;
           d4_pixel(n, ix0, iy0, hm + 1, px, py);
           prefetch_plan(plans, (long long)py * n + px, lane);
@@ -1453,7 +1511,9 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
         fast::chunk_weights_flat(
             g, sh[warp], sp[warp], z0, z1,
             [&](int iz, int my, int mz, double w) {
+#if !CTSM_BWD3_NOPRECHK
               pre_row(my, mz);  // already loaded by the walk's pre() (no-op here)
+#endif
               const AccT wa = (AccT)w;
               add_side(pv0, iz - z0, wa);
               if (zmir) add_side(pv1, kM + iz - z0, wa);
@@ -1467,8 +1527,8 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
       for (int e = 0; e < G; ++e) {
         int px, py;
         d4_pixel(n, ix0, iy0, d4_compose(e, hm), px, py);
-        T* col = xout + ((long long)py * n + px) * g.n_z;  // z-fastest volume
-        const bool init = hm == 0 && !accumulate && (e < 4 || !diag);
+        T* col = xw + ((long long)py * n + px) * g.n_z;  // z-fastest (partial) volume
+        const bool init = hm == m_lo && !accumulate && (e < 4 || !diag);
         for (int t = 0; t < zc; ++t) {
           const int iz = z0 + t;
           if (iz >= z1) break;
@@ -1758,6 +1818,38 @@ __global__ void transpose2d_kernel(const T* __restrict__ in, T* __restrict__ out
   }
 }
 
+// out[c][r] = in[r][c] + in2[r][c] (the two partial volumes of the split
+// back-projection), summed in fp64
+template <typename T>
+__global__ void transpose2d_add_kernel(const T* __restrict__ in, const T* __restrict__ in2,
+                                       T* __restrict__ out, long long rows, long long cols) {
+  __shared__ T tile[32][33];
+  const long long c0 = (long long)blockIdx.x * 32, r0 = (long long)blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const long long r = r0 + j, c = c0 + threadIdx.x;
+    if (r < rows && c < cols)
+      tile[j][threadIdx.x] = (T)((double)in[r * cols + c] + (double)in2[r * cols + c]);
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const long long c = c0 + j, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][j];
+  }
+}
+
+static cudaError_t transpose2d_add(int dtype, const void* in, const void* in2, void* out,
+                                   long long rows, long long cols, cudaStream_t st) {
+  const dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  if (dtype == CTSM_F64)
+    transpose2d_add_kernel<double><<<grid, dim3(32, 8), 0, st>>>(
+        (const double*)in, (const double*)in2, (double*)out, rows, cols);
+  else
+    transpose2d_add_kernel<float><<<grid, dim3(32, 8), 0, st>>>(
+        (const float*)in, (const float*)in2, (float*)out, rows, cols);
+  count_launch();
+  return cudaGetLastError();
+}
+
 static cudaError_t transpose2d(int dtype, const void* in, void* out, long long rows,
                                long long cols, cudaStream_t st) {
   const dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
@@ -1951,6 +2043,9 @@ cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const i
   const unsigned blocks = (unsigned)((n_orb + kWS - 1) / kWS);
   const int chunk = sym3d_chunk(g, order, dtype == CTSM_F64 ? 8 : 4);
   const bool tr = scratch != nullptr && n_base > 0;
+  // split back-projection: a block per orbit, two partial volumes in vol_t
+  const bool split = CTSM_BWD3_SPLIT && CTSM_BWD3_VEC && tr && plans != nullptr;
+  const unsigned vblocks = split ? (unsigned)n_orb : blocks;
   // chunks accumulate into x in ascending order (deterministic)
   for (int k0 = 0; k0 < (n_base > 0 ? n_base : 1); k0 += chunk) {
     const int nk = n_base - k0 < chunk ? n_base - k0 : chunk;
@@ -1973,7 +2068,7 @@ cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const i
 #define CTSM_LAUNCH(T, G)                                                                      \
   do {                                                                                         \
     if (tr && CTSM_BWD3_VEC && pl)                                                             \
-      bwd3d_sym_v_kernel<T, G><<<blocks, bwd3_warps<T>() * 32, 0, st>>>(                       \
+      bwd3d_sym_v_kernel<T, G><<<vblocks, bwd3_warps<T>() * 32, 0, st>>>(                      \
           g, cs + k0, base + k0, nk, (const T*)scratch, (T*)x, k0 > 0, status,                 \
           (const FastPlan*)pl);                                                                \
     else if (tr)                                                                               \
@@ -1992,6 +2087,10 @@ cudaError_t bwd3d_mf_sym(const DevGeom& g, int dtype, const AngleCS* cs, const i
 #undef CTSM_LAUNCH
     count_launch();
   }
+  if (split)
+    return transpose2d_add(dtype, vol_t,
+                           (const char*)vol_t + (size_t)g.n_vox * (dtype == CTSM_F64 ? 8 : 4), x_out,
+                           (long long)g.n_x * g.n_y, g.n_z, st);
   return transpose2d(dtype, vol_t, x_out, (long long)g.n_x * g.n_y, g.n_z, st);
 }
 
