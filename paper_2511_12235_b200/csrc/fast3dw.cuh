@@ -1043,9 +1043,6 @@ __device__ __forceinline__ void chunk_weights_flat(const DevGeom& g, const Colum
     };
     auto above = [&](int Lq) -> double {
       const double kk = (double)Lq;
-#if !CTSM_FLAT_NOLOCHK
-      if (Lq <= vfl) return w2d;
-#endif
       // (Lq > vfl always holds in this walk: it starts above floor(m_min))
       if (Lq > vchi) return 0.0;
       if (Lq == 0) {

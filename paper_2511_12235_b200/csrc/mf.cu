@@ -204,10 +204,10 @@ __device__ __forceinline__ const fast::GroupTable* table3d(const fast::ColumnHea
 #define CTSM_BWD3_EARLY_LOAD 1  // C3 bwd 97 -> 92 ms per projection
 #endif
 // flattened walk of the forward: row runs flushed at the end of their cell group
-// fp32 forward without row runs (every weight reduced to memory directly)
-#ifndef CTSM_FWD3_DIRECT
-#define CTSM_FWD3_DIRECT 0
-#endif
+// (An fp32 forward without row runs -- every weight reduced to memory
+// directly, no pending sums, no flush branch, 16 registers fewer -- issues 1.3x
+// the vector reductions and is 26 % slower, 99 vs 78 ms per projection: the
+// forward runs close to the SM's global-reduction throughput.)
 #ifndef CTSM_FWD3_GEND
 #define CTSM_FWD3_GEND 1  // C3 fwd 85 -> 83 ms per projection
 #endif
@@ -1020,35 +1020,6 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
       };
 #if CTSM_FLAT && !defined(CTSM_NO_BATCH) && !defined(CTSM_TABLE3D)
       (void)TB;
-#if CTSM_FWD3_DIRECT
-      if constexpr (FA && sizeof(T) == 4) {
-        // no row runs: every weight goes straight to the interleaved rows (two
-        // vector reductions per side), no pending sums, no flush branch
-        fast::chunk_weights_flat<true>(
-            g, sh[warp], sp[warp], z0, z1,
-            [&](int iz, int my, int mz, double w) {
-              ++nw;
-              const float wf = (float)w;
-              const int rz = mz + hz;
-              float* cellp = yt + (unsigned)(((kk * ndy + (my + hy)) * g.n_det_z) * G);
-              auto side = [&](const int slot, const int row) {
-                const float4* xv = reinterpret_cast<const float4*>(xsm + xidx(slot, 0, lane));
-                float* dst = cellp + row * G;
-#pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                  const float4 q = xv[c * 32];
-                  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * c),
-                               "f"(wf * q.x), "f"(wf * q.y), "f"(wf * q.z), "f"(wf * q.w)
-                               : "memory");
-                }
-              };
-              side(iz - z0, rz);
-              if (zmir) side(kMF + iz - z0, g.n_det_z - 1 - rz);
-            },
-            CTSM_BATCH_PTR, lane);
-        pr = -1;
-      } else
-#endif
       {
 #if CTSM_FWD3_GEND
       // runs end with their cell group: the pending run's cell is the group's
@@ -1511,9 +1482,7 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
         fast::chunk_weights_flat(
             g, sh[warp], sp[warp], z0, z1,
             [&](int iz, int my, int mz, double w) {
-#if !CTSM_BWD3_NOPRECHK
-              pre_row(my, mz);  // already loaded by the walk's pre() (no-op here)
-#endif
+              // (pv0 / pv1 hold this row: the walk's pre() precedes every emit)
               const AccT wa = (AccT)w;
               add_side(pv0, iz - z0, wa);
               if (zmir) add_side(pv1, kM + iz - z0, wa);
