@@ -417,20 +417,35 @@ def fp64_roofline(torch, g, cfg, dtype, world, ms_f, ms_b):
         kname = kname.replace("2d", "3d")
     # DRAM traffic and pipe utilisation of the same kernel and workload from one
     # committed `ncu --set full` capture (profiles/ncu_kernels.json)
-    traffic = ncu_pipe = ncu_ms = None
+    traffic = ncu_pipe = ncu_ms = ncu_red = None
     try:
         ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_kernels.json")))
         tname = "double" if dtype == "f64" else "float"
         kbase = kname.replace("3d_d8", "3d_sym")
         prefix = f"{cfg}_{dtype}:{kbase}_kernel<{tname}"
-        hits = [k for k in sorted(ncu) if k == prefix + ">" or k.startswith(prefix + ",")]
+        # (the 3D back-projection runs as bwd3d_sym_v_kernel)
+        prefixes = (prefix, f"{cfg}_{dtype}:{kbase}_v_kernel<{tname}")
+        hits = [k for k in sorted(ncu)
+                if any(k == p + ">" or k.startswith(p + ",") for p in prefixes)]
         if hits:
-            traffic = ncu[hits[0]]["dram_bytes"]
-            ncu_pipe = ncu[hits[0]].get("fp64_pipe_pct")
-            ncu_ms = ncu[hits[0]].get("duration_ms")
+            e = ncu[hits[-1]]
+            traffic = e["dram_bytes"]
+            ncu_pipe = e.get("fp64_pipe_pct")
+            ncu_ms = e.get("duration_ms")
+            if e.get("global_red_warp_insts") and e.get("sm_cycles"):
+                # the fp32 3D forward leaves through 16-byte vector reductions;
+                # tools/micro/red_bench.cu measures what an SM sustains
+                lane_ops = e["global_red_warp_insts"] * e.get("active_lanes", 32.0)
+                ncu_red = {"lane_reductions_per_clk_sm": lane_ops / 148.0 / e["sm_cycles"],
+                           "microbench_peak_per_clk_sm": [0.47, 0.65],
+                           "note": "16-byte red.global.add.v4.f32 per lane; the peak is the "
+                                   "two-reductions-per-32-byte-segment microbenchmark, lanes 5 rows "
+                                   "apart / adjacent (profiles/r3l_red_bench.log); upper estimate: "
+                                   "the kernel's average active lanes applied to its reductions"}
     except (OSError, ValueError, KeyError):
         pass
-    return {"bound": "fp64", "kernel": kname, "achieved": achieved, "peak": peak_ops,
+    extra = {"ncu_global_reductions": ncu_red} if ncu_red else {}
+    return {**extra, "bound": "fp64", "kernel": kname, "achieved": achieved, "peak": peak_ops,
             "unit": "T FP64 op/s (arithmetic instructions, FMA = 1 op; SURVEY.md §8(d))",
             "frac": (achieved / peak_ops) if peak_ops else None,
             "frac_flops_convention": (achieved / peak_flops) if peak_flops else None,

@@ -22,9 +22,12 @@ METRICS = {
     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
     "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
     "sm__warps_active.avg.pct_of_peak_sustained_active": "occupancy_pct",
+    "smsp__inst_executed_op_global_red.sum": "global_red_warp_insts",
+    "smsp__thread_inst_executed_per_inst_executed.ratio": "active_lanes",
+    "sm__cycles_elapsed.max": "sm_cycles",
 }
 SCALE = {"ms": 1.0, "us": 1e-3, "ns": 1e-6, "s": 1e3, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6,
-         "Gbyte": 1e9, "%": 1.0}
+         "Gbyte": 1e9, "%": 1.0, "inst": 1.0, "cycle": 1.0}
 
 
 def main():
