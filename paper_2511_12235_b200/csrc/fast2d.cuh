@@ -25,10 +25,6 @@
 #pragma once
 #include "common.cuh"
 
-#ifndef CTSM_CA_BF
-#define CTSM_CA_BF 0
-#endif
-
 namespace ctsmb {
 namespace fast {
 
@@ -245,23 +241,8 @@ __device__ __forceinline__ bool pixel_weights(const DevGeom& g, double C, double
   const double ipT2 = d23 > 0.0 ? p_inv(T2) : 0.0;
   const double bandT = d23 > 0.0 ? w.band_k * d23 * ipT2 * p_inv(T3) : 0.0;
   const double base2 = A1T2 + bandT + A4T3;  // CA(T4) (== 1 up to rounding)
-#if CTSM_CA_BF
-  // branch-free form: the three zones share one reciprocal (of |d1 d2| in
-  // the corner triangles, of |d1| or |d2| in the band) and differ in an
-  // additive constant and a factor picked by selects -- the lanes of a warp
-  // sit in different zones, so the branches ran one after the other
-  auto CA = [&](double t) -> double {
-    const double d1 = C + t * S, d2 = t * C - S;
-    const bool z0 = t <= T2, z1 = !z0 && t < T3;
-    const double den = fabs(z1 ? (bv ? d1 : d2) : d1 * d2);
-    const double r = den > kEpsAngle ? frcp(den) : 0.0;
-    double d = z0 ? t - T1 : T4 - t;
-    d = d > 0.0 ? d : 0.0;
-    const double tri = (z0 ? w.K1 : w.K4) * d * d * r;
-    const double band = w.band_k * (t - T2) * ipT2 * r;
-    return z1 ? A1T2 + band : (z0 ? tri : base2 - tri);
-  };
-#else
+  // (a branch-free form -- one shared reciprocal, the zone's constant and
+  // factor picked by selects -- was neutral: C1 1.705 vs 1.710 ms per step)
   auto CA = [&](double t) -> double {
     if (t <= T2) {
       const double d = t - T1;
@@ -271,7 +252,6 @@ __device__ __forceinline__ bool pixel_weights(const DevGeom& g, double C, double
     const double d = T4 - t;
     return base2 - (d > 0.0 ? w.K4 * d * d * pq_inv(t) : 0.0);
   };
-#endif
   const double scale = g.u_scale;
   const double inv_scale = g.t_scale;
   // |t| * scale is bounded by the edge-table extent (dev_geom), so 32-bit

@@ -265,6 +265,16 @@ __global__ void __launch_bounds__(128) plan3d_fast_kernel(DevGeom g, const Angle
                  : "memory");
 }
 
+// Plans are read once per z-block: streaming (evict-first) loads keep them
+// from displacing the forward's reduction rows in L2 (CTSM_PLAN_STREAM)
+#ifndef CTSM_PLAN_STREAM
+#define CTSM_PLAN_STREAM 1  // C3 bwd 74.2 -> 73.7 ms; an evict-last hint on the forward's reductions: no gain
+#endif
+#if CTSM_PLAN_STREAM
+#define CTSM_PLAN_LD(p) __ldcs(p)
+#else
+#define CTSM_PLAN_LD(p) __ldg(p)
+#endif
 // Loads the plan of (column, slot kk) into the warp's shared head / pieces.
 // Returns false for a column without work (failed sweep or no cell group).
 __device__ __forceinline__ bool load_plan(const FastPlan* __restrict__ plans, long long idx,
@@ -273,14 +283,14 @@ __device__ __forceinline__ bool load_plan(const FastPlan* __restrict__ plans, lo
   {
     const double2* s2 = reinterpret_cast<const double2*>(&src->H);
     double2* d2 = reinterpret_cast<double2*>(&H);
-    for (int i = lane; i < (int)(sizeof(fast::ColumnHead) / 16); i += 32) d2[i] = __ldg(&s2[i]);
+    for (int i = lane; i < (int)(sizeof(fast::ColumnHead) / 16); i += 32) d2[i] = CTSM_PLAN_LD(&s2[i]);
   }
   __syncwarp();
   const int np = H.np;
   {
     const double2* s2 = reinterpret_cast<const double2*>(src->P);
     double2* d2 = reinterpret_cast<double2*>(P);
-    for (int i = lane; i < np * (int)(sizeof(fast::PieceCoef) / 16); i += 32) d2[i] = __ldg(&s2[i]);
+    for (int i = lane; i < np * (int)(sizeof(fast::PieceCoef) / 16); i += 32) d2[i] = CTSM_PLAN_LD(&s2[i]);
   }
   return H.ng > 0;
 }
@@ -1484,6 +1494,7 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
             [&](int iz, int my, int mz, double w) {
               // (pv0 / pv1 hold this row: the walk's pre() precedes every emit)
               const AccT wa = (AccT)w;
+              // (loading both sides' vectors before updating either: no gain)
               add_side(pv0, iz - z0, wa);
               if (zmir) add_side(pv1, kM + iz - z0, wa);
             },

@@ -46,7 +46,8 @@ __global__ void __launch_bounds__(128) k(float* __restrict__ y, unsigned nseg, i
 }
 
 int main(int argc, char** argv) {
-  const unsigned nseg = 1u << 24;  // 512 MB of 32-byte segments
+  // 32-byte segments: 2^24 = 512 MB (default; mostly L2 misses), 2^21 = 64 MB (L2-resident)
+  const unsigned nseg = 1u << (argc > 2 ? atoi(argv[2]) : 24);
   const int iters = argc > 1 ? atoi(argv[1]) : 4096;
   float* y;
   cudaMalloc(&y, (size_t)nseg * 32);
