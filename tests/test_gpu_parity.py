@@ -225,6 +225,42 @@ def test_spmv_and_transpose(name, oracle_cr):
 
 
 # ---- K5/K6: matrix-free ---------------------------------------------------------
+@pytest.mark.parametrize("case", ["odd_nz", "two_zblocks", "quarter_odd_nz"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_symmetric_3d_shapes_vs_oracle(case, dtype, oracle_cr, monkeypatch):
+    """Symmetric 3D kernels against the oracle on the column shapes the
+    BASELINE configs do not reach: odd n_z (no z mirror: every voxel
+    evaluated, all accumulator slots on one side), a column longer than one
+    z-block (two passes over the plans), and the quarter-turn (order 4) form
+    of the member-outer back-projection."""
+    from paper_2511_12235_b200.projector import symmetry_order
+    base = TEST_GEOMETRIES["cone3d"].with_(n_angles=16)
+    if case == "odd_nz":
+        g = base.with_(n_z=5)
+    elif case == "two_zblocks":  # 300 voxels: mirror half 150 > 128 per z-block
+        g = base.with_(n_z=300, c=0.1)
+    else:
+        g = base.with_(n_z=7)
+        monkeypatch.setenv("CTSM_NO_DIHEDRAL", "1")
+    assert symmetry_order(g) == (4 if case == "quarter_odd_nz" else 8)
+    rng = np.random.default_rng(11)
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    tol = TOL64 if dtype == "f64" else TOL32
+    xt = torch.tensor(rng.uniform(0, 1, g.n_voxels), dtype=tdt, device="cuda")
+    yt = torch.tensor(rng.uniform(0, 1, g.n_measurements), dtype=tdt, device="cuda")
+    yg = forward_project_matrix_free(g, "consistent", 1, xt).double().cpu().numpy()
+    xg = back_project_matrix_free(g, "consistent", 1, yt).double().cpu().numpy()
+    yref = oracle_cr.forward_project_matrix_free(g, xt.double().cpu().numpy(), NTHREADS)
+    xref = oracle_cr.back_project_matrix_free(g, yt.double().cpu().numpy(), NTHREADS)
+    assert rel_err(yg, yref) <= tol
+    assert rel_err(xg, xref) <= tol
+    # repeated calls are bit-equal in fp64 (fixed point / fixed order)
+    if dtype == "f64":
+        yg2 = forward_project_matrix_free(g, "consistent", 1, xt).double().cpu().numpy()
+        xg2 = back_project_matrix_free(g, "consistent", 1, yt).double().cpu().numpy()
+        assert np.array_equal(yg, yg2) and np.array_equal(xg, xg2)
+
+
 @pytest.mark.parametrize("name", ["proj2d", "wide2d", "proj3d", "cone3d"])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_matrix_free_small(name, dtype, oracle_cr):
