@@ -1110,151 +1110,10 @@ __device__ __forceinline__ void chunk_weights_flat(const DevGeom& g, const Colum
   }
 }
 
-
-// chunk_weights_flat with the walks fused across cell groups: the row range
-// of a voxel does not depend on the group, so ONE walk emits the weights of
-// group w - 1 (pass 3) while it lists the cubic faces of group w (pass 1):
-// ng + 1 walks instead of 2 ng, the per-edge quantities (|L|, the face
-// heights' products with ga) shared by both duties, and two independent
-// dependent chains per trip. The batch's kRq slots are split into two halves
-// used alternately (group parity), so the values pass 3 reads are not
-// overwritten by the requests pass 1 lists; a lane's faces beyond its kRq / 2
-// slots go through the out-of-line atom sum. Per lane the evaluations, their
-// operands and the emission order are those of chunk_weights_flat.
-template <typename Emit, typename Pre = NoPre, typename GEnd = NoGroupEnd>
-__device__ __forceinline__ void chunk_weights_fused(const DevGeom& g, const ColumnHead& H,
-                                                    const PieceCoef* P, int z0, int z1,
-                                                    Emit&& emit, CubicBatch* B, int lane,
-                                                    Pre&& pre = NoPre(),
-                                                    GEnd&& gend = NoGroupEnd()) {
-  constexpr int kH = kRq / 2;
-  const int row_lo = -g.n_det_z / 2, row_hi = g.n_det_z / 2 - 1;
-  const double dz_sdd = g.dz_sdd, sdd_dz = g.sdd_dz;
-  const double c_mn = sdd_dz * H.dmin_inv, c_mx = sdd_dz * H.dmax_inv;
-  const double c_lo = fmin(c_mn, c_mx), c_hi = fmax(c_mn, c_mx);
-  const double ga = H.inv_a * sdd_dz;  // G = zref * ga / |L|
-  const double hz = g.n_z / 2.0, vc = g.c;
-  const int ng = H.ng;
-  int nl_e = 0;  // listed faces of the emitting group (previous walk)
-  for (int w = 0; w <= ng; ++w) {
-    const bool has_e = w > 0, has_l = w < ng;
-    const int qe = has_e ? w - 1 : 0, ql = has_l ? w : 0;
-    const int be = (qe & 1) * kH, bl = (ql & 1) * kH;
-    const double w2d = H.gw2d[qe];
-    const int cell = H.gcell[qe];
-    const double gmn_e = H.gmin[qe], gmx_e = H.gmax[qe];
-    const double l1 = H.kappa * H.galpha[qe] * ga * dz_sdd, l2 = H.kappa * H.gbeta[qe] * dz_sdd;
-    const double gmn_l = H.gmin[ql], gmx_l = H.gmax[ql];
-    int iz, L = 0, Le = -1, k_lo = 0, vchi = 0;
-    double zb = 0.0, zt = 0.0, prev = 0.0;
-    int nreq = 0, used = 0;
-    auto setup = [&]() {
-      for (; iz < z1; ++iz) {
-        const double zb0 = ((double)iz - hz) * vc, zt0 = zb0 + vc;
-        const double m_min = zb0 * (zb0 >= 0.0 ? c_lo : c_hi);
-        const double m_max = zt0 * (zt0 <= 0.0 ? c_lo : c_hi);
-        const int vfl = (int)floor(m_min);
-        vchi = (int)ceil(m_max) - 1;
-        k_lo = (vfl < row_lo) ? row_lo : vfl;
-        const int k_hi = (vchi < row_hi) ? vchi : row_hi;
-        const bool lo_free = vfl >= row_lo;
-        prev = lo_free ? w2d : 0.0;
-        L = k_lo + (lo_free ? 1 : 0);
-        Le = k_hi + 1;
-        if (k_hi >= k_lo) {
-          zb = zb0;
-          zt = zt0;
-          return;
-        }
-      }
-    };
-    iz = z0;
-    setup();
-#pragma unroll 1
-    while (iz < z1) {
-      if (has_e && L > k_lo) pre(cell, L - 1);
-      double cur;
-      if (L > vchi) {
-        cur = 0.0;  // at or above ceil(m_max): nothing above the edge, nothing to list
-      } else if (L == 0) {
-        cur = zb >= 0.0 ? w2d : (zt <= 0.0 ? 0.0 : w2d * zt / (zt - zb));
-      } else {
-        const double aL = fabs((double)L);
-        const double zt_s = L > 0 ? zt : -zt, zb_s = L > 0 ? zb : -zb;
-        const double ub = zb_s * ga, ut = zt_s * ga;
-        if (has_l) {
-          // pass 1 of group ql: the cubic faces (neither zero nor linear)
-          const double lo_l = gmn_l * aL, hi_l = gmx_l * aL;
-          if (!(ub <= lo_l || ub > hi_l)) {
-            if (nreq < kH) B->rq[bl + nreq][lane] = ub * frcp(aL);
-            ++nreq;
-          }
-          if (!(ut <= lo_l || ut > hi_l)) {
-            if (nreq < kH) B->rq[bl + nreq][lane] = ut * frcp(aL);
-            ++nreq;
-          }
-        }
-        // pass 3 of group qe
-        cur = 0.0;
-        if (has_e) {
-          const double lo_e = gmn_e * aL, hi_e = gmx_e * aL;
-          const bool zero_b = ub <= lo_e, zero_t = ut <= lo_e;
-          const bool need_b = !zero_b && !(ub > hi_e), need_t = !zero_t && !(ut > hi_e);
-          double Fb = zero_b ? 0.0 : l1 * zb_s - l2 * aL;
-          double Ft = zero_t ? 0.0 : l1 * zt_s - l2 * aL;
-          if (need_b || need_t) {
-            const double kap = H.kappa * (aL * dz_sdd);
-            if (need_b) {
-              const int k = used++;
-              Fb = kap * (k < nl_e ? B->rq[be + k][lane] : group_raw_ool(H, P, qe, ub * frcp(aL)));
-            }
-            if (need_t) {
-              const int k = used++;
-              Ft = kap * (k < nl_e ? B->rq[be + k][lane] : group_raw_ool(H, P, qe, ut * frcp(aL)));
-            }
-          }
-          cur = L > 0 ? Ft - Fb : w2d - (Fb - Ft);
-        }
-      }
-      if (has_e && L > k_lo) {
-        const double v = prev - cur;
-        if (v > kEpsWeight) emit(iz, cell, L - 1, v);
-      }
-      prev = cur;
-      if (++L > Le) {
-        ++iz;
-        setup();
-      }
-    }
-    if (has_e) gend(cell);
-    // pass 2 of group ql: the warp evaluates the listed faces in place
-    if (has_l) {
-      const int nl = nreq < kH ? nreq : kH;
-      int incl = nl;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      if (total > 0) {
-        B->roff[lane] = incl - nl;
-        __syncwarp();
-#pragma unroll 1
-        for (int f = lane; f < total; f += 32) {
-          int o = 0;
-#pragma unroll
-          for (int st = 16; st >= 1; st >>= 1)
-            if (o + st < 32 && B->roff[o + st] <= f) o += st;
-          const int k = f - B->roff[o];
-          B->rq[bl + k][o] = group_raw(H, P, ql, B->rq[bl + k][o]);
-        }
-        __syncwarp();
-      }
-      nl_e = nl;
-    }
-  }
-}
+// (A variant with the walks fused across cell groups -- one walk emitting
+// group w - 1 while listing the cubic faces of group w, ng + 1 walks instead
+// of 2 ng, the batch split into two halves -- was correct but slower: C3 fwd
+// 79 vs 78, bwd 77 vs 75 ms per projection, profiles/r3v_sweep3d.log.)
 
 }  // namespace fast
 }  // namespace ctsmb

@@ -208,10 +208,6 @@ __device__ __forceinline__ const fast::GroupTable* table3d(const fast::ColumnHea
 // directly, no pending sums, no flush branch, 16 registers fewer -- issues 1.3x
 // the vector reductions and is 26 % slower, 99 vs 78 ms per projection: the
 // forward runs close to the SM's global-reduction throughput.)
-// fused walks (fast3dw.cuh chunk_weights_fused): bit 0 forward, bit 1 back-projection
-#ifndef CTSM_FUSED
-#define CTSM_FUSED 0
-#endif
 #ifndef CTSM_FWD3_GEND
 #define CTSM_FWD3_GEND 1  // C3 fwd 85 -> 83 ms per projection
 #endif
@@ -1045,11 +1041,7 @@ __global__ void __launch_bounds__(kWarps3 * 32, fwd3_minb<T, G>()) fwd3d_sym_ker
         flush_side(pv, prz);
         if (zmir) flush_side(pm, g.n_det_z - 1 - prz);
       };
-#if CTSM_FUSED & 1
-      fast::chunk_weights_fused(
-#else
       fast::chunk_weights_flat<true>(
-#endif
           g, sh[warp], sp[warp], z0, z1,
           [&](int iz, int my, int mz, double w) {
             ++nw;
@@ -1497,11 +1489,7 @@ __global__ void __launch_bounds__(bwd3_warps<T>() * 32, bwd3_minb<T>()) bwd3d_sy
             }
           }
         };
-#if CTSM_FUSED & 2
-        fast::chunk_weights_fused(
-#else
         fast::chunk_weights_flat(
-#endif
             g, sh[warp], sp[warp], z0, z1,
             [&](int iz, int my, int mz, double w) {
               // (pv0 / pv1 hold this row: the walk's pre() precedes every emit)
