@@ -898,6 +898,34 @@ def run_csr(args):
         ev1.record()
         torch.cuda.synchronize()
         ms_spmvt += ev0.elapsed_time(ev1) / 5
+    # K4 as a gather over the CSC transpose (ctsm_csc_build), when the copy
+    # fits beside the CSR: same bits as the scatter (tests/test_gpu_parity.py)
+    ms_spmvt_csc = ms_csc_build = None
+    try:
+        from paper_2511_12235_b200.projector import build_transpose, drop_transpose
+        free_b, _tot = torch.cuda.mem_get_info()
+        if free_b > 1.15 * (12.0 * nnz + 8.0 * w.n_cols):
+            xs = back_project(w, yb)
+            ev0.record()
+            build_transpose(w)
+            ev1.record()
+            torch.cuda.synchronize()
+            ms_csc_build = ev0.elapsed_time(ev1)
+            for _ in range(3):
+                xc = back_project(w, yb)
+            assert torch.equal(xs, xc), "CSC back_project differs from the scatter"
+            del xs, xc
+            torch.cuda.synchronize()
+            ms_spmvt_csc = 0.0
+            for _ in range(5):
+                ev0.record()
+                back_project(w, yb)
+                ev1.record()
+                torch.cuda.synchronize()
+                ms_spmvt_csc += ev0.elapsed_time(ev1) / 5
+            drop_transpose(w)
+    except torch.cuda.OutOfMemoryError:
+        ms_spmvt_csc = None
     clk = clocks.stop()
     bytes_spmv = 12.0 * nnz + 16.0 * w.n_rows + 8.0 * w.n_cols
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -948,6 +976,12 @@ def run_csr(args):
                    "frac": bytes_spmv / (ms_spmvt * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
                    "note": "back_project: int64 fixed-point scatter (deterministic) with the matrix's "
                            "column-sum bound, computed once per matrix (cached, outside the timed calls)"},
+        "spmv_t_csc": None if ms_spmvt_csc is None else {
+            "ms": ms_spmvt_csc, "GB/s": bytes_spmv / (ms_spmvt_csc * 1e-3) / 1e9,
+            "frac": bytes_spmv / (ms_spmvt_csc * 1e-3) / 1e9 / peaks.get("hbm_gbs", 6650.0),
+            "transpose_build_ms": ms_csc_build,
+            "note": "back_project as a gather over a CSC transpose kept beside the CSR "
+                    "(build_transpose; bit-identical to the scatter, checked in this run)"},
         "e2e": e2e,
         "gpu_launches": int(launches), "clocks": clk,
     }

@@ -149,6 +149,20 @@ int ctsm_spmv_t_bound(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols,
                       const double* val_dev, double colsum_max, const double* y_dev,
                       double* x_dev, void* stream);
 
+/* K4 as a gather: the CSC transpose of a device CSR (col_start u64[n_cols+1],
+ * row u32[nnz], val f64[nnz], caller-allocated; the entries of a column come
+ * in schedule order) and back_project through it (projector.cpp:219-233). It
+ * sums the same fixed-point integers as ctsm_spmv_t_bound, so the two agree
+ * bit for bit; it reads every entry once instead of issuing one 64-bit
+ * reduction per entry. n_rows must be < 2^32. */
+int ctsm_csc_build(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols,
+                   const uint64_t* row_start_dev, const uint32_t* col_dev, const double* val_dev,
+                   uint64_t* col_start_dev, uint32_t* row_dev, double* valt_dev, void* stream);
+int ctsm_spmv_t_csc(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols,
+                    const uint64_t* col_start_dev, const uint32_t* row_dev,
+                    const double* valt_dev, double colsum_max, const double* y_dev,
+                    double* x_dev, void* stream);
+
 /* ---- K5/K6: matrix-free projectors (forward_project_matrix_free,
  * projector.hpp:56-59; back_project_matrix_free is the rebuild's addition).
  * The angle shard is {angle_begin + k * angle_step < angle_end}. Forward

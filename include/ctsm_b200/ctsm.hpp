@@ -190,6 +190,11 @@ class DeviceSystemMatrix {
   const std::string& meta() const;
   SparseSystemMatrix download() const;
   void scale_values(double factor);
+  // keeps a CSC transpose beside the CSR (the CSR's col / val bytes again):
+  // back_project(*this, y) then gathers instead of scattering, same bits;
+  // scale_values drops it
+  void build_transpose();
+  bool has_transpose() const;
   struct Impl;
   const Impl& impl() const { return *impl_; }
 

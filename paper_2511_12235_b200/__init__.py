@@ -14,6 +14,8 @@ from .projector import (  # noqa: F401
     back_project,
     back_project_matrix_free,
     build_system_matrix,
+    build_transpose,
+    drop_transpose,
     forward_project,
     forward_project_matrix_free,
     matrix_mode_name,

@@ -67,6 +67,8 @@ SIGNATURES = {
     "ctsm_spmv_t": (_I, [_P, _U64, _U64, _P, _P, _P, _P, _P, _P]),
     "ctsm_csr_colsum_max": (_I, [_P, _U64, _U64, _P, _P, _P, ctypes.POINTER(_D), _P]),
     "ctsm_spmv_t_bound": (_I, [_P, _U64, _U64, _P, _P, _P, _D, _P, _P, _P]),
+    "ctsm_csc_build": (_I, [_P, _U64, _U64, _P, _P, _P, _P, _P, _P, _P]),
+    "ctsm_spmv_t_csc": (_I, [_P, _U64, _U64, _P, _P, _P, _D, _P, _P, _P]),
     "ctsm_fwd_mf": (_I, [_P, _GP, _I, _I, _I, _I, _P, _P, _P]),
     "ctsm_bwd_mf": (_I, [_P, _GP, _I, _I, _I, _I, _P, _P, _P]),
     "ctsm_last_update_count": (_U64, [_P]),

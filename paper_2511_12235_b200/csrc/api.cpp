@@ -612,6 +612,12 @@ struct DeviceSystemMatrix::Impl {
   DevBuf<std::uint64_t> rs{0};
   DevBuf<std::uint32_t> col{0};
   DevBuf<double> val{0};
+  // CSC transpose (build_transpose) and the column-sum bound of K4
+  bool csc = false;
+  double colsum_max = 0.0;
+  DevBuf<std::uint64_t> cs{0};
+  DevBuf<std::uint32_t> trow{0};
+  DevBuf<double> tval{0};
   ctsm_operator op() const {
     ctsm_operator o{};
     o.kind = CTSM_OP_CSR;
@@ -680,7 +686,25 @@ SparseSystemMatrix DeviceSystemMatrix::download() const {
 void DeviceSystemMatrix::scale_values(double factor) {
   if (!std::isfinite(factor)) throw Error(ErrorCode::NonFinite, "scale factor must be finite");
   check(ctsm_scale_values(ctx(), impl_->nnz, impl_->val.p, factor, nullptr));
+  impl_->csc = false;  // the transpose held the old values
+  impl_->cs.reset(0);
+  impl_->trow.reset(0);
+  impl_->tval.reset(0);
 }
+
+void DeviceSystemMatrix::build_transpose() {
+  Impl& m = *impl_;
+  m.cs.reset(m.n_cols + 1);
+  m.trow.reset(m.nnz);
+  m.tval.reset(m.nnz);
+  check(ctsm_csc_build(ctx(), m.n_rows, m.n_cols, m.rs.p, m.col.p, m.val.p, m.cs.p, m.trow.p,
+                       m.tval.p, nullptr));
+  check(ctsm_csr_colsum_max(ctx(), m.n_rows, m.n_cols, m.rs.p, m.col.p, m.val.p, &m.colsum_max,
+                            nullptr));
+  m.csc = true;
+}
+
+bool DeviceSystemMatrix::has_transpose() const { return impl_->csc; }
 
 std::vector<double> forward_project(const DeviceSystemMatrix& w, const std::vector<double>& x) {
   const auto& m = w.impl();
@@ -700,7 +724,11 @@ std::vector<double> back_project(const DeviceSystemMatrix& w, const std::vector<
     throw Error(ErrorCode::DimensionMismatch, "sinogram size does not match matrix rows");
   DevBuf<double> yd(y.size()), xd(m.n_cols);
   h2d(yd.p, y.data(), y.size());
-  check(ctsm_spmv_t(ctx(), m.n_rows, m.n_cols, m.rs.p, m.col.p, m.val.p, yd.p, xd.p, nullptr));
+  if (m.csc)
+    check(ctsm_spmv_t_csc(ctx(), m.n_rows, m.n_cols, m.cs.p, m.trow.p, m.tval.p, m.colsum_max,
+                          yd.p, xd.p, nullptr));
+  else
+    check(ctsm_spmv_t(ctx(), m.n_rows, m.n_cols, m.rs.p, m.col.p, m.val.p, yd.p, xd.p, nullptr));
   std::vector<double> x(m.n_cols);
   d2h(x.data(), xd.p, x.size());
   return x;

@@ -846,6 +846,55 @@ int ctsm_spmv_t_bound(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols,
   return check_status(ctx, st, "back projection");
 }
 
+int ctsm_csc_build(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols,
+                   const uint64_t* row_start_dev, const uint32_t* col_dev, const double* val_dev,
+                   uint64_t* col_start_dev, uint32_t* row_dev, double* valt_dev, void* stream) {
+  CT_TRY(set_device(ctx));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_rows >= (1ull << 32)) return fail(CTSM_ERR_TOO_LARGE, "CSC row indices are 32-bit");
+  uint64_t nnz = 0;
+  CT_CUDA(cudaMemcpyAsync(&nnz, row_start_dev + n_rows, sizeof nnz, cudaMemcpyDeviceToHost, st));
+  CT_CUDA(cudaStreamSynchronize(st));
+  // counts and cursors (u32 per column), scan scratch
+  CT_TRY(ensure(ctx, ctx->tmp_a, n_cols * sizeof(unsigned)));
+  CT_TRY(ensure(ctx, ctx->tmp_b, n_cols * sizeof(unsigned long long)));
+  CT_TRY(ensure(ctx, ctx->tmp_c, scan_scratch_bytes(n_cols)));
+  unsigned* counts = (unsigned*)ctx->tmp_a.p;
+  unsigned* cursor = (unsigned*)ctx->tmp_b.p;
+  CT_CUDA(cudaMemsetAsync(counts, 0, n_cols * sizeof(unsigned), st));
+  CT_CUDA(cudaMemsetAsync(cursor, 0, n_cols * sizeof(unsigned), st));
+  CT_CUDA(csc_count(nnz, col_dev, counts, st));
+  CT_CUDA(exclusive_scan_u32_u64(counts, n_cols, col_start_dev, ctx->tmp_c.p, st));
+  CT_CUDA(csc_scatter(n_rows, row_start_dev, col_dev, val_dev, col_start_dev, cursor, row_dev,
+                      valt_dev, st));
+  CT_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int ctsm_spmv_t_csc(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols,
+                    const uint64_t* col_start_dev, const uint32_t* row_dev,
+                    const double* valt_dev, double colsum_max, const double* y_dev,
+                    double* x_dev, void* stream) {
+  CT_TRY(set_device(ctx));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!std::isfinite(colsum_max) || colsum_max < 0.0)
+    return fail(CTSM_ERR_NON_FINITE, "column-sum bound not finite");
+  double my = 0.0;
+  CT_TRY(fetch_max_abs(ctx, CTSM_F64, n_rows, y_dev, st, &my));
+  if (!std::isfinite(my)) return fail(CTSM_ERR_NON_FINITE, "back projection not finite");
+  const double scale = csr_fixed_scale(colsum_max, my);  // the scatter's scale: same integers
+  if (!(scale > 0.0)) {
+    CT_CUDA(cudaMemsetAsync(x_dev, 0, n_cols * sizeof(double), st));
+    CT_CUDA(cudaStreamSynchronize(st));
+    return 0;
+  }
+  CT_TRY(ensure(ctx, ctx->tmp_b, n_cols * sizeof(unsigned long long)));
+  CT_CUDA(spmvt_csc_fixed(n_cols, col_start_dev, row_dev, valt_dev, y_dev,
+                          (unsigned long long*)ctx->tmp_b.p, scale, st));
+  CT_CUDA(fixed_to_double(n_cols, (const unsigned long long*)ctx->tmp_b.p, scale, x_dev, st));
+  return check_status(ctx, st, "back projection");
+}
+
 int ctsm_spmv_t(ctsm_ctx* ctx, uint64_t n_rows, uint64_t n_cols, const uint64_t* row_start_dev,
                 const uint32_t* col_dev, const double* val_dev, const double* y_dev,
                 double* x_dev, void* stream) {

@@ -583,6 +583,59 @@ __global__ void spmvt_fixed_kernel(uint64_t n_rows, const uint64_t* __restrict__
       atomicAdd(&acc[__ldcs(&col[j])], (unsigned long long)__double2ll_rn(__ldcs(&val[j]) * ys));
   }
 }
+// ---- K4 as a gather: CSC transpose of a device CSR --------------------------
+// The scatter above is bound by the L2's 64-bit reductions (4.6 G of them for
+// C2: 49 % of the HBM time of the matrix). With the transpose kept beside the
+// CSR (C2: 2 x 55 GB of 180) A^T y reads each entry once and gathers y.
+// csc_count / csc_scatter build it: column counts, their scan (the caller),
+// then every CSR entry takes a slot of its column from a cursor. The order of
+// a column's entries depends on the schedule; the applier sums the same
+// rounded fixed-point integers as the scatter, so its result does not, and it
+// is bit-identical to spmvt_fixed_kernel's.
+__global__ void csc_count_kernel(uint64_t nnz, const uint32_t* __restrict__ col,
+                                 unsigned* __restrict__ counts) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nnz; j += stride)
+    atomicAdd(&counts[__ldcs(&col[j])], 1u);
+}
+
+__global__ void csc_scatter_kernel(uint64_t n_rows, const uint64_t* __restrict__ rs,
+                                   const uint32_t* __restrict__ col,
+                                   const double* __restrict__ val,
+                                   const uint64_t* __restrict__ col_start, unsigned* cursor,
+                                   uint32_t* __restrict__ row_out, double* __restrict__ val_out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps_total = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rows;
+       r += warps_total) {
+    for (uint64_t j = rs[r] + lane; j < rs[r + 1]; j += 32) {
+      const uint32_t c = __ldcs(&col[j]);
+      const uint64_t pos = col_start[c] + atomicAdd(&cursor[c], 1u);
+      row_out[pos] = (uint32_t)r;
+      val_out[pos] = __ldcs(&val[j]);
+    }
+  }
+}
+
+// warp per column: acc = sum_j round(val_j * (y[row_j] * scale)), the
+// scatter's integers (spmvt_fixed_kernel) in another order
+__global__ void spmvt_csc_fixed_kernel(uint64_t n_cols, const uint64_t* __restrict__ cs,
+                                       const uint32_t* __restrict__ row,
+                                       const double* __restrict__ val,
+                                       const double* __restrict__ y,
+                                       unsigned long long* __restrict__ acc, double scale) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps_total = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t c = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < n_cols;
+       c += warps_total) {
+    long long a = 0;
+    for (uint64_t j = cs[c] + lane; j < cs[c + 1]; j += 32)
+      a += __double2ll_rn(__ldcs(&val[j]) * (__ldg(&y[__ldcs(&row[j])]) * scale));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) acc[c] = (unsigned long long)a;
+  }
+}
 }  // namespace
 
 static unsigned row_grid(uint64_t n_rows, int warps_per_block, int blocks_per_sm = 32) {
@@ -602,6 +655,32 @@ cudaError_t spmv_csr(uint64_t n_rows, const uint64_t* row_start, const uint32_t*
 cudaError_t colsum_abs(uint64_t n_rows, const uint64_t* row_start, const uint32_t* col,
                        const double* val, double* colsum, cudaStream_t st) {
   colsum_abs_kernel<<<row_grid(n_rows, 8), 256, 0, st>>>(n_rows, row_start, col, val, colsum);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t csc_count(uint64_t nnz, const uint32_t* col, unsigned* counts, cudaStream_t st) {
+  const uint64_t blocks = (nnz + 255) / 256;
+  csc_count_kernel<<<(unsigned)(blocks < 148ull * 32 ? (blocks ? blocks : 1) : 148ull * 32), 256, 0,
+                     st>>>(nnz, col, counts);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t csc_scatter(uint64_t n_rows, const uint64_t* row_start, const uint32_t* col,
+                        const double* val, const uint64_t* col_start, unsigned* cursor,
+                        uint32_t* row_out, double* val_out, cudaStream_t st) {
+  csc_scatter_kernel<<<row_grid(n_rows, 8), 256, 0, st>>>(n_rows, row_start, col, val, col_start,
+                                                          cursor, row_out, val_out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t spmvt_csc_fixed(uint64_t n_cols, const uint64_t* col_start, const uint32_t* row,
+                            const double* val, const double* y, unsigned long long* acc,
+                            double scale, cudaStream_t st) {
+  spmvt_csc_fixed_kernel<<<row_grid(n_cols, 8), 256, 0, st>>>(n_cols, col_start, row, val, y, acc,
+                                                              scale);
   count_launch();
   return cudaGetLastError();
 }

@@ -89,6 +89,15 @@ cudaError_t colsum_abs(uint64_t n_rows, const uint64_t* row_start, const uint32_
 cudaError_t spmvt_csr_fixed(uint64_t n_rows, const uint64_t* row_start, const uint32_t* col,
                             const double* val, const double* y, unsigned long long* acc,
                             double scale, cudaStream_t st);
+// K4 as a gather over a CSC transpose (csr.cu): column counts, slot scatter
+// (after the caller's scan of the counts), and the fixed-point applier
+cudaError_t csc_count(uint64_t nnz, const uint32_t* col, unsigned* counts, cudaStream_t st);
+cudaError_t csc_scatter(uint64_t n_rows, const uint64_t* row_start, const uint32_t* col,
+                        const double* val, const uint64_t* col_start, unsigned* cursor,
+                        uint32_t* row_out, double* val_out, cudaStream_t st);
+cudaError_t spmvt_csc_fixed(uint64_t n_cols, const uint64_t* col_start, const uint32_t* row,
+                            const double* val, const double* y, unsigned long long* acc,
+                            double scale, cudaStream_t st);
 
 // ---- weights.cu: the reference's weight API on the device ------------------
 // pixel_area_factors / voxel_volume_factors (weights2d.cpp:105-129,

@@ -366,17 +366,55 @@ def _colsum_max(w: SparseSystemMatrix) -> float:
     return out.value
 
 
+def _csr_key(w: SparseSystemMatrix):
+    return (w.col.data_ptr(), w.col._version, w.val.data_ptr(), w.val._version,
+            w.row_start.data_ptr(), w.row_start._version)
+
+
+def build_transpose(w: SparseSystemMatrix) -> None:
+    """Keeps a CSC transpose of the matrix beside the CSR (``ctsm_csc_build``):
+    ``back_project`` then gathers (every entry read once) instead of issuing
+    one 64-bit reduction per entry, with bit-identical results. Costs the
+    CSR's col / val bytes again (C2: 55 GB); dropped when the arrays change."""
+    if w.n_rows >= 1 << 32:
+        raise CtsmError("TooLarge", "CSC row indices are 32-bit")
+    ctx = Context.get(w.device)
+    dev = w.val.device
+    col_start = torch.empty(w.n_cols + 1, dtype=torch.int64, device=dev)
+    row = torch.empty(w.nnz(), dtype=torch.int32, device=dev)
+    valt = torch.empty(w.nnz(), dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().ctsm_csc_build(ctx.handle, w.n_rows, w.n_cols, _dev_ptr(w.row_start),
+                                         _dev_ptr(w.col), _dev_ptr(w.val), _dev_ptr(col_start),
+                                         _dev_ptr(row), _dev_ptr(valt), _stream(w.device)))
+    w._csc = (_csr_key(w), col_start, row, valt)
+
+
+def drop_transpose(w: SparseSystemMatrix) -> None:
+    w._csc = None
+
+
 def back_project(w: SparseSystemMatrix, y):
-    """projector.cpp:219-233 (K4)."""
+    """projector.cpp:219-233 (K4): the fixed-point scatter over the CSR, or,
+    after ``build_transpose(w)``, the gather over its CSC transpose (same
+    bits)."""
     n = int(y.numel()) if (torch is not None and isinstance(y, torch.Tensor)) else int(np.size(y))
     if n != w.n_rows:
         raise CtsmError("DimensionMismatch", "sinogram size does not match matrix rows")
     ctx = Context.get(w.device)
     yt, was_t = _to_device(y, w.device, torch.float64)
     x = torch.empty(w.n_cols, dtype=torch.float64, device=yt.device)
-    _lib.check(_lib.lib().ctsm_spmv_t_bound(ctx.handle, w.n_rows, w.n_cols, _dev_ptr(w.row_start),
-                                            _dev_ptr(w.col), _dev_ptr(w.val), _colsum_max(w),
-                                            _dev_ptr(yt), _dev_ptr(x), _stream(w.device)))
+    csc = getattr(w, "_csc", None)
+    if csc is not None and csc[0] != _csr_key(w):
+        csc = w._csc = None  # the arrays changed under the transpose
+    if csc is not None:
+        _lib.check(_lib.lib().ctsm_spmv_t_csc(ctx.handle, w.n_rows, w.n_cols, _dev_ptr(csc[1]),
+                                              _dev_ptr(csc[2]), _dev_ptr(csc[3]), _colsum_max(w),
+                                              _dev_ptr(yt), _dev_ptr(x), _stream(w.device)))
+    else:
+        _lib.check(_lib.lib().ctsm_spmv_t_bound(ctx.handle, w.n_rows, w.n_cols,
+                                                _dev_ptr(w.row_start), _dev_ptr(w.col),
+                                                _dev_ptr(w.val), _colsum_max(w), _dev_ptr(yt),
+                                                _dev_ptr(x), _stream(w.device)))
     return x if was_t else x.cpu().numpy()
 
 
@@ -386,6 +424,7 @@ def scale_values(w: SparseSystemMatrix, factor: float) -> None:
         raise CtsmError("NonFinite", "scale factor must be finite")
     ctx = Context.get(w.device)
     w._colsum_cache = None  # values change through the C-ABI, not a torch op
+    w._csc = None
     _lib.check(_lib.lib().ctsm_scale_values(ctx.handle, w.nnz(), _dev_ptr(w.val), float(factor),
                                             _stream(ctx.device)))
 

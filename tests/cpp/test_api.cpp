@@ -299,9 +299,15 @@ int main() {
     const auto x = randn(w.n_cols, 5), y = randn(w.n_rows, 6);
     EXPECT(forward_project(dm, x) == forward_project(w, x));
     EXPECT(back_project(db, y) == back_project(w, y));
+    // K4 as a gather over the CSC transpose: the same bits as the scatter
+    db.build_transpose();
+    EXPECT(db.has_transpose());
+    EXPECT(back_project(db, y) == back_project(w, y));
     EXPECT(spectral_norm_power(dm, 30, 7) == spectral_norm_power(w, 30, 7));
     const double nrm = spectral_norm_power(dm, 100, 7);
+    dm.build_transpose();
     dm.scale_values(1.0 / nrm);
+    EXPECT(!dm.has_transpose());  // the transpose held the old values
     EXPECT(std::abs(spectral_norm_power(dm, 100, 7) - 1.0) <= 1e-8);
     SolveOptions opt;
     opt.lambda = 1e-2;

@@ -222,6 +222,42 @@ def test_spmv_and_transpose(name, oracle_cr):
     with pytest.raises(CtsmError) as e:
         forward_project(w, np.zeros(g.n_voxels + 1))
     assert e.value.code == "DimensionMismatch"
+    # K4 as a gather over the CSC transpose: the same fixed-point integers in
+    # another order, so the same bits
+    from paper_2511_12235_b200 import build_transpose, drop_transpose, scale_values
+    build_transpose(w)
+    xc = back_project(w, y)
+    assert np.array_equal(np.asarray(xb).view(np.uint64), np.asarray(xc).view(np.uint64))
+    key, col_start, row, valt = w._csc
+    cs = col_start.cpu().numpy().view(np.uint64)
+    assert cs[0] == 0 and cs[-1] == w.nnz()
+    assert np.array_equal(np.diff(cs.astype(np.int64)), np.bincount(ref.col, minlength=g.n_voxels))
+    # a column's entries are its (row, value) pairs, in any order
+    rr, vv = row.cpu().numpy().view(np.uint32), valt.cpu().numpy()
+    c = int(np.argmax(np.diff(cs.astype(np.int64))))
+    got = sorted(zip(rr[cs[c]:cs[c + 1]].tolist(), vv[cs[c]:cs[c + 1]].tolist()))
+    sel = np.nonzero(ref.col == c)[0]
+    assert got == sorted(zip(rows[sel].tolist(), ref.val[sel].tolist()))
+    scale_values(w, 2.0)  # drops the transpose with the column-sum bound
+    assert w._csc is None
+    assert rel_err(back_project(w, y), 2.0 * xr) <= 1e-13
+    drop_transpose(w)
+
+
+def test_csc_back_project_c0_bitexact():
+    """C0 in full: back_project through the CSC transpose equals the scatter
+    bit for bit (18.3 M entries, random sinogram with zeros)."""
+    from paper_2511_12235_b200 import build_transpose
+    g = CONFIGS["c0"]
+    w = build_system_matrix(g)
+    gen = torch.Generator().manual_seed(5)
+    y = torch.rand(g.n_measurements, generator=gen, dtype=torch.float64)
+    y[::7] = 0.0
+    y = y.cuda()
+    xs = back_project(w, y)
+    build_transpose(w)
+    xc = back_project(w, y)
+    assert torch.equal(xs, xc)
 
 
 # ---- K5/K6: matrix-free ---------------------------------------------------------
