@@ -247,6 +247,12 @@ typedef struct ctsm_operator {
   const double* val;                /* CSR, device */
   const ctsm_geometry* geom;        /* matrix-free */
   double scale;                     /* matrix-free: W = scale * A (CSR: must be 1) */
+  /* CSR, optional (all three or none; zero-initialise otherwise): the CSC
+   * transpose of ctsm_csc_build; W^T then gathers instead of scattering,
+   * with the same bits */
+  const uint64_t* col_start;
+  const uint32_t* trow;
+  const double* tval;
 } ctsm_operator;
 
 /* spectral_norm_power (projector.cpp:262-280): v_inout holds the start vector

@@ -31,7 +31,9 @@ class COperator(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int), ("pad0", ctypes.c_int),
                 ("n_rows", ctypes.c_uint64), ("n_cols", ctypes.c_uint64),
                 ("row_start", ctypes.c_void_p), ("col", ctypes.c_void_p), ("val", ctypes.c_void_p),
-                ("geom", _GP), ("scale", ctypes.c_double)]
+                ("geom", _GP), ("scale", ctypes.c_double),
+                ("col_start", ctypes.c_void_p), ("trow", ctypes.c_void_p),
+                ("tval", ctypes.c_void_p)]
 
 
 _OP = ctypes.POINTER(COperator)

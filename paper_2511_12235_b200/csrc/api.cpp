@@ -627,6 +627,11 @@ struct DeviceSystemMatrix::Impl {
     o.col = col.p;
     o.val = val.p;
     o.scale = 1.0;
+    if (csc) {
+      o.col_start = cs.p;
+      o.trow = trow.p;
+      o.tval = tval.p;
+    }
     return o;
   }
 };

@@ -1610,9 +1610,15 @@ int op_bwd(ctsm_ctx* ctx, const OpRun& r, const double* y, double* x, cudaStream
       return 0;
     }
     CT_TRY(ensure(ctx, ctx->tmp_b, r.n_cols * sizeof(unsigned long long)));
-    CT_CUDA(cudaMemsetAsync(ctx->tmp_b.p, 0, r.n_cols * sizeof(unsigned long long), st));
-    CT_CUDA(spmvt_csr_fixed(r.n_rows, op->row_start, op->col, op->val, y,
-                            (unsigned long long*)ctx->tmp_b.p, scale, st));
+    if (op->col_start && op->trow && op->tval) {
+      // the caller keeps a CSC transpose: gather (same integers, same bits)
+      CT_CUDA(spmvt_csc_fixed(r.n_cols, op->col_start, op->trow, op->tval, y,
+                              (unsigned long long*)ctx->tmp_b.p, scale, st));
+    } else {
+      CT_CUDA(cudaMemsetAsync(ctx->tmp_b.p, 0, r.n_cols * sizeof(unsigned long long), st));
+      CT_CUDA(spmvt_csr_fixed(r.n_rows, op->row_start, op->col, op->val, y,
+                              (unsigned long long*)ctx->tmp_b.p, scale, st));
+    }
     CT_CUDA(fixed_to_double(r.n_cols, (const unsigned long long*)ctx->tmp_b.p, scale, x, st));
     return 0;
   }

@@ -436,6 +436,9 @@ def csr_operator(w: SparseSystemMatrix):
     op.n_rows, op.n_cols = w.n_rows, w.n_cols
     op.row_start, op.col, op.val = w.row_start.data_ptr(), w.col.data_ptr(), w.val.data_ptr()
     op.scale = 1.0
+    csc = getattr(w, "_csc", None)
+    if csc is not None and csc[0] == _csr_key(w):  # build_transpose: W^T as a gather
+        op.col_start, op.trow, op.tval = csc[1].data_ptr(), csc[2].data_ptr(), csc[3].data_ptr()
     return op, None
 
 

@@ -55,6 +55,13 @@ def test_spectral_norm_and_nag_match_restatement(name):
     assert np.array_equal(tr[:, 0], tr_ref[:, 0])
     assert rel(tr[:, 1], tr_ref[:, 1]) <= 1e-10
     assert np.max(np.abs(tr[:, 2] - tr_ref[:, 2]) / tr_ref[:, 2]) <= 1e-8
+    # with the CSC transpose kept beside the CSR the solvers' W^T gathers:
+    # the same fixed-point integers, so the same iterates bit for bit
+    from paper_2511_12235_b200 import build_transpose
+    build_transpose(w)
+    rt = nag_tikhonov(w, p, opt)
+    assert torch.equal(rt.u, r.u) and rt.iterations == r.iterations
+    assert spectral_norm_power(w, 30, 7) == 1.0 * spectral_norm_power(w, 30, 7)
     # matrix-free NAG on W = A / ||A||
     rm = nag_tikhonov_matrix_free(g, p, opt, scale=1.0 / nrm)
     assert rm.iterations == 40
