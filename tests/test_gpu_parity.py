@@ -336,6 +336,25 @@ def test_matrix_free_deterministic():
     assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_symmetric_back_projection_deterministic(dtype):
+    """The 3D symmetric back-projection (orbit shared by a warp pair, two
+    partial volumes, member sums folded with plain loads and stores) repeats
+    bit for bit in fp64 and in fp32 -- a race on the fold would show here --
+    and so does the fp64 forward (fixed point)."""
+    g = CONFIGS["c3"].with_(n_x=64, n_y=64, n_z=32, n_det_z=96, n_angles=64)
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    gen = torch.Generator().manual_seed(9)
+    y = torch.rand(g.n_measurements, generator=gen, dtype=tdt).cuda()
+    x = torch.rand(g.n_voxels, generator=gen, dtype=tdt).cuda()
+    a = back_project_matrix_free(g, "consistent", 1, y)
+    for _ in range(3):
+        assert torch.equal(a, back_project_matrix_free(g, "consistent", 1, y))
+    if dtype == "f64":
+        f = forward_project_matrix_free(g, "consistent", 1, x)
+        assert torch.equal(f, forward_project_matrix_free(g, "consistent", 1, x))
+
+
 # Matrix-free parity at BASELINE sizes is tolerance-checked, so the faster
 # glibc-libm oracle is used (crmath costs ~10x on the CPU); angle blocks are
 # split into slabs to use all host cores.
