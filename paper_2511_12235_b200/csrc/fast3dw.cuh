@@ -667,7 +667,10 @@ __device__ __noinline__ double atom_sum3_slow(const ColumnHead& H, const PieceCo
 // in the order pass 1 listed them. Faces beyond a lane's kRq slots are
 // evaluated in place. The classification is the same products and compares
 // in both passes, so the two passes agree face by face.
-constexpr int kRq = 8;
+#ifndef CTSM_KRQ
+#define CTSM_KRQ 8
+#endif
+constexpr int kRq = CTSM_KRQ;
 struct CubicBatch {
   double rq[kRq][32];  // [slot][lane]: G in pass 1, the raw atom sum after pass 2
   int roff[32];
