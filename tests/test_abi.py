@@ -36,6 +36,14 @@ def test_python_binding_covers_header():
     assert names <= bound, names - bound
 
 
+def test_integration_doc_lists_every_entry_point():
+    """INTEGRATION.md names every exported entry point beside the reference
+    interface it replaces."""
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    missing = [n for n in declared_functions() if n not in doc]
+    assert not missing, missing
+
+
 def test_no_cpu_fallback_symbols():
     """The product library links no oracle code."""
     L = ctypes.CDLL(_lib.LIB_PATH)
