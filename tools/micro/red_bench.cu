@@ -25,7 +25,18 @@ __global__ void __launch_bounds__(128) k(float* __restrict__ y, unsigned nseg, i
   for (int i = 0; i < iters; ++i) {
     if ((i & 7) == 0) seg = (hash((tid >> 5) * 977u + (unsigned)i) + (threadIdx.x & 31) * stride_rows) % (nseg - 16);
     float* dst = y + (size_t)(seg + (i & 7)) * 8;
-    if (MODE == 0 || MODE == 2) {
+    if (MODE == 3 || MODE == 4) {
+      // the forward's flush: two segments per lane and trip (a row and its z
+      // mirror), far apart (3: rows r and N-1-r) or adjacent (4: a paired layout)
+      float* d2 = MODE == 3 ? y + (size_t)(nseg - 1 - (seg + (i & 7))) * 8
+                            : y + (size_t)((seg + (i & 7)) ^ 1u) * 8;
+      float* d1 = MODE == 3 ? dst : y + (size_t)((seg + (i & 7)) & ~1u) * 8;
+      if (MODE == 4) d2 = d1 + 8;
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d1), "f"(v), "f"(v), "f"(v), "f"(v) : "memory");
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d1 + 4), "f"(v), "f"(v), "f"(v), "f"(v) : "memory");
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d2), "f"(v), "f"(v), "f"(v), "f"(v) : "memory");
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d2 + 4), "f"(v), "f"(v), "f"(v), "f"(v) : "memory");
+    } else if (MODE == 0 || MODE == 2) {
       asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(v), "f"(v), "f"(v), "f"(v) : "memory");
       if (MODE == 0)
         asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4), "f"(v), "f"(v), "f"(v), "f"(v) : "memory");
@@ -57,20 +68,22 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e1);
   const int blocks = 148 * 4;
   for (int stride = 1; stride <= 5; stride += 4)
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 5; ++mode) {
       for (int rep = 0; rep < 2; ++rep) {
         cudaEventRecord(e0);
         if (mode == 0) k<0><<<blocks, 128>>>(y, nseg, iters, stride);
         if (mode == 1) k<1><<<blocks, 128>>>(y, nseg, iters, stride);
         if (mode == 2) k<2><<<blocks, 128>>>(y, nseg, iters, stride);
+        if (mode == 3) k<3><<<blocks, 128>>>(y, nseg, iters, 2 * stride);
+        if (mode == 4) k<4><<<blocks, 128>>>(y, nseg, iters, 2 * stride);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
         if (rep == 1) {
-          const double segs = (double)blocks * 128 * iters;
+          const double segs = (double)blocks * 128 * iters * (mode >= 3 ? 2 : 1);
           printf("mode %d (%s) lane stride %d rows: %.3f ms, %.2f G segments/s, %.3f segments/clk/SM @1.9GHz  err=%s\n",
-                 mode, mode == 0 ? "2 x red.v4" : mode == 1 ? "1 x bulk reduce 32 B" : "1 x red.v4 (half)",
+                 mode, mode == 0 ? "2 x red.v4" : mode == 1 ? "1 x bulk reduce 32 B" : mode == 2 ? "1 x red.v4 (half)" : mode == 3 ? "row + far mirror row (2 segments per trip)" : "row + adjacent mirror row (2 segments per trip)",
                  stride, ms, segs / ms * 1e-6, segs / (ms * 1e-3) / 148 / 1.9e9,
                  cudaGetErrorString(cudaGetLastError()));
         }
